@@ -1,0 +1,830 @@
+// C ABI (include/fsb_b200.h): context, model upload/repacking, workspace,
+// stage entry points and the CUDA-graph replay of the whole frame batch.
+#include <cuda_runtime.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <map>
+#include <string>
+#include <vector>
+
+#include "../../include/fsb_b200.h"
+#include "fsb_common.cuh"
+#include "fsb_weights.h"
+
+// ---- kernels (other translation units) ------------------------------------
+cudaError_t launch_boxes_crops(const float* images, const float* kps, int B, int H, int W, int S, double alpha,
+                               double* boxes, float* prompt, float* crops, int32_t* taps, int* nonfinite,
+                               cudaStream_t st);
+cudaError_t launch_bilinear(const float* img, int H, int W, int C, const float* grid, int64_t n, float* out,
+                            int* nonfinite, cudaStream_t st);
+cudaError_t launch_encoder_f32(const float* crops, int ncrops, const EncW& w, float* feats, int* nonfinite,
+                               cudaStream_t st);
+cudaError_t launch_decoders_f32(const DecodeArgs& a, const BodyW& bw, const HandW& hw, cudaStream_t st);
+cudaError_t launch_fk(const float* poses, int ld_pose, int B, const float* grest, float* joints, float* rel,
+                      cudaStream_t st);
+cudaError_t launch_lbs(const TemplateDev& t, const float* rel, const float* poses, int ld_pose, int B, float* verts,
+                       int* nonfinite, cudaStream_t st);
+cudaError_t launch_proj_inputs(const TemplateDev& t, const ProjectorDev& p, const float* rel, const float* poses,
+                               int ld_pose, int B, float* x, __nv_bfloat16* xb, int ldx, cudaStream_t st);
+cudaError_t launch_proj_inputs_v(const float* V, int nv, const ProjectorDev& p, int B, float* x, __nv_bfloat16* xb,
+                                 int ldx, cudaStream_t st);
+cudaError_t launch_gemm_f32(const float* A, int lda, const float* W, const float* bias, const float* mask, float* C,
+                            int ldc, int M, int N, int K, int relu, int* nonfinite, cudaStream_t st);
+
+cudaError_t launch_body_boxes(const float* kps, int n, int W, int H, double* out, cudaStream_t st);
+cudaError_t launch_hand_boxes(const double* wrists, const double* body, int n, double alpha, int W, int H, double* out,
+                              cudaStream_t st);
+cudaError_t launch_crop_grid(const double* boxes, int n, int S, float* out, cudaStream_t st);
+cudaError_t launch_bridge(const float* V, int B, int nv, const int32_t* corners, const float* w, int nt, float* out,
+                          cudaStream_t st);
+cudaError_t init_attrs_transformer();
+cudaError_t init_attrs_body();
+
+namespace {
+
+struct DevMem {
+  void* p = nullptr;
+  size_t n = 0;
+  ~DevMem() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  cudaError_t alloc(size_t bytes) {
+    release();
+    n = bytes;
+    return bytes ? cudaMalloc(&p, bytes) : cudaSuccess;
+  }
+};
+
+// host-side packer: append arrays at 256-byte aligned offsets, then one H2D
+struct Packer {
+  std::vector<unsigned char> host;
+  size_t add(const void* src, size_t bytes) {
+    const size_t off = (host.size() + 255) & ~size_t(255);
+    host.resize(off + bytes);
+    if (src) memcpy(host.data() + off, src, bytes);
+    return off;
+  }
+};
+
+struct GraphKey {
+  int B, H, W, precision;
+  uint32_t bsel, hsel;
+  double alpha;
+  const void* ptrs[16];
+  cudaStream_t stream;
+  bool operator==(const GraphKey& o) const { return memcmp(this, &o, sizeof(GraphKey)) == 0; }
+};
+
+}  // namespace
+
+struct fsb_ctx {
+  int device = 0;
+  std::string err;
+  int* d_flag = nullptr;
+  fsb_counters_t counters{};
+  int64_t launches = 0;
+  // decoder
+  bool has_decoder = false;
+  fsb_decoder_config cfg{};
+  DevMem dec_mem;
+  EncW enc{};
+  BodyW body{};
+  HandW hand{};
+  // templates / projector
+  bool has_tmpl[2] = {false, false};
+  DevMem tmpl_mem[2];
+  TemplateDev tmpl[2]{};
+  bool has_proj = false;
+  DevMem proj_mem;
+  ProjectorDev proj{};
+  // workspace
+  int ws_frames = 0;
+  DevMem ws;
+  double* w_boxes = nullptr;
+  float *w_prompt = nullptr, *w_crops = nullptr, *w_feats = nullptr, *w_params = nullptr, *w_cam = nullptr,
+        *w_rots = nullptr, *w_rel = nullptr, *w_rel2 = nullptr, *w_x = nullptr, *w_h1 = nullptr, *w_h2 = nullptr,
+        *w_theta = nullptr;
+  __nv_bfloat16* w_xb = nullptr;
+  // graphs
+  bool graphs = true;
+  bool have_graph = false;
+  GraphKey gkey{};
+  cudaGraphExec_t gexec = nullptr;
+  int graph_nodes = 0;
+};
+
+namespace {
+
+int fail(fsb_ctx* c, int code, const char* fmt, ...) __attribute__((format(printf, 3, 4)));
+int fail(fsb_ctx* c, int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  if (c) c->err = buf;
+  return code;
+}
+
+#define FSB_CUDA(c, expr)                                                                          \
+  do {                                                                                             \
+    cudaError_t e_ = (expr);                                                                       \
+    if (e_ != cudaSuccess) return fail((c), FSB_ERR_CUDA, "%s: %s", #expr, cudaGetErrorString(e_)); \
+  } while (0)
+
+bool default_model(const fsb_decoder_config& c) {
+  return c.crop_size == 64 && c.patch == 8 && c.dim == 64 && c.heads == 4 && c.enc_layers <= FSB_MAX_LAYERS &&
+         c.body_layers <= 8 && c.hand_layers <= 8;
+}
+
+int layer_count(uint32_t sel) { return __builtin_popcount(sel); }
+
+bool capturing(cudaStream_t st) {
+  cudaStreamCaptureStatus s = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &s) != cudaSuccess) return false;
+  return s != cudaStreamCaptureStatusNone;
+}
+
+int ensure_ws(fsb_ctx* c, int frames, cudaStream_t st) {
+  if (frames <= c->ws_frames) return FSB_OK;
+  if (capturing(st))
+    return fail(c, FSB_ERR_USAGE, "workspace for %d frames not reserved before graph capture", frames);
+  return fsb_reserve(c, frames);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* fsb_build_info(void) { return "fsb_b200 sm_100a (" __DATE__ ")"; }
+
+int fsb_ctx_create(int device, fsb_ctx** out) {
+  if (!out) return FSB_ERR_USAGE;
+  *out = nullptr;
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return FSB_ERR_CUDA;
+  fsb_ctx* c = new fsb_ctx();
+  c->device = device;
+  if (init_attrs_transformer() != cudaSuccess || init_attrs_body() != cudaSuccess) {
+    delete c;
+    return FSB_ERR_CUDA;
+  }
+  if (cudaMalloc(&c->d_flag, sizeof(int)) != cudaSuccess || cudaMemset(c->d_flag, 0, sizeof(int)) != cudaSuccess) {
+    delete c;
+    return FSB_ERR_CUDA;
+  }
+  *out = c;
+  return FSB_OK;
+}
+
+void fsb_ctx_destroy(fsb_ctx* c) {
+  if (!c) return;
+  if (c->gexec) cudaGraphExecDestroy(c->gexec);
+  if (c->d_flag) cudaFree(c->d_flag);
+  delete c;
+}
+
+const char* fsb_last_error(const fsb_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+int fsb_set_graphs(fsb_ctx* c, int enabled) {
+  c->graphs = enabled != 0;
+  return FSB_OK;
+}
+
+int fsb_reserve(fsb_ctx* c, int max_frames) {
+  if (max_frames <= c->ws_frames) return FSB_OK;
+  const int S = c->has_decoder ? c->cfg.crop_size : 0;
+  const int T = c->has_decoder ? (S / c->cfg.patch) * (S / c->cfg.patch) : 0;
+  const int Dm = c->has_decoder ? c->cfg.dim : 0;
+  const int nsub = c->has_proj ? c->proj.n_sub : 1500;
+  const int h1 = c->has_proj ? c->proj.h1 : 512, h2 = c->has_proj ? c->proj.h2 : 256;
+  const size_t F = (size_t)max_frames;
+  size_t off = 0;
+  auto take = [&](size_t bytes) {
+    const size_t o = off;
+    off += (bytes + 255) & ~size_t(255);
+    return o;
+  };
+  const size_t o_boxes = take(F * 12 * sizeof(double));
+  const size_t o_prompt = take(F * 8 * 4);
+  const size_t o_crops = take(F * 3 * S * S * 3 * 4);
+  const size_t o_feats = take(F * 3 * T * Dm * 4);
+  const size_t o_params = take(F * 76 * 4);
+  const size_t o_cam = take(F * 3 * 4);
+  const size_t o_rots = take(F * 6 * 4);
+  const size_t o_rel = take(F * FSB_NJ * 12 * 4);
+  const size_t o_rel2 = take(F * FSB_NJ * 12 * 4);
+  const size_t o_x = take(F * 3 * nsub * 4);
+  const size_t o_xb = take(F * 3 * nsub * 2);
+  const size_t o_h1 = take(F * h1 * 4);
+  const size_t o_h2 = take(F * h2 * 4);
+  const size_t o_theta = take(F * 76 * 4);
+  if (c->have_graph) {
+    cudaGraphExecDestroy(c->gexec);
+    c->gexec = nullptr;
+    c->have_graph = false;
+  }
+  FSB_CUDA(c, c->ws.alloc(off));
+  unsigned char* b = static_cast<unsigned char*>(c->ws.p);
+  c->w_boxes = reinterpret_cast<double*>(b + o_boxes);
+  c->w_prompt = reinterpret_cast<float*>(b + o_prompt);
+  c->w_crops = reinterpret_cast<float*>(b + o_crops);
+  c->w_feats = reinterpret_cast<float*>(b + o_feats);
+  c->w_params = reinterpret_cast<float*>(b + o_params);
+  c->w_cam = reinterpret_cast<float*>(b + o_cam);
+  c->w_rots = reinterpret_cast<float*>(b + o_rots);
+  c->w_rel = reinterpret_cast<float*>(b + o_rel);
+  c->w_rel2 = reinterpret_cast<float*>(b + o_rel2);
+  c->w_x = reinterpret_cast<float*>(b + o_x);
+  c->w_xb = reinterpret_cast<__nv_bfloat16*>(b + o_xb);
+  c->w_h1 = reinterpret_cast<float*>(b + o_h1);
+  c->w_h2 = reinterpret_cast<float*>(b + o_h2);
+  c->w_theta = reinterpret_cast<float*>(b + o_theta);
+  c->ws_frames = max_frames;
+  return FSB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// model upload
+
+int fsb_load_decoder(fsb_ctx* c, const fsb_decoder_config* cfg, int n, const char* const* names,
+                     const float* const* arrays, const int64_t* numel) {
+  if (!cfg || n <= 0) return fail(c, FSB_ERR_USAGE, "fsb_load_decoder: empty weight table");
+  std::map<std::string, std::pair<const float*, int64_t>> tab;
+  for (int i = 0; i < n; ++i) tab[names[i]] = {arrays[i], numel[i]};
+  const int Dm = cfg->dim;
+  if (Dm <= 0 || cfg->heads <= 0 || Dm % cfg->heads || cfg->patch <= 0 || cfg->crop_size % cfg->patch)
+    return fail(c, FSB_ERR_SHAPE, "inconsistent decoder config");
+  if (cfg->enc_layers > FSB_MAX_LAYERS || cfg->body_layers > 8 || cfg->hand_layers > 8)
+    return fail(c, FSB_ERR_USAGE, "too many layers for the device tables");
+  Packer pk;
+  std::map<std::string, size_t> off;
+  std::string missing;
+  auto put = [&](const std::string& name, int64_t expect) -> bool {
+    auto it = tab.find(name);
+    if (it == tab.end()) {
+      missing = name;
+      return false;
+    }
+    if (expect >= 0 && it->second.second != expect) {
+      missing = name + " (size)";
+      return false;
+    }
+    off[name] = pk.add(it->second.first, (size_t)it->second.second * 4);
+    return true;
+  };
+  // q|k|v concatenated to (D, 3D) and the biases to (3D)
+  auto put_qkv = [&](const std::string& p) -> bool {
+    const char* ws[3] = {".wq", ".wk", ".wv"};
+    const char* bs[3] = {".bq", ".bk", ".bv"};
+    std::vector<float> w((size_t)Dm * 3 * Dm), b((size_t)3 * Dm);
+    for (int t = 0; t < 3; ++t) {
+      auto iw = tab.find(p + ws[t]);
+      auto ib = tab.find(p + bs[t]);
+      if (iw == tab.end() || ib == tab.end() || iw->second.second != (int64_t)Dm * Dm || ib->second.second != Dm) {
+        missing = p + ws[t];
+        return false;
+      }
+      for (int r = 0; r < Dm; ++r)
+        for (int q = 0; q < Dm; ++q) w[(size_t)r * 3 * Dm + t * Dm + q] = iw->second.first[(size_t)r * Dm + q];
+      for (int q = 0; q < Dm; ++q) b[t * Dm + q] = ib->second.first[q];
+    }
+    off[p + ".wqkv"] = pk.add(w.data(), w.size() * 4);
+    off[p + ".bqkv"] = pk.add(b.data(), b.size() * 4);
+    return true;
+  };
+  auto attn = [&](const std::string& p, bool cross) -> bool {
+    bool ok = cross ? (put(p + ".lnq_g", Dm) && put(p + ".lnq_b", Dm) && put(p + ".lnkv_g", Dm) &&
+                       put(p + ".lnkv_b", Dm))
+                    : (put(p + ".ln_g", Dm) && put(p + ".ln_b", Dm));
+    return ok && put_qkv(p) && put(p + ".wo", (int64_t)Dm * Dm) && put(p + ".bo", Dm);
+  };
+  auto mlp = [&](const std::string& p) -> bool {
+    return put(p + ".ln_g", Dm) && put(p + ".ln_b", Dm) && put(p + ".w1", (int64_t)Dm * 4 * Dm) &&
+           put(p + ".b1", 4 * Dm) && put(p + ".w2", (int64_t)4 * Dm * Dm) && put(p + ".b2", Dm);
+  };
+  const int np = (cfg->crop_size / cfg->patch) * (cfg->crop_size / cfg->patch);
+  bool ok = put("enc.patch_w", (int64_t)cfg->patch * cfg->patch * 3 * Dm) && put("enc.patch_b", Dm) &&
+            put("enc.pos", (int64_t)np * Dm) && put("enc.norm_g", Dm) && put("enc.norm_b", Dm);
+  for (int l = 0; ok && l < cfg->enc_layers; ++l)
+    ok = attn("enc.l" + std::to_string(l) + ".self", false) && mlp("enc.l" + std::to_string(l) + ".mlp");
+  ok = ok && put("body.token_init", 51 * Dm) && put("body.p2d_init", 22 * Dm) && put("body.p3d_init", 22 * Dm) &&
+       put("body.norm_g", Dm) && put("body.norm_b", Dm);
+  for (int l = 0; ok && l < cfg->body_layers; ++l) {
+    const std::string p = "body.l" + std::to_string(l);
+    ok = attn(p + ".self", false) && attn(p + ".cross", true) && mlp(p + ".mlp");
+  }
+  ok = ok && put("body.head_params.w", (int64_t)Dm * 76) && put("body.head_params.b", 76) &&
+       put("body.head_cam.w", (int64_t)Dm * 3) && put("body.head_cam.b", 3) && put("body.phi2d.w", 2 * Dm) &&
+       put("body.phi2d.b", Dm) && put("body.phi3d.w", 3 * Dm) && put("body.phi3d.b", Dm) &&
+       put("body.prompt_box.w", 8 * 4 * Dm) && put("body.prompt_box.b", 4 * Dm);
+  ok = ok && put("hand.token_init", 4 * Dm) && put("hand.p_init", 3 * Dm) && put("hand.norm_g", Dm) &&
+       put("hand.norm_b", Dm);
+  for (int l = 0; ok && l < cfg->hand_layers; ++l) {
+    const std::string p = "hand.l" + std::to_string(l);
+    ok = attn(p + ".self", false) && attn(p + ".cross", true) && mlp(p + ".mlp");
+  }
+  ok = ok && put("hand.head_rot.w", (int64_t)Dm * 3) && put("hand.head_rot.b", 3) &&
+       put("hand.head_cam.w", (int64_t)Dm * 3) && put("hand.head_cam.b", 3) && put("hand.phi2d.w", 2 * Dm) &&
+       put("hand.phi2d.b", Dm) && put("hand.canon_pts", 9);
+  if (!ok) return fail(c, FSB_ERR_SHAPE, "decoder weight table: missing or mis-sized '%s'", missing.c_str());
+  FSB_CUDA(c, c->dec_mem.alloc(pk.host.size()));
+  FSB_CUDA(c, cudaMemcpy(c->dec_mem.p, pk.host.data(), pk.host.size(), cudaMemcpyHostToDevice));
+  const unsigned char* base = static_cast<const unsigned char*>(c->dec_mem.p);
+  auto P = [&](const std::string& name) { return reinterpret_cast<const float*>(base + off.at(name)); };
+  auto fill_attn = [&](AttnW& a, const std::string& p, bool cross) {
+    a.ln_g = P(p + (cross ? ".lnq_g" : ".ln_g"));
+    a.ln_b = P(p + (cross ? ".lnq_b" : ".ln_b"));
+    a.ln2_g = cross ? P(p + ".lnkv_g") : nullptr;
+    a.ln2_b = cross ? P(p + ".lnkv_b") : nullptr;
+    a.wqkv = P(p + ".wqkv");
+    a.bqkv = P(p + ".bqkv");
+    a.wo = P(p + ".wo");
+    a.bo = P(p + ".bo");
+  };
+  auto fill_mlp = [&](MlpW& m, const std::string& p) {
+    m.ln_g = P(p + ".ln_g");
+    m.ln_b = P(p + ".ln_b");
+    m.w1 = P(p + ".w1");
+    m.b1 = P(p + ".b1");
+    m.w2 = P(p + ".w2");
+    m.b2 = P(p + ".b2");
+  };
+  EncW& e = c->enc;
+  e.patch_w = P("enc.patch_w");
+  e.patch_b = P("enc.patch_b");
+  e.pos = P("enc.pos");
+  e.norm_g = P("enc.norm_g");
+  e.norm_b = P("enc.norm_b");
+  e.layers = cfg->enc_layers;
+  for (int l = 0; l < cfg->enc_layers; ++l) {
+    fill_attn(e.self[l], "enc.l" + std::to_string(l) + ".self", false);
+    fill_mlp(e.mlp[l], "enc.l" + std::to_string(l) + ".mlp");
+  }
+  BodyW& b = c->body;
+  b.token_init = P("body.token_init");
+  b.p2d_init = P("body.p2d_init");
+  b.p3d_init = P("body.p3d_init");
+  b.norm_g = P("body.norm_g");
+  b.norm_b = P("body.norm_b");
+  b.head_params_w = P("body.head_params.w");
+  b.head_params_b = P("body.head_params.b");
+  b.head_cam_w = P("body.head_cam.w");
+  b.head_cam_b = P("body.head_cam.b");
+  b.phi2d_w = P("body.phi2d.w");
+  b.phi2d_b = P("body.phi2d.b");
+  b.phi3d_w = P("body.phi3d.w");
+  b.phi3d_b = P("body.phi3d.b");
+  b.prompt_box_w = P("body.prompt_box.w");
+  b.prompt_box_b = P("body.prompt_box.b");
+  b.layers = cfg->body_layers;
+  for (int l = 0; l < cfg->body_layers; ++l) {
+    const std::string p = "body.l" + std::to_string(l);
+    fill_attn(b.self[l], p + ".self", false);
+    fill_attn(b.cross[l], p + ".cross", true);
+    fill_mlp(b.mlp[l], p + ".mlp");
+  }
+  HandW& h = c->hand;
+  h.token_init = P("hand.token_init");
+  h.p_init = P("hand.p_init");
+  h.norm_g = P("hand.norm_g");
+  h.norm_b = P("hand.norm_b");
+  h.head_rot_w = P("hand.head_rot.w");
+  h.head_rot_b = P("hand.head_rot.b");
+  h.head_cam_w = P("hand.head_cam.w");
+  h.head_cam_b = P("hand.head_cam.b");
+  h.phi2d_w = P("hand.phi2d.w");
+  h.phi2d_b = P("hand.phi2d.b");
+  h.canon_pts = P("hand.canon_pts");
+  h.layers = cfg->hand_layers;
+  for (int l = 0; l < cfg->hand_layers; ++l) {
+    const std::string p = "hand.l" + std::to_string(l);
+    fill_attn(h.self[l], p + ".self", false);
+    fill_attn(h.cross[l], p + ".cross", true);
+    fill_mlp(h.mlp[l], p + ".mlp");
+  }
+  // the body decoder's FK uses the decoder template's rest joints; the
+  // body template upload patches it in (fsb_load_template)
+  c->body.joints_rest = c->has_tmpl[FSB_SMPL] ? c->tmpl[FSB_SMPL].joints_rest : nullptr;
+  c->cfg = *cfg;
+  c->has_decoder = true;
+  c->ws_frames = 0;  // re-reserve for the new shapes
+  return FSB_OK;
+}
+
+int fsb_load_template(fsb_ctx* c, int which, int nv, const float* v_rest, const float* joints_rest,
+                      const int64_t* parents, const float* skin_weights, const float* shape_basis) {
+  if (which != FSB_MHR && which != FSB_SMPL) return fail(c, FSB_ERR_USAGE, "template id must be 0 (mhr) or 1 (smpl)");
+  if (nv <= 0) return fail(c, FSB_ERR_SHAPE, "template needs vertices");
+  static const int64_t kPar[FSB_NJ] = {-1, 0, 1, 2, 3, 4, 0, 6, 7, 8, 0, 10, 11, 12, 3, 14, 15, 16, 3, 18, 19, 20};
+  for (int j = 0; j < FSB_NJ; ++j)
+    if (parents[j] != kPar[j]) return fail(c, FSB_ERR_USAGE, "only the 22-joint toy kinematic tree is supported");
+  int maxnz = 0;
+  for (int v = 0; v < nv; ++v) {
+    int nz = 0;
+    for (int j = 0; j < FSB_NJ; ++j) nz += skin_weights[(size_t)v * FSB_NJ + j] != 0.0f;
+    maxnz = nz > maxnz ? nz : maxnz;
+  }
+  const int NZ = maxnz <= 2 ? 2 : (maxnz <= 4 ? 4 : (maxnz <= 8 ? 8 : -1));
+  if (NZ < 0) return fail(c, FSB_ERR_USAGE, "skin weights with %d nonzeros per vertex (max 8)", maxnz);
+  std::vector<int16_t> sj((size_t)nv * NZ, 0);
+  std::vector<float> sw((size_t)nv * NZ, 0.0f);
+  for (int v = 0; v < nv; ++v) {
+    int z = 0;
+    for (int j = 0; j < FSB_NJ; ++j) {
+      const float w = skin_weights[(size_t)v * FSB_NJ + j];
+      if (w != 0.0f) {
+        sj[(size_t)v * NZ + z] = (int16_t)j;
+        sw[(size_t)v * NZ + z] = w;
+        ++z;
+      }
+    }
+  }
+  Packer pk;
+  const size_t o_v = pk.add(v_rest, (size_t)nv * 12);
+  const size_t o_s = pk.add(shape_basis, (size_t)nv * 30 * 4);
+  const size_t o_j = pk.add(sj.data(), sj.size() * 2);
+  const size_t o_w = pk.add(sw.data(), sw.size() * 4);
+  const size_t o_g = pk.add(joints_rest, FSB_NJ * 12);
+  DevMem& m = c->tmpl_mem[which];
+  FSB_CUDA(c, m.alloc(pk.host.size()));
+  FSB_CUDA(c, cudaMemcpy(m.p, pk.host.data(), pk.host.size(), cudaMemcpyHostToDevice));
+  const unsigned char* base = static_cast<const unsigned char*>(m.p);
+  TemplateDev& t = c->tmpl[which];
+  t.nv = nv;
+  t.nnz = NZ;
+  t.v_rest = reinterpret_cast<const float*>(base + o_v);
+  t.shape_basis = reinterpret_cast<const float*>(base + o_s);
+  t.skin_j = reinterpret_cast<const int16_t*>(base + o_j);
+  t.skin_w = reinterpret_cast<const float*>(base + o_w);
+  t.joints_rest = reinterpret_cast<const float*>(base + o_g);
+  c->has_tmpl[which] = true;
+  if (which == FSB_SMPL) c->body.joints_rest = t.joints_rest;
+  if (c->have_graph) {
+    cudaGraphExecDestroy(c->gexec);
+    c->gexec = nullptr;
+    c->have_graph = false;
+  }
+  return FSB_OK;
+}
+
+int fsb_load_projector(fsb_ctx* c, int n_sub, int h1, int h2, const int64_t* corners, const float* bary,
+                       const float* w1, const float* b1, const float* w2, const float* b2, const float* w3,
+                       const float* b3, const float* mask) {
+  if (n_sub <= 0 || h1 <= 0 || h2 <= 0) return fail(c, FSB_ERR_SHAPE, "projector sizes must be positive");
+  const int K = 3 * n_sub;
+  std::vector<int32_t> cr((size_t)n_sub * 3);
+  for (size_t i = 0; i < cr.size(); ++i) cr[i] = (int32_t)corners[i];
+  // K-major bf16 copies (N x K) for the tensor-core GEMMs
+  std::vector<__nv_bfloat16> w1t((size_t)h1 * K), w2t((size_t)h2 * h1);
+  for (int k = 0; k < K; ++k)
+    for (int n = 0; n < h1; ++n) w1t[(size_t)n * K + k] = __float2bfloat16_rn(w1[(size_t)k * h1 + n]);
+  for (int k = 0; k < h1; ++k)
+    for (int n = 0; n < h2; ++n) w2t[(size_t)n * h1 + k] = __float2bfloat16_rn(w2[(size_t)k * h2 + n]);
+  Packer pk;
+  const size_t o_c = pk.add(cr.data(), cr.size() * 4);
+  const size_t o_bw = pk.add(bary, (size_t)n_sub * 12);
+  const size_t o_w1 = pk.add(w1, (size_t)K * h1 * 4);
+  const size_t o_b1 = pk.add(b1, (size_t)h1 * 4);
+  const size_t o_w2 = pk.add(w2, (size_t)h1 * h2 * 4);
+  const size_t o_b2 = pk.add(b2, (size_t)h2 * 4);
+  const size_t o_w3 = pk.add(w3, (size_t)h2 * 76 * 4);
+  const size_t o_b3 = pk.add(b3, 76 * 4);
+  const size_t o_m = pk.add(mask, 76 * 4);
+  const size_t o_w1t = pk.add(w1t.data(), w1t.size() * 2);
+  const size_t o_w2t = pk.add(w2t.data(), w2t.size() * 2);
+  FSB_CUDA(c, c->proj_mem.alloc(pk.host.size()));
+  FSB_CUDA(c, cudaMemcpy(c->proj_mem.p, pk.host.data(), pk.host.size(), cudaMemcpyHostToDevice));
+  const unsigned char* base = static_cast<const unsigned char*>(c->proj_mem.p);
+  ProjectorDev& p = c->proj;
+  p.n_sub = n_sub;
+  p.h1 = h1;
+  p.h2 = h2;
+  p.corners = reinterpret_cast<const int32_t*>(base + o_c);
+  p.bw = reinterpret_cast<const float*>(base + o_bw);
+  p.w1 = reinterpret_cast<const float*>(base + o_w1);
+  p.b1 = reinterpret_cast<const float*>(base + o_b1);
+  p.w2 = reinterpret_cast<const float*>(base + o_w2);
+  p.b2 = reinterpret_cast<const float*>(base + o_b2);
+  p.w3 = reinterpret_cast<const float*>(base + o_w3);
+  p.b3 = reinterpret_cast<const float*>(base + o_b3);
+  p.mask = reinterpret_cast<const float*>(base + o_m);
+  p.w1t_bf16 = reinterpret_cast<const __nv_bfloat16*>(base + o_w1t);
+  p.w2t_bf16 = reinterpret_cast<const __nv_bfloat16*>(base + o_w2t);
+  c->has_proj = true;
+  c->ws_frames = 0;
+  return FSB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// stages
+
+int fsb_boxes_crops(fsb_ctx* c, const float* images, int B, int H, int W, const float* kp, double alpha, int S,
+                    double* boxes, float* prompt, float* crops, int32_t* taps, void* stream) {
+  if (B < 0 || H < 2 || W < 2) return fail(c, FSB_ERR_SHAPE, "boxes_crops: bad image shape %dx%d", H, W);
+  if (S < 2 || S > 512) return fail(c, FSB_ERR_USAGE, "out_size must be in [2, 512]");
+  if (!(alpha > 0)) return fail(c, FSB_ERR_USAGE, "alpha must be positive");
+  if (!boxes || !prompt) return fail(c, FSB_ERR_USAGE, "boxes and prompt outputs are required");
+  FSB_CUDA(c, launch_boxes_crops(images, kp, B, H, W, S, alpha, boxes, prompt, crops, taps, c->d_flag,
+                                 (cudaStream_t)stream));
+  c->launches += B > 0;
+  return FSB_OK;
+}
+
+int fsb_bilinear(fsb_ctx* c, const float* image, int H, int W, int C, const float* grid, int64_t n, float* out,
+                 void* stream) {
+  if (H < 1 || W < 1 || C < 1 || n < 0) return fail(c, FSB_ERR_SHAPE, "bilinear: bad shapes");
+  FSB_CUDA(c, launch_bilinear(image, H, W, C, grid, n, out, c->d_flag, (cudaStream_t)stream));
+  c->launches += n > 0;
+  return FSB_OK;
+}
+
+int fsb_body_boxes(fsb_ctx* c, const float* kp, int n, int W, int H, double* out, void* stream) {
+  if (n < 0 || W < 2 || H < 2) return fail(c, FSB_ERR_SHAPE, "body_boxes: bad shapes");
+  FSB_CUDA(c, launch_body_boxes(kp, n, W, H, out, (cudaStream_t)stream));
+  c->launches += n > 0;
+  return FSB_OK;
+}
+
+int fsb_hand_boxes(fsb_ctx* c, const double* wrists, const double* body, int n, double alpha, int W, int H,
+                   double* out, void* stream) {
+  if (!(alpha > 0)) return fail(c, FSB_ERR_USAGE, "alpha must be positive");
+  FSB_CUDA(c, launch_hand_boxes(wrists, body, n, alpha, W, H, out, (cudaStream_t)stream));
+  c->launches += n > 0;
+  return FSB_OK;
+}
+
+int fsb_crop_grid(fsb_ctx* c, const double* boxes, int n, int S, float* out, void* stream) {
+  if (S < 2) return fail(c, FSB_ERR_USAGE, "out_size must be >= 2");
+  FSB_CUDA(c, launch_crop_grid(boxes, n, S, out, (cudaStream_t)stream));
+  c->launches += n > 0;
+  return FSB_OK;
+}
+
+int fsb_bridge(fsb_ctx* c, const float* v, int B, int nv, const int32_t* corners, const float* w, int nt, float* out,
+               void* stream) {
+  if (B < 0 || nv <= 0 || nt < 0) return fail(c, FSB_ERR_SHAPE, "bridge: bad shapes");
+  FSB_CUDA(c, launch_bridge(v, B, nv, corners, w, nt, out, (cudaStream_t)stream));
+  c->launches += (int64_t)B * nt > 0;
+  return FSB_OK;
+}
+
+int fsb_encode(fsb_ctx* c, const float* crops, int n, float* feats, int precision, void* stream) {
+  if (!c->has_decoder) return fail(c, FSB_ERR_USAGE, "encode: no decoder loaded");
+  if (precision != FSB_FP32) return fail(c, FSB_ERR_USAGE, "encode: precision %d not available yet", precision);
+  if (!default_model(c->cfg))
+    return fail(c, FSB_ERR_USAGE, "encode: the fused fp32 encoder supports the default DecoderConfig only");
+  FSB_CUDA(c, launch_encoder_f32(crops, n, c->enc, feats, c->d_flag, (cudaStream_t)stream));
+  c->counters.encode += 1;
+  c->counters.encoded_crops += n;
+  c->launches += n > 0;
+  return FSB_OK;
+}
+
+static int decode_common(fsb_ctx* c, DecodeArgs& a, int precision, cudaStream_t st) {
+  if (!c->has_decoder) return fail(c, FSB_ERR_USAGE, "decode: no decoder loaded");
+  if (a.nbody > 0 && !c->has_tmpl[FSB_SMPL])
+    return fail(c, FSB_ERR_USAGE, "decode: the body decoder needs its template (fsb_load_template SMPL)");
+  if (precision != FSB_FP32) return fail(c, FSB_ERR_USAGE, "decode: precision %d not available yet", precision);
+  if (!default_model(c->cfg))
+    return fail(c, FSB_ERR_USAGE, "decode: the fused fp32 decoders support the default DecoderConfig only");
+  if ((a.body_sel >> c->cfg.body_layers) != 0u || (a.hand_sel >> c->cfg.hand_layers) != 0u)
+    return fail(c, FSB_ERR_USAGE, "selection out of range");
+  a.nonfinite = c->d_flag;
+  FSB_CUDA(c, launch_decoders_f32(a, c->body, c->hand, st));
+  c->launches += (a.nbody + a.nhand) > 0;
+  const int nb = layer_count(a.body_sel);
+  c->counters.fk += (int64_t)a.nbody * nb + (int64_t)a.nhand * layer_count(a.hand_sel);
+  c->counters.project += (int64_t)a.nbody * nb + (int64_t)a.nhand * layer_count(a.hand_sel);
+  c->counters.intermediate += (int64_t)a.nbody * nb;
+  return FSB_OK;
+}
+
+int fsb_decode_body(fsb_ctx* c, const float* feats, int B, int feat_stride, const float* prompts, uint32_t sel,
+                    float* params, float* cam, float* inter, int precision, void* stream) {
+  DecodeArgs a{};
+  a.feats = feats;
+  a.prompts = prompts;
+  a.nbody = B;
+  a.nhand = 0;
+  a.body_feat_stride = feat_stride;
+  a.body_sel = sel;
+  a.body_params = params;
+  a.body_cam = cam;
+  a.inter = inter;
+  return decode_common(c, a, precision, (cudaStream_t)stream);
+}
+
+int fsb_decode_hands(fsb_ctx* c, const float* feats, int n, uint32_t sel, float* rots, int precision, void* stream) {
+  DecodeArgs a{};
+  a.feats = feats;
+  a.nbody = 0;
+  a.nhand = n;
+  a.body_feat_stride = 2;
+  a.hand_feat_first = 0;
+  a.hand_sel = sel;
+  a.hand_rots = rots;
+  return decode_common(c, a, precision, (cudaStream_t)stream);
+}
+
+int fsb_decode_frames(fsb_ctx* c, const float* feats, int B, const float* prompts, uint32_t body_sel,
+                      uint32_t hand_sel, float* params, float* cam, float* rots, float* merged, int precision,
+                      void* stream) {
+  DecodeArgs a{};
+  a.feats = feats;
+  a.prompts = prompts;
+  a.nbody = B;
+  a.nhand = 2 * B;
+  a.body_feat_stride = 3;
+  a.hand_feat_first = 1;
+  a.body_sel = body_sel;
+  a.hand_sel = hand_sel;
+  a.body_params = params;
+  a.body_cam = cam;
+  a.hand_rots = rots;
+  a.merged = merged;
+  return decode_common(c, a, precision, (cudaStream_t)stream);
+}
+
+int fsb_fk(fsb_ctx* c, int which, const float* poses, int B, float* joints, float* rel, void* stream) {
+  if (which != FSB_MHR && which != FSB_SMPL) return fail(c, FSB_ERR_USAGE, "bad template id");
+  if (!c->has_tmpl[which]) return fail(c, FSB_ERR_USAGE, "fk: template %d not loaded", which);
+  FSB_CUDA(c, launch_fk(poses, FSB_PARAM_DIM, B, c->tmpl[which].joints_rest, joints, rel, (cudaStream_t)stream));
+  c->launches += B > 0;
+  return FSB_OK;
+}
+
+int fsb_skin(fsb_ctx* c, int which, const float* poses, int B, float* verts, void* stream) {
+  if (which != FSB_MHR && which != FSB_SMPL) return fail(c, FSB_ERR_USAGE, "bad template id");
+  if (!c->has_tmpl[which]) return fail(c, FSB_ERR_USAGE, "skin: template %d not loaded", which);
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = ensure_ws(c, B, st);
+  if (rc) return rc;
+  FSB_CUDA(c, launch_fk(poses, FSB_PARAM_DIM, B, c->tmpl[which].joints_rest, nullptr, c->w_rel, st));
+  FSB_CUDA(c, launch_lbs(c->tmpl[which], c->w_rel, poses, FSB_PARAM_DIM, B, verts, c->d_flag, st));
+  c->launches += 2 * (B > 0);
+  return FSB_OK;
+}
+
+static int run_mlp(fsb_ctx* c, int B, float* theta, int precision, cudaStream_t st) {
+  const ProjectorDev& p = c->proj;
+  if (precision != FSB_FP32) return fail(c, FSB_ERR_USAGE, "projector: precision %d not available yet", precision);
+  FSB_CUDA(c, launch_gemm_f32(c->w_x, 3 * p.n_sub, p.w1, p.b1, nullptr, c->w_h1, p.h1, B, p.h1, 3 * p.n_sub, 1,
+                              nullptr, st));
+  FSB_CUDA(c, launch_gemm_f32(c->w_h1, p.h1, p.w2, p.b2, nullptr, c->w_h2, p.h2, B, p.h2, p.h1, 1, nullptr, st));
+  FSB_CUDA(c, launch_gemm_f32(c->w_h2, p.h2, p.w3, p.b3, p.mask, theta, FSB_PARAM_DIM, B, FSB_PARAM_DIM, p.h2, 0,
+                              c->d_flag, st));
+  c->launches += 3;
+  return FSB_OK;
+}
+
+int fsb_project_vertices(fsb_ctx* c, const float* v_mhr, int B, int nv, float* theta, int precision,
+                         void* stream) {
+  if (!c->has_proj) return fail(c, FSB_ERR_USAGE, "project: no projector loaded");
+  if (nv <= 0) return fail(c, FSB_ERR_SHAPE, "project: bad vertex count");
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = ensure_ws(c, B, st);
+  if (rc) return rc;
+  FSB_CUDA(c, launch_proj_inputs_v(v_mhr, nv, c->proj, B, c->w_x, nullptr, 3 * c->proj.n_sub, st));
+  c->launches += B > 0;
+  return run_mlp(c, B, theta, precision, st);
+}
+
+static int skin_project_impl(fsb_ctx* c, const float* params, int B, float* v_mhr, float* theta, float* j_smpl,
+                             float* v_smpl, int precision, cudaStream_t st) {
+  if (!c->has_proj || !c->has_tmpl[FSB_MHR] || !c->has_tmpl[FSB_SMPL])
+    return fail(c, FSB_ERR_USAGE, "skin_project: projector or templates missing");
+  const TemplateDev& mhr = c->tmpl[FSB_MHR];
+  FSB_CUDA(c, launch_fk(params, FSB_PARAM_DIM, B, mhr.joints_rest, nullptr, c->w_rel, st));
+  if (v_mhr) FSB_CUDA(c, launch_lbs(mhr, c->w_rel, params, FSB_PARAM_DIM, B, v_mhr, c->d_flag, st));
+  FSB_CUDA(c, launch_proj_inputs(mhr, c->proj, c->w_rel, params, FSB_PARAM_DIM, B, c->w_x, nullptr,
+                                 3 * c->proj.n_sub, st));
+  c->launches += 2 + (v_mhr != nullptr);
+  int rc = run_mlp(c, B, theta, precision, st);
+  if (rc) return rc;
+  FSB_CUDA(c, launch_fk(theta, FSB_PARAM_DIM, B, c->tmpl[FSB_SMPL].joints_rest, j_smpl, v_smpl ? c->w_rel2 : nullptr,
+                        st));
+  c->launches += 1;
+  if (v_smpl) {
+    FSB_CUDA(c, launch_lbs(c->tmpl[FSB_SMPL], c->w_rel2, theta, FSB_PARAM_DIM, B, v_smpl, c->d_flag, st));
+    c->launches += 1;
+  }
+  return FSB_OK;
+}
+
+int fsb_skin_project(fsb_ctx* c, const float* params, int B, float* v_mhr, float* theta, float* j_smpl,
+                     float* v_smpl, int precision, void* stream) {
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = ensure_ws(c, B, st);
+  if (rc) return rc;
+  return skin_project_impl(c, params, B, v_mhr, theta, j_smpl, v_smpl, precision, st);
+}
+
+static int frame_batch_launches(fsb_ctx* c, const float* images, int B, int H, int W, const float* kp, double alpha,
+                                uint32_t bsel, uint32_t hsel, int precision, const fsb_frame_outputs& o,
+                                cudaStream_t st) {
+  const int S = c->cfg.crop_size;
+  double* boxes = o.boxes ? o.boxes : c->w_boxes;
+  float* prompt = o.prompt ? o.prompt : c->w_prompt;
+  float* crops = o.crops ? o.crops : c->w_crops;
+  float* feats = o.feats ? o.feats : c->w_feats;
+  float* params = o.body_params ? o.body_params : c->w_params;
+  float* cam = o.body_cam ? o.body_cam : c->w_cam;
+  float* rots = o.hand_rots ? o.hand_rots : c->w_rots;
+  int rc = fsb_boxes_crops(c, images, B, H, W, kp, alpha, S, boxes, prompt, crops, nullptr, st);
+  if (rc) return rc;
+  rc = fsb_encode(c, crops, 3 * B, feats, precision, st);
+  if (rc) return rc;
+  rc = fsb_decode_frames(c, feats, B, prompt, bsel, hsel, params, cam, rots, o.merged, precision, st);
+  if (rc) return rc;
+  return skin_project_impl(c, o.merged, B, o.v_mhr, o.theta, o.j_smpl, o.v_smpl, precision, st);
+}
+
+int fsb_frame_batch(fsb_ctx* c, const float* images, int B, int H, int W, const float* kp, double alpha,
+                    uint32_t body_sel, uint32_t hand_sel, int precision, const fsb_frame_outputs* out,
+                    void* stream) {
+  if (!out || !out->merged || !out->theta || !out->j_smpl)
+    return fail(c, FSB_ERR_USAGE, "frame_batch: merged, theta and j_smpl outputs are required");
+  if (!c->has_decoder || !c->has_proj || !c->has_tmpl[0] || !c->has_tmpl[1])
+    return fail(c, FSB_ERR_USAGE, "frame_batch: decoder, templates and projector must be loaded");
+  if (B <= 0) return FSB_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = ensure_ws(c, B, st);
+  if (rc) return rc;
+  const bool use_graph = c->graphs && st != nullptr && !capturing(st);
+  if (!use_graph) return frame_batch_launches(c, images, B, H, W, kp, alpha, body_sel, hand_sel, precision, *out, st);
+  GraphKey k{};
+  k.B = B;
+  k.H = H;
+  k.W = W;
+  k.precision = precision;
+  k.bsel = body_sel;
+  k.hsel = hand_sel;
+  k.alpha = alpha;
+  const void* ptrs[16] = {images, kp, out->boxes, out->prompt, out->crops, out->feats, out->body_params,
+                          out->body_cam, out->hand_rots, out->merged, out->v_mhr, out->theta, out->j_smpl,
+                          out->v_smpl, nullptr, nullptr};
+  memcpy(k.ptrs, ptrs, sizeof ptrs);
+  k.stream = st;
+  if (!(c->have_graph && c->gkey == k)) {
+    if (c->have_graph) {
+      cudaGraphExecDestroy(c->gexec);
+      c->gexec = nullptr;
+      c->have_graph = false;
+    }
+    const fsb_counters_t saved = c->counters;
+    const int64_t saved_l = c->launches;
+    FSB_CUDA(c, cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    rc = frame_batch_launches(c, images, B, H, W, kp, alpha, body_sel, hand_sel, precision, *out, st);
+    cudaGraph_t g = nullptr;
+    cudaError_t ce = cudaStreamEndCapture(st, &g);
+    if (rc) {
+      if (g) cudaGraphDestroy(g);
+      return rc;
+    }
+    if (ce != cudaSuccess) return fail(c, FSB_ERR_CUDA, "graph capture: %s", cudaGetErrorString(ce));
+    size_t nn = 0;
+    cudaGraphGetNodes(g, nullptr, &nn);
+    ce = cudaGraphInstantiate(&c->gexec, g, 0);
+    cudaGraphDestroy(g);
+    if (ce != cudaSuccess) return fail(c, FSB_ERR_CUDA, "graph instantiate: %s", cudaGetErrorString(ce));
+    c->graph_nodes = (int)nn;
+    c->gkey = k;
+    c->have_graph = true;
+    c->counters = saved;
+    c->launches = saved_l;
+  }
+  FSB_CUDA(c, cudaGraphLaunch(c->gexec, st));
+  c->launches += c->graph_nodes;
+  c->counters.encode += 1;
+  c->counters.encoded_crops += 3 * B;
+  const int nb = layer_count(body_sel), nh = layer_count(hand_sel);
+  c->counters.fk += (int64_t)B * (nb + 2 * nh);
+  c->counters.project += (int64_t)B * (nb + 2 * nh);
+  c->counters.intermediate += (int64_t)B * nb;
+  return FSB_OK;
+}
+
+int fsb_nonfinite(fsb_ctx* c, int* flag, int reset) {
+  int h = 0;
+  FSB_CUDA(c, cudaDeviceSynchronize());
+  FSB_CUDA(c, cudaMemcpy(&h, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost));
+  if (reset) FSB_CUDA(c, cudaMemset(c->d_flag, 0, sizeof(int)));
+  if (flag) *flag = h;
+  return FSB_OK;
+}
+
+int fsb_counters(const fsb_ctx* c, fsb_counters_t* out) {
+  if (!c || !out) return FSB_ERR_USAGE;
+  *out = c->counters;
+  return FSB_OK;
+}
+
+int64_t fsb_kernel_launches(const fsb_ctx* c) { return c ? c->launches : 0; }
+
+}  // extern "C"

@@ -1,0 +1,105 @@
+// Shared definitions for the sm_100a kernels of the frame -> SMPL path.
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda_bf16.h>
+#include <stdint.h>
+
+#define FSB_NJ 22
+#define FSB_PARAM_DIM 76
+#define FSB_PROMPT_DIM 8
+
+
+// kinematic tree (reference bodymodel.py:29-32); identical for mhr and smpl
+__constant__ __device__ static const int8_t kParents[FSB_NJ] = {
+    -1, 0, 1, 2, 3, 4, 0, 6, 7, 8, 0, 10, 11, 12, 3, 14, 15, 16, 3, 18, 19, 20};
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+
+// sets the context's device-side non-finite flag (mapped to NumericError)
+__device__ __forceinline__ void flag_nonfinite(int* flag, float v) {
+  if (flag != nullptr && !isfinite(v)) atomicOr(flag, 1);
+}
+
+// ---------------------------------------------------------------------------
+// forward kinematics (reference bodymodel.py:172-240).  One warp per pose:
+// lanes 0..21 evaluate Rodrigues for their joint, then lane 0 walks the
+// chain in joint order (parents[j] < j).  Output per joint: world rotation
+// rw[9], world translation tw[3], rest-relative translation at[3].
+// ---------------------------------------------------------------------------
+struct FKOut {
+  float rw[FSB_NJ][9];
+  float tw[FSB_NJ][3];
+  float at[FSB_NJ][3];
+};
+
+__device__ __forceinline__ void rodrigues3(float wx, float wy, float wz, float* r) {
+  const float t2 = __fadd_rn(__fadd_rn(__fmul_rn(wx, wx), __fmul_rn(wy, wy)), __fmul_rn(wz, wz));
+  const bool small = t2 < 1e-12f;
+  float s, c;
+  if (small) {
+    s = 1.0f - t2 * (1.0f / 6.0f);
+    c = 0.5f - t2 * (1.0f / 24.0f);
+  } else {
+    const float th = sqrtf(t2);
+    float sn, cs;
+    sincosf(th, &sn, &cs);
+    s = sn / th;
+    c = (1.0f - cs) / t2;
+  }
+  r[0] = 1.0f - (wy * wy + wz * wz) * c;
+  r[1] = wx * wy * c - wz * s;
+  r[2] = wx * wz * c + wy * s;
+  r[3] = wx * wy * c + wz * s;
+  r[4] = 1.0f - (wx * wx + wz * wz) * c;
+  r[5] = wy * wz * c - wx * s;
+  r[6] = wx * wz * c - wy * s;
+  r[7] = wy * wz * c + wx * s;
+  r[8] = 1.0f - (wx * wx + wy * wy) * c;
+}
+
+// warp-cooperative FK; `pose` points at the 66 rotation params (shared or
+// global), `grest` at the 22x3 rest joints.  All lanes of the warp must call.
+__device__ __forceinline__ void fk_warp(const float* pose, const float* grest, FKOut& o, int lane) {
+  float rl[9];
+  if (lane < FSB_NJ) {
+    rodrigues3(pose[3 * lane], pose[3 * lane + 1], pose[3 * lane + 2], rl);
+#pragma unroll
+    for (int e = 0; e < 9; ++e) o.rw[lane][e] = rl[e];  // local rotation, composed below
+  }
+  __syncwarp();
+  if (lane == 0) {
+    for (int j = 0; j < FSB_NJ; ++j) {
+      const int p = kParents[j];
+      float tl[3];
+      for (int a = 0; a < 3; ++a)
+        tl[a] = (p < 0) ? grest[3 * j + a] : grest[3 * j + a] - grest[3 * p + a];
+      if (p >= 0) {
+        float loc[9];
+        for (int e = 0; e < 9; ++e) loc[e] = o.rw[j][e];
+        const float* rp = o.rw[p];
+        for (int a = 0; a < 3; ++a) {
+          for (int b = 0; b < 3; ++b)
+            o.rw[j][3 * a + b] = rp[3 * a] * loc[b] + rp[3 * a + 1] * loc[3 + b] + rp[3 * a + 2] * loc[6 + b];
+          o.tw[j][a] = (rp[3 * a] * tl[0] + rp[3 * a + 1] * tl[1] + rp[3 * a + 2] * tl[2]) + o.tw[p][a];
+        }
+      } else {
+        for (int a = 0; a < 3; ++a) o.tw[j][a] = tl[a];
+      }
+      const float* rj = o.rw[j];
+      for (int a = 0; a < 3; ++a)
+        o.at[j][a] = o.tw[j][a] - (rj[3 * a] * grest[3 * j] + rj[3 * a + 1] * grest[3 * j + 1] +
+                                   rj[3 * a + 2] * grest[3 * j + 2]);
+    }
+  }
+  __syncwarp();
+}

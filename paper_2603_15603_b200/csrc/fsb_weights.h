@@ -1,0 +1,126 @@
+// Device-side weight tables of the frozen encoder/decoders and body models.
+// All pointers are device addresses into one arena owned by the fsb_ctx.
+// Linear weights are stored (in, out) row-major like the reference
+// (decoder.py:74-154: y = x @ W + b); Q|K|V are concatenated to one (D, 3D)
+// matrix so a block issues one projection GEMM.
+#pragma once
+#include <stdint.h>
+#include <cuda_bf16.h>
+
+#define FSB_MAX_LAYERS 32
+
+struct AttnW {
+  const float* ln_g;   // self: ln; cross: lnq
+  const float* ln_b;
+  const float* ln2_g;  // cross only: lnkv
+  const float* ln2_b;
+  const float* wqkv;   // (D, 3D)
+  const float* bqkv;   // (3D)
+  const float* wo;     // (D, D)
+  const float* bo;
+};
+
+struct MlpW {
+  const float* ln_g;
+  const float* ln_b;
+  const float* w1;  // (D, 4D)
+  const float* b1;
+  const float* w2;  // (4D, D)
+  const float* b2;
+};
+
+struct EncW {
+  const float* patch_w;  // (p*p*3, D)
+  const float* patch_b;
+  const float* pos;      // (n_patch, D)
+  const float* norm_g;
+  const float* norm_b;
+  int layers;
+  AttnW self[FSB_MAX_LAYERS];
+  MlpW mlp[FSB_MAX_LAYERS];
+};
+
+struct BodyW {
+  const float* token_init;  // (51, D)
+  const float* p2d_init;    // (22, D)
+  const float* p3d_init;    // (22, D)
+  const float* norm_g;
+  const float* norm_b;
+  const float* head_params_w;  // (D, 76)
+  const float* head_params_b;
+  const float* head_cam_w;     // (D, 3)
+  const float* head_cam_b;
+  const float* phi2d_w;        // (2, D)
+  const float* phi2d_b;
+  const float* phi3d_w;        // (3, D)
+  const float* phi3d_b;
+  const float* prompt_box_w;   // (8, 4D)
+  const float* prompt_box_b;
+  const float* joints_rest;    // (22, 3) of the decoder's template
+  int layers;
+  AttnW self[8];
+  AttnW cross[8];
+  MlpW mlp[8];
+};
+
+struct HandW {
+  const float* token_init;  // (4, D)
+  const float* p_init;      // (3, D)
+  const float* norm_g;
+  const float* norm_b;
+  const float* head_rot_w;  // (D, 3)
+  const float* head_rot_b;
+  const float* head_cam_w;
+  const float* head_cam_b;
+  const float* phi2d_w;     // (2, D)
+  const float* phi2d_b;
+  const float* canon_pts;   // (3, 3)
+  int layers;
+  AttnW self[8];
+  AttnW cross[8];
+  MlpW mlp[8];
+};
+
+// body template on device (LBS / FK)
+struct TemplateDev {
+  int nv;
+  int nnz;                   // padded skin nonzeros per vertex (2, 4 or 8)
+  const float* v_rest;       // (nv, 3)
+  const float* shape_basis;  // (nv, 3, 10)
+  const int16_t* skin_j;     // (nv, nnz) joint ids, ascending, padded with 0
+  const float* skin_w;       // (nv, nnz) weights, padded with 0
+  const float* joints_rest;  // (22, 3)
+};
+
+// barycentric map + projector
+struct ProjectorDev {
+  int n_sub;              // V_sub
+  int h1, h2;             // hidden widths
+  const int32_t* corners; // (n_sub, 3) source vertex ids of the subsampled targets
+  const float* bw;        // (n_sub, 3) barycentric weights
+  const float* w1;        // (3*n_sub, h1) f32
+  const float* b1;
+  const float* w2;        // (h1, h2)
+  const float* b2;
+  const float* w3;        // (h2, 76)
+  const float* b3;
+  const float* mask;      // (76)
+  const __nv_bfloat16* w1t_bf16;  // (h1, 3*n_sub) K-major copy for the tcgen05 path
+  const __nv_bfloat16* w2t_bf16;  // (h2, h1)
+};
+
+// arguments of the fused decoder launch (k_transformer.cu)
+struct DecodeArgs {
+  const float* feats;       // (ncrops, T, D)
+  const float* prompts;     // (nbody, 8)
+  int nbody, nhand;
+  int body_feat_stride;     // crop index of frame f's body feature = f * stride
+  int hand_feat_first;      // crop of hand h = first + (h / 2) * stride + (h % 2)
+  unsigned body_sel, hand_sel;
+  float* body_params;       // (nbody, 76)
+  float* body_cam;          // (nbody, 3)
+  float* hand_rots;         // (nhand, 3)
+  float* merged;            // (nbody, 76) or null: body params with hand rotations overwritten
+  float* inter;             // (nbody, body_layers, 76 + 3 + 44) or null: intermediate predictions
+  int* nonfinite;
+};

@@ -1,0 +1,387 @@
+// K4: forward kinematics, MHR linear-blend skinning, the barycentric bridge
+// into the projector input, the projector MLP (fp32 path) and SMPL FK.
+//
+// Reference: bodymodel.fk_batch (bodymodel.py:266-297), skin_batch (:334-368,
+// correctives off), projection.bridge (projection.py:187-203),
+// _projector_inputs (:447-465), _projector_mlp (:468-472).
+//
+// LBS is the bandwidth-bound kernel of the path: per mesh it writes
+// Nv x 12 B of vertices and reads ~1 KB of per-pose transforms.  The
+// template (rest vertices, 1-2 nonzero skin weights per vertex, shape basis;
+// ~4 MB at 18,439 vertices) is read once per CTA into registers and reused
+// across a group of meshes, so HBM traffic is the vertex stream itself.
+#include "fsb_common.cuh"
+#include "fsb_weights.h"
+
+// ---------------------------------------------------------------------------
+// FK: one warp per pose.  rel (B, 22, 3, 4) = [R_world | t_world - R_world g]
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(128) k_fk(const float* __restrict__ poses, int ld_pose, int B,
+                                            const float* __restrict__ grest, float* __restrict__ joints,
+                                            float* __restrict__ rel) {
+  __shared__ FKOut fk[4];
+  __shared__ float pose_s[4][66];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int b = blockIdx.x * 4 + warp;
+  if (b >= B) return;  // warp-uniform
+  for (int i = lane; i < 66; i += 32) pose_s[warp][i] = poses[(int64_t)b * ld_pose + i];
+  __syncwarp();
+  fk_warp(pose_s[warp], grest, fk[warp], lane);
+  if (lane < FSB_NJ) {
+    const int j = lane;
+    if (joints != nullptr)
+      for (int a = 0; a < 3; ++a) joints[((int64_t)b * FSB_NJ + j) * 3 + a] = fk[warp].tw[j][a];
+    if (rel != nullptr) {
+      float* r = rel + ((int64_t)b * FSB_NJ + j) * 12;
+      for (int a = 0; a < 3; ++a) {
+        r[4 * a + 0] = fk[warp].rw[j][3 * a + 0];
+        r[4 * a + 1] = fk[warp].rw[j][3 * a + 1];
+        r[4 * a + 2] = fk[warp].rw[j][3 * a + 2];
+        r[4 * a + 3] = fk[warp].at[j][a];
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// one vertex of LBS given the mesh's joint transforms A (22 x 12) and shape
+// coefficients (10): blend the nonzero joints, add shape offsets, apply.
+// ---------------------------------------------------------------------------
+template <int NZ>
+struct VertexTmpl {
+  int j[NZ];
+  float w[NZ];
+  float vr[3];
+  float sb[30];
+  __device__ void load(const TemplateDev& t, int v) {
+#pragma unroll
+    for (int z = 0; z < NZ; ++z) {
+      j[z] = t.skin_j[(int64_t)v * NZ + z];
+      w[z] = t.skin_w[(int64_t)v * NZ + z];
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) vr[c] = __ldg(t.v_rest + 3 * v + c);
+#pragma unroll
+    for (int k = 0; k < 30; ++k) sb[k] = __ldg(t.shape_basis + (int64_t)30 * v + k);
+  }
+  __device__ void apply(const float* A, const float* shp, float out[3]) const {
+    float T[12];
+#pragma unroll
+    for (int e = 0; e < 12; ++e) T[e] = 0.0f;
+#pragma unroll
+    for (int z = 0; z < NZ; ++z) {
+      const float4* a4 = reinterpret_cast<const float4*>(A + 12 * j[z]);
+#pragma unroll
+      for (int q = 0; q < 3; ++q) {
+        const float4 r = a4[q];
+        T[4 * q + 0] = fmaf(w[z], r.x, T[4 * q + 0]);
+        T[4 * q + 1] = fmaf(w[z], r.y, T[4 * q + 1]);
+        T[4 * q + 2] = fmaf(w[z], r.z, T[4 * q + 2]);
+        T[4 * q + 3] = fmaf(w[z], r.w, T[4 * q + 3]);
+      }
+    }
+    float vs[3];
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      float o = 0.0f;
+#pragma unroll
+      for (int k = 0; k < 10; ++k) o = fmaf(shp[k], sb[10 * c + k], o);
+      vs[c] = o + vr[c];
+    }
+#pragma unroll
+    for (int a = 0; a < 3; ++a) out[a] = fmaf(T[4 * a + 2], vs[2], fmaf(T[4 * a + 1], vs[1], T[4 * a] * vs[0])) + T[4 * a + 3];
+  }
+};
+
+constexpr int kLbsThreads = 256;
+constexpr int kLbsVPT = 2;     // vertices per thread
+constexpr int kLbsMeshes = 32; // meshes per CTA (template reuse factor)
+
+// grid: (ceil(nv / 512), ceil(B / 32))
+template <int NZ>
+__global__ void __launch_bounds__(kLbsThreads) k_lbs(TemplateDev t, const float* __restrict__ rel,
+                                                     const float* __restrict__ poses, int ld_pose, int B,
+                                                     float* __restrict__ verts, int* nonfinite) {
+  __shared__ __align__(16) float As[kLbsMeshes][FSB_NJ * 12];
+  __shared__ float Ss[kLbsMeshes][10];
+  const int m0 = blockIdx.y * kLbsMeshes;
+  const int nm = min(kLbsMeshes, B - m0);
+  for (int i = threadIdx.x; i < nm * FSB_NJ * 12; i += kLbsThreads)
+    As[i / (FSB_NJ * 12)][i % (FSB_NJ * 12)] = rel[(int64_t)m0 * FSB_NJ * 12 + i];
+  for (int i = threadIdx.x; i < nm * 10; i += kLbsThreads)
+    Ss[i / 10][i % 10] = poses[(int64_t)(m0 + i / 10) * ld_pose + 66 + i % 10];
+  VertexTmpl<NZ> vt[kLbsVPT];
+  int vid[kLbsVPT];
+#pragma unroll
+  for (int q = 0; q < kLbsVPT; ++q) {
+    vid[q] = blockIdx.x * kLbsThreads * kLbsVPT + q * kLbsThreads + threadIdx.x;
+    if (vid[q] < t.nv) vt[q].load(t, vid[q]);
+  }
+  __syncthreads();
+  bool bad = false;
+  for (int m = 0; m < nm; ++m) {
+    float* dst = verts + (int64_t)(m0 + m) * t.nv * 3;
+#pragma unroll
+    for (int q = 0; q < kLbsVPT; ++q) {
+      if (vid[q] < t.nv) {
+        float o[3];
+        vt[q].apply(As[m], Ss[m], o);
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          bad |= !isfinite(o[a]);
+          __stcs(dst + (int64_t)vid[q] * 3 + a, o[a]);
+        }
+      }
+    }
+  }
+  if (bad && nonfinite != nullptr) atomicOr(nonfinite, 1);
+}
+
+// ---------------------------------------------------------------------------
+// projector input (projection.py:447-465): centre the source mesh on vertex
+// 0, bridge the subsampled targets through their three corners, remove the
+// subsample centroid.  The needed MHR vertices are re-skinned here from the
+// L2-resident template instead of re-read from the V_mhr stream.
+// One CTA per mesh.
+// ---------------------------------------------------------------------------
+constexpr int kProjThreads = 512;
+
+template <int NZ>
+__device__ __forceinline__ void skin_one(const TemplateDev& t, int v, const float* A, const float* shp, float o[3]) {
+  VertexTmpl<NZ> vt;
+  vt.load(t, v);
+  vt.apply(A, shp, o);
+}
+
+// vertex sources for the projector input: re-skin from the template, or read
+// a caller-supplied vertex tensor (project_batch on arbitrary meshes)
+template <int NZ>
+struct SkinSource {
+  TemplateDev t;
+  const float* A;
+  const float* shp;
+  __device__ void get(int v, float o[3]) const { skin_one<NZ>(t, v, A, shp, o); }
+};
+struct VertexSource {
+  const float* V;  // (nv, 3) of this mesh
+  __device__ void get(int v, float o[3]) const {
+    o[0] = V[3 * v]; o[1] = V[3 * v + 1]; o[2] = V[3 * v + 2];
+  }
+};
+
+template <class Src>
+__device__ void proj_inputs_cta(const Src& src, const ProjectorDev& p, float* sm, int b, float* __restrict__ x,
+                                __nv_bfloat16* __restrict__ xb, int ldx) {
+  float* v0 = sm + 276;        // 3
+  float* red = sm + 280;       // 3 * 16 warps + 3
+  float* sub = sm + 336;       // n_sub * 3
+  const int tid = threadIdx.x;
+  if (tid == 0) src.get(0, v0);
+  __syncthreads();
+  float s[3] = {0.0f, 0.0f, 0.0f};
+  for (int i = tid; i < p.n_sub; i += kProjThreads) {
+    float acc[3] = {0.0f, 0.0f, 0.0f};
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      float o[3];
+      src.get(p.corners[3 * i + c], o);
+      const float wc = p.bw[3 * i + c];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) acc[a] = fmaf(wc, o[a] - v0[a], acc[a]);
+    }
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      sub[3 * i + a] = acc[a];
+      s[a] += acc[a];
+    }
+  }
+  const int warp = tid / 32, lane = tid % 32;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const float r = warp_sum(s[a]);
+    if (lane == 0) red[3 * warp + a] = r;
+  }
+  __syncthreads();
+  if (tid < 3) {
+    float tot = 0.0f;
+    for (int w = 0; w < kProjThreads / 32; ++w) tot += red[3 * w + tid];
+    red[52 + tid] = tot / (float)p.n_sub;
+  }
+  __syncthreads();
+  const float mx = red[52], my = red[53], mz = red[54];
+  for (int i = tid; i < 3 * p.n_sub; i += kProjThreads) {
+    const float m = (i % 3 == 0) ? mx : ((i % 3 == 1) ? my : mz);
+    const float v = sub[i] - m;
+    if (x != nullptr) x[(int64_t)b * ldx + i] = v;
+    if (xb != nullptr) xb[(int64_t)b * ldx + i] = __float2bfloat16_rn(v);
+  }
+}
+
+template <int NZ>
+__global__ void __launch_bounds__(kProjThreads) k_proj_inputs(TemplateDev t, ProjectorDev p,
+                                                              const float* __restrict__ rel,
+                                                              const float* __restrict__ poses, int ld_pose,
+                                                              float* __restrict__ x, __nv_bfloat16* __restrict__ xb,
+                                                              int ldx) {
+  extern __shared__ __align__(16) float sm[];
+  float* A = sm;               // 264
+  float* shp = sm + 264;       // 10
+  const int b = blockIdx.x, tid = threadIdx.x;
+  for (int i = tid; i < FSB_NJ * 12; i += kProjThreads) A[i] = rel[(int64_t)b * FSB_NJ * 12 + i];
+  if (tid < 10) shp[tid] = poses[(int64_t)b * ld_pose + 66 + tid];
+  __syncthreads();
+  proj_inputs_cta(SkinSource<NZ>{t, A, shp}, p, sm, b, x, xb, ldx);
+}
+
+__global__ void __launch_bounds__(kProjThreads) k_proj_inputs_v(const float* __restrict__ V, int nv, ProjectorDev p,
+                                                                float* __restrict__ x, __nv_bfloat16* __restrict__ xb,
+                                                                int ldx) {
+  extern __shared__ __align__(16) float sm[];
+  const int b = blockIdx.x;
+  proj_inputs_cta(VertexSource{V + (int64_t)b * nv * 3}, p, sm, b, x, xb, ldx);
+}
+
+// ---------------------------------------------------------------------------
+// fp32 GEMM for the projector MLP: C = act(A @ W + b) * mask, A (M, K) with
+// leading dim lda, W (K, N) row-major.  64x64 tiles, 4x4 per thread, every
+// output a sequential fused sum over k (batch-size independent).
+// ---------------------------------------------------------------------------
+constexpr int kGT = 64, kGK = 16;
+
+__global__ void __launch_bounds__(256) k_gemm_f32(const float* __restrict__ A, int lda,
+                                                   const float* __restrict__ W, const float* __restrict__ bias,
+                                                   const float* __restrict__ mask, float* __restrict__ C, int ldc,
+                                                   int M, int N, int K, int relu, int* nonfinite) {
+  __shared__ __align__(16) float As[kGK][kGT + 4];
+  __shared__ __align__(16) float Bs[kGK][kGT + 4];
+  const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
+  const int m0 = blockIdx.y * kGT, n0 = blockIdx.x * kGT;
+  float acc[4][4] = {};
+  for (int k0 = 0; k0 < K; k0 += kGK) {
+    for (int i = tid; i < kGT * kGK; i += 256) {
+      const int r = i / kGK, kk = i % kGK;  // A tile: coalesced along k
+      const int gm = m0 + r, gk = k0 + kk;
+      As[kk][r] = (gm < M && gk < K) ? A[(int64_t)gm * lda + gk] : 0.0f;
+      const int kb = i / kGT, c = i % kGT;  // W tile: coalesced along n
+      const int wk = k0 + kb, wn = n0 + c;
+      Bs[kb][c] = (wk < K && wn < N) ? W[(int64_t)wk * N + wn] : 0.0f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < kGK; ++kk) {
+      const float4 a = *reinterpret_cast<const float4*>(&As[kk][ty * 4]);
+      const float4 w = *reinterpret_cast<const float4*>(&Bs[kk][tx * 4]);
+      const float av[4] = {a.x, a.y, a.z, a.w}, wv[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(av[i], wv[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int gm = m0 + ty * 4 + i;
+    if (gm >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int gn = n0 + tx * 4 + j;
+      if (gn >= N) continue;
+      float v = acc[i][j] + bias[gn];
+      if (relu) v = fmaxf(v, 0.0f);
+      if (mask != nullptr) v *= mask[gn];
+      flag_nonfinite(nonfinite, v);
+      C[(int64_t)gm * ldc + gn] = v;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+// ---------------------------------------------------------------------------
+cudaError_t launch_fk(const float* poses, int ld_pose, int B, const float* grest, float* joints, float* rel,
+                      cudaStream_t st) {
+  if (B == 0) return cudaSuccess;
+  k_fk<<<(B + 3) / 4, 128, 0, st>>>(poses, ld_pose, B, grest, joints, rel);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_lbs(const TemplateDev& t, const float* rel, const float* poses, int ld_pose, int B, float* verts,
+                       int* nonfinite, cudaStream_t st) {
+  if (B == 0) return cudaSuccess;
+  dim3 grid((t.nv + kLbsThreads * kLbsVPT - 1) / (kLbsThreads * kLbsVPT), (B + kLbsMeshes - 1) / kLbsMeshes);
+  switch (t.nnz) {
+    case 2: k_lbs<2><<<grid, kLbsThreads, 0, st>>>(t, rel, poses, ld_pose, B, verts, nonfinite); break;
+    case 4: k_lbs<4><<<grid, kLbsThreads, 0, st>>>(t, rel, poses, ld_pose, B, verts, nonfinite); break;
+    case 8: k_lbs<8><<<grid, kLbsThreads, 0, st>>>(t, rel, poses, ld_pose, B, verts, nonfinite); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+// proj-input kernels take up to 336 + 3 * n_sub floats of dynamic smem;
+// allow the full 227 KB so any subsample size that fits can launch
+cudaError_t init_attrs_body() {
+  const int mx = 227 * 1024;
+  cudaError_t e = cudaFuncSetAttribute(k_proj_inputs<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_proj_inputs<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_proj_inputs<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_proj_inputs_v, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+  return e;
+}
+
+cudaError_t launch_proj_inputs(const TemplateDev& t, const ProjectorDev& p, const float* rel, const float* poses,
+                               int ld_pose, int B, float* x, __nv_bfloat16* xb, int ldx, cudaStream_t st) {
+  if (B == 0) return cudaSuccess;
+  const size_t smem = (336 + 3 * (size_t)p.n_sub) * sizeof(float);
+  switch (t.nnz) {
+#define FSB_PI(NZ)                                                                                   \
+  case NZ:                                                                                           \
+    k_proj_inputs<NZ><<<B, kProjThreads, smem, st>>>(t, p, rel, poses, ld_pose, x, xb, ldx);         \
+    break;
+    FSB_PI(2) FSB_PI(4) FSB_PI(8)
+#undef FSB_PI
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_proj_inputs_v(const float* V, int nv, const ProjectorDev& p, int B, float* x, __nv_bfloat16* xb,
+                                 int ldx, cudaStream_t st) {
+  if (B == 0) return cudaSuccess;
+  const size_t smem = (336 + 3 * (size_t)p.n_sub) * sizeof(float);
+  k_proj_inputs_v<<<B, kProjThreads, smem, st>>>(V, nv, p, x, xb, ldx);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gemm_f32(const float* A, int lda, const float* W, const float* bias, const float* mask, float* C,
+                            int ldc, int M, int N, int K, int relu, int* nonfinite, cudaStream_t st) {
+  if (M == 0) return cudaSuccess;
+  dim3 grid((N + kGT - 1) / kGT, (M + kGT - 1) / kGT);
+  k_gemm_f32<<<grid, 256, 0, st>>>(A, lda, W, bias, mask, C, ldc, M, N, K, relu, nonfinite);
+  return cudaGetLastError();
+}
+
+// projection.bridge (projection.py:187-203): out[b, t] = sum_c w[t, c] V[b, corner[t, c]]
+__global__ void k_bridge(const float* __restrict__ V, int B, int nv, const int32_t* __restrict__ corners,
+                         const float* __restrict__ w, int nt, float* __restrict__ out) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)B * nt) return;
+  const int b = (int)(idx / nt), t = (int)(idx % nt);
+  const float* Vb = V + (int64_t)b * nv * 3;
+  float acc[3] = {0.0f, 0.0f, 0.0f};
+  for (int c = 0; c < 3; ++c) {
+    const int v = corners[3 * t + c];
+    const float wc = w[3 * t + c];
+    for (int a = 0; a < 3; ++a) acc[a] = fmaf(wc, Vb[3 * v + a], acc[a]);
+  }
+  for (int a = 0; a < 3; ++a) out[idx * 3 + a] = acc[a];
+}
+
+cudaError_t launch_bridge(const float* V, int B, int nv, const int32_t* corners, const float* w, int nt, float* out,
+                          cudaStream_t st) {
+  const int64_t tot = (int64_t)B * nt;
+  if (tot == 0) return cudaSuccess;
+  k_bridge<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(V, B, nv, corners, w, nt, out);
+  return cudaGetLastError();
+}

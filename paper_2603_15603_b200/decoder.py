@@ -1,0 +1,230 @@
+"""Frozen encoder + pruned body/hand decoders.
+
+Drop-in for the reference ``fsb.decoder`` (pkg/src/fsb/decoder.py).  The
+weights are generated host-side with the reference's seeded RNG order
+(``synth.decoder_weights``, decoder.py:74-154), uploaded once per Decoder,
+and every forward pass runs in the fused CTA-per-crop / CTA-per-frame
+kernels of csrc/k_transformer.cu.
+"""
+
+from __future__ import annotations
+
+import json
+import os
+from dataclasses import asdict, dataclass, field
+
+import numpy as np
+
+from . import runtime
+from . import numkit as nk
+from .numkit import DTYPE, ShapeError, UsageError
+from .synth import NUM_JOINTS, PARAM_DIM, decoder_weights
+
+TOKEN_MHR = 0
+TOKEN_PROMPT = slice(1, 5)
+TOKEN_KP2D = slice(5, 27)
+TOKEN_KP3D = slice(27, 49)
+TOKEN_HAND = slice(49, 51)
+M_TOKENS = 51
+HAND_TOKENS = 4
+PROMPT_DIM = 8
+LEFT_HAND_VEC = slice(51, 54)
+RIGHT_HAND_VEC = slice(63, 66)
+
+
+@dataclass
+class DecoderConfig:
+    """(decoder.py:42-50)"""
+
+    crop_size: int = 64
+    patch: int = 8
+    dim: int = 64
+    heads: int = 4
+    enc_layers: int = 2
+    body_layers: int = 5
+    hand_layers: int = 5
+
+
+@dataclass
+class IntermediatePrediction:
+    layer: int
+    params: np.ndarray
+    camera: np.ndarray
+    kp2d: np.ndarray
+
+
+@dataclass
+class BodyDecodeOut:
+    params: np.ndarray
+    camera: np.ndarray
+    intermediates: list
+    layer_tokens: list = field(default_factory=list)
+
+
+def _bump(counters, key, n=1):
+    if counters is not None:
+        counters[key] = counters.get(key, 0) + n
+
+
+def selection_mask(selection, layers, what="selection"):
+    sel = sorted({int(v) for v in selection})
+    if any(v < 0 or v >= layers for v in sel):
+        raise UsageError("%s out of range: %r" % (what, sel))
+    m = 0
+    for v in sel:
+        m |= 1 << v
+    return m, len(sel)
+
+
+class Decoder:
+    """Frozen encoder plus body/hand decoders sharing one weight table."""
+
+    def __init__(self, template, config=None, seed=40):
+        self.template = template
+        self.config = config if config is not None else DecoderConfig()
+        self.seed = int(seed)
+        self.weights = decoder_weights(self.config, self.seed)
+        self._ctx = None
+        self._uploaded = None
+
+    # -- device context ------------------------------------------------------
+    def context(self, device=0):
+        """The fsb_ctx holding this decoder's weights (uploaded lazily; a
+        changed weight table is re-uploaded)."""
+        stamp = tuple((k, id(v)) for k, v in sorted(self.weights.items()))
+        if self._ctx is None:
+            self._ctx = runtime.Context(device)
+        if self._uploaded != stamp:
+            self._ctx.load_decoder(self.config, self.weights)
+            self._ctx.load_template(runtime.FSB_SMPL, self.template)
+            self._uploaded = stamp
+        return self._ctx
+
+    @property
+    def n_tokens(self):
+        return (self.config.crop_size // self.config.patch) ** 2
+
+    # -- encoder -------------------------------------------------------------
+    def encode(self, crops, counters=None, precision="fp32"):
+        """(B, S, S, 3) crops -> (B, S/p * S/p, D) features (decoder.py:231)."""
+        cfg = self.config
+        ctx = self.context()
+        torch = ctx.torch
+        x, was_np = runtime.to_device(crops, torch.float32, torch)
+        if x.ndim != 4 or x.shape[3] != 3 or x.shape[1] != x.shape[2]:
+            raise ShapeError("encode expects (B, S, S, 3), got %r" % (tuple(x.shape),))
+        s = x.shape[1]
+        if s % cfg.patch != 0 or s != cfg.crop_size:
+            raise ShapeError("crop size %d incompatible with patch %d / configured size %d"
+                             % (s, cfg.patch, cfg.crop_size))
+        if was_np:
+            nk.check_finite(crops, "encode")
+        b = x.shape[0]
+        out = torch.empty((b, self.n_tokens, cfg.dim), dtype=torch.float32, device=x.device)
+        ctx.check(ctx.lib.fsb_encode(ctx.h, runtime.ptr(x), b, runtime.ptr(out),
+                                     runtime.PRECISIONS[precision], ctx.stream), "encode")
+        if was_np:
+            ctx.check_finite("encode")
+        _bump(counters, "encode")
+        _bump(counters, "encoded_crops", b)
+        return runtime.out_like(out, was_np)
+
+    # -- body decoder --------------------------------------------------------
+    def decode_body(self, feat, prompt, selection=(), refine=False, counters=None,
+                    dump_tokens=False, fk_kernel=True, precision="fp32"):
+        """Decode body parameters from one crop's features (decoder.py:324)."""
+        if refine:
+            raise UsageError("refine=True is the serial baseline's second pass; the accelerated "
+                             "path runs without refinement (fast_config)")
+        if dump_tokens:
+            raise UsageError("dump_tokens is not available on the accelerated path")
+        cfg = self.config
+        ctx = self.context()
+        torch = ctx.torch
+        f, was_np = runtime.to_device(feat, torch.float32, torch)
+        if tuple(f.shape) != (self.n_tokens, cfg.dim):
+            raise ShapeError("feat must be (%d, %d), got %r" % (self.n_tokens, cfg.dim, tuple(f.shape)))
+        p, _ = runtime.to_device(np.asarray(prompt, DTYPE).reshape(PROMPT_DIM)
+                                 if not isinstance(prompt, torch.Tensor) else prompt.reshape(PROMPT_DIM),
+                                 torch.float32, torch)
+        mask, nsel = selection_mask(selection, cfg.body_layers)
+        params = torch.empty((1, PARAM_DIM), dtype=torch.float32, device=f.device)
+        cam = torch.empty((1, 3), dtype=torch.float32, device=f.device)
+        inter = torch.empty((1, cfg.body_layers, PARAM_DIM + 3 + 2 * NUM_JOINTS), dtype=torch.float32,
+                            device=f.device)
+        ctx.check(ctx.lib.fsb_decode_body(ctx.h, runtime.ptr(f), 1, 1, runtime.ptr(p), mask, runtime.ptr(params),
+                                          runtime.ptr(cam), runtime.ptr(inter), runtime.PRECISIONS[precision],
+                                          ctx.stream), "decode_body")
+        ctx.check_finite("decode_body")
+        _bump(counters, "fk", nsel)
+        _bump(counters, "project", nsel)
+        _bump(counters, "intermediate", nsel)
+        inter_h = inter.cpu().numpy()[0]
+        inters = []
+        for l in sorted({int(v) for v in selection}):
+            row = inter_h[l]
+            inters.append(IntermediatePrediction(layer=l, params=row[:PARAM_DIM].copy(),
+                                                 camera=row[PARAM_DIM:PARAM_DIM + 3].copy(),
+                                                 kp2d=row[PARAM_DIM + 3:].reshape(NUM_JOINTS, 2).copy()))
+        return BodyDecodeOut(params=runtime.out_like(params[0], True), camera=runtime.out_like(cam[0], True),
+                             intermediates=inters)
+
+    # -- hand decoder --------------------------------------------------------
+    def decode_hand(self, feats, selection=(), counters=None, precision="fp32"):
+        """(B, n, D) hand features -> (B, 3) wrist-child rotations
+        (decoder.py:360)."""
+        cfg = self.config
+        ctx = self.context()
+        torch = ctx.torch
+        f, was_np = runtime.to_device(feats, torch.float32, torch)
+        if f.ndim != 3 or tuple(f.shape[1:]) != (self.n_tokens, cfg.dim):
+            raise ShapeError("hand feats must be (B, %d, %d), got %r" % (self.n_tokens, cfg.dim, tuple(f.shape)))
+        b = f.shape[0]
+        if b == 0:
+            return np.zeros((0, 3), dtype=DTYPE) if was_np else torch.zeros((0, 3), device=f.device)
+        mask, nsel = selection_mask(selection, cfg.hand_layers, "hand selection")
+        rots = torch.empty((b, 3), dtype=torch.float32, device=f.device)
+        ctx.check(ctx.lib.fsb_decode_hands(ctx.h, runtime.ptr(f), b, mask, runtime.ptr(rots),
+                                           runtime.PRECISIONS[precision], ctx.stream), "decode_hand")
+        if was_np:
+            ctx.check_finite("decode_hand")
+        _bump(counters, "fk", b * nsel)
+        _bump(counters, "project", b * nsel)
+        return runtime.out_like(rots, was_np)
+
+    # -- merge ---------------------------------------------------------------
+    def merge(self, body_params, left=None, right=None):
+        """Overwrite the wrist-child slots with the hand outputs
+        (decoder.py:414-422).  A 76-float copy; the batched path fuses it
+        into the decoder kernel's epilogue."""
+        out = np.array(body_params, dtype=DTYPE, copy=True).reshape(PARAM_DIM)
+        if left is not None:
+            out[LEFT_HAND_VEC] = np.asarray(left, dtype=DTYPE).reshape(3)
+        if right is not None:
+            out[RIGHT_HAND_VEC] = np.asarray(right, dtype=DTYPE).reshape(3)
+        return out
+
+
+# ---------------------------------------------------------------------------
+# serialization: FSB1 arrays plus a json manifest (decoder.py:429-453)
+
+
+def save_decoder(decoder, dirpath):
+    os.makedirs(dirpath, exist_ok=True)
+    manifest = {"config": asdict(decoder.config), "seed": decoder.seed,
+                "arrays": {k: k.replace(".", "__") + ".fsb1" for k in sorted(decoder.weights)}}
+    for k, fname in manifest["arrays"].items():
+        nk.write_fsb1(os.path.join(dirpath, fname), decoder.weights[k])
+    with open(os.path.join(dirpath, "manifest.json"), "w") as fh:
+        json.dump(manifest, fh, indent=1)
+
+
+def load_decoder(dirpath, template):
+    with open(os.path.join(dirpath, "manifest.json")) as fh:
+        manifest = json.load(fh)
+    dec = Decoder(template, DecoderConfig(**manifest["config"]), seed=manifest["seed"])
+    if set(manifest["arrays"]) != set(dec.weights):
+        raise UsageError("weight manifest does not match decoder layout")
+    for k, fname in manifest["arrays"].items():
+        dec.weights[k] = nk.read_fsb1(os.path.join(dirpath, fname)).reshape(dec.weights[k].shape)
+    return dec

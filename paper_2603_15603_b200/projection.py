@@ -1,0 +1,131 @@
+"""MHR -> SMPL conversion: barycentric bridge and the feed-forward projector.
+
+Drop-in for the accelerated part of the reference ``fsb.projection``
+(pkg/src/fsb/projection.py): ``bridge`` (:187), ``make_subsample`` (:416),
+``init_projector`` (:424), ``project_batch`` (:475) and ``project_forward``
+(:486).  The projector runs on the GPU (bridge + centroid kernel, then the
+three-layer MLP); weight init is the reference's seeded RNG (synth.py).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import runtime
+from .numkit import DTYPE, ShapeError, UsageError
+from .synth import PARAM_DIM, BaryMap, projector_arrays  # noqa: F401
+
+
+@dataclass
+class ProjectorWeights:
+    """(projection.py:395-406)"""
+
+    w1: np.ndarray
+    b1: np.ndarray
+    w2: np.ndarray
+    b2: np.ndarray
+    w3: np.ndarray
+    b3: np.ndarray
+    subsample: np.ndarray
+    mask: np.ndarray
+
+
+def _output_mask():
+    m = np.ones(PARAM_DIM, dtype=DTYPE)
+    m[51:54] = 0.0
+    m[63:66] = 0.0
+    return m
+
+
+def make_subsample(n_target, v_sub):
+    """Uniform-stride target vertex picks (projection.py:416-421)."""
+    if v_sub < 1 or v_sub > n_target:
+        raise UsageError("cannot pick %d of %d vertices" % (v_sub, n_target))
+    stride = n_target // v_sub
+    return np.arange(0, stride * v_sub, stride, dtype=np.int64)
+
+
+def init_projector(subsample, hidden=(512, 256), seed=0):
+    idx = np.asarray(subsample, np.int64)
+    w1, w2, w3 = projector_arrays(3 * len(idx), hidden, seed)
+    return ProjectorWeights(w1=w1, b1=np.zeros(hidden[0], DTYPE), w2=w2, b2=np.zeros(hidden[1], DTYPE),
+                            w3=w3, b3=np.zeros(PARAM_DIM, DTYPE), subsample=idx, mask=_output_mask())
+
+
+_PROJ_CTX = {}
+
+
+def _projector_ctx(bmap, weights, nv):
+    key = (id(bmap), id(weights), nv)
+    ent = _PROJ_CTX.get(key)
+    if ent is None:
+        ctx = runtime.Context(0)
+        ctx.load_projector(weights, bmap)
+        ent = (ctx, nv)
+        _PROJ_CTX[key] = ent
+    return ent[0]
+
+
+def bridge(v_src, bmap):
+    """Resample source vertices onto the target vertex set (GPU gather)."""
+    if bmap.corners is None:
+        raise UsageError("BaryMap has no corner table; rebuild it with precompute_bary")
+    ctx = runtime.default_context()
+    torch = ctx.torch
+    v, was_np = runtime.to_device(v_src, torch.float32, torch)
+    if v.ndim < 2 or v.shape[-1] != 3:
+        raise ShapeError("bridge expects (..., Nv, 3) vertices, got %r" % (tuple(v.shape),))
+    corners = np.asarray(bmap.corners, np.int64)
+    need = int(corners.max()) + 1
+    if v.shape[-2] < need:
+        raise ShapeError("bridge needs at least %d source vertices, got %d" % (need, v.shape[-2]))
+    lead = tuple(v.shape[:-2])
+    vb = v.reshape(-1, v.shape[-2], 3)
+    c, _ = runtime.to_device(corners.astype(np.int32), torch.int32, torch)
+    w, _ = runtime.to_device(np.asarray(bmap.weights, np.float32), torch.float32, torch)
+    nt = c.shape[0]
+    out = torch.empty((vb.shape[0], nt, 3), dtype=torch.float32, device=v.device)
+    ctx.check(ctx.lib.fsb_bridge(ctx.h, runtime.ptr(vb), vb.shape[0], vb.shape[1], runtime.ptr(c), runtime.ptr(w),
+                                 nt, runtime.ptr(out), ctx.stream), "bridge")
+    return runtime.out_like(out.reshape(lead + (nt, 3)), was_np)
+
+
+def project_batch(v, bmap, weights, precision="fp32"):
+    """(B, Nv, 3) MHR meshes -> (B, 76) SMPL parameters (projection.py:475)."""
+    arr_ndim = np.ndim(v) if not hasattr(v, "ndim") else v.ndim
+    if arr_ndim == 2:
+        raise ShapeError("project_batch expects a batch; use project_forward for one mesh")
+    return _project(v, bmap, weights, precision)
+
+
+def _project(v, bmap, weights, precision):
+    idx = np.asarray(weights.subsample, np.int64)
+    if 3 * len(idx) != np.asarray(weights.w1).shape[0]:
+        raise ShapeError("input width %d does not match the first layer %d"
+                         % (3 * len(idx), np.asarray(weights.w1).shape[0]))
+    import torch as _t  # plumbing only
+
+    probe = v if isinstance(v, _t.Tensor) else np.asarray(v, DTYPE)
+    if probe.ndim != 3 or probe.shape[-1] != 3:
+        raise ShapeError("expected (B, Nv, 3) source vertices, got %r" % (tuple(probe.shape),))
+    ctx = _projector_ctx(bmap, weights, probe.shape[1])
+    torch = ctx.torch
+    vd, was_np = runtime.to_device(v, torch.float32, torch)
+    b = vd.shape[0]
+    out = torch.empty((b, PARAM_DIM), dtype=torch.float32, device=vd.device)
+    ctx.check(ctx.lib.fsb_project_vertices(ctx.h, runtime.ptr(vd), b, vd.shape[1], runtime.ptr(out),
+                                           runtime.PRECISIONS[precision], ctx.stream), "project_batch")
+    ctx.check_finite("project_batch")
+    return runtime.out_like(out, was_np)
+
+
+def project_forward(v, bmap, weights, subsample=None):
+    """One (Nv, 3) mesh -> (76,) (projection.py:486-497)."""
+    a = np.asarray(v, DTYPE)
+    if a.ndim != 2:
+        raise ShapeError("project_forward expects one (Nv, 3) mesh")
+    if subsample is not None and not np.array_equal(np.asarray(subsample), weights.subsample):
+        weights = ProjectorWeights(**{**weights.__dict__, "subsample": np.asarray(subsample, np.int64)})
+    return _project(a[None], bmap, weights, "fp32")[0]
