@@ -1,0 +1,528 @@
+#!/usr/bin/env python
+"""Benchmark of the frame -> SMPL hot path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--batch B]
+                    [--precision fp32|bf16] [--impl ours|reference]
+
+One step = one batch of B synthetic 512x512 frames per GPU through the whole
+path (K1 boxes+crops -> K2 encoder -> K3 decoders+merge -> K4 MHR LBS,
+bridge, projector, SMPL FK), replayed from a CUDA graph; with N > 1 every
+rank runs its own frames (weak scaling, one process per GPU under torchrun)
+and the per-step SMPL outputs (theta + joints) are all-gathered over NCCL,
+the path's only collective.  Rank 0 prints one JSON line.
+
+`value` is device-timed throughput with inputs resident in HBM; `e2e` is
+the same metric through Pipeline.run_batch with pinned host frames copied
+in and SMPL results copied out every step.  `--impl reference` times the
+CPU restatement of the reference (oracle/) on all host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import multiprocessing as mp
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "frames/sec at 1/2/4/8 B200 and p50 frame latency (crop→encode→SMPL)"
+UNIT = "frames/s"
+
+# algorithmic work per unit; see DESIGN.md
+FLOP_ENC_FRAME = 48_758_784
+FLOP_DEC_FRAME = 57_853_440
+BYTES_K1_FRAME = 737_280 + 304
+BYTES_LBS_MESH = 221_268 + 304 + 1_056
+FLOP_MLP_MESH = 4_909_056
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=400)
+    ap.add_argument("--warmup", type=int, default=20)
+    ap.add_argument("--batch", type=int, default=32, help="frames per GPU per step (C2: 32)")
+    ap.add_argument("--bank", type=int, default=256, help="distinct frames per GPU cycled through")
+    ap.add_argument("--precision", default="fp32", choices=("fp32", "bf16"))
+    ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------------------
+# distributed plumbing
+
+
+def dist_setup(torch, want):
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if ws > 1:
+        import torch.distributed as dist
+
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        return dist, rank, ws, local
+    return None, 0, 1, 0
+
+
+def frame_seeds(rank, bank):
+    """Rank r's frames are scenes 5000 + r * bank + i (disjoint per rank)."""
+    return [5000 + rank * bank + i for i in range(bank)]
+
+
+def shard_bounds(n_frames, rank, world):
+    """Contiguous shard of a frame stream: [r*n/G, (r+1)*n/G)."""
+    return rank * n_frames // world, (rank + 1) * n_frames // world
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region (B200_PROFILING.md)
+
+_REASONS = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+
+
+class ClockSampler:
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + q,
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                s, m = float(parts[0]), float(parts[1])
+            except ValueError:
+                continue
+            mx = m
+            if s > 0.5 * m:  # under load
+                sm.append(s)
+            for name, val in zip(_REASONS, parts[3:7]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(self.lines)}
+
+
+# ---------------------------------------------------------------------------
+# models and synthetic frames
+
+
+def build_models(precision):
+    from paper_2603_15603_b200 import decoder as dc
+    from paper_2603_15603_b200 import pipeline as pl
+    from paper_2603_15603_b200 import projection as pj
+    from paper_2603_15603_b200 import synth
+
+    mhr, smpl, gt = synth.make_toy_models(0, 18439, 6890)
+    dec = dc.Decoder(smpl, dc.DecoderConfig(), seed=40)
+    proj = pj.init_projector(pj.make_subsample(6890, 1500), (512, 256), seed=0)
+    return pl.Pipeline(dec, mhr=mhr, bmap=gt, projector=proj, precision=precision), (mhr, smpl, gt, dec, proj)
+
+
+def make_scenes(smpl, seeds):
+    from paper_2603_15603_b200 import synth
+
+    return [synth.random_scene(np.random.default_rng(s), smpl, (512, 512)) for s in seeds]
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle (baseline / reference arm)
+
+
+def _cpu_worker(args):
+    frames, kps, deadline_s, min_frames, warm = args
+    os.environ["OMP_NUM_THREADS"] = "1"
+    import oracle as orc
+    from paper_2603_15603_b200 import decoder as dc
+    from paper_2603_15603_b200 import projection as pj
+    from paper_2603_15603_b200 import synth
+
+    mhr, smpl, gt = synth.make_toy_models(0, 18439, 6890)
+    cfg = dc.DecoderConfig()
+    w = synth.decoder_weights(cfg, 40)
+    p = pj.init_projector(pj.make_subsample(6890, 1500), (512, 256), seed=0)
+    pw = dict(w1=p.w1, b1=p.b1, w2=p.w2, b2=p.b2, w3=p.w3, b3=p.b3, subsample=p.subsample, mask=p.mask)
+    for i in range(max(1, warm)):  # untimed warm-up frames
+        orc.frame_to_smpl(frames[i % len(frames)], kps[i % len(frames)], w, cfg, mhr, smpl, gt, pw)
+    done, lat = 0, []
+    t0 = time.perf_counter()
+    while done < min_frames or (time.perf_counter() - t0) < deadline_s:
+        i = done % len(frames)
+        a = time.perf_counter()
+        orc.frame_to_smpl(frames[i], kps[i], w, cfg, mhr, smpl, gt, pw)
+        lat.append(time.perf_counter() - a)
+        done += 1
+    return done, time.perf_counter() - t0, lat
+
+
+def cpu_oracle_run(frames, kps, seconds, min_frames=1, workers=None, warm=1):
+    """Oracle frames/s on `workers` host processes (spawn), disjoint frames."""
+    n = workers or len(os.sched_getaffinity(0))
+    n = max(1, min(n, 64))
+    chunks = [(frames[i::n] if len(frames[i::n]) else frames[:1], kps[i::n] if len(kps[i::n]) else kps[:1],
+               seconds, min_frames, warm) for i in range(n)]
+    ctx = mp.get_context("spawn")
+    with ctx.Pool(n) as pool:
+        res = pool.map(_cpu_worker, chunks)
+    frames_done = sum(r[0] for r in res)
+    wall = max(r[1] for r in res)
+    lat = [x for r in res for x in r[2]]
+    return frames_done / wall, n, frames_done, statistics.median(lat) * 1e3
+
+
+def reference_arm(args):
+    """--impl reference: the oracle port on all host cores, rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    if rank != 0:
+        return
+    from paper_2603_15603_b200 import synth
+
+    _, smpl, _ = synth.make_toy_models(0, 18439, 6890)
+    n = len(os.sched_getaffinity(0))
+    scenes = make_scenes(smpl, frame_seeds(0, max(8, min(n, 32))))
+    frames = np.stack([synth.render_scene(s, smpl) for s in scenes])
+    kps = np.stack([s.keypoints2d for s in scenes])
+    # one step = one frame on every host worker; W untimed warm-up frames per
+    # worker, then K timed frames per worker (capped so the run stays short)
+    warm = max(0, args.warmup)
+    steps = max(1, min(args.steps, 600))
+    fps, cores, done, p50 = cpu_oracle_run(frames, kps, 0.0, min_frames=steps, workers=n, warm=warm)
+    per_step_s = n / fps
+    line = {"impl": "reference", "metric": METRIC, "value": fps, "unit": UNIT, "n_gpus": ws, "steps": steps,
+            "warmup": warm, "ms_per_step": per_step_s * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "C2 frame->SMPL, 512x512 frames, default encoder/decoders, full-size "
+                                   "MHR 18439 / SMPL 6890 tail (CPU oracle restatement of the reference)",
+                       "frames_per_step": n},
+            "cpu_baseline": {"value": fps, "unit": UNIT, "cores": cores, "kind": "port",
+                             "sample": "%d timed frames on %d host processes (one frame per process per step, %d "
+                                       "steps), p50 %.1f ms/frame" % (done, cores, steps, p50)},
+            "e2e": {"value": fps, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "p50_frame_latency_ms": p50}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# the GPU arm
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        reference_arm(args)
+        return
+    import torch
+
+    dist, rank, world, local = dist_setup(torch, args.gpus)
+    dev = torch.device("cuda", local)
+    torch.cuda.set_device(dev)
+    from paper_2603_15603_b200 import priors as pr
+
+    pipe, (mhr, smpl, gt, dec, proj) = build_models(args.precision)
+    ctx = pipe.context()
+    B, bank = args.batch, max(args.bank, args.batch)
+    bank -= bank % B
+    ctx.reserve(max(B, 1))
+
+    scenes = make_scenes(smpl, frame_seeds(rank, bank))
+    images = pr.render_scenes(scenes)                      # (bank, 512, 512, 3) resident in HBM
+    kps = torch.from_numpy(np.stack([s.keypoints2d for s in scenes])).to(dev)
+    nslot = bank // B
+    outs = pipe.allocate_outputs(B, tail=True)
+    cfg = None
+    from paper_2603_15603_b200 import pipeline as pl
+
+    cfg = pl.fast_config()
+    gathered = None
+    if dist is not None:
+        gathered = torch.empty((world * B, 76 + 66), dtype=torch.float32, device=dev)
+        packed = torch.empty((B, 76 + 66), dtype=torch.float32, device=dev)
+
+    def step(i):
+        s = i % nslot
+        pipe.launch(images[s * B:(s + 1) * B], kps[s * B:(s + 1) * B], outs, cfg)
+        if dist is not None:
+            packed[:, :76].copy_(outs["theta"])
+            packed[:, 76:].copy_(outs["j_smpl"].reshape(B, 66))
+            dist.all_gather_into_tensor(gathered, packed)
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    # warm-up (captures one graph per input slot)
+    for i in range(max(args.warmup, 3, nslot)):
+        step(i)
+    ctx.check_finite("bench warm-up")
+    barrier()
+    launches0 = ctx.launches()
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        e0.record(st)
+        for i in range(args.steps):
+            step(i)
+        e1.record(st)
+        barrier()
+    launches = ctx.launches() - launches0
+    ms = e0.elapsed_time(e1)
+    t_max = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if dist is not None:
+        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
+    ms = float(t_max.item())
+    frames_total = world * B * args.steps
+    value = frames_total / (ms / 1e3)
+    ctx.check_finite("bench")
+
+    # -- per-stage attribution (graphs off, CUDA events between stages) -------
+    stage_ms = attribute_stages(torch, pipe, ctx, images[:B], kps[:B], outs, cfg, reps=min(50, max(5, args.steps)))
+
+    # -- p50 single-frame latency (B = 1 graph replay) -------------------------
+    lat = frame_latency(torch, pipe, images, kps, cfg, reps=200)
+
+    # -- end-to-end through the public API with host buffers -------------------
+    e2e = None if args.no_e2e else end_to_end(torch, pipe, images, kps, cfg, B, args.steps, args.warmup, dist,
+                                              world)
+
+    if rank != 0:
+        if dist is not None:
+            dist.destroy_process_group()
+        return
+    roof = roofline(stage_ms, B)
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        n_host = min(len(scenes), 64)
+        fr = images[:n_host].cpu().numpy()
+        kk = kps[:n_host].cpu().numpy()
+        fps, cores, done, p50c = cpu_oracle_run(fr, kk, args.cpu_seconds)
+        cpu = {"value": fps, "unit": UNIT, "cores": cores, "kind": "port",
+               "sample": "%d frames (C2 frame->SMPL, full-size tail) on %d host processes over ~%.0f s; "
+                         "p50 %.1f ms/frame single process" % (done, cores, args.cpu_seconds, p50c)}
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32" if args.precision == "fp32" else "bf16", "data": "synthetic",
+        "config": {"workload": "C2: %d synthetic 512x512 frames per GPU per step, body + 2 hand crops -> "
+                               "encoder -> pruned decoders -> MHR LBS (18439 v) -> projector -> SMPL FK" % B,
+                   "frames_per_gpu_per_step": B, "global_batch": B * world,
+                   "parallelism": "dp%d (frame sharding, NCCL all-gather of SMPL outputs)" % world
+                   if world > 1 else "single GPU",
+                   "l2": "inputs cycle through a %d-frame bank (%.0f MB in HBM) > 126 MB L2" %
+                         (bank, bank * 512 * 512 * 12 / 1e6),
+                   "precision": args.precision, "graphs": True},
+        "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+        "clocks": clk.summary(), "p50_frame_latency_ms": lat["p50_ms"], "frame_latency": lat,
+        "stage_ms": stage_ms,
+    }
+    print(json.dumps(line), flush=True)
+    if dist is not None:
+        dist.destroy_process_group()
+
+
+def attribute_stages(torch, pipe, ctx, img, kp, outs, cfg, reps):
+    """Average device time of each stage kernel on one batch (graphs off)."""
+    from paper_2603_15603_b200 import decoder as dc
+    from paper_2603_15603_b200 import runtime as rt
+
+    B = img.shape[0]
+    lib, h = ctx.lib, ctx.h
+    prec = rt.PRECISIONS[pipe.precision]
+    dev = img.device
+    crops = torch.empty((B, 3, 64, 64, 3), dtype=torch.float32, device=dev)
+    feats = torch.empty((B, 3, 64, 64), dtype=torch.float32, device=dev)
+    bsel, _ = dc.selection_mask(cfg.selection, 5)
+    names = ["k1_boxes_crops", "k2_encoder", "k3_decoders", "k4_fk_lbs", "k4_proj_mlp_smplfk"]
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(len(names) + 1)]
+    acc = np.zeros(len(names))
+    st = torch.cuda.current_stream()
+    for r in range(reps + 3):
+        s = ctx.stream
+        ev[0].record(st)
+        ctx.check(lib.fsb_boxes_crops(h, rt.ptr(img), B, 512, 512, rt.ptr(kp), 3.0, 64, rt.ptr(outs["boxes"]),
+                                      rt.ptr(outs["prompt"]), rt.ptr(crops), None, s))
+        ev[1].record(st)
+        ctx.check(lib.fsb_encode(h, rt.ptr(crops), 3 * B, rt.ptr(feats), prec, s))
+        ev[2].record(st)
+        ctx.check(lib.fsb_decode_frames(h, rt.ptr(feats), B, rt.ptr(outs["prompt"]), bsel, 0,
+                                        rt.ptr(outs["body_params"]), rt.ptr(outs["body_cam"]),
+                                        rt.ptr(outs["hand_rots"]), rt.ptr(outs["merged"]), prec, s))
+        ev[3].record(st)
+        ctx.check(lib.fsb_skin(h, 0, rt.ptr(outs["merged"]), B, rt.ptr(outs["v_mhr"]), s))
+        ev[4].record(st)
+        ctx.check(lib.fsb_skin_project(h, rt.ptr(outs["merged"]), B, None, rt.ptr(outs["theta"]),
+                                       rt.ptr(outs["j_smpl"]), None, prec, s))
+        ev[5].record(st)
+        torch.cuda.synchronize()
+        if r >= 3:
+            acc += [ev[i].elapsed_time(ev[i + 1]) for i in range(len(names))]
+    return {n: float(v / reps) for n, v in zip(names, acc)}
+
+
+def roofline(stage_ms, B):
+    """Roofline of the dominant stage kernel against MEASURED_PEAKS.json."""
+    peaks = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "src": "fallback (B200_PROFILING.md)"}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            m = json.load(fh)
+        peaks = {"hbm_gbs": float(m["hbm_gbs"]), "bf16_tflops": float(m["bf16_tflops"]), "src": "measured"}
+    except (OSError, KeyError, ValueError):
+        pass
+    work = {  # name -> (bound, algorithmic units per launch, unit)
+        "k1_boxes_crops": ("hbm", BYTES_K1_FRAME * B),
+        "k2_encoder": ("tensor", FLOP_ENC_FRAME * B),
+        "k3_decoders": ("tensor", FLOP_DEC_FRAME * B),
+        "k4_fk_lbs": ("hbm", BYTES_LBS_MESH * B),
+        "k4_proj_mlp_smplfk": ("tensor", FLOP_MLP_MESH * B),
+    }
+    dom = max(stage_ms, key=stage_ms.get)
+    bound, amount = work[dom]
+    sec = stage_ms[dom] / 1e3
+    if bound == "hbm":
+        achieved, peak, unit = amount / sec / 1e9, peaks["hbm_gbs"], "GB/s"
+    else:
+        achieved, peak, unit = amount / sec / 1e12, peaks["bf16_tflops"], "TFLOP/s"
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
+            tr = json.load(fh)
+        if dom in tr:
+            traffic = tr[dom].get("dram_bytes_per_launch")
+    except (OSError, ValueError):
+        pass
+    return {"kernel": dom, "bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
+            "frac": achieved / peak, "traffic": traffic, "peak_source": peaks["src"],
+            "share_of_step": stage_ms[dom] / sum(stage_ms.values()),
+            "algorithmic_per_launch": amount, "launch_ms": stage_ms[dom]}
+
+
+def frame_latency(torch, pipe, images, kps, cfg, reps):
+    """p50 latency of one frame through the whole path (graph replay)."""
+    outs = pipe.allocate_outputs(1, tail=True)
+    st = torch.cuda.current_stream()
+    for i in range(5):
+        pipe.launch(images[i:i + 1], kps[i:i + 1], outs, cfg)
+    torch.cuda.synchronize()
+    ts = []
+    for r in range(reps):
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(st)
+        pipe.launch(images[0:1], kps[0:1], outs, cfg)
+        b.record(st)
+        b.synchronize()
+        ts.append(a.elapsed_time(b))
+    ts.sort()
+    return {"p50_ms": ts[len(ts) // 2], "p95_ms": ts[int(len(ts) * 0.95)], "reps": reps, "batch": 1}
+
+
+def end_to_end(torch, pipe, images, kps, cfg, B, steps, warmup, dist, world):
+    """Pipeline.run_batch on pinned host frames: per step H2D of the frames
+    and keypoints, the whole path, D2H of merged/theta/j_smpl.  Copies run
+    on a side stream double-buffered against compute."""
+    dev = images.device
+    nhost = min(images.shape[0], 4 * B)
+    h_img = images[:nhost].cpu().pin_memory()
+    h_kp = kps[:nhost].cpu().pin_memory()
+    nslot = nhost // B
+    d_img = [torch.empty((B,) + tuple(images.shape[1:]), dtype=torch.float32, device=dev) for _ in range(2)]
+    d_kp = [torch.empty((B, 22, 2), dtype=torch.float32, device=dev) for _ in range(2)]
+    outs = [pipe.allocate_outputs(B, tail=True) for _ in range(2)]
+    h_out = [{k: torch.empty(outs[0][k].shape, dtype=torch.float32).pin_memory()
+              for k in ("merged", "theta", "j_smpl")} for _ in range(2)]
+    comp = torch.cuda.current_stream()
+    copy = torch.cuda.Stream(device=dev)
+    ready = [torch.cuda.Event() for _ in range(2)]
+    done = [torch.cuda.Event() for _ in range(2)]
+    for d in done:
+        d.record(comp)
+
+    def h2d(i):
+        j = i % 2
+        s = i % nslot
+        with torch.cuda.stream(copy):
+            copy.wait_event(done[j])
+            d_img[j].copy_(h_img[s * B:(s + 1) * B], non_blocking=True)
+            d_kp[j].copy_(h_kp[s * B:(s + 1) * B], non_blocking=True)
+            ready[j].record(copy)
+
+    def run(i):
+        j = i % 2
+        comp.wait_event(ready[j])
+        pipe.run_batch(d_img[j], d_kp[j], cfg, outputs=outs[j], sync=False)
+        for k in ("merged", "theta", "j_smpl"):
+            h_out[j][k].copy_(outs[j][k], non_blocking=True)
+        done[j].record(comp)
+
+    total = warmup + steps
+    h2d(0)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    for i in range(total):
+        if i == warmup:
+            torch.cuda.synchronize()
+            if dist is not None:
+                dist.barrier()
+            e0.record(comp)
+        if i + 1 < total:
+            h2d(i + 1)
+        run(i)
+    e1.record(comp)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    h2d_b = B * (images[0].numel() + 44) * 4
+    d2h_b = B * (76 + 76 + 66) * 4
+    return {"value": world * B * steps / (ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d_b,
+            "d2h_bytes_per_step": d2h_b, "ms_per_step": ms / steps,
+            "api": "Pipeline.run_batch (pinned host frames, copy stream double-buffered)"}
+
+
+if __name__ == "__main__":
+    main()

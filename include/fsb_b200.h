@@ -152,6 +152,11 @@ int fsb_frame_batch(fsb_ctx* ctx, const float* images, int B, int H, int W, cons
                     uint32_t body_sel, uint32_t hand_sel, int precision, const fsb_frame_outputs* out,
                     void* stream);
 
+/* priors.render_scene (priors.py:237-252) for B scenes: `scenes` is a
+ * device array of 464-byte records {float kp[44]; float half_color[66];
+ * float inv_two_sigma2; float pad; double gdir[2]} -> (B, H, W, 3) f32 */
+int fsb_render(fsb_ctx* ctx, const void* scenes, int B, int H, int W, float* out, void* stream);
+
 /* ---- diagnostics -------------------------------------------------------- */
 /* reads (and optionally clears) the device non-finite flag; synchronises */
 int fsb_nonfinite(fsb_ctx* ctx, int* flag, int reset);

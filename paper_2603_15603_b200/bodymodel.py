@@ -85,7 +85,7 @@ def _template_ctx(template):
     key = (id(template), template.vertices_rest.ctypes.data, template.num_vertices)
     ctx = _TEMPLATE_CTX.get(key)
     if ctx is None:
-        ctx = runtime.Context(0)
+        ctx = runtime.Context()
         ctx.load_template(runtime.FSB_MHR, template)
         _TEMPLATE_CTX[key] = ctx
     return ctx

@@ -39,6 +39,7 @@ cudaError_t launch_hand_boxes(const double* wrists, const double* body, int n, d
 cudaError_t launch_crop_grid(const double* boxes, int n, int S, float* out, cudaStream_t st);
 cudaError_t launch_bridge(const float* V, int B, int nv, const int32_t* corners, const float* w, int nt, float* out,
                           cudaStream_t st);
+cudaError_t launch_render(const void* scenes, int B, int H, int W, float* out, cudaStream_t st);
 cudaError_t init_attrs_transformer();
 cudaError_t init_attrs_body();
 
@@ -112,10 +113,18 @@ struct fsb_ctx {
   __nv_bfloat16* w_xb = nullptr;
   // graphs
   bool graphs = true;
-  bool have_graph = false;
-  GraphKey gkey{};
-  cudaGraphExec_t gexec = nullptr;
-  int graph_nodes = 0;
+  struct GraphEntry {
+    GraphKey key;
+    cudaGraphExec_t exec;
+    int nodes;
+    uint64_t used;
+  };
+  std::vector<GraphEntry> gcache;  // LRU of captured frame-batch graphs
+  uint64_t gclock = 0;
+  void drop_graphs() {
+    for (auto& e : gcache) cudaGraphExecDestroy(e.exec);
+    gcache.clear();
+  }
 };
 
 namespace {
@@ -184,7 +193,7 @@ int fsb_ctx_create(int device, fsb_ctx** out) {
 
 void fsb_ctx_destroy(fsb_ctx* c) {
   if (!c) return;
-  if (c->gexec) cudaGraphExecDestroy(c->gexec);
+  c->drop_graphs();
   if (c->d_flag) cudaFree(c->d_flag);
   delete c;
 }
@@ -224,11 +233,7 @@ int fsb_reserve(fsb_ctx* c, int max_frames) {
   const size_t o_h1 = take(F * h1 * 4);
   const size_t o_h2 = take(F * h2 * 4);
   const size_t o_theta = take(F * 76 * 4);
-  if (c->have_graph) {
-    cudaGraphExecDestroy(c->gexec);
-    c->gexec = nullptr;
-    c->have_graph = false;
-  }
+  c->drop_graphs();
   FSB_CUDA(c, c->ws.alloc(off));
   unsigned char* b = static_cast<unsigned char*>(c->ws.p);
   c->w_boxes = reinterpret_cast<double*>(b + o_boxes);
@@ -465,11 +470,7 @@ int fsb_load_template(fsb_ctx* c, int which, int nv, const float* v_rest, const 
   t.joints_rest = reinterpret_cast<const float*>(base + o_g);
   c->has_tmpl[which] = true;
   if (which == FSB_SMPL) c->body.joints_rest = t.joints_rest;
-  if (c->have_graph) {
-    cudaGraphExecDestroy(c->gexec);
-    c->gexec = nullptr;
-    c->have_graph = false;
-  }
+  c->drop_graphs();
   return FSB_OK;
 }
 
@@ -771,11 +772,17 @@ int fsb_frame_batch(fsb_ctx* c, const float* images, int B, int H, int W, const 
                           out->v_smpl, nullptr, nullptr};
   memcpy(k.ptrs, ptrs, sizeof ptrs);
   k.stream = st;
-  if (!(c->have_graph && c->gkey == k)) {
-    if (c->have_graph) {
-      cudaGraphExecDestroy(c->gexec);
-      c->gexec = nullptr;
-      c->have_graph = false;
+  fsb_ctx::GraphEntry* hit = nullptr;
+  for (auto& e : c->gcache)
+    if (e.key == k) hit = &e;
+  if (!hit) {
+    constexpr size_t kMaxGraphs = 32;
+    if (c->gcache.size() >= kMaxGraphs) {
+      size_t lru = 0;
+      for (size_t i = 1; i < c->gcache.size(); ++i)
+        if (c->gcache[i].used < c->gcache[lru].used) lru = i;
+      cudaGraphExecDestroy(c->gcache[lru].exec);
+      c->gcache.erase(c->gcache.begin() + lru);
     }
     const fsb_counters_t saved = c->counters;
     const int64_t saved_l = c->launches;
@@ -783,6 +790,8 @@ int fsb_frame_batch(fsb_ctx* c, const float* images, int B, int H, int W, const 
     rc = frame_batch_launches(c, images, B, H, W, kp, alpha, body_sel, hand_sel, precision, *out, st);
     cudaGraph_t g = nullptr;
     cudaError_t ce = cudaStreamEndCapture(st, &g);
+    c->counters = saved;
+    c->launches = saved_l;
     if (rc) {
       if (g) cudaGraphDestroy(g);
       return rc;
@@ -790,23 +799,29 @@ int fsb_frame_batch(fsb_ctx* c, const float* images, int B, int H, int W, const 
     if (ce != cudaSuccess) return fail(c, FSB_ERR_CUDA, "graph capture: %s", cudaGetErrorString(ce));
     size_t nn = 0;
     cudaGraphGetNodes(g, nullptr, &nn);
-    ce = cudaGraphInstantiate(&c->gexec, g, 0);
+    cudaGraphExec_t ex = nullptr;
+    ce = cudaGraphInstantiate(&ex, g, 0);
     cudaGraphDestroy(g);
     if (ce != cudaSuccess) return fail(c, FSB_ERR_CUDA, "graph instantiate: %s", cudaGetErrorString(ce));
-    c->graph_nodes = (int)nn;
-    c->gkey = k;
-    c->have_graph = true;
-    c->counters = saved;
-    c->launches = saved_l;
+    c->gcache.push_back({k, ex, (int)nn, 0});
+    hit = &c->gcache.back();
   }
-  FSB_CUDA(c, cudaGraphLaunch(c->gexec, st));
-  c->launches += c->graph_nodes;
+  hit->used = ++c->gclock;
+  FSB_CUDA(c, cudaGraphLaunch(hit->exec, st));
+  c->launches += hit->nodes;
   c->counters.encode += 1;
   c->counters.encoded_crops += 3 * B;
   const int nb = layer_count(body_sel), nh = layer_count(hand_sel);
   c->counters.fk += (int64_t)B * (nb + 2 * nh);
   c->counters.project += (int64_t)B * (nb + 2 * nh);
   c->counters.intermediate += (int64_t)B * nb;
+  return FSB_OK;
+}
+
+int fsb_render(fsb_ctx* c, const void* scenes, int B, int H, int W, float* out, void* stream) {
+  if (B < 0 || H < 1 || W < 1) return fail(c, FSB_ERR_SHAPE, "render: bad shapes");
+  FSB_CUDA(c, launch_render(scenes, B, H, W, out, (cudaStream_t)stream));
+  c->launches += B > 0;
   return FSB_OK;
 }
 

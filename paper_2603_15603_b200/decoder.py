@@ -88,7 +88,7 @@ class Decoder:
         self._uploaded = None
 
     # -- device context ------------------------------------------------------
-    def context(self, device=0):
+    def context(self, device=None):
         """The fsb_ctx holding this decoder's weights (uploaded lazily; a
         changed weight table is re-uploaded)."""
         stamp = tuple((k, id(v)) for k, v in sorted(self.weights.items()))

@@ -265,12 +265,16 @@ _STAGE_GROUPS = (("crop", ("detect", "hand_boxes", "crop_body", "crop_hands")),
 class Pipeline:
     """Runs one Decoder (and, when given, the MHR -> SMPL tail) on the GPU."""
 
-    def __init__(self, decoder, mhr=None, bmap=None, projector=None, precision="fp32", device=0):
+    def __init__(self, decoder, mhr=None, bmap=None, projector=None, precision="fp32", device=None):
         self.decoder = decoder
         self.template = decoder.template
         self.crop_size = decoder.config.crop_size
         self.mhr, self.bmap, self.projector = mhr, bmap, projector
         self.precision = precision
+        if device is None:
+            import torch
+
+            device = torch.cuda.current_device()
         self.device = device
         self.last_counters = {}
         self._tail_loaded = None

@@ -111,6 +111,41 @@ def hand_box(wrist, body_box, alpha=3.0, image_size=None):
     return BBox(*map(float, out.cpu().numpy()[0]))
 
 
+def render_records(scenes):
+    """Per-scene parameters of render_scene (priors.py:237-252) packed in the
+    464-byte layout of fsb_render: keypoints, 0.5 * colours (the seeded RNG
+    draws of the reference), float32(-0.5 / sigma^2) and the ramp slope."""
+    rec = np.zeros((len(scenes), 116), dtype=np.float32)
+    for i, sc in enumerate(scenes):
+        kp = np.asarray(sc.keypoints2d, DTYPE)
+        rng = np.random.default_rng(sc.seed)
+        colors = rng.uniform(0.4, 1.0, size=(kp.shape[0], 3)).astype(DTYPE)
+        gdir = rng.uniform(-1.0, 1.0, size=2)
+        span = max(float(np.ptp(kp[:, 0])), float(np.ptp(kp[:, 1])))
+        sigma = max(6.0, 0.085 * span)
+        rec[i, :44] = kp.reshape(-1)
+        rec[i, 44:110] = (0.5 * colors).reshape(-1)
+        rec[i, 110] = np.float32(-0.5 / (sigma * sigma))
+        rec[i, 112:116] = np.asarray(gdir, np.float64).view(np.float32)
+    return rec
+
+
+def render_scenes(scenes, out=None):
+    """Render a batch of same-size scenes on the GPU -> CUDA tensor
+    (B, H, W, 3) float32 (the benchmark's frame generator)."""
+    ctx = runtime.default_context()
+    torch = ctx.torch
+    w, h = scenes[0].image_size
+    if any(tuple(s.image_size) != (w, h) for s in scenes):
+        raise UsageError("render_scenes needs scenes of one image size")
+    rec = _dev(render_records(scenes), torch, torch.float32)
+    if out is None:
+        out = torch.empty((len(scenes), h, w, 3), dtype=torch.float32, device=rec.device)
+    ctx.check(ctx.lib.fsb_render(ctx.h, runtime.ptr(rec), len(scenes), int(h), int(w), runtime.ptr(out),
+                                 ctx.stream), "render_scenes")
+    return out
+
+
 def crop_grid(box, out_size):
     """(S, S, 2) float32 sampling grid spanning the box inclusively
     (priors.py:220-230)."""

@@ -61,7 +61,7 @@ def _projector_ctx(bmap, weights, nv):
     key = (id(bmap), id(weights), nv)
     ent = _PROJ_CTX.get(key)
     if ent is None:
-        ctx = runtime.Context(0)
+        ctx = runtime.Context()
         ctx.load_projector(weights, bmap)
         ent = (ctx, nv)
         _PROJ_CTX[key] = ent

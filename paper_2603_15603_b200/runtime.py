@@ -73,6 +73,7 @@ _SIGS = {
     "fsb_project_vertices": (_i, [_p, _p, _i, _i, _p, _i, _p]),
     "fsb_skin_project": (_i, [_p, _p, _i, _p, _p, _p, _p, _i, _p]),
     "fsb_frame_batch": (_i, [_p, _p, _i, _i, _i, _p, _d, _u32, _u32, _i, ctypes.POINTER(FrameOutputsC), _p]),
+    "fsb_render": (_i, [_p, _p, _i, _i, _i, _p, _p]),
     "fsb_nonfinite": (_i, [_p, ctypes.POINTER(_i), _i]),
     "fsb_counters": (_i, [_p, ctypes.POINTER(CountersC)]),
     "fsb_kernel_launches": (_i64, [_p]),
@@ -125,9 +126,9 @@ _ERRORS = {1: ShapeError, 2: NumericError, 3: UsageError}
 class Context:
     """One fsb_ctx on one GPU: uploaded models, workspace, graph cache."""
 
-    def __init__(self, device=0):
+    def __init__(self, device=None):
         self.torch = _torch()
-        self.device = int(device)
+        self.device = int(self.torch.cuda.current_device() if device is None else device)
         self.lib = lib()
         h = ctypes.c_void_p()
         with self.torch.cuda.device(self.device):
@@ -223,9 +224,11 @@ class Context:
 # array plumbing
 
 
-def to_device(x, dtype, torch, device=0):
+def to_device(x, dtype, torch, device=None):
     """numpy / torch -> contiguous CUDA tensor of `dtype` (copies only when
     needed); returns (tensor, was_numpy)."""
+    if device is None:
+        device = torch.cuda.current_device()
     if isinstance(x, torch.Tensor):
         t = x.to(device=torch.device("cuda", device), dtype=dtype)
         return t.contiguous(), False
@@ -241,8 +244,10 @@ def out_like(t, was_numpy):
 _DEFAULT = {}
 
 
-def default_context(device=0):
-    """Process-wide context for the stand-alone functional API."""
+def default_context(device=None):
+    """Process-wide context (per device) for the stand-alone functional API."""
+    if device is None:
+        device = _torch().cuda.current_device()
     ctx = _DEFAULT.get(device)
     if ctx is None:
         ctx = Context(device)
