@@ -163,6 +163,9 @@ int fsb_nonfinite(fsb_ctx* ctx, int* flag, int reset);
 int fsb_counters(const fsb_ctx* ctx, fsb_counters_t* out);
 /* number of kernels this context launched (graph replays count their nodes) */
 int64_t fsb_kernel_launches(const fsb_ctx* ctx);
+/* tcgen05 self-test: C (128 x N) f32 = A (128 x K, bf16 row-major) * B^T,
+ * B (N x K) given pre-packed in the K-major canonical UMMA layout */
+int fsb_selftest_umma(fsb_ctx* ctx, const void* A, const void* Bpacked, int N, int K, float* C, void* stream);
 
 #ifdef __cplusplus
 }

@@ -31,7 +31,9 @@ cudaError_t launch_proj_inputs(const TemplateDev& t, const ProjectorDev& p, cons
 cudaError_t launch_proj_inputs_v(const float* V, int nv, const ProjectorDev& p, int B, float* x, __nv_bfloat16* xb,
                                  int ldx, cudaStream_t st);
 cudaError_t launch_gemm_f32(const float* A, int lda, const float* W, const float* bias, const float* mask, float* C,
-                            int ldc, int M, int N, int K, int relu, int* nonfinite, cudaStream_t st);
+                            int ldc, int M, int N, int K, int relu, int* nonfinite, float* partial,
+                            cudaStream_t st);
+int gemm_f32_splits(int K);
 
 cudaError_t launch_body_boxes(const float* kps, int n, int W, int H, double* out, cudaStream_t st);
 cudaError_t launch_hand_boxes(const double* wrists, const double* body, int n, double alpha, int W, int H, double* out,
@@ -109,7 +111,7 @@ struct fsb_ctx {
   double* w_boxes = nullptr;
   float *w_prompt = nullptr, *w_crops = nullptr, *w_feats = nullptr, *w_params = nullptr, *w_cam = nullptr,
         *w_rots = nullptr, *w_rel = nullptr, *w_rel2 = nullptr, *w_x = nullptr, *w_h1 = nullptr, *w_h2 = nullptr,
-        *w_theta = nullptr;
+        *w_theta = nullptr, *w_part = nullptr;
   __nv_bfloat16* w_xb = nullptr;
   // graphs
   bool graphs = true;
@@ -233,6 +235,8 @@ int fsb_reserve(fsb_ctx* c, int max_frames) {
   const size_t o_h1 = take(F * h1 * 4);
   const size_t o_h2 = take(F * h2 * 4);
   const size_t o_theta = take(F * 76 * 4);
+  const int hmax = h1 > h2 ? (h1 > 76 ? h1 : 76) : (h2 > 76 ? h2 : 76);
+  const size_t o_part = take(F * 16 * (size_t)hmax * 4);  // split-K partials (<= 16 chunks)
   c->drop_graphs();
   FSB_CUDA(c, c->ws.alloc(off));
   unsigned char* b = static_cast<unsigned char*>(c->ws.p);
@@ -250,6 +254,7 @@ int fsb_reserve(fsb_ctx* c, int max_frames) {
   c->w_h1 = reinterpret_cast<float*>(b + o_h1);
   c->w_h2 = reinterpret_cast<float*>(b + o_h2);
   c->w_theta = reinterpret_cast<float*>(b + o_theta);
+  c->w_part = reinterpret_cast<float*>(b + o_part);
   c->ws_frames = max_frames;
   return FSB_OK;
 }
@@ -676,11 +681,12 @@ static int run_mlp(fsb_ctx* c, int B, float* theta, int precision, cudaStream_t 
   const ProjectorDev& p = c->proj;
   if (precision != FSB_FP32) return fail(c, FSB_ERR_USAGE, "projector: precision %d not available yet", precision);
   FSB_CUDA(c, launch_gemm_f32(c->w_x, 3 * p.n_sub, p.w1, p.b1, nullptr, c->w_h1, p.h1, B, p.h1, 3 * p.n_sub, 1,
-                              nullptr, st));
-  FSB_CUDA(c, launch_gemm_f32(c->w_h1, p.h1, p.w2, p.b2, nullptr, c->w_h2, p.h2, B, p.h2, p.h1, 1, nullptr, st));
+                              nullptr, c->w_part, st));
+  FSB_CUDA(c, launch_gemm_f32(c->w_h1, p.h1, p.w2, p.b2, nullptr, c->w_h2, p.h2, B, p.h2, p.h1, 1, nullptr,
+                              c->w_part, st));
   FSB_CUDA(c, launch_gemm_f32(c->w_h2, p.h2, p.w3, p.b3, p.mask, theta, FSB_PARAM_DIM, B, FSB_PARAM_DIM, p.h2, 0,
-                              c->d_flag, st));
-  c->launches += 3;
+                              c->d_flag, c->w_part, st));
+  c->launches += 3 + (gemm_f32_splits(3 * p.n_sub) > 1) + (gemm_f32_splits(p.h1) > 1) + (gemm_f32_splits(p.h2) > 1);
   return FSB_OK;
 }
 
@@ -843,3 +849,12 @@ int fsb_counters(const fsb_ctx* c, fsb_counters_t* out) {
 int64_t fsb_kernel_launches(const fsb_ctx* c) { return c ? c->launches : 0; }
 
 }  // extern "C"
+
+cudaError_t launch_tc_selftest(const void* A, const void* Bpacked, int N, int K, float* C, cudaStream_t st);
+
+extern "C" int fsb_selftest_umma(fsb_ctx* c, const void* A, const void* Bpacked, int N, int K, float* C,
+                                 void* stream) {
+  FSB_CUDA(c, launch_tc_selftest(A, Bpacked, N, K, C, (cudaStream_t)stream));
+  c->launches += 1;
+  return FSB_OK;
+}

@@ -243,28 +243,35 @@ __global__ void __launch_bounds__(kProjThreads) k_proj_inputs_v(const float* __r
 
 // ---------------------------------------------------------------------------
 // fp32 GEMM for the projector MLP: C = act(A @ W + b) * mask, A (M, K) with
-// leading dim lda, W (K, N) row-major.  64x64 tiles, 4x4 per thread, every
-// output a sequential fused sum over k (batch-size independent).
+// leading dim lda, W (K, N) row-major.  64x64 tiles, 4x4 per thread.  The
+// K axis is cut into a fixed number of chunks per layer (blockIdx.z), chosen
+// from K alone: each chunk's partial sum lands in P[split][M][N] and a
+// second kernel adds the partials in split order.  The partition never
+// depends on M, so a mesh projected in a batch of 4096 is bit-identical to
+// the same mesh projected alone, while a batch of 32 still fills the GPU
+// (W1 is 4500 x 512: 8 column tiles alone would occupy 8 SMs).
 // ---------------------------------------------------------------------------
 constexpr int kGT = 64, kGK = 16;
 
 __global__ void __launch_bounds__(256) k_gemm_f32(const float* __restrict__ A, int lda,
                                                    const float* __restrict__ W, const float* __restrict__ bias,
                                                    const float* __restrict__ mask, float* __restrict__ C, int ldc,
-                                                   int M, int N, int K, int relu, int* nonfinite) {
+                                                   int M, int N, int K, int relu, int* nonfinite, int kchunk,
+                                                   float* __restrict__ P) {
   __shared__ __align__(16) float As[kGK][kGT + 4];
   __shared__ __align__(16) float Bs[kGK][kGT + 4];
   const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
   const int m0 = blockIdx.y * kGT, n0 = blockIdx.x * kGT;
+  const int kb0 = blockIdx.z * kchunk, kb1 = min(K, kb0 + kchunk);
   float acc[4][4] = {};
-  for (int k0 = 0; k0 < K; k0 += kGK) {
+  for (int k0 = kb0; k0 < kb1; k0 += kGK) {
     for (int i = tid; i < kGT * kGK; i += 256) {
       const int r = i / kGK, kk = i % kGK;  // A tile: coalesced along k
       const int gm = m0 + r, gk = k0 + kk;
-      As[kk][r] = (gm < M && gk < K) ? A[(int64_t)gm * lda + gk] : 0.0f;
+      As[kk][r] = (gm < M && gk < kb1) ? A[(int64_t)gm * lda + gk] : 0.0f;
       const int kb = i / kGT, c = i % kGT;  // W tile: coalesced along n
       const int wk = k0 + kb, wn = n0 + c;
-      Bs[kb][c] = (wk < K && wn < N) ? W[(int64_t)wk * N + wn] : 0.0f;
+      Bs[kb][c] = (wk < kb1 && wn < N) ? __ldg(W + (int64_t)wk * N + wn) : 0.0f;
     }
     __syncthreads();
 #pragma unroll
@@ -287,6 +294,10 @@ __global__ void __launch_bounds__(256) k_gemm_f32(const float* __restrict__ A, i
     for (int j = 0; j < 4; ++j) {
       const int gn = n0 + tx * 4 + j;
       if (gn >= N) continue;
+      if (P != nullptr) {
+        P[((int64_t)blockIdx.z * M + gm) * N + gn] = acc[i][j];
+        continue;
+      }
       float v = acc[i][j] + bias[gn];
       if (relu) v = fmaxf(v, 0.0f);
       if (mask != nullptr) v *= mask[gn];
@@ -294,6 +305,22 @@ __global__ void __launch_bounds__(256) k_gemm_f32(const float* __restrict__ A, i
       C[(int64_t)gm * ldc + gn] = v;
     }
   }
+}
+
+// C = act(sum_s P[s] + b) * mask, partials added in split order
+__global__ void k_splitk_reduce(const float* __restrict__ P, int S, int M, int N, const float* __restrict__ bias,
+                                const float* __restrict__ mask, float* __restrict__ C, int ldc, int relu,
+                                int* nonfinite) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)M * N) return;
+  const int m = (int)(idx / N), n = (int)(idx % N);
+  float v = P[idx];
+  for (int s = 1; s < S; ++s) v += P[(int64_t)s * M * N + idx];
+  v += bias[n];
+  if (relu) v = fmaxf(v, 0.0f);
+  if (mask != nullptr) v *= mask[n];
+  flag_nonfinite(nonfinite, v);
+  C[(int64_t)m * ldc + n] = v;
 }
 
 // ---------------------------------------------------------------------------
@@ -354,11 +381,29 @@ cudaError_t launch_proj_inputs_v(const float* V, int nv, const ProjectorDev& p, 
   return cudaGetLastError();
 }
 
+// number of K chunks of a layer: a function of K only (batch independence);
+// ~288-wide chunks, at most 16
+int gemm_f32_splits(int K) {
+  const int s = (K + 287) / 288;
+  return s < 1 ? 1 : (s > 16 ? 16 : s);
+}
+
 cudaError_t launch_gemm_f32(const float* A, int lda, const float* W, const float* bias, const float* mask, float* C,
-                            int ldc, int M, int N, int K, int relu, int* nonfinite, cudaStream_t st) {
+                            int ldc, int M, int N, int K, int relu, int* nonfinite, float* partial,
+                            cudaStream_t st) {
   if (M == 0) return cudaSuccess;
-  dim3 grid((N + kGT - 1) / kGT, (M + kGT - 1) / kGT);
-  k_gemm_f32<<<grid, 256, 0, st>>>(A, lda, W, bias, mask, C, ldc, M, N, K, relu, nonfinite);
+  const int S = partial ? gemm_f32_splits(K) : 1;
+  int kchunk = (K + S - 1) / S;
+  kchunk = (kchunk + kGK - 1) / kGK * kGK;
+  const int Seff = (K + kchunk - 1) / kchunk;
+  dim3 grid((N + kGT - 1) / kGT, (M + kGT - 1) / kGT, Seff);
+  k_gemm_f32<<<grid, 256, 0, st>>>(A, lda, W, bias, mask, C, ldc, M, N, K, relu, nonfinite, kchunk,
+                                   Seff > 1 ? partial : nullptr);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess || Seff == 1) return e;
+  const int64_t tot = (int64_t)M * N;
+  k_splitk_reduce<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(partial, Seff, M, N, bias, mask, C, ldc, relu,
+                                                                 nonfinite);
   return cudaGetLastError();
 }
 

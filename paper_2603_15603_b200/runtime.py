@@ -77,7 +77,30 @@ _SIGS = {
     "fsb_nonfinite": (_i, [_p, ctypes.POINTER(_i), _i]),
     "fsb_counters": (_i, [_p, ctypes.POINTER(CountersC)]),
     "fsb_kernel_launches": (_i64, [_p]),
+    "fsb_selftest_umma": (_i, [_p, _p, _p, _i, _i, _p, _p]),
 }
+
+
+def pack_kmajor(mat_bf16_u16):
+    """Host packing of an (R, K) bf16 matrix (as uint16) into the K-major
+    no-swizzle UMMA byte image: element (r, k) at
+    (r // 8) * K * 16 + (k // 8) * 128 + (r % 8) * 16 + (k % 8) * 2."""
+    m = np.ascontiguousarray(mat_bf16_u16, dtype=np.uint16)
+    r, k = m.shape
+    if r % 8 or k % 8:
+        raise ShapeError("K-major packing needs rows and columns in multiples of 8")
+    return np.ascontiguousarray(m.reshape(r // 8, 8, k // 8, 8).transpose(0, 2, 1, 3)).reshape(-1)
+
+
+def to_bf16_bits(x):
+    """float32 -> bfloat16 bit patterns (round to nearest even)."""
+    a = np.ascontiguousarray(x, dtype=np.float32).view(np.uint32)
+    rnd = ((a >> 16) & 1) + 0x7FFF
+    return ((a + rnd) >> 16).astype(np.uint16)
+
+
+def bf16_bits_to_f32(b):
+    return (np.asarray(b, np.uint16).astype(np.uint32) << 16).view(np.float32)
 
 _LIB = None
 _LOCK = threading.Lock()
