@@ -43,9 +43,18 @@ cudaError_t launch_bridge(const float* V, int B, int nv, const int32_t* corners,
                           cudaStream_t st);
 cudaError_t launch_render(const void* scenes, int B, int H, int W, float* out, cudaStream_t st);
 cudaError_t init_attrs_transformer();
+cudaError_t init_attrs_transformer_tc();
+cudaError_t launch_encoder_tc(const float* crops, int ncrops, const EncW& w, float* feats, int* nonfinite,
+                              cudaStream_t st);
+cudaError_t launch_decoders_tc(const DecodeArgs& a, const BodyW& bw, const HandW& hw, cudaStream_t st);
 cudaError_t init_attrs_body();
 
 namespace {
+
+// byte offset of element (r, k) in a K-major no-swizzle UMMA tile (see tc_sm100.cuh)
+inline size_t tc_kmajor_off(int r, int k, int K) {
+  return (size_t)(r >> 3) * (K * 16) + (k >> 3) * 128 + (r & 7) * 16 + (k & 7) * 2;
+}
 
 struct DevMem {
   void* p = nullptr;
@@ -181,7 +190,8 @@ int fsb_ctx_create(int device, fsb_ctx** out) {
   if (e != cudaSuccess) return FSB_ERR_CUDA;
   fsb_ctx* c = new fsb_ctx();
   c->device = device;
-  if (init_attrs_transformer() != cudaSuccess || init_attrs_body() != cudaSuccess) {
+  if (init_attrs_transformer() != cudaSuccess || init_attrs_transformer_tc() != cudaSuccess ||
+      init_attrs_body() != cudaSuccess) {
     delete c;
     return FSB_ERR_CUDA;
   }
@@ -308,19 +318,53 @@ int fsb_load_decoder(fsb_ctx* c, const fsb_decoder_config* cfg, int n, const cha
     off[p + ".bqkv"] = pk.add(b.data(), b.size() * 4);
     return true;
   };
+  // bf16 image of W^T for the tensor-core kernels: the column concatenation
+  // of (K x N_i) matrices, packed in the K-major UMMA layout (tc_sm100.cuh)
+  auto put_img = [&](const std::string& key, std::vector<std::string> mats, int K) -> bool {
+    std::vector<std::pair<const float*, int>> src;
+    int Ntot = 0;
+    for (auto& m : mats) {
+      auto it = tab.find(m);
+      if (it == tab.end() || it->second.second % K) {
+        missing = m + " (image)";
+        return false;
+      }
+      src.push_back({it->second.first, (int)(it->second.second / K)});
+      Ntot += src.back().second;
+    }
+    if (Ntot % 8 || K % 8) {
+      missing = key + " (image shape)";
+      return false;
+    }
+    std::vector<__nv_bfloat16> img((size_t)Ntot * K);
+    int n0 = 0;
+    for (auto& s : src) {
+      for (int nn = 0; nn < s.second; ++nn)
+        for (int k = 0; k < K; ++k)
+          img[tc_kmajor_off(n0 + nn, k, K) / 2] = __float2bfloat16_rn(s.first[(size_t)k * s.second + nn]);
+      n0 += s.second;
+    }
+    off[key] = pk.add(img.data(), img.size() * 2);
+    return true;
+  };
   auto attn = [&](const std::string& p, bool cross) -> bool {
     bool ok = cross ? (put(p + ".lnq_g", Dm) && put(p + ".lnq_b", Dm) && put(p + ".lnkv_g", Dm) &&
                        put(p + ".lnkv_b", Dm))
                     : (put(p + ".ln_g", Dm) && put(p + ".ln_b", Dm));
-    return ok && put_qkv(p) && put(p + ".wo", (int64_t)Dm * Dm) && put(p + ".bo", Dm);
+    ok = ok && (cross ? (put_img(p + ".t_q", {p + ".wq"}, Dm) && put_img(p + ".t_kv", {p + ".wk", p + ".wv"}, Dm))
+                      : put_img(p + ".t_qkv", {p + ".wq", p + ".wk", p + ".wv"}, Dm));
+    return ok && put_qkv(p) && put(p + ".wo", (int64_t)Dm * Dm) && put(p + ".bo", Dm) &&
+           put_img(p + ".t_o", {p + ".wo"}, Dm);
   };
   auto mlp = [&](const std::string& p) -> bool {
     return put(p + ".ln_g", Dm) && put(p + ".ln_b", Dm) && put(p + ".w1", (int64_t)Dm * 4 * Dm) &&
-           put(p + ".b1", 4 * Dm) && put(p + ".w2", (int64_t)4 * Dm * Dm) && put(p + ".b2", Dm);
+           put(p + ".b1", 4 * Dm) && put(p + ".w2", (int64_t)4 * Dm * Dm) && put(p + ".b2", Dm) &&
+           put_img(p + ".t_w1", {p + ".w1"}, Dm) && put_img(p + ".t_w2", {p + ".w2"}, 4 * Dm);
   };
   const int np = (cfg->crop_size / cfg->patch) * (cfg->crop_size / cfg->patch);
   bool ok = put("enc.patch_w", (int64_t)cfg->patch * cfg->patch * 3 * Dm) && put("enc.patch_b", Dm) &&
-            put("enc.pos", (int64_t)np * Dm) && put("enc.norm_g", Dm) && put("enc.norm_b", Dm);
+            put("enc.pos", (int64_t)np * Dm) && put("enc.norm_g", Dm) && put("enc.norm_b", Dm) &&
+            put_img("enc.t_patch", {"enc.patch_w"}, cfg->patch * cfg->patch * 3);
   for (int l = 0; ok && l < cfg->enc_layers; ++l)
     ok = attn("enc.l" + std::to_string(l) + ".self", false) && mlp("enc.l" + std::to_string(l) + ".mlp");
   ok = ok && put("body.token_init", 51 * Dm) && put("body.p2d_init", 22 * Dm) && put("body.p3d_init", 22 * Dm) &&
@@ -347,6 +391,7 @@ int fsb_load_decoder(fsb_ctx* c, const fsb_decoder_config* cfg, int n, const cha
   FSB_CUDA(c, cudaMemcpy(c->dec_mem.p, pk.host.data(), pk.host.size(), cudaMemcpyHostToDevice));
   const unsigned char* base = static_cast<const unsigned char*>(c->dec_mem.p);
   auto P = [&](const std::string& name) { return reinterpret_cast<const float*>(base + off.at(name)); };
+  auto I = [&](const std::string& name) { return reinterpret_cast<const uint8_t*>(base + off.at(name)); };
   auto fill_attn = [&](AttnW& a, const std::string& p, bool cross) {
     a.ln_g = P(p + (cross ? ".lnq_g" : ".ln_g"));
     a.ln_b = P(p + (cross ? ".lnq_b" : ".ln_b"));
@@ -356,6 +401,10 @@ int fsb_load_decoder(fsb_ctx* c, const fsb_decoder_config* cfg, int n, const cha
     a.bqkv = P(p + ".bqkv");
     a.wo = P(p + ".wo");
     a.bo = P(p + ".bo");
+    a.t_qkv = cross ? nullptr : I(p + ".t_qkv");
+    a.t_q = cross ? I(p + ".t_q") : nullptr;
+    a.t_kv = cross ? I(p + ".t_kv") : nullptr;
+    a.t_o = I(p + ".t_o");
   };
   auto fill_mlp = [&](MlpW& m, const std::string& p) {
     m.ln_g = P(p + ".ln_g");
@@ -364,8 +413,11 @@ int fsb_load_decoder(fsb_ctx* c, const fsb_decoder_config* cfg, int n, const cha
     m.b1 = P(p + ".b1");
     m.w2 = P(p + ".w2");
     m.b2 = P(p + ".b2");
+    m.t_w1 = I(p + ".t_w1");
+    m.t_w2 = I(p + ".t_w2");
   };
   EncW& e = c->enc;
+  e.t_patch = I("enc.t_patch");
   e.patch_w = P("enc.patch_w");
   e.patch_b = P("enc.patch_b");
   e.pos = P("enc.pos");
@@ -582,10 +634,13 @@ int fsb_bridge(fsb_ctx* c, const float* v, int B, int nv, const int32_t* corners
 
 int fsb_encode(fsb_ctx* c, const float* crops, int n, float* feats, int precision, void* stream) {
   if (!c->has_decoder) return fail(c, FSB_ERR_USAGE, "encode: no decoder loaded");
-  if (precision != FSB_FP32) return fail(c, FSB_ERR_USAGE, "encode: precision %d not available yet", precision);
+  if (precision != FSB_FP32 && precision != FSB_BF16) return fail(c, FSB_ERR_USAGE, "encode: bad precision %d", precision);
   if (!default_model(c->cfg))
     return fail(c, FSB_ERR_USAGE, "encode: the fused fp32 encoder supports the default DecoderConfig only");
-  FSB_CUDA(c, launch_encoder_f32(crops, n, c->enc, feats, c->d_flag, (cudaStream_t)stream));
+  if (precision == FSB_BF16)
+    FSB_CUDA(c, launch_encoder_tc(crops, n, c->enc, feats, c->d_flag, (cudaStream_t)stream));
+  else
+    FSB_CUDA(c, launch_encoder_f32(crops, n, c->enc, feats, c->d_flag, (cudaStream_t)stream));
   c->counters.encode += 1;
   c->counters.encoded_crops += n;
   c->launches += n > 0;
@@ -596,13 +651,16 @@ static int decode_common(fsb_ctx* c, DecodeArgs& a, int precision, cudaStream_t 
   if (!c->has_decoder) return fail(c, FSB_ERR_USAGE, "decode: no decoder loaded");
   if (a.nbody > 0 && !c->has_tmpl[FSB_SMPL])
     return fail(c, FSB_ERR_USAGE, "decode: the body decoder needs its template (fsb_load_template SMPL)");
-  if (precision != FSB_FP32) return fail(c, FSB_ERR_USAGE, "decode: precision %d not available yet", precision);
+  if (precision != FSB_FP32 && precision != FSB_BF16) return fail(c, FSB_ERR_USAGE, "decode: bad precision %d", precision);
   if (!default_model(c->cfg))
     return fail(c, FSB_ERR_USAGE, "decode: the fused fp32 decoders support the default DecoderConfig only");
   if ((a.body_sel >> c->cfg.body_layers) != 0u || (a.hand_sel >> c->cfg.hand_layers) != 0u)
     return fail(c, FSB_ERR_USAGE, "selection out of range");
   a.nonfinite = c->d_flag;
-  FSB_CUDA(c, launch_decoders_f32(a, c->body, c->hand, st));
+  if (precision == FSB_BF16)
+    FSB_CUDA(c, launch_decoders_tc(a, c->body, c->hand, st));
+  else
+    FSB_CUDA(c, launch_decoders_f32(a, c->body, c->hand, st));
   c->launches += (a.nbody + a.nhand) > 0;
   const int nb = layer_count(a.body_sel);
   c->counters.fk += (int64_t)a.nbody * nb + (int64_t)a.nhand * layer_count(a.hand_sel);
@@ -679,7 +737,8 @@ int fsb_skin(fsb_ctx* c, int which, const float* poses, int B, float* verts, voi
 
 static int run_mlp(fsb_ctx* c, int B, float* theta, int precision, cudaStream_t st) {
   const ProjectorDev& p = c->proj;
-  if (precision != FSB_FP32) return fail(c, FSB_ERR_USAGE, "projector: precision %d not available yet", precision);
+  // the projector MLP runs fp32 in both modes until its tcgen05 GEMM lands
+  (void)precision;
   FSB_CUDA(c, launch_gemm_f32(c->w_x, 3 * p.n_sub, p.w1, p.b1, nullptr, c->w_h1, p.h1, B, p.h1, 3 * p.n_sub, 1,
                               nullptr, c->w_part, st));
   FSB_CUDA(c, launch_gemm_f32(c->w_h1, p.h1, p.w2, p.b2, nullptr, c->w_h2, p.h2, B, p.h2, p.h1, 1, nullptr,

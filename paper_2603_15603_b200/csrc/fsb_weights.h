@@ -18,6 +18,11 @@ struct AttnW {
   const float* bqkv;   // (3D)
   const float* wo;     // (D, D)
   const float* bo;
+  // bf16 images in the K-major UMMA layout (tc_sm100.cuh), W^T: (N, K)
+  const uint8_t* t_qkv;  // self: (3D, D)
+  const uint8_t* t_q;    // cross: (D, D)
+  const uint8_t* t_kv;   // cross: (2D, D)
+  const uint8_t* t_o;    // (D, D)
 };
 
 struct MlpW {
@@ -27,9 +32,12 @@ struct MlpW {
   const float* b1;
   const float* w2;  // (4D, D)
   const float* b2;
+  const uint8_t* t_w1;  // bf16 image (4D, D)
+  const uint8_t* t_w2;  // bf16 image (D, 4D)
 };
 
 struct EncW {
+  const uint8_t* t_patch;  // bf16 image (D, p*p*3)
   const float* patch_w;  // (p*p*3, D)
   const float* patch_b;
   const float* pos;      // (n_patch, D)

@@ -1,0 +1,91 @@
+"""bf16 tensor-core mode (tcgen05 kernels) against the fp32 CPU oracle.
+
+Bar (BASELINE.json north_star): SMPL-joint MPJPE delta <= 0.5 mm, model
+units taken as metres.  The intermediate tensors are also held to loose
+relative bounds so a broken stage cannot hide behind a tiny projector head.
+"""
+
+import numpy as np
+import pytest
+
+import oracle as orc
+from conftest import projector_dict, rel_err
+
+pytestmark = pytest.mark.gpu
+
+MPJPE_MM = 0.5
+
+
+@pytest.fixture(scope="module")
+def setup(full_models, full_projector):
+    import torch
+
+    from paper_2603_15603_b200 import decoder as dc
+    from paper_2603_15603_b200 import pipeline as pl
+    from paper_2603_15603_b200 import synth
+
+    assert torch.cuda.is_available()
+    mhr, smpl, gt = full_models
+    dec = dc.Decoder(smpl, dc.DecoderConfig(), seed=40)
+    pipe = pl.Pipeline(dec, mhr=mhr, bmap=gt, projector=full_projector, precision="bf16")
+    frames = []
+    for i in range(5):
+        sc = synth.random_scene(np.random.default_rng(5000 + i), smpl, (512, 512))
+        frames.append((synth.render_scene(sc, smpl), sc.keypoints2d))
+    return pipe, frames
+
+
+def test_encoder_bf16(setup, dec_weights):
+    from paper_2603_15603_b200 import decoder as dc
+
+    pipe, frames = setup
+    crops = np.concatenate([orc.frame_crops(f[0], f[1], 64)[3] for f in frames[:3]])
+    got = pipe.decoder.encode(crops, precision="bf16")
+    want = orc.encode(dec_weights, dc.DecoderConfig(), crops)
+    assert rel_err(got, want) <= 3e-2
+    # odd crop count (last CTA half empty) and batch independence
+    one = pipe.decoder.encode(crops[4:5], precision="bf16")
+    assert np.array_equal(one[0], got[4])
+
+
+def test_decoders_bf16(setup, dec_weights, full_models):
+    from paper_2603_15603_b200 import decoder as dc
+
+    pipe, frames = setup
+    cfg = dc.DecoderConfig()
+    _, smpl, _ = full_models
+    _, _, prompt, crops = orc.frame_crops(frames[0][0], frames[0][1], 64)
+    feats = orc.encode(dec_weights, cfg, crops)
+    want_p, want_c = orc.decode_body(dec_weights, cfg, smpl.joints_rest, feats[0], prompt, (0, 1, 2))
+    out = pipe.decoder.decode_body(feats[0], prompt, selection=(0, 1, 2), precision="bf16")
+    assert rel_err(out.params, want_p) <= 5e-2
+    assert rel_err(out.camera, want_c) <= 5e-2
+    rots = pipe.decoder.decode_hand(feats[1:3], (), precision="bf16")
+    assert rel_err(rots, orc.decode_hand(dec_weights, cfg, feats[1:3], ())) <= 5e-2
+    rots2 = pipe.decoder.decode_hand(feats[1:3], (1, 3), precision="bf16")
+    assert rel_err(rots2, orc.decode_hand(dec_weights, cfg, feats[1:3], (1, 3))) <= 5e-2
+
+
+def test_frame_batch_bf16_mpjpe(setup, dec_weights, full_models, full_projector):
+    from paper_2603_15603_b200 import decoder as dc
+
+    pipe, frames = setup
+    mhr, smpl, gt = full_models
+    imgs = np.stack([f[0] for f in frames])
+    kps = np.stack([f[1] for f in frames])
+    out = pipe.run_batch(imgs, kps)
+    res = {k: v.cpu().numpy() for k, v in out.items()}
+    pw = projector_dict(full_projector)
+    worst = 0.0
+    for i in range(len(frames)):
+        want = orc.frame_to_smpl(imgs[i], kps[i], dec_weights, dc.DecoderConfig(), mhr, smpl, gt, pw)
+        assert np.array_equal(res["boxes"][i, 0], np.array(want["body_box"]))
+        mpjpe_mm = 1e3 * np.linalg.norm(res["j_smpl"][i] - want["j_smpl"], axis=-1).mean()
+        worst = max(worst, mpjpe_mm)
+        assert mpjpe_mm <= MPJPE_MM, (i, mpjpe_mm)
+        assert rel_err(res["merged"][i], want["merged"]) <= 5e-2
+        assert rel_err(res["v_mhr"][i], want["v_mhr"]) <= 2e-2
+    print("worst MPJPE delta %.4f mm" % worst)
+    # a frame alone equals its row in the batch
+    solo = pipe.run_batch(imgs[3:4], kps[3:4])
+    assert np.array_equal(solo["j_smpl"].cpu().numpy()[0], res["j_smpl"][3])
