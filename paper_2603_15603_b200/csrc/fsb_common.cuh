@@ -67,39 +67,53 @@ __device__ __forceinline__ void rodrigues3(float wx, float wy, float wz, float* 
   r[8] = 1.0f - (wx * wx + wy * wy) * c;
 }
 
+// depth of each joint in the kinematic tree (depth[j] = depth[parent] + 1)
+__constant__ __device__ static const int8_t kDepth[FSB_NJ] = {0, 1, 2, 3, 4, 5, 1, 2, 3, 4, 1,
+                                                            2, 3, 4, 4, 5, 6, 7, 4, 5, 6, 7};
+
 // warp-cooperative FK; `pose` points at the 66 rotation params (shared or
 // global), `grest` at the 22x3 rest joints.  All lanes of the warp must call.
+// Lane j owns joint j: Rodrigues in parallel, then the chain is composed one
+// tree level at a time (8 levels instead of 22 serial joints), each joint
+// with the reference's fixed three-term accumulation order.
 __device__ __forceinline__ void fk_warp(const float* pose, const float* grest, FKOut& o, int lane) {
-  float rl[9];
-  if (lane < FSB_NJ) {
-    rodrigues3(pose[3 * lane], pose[3 * lane + 1], pose[3 * lane + 2], rl);
+  const int j = lane;
+  const int p = j < FSB_NJ ? kParents[j] : -1;
+  float loc[9], tl[3], g[3];
+  if (j < FSB_NJ) {
+    rodrigues3(pose[3 * j], pose[3 * j + 1], pose[3 * j + 2], loc);
 #pragma unroll
-    for (int e = 0; e < 9; ++e) o.rw[lane][e] = rl[e];  // local rotation, composed below
+    for (int a = 0; a < 3; ++a) {
+      g[a] = grest[3 * j + a];
+      tl[a] = (p < 0) ? g[a] : g[a] - grest[3 * p + a];
+    }
+    if (p < 0) {
+#pragma unroll
+      for (int e = 0; e < 9; ++e) o.rw[0][e] = loc[e];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) o.tw[0][a] = tl[a];
+    }
   }
   __syncwarp();
-  if (lane == 0) {
-    for (int j = 0; j < FSB_NJ; ++j) {
-      const int p = kParents[j];
-      float tl[3];
-      for (int a = 0; a < 3; ++a)
-        tl[a] = (p < 0) ? grest[3 * j + a] : grest[3 * j + a] - grest[3 * p + a];
-      if (p >= 0) {
-        float loc[9];
-        for (int e = 0; e < 9; ++e) loc[e] = o.rw[j][e];
-        const float* rp = o.rw[p];
-        for (int a = 0; a < 3; ++a) {
-          for (int b = 0; b < 3; ++b)
-            o.rw[j][3 * a + b] = rp[3 * a] * loc[b] + rp[3 * a + 1] * loc[3 + b] + rp[3 * a + 2] * loc[6 + b];
-          o.tw[j][a] = (rp[3 * a] * tl[0] + rp[3 * a + 1] * tl[1] + rp[3 * a + 2] * tl[2]) + o.tw[p][a];
-        }
-      } else {
-        for (int a = 0; a < 3; ++a) o.tw[j][a] = tl[a];
+#pragma unroll 1
+  for (int lvl = 1; lvl < 8; ++lvl) {
+    if (j < FSB_NJ && kDepth[j] == lvl) {
+      const float* rp = o.rw[p];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+#pragma unroll
+        for (int b = 0; b < 3; ++b)
+          o.rw[j][3 * a + b] = rp[3 * a] * loc[b] + rp[3 * a + 1] * loc[3 + b] + rp[3 * a + 2] * loc[6 + b];
+        o.tw[j][a] = (rp[3 * a] * tl[0] + rp[3 * a + 1] * tl[1] + rp[3 * a + 2] * tl[2]) + o.tw[p][a];
       }
-      const float* rj = o.rw[j];
-      for (int a = 0; a < 3; ++a)
-        o.at[j][a] = o.tw[j][a] - (rj[3 * a] * grest[3 * j] + rj[3 * a + 1] * grest[3 * j + 1] +
-                                   rj[3 * a + 2] * grest[3 * j + 2]);
     }
+    __syncwarp();
+  }
+  if (j < FSB_NJ) {
+    const float* rj = o.rw[j];
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+      o.at[j][a] = o.tw[j][a] - (rj[3 * a] * g[0] + rj[3 * a + 1] * g[1] + rj[3 * a + 2] * g[2]);
   }
   __syncwarp();
 }

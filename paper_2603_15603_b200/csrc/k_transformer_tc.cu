@@ -113,81 +113,89 @@ __device__ __forceinline__ void st_row_zero8(uint8_t* tile, int r, int k0, int K
   *reinterpret_cast<uint4*>(tile + tc::kmajor_off(r, k0, K)) = make_uint4(0u, 0u, 0u, 0u);
 }
 
-// LayerNorm of the thread's row (numkit.py:198-202), bf16 into the A tile
-__device__ __forceinline__ void ln_to_tile(const float* x, const float* g, const float* b, uint8_t* tile, int r) {
-  float s = 0.0f;
+// 64-element row reductions with 8 independent partial chains
+__device__ __forceinline__ float sum64(const float* v) {
+  float p[8];
 #pragma unroll
-  for (int c = 0; c < D; ++c) s += x[c];
-  const float mu = s * (1.0f / D);
-  float q = 0.0f;
+  for (int i = 0; i < 8; ++i) p[i] = v[i];
+#pragma unroll
+  for (int c = 8; c < 64; ++c) p[c & 7] += v[c];
+  return ((p[0] + p[1]) + (p[2] + p[3])) + ((p[4] + p[5]) + (p[6] + p[7]));
+}
+
+// mean and 1/sqrt(var + eps) of a 64-float row (numkit.py:198-202)
+__device__ __forceinline__ void row_stats(const float* x, float& mu, float& rstd) {
+  mu = sum64(x) * (1.0f / D);
+  float p[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) p[i] = 0.0f;
 #pragma unroll
   for (int c = 0; c < D; ++c) {
     const float d = x[c] - mu;
-    q = fmaf(d, d, q);
+    p[c & 7] = fmaf(d, d, p[c & 7]);
   }
-  const float sd = sqrtf(q * (1.0f / D) + 1e-5f);
+  const float q = ((p[0] + p[1]) + (p[2] + p[3])) + ((p[4] + p[5]) + (p[6] + p[7]));
+  rstd = 1.0f / sqrtf(q * (1.0f / D) + 1e-5f);
+}
+
+// LayerNorm of the thread's row, bf16 into the A tile
+__device__ __forceinline__ void ln_to_tile(const float* x, const float* g, const float* b, uint8_t* tile, int r) {
+  float mu, rstd;
+  row_stats(x, mu, rstd);
 #pragma unroll
   for (int c0 = 0; c0 < D; c0 += 8) {
     float v[8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) v[i] = (x[c0 + i] - mu) / sd * __ldg(g + c0 + i) + __ldg(b + c0 + i);
+    for (int i = 0; i < 8; ++i) v[i] = fmaf((x[c0 + i] - mu) * rstd, __ldg(g + c0 + i), __ldg(b + c0 + i));
     st_row8(tile, r, c0, D, v);
   }
 }
 
 __device__ __forceinline__ void ln_row(const float* x, const float* g, const float* b, float* y) {
-  float s = 0.0f;
+  float mu, rstd;
+  row_stats(x, mu, rstd);
 #pragma unroll
-  for (int c = 0; c < D; ++c) s += x[c];
-  const float mu = s * (1.0f / D);
-  float q = 0.0f;
-#pragma unroll
-  for (int c = 0; c < D; ++c) {
-    const float d = x[c] - mu;
-    q = fmaf(d, d, q);
-  }
-  const float sd = sqrtf(q * (1.0f / D) + 1e-5f);
-#pragma unroll
-  for (int c = 0; c < D; ++c) y[c] = (x[c] - mu) / sd * __ldg(g + c) + __ldg(b + c);
+  for (int c = 0; c < D; ++c) y[c] = fmaf((x[c] - mu) * rstd, __ldg(g + c), __ldg(b + c));
 }
 
 // q (cols qcol..+64 of TMEM) + bias -> per-head query tiles
 __device__ void drain_q(Pipe& P, uint32_t qcol, const float* bq) {
   const int t = P.tid;
+  float v[64];
+  tc::tmem_ld64(P.lane_addr(qcol), v);
 #pragma unroll
   for (int h = 0; h < 4; ++h) {
-    float v[16];
-    tc::tmem_ld16(P.lane_addr(qcol + 16 * h), v);
 #pragma unroll
-    for (int i = 0; i < 16; ++i) v[i] += __ldg(bq + 16 * h + i);
+    for (int i = 0; i < 16; ++i) v[16 * h + i] += __ldg(bq + 16 * h + i);
     uint8_t* tq = P.smem + S_Q + h * 4096;
-    st_row8(tq, t, 0, DH, v);
-    st_row8(tq, t, 8, DH, v + 8);
+    st_row8(tq, t, 0, DH, v + 16 * h);
+    st_row8(tq, t, 8, DH, v + 16 * h + 8);
   }
 }
 
 // k | v (cols kcol..+128) + bias -> per-head key tiles and transposed values
 __device__ void drain_kv(Pipe& P, uint32_t kcol, const float* bk, const float* bv) {
   const int t = P.tid;
+  float v[64];
+  tc::tmem_ld64(P.lane_addr(kcol), v);
 #pragma unroll
   for (int h = 0; h < 4; ++h) {
-    float v[16];
-    tc::tmem_ld16(P.lane_addr(kcol + 16 * h), v);
 #pragma unroll
-    for (int i = 0; i < 16; ++i) v[i] += __ldg(bk + 16 * h + i);
+    for (int i = 0; i < 16; ++i) v[16 * h + i] += __ldg(bk + 16 * h + i);
     uint8_t* tk = P.smem + S_K + h * 4096;
-    st_row8(tk, t, 0, DH, v);
-    st_row8(tk, t, 8, DH, v + 8);
+    st_row8(tk, t, 0, DH, v + 16 * h);
+    st_row8(tk, t, 8, DH, v + 16 * h + 8);
   }
+  tc::tmem_ld64(P.lane_addr(kcol + 64), v);
+  // V^T tile (16 x 128 per head): row d, column = this thread's key index
+  const uint32_t col_off = (uint32_t)(t >> 3) * 128u + (uint32_t)(t & 7) * 2u;
 #pragma unroll
   for (int h = 0; h < 4; ++h) {
-    float v[16];
-    tc::tmem_ld16(P.lane_addr(kcol + 64 + 16 * h), v);
-    uint8_t* tv = P.smem + S_VT + h * 4096;
+    uint8_t* tv = P.smem + S_VT + h * 4096 + col_off;
 #pragma unroll
     for (int d = 0; d < DH; ++d) {
-      const __nv_bfloat16 hv = __float2bfloat16_rn(v[d] + __ldg(bv + 16 * h + d));
-      *reinterpret_cast<__nv_bfloat16*>(tv + tc::kmajor_off(d, t, 128)) = hv;
+      const __nv_bfloat16 hv = __float2bfloat16_rn(v[16 * h + d] + __ldg(bv + 16 * h + d));
+      *reinterpret_cast<__nv_bfloat16*>(tv + (d >> 3) * 2048 + (d & 7) * 16) = hv;
     }
   }
 }
@@ -198,21 +206,22 @@ __device__ void softmax_pair(Pipe& P, int nk) {
 #pragma unroll 1
   for (int j = 0; j < 2; ++j) {
     float s[64];
+    tc::tmem_ld64(P.lane_addr(T_GEN + 128 * j + 64 * blk), s);
+    float m8[8];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) tc::tmem_ld16(P.lane_addr(T_GEN + 128 * j + 64 * blk + 16 * q), s + 16 * q);
-    float mx = -INFINITY;
-#pragma unroll
-    for (int k = 0; k < 64; ++k) {
-      s[k] = (k < nk) ? s[k] * 0.25f : -INFINITY;  // f32(1/sqrt(16))
-      mx = fmaxf(mx, s[k]);
-    }
-    float sum = 0.0f;
+    for (int i = 0; i < 8; ++i) m8[i] = -INFINITY;
+    // logits scaled by f32(1/sqrt(16)) and by log2(e) for the exp2 below
+    constexpr float kScale = 0.25f * 1.4426950408889634f;
 #pragma unroll
     for (int k = 0; k < 64; ++k) {
-      s[k] = (k < nk) ? expf(s[k] - mx) : 0.0f;
-      sum += s[k];
+      s[k] = (k < nk) ? s[k] * kScale : -INFINITY;
+      m8[k & 7] = fmaxf(m8[k & 7], s[k]);
     }
-    const float inv = 1.0f / sum;
+    const float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
+                           fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
+#pragma unroll
+    for (int k = 0; k < 64; ++k) s[k] = (k < nk) ? exp2f(s[k] - mx) : 0.0f;
+    const float inv = 1.0f / sum64(s);
     uint8_t* tp = P.smem + S_HP + j * 32768;
 #pragma unroll
     for (int q = 0; q < 8; ++q) {
@@ -253,8 +262,7 @@ __device__ void attn_core(Pipe& P, int nk, float* ctx) {
     }
     P.commit_wait();
   }
-#pragma unroll
-  for (int q = 0; q < 4; ++q) tc::tmem_ld16(P.lane_addr(T_O + 16 * q), ctx + 16 * q);
+  tc::tmem_ld64(P.lane_addr(T_O), ctx);
 }
 
 // x += Wo . ctx + bo for valid rows
@@ -267,14 +275,11 @@ __device__ void out_proj(Pipe& P, const float* ctx, const float* bo, float* x, b
   if (P.tid == 0) gemm(P.sbase + S_A, D, w, D, T_GEN, P.tmem);
   P.prefetch();
   P.commit_wait();
-  float v[16];
+  float v[64];
+  tc::tmem_ld64(P.lane_addr(T_GEN), v);
+  if (valid)
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    tc::tmem_ld16(P.lane_addr(T_GEN + 16 * q), v);
-    if (valid)
-#pragma unroll
-      for (int i = 0; i < 16; ++i) x[16 * q + i] += v[i] + __ldg(bo + 16 * q + i);
-  }
+    for (int c = 0; c < D; ++c) x[c] += v[c] + __ldg(bo + c);
 }
 
 // self attention sub-layer: x += MHA(LN(x + pos))  (decoder.py:214-218)
@@ -332,27 +337,24 @@ __device__ void mlp(Pipe& P, const MlpW& w, float* x, bool valid) {
   P.commit_wait();
   uint8_t* th = P.smem + S_HP;
 #pragma unroll 1
-  for (int q = 0; q < 16; ++q) {
-    float v[16];
-    tc::tmem_ld16(P.lane_addr(T_GEN + 16 * q), v);
+  for (int q = 0; q < 4; ++q) {
+    float v[64];
+    tc::tmem_ld64(P.lane_addr(T_GEN + 64 * q), v);
 #pragma unroll
-    for (int i = 0; i < 16; ++i) v[i] = fmaxf(v[i] + __ldg(w.b1 + 16 * q + i), 0.0f);
-    st_row8(th, P.tid, 16 * q, 4 * D, v);
-    st_row8(th, P.tid, 16 * q + 8, 4 * D, v + 8);
+    for (int i = 0; i < 64; ++i) v[i] = fmaxf(v[i] + __ldg(w.b1 + 64 * q + i), 0.0f);
+#pragma unroll
+    for (int i = 0; i < 64; i += 8) st_row8(th, P.tid, 64 * q + i, 4 * D, v + i);
   }
   const uint32_t w2 = P.acquire();
   P.before_issue();
   if (P.tid == 0) gemm(P.sbase + S_HP, 4 * D, w2, D, T_GEN, P.tmem);
   P.prefetch();
   P.commit_wait();
-  float v[16];
+  float v[64];
+  tc::tmem_ld64(P.lane_addr(T_GEN), v);
+  if (valid)
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    tc::tmem_ld16(P.lane_addr(T_GEN + 16 * q), v);
-    if (valid)
-#pragma unroll
-      for (int i = 0; i < 16; ++i) x[16 * q + i] += v[i] + __ldg(w.b2 + 16 * q + i);
-  }
+    for (int c = 0; c < D; ++c) x[c] += v[c] + __ldg(w.b2 + c);
 }
 
 __device__ void setup(Pipe& P, Shared& sh, uint8_t* smem) {
@@ -478,6 +480,7 @@ struct BodyAux {  // fp32 scratch per block
   float jc[2][66];
   int pred[2];
   FKOut fk[2];
+  float boxtok[2][4 * D];
 };
 struct HandAux {
   float t0[2][D];
@@ -496,16 +499,20 @@ __device__ void body_heads(Pipe& P, BodyAux& ax, const BodyW& w, const float* x)
     for (int c = 0; c < D; ++c) ax.t0[blk][c] = y[c];
   }
   __syncthreads();
-  for (int j = t; j < 2 * 79; j += NTH) {
-    const int b = j / 79, o = j % 79;
-    const float* W = o < FSB_PARAM_DIM ? w.head_params_w : w.head_cam_w;
-    const int n = o < FSB_PARAM_DIM ? FSB_PARAM_DIM : 3, oo = o < FSB_PARAM_DIM ? o : o - FSB_PARAM_DIM;
-    float acc = 0.0f;
-    for (int k = 0; k < D; ++k) acc = fmaf(ax.t0[b][k], __ldg(W + k * n + oo), acc);
-    if (o < FSB_PARAM_DIM)
-      ax.params[b][oo] = acc + __ldg(w.head_params_b + oo);
+  // thread (blk, r) evaluates outputs r and r + 64 of its block's 79 head
+  // outputs (76 params + 3 camera); 64 independent loads per output
+  for (int o = r; o < 79; o += 64) {
+    const bool is_p = o < FSB_PARAM_DIM;
+    const float* W = is_p ? w.head_params_w : w.head_cam_w;
+    const int n = is_p ? FSB_PARAM_DIM : 3, oo = is_p ? o : o - FSB_PARAM_DIM;
+    float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+    for (int k = 0; k < D; ++k) acc[k & 3] = fmaf(ax.t0[blk][k], __ldg(W + k * n + oo), acc[k & 3]);
+    const float v = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+    if (is_p)
+      ax.params[blk][oo] = v + __ldg(w.head_params_b + oo);
     else
-      ax.cam[b][oo] = acc + __ldg(w.head_cam_b + oo);
+      ax.cam[blk][oo] = v + __ldg(w.head_cam_b + oo);
   }
   __syncthreads();
 }
@@ -556,23 +563,26 @@ __global__ void __launch_bounds__(NTH, 1) k_decoders_tc(DecodeArgs a, BodyW bw, 
   BodyAux& bx = *reinterpret_cast<BodyAux*>(smem + S_AUX);
   HandAux& hx = *reinterpret_cast<HandAux*>(smem + S_AUX);
   if (body) {
-    // tokens = token_init, rows 1..4 += prompt_box(prompt)  (decoder.py:287-293)
-    float pr[8];
+    // tokens = token_init, rows 1..4 += prompt_box(prompt)  (decoder.py:287-293);
+    // the 2 x 256 box-token outputs are spread over the CTA, 4 per thread
+    for (int i = 0; i < 4; ++i) {
+      const int idx = 4 * t + i, b = idx / (4 * D), o = idx % (4 * D);
+      const int u = 2 * blockIdx.x + b;
+      float acc = 0.0f;
+      if (u < a.nbody) {
 #pragma unroll
-    for (int k = 0; k < 8; ++k) pr[k] = uvalid ? a.prompts[(int64_t)unit * 8 + k] : 0.0f;
+        for (int k = 0; k < 8; ++k) acc = fmaf(a.prompts[(int64_t)u * 8 + k], __ldg(bw.prompt_box_w + k * 4 * D + o), acc);
+      }
+      bx.boxtok[b][o] = acc + __ldg(bw.prompt_box_b + o);
+    }
+    if (t < 2) bx.pred[t] = 0;
+    __syncthreads();
 #pragma unroll
     for (int c = 0; c < D; ++c) {
       float v = valid ? __ldg(bw.token_init + r * D + c) : 0.0f;
-      if (valid && r >= 1 && r < 5) {
-        const int o = (r - 1) * D + c;
-        float acc = 0.0f;
-#pragma unroll
-        for (int k = 0; k < 8; ++k) acc = fmaf(pr[k], __ldg(bw.prompt_box_w + k * 4 * D + o), acc);
-        v += acc + __ldg(bw.prompt_box_b + o);
-      }
+      if (valid && r >= 1 && r < 5) v += bx.boxtok[blk][(r - 1) * D + c];
       x[c] = v;
     }
-    if (t < 2) bx.pred[t] = 0;
   } else {
 #pragma unroll
     for (int c = 0; c < D; ++c) x[c] = valid ? __ldg(hw.token_init + r * D + c) : 0.0f;
