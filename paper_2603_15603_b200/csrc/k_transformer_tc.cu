@@ -7,22 +7,24 @@
 // are fp32 in TMEM, and the LayerNorm / softmax / residual / ReLU
 // epilogues run in fp32 registers.
 //
-// One CTA = 4 warps = 128 TMEM lanes = 128 token rows, organised as two
-// 64-row blocks: two crops (encoder), two frames' body tokens (51 valid
-// rows each) or two hands (4 valid rows each).  Thread t owns row t for the
-// whole network: its residual-stream row lives in 64 registers, LayerNorm
-// and softmax are per-thread row reductions with no shuffles, and it writes
-// its own row of every bf16 operand.  Attention of the two blocks is done
-// as one 128 x 128 score tile whose off-diagonal block is masked to zero, so
-// P.V stays a single MMA chain.  Weights (pre-packed bf16 W^T images) stream
-// through two 32 KB slots with cp.async.bulk, one GEMM ahead of use.
+// One CTA = 8 warps = 256 threads over 128 TMEM lanes = 128 token rows,
+// organised as two 64-row blocks: two crops (encoder), two frames' body
+// tokens (51 valid rows each) or two hands (4 valid rows each).  Row r is
+// owned by threads r and r + 128 (warps w and w + 4 read the same TMEM lane
+// quadrant): each holds 32 of the row's 64 residual-stream values in
+// registers, LayerNorm sums are combined through a double-buffered shared
+// exchange (one barrier per reduction), and in attention each of the two
+// threads runs the softmax of a different head.  Attention of the two
+// blocks is one 128 x 128 score tile whose off-diagonal block is masked to
+// zero, so P.V stays a single MMA chain.  Weights (pre-packed bf16 W^T
+// images) stream through two 32 KB slots with cp.async.bulk, one GEMM ahead.
 #include "fsb_common.cuh"
 #include "fsb_weights.h"
 #include "tc_sm100.cuh"
 
 namespace {
 
-constexpr int D = 64, DH = 16, NTH = 128, BLK = 64;
+constexpr int D = 64, DH = 16, NTH = 256, ROWS = 128, BLK = 64, HC = 32;  // HC: columns per thread
 
 // shared memory map (bytes)
 constexpr uint32_t S_A = 0;         // 128 x 64 bf16 GEMM A operand           16 KB
@@ -48,17 +50,18 @@ struct Shared {
   int nw;
   const uint8_t* wptr[kMaxW];
   uint32_t wbytes[kMaxW];
+  float xch[2][2 * ROWS];  // row-reduction exchange, double buffered
 };
 
 // per-thread pipeline state (every thread tracks the same phases)
 struct Pipe {
   Shared* sh;
   uint8_t* smem;
-  uint32_t sbase;   // shared-space address of smem
+  uint32_t sbase;  // shared-space address of smem
   uint32_t tmem;
   uint32_t mphase;
-  int wload, wuse;
-  int tid;
+  int wload, wuse, xc;
+  int tid, r, h;
 
   __device__ void prefetch() {  // next weight image into its ring slot
     if (wload < sh->nw) {
@@ -90,13 +93,26 @@ struct Pipe {
     tc::fence_after();
   }
   __device__ uint32_t lane_addr(uint32_t col) const {
-    return tmem + ((uint32_t)((tid >> 5) * 32) << 16) + col;
+    return tmem + ((uint32_t)(((tid >> 5) & 3) * 32) << 16) + col;
+  }
+  // sum of the two threads' partials of row r (one barrier)
+  __device__ float row_total(float part) {
+    float* b = sh->xch[xc & 1];
+    ++xc;
+    b[h * ROWS + r] = part;
+    __syncthreads();
+    return b[r] + b[ROWS + r];
   }
 };
 
 __device__ __forceinline__ void gemm(uint32_t a, int K, uint32_t b, int N, uint32_t dcol, uint32_t tmem) {
   const uint32_t id = tc::idesc_bf16(128, N);
   for (int k = 0; k < K; k += 16) tc::mma_bf16(tmem + dcol, tc::kmajor_desc(a, K, k), tc::kmajor_desc(b, K, k), id, k > 0);
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+  tc::tmem_ld16(taddr, v);
+  tc::tmem_ld16(taddr + 16, v + 16);
 }
 
 // store 8 consecutive bf16 values of row r at column k0 of a K-major tile
@@ -113,129 +129,120 @@ __device__ __forceinline__ void st_row_zero8(uint8_t* tile, int r, int k0, int K
   *reinterpret_cast<uint4*>(tile + tc::kmajor_off(r, k0, K)) = make_uint4(0u, 0u, 0u, 0u);
 }
 
-// 64-element row reductions with 8 independent partial chains
-__device__ __forceinline__ float sum64(const float* v) {
+// 32-element sum with 8 independent partial chains
+__device__ __forceinline__ float sum32(const float* v) {
   float p[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) p[i] = v[i];
 #pragma unroll
-  for (int c = 8; c < 64; ++c) p[c & 7] += v[c];
+  for (int c = 8; c < 32; ++c) p[c & 7] += v[c];
   return ((p[0] + p[1]) + (p[2] + p[3])) + ((p[4] + p[5]) + (p[6] + p[7]));
 }
 
-// mean and 1/sqrt(var + eps) of a 64-float row (numkit.py:198-202)
-__device__ __forceinline__ void row_stats(const float* x, float& mu, float& rstd) {
-  mu = sum64(x) * (1.0f / D);
-  float p[8];
+// LayerNorm (numkit.py:198-202) of row r split over the thread pair: this
+// thread's 32 columns [32h, 32h + 32) normalised into y
+__device__ __forceinline__ void ln_half(Pipe& P, const float* x, const float* g, const float* b, float* y) {
+  const float mu = P.row_total(sum32(x)) * (1.0f / D);
+  float d[HC];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) p[i] = 0.0f;
-#pragma unroll
-  for (int c = 0; c < D; ++c) {
-    const float d = x[c] - mu;
-    p[c & 7] = fmaf(d, d, p[c & 7]);
+  for (int c = 0; c < HC; ++c) {
+    const float e = x[c] - mu;
+    d[c] = e * e;
   }
-  const float q = ((p[0] + p[1]) + (p[2] + p[3])) + ((p[4] + p[5]) + (p[6] + p[7]));
-  rstd = 1.0f / sqrtf(q * (1.0f / D) + 1e-5f);
+  const float rstd = 1.0f / sqrtf(P.row_total(sum32(d)) * (1.0f / D) + 1e-5f);
+  const int c0 = HC * P.h;
+#pragma unroll
+  for (int c = 0; c < HC; ++c) y[c] = fmaf((x[c] - mu) * rstd, __ldg(g + c0 + c), __ldg(b + c0 + c));
 }
 
-// LayerNorm of the thread's row, bf16 into the A tile
-__device__ __forceinline__ void ln_to_tile(const float* x, const float* g, const float* b, uint8_t* tile, int r) {
-  float mu, rstd;
-  row_stats(x, mu, rstd);
+__device__ __forceinline__ void ln_half_to_tile(Pipe& P, const float* x, const float* g, const float* b) {
+  float y[HC];
+  ln_half(P, x, g, b, y);
 #pragma unroll
-  for (int c0 = 0; c0 < D; c0 += 8) {
-    float v[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) v[i] = fmaf((x[c0 + i] - mu) * rstd, __ldg(g + c0 + i), __ldg(b + c0 + i));
-    st_row8(tile, r, c0, D, v);
-  }
+  for (int q = 0; q < HC; q += 8) st_row8(P.smem + S_A, P.r, HC * P.h + q, D, y + q);
 }
 
-__device__ __forceinline__ void ln_row(const float* x, const float* g, const float* b, float* y) {
-  float mu, rstd;
-  row_stats(x, mu, rstd);
-#pragma unroll
-  for (int c = 0; c < D; ++c) y[c] = fmaf((x[c] - mu) * rstd, __ldg(g + c), __ldg(b + c));
-}
-
-// q (cols qcol..+64 of TMEM) + bias -> per-head query tiles
+// query columns [qcol, +64) + bias -> heads 2h, 2h+1 of the query tiles
 __device__ void drain_q(Pipe& P, uint32_t qcol, const float* bq) {
-  const int t = P.tid;
-  float v[64];
-  tc::tmem_ld64(P.lane_addr(qcol), v);
+  float v[HC];
+  tmem_ld32(P.lane_addr(qcol + HC * P.h), v);
 #pragma unroll
-  for (int h = 0; h < 4; ++h) {
+  for (int j = 0; j < 2; ++j) {
+    const int hd = 2 * P.h + j;
 #pragma unroll
-    for (int i = 0; i < 16; ++i) v[16 * h + i] += __ldg(bq + 16 * h + i);
-    uint8_t* tq = P.smem + S_Q + h * 4096;
-    st_row8(tq, t, 0, DH, v + 16 * h);
-    st_row8(tq, t, 8, DH, v + 16 * h + 8);
+    for (int i = 0; i < 16; ++i) v[16 * j + i] += __ldg(bq + 16 * hd + i);
+    uint8_t* tq = P.smem + S_Q + hd * 4096;
+    st_row8(tq, P.r, 0, DH, v + 16 * j);
+    st_row8(tq, P.r, 8, DH, v + 16 * j + 8);
   }
 }
 
-// k | v (cols kcol..+128) + bias -> per-head key tiles and transposed values
+// key | value columns [kcol, +128) + bias -> key tiles and transposed values
 __device__ void drain_kv(Pipe& P, uint32_t kcol, const float* bk, const float* bv) {
-  const int t = P.tid;
-  float v[64];
-  tc::tmem_ld64(P.lane_addr(kcol), v);
+  float v[HC];
+  tmem_ld32(P.lane_addr(kcol + HC * P.h), v);
 #pragma unroll
-  for (int h = 0; h < 4; ++h) {
+  for (int j = 0; j < 2; ++j) {
+    const int hd = 2 * P.h + j;
 #pragma unroll
-    for (int i = 0; i < 16; ++i) v[16 * h + i] += __ldg(bk + 16 * h + i);
-    uint8_t* tk = P.smem + S_K + h * 4096;
-    st_row8(tk, t, 0, DH, v + 16 * h);
-    st_row8(tk, t, 8, DH, v + 16 * h + 8);
+    for (int i = 0; i < 16; ++i) v[16 * j + i] += __ldg(bk + 16 * hd + i);
+    uint8_t* tk = P.smem + S_K + hd * 4096;
+    st_row8(tk, P.r, 0, DH, v + 16 * j);
+    st_row8(tk, P.r, 8, DH, v + 16 * j + 8);
   }
-  tc::tmem_ld64(P.lane_addr(kcol + 64), v);
-  // V^T tile (16 x 128 per head): row d, column = this thread's key index
-  const uint32_t col_off = (uint32_t)(t >> 3) * 128u + (uint32_t)(t & 7) * 2u;
+  tmem_ld32(P.lane_addr(kcol + 64 + HC * P.h), v);
+  // V^T tile per head (16 x 128): row d, column = this row's key index
+  const uint32_t col_off = (uint32_t)(P.r >> 3) * 128u + (uint32_t)(P.r & 7) * 2u;
 #pragma unroll
-  for (int h = 0; h < 4; ++h) {
-    uint8_t* tv = P.smem + S_VT + h * 4096 + col_off;
+  for (int j = 0; j < 2; ++j) {
+    const int hd = 2 * P.h + j;
+    uint8_t* tv = P.smem + S_VT + hd * 4096 + col_off;
 #pragma unroll
     for (int d = 0; d < DH; ++d) {
-      const __nv_bfloat16 hv = __float2bfloat16_rn(v[16 * h + d] + __ldg(bv + 16 * h + d));
+      const __nv_bfloat16 hv = __float2bfloat16_rn(v[16 * j + d] + __ldg(bv + 16 * hd + d));
       *reinterpret_cast<__nv_bfloat16*>(tv + (d >> 3) * 2048 + (d & 7) * 16) = hv;
     }
   }
 }
 
-// softmax of heads (2p, 2p+1) over the thread's own key block
-__device__ void softmax_pair(Pipe& P, int nk) {
-  const int t = P.tid, blk = t / BLK;
-#pragma unroll 1
-  for (int j = 0; j < 2; ++j) {
-    float s[64];
-    tc::tmem_ld64(P.lane_addr(T_GEN + 128 * j + 64 * blk), s);
-    float m8[8];
+// softmax of head (2 * pair + h) over the row's own key block -> P tile h
+__device__ void softmax_head(Pipe& P, int nk) {
+  const int blk = P.r / BLK;
+  float s[64];
+  tc::tmem_ld64(P.lane_addr(T_GEN + 128 * P.h + 64 * blk), s);
+  float m8[8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) m8[i] = -INFINITY;
-    // logits scaled by f32(1/sqrt(16)) and by log2(e) for the exp2 below
-    constexpr float kScale = 0.25f * 1.4426950408889634f;
+  for (int i = 0; i < 8; ++i) m8[i] = -INFINITY;
+  constexpr float kScale = 0.25f * 1.4426950408889634f;  // f32(1/sqrt(16)) * log2(e)
 #pragma unroll
-    for (int k = 0; k < 64; ++k) {
-      s[k] = (k < nk) ? s[k] * kScale : -INFINITY;
-      m8[k & 7] = fmaxf(m8[k & 7], s[k]);
-    }
-    const float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])),
-                           fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
+  for (int k = 0; k < 64; ++k) {
+    s[k] = (k < nk) ? s[k] * kScale : -INFINITY;
+    m8[k & 7] = fmaxf(m8[k & 7], s[k]);
+  }
+  const float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])), fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
+  float p8[8];
 #pragma unroll
-    for (int k = 0; k < 64; ++k) s[k] = (k < nk) ? exp2f(s[k] - mx) : 0.0f;
-    const float inv = 1.0f / sum64(s);
-    uint8_t* tp = P.smem + S_HP + j * 32768;
+  for (int i = 0; i < 8; ++i) p8[i] = 0.0f;
 #pragma unroll
-    for (int q = 0; q < 8; ++q) {
-      float v[8];
+  for (int k = 0; k < 64; ++k) {
+    s[k] = (k < nk) ? exp2f(s[k] - mx) : 0.0f;
+    p8[k & 7] += s[k];
+  }
+  const float inv = 1.0f / (((p8[0] + p8[1]) + (p8[2] + p8[3])) + ((p8[4] + p8[5]) + (p8[6] + p8[7])));
+  uint8_t* tp = P.smem + S_HP + P.h * 32768;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) v[i] = s[8 * q + i] * inv;
-      st_row8(tp, t, 64 * blk + 8 * q, 128, v);
-      st_row_zero8(tp, t, 64 * (1 - blk) + 8 * q, 128);
-    }
+  for (int q = 0; q < 8; ++q) {
+    float v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = s[8 * q + i] * inv;
+    st_row8(tp, P.r, 64 * blk + 8 * q, 128, v);
+    st_row_zero8(tp, P.r, 64 * (1 - blk) + 8 * q, 128);
   }
 }
 
-// the four heads of one attention given sQ / sK / sVt; context -> ctx[64]
-__device__ void attn_core(Pipe& P, int nk, float* ctx) {
+// the four heads of one attention given sQ / sK / sVt; the context is
+// written as bf16 straight into the A tile of the output projection
+__device__ void attn_core(Pipe& P, int nk) {
   const uint32_t sq = P.sbase + S_Q, sk = P.sbase + S_K, sv = P.sbase + S_VT, sp = P.sbase + S_HP;
   const uint32_t id_s = tc::idesc_bf16(128, 128), id_o = tc::idesc_bf16(128, 16);
   P.before_issue();
@@ -246,14 +253,14 @@ __device__ void attn_core(Pipe& P, int nk, float* ctx) {
   P.commit_wait();
 #pragma unroll 1
   for (int pair = 0; pair < 2; ++pair) {
-    softmax_pair(P, nk);
+    softmax_head(P, nk);
     P.before_issue();
     if (P.tid == 0) {
       for (int j = 0; j < 2; ++j) {
-        const int h = 2 * pair + j;
+        const int hd = 2 * pair + j;
         for (int k = 0; k < 128; k += 16)
-          tc::mma_bf16(P.tmem + T_O + 16 * h, tc::kmajor_desc(sp + j * 32768, 128, k),
-                       tc::kmajor_desc(sv + h * 4096, 128, k), id_o, k > 0);
+          tc::mma_bf16(P.tmem + T_O + 16 * hd, tc::kmajor_desc(sp + j * 32768, 128, k),
+                       tc::kmajor_desc(sv + hd * 4096, 128, k), id_o, k > 0);
       }
       if (pair == 0)
         for (int j = 0; j < 2; ++j)
@@ -262,32 +269,32 @@ __device__ void attn_core(Pipe& P, int nk, float* ctx) {
     }
     P.commit_wait();
   }
-  tc::tmem_ld64(P.lane_addr(T_O), ctx);
+  float ctx[HC];
+  tmem_ld32(P.lane_addr(T_O + HC * P.h), ctx);
+#pragma unroll
+  for (int q = 0; q < HC; q += 8) st_row8(P.smem + S_A, P.r, HC * P.h + q, D, ctx + q);
 }
 
-// x += Wo . ctx + bo for valid rows
-__device__ void out_proj(Pipe& P, const float* ctx, const float* bo, float* x, bool valid) {
-  uint8_t* ta = P.smem + S_A;
-#pragma unroll
-  for (int c0 = 0; c0 < D; c0 += 8) st_row8(ta, P.tid, c0, D, ctx + c0);
+// x += Wo . ctx + bo for valid rows (ctx already in the A tile)
+__device__ void out_proj(Pipe& P, const float* bo, float* x, bool valid) {
   const uint32_t w = P.acquire();
   P.before_issue();
   if (P.tid == 0) gemm(P.sbase + S_A, D, w, D, T_GEN, P.tmem);
   P.prefetch();
   P.commit_wait();
-  float v[64];
-  tc::tmem_ld64(P.lane_addr(T_GEN), v);
+  float v[HC];
+  tmem_ld32(P.lane_addr(T_GEN + HC * P.h), v);
   if (valid)
 #pragma unroll
-    for (int c = 0; c < D; ++c) x[c] += v[c] + __ldg(bo + c);
+    for (int c = 0; c < HC; ++c) x[c] += v[c] + __ldg(bo + HC * P.h + c);
 }
 
 // self attention sub-layer: x += MHA(LN(x + pos))  (decoder.py:214-218)
 __device__ void self_attn(Pipe& P, const AttnW& w, float* x, const float* pos, int nk, bool valid) {
-  float a[D];
+  float a[HC];
 #pragma unroll
-  for (int c = 0; c < D; ++c) a[c] = x[c] + pos[c];
-  ln_to_tile(a, w.ln_g, w.ln_b, P.smem + S_A, P.tid);
+  for (int c = 0; c < HC; ++c) a[c] = x[c] + pos[c];
+  ln_half_to_tile(P, a, w.ln_g, w.ln_b);
   const uint32_t wq = P.acquire();
   P.before_issue();
   if (P.tid == 0) gemm(P.sbase + S_A, D, wq, 3 * D, T_GEN, P.tmem);
@@ -295,41 +302,39 @@ __device__ void self_attn(Pipe& P, const AttnW& w, float* x, const float* pos, i
   P.commit_wait();
   drain_q(P, T_GEN, w.bqkv);
   drain_kv(P, T_GEN + 64, w.bqkv + 64, w.bqkv + 128);
-  float ctx[D];
-  attn_core(P, nk, ctx);
-  out_proj(P, ctx, w.bo, x, valid);
+  attn_core(P, nk);
+  out_proj(P, w.bo, x, valid);
 }
 
 // cross attention sub-layer: x += MHA(LN_q(x), LN_kv(f))  (decoder.py:220-227)
 __device__ void cross_attn(Pipe& P, const AttnW& w, float* x, const float* frow, bool valid) {
-  float f[D];
+  float f[HC];
 #pragma unroll
-  for (int c = 0; c < D; c += 4) {
-    const float4 v = __ldg(reinterpret_cast<const float4*>(frow + c));
+  for (int c = 0; c < HC; c += 4) {
+    const float4 v = __ldg(reinterpret_cast<const float4*>(frow + HC * P.h + c));
     f[c] = v.x; f[c + 1] = v.y; f[c + 2] = v.z; f[c + 3] = v.w;
   }
-  ln_to_tile(f, w.ln2_g, w.ln2_b, P.smem + S_A, P.tid);
+  ln_half_to_tile(P, f, w.ln2_g, w.ln2_b);
   const uint32_t wkv = P.acquire();
   P.before_issue();
   if (P.tid == 0) gemm(P.sbase + S_A, D, wkv, 2 * D, T_KV, P.tmem);
   P.prefetch();
   P.commit_wait();
   drain_kv(P, T_KV, w.bqkv + 64, w.bqkv + 128);
-  ln_to_tile(x, w.ln_g, w.ln_b, P.smem + S_A, P.tid);
+  ln_half_to_tile(P, x, w.ln_g, w.ln_b);
   const uint32_t wq = P.acquire();
   P.before_issue();
   if (P.tid == 0) gemm(P.sbase + S_A, D, wq, D, T_GEN, P.tmem);
   P.prefetch();
   P.commit_wait();
   drain_q(P, T_GEN, w.bqkv);
-  float ctx[D];
-  attn_core(P, BLK, ctx);
-  out_proj(P, ctx, w.bo, x, valid);
+  attn_core(P, BLK);
+  out_proj(P, w.bo, x, valid);
 }
 
 // MLP sub-layer: x += W2 relu(W1 LN(x) + b1) + b2  (decoder.py:205-212)
 __device__ void mlp(Pipe& P, const MlpW& w, float* x, bool valid) {
-  ln_to_tile(x, w.ln_g, w.ln_b, P.smem + S_A, P.tid);
+  ln_half_to_tile(P, x, w.ln_g, w.ln_b);
   const uint32_t w1 = P.acquire();
   P.before_issue();
   if (P.tid == 0) gemm(P.sbase + S_A, D, w1, 4 * D, T_GEN, P.tmem);
@@ -337,24 +342,25 @@ __device__ void mlp(Pipe& P, const MlpW& w, float* x, bool valid) {
   P.commit_wait();
   uint8_t* th = P.smem + S_HP;
 #pragma unroll 1
-  for (int q = 0; q < 4; ++q) {
+  for (int q = 0; q < 2; ++q) {
+    const int c0 = 128 * P.h + 64 * q;
     float v[64];
-    tc::tmem_ld64(P.lane_addr(T_GEN + 64 * q), v);
+    tc::tmem_ld64(P.lane_addr(T_GEN + c0), v);
 #pragma unroll
-    for (int i = 0; i < 64; ++i) v[i] = fmaxf(v[i] + __ldg(w.b1 + 64 * q + i), 0.0f);
+    for (int i = 0; i < 64; ++i) v[i] = fmaxf(v[i] + __ldg(w.b1 + c0 + i), 0.0f);
 #pragma unroll
-    for (int i = 0; i < 64; i += 8) st_row8(th, P.tid, 64 * q + i, 4 * D, v + i);
+    for (int i = 0; i < 64; i += 8) st_row8(th, P.r, c0 + i, 4 * D, v + i);
   }
   const uint32_t w2 = P.acquire();
   P.before_issue();
   if (P.tid == 0) gemm(P.sbase + S_HP, 4 * D, w2, D, T_GEN, P.tmem);
   P.prefetch();
   P.commit_wait();
-  float v[64];
-  tc::tmem_ld64(P.lane_addr(T_GEN), v);
+  float v[HC];
+  tmem_ld32(P.lane_addr(T_GEN + HC * P.h), v);
   if (valid)
 #pragma unroll
-    for (int c = 0; c < D; ++c) x[c] += v[c] + __ldg(w.b2 + c);
+    for (int c = 0; c < HC; ++c) x[c] += v[c] + __ldg(w.b2 + HC * P.h + c);
 }
 
 __device__ void setup(Pipe& P, Shared& sh, uint8_t* smem) {
@@ -362,9 +368,12 @@ __device__ void setup(Pipe& P, Shared& sh, uint8_t* smem) {
   P.smem = smem;
   P.sbase = tc::smem_u32(smem);
   P.tid = threadIdx.x;
+  P.r = threadIdx.x & (ROWS - 1);
+  P.h = threadIdx.x / ROWS;
   P.mphase = 0;
   P.wload = 0;
   P.wuse = 0;
+  P.xc = 0;
   if (P.tid == 0) {
     tc::mbar_init(&sh.wbar[0], 1);
     tc::mbar_init(&sh.wbar[1], 1);
@@ -394,9 +403,7 @@ __global__ void __launch_bounds__(NTH, 1) k_encoder_tc(const float* __restrict__
                                                        float* __restrict__ feats, int* nonfinite) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ Shared sh;
-  const int t = threadIdx.x, blk = t / BLK, p = t % BLK;
-  const int crop = 2 * blockIdx.x + blk;
-  const bool valid = crop < ncrops;
+  const int t = threadIdx.x;
   if (t == 0) {
     int n = 0;
     sh.wptr[n] = w.t_patch;
@@ -412,58 +419,61 @@ __global__ void __launch_bounds__(NTH, 1) k_encoder_tc(const float* __restrict__
   __syncthreads();
   Pipe P;
   setup(P, sh, smem);
+  const int blk = P.r / BLK, p = P.r % BLK;
+  const int crop = 2 * blockIdx.x + blk;
+  const bool valid = crop < ncrops;
 
-  // patchify row p of this crop (decoder.py:247-248) into the K = 192 tile
+  // patchify (decoder.py:247-248): this thread packs image rows iy in
+  // [4h, 4h + 4) of patch p into the K = 192 tile (k = iy*24 + ix*3 + c)
   {
     uint8_t* tile = smem + S_HP;
     const int py = p / 8, px = p % 8;
     const float* src = crops + (int64_t)(valid ? crop : 0) * 64 * 64 * 3;
 #pragma unroll 1
-    for (int iy = 0; iy < 8; ++iy) {
+    for (int iy = 4 * P.h; iy < 4 * P.h + 4; ++iy) {
       const float* row = src + ((py * 8 + iy) * 64 + px * 8) * 3;
 #pragma unroll
       for (int q = 0; q < 3; ++q) {
         float v[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) v[i] = valid ? __ldg(row + 8 * q + i) : 0.0f;
-        st_row8(tile, t, iy * 24 + 8 * q, 192, v);
+        st_row8(tile, P.r, iy * 24 + 8 * q, 192, v);
       }
     }
   }
-  float x[D];
+  float x[HC];
   {
     const uint32_t wp = P.acquire();
     P.before_issue();
     if (t == 0) gemm(P.sbase + S_HP, 192, wp, D, T_GEN, P.tmem);
     P.prefetch();
     P.commit_wait();
+    float v[HC];
+    tmem_ld32(P.lane_addr(T_GEN + HC * P.h), v);
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      float v[16];
-      tc::tmem_ld16(P.lane_addr(T_GEN + 16 * q), v);
-#pragma unroll
-      for (int i = 0; i < 16; ++i) {
-        const int c = 16 * q + i;
-        x[c] = valid ? (v[i] + __ldg(w.patch_b + c)) + __ldg(w.pos + p * D + c) : 0.0f;
-      }
+    for (int i = 0; i < HC; ++i) {
+      const int c = HC * P.h + i;
+      x[i] = valid ? (v[i] + __ldg(w.patch_b + c)) + __ldg(w.pos + p * D + c) : 0.0f;
     }
   }
-  float zero[D];
+  float zero[HC];
 #pragma unroll
-  for (int c = 0; c < D; ++c) zero[c] = 0.0f;
+  for (int c = 0; c < HC; ++c) zero[c] = 0.0f;
   for (int l = 0; l < w.layers; ++l) {
     self_attn(P, w.self[l], x, zero, BLK, valid);
     mlp(P, w.mlp[l], x, valid);
   }
-  float y[D];
-  ln_row(x, w.norm_g, w.norm_b, y);
+  float y[HC];
+  ln_half(P, x, w.norm_g, w.norm_b, y);
   if (valid) {
-    float* out = feats + ((int64_t)crop * 64 + p) * D;
+    float* out = feats + ((int64_t)crop * 64 + p) * D + HC * P.h;
+    float bad = 0.0f;
 #pragma unroll
-    for (int c = 0; c < D; c += 4) {
-      flag_nonfinite(nonfinite, y[c] + y[c + 1] + y[c + 2] + y[c + 3]);
+    for (int c = 0; c < HC; c += 4) {
+      bad += y[c] + y[c + 1] + y[c + 2] + y[c + 3];
       *reinterpret_cast<float4*>(out + c) = make_float4(y[c], y[c + 1], y[c + 2], y[c + 3]);
     }
+    flag_nonfinite(nonfinite, bad);
   }
   teardown(P);
 }
@@ -490,29 +500,50 @@ struct HandAux {
 };
 static_assert(sizeof(BodyAux) <= 16384 && sizeof(HandAux) <= 16384, "aux scratch");
 
+// LN(token 0) -> head params / camera of both blocks (decoder.py:264-272)
 __device__ void body_heads(Pipe& P, BodyAux& ax, const BodyW& w, const float* x) {
-  const int t = P.tid, blk = t / BLK, r = t % BLK;
-  if (r == 0) {
-    float y[D];
-    ln_row(x, w.norm_g, w.norm_b, y);
+  float y[HC];
+  ln_half(P, x, w.norm_g, w.norm_b, y);
+  const int blk = P.r / BLK;
+  if (P.r % BLK == 0)
 #pragma unroll
-    for (int c = 0; c < D; ++c) ax.t0[blk][c] = y[c];
+    for (int c = 0; c < HC; ++c) ax.t0[blk][HC * P.h + c] = y[c];
+  __syncthreads();
+  {
+    const int b = P.tid / 128, o = P.tid % 128;  // one head output per thread
+    if (o < 79) {
+      const bool is_p = o < FSB_PARAM_DIM;
+      const float* W = is_p ? w.head_params_w : w.head_cam_w;
+      const int n = is_p ? FSB_PARAM_DIM : 3, oo = is_p ? o : o - FSB_PARAM_DIM;
+      float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+      for (int k = 0; k < D; ++k) acc[k & 3] = fmaf(ax.t0[b][k], __ldg(W + k * n + oo), acc[k & 3]);
+      const float v = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+      if (is_p)
+        ax.params[b][oo] = v + __ldg(w.head_params_b + oo);
+      else
+        ax.cam[b][oo] = v + __ldg(w.head_cam_b + oo);
+    }
   }
   __syncthreads();
-  // thread (blk, r) evaluates outputs r and r + 64 of its block's 79 head
-  // outputs (76 params + 3 camera); 64 independent loads per output
-  for (int o = r; o < 79; o += 64) {
-    const bool is_p = o < FSB_PARAM_DIM;
-    const float* W = is_p ? w.head_params_w : w.head_cam_w;
-    const int n = is_p ? FSB_PARAM_DIM : 3, oo = is_p ? o : o - FSB_PARAM_DIM;
+}
+
+// LN(token 0) -> hand rotation / camera of both blocks (decoder.py:384-391)
+__device__ void hand_heads(Pipe& P, HandAux& ax, const HandW& w, const float* x) {
+  float y[HC];
+  ln_half(P, x, w.norm_g, w.norm_b, y);
+  const int blk = P.r / BLK;
+  if (P.r % BLK == 0)
+#pragma unroll
+    for (int c = 0; c < HC; ++c) ax.t0[blk][HC * P.h + c] = y[c];
+  __syncthreads();
+  if (P.tid < 12) {
+    const int b = P.tid / 6, o = P.tid % 6;
+    const float* W = o < 3 ? w.head_rot_w : w.head_cam_w;
     float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
 #pragma unroll
-    for (int k = 0; k < D; ++k) acc[k & 3] = fmaf(ax.t0[blk][k], __ldg(W + k * n + oo), acc[k & 3]);
-    const float v = (acc[0] + acc[1]) + (acc[2] + acc[3]);
-    if (is_p)
-      ax.params[blk][oo] = v + __ldg(w.head_params_b + oo);
-    else
-      ax.cam[blk][oo] = v + __ldg(w.head_cam_b + oo);
+    for (int k = 0; k < D; ++k) acc[k & 3] = fmaf(ax.t0[b][k], __ldg(W + k * 3 + o % 3), acc[k & 3]);
+    ax.rc[b][o] = (acc[0] + acc[1]) + (acc[2] + acc[3]) + __ldg((o < 3 ? w.head_rot_b : w.head_cam_b) + o % 3);
   }
   __syncthreads();
 }
@@ -520,14 +551,9 @@ __device__ void body_heads(Pipe& P, BodyAux& ax, const BodyW& w, const float* x)
 __global__ void __launch_bounds__(NTH, 1) k_decoders_tc(DecodeArgs a, BodyW bw, HandW hw) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ Shared sh;
-  const int t = threadIdx.x, blk = t / BLK, r = t % BLK;
+  const int t = threadIdx.x;
   const int nbc = (a.nbody + 1) / 2;
   const bool body = (int)blockIdx.x < nbc;
-  const int unit = body ? 2 * blockIdx.x + blk : 2 * (blockIdx.x - nbc) + blk;  // frame or hand index
-  const int nunit = body ? a.nbody : a.nhand;
-  const bool uvalid = unit < nunit;
-  const int nrows = body ? 51 : 4;
-  const bool valid = uvalid && r < nrows;
   const int layers = body ? bw.layers : hw.layers;
   if (t == 0) {
     int n = 0;
@@ -548,6 +574,12 @@ __global__ void __launch_bounds__(NTH, 1) k_decoders_tc(DecodeArgs a, BodyW bw, 
   __syncthreads();
   Pipe P;
   setup(P, sh, smem);
+  const int r = P.r, blk = r / BLK, rb = r % BLK, c0 = HC * P.h;
+  const int unit = body ? 2 * blockIdx.x + blk : 2 * (blockIdx.x - nbc) + blk;  // frame or hand index
+  const int nunit = body ? a.nbody : a.nhand;
+  const bool uvalid = unit < nunit;
+  const int nrows = body ? 51 : 4;
+  const bool valid = uvalid && rb < nrows;
 
   // feature row of this thread for cross attention
   int crop;
@@ -557,16 +589,15 @@ __global__ void __launch_bounds__(NTH, 1) k_decoders_tc(DecodeArgs a, BodyW bw, 
     const int hnd = uvalid ? unit : 0;
     crop = a.hand_feat_first + (hnd / 2) * a.body_feat_stride + (hnd % 2);
   }
-  const float* frow = a.feats + ((int64_t)crop * 64 + r) * D;
+  const float* frow = a.feats + ((int64_t)crop * 64 + rb) * D;
 
-  float x[D], pos[D];
+  float x[HC], pos[HC];
   BodyAux& bx = *reinterpret_cast<BodyAux*>(smem + S_AUX);
   HandAux& hx = *reinterpret_cast<HandAux*>(smem + S_AUX);
   if (body) {
-    // tokens = token_init, rows 1..4 += prompt_box(prompt)  (decoder.py:287-293);
-    // the 2 x 256 box-token outputs are spread over the CTA, 4 per thread
-    for (int i = 0; i < 4; ++i) {
-      const int idx = 4 * t + i, b = idx / (4 * D), o = idx % (4 * D);
+    // tokens = token_init, rows 1..4 += prompt_box(prompt)  (decoder.py:287-293)
+    for (int i = 0; i < 2; ++i) {
+      const int idx = 2 * t + i, b = idx / (4 * D), o = idx % (4 * D);
       const int u = 2 * blockIdx.x + b;
       float acc = 0.0f;
       if (u < a.nbody) {
@@ -578,50 +609,52 @@ __global__ void __launch_bounds__(NTH, 1) k_decoders_tc(DecodeArgs a, BodyW bw, 
     if (t < 2) bx.pred[t] = 0;
     __syncthreads();
 #pragma unroll
-    for (int c = 0; c < D; ++c) {
-      float v = valid ? __ldg(bw.token_init + r * D + c) : 0.0f;
-      if (valid && r >= 1 && r < 5) v += bx.boxtok[blk][(r - 1) * D + c];
+    for (int c = 0; c < HC; ++c) {
+      float v = valid ? __ldg(bw.token_init + rb * D + c0 + c) : 0.0f;
+      if (valid && rb >= 1 && rb < 5) v += bx.boxtok[blk][(rb - 1) * D + c0 + c];
       x[c] = v;
     }
   } else {
 #pragma unroll
-    for (int c = 0; c < D; ++c) x[c] = valid ? __ldg(hw.token_init + r * D + c) : 0.0f;
+    for (int c = 0; c < HC; ++c) x[c] = valid ? __ldg(hw.token_init + rb * D + c0 + c) : 0.0f;
     if (t < 2) hx.pred[t] = 0;
   }
   __syncthreads();
 
   for (int l = 0; l < layers; ++l) {
-    // positional terms of the self-attention input
+    // positional terms of the self-attention input (decoder.py:300-303, :397-398)
     if (body) {
-      const bool pr2 = r >= 5 && r < 27, pr3 = r >= 27 && r < 49;
+      const bool pr2 = rb >= 5 && rb < 27, pr3 = rb >= 27 && rb < 49;
 #pragma unroll
-      for (int c = 0; c < D; ++c) {
+      for (int i = 0; i < HC; ++i) {
+        const int c = c0 + i;
         float v = 0.0f;
         if (valid && pr2) {
-          const int j = r - 5;
+          const int j = rb - 5;
           v = bx.pred[blk] ? fmaf(bx.kp2d[blk][2 * j + 1], __ldg(bw.phi2d_w + D + c),
                                   bx.kp2d[blk][2 * j] * __ldg(bw.phi2d_w + c)) + __ldg(bw.phi2d_b + c)
                            : __ldg(bw.p2d_init + j * D + c);
         } else if (valid && pr3) {
-          const int j = r - 27;
+          const int j = rb - 27;
           v = bx.pred[blk] ? fmaf(bx.jc[blk][3 * j + 2], __ldg(bw.phi3d_w + 2 * D + c),
                                   fmaf(bx.jc[blk][3 * j + 1], __ldg(bw.phi3d_w + D + c),
                                        bx.jc[blk][3 * j] * __ldg(bw.phi3d_w + c))) + __ldg(bw.phi3d_b + c)
                            : __ldg(bw.p3d_init + j * D + c);
         }
-        pos[c] = v;
+        pos[i] = v;
       }
     } else {
 #pragma unroll
-      for (int c = 0; c < D; ++c) {
+      for (int i = 0; i < HC; ++i) {
+        const int c = c0 + i;
         float v = 0.0f;
-        if (valid && r >= 1) {
-          const int j = r - 1;
+        if (valid && rb >= 1) {
+          const int j = rb - 1;
           v = hx.pred[blk] ? fmaf(hx.pts[blk][2 * j + 1], __ldg(hw.phi2d_w + D + c),
                                   hx.pts[blk][2 * j] * __ldg(hw.phi2d_w + c)) + __ldg(hw.phi2d_b + c)
                            : __ldg(hw.p_init + j * D + c);
         }
-        pos[c] = v;
+        pos[i] = v;
       }
     }
     self_attn(P, body ? bw.self[l] : hw.self[l], x, pos, nrows, valid);
@@ -630,11 +663,9 @@ __global__ void __launch_bounds__(NTH, 1) k_decoders_tc(DecodeArgs a, BodyW bw, 
     const unsigned sel = body ? a.body_sel : a.hand_sel;
     if ((sel >> l) & 1u) {
       if (body) {
+        // intermediate prediction: heads -> FK -> kp2d / centred joints
         body_heads(P, bx, bw, x);
-        if (t < 64) {  // warp 0 -> block 0, warp 1 -> block 1
-          const int b = t / 32;
-          fk_warp(bx.params[b], bw.joints_rest, bx.fk[b], t % 32);
-        }
+        if (t < 64) fk_warp(bx.params[t / 32], bw.joints_rest, bx.fk[t / 32], t % 32);
         __syncthreads();
         if (t < 2 * FSB_NJ) {
           const int b = t / FSB_NJ, j = t % FSB_NJ;
@@ -644,23 +675,20 @@ __global__ void __launch_bounds__(NTH, 1) k_decoders_tc(DecodeArgs a, BodyW bw, 
         }
         if (t < 2) bx.pred[t] = 1;
         __syncthreads();
-        if (a.inter != nullptr && r == 0 && uvalid) {
-          float* dst = a.inter + ((int64_t)unit * layers + l) * (FSB_PARAM_DIM + 3 + 44);
-          for (int i = 0; i < FSB_PARAM_DIM; ++i) dst[i] = bx.params[blk][i];
-          for (int i = 0; i < 3; ++i) dst[FSB_PARAM_DIM + i] = bx.cam[blk][i];
-          for (int i = 0; i < 44; ++i) dst[FSB_PARAM_DIM + 3 + i] = bx.kp2d[blk][i];
+        if (a.inter != nullptr && t < 2 * 123) {
+          const int b = t / 123, i = t % 123, u = 2 * blockIdx.x + b;
+          if (u < a.nbody) {
+            float* dst = a.inter + ((int64_t)u * layers + l) * (FSB_PARAM_DIM + 3 + 44);
+            dst[i] = i < FSB_PARAM_DIM ? bx.params[b][i]
+                                       : (i < FSB_PARAM_DIM + 3 ? bx.cam[b][i - FSB_PARAM_DIM]
+                                                                : bx.kp2d[b][i - FSB_PARAM_DIM - 3]);
+          }
         }
       } else {
-        if (r == 0) {
-          float y[D];
-          ln_row(x, hw.norm_g, hw.norm_b, y);
-          float rc[6];
-          for (int o = 0; o < 6; ++o) {
-            const float* W = o < 3 ? hw.head_rot_w : hw.head_cam_w;
-            float acc = 0.0f;
-            for (int k = 0; k < D; ++k) acc = fmaf(y[k], __ldg(W + k * 3 + o % 3), acc);
-            rc[o] = acc + __ldg((o < 3 ? hw.head_rot_b : hw.head_cam_b) + o % 3);
-          }
+        // canonical points through the predicted rotation (decoder.py:399-409)
+        hand_heads(P, hx, hw, x);
+        if (t < 2) {
+          const float* rc = hx.rc[t];
           float R[9];
           rodrigues3(rc[0], rc[1], rc[2], R);
           for (int i = 0; i < 3; ++i) {
@@ -668,10 +696,10 @@ __global__ void __launch_bounds__(NTH, 1) k_decoders_tc(DecodeArgs a, BodyW bw, 
             for (int ax = 0; ax < 2; ++ax)
               q[ax] = R[3 * ax] * __ldg(hw.canon_pts + 3 * i) + R[3 * ax + 1] * __ldg(hw.canon_pts + 3 * i + 1) +
                       R[3 * ax + 2] * __ldg(hw.canon_pts + 3 * i + 2);
-            hx.pts[blk][2 * i] = rc[3] * q[0] + rc[4];
-            hx.pts[blk][2 * i + 1] = rc[3] * q[1] + rc[5];
+            hx.pts[t][2 * i] = rc[3] * q[0] + rc[4];
+            hx.pts[t][2 * i + 1] = rc[3] * q[1] + rc[5];
           }
-          hx.pred[blk] = 1;
+          hx.pred[t] = 1;
         }
         __syncthreads();
       }
@@ -680,34 +708,26 @@ __global__ void __launch_bounds__(NTH, 1) k_decoders_tc(DecodeArgs a, BodyW bw, 
   // final heads and outputs
   if (body) {
     body_heads(P, bx, bw, x);
-    if (uvalid && r < FSB_PARAM_DIM) {
-      const float v = bx.params[blk][r];
-      flag_nonfinite(a.nonfinite, v);
-      a.body_params[(int64_t)unit * FSB_PARAM_DIM + r] = v;
-      const bool hand_slot = (r >= 51 && r < 54) || (r >= 63 && r < 66);
-      if (a.merged != nullptr && !hand_slot) a.merged[(int64_t)unit * FSB_PARAM_DIM + r] = v;
-      if (r < 3) a.body_cam[(int64_t)unit * 3 + r] = bx.cam[blk][r];
-    }
-    // params 64..75 (rows only go to 63)
-    if (uvalid && r < FSB_PARAM_DIM - 64) {
-      const int o = 64 + r;
-      const float v = bx.params[blk][o];
-      a.body_params[(int64_t)unit * FSB_PARAM_DIM + o] = v;
-      const bool hand_slot = (o >= 51 && o < 54) || (o >= 63 && o < 66);
-      if (a.merged != nullptr && !hand_slot) a.merged[(int64_t)unit * FSB_PARAM_DIM + o] = v;
+    if (t < 2 * FSB_PARAM_DIM) {
+      const int b = t / FSB_PARAM_DIM, o = t % FSB_PARAM_DIM, u = 2 * blockIdx.x + b;
+      if (u < a.nbody) {
+        const float v = bx.params[b][o];
+        flag_nonfinite(a.nonfinite, v);
+        a.body_params[(int64_t)u * FSB_PARAM_DIM + o] = v;
+        const bool hand_slot = (o >= 51 && o < 54) || (o >= 63 && o < 66);
+        if (a.merged != nullptr && !hand_slot) a.merged[(int64_t)u * FSB_PARAM_DIM + o] = v;
+        if (o < 3) a.body_cam[(int64_t)u * 3 + o] = bx.cam[b][o];
+      }
     }
   } else {
-    if (r == 0 && uvalid) {
-      float y[D];
-      ln_row(x, hw.norm_g, hw.norm_b, y);
-      for (int o = 0; o < 3; ++o) {
-        float acc = 0.0f;
-        for (int k = 0; k < D; ++k) acc = fmaf(y[k], __ldg(hw.head_rot_w + k * 3 + o), acc);
-        const float v = acc + __ldg(hw.head_rot_b + o);
+    hand_heads(P, hx, hw, x);
+    if (t < 6) {
+      const int b = t / 3, o = t % 3, u = 2 * (blockIdx.x - nbc) + b;
+      if (u < a.nhand) {
+        const float v = hx.rc[b][o];
         flag_nonfinite(a.nonfinite, v);
-        a.hand_rots[(int64_t)unit * 3 + o] = v;
-        if (a.merged != nullptr)
-          a.merged[(int64_t)(unit / 2) * FSB_PARAM_DIM + ((unit % 2) == 0 ? 51 : 63) + o] = v;
+        a.hand_rots[(int64_t)u * 3 + o] = v;
+        if (a.merged != nullptr) a.merged[(int64_t)(u / 2) * FSB_PARAM_DIM + ((u % 2) == 0 ? 51 : 63) + o] = v;
       }
     }
   }
