@@ -44,6 +44,10 @@ cudaError_t launch_bridge(const float* V, int B, int nv, const int32_t* corners,
 cudaError_t launch_render(const void* scenes, int B, int H, int W, float* out, cudaStream_t st);
 cudaError_t init_attrs_transformer();
 cudaError_t init_attrs_transformer_tc();
+cudaError_t init_attrs_mlp_tc();
+cudaError_t launch_tile_layer(const uint8_t* Aimg, const uint8_t* Bimg, int KT, int G, int M, int N, float* partial,
+                              const float* bias, const float* mask, int relu, float* out, int ldo, uint8_t* out_img,
+                              int KT_out, int* nonfinite, cudaStream_t st);
 cudaError_t launch_encoder_tc(const float* crops, int ncrops, const EncW& w, float* feats, int* nonfinite,
                               cudaStream_t st);
 cudaError_t launch_decoders_tc(const DecodeArgs& a, const BodyW& bw, const HandW& hw, cudaStream_t st);
@@ -121,7 +125,8 @@ struct fsb_ctx {
   float *w_prompt = nullptr, *w_crops = nullptr, *w_feats = nullptr, *w_params = nullptr, *w_cam = nullptr,
         *w_rots = nullptr, *w_rel = nullptr, *w_rel2 = nullptr, *w_x = nullptr, *w_h1 = nullptr, *w_h2 = nullptr,
         *w_theta = nullptr, *w_part = nullptr;
-  __nv_bfloat16* w_xb = nullptr;
+  __nv_bfloat16* w_xb = nullptr;  // projector input as a bf16 A-tile image
+  unsigned char *w_h1img = nullptr, *w_h2img = nullptr;
   // graphs
   bool graphs = true;
   struct GraphEntry {
@@ -191,7 +196,7 @@ int fsb_ctx_create(int device, fsb_ctx** out) {
   fsb_ctx* c = new fsb_ctx();
   c->device = device;
   if (init_attrs_transformer() != cudaSuccess || init_attrs_transformer_tc() != cudaSuccess ||
-      init_attrs_body() != cudaSuccess) {
+      init_attrs_mlp_tc() != cudaSuccess || init_attrs_body() != cudaSuccess) {
     delete c;
     return FSB_ERR_CUDA;
   }
@@ -241,7 +246,14 @@ int fsb_reserve(fsb_ctx* c, int max_frames) {
   const size_t o_rel = take(F * FSB_NJ * 12 * 4);
   const size_t o_rel2 = take(F * FSB_NJ * 12 * 4);
   const size_t o_x = take(F * 3 * nsub * 4);
-  const size_t o_xb = take(F * 3 * nsub * 2);
+  // bf16 A-tile images of the tensor-core projector (k_mlp_tc.cu)
+  const size_t mtiles = (F + 127) / 128;
+  const size_t ximg_bytes = mtiles * ((3 * (size_t)nsub + 127) / 128) * 32768;
+  const size_t h1img_bytes = mtiles * ((h1 + 127) / 128) * 32768;
+  const size_t h2img_bytes = mtiles * ((h2 + 127) / 128) * 32768;
+  const size_t o_xb = take(ximg_bytes);
+  const size_t o_h1i = take(h1img_bytes);
+  const size_t o_h2i = take(h2img_bytes);
   const size_t o_h1 = take(F * h1 * 4);
   const size_t o_h2 = take(F * h2 * 4);
   const size_t o_theta = take(F * 76 * 4);
@@ -250,6 +262,11 @@ int fsb_reserve(fsb_ctx* c, int max_frames) {
   c->drop_graphs();
   FSB_CUDA(c, c->ws.alloc(off));
   unsigned char* b = static_cast<unsigned char*>(c->ws.p);
+  // zero padding of the tile images (k columns past K, rows past B) must stay
+  // finite: clear once, kernels only ever write the live region
+  FSB_CUDA(c, cudaMemset(b + o_xb, 0, ximg_bytes + h1img_bytes + h2img_bytes + 2 * 256));
+  c->w_h1img = b + o_h1i;
+  c->w_h2img = b + o_h2i;
   c->w_boxes = reinterpret_cast<double*>(b + o_boxes);
   c->w_prompt = reinterpret_cast<float*>(b + o_prompt);
   c->w_crops = reinterpret_cast<float*>(b + o_crops);
@@ -538,12 +555,25 @@ int fsb_load_projector(fsb_ctx* c, int n_sub, int h1, int h2, const int64_t* cor
   const int K = 3 * n_sub;
   std::vector<int32_t> cr((size_t)n_sub * 3);
   for (size_t i = 0; i < cr.size(); ++i) cr[i] = (int32_t)corners[i];
-  // K-major bf16 copies (N x K) for the tensor-core GEMMs
-  std::vector<__nv_bfloat16> w1t((size_t)h1 * K), w2t((size_t)h2 * h1);
-  for (int k = 0; k < K; ++k)
-    for (int n = 0; n < h1; ++n) w1t[(size_t)n * K + k] = __float2bfloat16_rn(w1[(size_t)k * h1 + n]);
-  for (int k = 0; k < h1; ++k)
-    for (int n = 0; n < h2; ++n) w2t[(size_t)n * h1 + k] = __float2bfloat16_rn(w2[(size_t)k * h2 + n]);
+  // bf16 tile images of W^T (k_mlp_tc.cu): [n_tile][k_tile] 128 x 128
+  // K-major tiles, zero padded in both n and k
+  auto tile_image = [](const float* W, int Kin, int Nout) {
+    const int KT = (Kin + 127) / 128, NT = (Nout + 127) / 128;
+    std::vector<__nv_bfloat16> img((size_t)NT * KT * 128 * 128, __float2bfloat16_rn(0.0f));
+    for (int k = 0; k < Kin; ++k)
+      for (int n = 0; n < Nout; ++n) {
+        const size_t tile = (size_t)(n / 128) * KT + (k / 128);
+        img[tile * 16384 + tc_kmajor_off(n % 128, k % 128, 128) / 2] = __float2bfloat16_rn(W[(size_t)k * Nout + n]);
+      }
+    return img;
+  };
+  const bool tc_ok = h1 % 128 == 0 && h2 % 128 == 0;
+  std::vector<__nv_bfloat16> i1, i2, i3;
+  if (tc_ok) {
+    i1 = tile_image(w1, K, h1);
+    i2 = tile_image(w2, h1, h2);
+    i3 = tile_image(w3, h2, 76);
+  }
   Packer pk;
   const size_t o_c = pk.add(cr.data(), cr.size() * 4);
   const size_t o_bw = pk.add(bary, (size_t)n_sub * 12);
@@ -554,8 +584,9 @@ int fsb_load_projector(fsb_ctx* c, int n_sub, int h1, int h2, const int64_t* cor
   const size_t o_w3 = pk.add(w3, (size_t)h2 * 76 * 4);
   const size_t o_b3 = pk.add(b3, 76 * 4);
   const size_t o_m = pk.add(mask, 76 * 4);
-  const size_t o_w1t = pk.add(w1t.data(), w1t.size() * 2);
-  const size_t o_w2t = pk.add(w2t.data(), w2t.size() * 2);
+  const size_t o_i1 = pk.add(i1.data(), i1.size() * 2);
+  const size_t o_i2 = pk.add(i2.data(), i2.size() * 2);
+  const size_t o_i3 = pk.add(i3.data(), i3.size() * 2);
   FSB_CUDA(c, c->proj_mem.alloc(pk.host.size()));
   FSB_CUDA(c, cudaMemcpy(c->proj_mem.p, pk.host.data(), pk.host.size(), cudaMemcpyHostToDevice));
   const unsigned char* base = static_cast<const unsigned char*>(c->proj_mem.p);
@@ -572,8 +603,12 @@ int fsb_load_projector(fsb_ctx* c, int n_sub, int h1, int h2, const int64_t* cor
   p.w3 = reinterpret_cast<const float*>(base + o_w3);
   p.b3 = reinterpret_cast<const float*>(base + o_b3);
   p.mask = reinterpret_cast<const float*>(base + o_m);
-  p.w1t_bf16 = reinterpret_cast<const __nv_bfloat16*>(base + o_w1t);
-  p.w2t_bf16 = reinterpret_cast<const __nv_bfloat16*>(base + o_w2t);
+  p.img_w1 = tc_ok ? base + o_i1 : nullptr;
+  p.img_w2 = tc_ok ? base + o_i2 : nullptr;
+  p.img_w3 = tc_ok ? base + o_i3 : nullptr;
+  p.KT1 = (K + 127) / 128;
+  p.KT2 = (h1 + 127) / 128;
+  p.KT3 = (h2 + 127) / 128;
   c->has_proj = true;
   c->ws_frames = 0;
   return FSB_OK;
@@ -735,10 +770,27 @@ int fsb_skin(fsb_ctx* c, int which, const float* poses, int B, float* verts, voi
   return FSB_OK;
 }
 
+// K tiles per reduction group of the tensor-core projector layers; fixed, so
+// the K partition (and the bits of a mesh's output) never depend on B
+constexpr int kMlpGroup = 4;
+
+static bool mlp_tc(const fsb_ctx* c, int precision) { return precision == FSB_BF16 && c->proj.img_w1 != nullptr; }
+
 static int run_mlp(fsb_ctx* c, int B, float* theta, int precision, cudaStream_t st) {
   const ProjectorDev& p = c->proj;
-  // the projector MLP runs fp32 in both modes until its tcgen05 GEMM lands
-  (void)precision;
+  if (mlp_tc(c, precision)) {
+    // relu(x W1 + b1) -> relu(h1 W2 + b2) -> (h2 W3 + b3) * mask on tcgen05;
+    // each reduce writes the next layer's bf16 A-tile image
+    const uint8_t* ximg = reinterpret_cast<const uint8_t*>(c->w_xb);
+    FSB_CUDA(c, launch_tile_layer(ximg, p.img_w1, p.KT1, kMlpGroup, B, p.h1, c->w_part, p.b1, nullptr, 1, nullptr, 0,
+                                  c->w_h1img, p.KT2, nullptr, st));
+    FSB_CUDA(c, launch_tile_layer(c->w_h1img, p.img_w2, p.KT2, kMlpGroup, B, p.h2, c->w_part, p.b2, nullptr, 1,
+                                  nullptr, 0, c->w_h2img, p.KT3, nullptr, st));
+    FSB_CUDA(c, launch_tile_layer(c->w_h2img, p.img_w3, p.KT3, kMlpGroup, B, FSB_PARAM_DIM, c->w_part, p.b3, p.mask,
+                                  0, theta, FSB_PARAM_DIM, nullptr, 0, c->d_flag, st));
+    c->launches += 6;
+    return FSB_OK;
+  }
   FSB_CUDA(c, launch_gemm_f32(c->w_x, 3 * p.n_sub, p.w1, p.b1, nullptr, c->w_h1, p.h1, B, p.h1, 3 * p.n_sub, 1,
                               nullptr, c->w_part, st));
   FSB_CUDA(c, launch_gemm_f32(c->w_h1, p.h1, p.w2, p.b2, nullptr, c->w_h2, p.h2, B, p.h2, p.h1, 1, nullptr,
@@ -756,7 +808,9 @@ int fsb_project_vertices(fsb_ctx* c, const float* v_mhr, int B, int nv, float* t
   cudaStream_t st = (cudaStream_t)stream;
   int rc = ensure_ws(c, B, st);
   if (rc) return rc;
-  FSB_CUDA(c, launch_proj_inputs_v(v_mhr, nv, c->proj, B, c->w_x, nullptr, 3 * c->proj.n_sub, st));
+  const bool tc = mlp_tc(c, precision);
+  FSB_CUDA(c, launch_proj_inputs_v(v_mhr, nv, c->proj, B, tc ? nullptr : c->w_x, tc ? c->w_xb : nullptr,
+                                   3 * c->proj.n_sub, st));
   c->launches += B > 0;
   return run_mlp(c, B, theta, precision, st);
 }
@@ -768,8 +822,9 @@ static int skin_project_impl(fsb_ctx* c, const float* params, int B, float* v_mh
   const TemplateDev& mhr = c->tmpl[FSB_MHR];
   FSB_CUDA(c, launch_fk(params, FSB_PARAM_DIM, B, mhr.joints_rest, nullptr, c->w_rel, st));
   if (v_mhr) FSB_CUDA(c, launch_lbs(mhr, c->w_rel, params, FSB_PARAM_DIM, B, v_mhr, c->d_flag, st));
-  FSB_CUDA(c, launch_proj_inputs(mhr, c->proj, c->w_rel, params, FSB_PARAM_DIM, B, c->w_x, nullptr,
-                                 3 * c->proj.n_sub, st));
+  const bool tc = mlp_tc(c, precision);
+  FSB_CUDA(c, launch_proj_inputs(mhr, c->proj, c->w_rel, params, FSB_PARAM_DIM, B, tc ? nullptr : c->w_x,
+                                 tc ? c->w_xb : nullptr, 3 * c->proj.n_sub, st));
   c->launches += 2 + (v_mhr != nullptr);
   int rc = run_mlp(c, B, theta, precision, st);
   if (rc) return rc;

@@ -113,8 +113,12 @@ struct ProjectorDev {
   const float* w3;        // (h2, 76)
   const float* b3;
   const float* mask;      // (76)
-  const __nv_bfloat16* w1t_bf16;  // (h1, 3*n_sub) K-major copy for the tcgen05 path
-  const __nv_bfloat16* w2t_bf16;  // (h2, h1)
+  // bf16 tile images of W^T for the tensor-core MLP (k_mlp_tc.cu):
+  // [n_tile][k_tile] 128 x 128 K-major tiles, zero padded
+  const uint8_t* img_w1;  // (h1 / 128) x KT1, KT1 = ceil(3 * n_sub / 128)
+  const uint8_t* img_w2;  // (h2 / 128) x KT2, KT2 = h1 / 128
+  const uint8_t* img_w3;  // 1 x KT3 (76 rows used), KT3 = h2 / 128
+  int KT1, KT2, KT3;
 };
 
 // arguments of the fused decoder launch (k_transformer.cu)

@@ -12,6 +12,7 @@
 // across a group of meshes, so HBM traffic is the vertex stream itself.
 #include "fsb_common.cuh"
 #include "fsb_weights.h"
+#include "tc_sm100.cuh"
 
 // ---------------------------------------------------------------------------
 // FK: one warp per pose.  rel (B, 22, 3, 4) = [R_world | t_world - R_world g]
@@ -213,7 +214,11 @@ __device__ void proj_inputs_cta(const Src& src, const ProjectorDev& p, float* sm
     const float m = (i % 3 == 0) ? mx : ((i % 3 == 1) ? my : mz);
     const float v = sub[i] - m;
     if (x != nullptr) x[(int64_t)b * ldx + i] = v;
-    if (xb != nullptr) xb[(int64_t)b * ldx + i] = __float2bfloat16_rn(v);
+    if (xb != nullptr) {  // bf16 A-tile image of the tensor-core MLP (k_mlp_tc.cu)
+      const int KT = (3 * p.n_sub + 127) / 128;
+      const size_t tile = (size_t)(b >> 7) * KT + (i >> 7);
+      xb[tile * 16384 + tc::kmajor_off(b & 127, i & 127, 128) / 2] = __float2bfloat16_rn(v);
+    }
   }
 }
 

@@ -66,6 +66,26 @@ def test_decoders_bf16(setup, dec_weights, full_models):
     assert rel_err(rots2, orc.decode_hand(dec_weights, cfg, feats[1:3], (1, 3))) <= 5e-2
 
 
+def test_projector_bf16_tensor_cores(full_models, full_projector):
+    """tcgen05 split-K projector on given meshes: close to the fp32 oracle,
+    and a mesh alone gives the same bits as inside a batch of 130 (two
+    128-row tiles)."""
+    from paper_2603_15603_b200 import projection as pj
+
+    mhr, smpl, gt = full_models
+    rng = np.random.default_rng(11)
+    poses = np.zeros((130, 76), np.float32)
+    poses[:, :66] = rng.normal(0.0, 0.2, size=(130, 66))
+    poses[:, 66:] = rng.normal(0.0, 0.45, size=(130, 10))
+    v = orc.skin_batch(mhr, poses)
+    th = pj.project_batch(v, gt, full_projector, precision="bf16")
+    want = orc.project_batch(v, gt.corners, gt.weights, projector_dict(full_projector))
+    assert rel_err(th, want) <= 5e-2
+    assert np.all(th[:, 51:54] == 0.0) and np.all(th[:, 63:66] == 0.0)
+    one = pj.project_batch(v[129:130], gt, full_projector, precision="bf16")
+    assert np.array_equal(one[0], th[129])
+
+
 def test_frame_batch_bf16_mpjpe(setup, dec_weights, full_models, full_projector):
     from paper_2603_15603_b200 import decoder as dc
 
