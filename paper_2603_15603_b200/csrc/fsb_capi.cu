@@ -27,9 +27,10 @@ cudaError_t launch_fk(const float* poses, int ld_pose, int B, const float* grest
 cudaError_t launch_lbs(const TemplateDev& t, const float* rel, const float* poses, int ld_pose, int B, float* verts,
                        int* nonfinite, cudaStream_t st);
 cudaError_t launch_proj_inputs(const TemplateDev& t, const ProjectorDev& p, const float* rel, const float* poses,
-                               int ld_pose, int B, float* x, __nv_bfloat16* xb, int ldx, cudaStream_t st);
-cudaError_t launch_proj_inputs_v(const float* V, int nv, const ProjectorDev& p, int B, float* x, __nv_bfloat16* xb,
-                                 int ldx, cudaStream_t st);
+                               int ld_pose, int B, float* sub, bool f32, __nv_bfloat16* xb, float* psum,
+                               cudaStream_t st);
+cudaError_t launch_proj_inputs_v(const float* V, int nv, const ProjectorDev& p, int B, float* sub, bool f32,
+                                 __nv_bfloat16* xb, float* psum, cudaStream_t st);
 cudaError_t launch_gemm_f32(const float* A, int lda, const float* W, const float* bias, const float* mask, float* C,
                             int ldc, int M, int N, int K, int relu, int* nonfinite, float* partial,
                             cudaStream_t st);
@@ -124,7 +125,7 @@ struct fsb_ctx {
   double* w_boxes = nullptr;
   float *w_prompt = nullptr, *w_crops = nullptr, *w_feats = nullptr, *w_params = nullptr, *w_cam = nullptr,
         *w_rots = nullptr, *w_rel = nullptr, *w_rel2 = nullptr, *w_x = nullptr, *w_h1 = nullptr, *w_h2 = nullptr,
-        *w_theta = nullptr, *w_part = nullptr;
+        *w_theta = nullptr, *w_part = nullptr, *w_psum = nullptr;
   __nv_bfloat16* w_xb = nullptr;  // projector input as a bf16 A-tile image
   unsigned char *w_h1img = nullptr, *w_h2img = nullptr;
   // graphs
@@ -259,6 +260,7 @@ int fsb_reserve(fsb_ctx* c, int max_frames) {
   const size_t o_theta = take(F * 76 * 4);
   const int hmax = h1 > h2 ? (h1 > 76 ? h1 : 76) : (h2 > 76 ? h2 : 76);
   const size_t o_part = take(F * 16 * (size_t)hmax * 4);  // split-K partials (<= 16 chunks)
+  const size_t o_psum = take(F * 8 * 3 * 4);               // projector-input centroid partials
   c->drop_graphs();
   FSB_CUDA(c, c->ws.alloc(off));
   unsigned char* b = static_cast<unsigned char*>(c->ws.p);
@@ -282,6 +284,7 @@ int fsb_reserve(fsb_ctx* c, int max_frames) {
   c->w_h2 = reinterpret_cast<float*>(b + o_h2);
   c->w_theta = reinterpret_cast<float*>(b + o_theta);
   c->w_part = reinterpret_cast<float*>(b + o_part);
+  c->w_psum = reinterpret_cast<float*>(b + o_psum);
   c->ws_frames = max_frames;
   return FSB_OK;
 }
@@ -524,12 +527,26 @@ int fsb_load_template(fsb_ctx* c, int which, int nv, const float* v_rest, const 
       }
     }
   }
+  // vertex records for vectorised loads (fsb_weights.h)
+  const int RS = vertex_record_floats(NZ);
+  std::vector<float> rec((size_t)nv * RS, 0.0f);
+  for (int v = 0; v < nv; ++v) {
+    float* r = rec.data() + (size_t)v * RS;
+    for (int a = 0; a < 3; ++a) r[a] = v_rest[(size_t)v * 3 + a];
+    for (int k = 0; k < 30; ++k) r[4 + k] = shape_basis[(size_t)v * 30 + k];
+    for (int z = 0; z < NZ; ++z) {
+      r[34 + z] = sw[(size_t)v * NZ + z];
+      const int jid = sj[(size_t)v * NZ + z];
+      memcpy(&r[34 + NZ + z], &jid, 4);
+    }
+  }
   Packer pk;
   const size_t o_v = pk.add(v_rest, (size_t)nv * 12);
   const size_t o_s = pk.add(shape_basis, (size_t)nv * 30 * 4);
   const size_t o_j = pk.add(sj.data(), sj.size() * 2);
   const size_t o_w = pk.add(sw.data(), sw.size() * 4);
   const size_t o_g = pk.add(joints_rest, FSB_NJ * 12);
+  const size_t o_r = pk.add(rec.data(), rec.size() * 4);
   DevMem& m = c->tmpl_mem[which];
   FSB_CUDA(c, m.alloc(pk.host.size()));
   FSB_CUDA(c, cudaMemcpy(m.p, pk.host.data(), pk.host.size(), cudaMemcpyHostToDevice));
@@ -542,6 +559,7 @@ int fsb_load_template(fsb_ctx* c, int which, int nv, const float* v_rest, const 
   t.skin_j = reinterpret_cast<const int16_t*>(base + o_j);
   t.skin_w = reinterpret_cast<const float*>(base + o_w);
   t.joints_rest = reinterpret_cast<const float*>(base + o_g);
+  t.rec = reinterpret_cast<const float*>(base + o_r);
   c->has_tmpl[which] = true;
   if (which == FSB_SMPL) c->body.joints_rest = t.joints_rest;
   c->drop_graphs();
@@ -809,9 +827,8 @@ int fsb_project_vertices(fsb_ctx* c, const float* v_mhr, int B, int nv, float* t
   int rc = ensure_ws(c, B, st);
   if (rc) return rc;
   const bool tc = mlp_tc(c, precision);
-  FSB_CUDA(c, launch_proj_inputs_v(v_mhr, nv, c->proj, B, tc ? nullptr : c->w_x, tc ? c->w_xb : nullptr,
-                                   3 * c->proj.n_sub, st));
-  c->launches += B > 0;
+  FSB_CUDA(c, launch_proj_inputs_v(v_mhr, nv, c->proj, B, c->w_x, !tc, tc ? c->w_xb : nullptr, c->w_psum, st));
+  c->launches += 2 * (B > 0);
   return run_mlp(c, B, theta, precision, st);
 }
 
@@ -823,9 +840,9 @@ static int skin_project_impl(fsb_ctx* c, const float* params, int B, float* v_mh
   FSB_CUDA(c, launch_fk(params, FSB_PARAM_DIM, B, mhr.joints_rest, nullptr, c->w_rel, st));
   if (v_mhr) FSB_CUDA(c, launch_lbs(mhr, c->w_rel, params, FSB_PARAM_DIM, B, v_mhr, c->d_flag, st));
   const bool tc = mlp_tc(c, precision);
-  FSB_CUDA(c, launch_proj_inputs(mhr, c->proj, c->w_rel, params, FSB_PARAM_DIM, B, tc ? nullptr : c->w_x,
-                                 tc ? c->w_xb : nullptr, 3 * c->proj.n_sub, st));
-  c->launches += 2 + (v_mhr != nullptr);
+  FSB_CUDA(c, launch_proj_inputs(mhr, c->proj, c->w_rel, params, FSB_PARAM_DIM, B, c->w_x, !tc,
+                                 tc ? c->w_xb : nullptr, c->w_psum, st));
+  c->launches += 3 + (v_mhr != nullptr);
   int rc = run_mlp(c, B, theta, precision, st);
   if (rc) return rc;
   FSB_CUDA(c, launch_fk(theta, FSB_PARAM_DIM, B, c->tmpl[FSB_SMPL].joints_rest, j_smpl, v_smpl ? c->w_rel2 : nullptr,

@@ -89,10 +89,15 @@ struct HandW {
   MlpW mlp[8];
 };
 
+// floats per vertex record: rest xyz + pad, shape basis (3 x 10), nnz skin
+// weights, nnz joint ids (int bits), padded to a multiple of 4 (float4 loads)
+__host__ __device__ constexpr int vertex_record_floats(int nnz) { return (34 + 2 * nnz + 3) / 4 * 4; }
+
 // body template on device (LBS / FK)
 struct TemplateDev {
   int nv;
   int nnz;                   // padded skin nonzeros per vertex (2, 4 or 8)
+  const float* rec;          // (nv, vertex_record_floats(nnz)) packed vertex records
   const float* v_rest;       // (nv, 3)
   const float* shape_basis;  // (nv, 3, 10)
   const int16_t* skin_j;     // (nv, nnz) joint ids, ascending, padded with 0

@@ -54,16 +54,25 @@ struct VertexTmpl {
   float w[NZ];
   float vr[3];
   float sb[30];
+  // one vectorised read of the vertex record (fsb_weights.h: TemplateDev::rec)
   __device__ void load(const TemplateDev& t, int v) {
+    constexpr int RS = vertex_record_floats(NZ);
+    float f[RS];
+    const float4* src = reinterpret_cast<const float4*>(t.rec) + (int64_t)v * (RS / 4);
 #pragma unroll
-    for (int z = 0; z < NZ; ++z) {
-      j[z] = t.skin_j[(int64_t)v * NZ + z];
-      w[z] = t.skin_w[(int64_t)v * NZ + z];
+    for (int q = 0; q < RS / 4; ++q) {
+      const float4 x = __ldg(src + q);
+      f[4 * q] = x.x; f[4 * q + 1] = x.y; f[4 * q + 2] = x.z; f[4 * q + 3] = x.w;
     }
 #pragma unroll
-    for (int c = 0; c < 3; ++c) vr[c] = __ldg(t.v_rest + 3 * v + c);
+    for (int c = 0; c < 3; ++c) vr[c] = f[c];
 #pragma unroll
-    for (int k = 0; k < 30; ++k) sb[k] = __ldg(t.shape_basis + (int64_t)30 * v + k);
+    for (int k = 0; k < 30; ++k) sb[k] = f[4 + k];
+#pragma unroll
+    for (int z = 0; z < NZ; ++z) {
+      w[z] = f[34 + z];
+      j[z] = __float_as_int(f[34 + NZ + z]);
+    }
   }
   __device__ void apply(const float* A, const float* shp, float out[3]) const {
     float T[12];
@@ -145,7 +154,6 @@ __global__ void __launch_bounds__(kLbsThreads) k_lbs(TemplateDev t, const float*
 // L2-resident template instead of re-read from the V_mhr stream.
 // One CTA per mesh.
 // ---------------------------------------------------------------------------
-constexpr int kProjThreads = 512;
 
 template <int NZ>
 __device__ __forceinline__ void skin_one(const TemplateDev& t, int v, const float* A, const float* shp, float o[3]) {
@@ -170,18 +178,24 @@ struct VertexSource {
   }
 };
 
+// The targets of one mesh are spread over kProjChunks CTAs (one target per
+// thread); each CTA writes its bridged, vertex-0-centred targets and its
+// partial sum, and k_proj_center removes the centroid (partials added in
+// chunk order, so the result does not depend on the batch).
+constexpr int kProjChunks = 8;
+
 template <class Src>
-__device__ void proj_inputs_cta(const Src& src, const ProjectorDev& p, float* sm, int b, float* __restrict__ x,
-                                __nv_bfloat16* __restrict__ xb, int ldx) {
-  float* v0 = sm + 276;        // 3
-  float* red = sm + 280;       // 3 * 16 warps + 3
-  float* sub = sm + 336;       // n_sub * 3
+__device__ void proj_inputs_cta(const Src& src, const ProjectorDev& p, float* sm, int b, int chunk,
+                                float* __restrict__ sub, float* __restrict__ psum) {
+  float* v0 = sm + 276;   // 3
+  float* red = sm + 280;  // 3 x warps
   const int tid = threadIdx.x;
+  const int per = (p.n_sub + kProjChunks - 1) / kProjChunks;
+  const int i = chunk * per + tid;
   if (tid == 0) src.get(0, v0);
   __syncthreads();
-  float s[3] = {0.0f, 0.0f, 0.0f};
-  for (int i = tid; i < p.n_sub; i += kProjThreads) {
-    float acc[3] = {0.0f, 0.0f, 0.0f};
+  float acc[3] = {0.0f, 0.0f, 0.0f};
+  if (tid < per && i < p.n_sub) {
 #pragma unroll
     for (int c = 0; c < 3; ++c) {
       float o[3];
@@ -191,59 +205,61 @@ __device__ void proj_inputs_cta(const Src& src, const ProjectorDev& p, float* sm
       for (int a = 0; a < 3; ++a) acc[a] = fmaf(wc, o[a] - v0[a], acc[a]);
     }
 #pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      sub[3 * i + a] = acc[a];
-      s[a] += acc[a];
-    }
+    for (int a = 0; a < 3; ++a) sub[((int64_t)b * p.n_sub + i) * 3 + a] = acc[a];
   }
   const int warp = tid / 32, lane = tid % 32;
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
-    const float r = warp_sum(s[a]);
+    const float r = warp_sum(acc[a]);
     if (lane == 0) red[3 * warp + a] = r;
   }
   __syncthreads();
   if (tid < 3) {
     float tot = 0.0f;
-    for (int w = 0; w < kProjThreads / 32; ++w) tot += red[3 * w + tid];
-    red[52 + tid] = tot / (float)p.n_sub;
+    for (int w = 0; w < (int)blockDim.x / 32; ++w) tot += red[3 * w + tid];
+    psum[((int64_t)b * kProjChunks + chunk) * 3 + tid] = tot;
   }
-  __syncthreads();
-  const float mx = red[52], my = red[53], mz = red[54];
-  for (int i = tid; i < 3 * p.n_sub; i += kProjThreads) {
-    const float m = (i % 3 == 0) ? mx : ((i % 3 == 1) ? my : mz);
-    const float v = sub[i] - m;
-    if (x != nullptr) x[(int64_t)b * ldx + i] = v;
-    if (xb != nullptr) {  // bf16 A-tile image of the tensor-core MLP (k_mlp_tc.cu)
-      const int KT = (3 * p.n_sub + 127) / 128;
-      const size_t tile = (size_t)(b >> 7) * KT + (i >> 7);
-      xb[tile * 16384 + tc::kmajor_off(b & 127, i & 127, 128) / 2] = __float2bfloat16_rn(v);
-    }
+}
+
+// x = sub - centroid (projection.py:464), as fp32 (in place) and/or as the
+// bf16 A-tile image of the tensor-core MLP (k_mlp_tc.cu)
+__global__ void k_proj_center(float* __restrict__ sub, const float* __restrict__ psum, int B, int n_sub,
+                              int write_f32, __nv_bfloat16* __restrict__ xb) {
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int K = 3 * n_sub;
+  if (idx >= (int64_t)B * K) return;
+  const int b = (int)(idx / K), i = (int)(idx % K), a = i % 3;
+  float s = 0.0f;
+#pragma unroll
+  for (int q = 0; q < kProjChunks; ++q) s += psum[((int64_t)b * kProjChunks + q) * 3 + a];
+  const float v = sub[idx] - s / (float)n_sub;
+  if (write_f32) sub[idx] = v;
+  if (xb != nullptr) {
+    const int KT = (K + 127) / 128;
+    const size_t tile = (size_t)(b >> 7) * KT + (i >> 7);
+    xb[tile * 16384 + tc::kmajor_off(b & 127, i & 127, 128) / 2] = __float2bfloat16_rn(v);
   }
 }
 
 template <int NZ>
-__global__ void __launch_bounds__(kProjThreads) k_proj_inputs(TemplateDev t, ProjectorDev p,
-                                                              const float* __restrict__ rel,
-                                                              const float* __restrict__ poses, int ld_pose,
-                                                              float* __restrict__ x, __nv_bfloat16* __restrict__ xb,
-                                                              int ldx) {
-  extern __shared__ __align__(16) float sm[];
-  float* A = sm;               // 264
-  float* shp = sm + 264;       // 10
+__global__ void __launch_bounds__(256) k_proj_inputs(TemplateDev t, ProjectorDev p, const float* __restrict__ rel,
+                                                     const float* __restrict__ poses, int ld_pose,
+                                                     float* __restrict__ sub, float* __restrict__ psum) {
+  __shared__ __align__(16) float sm[336];
+  float* A = sm;          // 264
+  float* shp = sm + 264;  // 10
   const int b = blockIdx.x, tid = threadIdx.x;
-  for (int i = tid; i < FSB_NJ * 12; i += kProjThreads) A[i] = rel[(int64_t)b * FSB_NJ * 12 + i];
+  for (int i = tid; i < FSB_NJ * 12; i += blockDim.x) A[i] = rel[(int64_t)b * FSB_NJ * 12 + i];
   if (tid < 10) shp[tid] = poses[(int64_t)b * ld_pose + 66 + tid];
   __syncthreads();
-  proj_inputs_cta(SkinSource<NZ>{t, A, shp}, p, sm, b, x, xb, ldx);
+  proj_inputs_cta(SkinSource<NZ>{t, A, shp}, p, sm, b, blockIdx.y, sub, psum);
 }
 
-__global__ void __launch_bounds__(kProjThreads) k_proj_inputs_v(const float* __restrict__ V, int nv, ProjectorDev p,
-                                                                float* __restrict__ x, __nv_bfloat16* __restrict__ xb,
-                                                                int ldx) {
-  extern __shared__ __align__(16) float sm[];
+__global__ void __launch_bounds__(256) k_proj_inputs_v(const float* __restrict__ V, int nv, ProjectorDev p,
+                                                       float* __restrict__ sub, float* __restrict__ psum) {
+  __shared__ __align__(16) float sm[336];
   const int b = blockIdx.x;
-  proj_inputs_cta(VertexSource{V + (int64_t)b * nv * 3}, p, sm, b, x, xb, ldx);
+  proj_inputs_cta(VertexSource{V + (int64_t)b * nv * 3}, p, sm, b, blockIdx.y, sub, psum);
 }
 
 // ---------------------------------------------------------------------------
@@ -351,39 +367,47 @@ cudaError_t launch_lbs(const TemplateDev& t, const float* rel, const float* pose
   return cudaGetLastError();
 }
 
-// proj-input kernels take up to 336 + 3 * n_sub floats of dynamic smem;
-// allow the full 227 KB so any subsample size that fits can launch
-cudaError_t init_attrs_body() {
-  const int mx = 227 * 1024;
-  cudaError_t e = cudaFuncSetAttribute(k_proj_inputs<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_proj_inputs<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_proj_inputs<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_proj_inputs_v, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-  return e;
+cudaError_t init_attrs_body() { return cudaSuccess; }
+
+static inline int proj_threads(const ProjectorDev& p) {
+  const int per = (p.n_sub + kProjChunks - 1) / kProjChunks;
+  return (per + 31) / 32 * 32;
 }
 
+static cudaError_t launch_proj_center(const ProjectorDev& p, int B, float* sub, const float* psum, bool f32,
+                                      __nv_bfloat16* xb, cudaStream_t st) {
+  const int64_t tot = (int64_t)B * 3 * p.n_sub;
+  k_proj_center<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(sub, psum, B, p.n_sub, f32 ? 1 : 0, xb);
+  return cudaGetLastError();
+}
+
+// sub: (B, n_sub, 3) fp32 scratch that receives x when f32 is set;
+// xb: the bf16 A-tile image (or null)
 cudaError_t launch_proj_inputs(const TemplateDev& t, const ProjectorDev& p, const float* rel, const float* poses,
-                               int ld_pose, int B, float* x, __nv_bfloat16* xb, int ldx, cudaStream_t st) {
+                               int ld_pose, int B, float* sub, bool f32, __nv_bfloat16* xb, float* psum,
+                               cudaStream_t st) {
   if (B == 0) return cudaSuccess;
-  const size_t smem = (336 + 3 * (size_t)p.n_sub) * sizeof(float);
+  const int nt = proj_threads(p);
+  if (nt > 1024) return cudaErrorInvalidValue;
+  const dim3 grid(B, kProjChunks);
   switch (t.nnz) {
-#define FSB_PI(NZ)                                                                                   \
-  case NZ:                                                                                           \
-    k_proj_inputs<NZ><<<B, kProjThreads, smem, st>>>(t, p, rel, poses, ld_pose, x, xb, ldx);         \
-    break;
-    FSB_PI(2) FSB_PI(4) FSB_PI(8)
-#undef FSB_PI
+    case 2: k_proj_inputs<2><<<grid, nt, 0, st>>>(t, p, rel, poses, ld_pose, sub, psum); break;
+    case 4: k_proj_inputs<4><<<grid, nt, 0, st>>>(t, p, rel, poses, ld_pose, sub, psum); break;
+    case 8: k_proj_inputs<8><<<grid, nt, 0, st>>>(t, p, rel, poses, ld_pose, sub, psum); break;
     default: return cudaErrorInvalidValue;
   }
-  return cudaGetLastError();
+  cudaError_t e = cudaGetLastError();
+  return e != cudaSuccess ? e : launch_proj_center(p, B, sub, psum, f32, xb, st);
 }
 
-cudaError_t launch_proj_inputs_v(const float* V, int nv, const ProjectorDev& p, int B, float* x, __nv_bfloat16* xb,
-                                 int ldx, cudaStream_t st) {
+cudaError_t launch_proj_inputs_v(const float* V, int nv, const ProjectorDev& p, int B, float* sub, bool f32,
+                                 __nv_bfloat16* xb, float* psum, cudaStream_t st) {
   if (B == 0) return cudaSuccess;
-  const size_t smem = (336 + 3 * (size_t)p.n_sub) * sizeof(float);
-  k_proj_inputs_v<<<B, kProjThreads, smem, st>>>(V, nv, p, x, xb, ldx);
-  return cudaGetLastError();
+  const int nt = proj_threads(p);
+  if (nt > 1024) return cudaErrorInvalidValue;
+  k_proj_inputs_v<<<dim3(B, kProjChunks), nt, 0, st>>>(V, nv, p, sub, psum);
+  cudaError_t e = cudaGetLastError();
+  return e != cudaSuccess ? e : launch_proj_center(p, B, sub, psum, f32, xb, st);
 }
 
 // number of K chunks of a layer: a function of K only (batch independence);
