@@ -26,6 +26,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
          "-Xptxas", "-warn-spills", "-I", os.path.join(ROOT, "include")]
+if os.environ.get("FSB_PROFILE"):  # cycle-attribution counters in the tcgen05 kernels
+    FLAGS.append("-DFSB_PROFILE")
 
 
 def _sources():

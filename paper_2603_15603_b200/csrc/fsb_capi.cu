@@ -406,6 +406,46 @@ int fsb_load_decoder(fsb_ctx* c, const fsb_decoder_config* cfg, int n, const cha
   ok = ok && put("hand.head_rot.w", (int64_t)Dm * 3) && put("hand.head_rot.b", 3) &&
        put("hand.head_cam.w", (int64_t)Dm * 3) && put("hand.head_cam.b", 3) && put("hand.phi2d.w", 2 * Dm) &&
        put("hand.phi2d.b", Dm) && put("hand.canon_pts", 9);
+  // per-layer TCP_* parameter blocks of the tensor-core kernels (fsb_weights.h)
+  auto put_params = [&](const std::string& key, const std::string& ps, const std::string& pc,
+                        const std::string& pm) -> bool {
+    std::vector<float> blk(TCP_FLOATS, 0.0f);
+    auto cp = [&](const std::string& name, int at, int n) -> bool {
+      auto it = tab.find(name);
+      if (it == tab.end() || it->second.second != n) {
+        missing = name + " (param block)";
+        return false;
+      }
+      memcpy(blk.data() + at, it->second.first, (size_t)n * 4);
+      return true;
+    };
+    bool good = cp(ps + ".ln_g", TCP_S_LN_G, Dm) && cp(ps + ".ln_b", TCP_S_LN_B, Dm) &&
+                cp(ps + ".bq", TCP_S_BQKV, Dm) && cp(ps + ".bk", TCP_S_BQKV + Dm, Dm) &&
+                cp(ps + ".bv", TCP_S_BQKV + 2 * Dm, Dm) && cp(ps + ".bo", TCP_S_BO, Dm) &&
+                cp(pm + ".ln_g", TCP_M_LN_G, Dm) && cp(pm + ".ln_b", TCP_M_LN_B, Dm) &&
+                cp(pm + ".b1", TCP_M_B1, 4 * Dm) && cp(pm + ".b2", TCP_M_B2, Dm);
+    if (good && !pc.empty())
+      good = cp(pc + ".lnq_g", TCP_C_LNQ_G, Dm) && cp(pc + ".lnq_b", TCP_C_LNQ_B, Dm) &&
+             cp(pc + ".lnkv_g", TCP_C_LNKV_G, Dm) && cp(pc + ".lnkv_b", TCP_C_LNKV_B, Dm) &&
+             cp(pc + ".bq", TCP_C_BQKV, Dm) && cp(pc + ".bk", TCP_C_BQKV + Dm, Dm) &&
+             cp(pc + ".bv", TCP_C_BQKV + 2 * Dm, Dm) && cp(pc + ".bo", TCP_C_BO, Dm);
+    if (good) off[key] = pk.add(blk.data(), blk.size() * 4);
+    return good;
+  };
+  if (ok && Dm == 64) {
+    for (int l = 0; ok && l < cfg->enc_layers; ++l) {
+      const std::string p = "enc.l" + std::to_string(l);
+      ok = put_params(p + ".tcp", p + ".self", "", p + ".mlp");
+    }
+    for (int l = 0; ok && l < cfg->body_layers; ++l) {
+      const std::string p = "body.l" + std::to_string(l);
+      ok = put_params(p + ".tcp", p + ".self", p + ".cross", p + ".mlp");
+    }
+    for (int l = 0; ok && l < cfg->hand_layers; ++l) {
+      const std::string p = "hand.l" + std::to_string(l);
+      ok = put_params(p + ".tcp", p + ".self", p + ".cross", p + ".mlp");
+    }
+  }
   if (!ok) return fail(c, FSB_ERR_SHAPE, "decoder weight table: missing or mis-sized '%s'", missing.c_str());
   FSB_CUDA(c, c->dec_mem.alloc(pk.host.size()));
   FSB_CUDA(c, cudaMemcpy(c->dec_mem.p, pk.host.data(), pk.host.size(), cudaMemcpyHostToDevice));
@@ -444,9 +484,11 @@ int fsb_load_decoder(fsb_ctx* c, const fsb_decoder_config* cfg, int n, const cha
   e.norm_g = P("enc.norm_g");
   e.norm_b = P("enc.norm_b");
   e.layers = cfg->enc_layers;
+  auto PT = [&](const std::string& name) { return off.count(name) ? P(name) : nullptr; };
   for (int l = 0; l < cfg->enc_layers; ++l) {
     fill_attn(e.self[l], "enc.l" + std::to_string(l) + ".self", false);
     fill_mlp(e.mlp[l], "enc.l" + std::to_string(l) + ".mlp");
+    e.tc_params[l] = PT("enc.l" + std::to_string(l) + ".tcp");
   }
   BodyW& b = c->body;
   b.token_init = P("body.token_init");
@@ -470,6 +512,7 @@ int fsb_load_decoder(fsb_ctx* c, const fsb_decoder_config* cfg, int n, const cha
     fill_attn(b.self[l], p + ".self", false);
     fill_attn(b.cross[l], p + ".cross", true);
     fill_mlp(b.mlp[l], p + ".mlp");
+    b.tc_params[l] = PT(p + ".tcp");
   }
   HandW& h = c->hand;
   h.token_init = P("hand.token_init");
@@ -489,6 +532,7 @@ int fsb_load_decoder(fsb_ctx* c, const fsb_decoder_config* cfg, int n, const cha
     fill_attn(h.self[l], p + ".self", false);
     fill_attn(h.cross[l], p + ".cross", true);
     fill_mlp(h.mlp[l], p + ".mlp");
+    h.tc_params[l] = PT(p + ".tcp");
   }
   // the body decoder's FK uses the decoder template's rest joints; the
   // body template upload patches it in (fsb_load_template)

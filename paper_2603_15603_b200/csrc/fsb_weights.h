@@ -9,6 +9,28 @@
 
 #define FSB_MAX_LAYERS 32
 
+// Per-layer block of the small fp32 parameters (LayerNorm affine, biases)
+// that the tensor-core kernels stage into shared memory with one bulk copy
+// per layer (offsets in floats, D = 64):
+//   self attention : ln_g, ln_b, bq|bk|bv, bo
+//   cross attention: lnq_g, lnq_b, lnkv_g, lnkv_b, bq|bk|bv, bo
+//   MLP            : ln_g, ln_b, b1 (4D), b2
+#define TCP_S_LN_G 0
+#define TCP_S_LN_B 64
+#define TCP_S_BQKV 128
+#define TCP_S_BO 320
+#define TCP_C_LNQ_G 384
+#define TCP_C_LNQ_B 448
+#define TCP_C_LNKV_G 512
+#define TCP_C_LNKV_B 576
+#define TCP_C_BQKV 640
+#define TCP_C_BO 832
+#define TCP_M_LN_G 896
+#define TCP_M_LN_B 960
+#define TCP_M_B1 1024
+#define TCP_M_B2 1280
+#define TCP_FLOATS 1344
+
 struct AttnW {
   const float* ln_g;   // self: ln; cross: lnq
   const float* ln_b;
@@ -46,6 +68,7 @@ struct EncW {
   int layers;
   AttnW self[FSB_MAX_LAYERS];
   MlpW mlp[FSB_MAX_LAYERS];
+  const float* tc_params[FSB_MAX_LAYERS];  // TCP_* blocks (cross part unused)
 };
 
 struct BodyW {
@@ -69,6 +92,7 @@ struct BodyW {
   AttnW self[8];
   AttnW cross[8];
   MlpW mlp[8];
+  const float* tc_params[8];  // TCP_* blocks
 };
 
 struct HandW {
@@ -87,6 +111,7 @@ struct HandW {
   AttnW self[8];
   AttnW cross[8];
   MlpW mlp[8];
+  const float* tc_params[8];  // TCP_* blocks
 };
 
 // floats per vertex record: rest xyz + pad, shape basis (3 x 10), nnz skin

@@ -34,7 +34,10 @@ constexpr uint32_t S_VT = 49152;    // 4 heads x (16 x 128) values^T          16
 constexpr uint32_t S_HP = 65536;    // MLP hidden 128x256 | P 2x(128x128) | patches 128x192   64 KB
 constexpr uint32_t S_W = 131072;    // 2 weight slots x 32 KB
 constexpr uint32_t S_AUX = 196608;  // fp32 role scratch                      16 KB
-constexpr uint32_t SMEM_TC = S_AUX + 16384;
+constexpr uint32_t S_PRM = S_AUX + 16384;  // 2 slots of the per-layer TCP_* parameter block
+constexpr uint32_t PRM_BYTES = TCP_FLOATS * 4;
+constexpr uint32_t SMEM_TC = S_PRM + 2 * PRM_BYTES;
+static_assert(SMEM_TC <= 227 * 1024, "shared memory budget");
 
 // TMEM columns
 constexpr uint32_t T_GEN = 0;   // GEMM accumulators / attention score pair
@@ -45,6 +48,7 @@ constexpr int kMaxW = 64;
 
 struct Shared {
   uint64_t wbar[2];
+  uint64_t pbar[2];
   uint64_t mbar;
   uint32_t tmem;
   int nw;
@@ -53,6 +57,18 @@ struct Shared {
   float xch[2][2 * ROWS];  // row-reduction exchange, double buffered
 };
 
+#ifdef FSB_PROFILE
+// cycle attribution of CTA 0 / thread 0 (build with FSB_PROFILE=1):
+// [0] total, [1] MMA waits, [2] weight waits, [3] issue barriers,
+// [4] row-exchange barriers
+__device__ unsigned long long g_tc_prof[2][2][8];  // [role][thread 0 | thread 255][counter]
+#define PROF_T0() const long long prof_t0_ = clock64()
+#define PROF_ADD(i) (prof[i] += clock64() - prof_t0_)
+#else
+#define PROF_T0()
+#define PROF_ADD(i)
+#endif
+
 // per-thread pipeline state (every thread tracks the same phases)
 struct Pipe {
   Shared* sh;
@@ -60,8 +76,28 @@ struct Pipe {
   uint32_t sbase;  // shared-space address of smem
   uint32_t tmem;
   uint32_t mphase;
-  int wload, wuse, xc;
+  int wload, wuse, xc, pload, puse;
   int tid, r, h;
+#ifdef FSB_PROFILE
+  long long prof[8];
+#endif
+
+  // per-layer parameter block ring (TCP_* layout): thread 0 issues, every
+  // thread waits on the slot it reads
+  __device__ void pprefetch(const float* src) {
+    if (tid == 0 && src != nullptr) {
+      const int slot = pload & 1;
+      tc::mbar_expect_tx(&sh->pbar[slot], PRM_BYTES);
+      tc::bulk_g2s(smem + S_PRM + slot * PRM_BYTES, src, PRM_BYTES, &sh->pbar[slot]);
+    }
+    ++pload;
+  }
+  __device__ const float* pacquire() {
+    const int slot = puse & 1;
+    tc::mbar_wait(&sh->pbar[slot], (uint32_t)((puse >> 1) & 1));
+    ++puse;
+    return reinterpret_cast<const float*>(smem + S_PRM + slot * PRM_BYTES);
+  }
 
   __device__ void prefetch() {  // next weight image into its ring slot
     if (wload < sh->nw) {
@@ -74,23 +110,29 @@ struct Pipe {
     }
   }
   __device__ uint32_t acquire() {  // wait for the next weight image; returns its address
+    PROF_T0();
     const int slot = wuse & 1;
     tc::mbar_wait(&sh->wbar[slot], (uint32_t)((wuse >> 1) & 1));
     ++wuse;
+    PROF_ADD(2);
     return sbase + S_W + slot * 32768u;
   }
   // operands written by threads -> visible to the tensor core; TMEM reads done
   __device__ void before_issue() {
+    PROF_T0();
     tc::fence_async_smem();
     tc::fence_before();
     __syncthreads();
     tc::fence_after();
+    PROF_ADD(3);
   }
   __device__ void commit_wait() {
+    PROF_T0();
     if (tid == 0) tc::mma_commit(&sh->mbar);
     tc::mbar_wait(&sh->mbar, mphase);
     mphase ^= 1u;
     tc::fence_after();
+    PROF_ADD(1);
   }
   __device__ uint32_t lane_addr(uint32_t col) const {
     return tmem + ((uint32_t)(((tid >> 5) & 3) * 32) << 16) + col;
@@ -100,7 +142,9 @@ struct Pipe {
     float* b = sh->xch[xc & 1];
     ++xc;
     b[h * ROWS + r] = part;
+    PROF_T0();
     __syncthreads();
+    PROF_ADD(4);
     return b[r] + b[ROWS + r];
   }
 };
@@ -152,7 +196,7 @@ __device__ __forceinline__ void ln_half(Pipe& P, const float* x, const float* g,
   const float rstd = 1.0f / sqrtf(P.row_total(sum32(d)) * (1.0f / D) + 1e-5f);
   const int c0 = HC * P.h;
 #pragma unroll
-  for (int c = 0; c < HC; ++c) y[c] = fmaf((x[c] - mu) * rstd, __ldg(g + c0 + c), __ldg(b + c0 + c));
+  for (int c = 0; c < HC; ++c) y[c] = fmaf((x[c] - mu) * rstd, g[c0 + c], b[c0 + c]);  // g, b: shared or global
 }
 
 __device__ __forceinline__ void ln_half_to_tile(Pipe& P, const float* x, const float* g, const float* b) {
@@ -170,7 +214,7 @@ __device__ void drain_q(Pipe& P, uint32_t qcol, const float* bq) {
   for (int j = 0; j < 2; ++j) {
     const int hd = 2 * P.h + j;
 #pragma unroll
-    for (int i = 0; i < 16; ++i) v[16 * j + i] += __ldg(bq + 16 * hd + i);
+    for (int i = 0; i < 16; ++i) v[16 * j + i] += bq[16 * hd + i];
     uint8_t* tq = P.smem + S_Q + hd * 4096;
     st_row8(tq, P.r, 0, DH, v + 16 * j);
     st_row8(tq, P.r, 8, DH, v + 16 * j + 8);
@@ -185,7 +229,7 @@ __device__ void drain_kv(Pipe& P, uint32_t kcol, const float* bk, const float* b
   for (int j = 0; j < 2; ++j) {
     const int hd = 2 * P.h + j;
 #pragma unroll
-    for (int i = 0; i < 16; ++i) v[16 * j + i] += __ldg(bk + 16 * hd + i);
+    for (int i = 0; i < 16; ++i) v[16 * j + i] += bk[16 * hd + i];
     uint8_t* tk = P.smem + S_K + hd * 4096;
     st_row8(tk, P.r, 0, DH, v + 16 * j);
     st_row8(tk, P.r, 8, DH, v + 16 * j + 8);
@@ -199,10 +243,17 @@ __device__ void drain_kv(Pipe& P, uint32_t kcol, const float* bk, const float* b
     uint8_t* tv = P.smem + S_VT + hd * 4096 + col_off;
 #pragma unroll
     for (int d = 0; d < DH; ++d) {
-      const __nv_bfloat16 hv = __float2bfloat16_rn(v[16 * j + d] + __ldg(bv + 16 * hd + d));
+      const __nv_bfloat16 hv = __float2bfloat16_rn(v[16 * j + d] + bv[16 * hd + d]);
       *reinterpret_cast<__nv_bfloat16*>(tv + (d >> 3) * 2048 + (d & 7) * 16) = hv;
     }
   }
+}
+
+// 2^x on the SFU (MUFU.EX2, ~2 ulp); arguments are <= 0 here
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
 }
 
 // softmax of head (2 * pair + h) over the row's own key block -> P tile h
@@ -225,7 +276,7 @@ __device__ void softmax_head(Pipe& P, int nk) {
   for (int i = 0; i < 8; ++i) p8[i] = 0.0f;
 #pragma unroll
   for (int k = 0; k < 64; ++k) {
-    s[k] = (k < nk) ? exp2f(s[k] - mx) : 0.0f;
+    s[k] = (k < nk) ? ex2_approx(s[k] - mx) : 0.0f;
     p8[k & 7] += s[k];
   }
   const float inv = 1.0f / (((p8[0] + p8[1]) + (p8[2] + p8[3])) + ((p8[4] + p8[5]) + (p8[6] + p8[7])));
@@ -286,55 +337,58 @@ __device__ void out_proj(Pipe& P, const float* bo, float* x, bool valid) {
   tmem_ld32(P.lane_addr(T_GEN + HC * P.h), v);
   if (valid)
 #pragma unroll
-    for (int c = 0; c < HC; ++c) x[c] += v[c] + __ldg(bo + HC * P.h + c);
+    for (int c = 0; c < HC; ++c) x[c] += v[c] + bo[HC * P.h + c];
 }
 
-// self attention sub-layer: x += MHA(LN(x + pos))  (decoder.py:214-218)
-__device__ void self_attn(Pipe& P, const AttnW& w, float* x, const float* pos, int nk, bool valid) {
+// Sub-layers.  `prm` is the layer's TCP_* parameter block staged in shared
+// memory (LayerNorm affine and biases); the weight images come from the ring.
+
+// self attention: x += MHA(LN(x + pos))  (decoder.py:214-218)
+__device__ void self_attn(Pipe& P, const float* prm, float* x, const float* pos, int nk, bool valid) {
   float a[HC];
 #pragma unroll
   for (int c = 0; c < HC; ++c) a[c] = x[c] + pos[c];
-  ln_half_to_tile(P, a, w.ln_g, w.ln_b);
+  ln_half_to_tile(P, a, prm + TCP_S_LN_G, prm + TCP_S_LN_B);
   const uint32_t wq = P.acquire();
   P.before_issue();
   if (P.tid == 0) gemm(P.sbase + S_A, D, wq, 3 * D, T_GEN, P.tmem);
   P.prefetch();
   P.commit_wait();
-  drain_q(P, T_GEN, w.bqkv);
-  drain_kv(P, T_GEN + 64, w.bqkv + 64, w.bqkv + 128);
+  drain_q(P, T_GEN, prm + TCP_S_BQKV);
+  drain_kv(P, T_GEN + 64, prm + TCP_S_BQKV + 64, prm + TCP_S_BQKV + 128);
   attn_core(P, nk);
-  out_proj(P, w.bo, x, valid);
+  out_proj(P, prm + TCP_S_BO, x, valid);
 }
 
-// cross attention sub-layer: x += MHA(LN_q(x), LN_kv(f))  (decoder.py:220-227)
-__device__ void cross_attn(Pipe& P, const AttnW& w, float* x, const float* frow, bool valid) {
+// cross attention: x += MHA(LN_q(x), LN_kv(f))  (decoder.py:220-227)
+__device__ void cross_attn(Pipe& P, const float* prm, float* x, const float* frow, bool valid) {
   float f[HC];
 #pragma unroll
   for (int c = 0; c < HC; c += 4) {
     const float4 v = __ldg(reinterpret_cast<const float4*>(frow + HC * P.h + c));
     f[c] = v.x; f[c + 1] = v.y; f[c + 2] = v.z; f[c + 3] = v.w;
   }
-  ln_half_to_tile(P, f, w.ln2_g, w.ln2_b);
+  ln_half_to_tile(P, f, prm + TCP_C_LNKV_G, prm + TCP_C_LNKV_B);
   const uint32_t wkv = P.acquire();
   P.before_issue();
   if (P.tid == 0) gemm(P.sbase + S_A, D, wkv, 2 * D, T_KV, P.tmem);
   P.prefetch();
   P.commit_wait();
-  drain_kv(P, T_KV, w.bqkv + 64, w.bqkv + 128);
-  ln_half_to_tile(P, x, w.ln_g, w.ln_b);
+  drain_kv(P, T_KV, prm + TCP_C_BQKV + 64, prm + TCP_C_BQKV + 128);
+  ln_half_to_tile(P, x, prm + TCP_C_LNQ_G, prm + TCP_C_LNQ_B);
   const uint32_t wq = P.acquire();
   P.before_issue();
   if (P.tid == 0) gemm(P.sbase + S_A, D, wq, D, T_GEN, P.tmem);
   P.prefetch();
   P.commit_wait();
-  drain_q(P, T_GEN, w.bqkv);
+  drain_q(P, T_GEN, prm + TCP_C_BQKV);
   attn_core(P, BLK);
-  out_proj(P, w.bo, x, valid);
+  out_proj(P, prm + TCP_C_BO, x, valid);
 }
 
-// MLP sub-layer: x += W2 relu(W1 LN(x) + b1) + b2  (decoder.py:205-212)
-__device__ void mlp(Pipe& P, const MlpW& w, float* x, bool valid) {
-  ln_half_to_tile(P, x, w.ln_g, w.ln_b);
+// MLP: x += W2 relu(W1 LN(x) + b1) + b2  (decoder.py:205-212)
+__device__ void mlp(Pipe& P, const float* prm, float* x, bool valid) {
+  ln_half_to_tile(P, x, prm + TCP_M_LN_G, prm + TCP_M_LN_B);
   const uint32_t w1 = P.acquire();
   P.before_issue();
   if (P.tid == 0) gemm(P.sbase + S_A, D, w1, 4 * D, T_GEN, P.tmem);
@@ -347,7 +401,7 @@ __device__ void mlp(Pipe& P, const MlpW& w, float* x, bool valid) {
     float v[64];
     tc::tmem_ld64(P.lane_addr(T_GEN + c0), v);
 #pragma unroll
-    for (int i = 0; i < 64; ++i) v[i] = fmaxf(v[i] + __ldg(w.b1 + c0 + i), 0.0f);
+    for (int i = 0; i < 64; ++i) v[i] = fmaxf(v[i] + prm[TCP_M_B1 + c0 + i], 0.0f);
 #pragma unroll
     for (int i = 0; i < 64; i += 8) st_row8(th, P.r, c0 + i, 4 * D, v + i);
   }
@@ -360,7 +414,7 @@ __device__ void mlp(Pipe& P, const MlpW& w, float* x, bool valid) {
   tmem_ld32(P.lane_addr(T_GEN + HC * P.h), v);
   if (valid)
 #pragma unroll
-    for (int c = 0; c < HC; ++c) x[c] += v[c] + __ldg(w.b2 + HC * P.h + c);
+    for (int c = 0; c < HC; ++c) x[c] += v[c] + prm[TCP_M_B2 + HC * P.h + c];
 }
 
 __device__ void setup(Pipe& P, Shared& sh, uint8_t* smem) {
@@ -374,9 +428,17 @@ __device__ void setup(Pipe& P, Shared& sh, uint8_t* smem) {
   P.wload = 0;
   P.wuse = 0;
   P.xc = 0;
+  P.pload = 0;
+  P.puse = 0;
+#ifdef FSB_PROFILE
+  for (int i = 0; i < 8; ++i) P.prof[i] = 0;
+  P.prof[0] = -clock64();
+#endif
   if (P.tid == 0) {
     tc::mbar_init(&sh.wbar[0], 1);
     tc::mbar_init(&sh.wbar[1], 1);
+    tc::mbar_init(&sh.pbar[0], 1);
+    tc::mbar_init(&sh.pbar[1], 1);
     tc::mbar_init(&sh.mbar, 1);
     tc::mbar_fence_init();
   }
@@ -388,10 +450,17 @@ __device__ void setup(Pipe& P, Shared& sh, uint8_t* smem) {
   P.prefetch();
 }
 
-__device__ void teardown(Pipe& P) {
+__device__ void teardown(Pipe& P, int role) {
   tc::fence_before();
   __syncthreads();
   if (P.tid < 32) tc::tmem_dealloc(P.tmem, 512);
+#ifdef FSB_PROFILE
+  P.prof[0] += clock64();
+  if ((P.tid == 0 || P.tid == NTH - 1) && blockIdx.x == 0)
+    for (int i = 0; i < 8; ++i) g_tc_prof[role][P.tid ? 1 : 0][i] = (unsigned long long)P.prof[i];
+#else
+  (void)role;
+#endif
 }
 
 }  // namespace
@@ -419,6 +488,7 @@ __global__ void __launch_bounds__(NTH, 1) k_encoder_tc(const float* __restrict__
   __syncthreads();
   Pipe P;
   setup(P, sh, smem);
+  if (w.layers > 0) P.pprefetch(w.tc_params[0]);
   const int blk = P.r / BLK, p = P.r % BLK;
   const int crop = 2 * blockIdx.x + blk;
   const bool valid = crop < ncrops;
@@ -460,8 +530,11 @@ __global__ void __launch_bounds__(NTH, 1) k_encoder_tc(const float* __restrict__
 #pragma unroll
   for (int c = 0; c < HC; ++c) zero[c] = 0.0f;
   for (int l = 0; l < w.layers; ++l) {
-    self_attn(P, w.self[l], x, zero, BLK, valid);
-    mlp(P, w.mlp[l], x, valid);
+    const float* prm = P.pacquire();
+    __syncthreads();  // every thread is past layer l - 1: its slot may be refilled
+    if (l + 1 < w.layers) P.pprefetch(w.tc_params[l + 1]);
+    self_attn(P, prm, x, zero, BLK, valid);
+    mlp(P, prm, x, valid);
   }
   float y[HC];
   ln_half(P, x, w.norm_g, w.norm_b, y);
@@ -475,7 +548,7 @@ __global__ void __launch_bounds__(NTH, 1) k_encoder_tc(const float* __restrict__
     }
     flag_nonfinite(nonfinite, bad);
   }
-  teardown(P);
+  teardown(P, 0);
 }
 
 // ===========================================================================
@@ -574,6 +647,7 @@ __global__ void __launch_bounds__(NTH, 1) k_decoders_tc(DecodeArgs a, BodyW bw, 
   __syncthreads();
   Pipe P;
   setup(P, sh, smem);
+  if (layers > 0) P.pprefetch(body ? bw.tc_params[0] : hw.tc_params[0]);
   const int r = P.r, blk = r / BLK, rb = r % BLK, c0 = HC * P.h;
   const int unit = body ? 2 * blockIdx.x + blk : 2 * (blockIdx.x - nbc) + blk;  // frame or hand index
   const int nunit = body ? a.nbody : a.nhand;
@@ -657,9 +731,12 @@ __global__ void __launch_bounds__(NTH, 1) k_decoders_tc(DecodeArgs a, BodyW bw, 
         pos[i] = v;
       }
     }
-    self_attn(P, body ? bw.self[l] : hw.self[l], x, pos, nrows, valid);
-    cross_attn(P, body ? bw.cross[l] : hw.cross[l], x, frow, valid);
-    mlp(P, body ? bw.mlp[l] : hw.mlp[l], x, valid);
+    const float* prm = P.pacquire();
+    __syncthreads();  // every thread is past layer l - 1: its slot may be refilled
+    if (l + 1 < layers) P.pprefetch(body ? bw.tc_params[l + 1] : hw.tc_params[l + 1]);
+    self_attn(P, prm, x, pos, nrows, valid);
+    cross_attn(P, prm, x, frow, valid);
+    mlp(P, prm, x, valid);
     const unsigned sel = body ? a.body_sel : a.hand_sel;
     if ((sel >> l) & 1u) {
       if (body) {
@@ -731,7 +808,17 @@ __global__ void __launch_bounds__(NTH, 1) k_decoders_tc(DecodeArgs a, BodyW bw, 
       }
     }
   }
-  teardown(P);
+  teardown(P, 1);
+}
+
+// debug export of the FSB_PROFILE cycle counters (not part of the public ABI)
+extern "C" int fsb_debug_tc_profile(unsigned long long* out32) {
+#ifdef FSB_PROFILE
+  return cudaMemcpyFromSymbol(out32, g_tc_prof, sizeof(unsigned long long) * 32) == cudaSuccess ? 0 : 4;
+#else
+  for (int i = 0; i < 32; ++i) out32[i] = 0;
+  return 3;
+#endif
 }
 
 cudaError_t init_attrs_transformer_tc() {

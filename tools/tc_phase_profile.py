@@ -1,0 +1,47 @@
+"""Cycle attribution of CTA 0 of the tcgen05 encoder / decoder kernels (needs
+a library built with FSB_PROFILE=1): total, MMA waits, weight waits, issue
+barriers and LayerNorm exchange barriers for thread 0 (the MMA / TMA issuer)
+and thread 255; the remainder is the thread's own work (epilogues)."""
+
+import ctypes
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def main():
+    import torch
+
+    import bench
+    from paper_2603_15603_b200 import pipeline as pl
+    from paper_2603_15603_b200 import priors as pr
+    from paper_2603_15603_b200 import runtime
+
+    pipe, (mhr, smpl, gt, dec, proj) = bench.build_models("bf16")
+    ctx = pipe.context()
+    ctx.set_graphs(False)
+    scenes = bench.make_scenes(smpl, bench.frame_seeds(0, 32))
+    images = pr.render_scenes(scenes)
+    kps = torch.from_numpy(np.stack([s.keypoints2d for s in scenes])).cuda()
+    outs = pipe.allocate_outputs(32, tail=True)
+    for _ in range(3):
+        pipe.launch(images, kps, outs, pl.fast_config())
+    torch.cuda.synchronize()
+    lib = ctypes.CDLL(runtime.LIB_PATH)
+    buf = (ctypes.c_ulonglong * 32)()
+    rc = lib.fsb_debug_tc_profile(buf)
+    names = ["total", "mma_wait", "weight_wait", "issue_bar", "xch_bar"]
+    for role, tag in ((0, "encoder"), (1, "decoder")):
+        for th, tname in ((0, "t0"), (1, "t255")):
+            v = [buf[role * 16 + th * 8 + i] for i in range(5)]
+            rest = v[0] - sum(v[1:])
+            print(tag, tname, "rc", rc,
+                  " ".join("%s=%d(%.1f%%)" % (n, x, 100.0 * x / max(v[0], 1)) for n, x in zip(names, v)),
+                  "work=%d(%.1f%%)" % (rest, 100.0 * rest / max(v[0], 1)))
+
+
+if __name__ == "__main__":
+    main()
