@@ -52,11 +52,12 @@ def parse():
     ap.add_argument("--warmup", type=int, default=20)
     ap.add_argument("--batch", type=int, default=32, help="frames per GPU per step (C2: 32)")
     ap.add_argument("--bank", type=int, default=256, help="distinct frames per GPU cycled through")
-    ap.add_argument("--precision", default="fp32", choices=("fp32", "bf16"))
+    ap.add_argument("--precision", default="bf16", choices=("fp32", "bf16"))
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-c3", action="store_true", help="skip the C3 LBS + projector microbench")
     return ap.parse_args()
 
 
@@ -330,6 +331,9 @@ def main():
     e2e = None if args.no_e2e else end_to_end(torch, pipe, images, kps, cfg, B, args.steps, args.warmup, dist,
                                               world)
 
+    # -- C3 microbench: LBS + projector on 4096 full-size meshes ---------------
+    c3 = None if args.no_c3 else c3_microbench(torch, pipe, ctx, meshes=4096, reps=10)
+
     if rank != 0:
         if dist is not None:
             dist.destroy_process_group()
@@ -358,11 +362,67 @@ def main():
                    "precision": args.precision, "graphs": True},
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
         "clocks": clk.summary(), "p50_frame_latency_ms": lat["p50_ms"], "frame_latency": lat,
-        "stage_ms": stage_ms,
+        "stage_ms": stage_ms, "c3": c3,
     }
     print(json.dumps(line), flush=True)
     if dist is not None:
         dist.destroy_process_group()
+
+
+def c3_microbench(torch, pipe, ctx, meshes, reps):
+    """C3: MHR LBS of `meshes` full-size meshes (18,439 v) plus
+    the MHR -> SMPL projector and SMPL FK, poses from rng(3) as the
+    acceptance suite draws them.  LBS is timed alone for its HBM roofline
+    (222,628 algorithmic bytes per mesh: V_mhr written + pose/transforms)."""
+    from paper_2603_15603_b200 import runtime as rt
+
+    rng = np.random.default_rng(3)
+    p = np.zeros((meshes, 76), np.float32)
+    p[:, :66] = rng.normal(0.0, 0.2, size=(meshes, 66))
+    p[:, 66:] = rng.normal(0.0, 0.45, size=(meshes, 10))
+    p[:, 51:54] = 0.0
+    p[:, 63:66] = 0.0
+    dev = torch.device("cuda", torch.cuda.current_device())
+    poses = torch.from_numpy(p).to(dev)
+    nv = pipe.mhr.num_vertices
+    v = torch.empty((meshes, nv, 3), dtype=torch.float32, device=dev)
+    th = torch.empty((meshes, 76), dtype=torch.float32, device=dev)
+    j = torch.empty((meshes, 22, 3), dtype=torch.float32, device=dev)
+    ctx.reserve(meshes)
+    prec = rt.PRECISIONS[pipe.precision]
+    st = torch.cuda.current_stream()
+
+    def full():
+        ctx.check(ctx.lib.fsb_skin_project(ctx.h, rt.ptr(poses), meshes, rt.ptr(v), rt.ptr(th), rt.ptr(j), None, prec,
+                                           ctx.stream))
+
+    def lbs():
+        ctx.check(ctx.lib.fsb_skin(ctx.h, 0, rt.ptr(poses), meshes, rt.ptr(v), ctx.stream))
+
+    out = {}
+    for name, fn in (("full", full), ("lbs", lbs)):
+        for _ in range(3):
+            fn()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(st)
+        for _ in range(reps):
+            fn()
+        e1.record(st)
+        torch.cuda.synchronize()
+        out[name] = e0.elapsed_time(e1) / reps
+    ctx.check_finite("c3")
+    peak = 6550.7
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            peak = float(json.load(fh)["hbm_gbs"])
+    except (OSError, KeyError, ValueError):
+        pass
+    lbs_gbs = meshes * BYTES_LBS_MESH / (out["lbs"] / 1e3) / 1e9
+    return {"workload": "C3: %d full-size meshes (MHR 18439 v) LBS + projector + SMPL FK, %s" % (meshes, pipe.precision),
+            "meshes_per_s": meshes / (out["full"] / 1e3), "ms_full": out["full"], "ms_lbs_fk": out["lbs"],
+            "lbs_achieved_gbs": lbs_gbs, "lbs_frac_of_hbm": lbs_gbs / peak,
+            "lbs_algorithmic_bytes": meshes * BYTES_LBS_MESH}
 
 
 def attribute_stages(torch, pipe, ctx, img, kp, outs, cfg, reps):

@@ -103,48 +103,117 @@ struct VertexTmpl {
   }
 };
 
-constexpr int kLbsThreads = 256;
-constexpr int kLbsVPT = 2;     // vertices per thread
-constexpr int kLbsMeshes = 32; // meshes per CTA (template reuse factor)
+// packed FP32x2 FMA (sm_100 FFMA2): d = a * b + c on both lanes
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+      "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
 
+constexpr int kLbsThreads = 256;
+constexpr int kLbsVPT = 2;      // consecutive vertices per thread (float2 stores)
+constexpr int kLbsMeshes = 32;  // meshes per CTA (template reuse factor), as 16 pairs
+
+// LBS of a vertex tile for up to 32 meshes.  Each thread keeps its two
+// vertices' template records in registers and walks the meshes two at a
+// time: the per-mesh transforms and shape coefficients of a mesh pair are
+// interleaved in shared memory as float2, so every multiply-add of the blend,
+// shape offset and apply is one FFMA2 serving both meshes.
 // grid: (ceil(nv / 512), ceil(B / 32))
 template <int NZ>
 __global__ void __launch_bounds__(kLbsThreads) k_lbs(TemplateDev t, const float* __restrict__ rel,
                                                      const float* __restrict__ poses, int ld_pose, int B,
                                                      float* __restrict__ verts, int* nonfinite) {
-  __shared__ __align__(16) float As[kLbsMeshes][FSB_NJ * 12];
-  __shared__ float Ss[kLbsMeshes][10];
+  __shared__ __align__(16) float2 A2[kLbsMeshes / 2][FSB_NJ * 12];
+  __shared__ __align__(16) float2 S2[kLbsMeshes / 2][10];
   const int m0 = blockIdx.y * kLbsMeshes;
   const int nm = min(kLbsMeshes, B - m0);
-  for (int i = threadIdx.x; i < nm * FSB_NJ * 12; i += kLbsThreads)
-    As[i / (FSB_NJ * 12)][i % (FSB_NJ * 12)] = rel[(int64_t)m0 * FSB_NJ * 12 + i];
-  for (int i = threadIdx.x; i < nm * 10; i += kLbsThreads)
-    Ss[i / 10][i % 10] = poses[(int64_t)(m0 + i / 10) * ld_pose + 66 + i % 10];
-  VertexTmpl<NZ> vt[kLbsVPT];
-  int vid[kLbsVPT];
-#pragma unroll
-  for (int q = 0; q < kLbsVPT; ++q) {
-    vid[q] = blockIdx.x * kLbsThreads * kLbsVPT + q * kLbsThreads + threadIdx.x;
-    if (vid[q] < t.nv) vt[q].load(t, vid[q]);
+  const int npair = (nm + 1) / 2;
+  for (int i = threadIdx.x; i < npair * 2 * FSB_NJ * 12; i += kLbsThreads) {
+    const int pr = i / (2 * FSB_NJ * 12), rem = i % (2 * FSB_NJ * 12), half = rem / (FSB_NJ * 12),
+              e = rem % (FSB_NJ * 12);
+    const int m = 2 * pr + half;
+    const float v = m < nm ? rel[(int64_t)(m0 + m) * FSB_NJ * 12 + e] : 0.0f;
+    reinterpret_cast<float*>(&A2[pr][e])[half] = v;
   }
+  for (int i = threadIdx.x; i < npair * 2 * 10; i += kLbsThreads) {
+    const int pr = i / 20, half = (i / 10) % 2, k = i % 10, m = 2 * pr + half;
+    reinterpret_cast<float*>(&S2[pr][k])[half] = m < nm ? poses[(int64_t)(m0 + m) * ld_pose + 66 + k] : 0.0f;
+  }
+  VertexTmpl<NZ> vt[kLbsVPT];
+  const int v0 = (blockIdx.x * kLbsThreads + threadIdx.x) * kLbsVPT;
+#pragma unroll
+  for (int q = 0; q < kLbsVPT; ++q)
+    if (v0 + q < t.nv) vt[q].load(t, v0 + q);
   __syncthreads();
-  bool bad = false;
-  for (int m = 0; m < nm; ++m) {
-    float* dst = verts + (int64_t)(m0 + m) * t.nv * 3;
+  if (v0 >= t.nv) return;
+  const bool both = v0 + 1 < t.nv;
+  float2 chk = make_float2(0.0f, 0.0f);
+  const float2 one2 = make_float2(1.0f, 1.0f);
+  for (int pr = 0; pr < npair; ++pr) {
+    float2 sh[10];
+#pragma unroll
+    for (int k = 0; k < 10; ++k) sh[k] = S2[pr][k];
+    float2 o[kLbsVPT][3];
 #pragma unroll
     for (int q = 0; q < kLbsVPT; ++q) {
-      if (vid[q] < t.nv) {
-        float o[3];
-        vt[q].apply(As[m], Ss[m], o);
+      const VertexTmpl<NZ>& V = vt[q];
+      float2 T[12];
 #pragma unroll
-        for (int a = 0; a < 3; ++a) {
-          bad |= !isfinite(o[a]);
-          __stcs(dst + (int64_t)vid[q] * 3 + a, o[a]);
+      for (int e = 0; e < 12; ++e) T[e] = make_float2(0.0f, 0.0f);
+#pragma unroll
+      for (int z = 0; z < NZ; ++z) {
+        const float2 wz = make_float2(V.w[z], V.w[z]);
+        const float4* row = reinterpret_cast<const float4*>(&A2[pr][12 * V.j[z]]);
+#pragma unroll
+        for (int e2 = 0; e2 < 6; ++e2) {
+          const float4 r = row[e2];
+          T[2 * e2] = ffma2(wz, make_float2(r.x, r.y), T[2 * e2]);
+          T[2 * e2 + 1] = ffma2(wz, make_float2(r.z, r.w), T[2 * e2 + 1]);
         }
+      }
+      float2 vs[3];
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        float2 acc = make_float2(0.0f, 0.0f);
+#pragma unroll
+        for (int k = 0; k < 10; ++k) acc = ffma2(make_float2(V.sb[10 * c + k], V.sb[10 * c + k]), sh[k], acc);
+        vs[c] = ffma2(acc, one2, make_float2(V.vr[c], V.vr[c]));
+      }
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        float2 acc = ffma2(T[4 * a], vs[0], T[4 * a + 3]);
+        acc = ffma2(T[4 * a + 1], vs[1], acc);
+        o[q][a] = ffma2(T[4 * a + 2], vs[2], acc);
+        if (q == 0 || both) chk = ffma2(o[q][a], one2, chk);
+      }
+    }
+    // mesh 2 pr (.x lanes) and 2 pr + 1 (.y lanes): 6 floats each; 8-byte
+    // vector stores when the mesh base keeps them aligned (odd nv, odd mesh:
+    // scalar stores)
+    const int m = m0 + 2 * pr;
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      if (2 * pr + half >= nm) break;
+      float* d = verts + ((int64_t)(m + half) * t.nv + v0) * 3;
+      const float f[6] = {half ? o[0][0].y : o[0][0].x, half ? o[0][1].y : o[0][1].x,
+                          half ? o[0][2].y : o[0][2].x, half ? o[1][0].y : o[1][0].x,
+                          half ? o[1][1].y : o[1][1].x, half ? o[1][2].y : o[1][2].x};
+      if (both && ((reinterpret_cast<uintptr_t>(d) & 7) == 0)) {
+        __stcs(reinterpret_cast<float2*>(d), make_float2(f[0], f[1]));
+        __stcs(reinterpret_cast<float2*>(d + 2), make_float2(f[2], f[3]));
+        __stcs(reinterpret_cast<float2*>(d + 4), make_float2(f[4], f[5]));
+      } else {
+        const int n = both ? 6 : 3;
+        for (int i = 0; i < n; ++i) __stcs(d + i, f[i]);
       }
     }
   }
-  if (bad && nonfinite != nullptr) atomicOr(nonfinite, 1);
+  if (nonfinite != nullptr && !(isfinite(chk.x) && isfinite(chk.y))) atomicOr(nonfinite, 1);
 }
 
 // ---------------------------------------------------------------------------

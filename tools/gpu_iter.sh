@@ -18,5 +18,7 @@ except Exception as e:
 print(p, "value %.0f e2e %.0f p50 %.3f ms" % (d["value"], d["e2e"]["value"], d["p50_frame_latency_ms"]))
 print("  stages", {k: round(v, 4) for k, v in d["stage_ms"].items()})
 r = d["roofline"]; print("  roofline", r["kernel"], r["bound"], "%.3g %s frac %.4f" % (r["achieved"], r["unit"], r["frac"]), "clocks", d["clocks"])
+c3 = d.get("c3")
+if c3: print("  c3 meshes/s %.0f full %.3f ms lbs %.3f ms %.0f GB/s frac %.3f" % (c3["meshes_per_s"], c3["ms_full"], c3["ms_lbs_fk"], c3["lbs_achieved_gbs"], c3["lbs_frac_of_hbm"]))
 EOF
 done
