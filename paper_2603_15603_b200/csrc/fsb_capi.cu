@@ -46,6 +46,7 @@ cudaError_t launch_render(const void* scenes, int B, int H, int W, float* out, c
 cudaError_t init_attrs_transformer();
 cudaError_t init_attrs_transformer_tc();
 cudaError_t init_attrs_mlp_tc();
+cudaError_t init_attrs_gemm_tc();
 cudaError_t launch_tile_layer(const uint8_t* Aimg, const uint8_t* Bimg, int KT, int G, int M, int N, float* partial,
                               const float* bias, const float* mask, int relu, float* out, int ldo, uint8_t* out_img,
                               int KT_out, int* nonfinite, cudaStream_t st);
@@ -197,7 +198,8 @@ int fsb_ctx_create(int device, fsb_ctx** out) {
   fsb_ctx* c = new fsb_ctx();
   c->device = device;
   if (init_attrs_transformer() != cudaSuccess || init_attrs_transformer_tc() != cudaSuccess ||
-      init_attrs_mlp_tc() != cudaSuccess || init_attrs_body() != cudaSuccess) {
+      init_attrs_mlp_tc() != cudaSuccess || init_attrs_gemm_tc() != cudaSuccess ||
+      init_attrs_body() != cudaSuccess) {
     delete c;
     return FSB_ERR_CUDA;
   }
