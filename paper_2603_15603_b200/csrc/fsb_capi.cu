@@ -11,6 +11,7 @@
 
 #include "../../include/fsb_b200.h"
 #include "fsb_common.cuh"
+#include "fsb_vit.h"
 #include "fsb_weights.h"
 
 // ---- kernels (other translation units) ------------------------------------
@@ -113,6 +114,11 @@ struct fsb_ctx {
   EncW enc{};
   BodyW body{};
   HandW hand{};
+  // large-config encoder (non-default DecoderConfig, k_vit.cu)
+  bool vit = false;
+  VitW vitw;
+  DevMem vit_ws_mem;
+  VitWs vit_ws{};
   // templates / projector
   bool has_tmpl[2] = {false, false};
   DevMem tmpl_mem[2];
@@ -169,6 +175,8 @@ bool default_model(const fsb_decoder_config& c) {
          c.body_layers <= 8 && c.hand_layers <= 8;
 }
 
+constexpr int kVitChunk = 128;  // crops per large-config encoder pass
+
 int layer_count(uint32_t sel) { return __builtin_popcount(sel); }
 
 bool capturing(cudaStream_t st) {
@@ -182,6 +190,109 @@ int ensure_ws(fsb_ctx* c, int frames, cudaStream_t st) {
   if (capturing(st))
     return fail(c, FSB_ERR_USAGE, "workspace for %d frames not reserved before graph capture", frames);
   return fsb_reserve(c, frames);
+}
+
+// Large-config encoder upload: bf16 W^T (N x K row-major) per linear layer,
+// q|k|v stacked to (3D x D); fp32 biases, LayerNorm affine and positions.
+// Only the encoder is device-resident for such configs;
+// the decoders stay on the default configuration.
+int load_vit(fsb_ctx* c, const fsb_decoder_config& cfg, const std::map<std::string, std::pair<const float*, int64_t>>& tab) {
+  const int D = cfg.dim, p = cfg.patch, K0 = p * p * 3;
+  if (D % 128 || D > 2048 || D / cfg.heads != 64 || D % cfg.heads || K0 % 64)
+    return fail(c, FSB_ERR_USAGE,
+                "large-config encoder needs dim %% 128 == 0 (<= 2048), head dim 64 and patch*patch*3 %% 64 == 0");
+  const int np = cfg.crop_size / p, T = np * np;
+  Packer pk;
+  std::map<std::string, size_t> off;
+  std::string missing;
+  auto find = [&](const std::string& name, int64_t n) -> const float* {
+    auto it = tab.find(name);
+    if (it == tab.end() || it->second.second != n) {
+      if (missing.empty()) missing = name;
+      return nullptr;
+    }
+    return it->second.first;
+  };
+  auto put = [&](const std::string& name, int64_t n) {
+    const float* a = find(name, n);
+    if (a) off[name] = pk.add(a, (size_t)n * 4);
+  };
+  // (K x N_i) matrices -> one (sum N_i x K) bf16 W^T, 32x32 blocked transpose
+  auto put_t = [&](const std::string& key, std::vector<std::string> mats, int K, int N) {
+    std::vector<const float*> src;
+    for (auto& m : mats) src.push_back(find(m, (int64_t)K * N));
+    for (auto* a : src)
+      if (!a) return;
+    const int R = N * (int)mats.size();
+    const size_t o = pk.add(nullptr, (size_t)R * K * 2);
+    __nv_bfloat16* dst = reinterpret_cast<__nv_bfloat16*>(pk.host.data() + o);
+    for (size_t t = 0; t < src.size(); ++t)
+      for (int k0 = 0; k0 < K; k0 += 32)
+        for (int n0 = 0; n0 < N; n0 += 32)
+          for (int k = k0; k < k0 + 32 && k < K; ++k)
+            for (int n = n0; n < n0 + 32 && n < N; ++n)
+              dst[(size_t)(t * N + n) * K + k] = __float2bfloat16_rn(src[t][(size_t)k * N + n]);
+    off[key] = o;
+  };
+  put_t("enc.wpatch", {"enc.patch_w"}, K0, D);
+  put("enc.patch_b", D);
+  put("enc.pos", (int64_t)T * D);
+  put("enc.norm_g", D);
+  put("enc.norm_b", D);
+  for (int l = 0; l < cfg.enc_layers; ++l) {
+    const std::string a = "enc.l" + std::to_string(l) + ".self", m = "enc.l" + std::to_string(l) + ".mlp";
+    put_t(a + ".wqkv_t", {a + ".wq", a + ".wk", a + ".wv"}, D, D);
+    put_t(a + ".wo_t", {a + ".wo"}, D, D);
+    put_t(m + ".w1_t", {m + ".w1"}, D, 4 * D);
+    put_t(m + ".w2_t", {m + ".w2"}, 4 * D, D);
+    put(a + ".ln_g", D);
+    put(a + ".ln_b", D);
+    put(a + ".bo", D);
+    put(m + ".ln_g", D);
+    put(m + ".ln_b", D);
+    put(m + ".b1", 4 * D);
+    put(m + ".b2", D);
+    // q|k|v biases stacked
+    const float *bq = find(a + ".bq", D), *bk = find(a + ".bk", D), *bv = find(a + ".bv", D);
+    if (bq && bk && bv) {
+      std::vector<float> b(3 * (size_t)D);
+      memcpy(b.data(), bq, D * 4);
+      memcpy(b.data() + D, bk, D * 4);
+      memcpy(b.data() + 2 * D, bv, D * 4);
+      off[a + ".bqkv"] = pk.add(b.data(), b.size() * 4);
+    }
+  }
+  if (!missing.empty()) return fail(c, FSB_ERR_SHAPE, "encoder weight table: missing or mis-sized '%s'", missing.c_str());
+  c->vit_ws_mem.release();
+  c->vit_ws = VitWs{};
+  FSB_CUDA(c, c->dec_mem.alloc(pk.host.size()));
+  FSB_CUDA(c, cudaMemcpy(c->dec_mem.p, pk.host.data(), pk.host.size(), cudaMemcpyHostToDevice));
+  const uint8_t* base = static_cast<const uint8_t*>(c->dec_mem.p);
+  auto F = [&](const std::string& n) { return reinterpret_cast<const float*>(base + off.at(n)); };
+  auto B = [&](const std::string& n) { return reinterpret_cast<const __nv_bfloat16*>(base + off.at(n)); };
+  VitW& w = c->vitw;
+  w.S = cfg.crop_size;
+  w.p = p;
+  w.D = D;
+  w.H = cfg.heads;
+  w.T = T;
+  w.wpatch = B("enc.wpatch");
+  w.patch_b = F("enc.patch_b");
+  w.pos = F("enc.pos");
+  w.norm_g = F("enc.norm_g");
+  w.norm_b = F("enc.norm_b");
+  w.layers.clear();
+  for (int l = 0; l < cfg.enc_layers; ++l) {
+    const std::string a = "enc.l" + std::to_string(l) + ".self", m = "enc.l" + std::to_string(l) + ".mlp";
+    w.layers.push_back(VitLayer{B(a + ".wqkv_t"), B(a + ".wo_t"), B(m + ".w1_t"), B(m + ".w2_t"), F(a + ".ln_g"),
+                                F(a + ".ln_b"), F(a + ".bqkv"), F(a + ".bo"), F(m + ".ln_g"), F(m + ".ln_b"),
+                                F(m + ".b1"), F(m + ".b2")});
+  }
+  c->cfg = cfg;
+  c->has_decoder = true;
+  c->vit = true;
+  c->ws_frames = 0;
+  return FSB_OK;
 }
 
 }  // namespace
@@ -304,6 +415,7 @@ int fsb_load_decoder(fsb_ctx* c, const fsb_decoder_config* cfg, int n, const cha
     return fail(c, FSB_ERR_SHAPE, "inconsistent decoder config");
   if (cfg->enc_layers > FSB_MAX_LAYERS || cfg->body_layers > 8 || cfg->hand_layers > 8)
     return fail(c, FSB_ERR_USAGE, "too many layers for the device tables");
+  if (!default_model(*cfg)) return load_vit(c, *cfg, tab);
   Packer pk;
   std::map<std::string, size_t> off;
   std::string missing;
@@ -541,6 +653,7 @@ int fsb_load_decoder(fsb_ctx* c, const fsb_decoder_config* cfg, int n, const cha
   c->body.joints_rest = c->has_tmpl[FSB_SMPL] ? c->tmpl[FSB_SMPL].joints_rest : nullptr;
   c->cfg = *cfg;
   c->has_decoder = true;
+  c->vit = false;
   c->ws_frames = 0;  // re-reserve for the new shapes
   return FSB_OK;
 }
@@ -734,6 +847,25 @@ int fsb_bridge(fsb_ctx* c, const float* v, int B, int nv, const int32_t* corners
 int fsb_encode(fsb_ctx* c, const float* crops, int n, float* feats, int precision, void* stream) {
   if (!c->has_decoder) return fail(c, FSB_ERR_USAGE, "encode: no decoder loaded");
   if (precision != FSB_FP32 && precision != FSB_BF16) return fail(c, FSB_ERR_USAGE, "encode: bad precision %d", precision);
+  if (c->vit) {
+    if (precision != FSB_BF16)
+      return fail(c, FSB_ERR_USAGE, "encode: the large-config encoder runs in bf16 only (precision='bf16')");
+    if (n <= 0) return FSB_OK;
+    const int want = n < kVitChunk ? n : kVitChunk;
+    if (c->vit_ws.max_crops < want) {
+      if (capturing((cudaStream_t)stream))
+        return fail(c, FSB_ERR_USAGE, "encode: encoder workspace for %d crops not allocated before graph capture", want);
+      FSB_CUDA(c, cudaStreamSynchronize((cudaStream_t)stream));
+      FSB_CUDA(c, c->vit_ws_mem.alloc(vit_ws_bytes(c->vitw, want)));
+      vit_ws_carve(c->vitw, want, c->vit_ws_mem.p, &c->vit_ws);
+    }
+    int nl = 0;
+    FSB_CUDA(c, launch_vit_encoder(c->vitw, c->vit_ws, crops, n, feats, c->d_flag, (cudaStream_t)stream, &nl));
+    c->counters.encode += 1;
+    c->counters.encoded_crops += n;
+    c->launches += nl;
+    return FSB_OK;
+  }
   if (!default_model(c->cfg))
     return fail(c, FSB_ERR_USAGE, "encode: the fused fp32 encoder supports the default DecoderConfig only");
   if (precision == FSB_BF16)

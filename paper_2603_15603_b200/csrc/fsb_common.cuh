@@ -26,6 +26,13 @@ __device__ __forceinline__ float warp_max(float v) {
 }
 
 // sets the context's device-side non-finite flag (mapped to NumericError)
+// 2^x on the SFU (MUFU.EX2, ~2 ulp); arguments are <= 0 where it is used
+__device__ __forceinline__ float ex2_approx(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 __device__ __forceinline__ void flag_nonfinite(int* flag, float v) {
   if (flag != nullptr && !isfinite(v)) atomicOr(flag, 1);
 }

@@ -18,17 +18,7 @@
 #include "fsb_common.cuh"
 #include "tc_sm100.cuh"
 
-enum { EPI_BIAS_BF16 = 0, EPI_RELU_BF16 = 1, EPI_RESID_F32 = 2, EPI_EMBED_F32 = 3 };
-
-struct GemmEpi {
-  const float* bias;        // (N)
-  __nv_bfloat16* out_bf16;  // (M, ldo)
-  float* x_f32;             // (M, ldo) residual stream
-  const float* pos;         // (T, N) for EPI_EMBED_F32
-  int ldo;
-  int T;
-  int kind;
-};
+#include "gemm_tc.h"
 
 namespace {
 constexpr int BM = 128, BK = 64, STAGES = 4;

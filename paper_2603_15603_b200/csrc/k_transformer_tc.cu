@@ -249,13 +249,6 @@ __device__ void drain_kv(Pipe& P, uint32_t kcol, const float* bk, const float* b
   }
 }
 
-// 2^x on the SFU (MUFU.EX2, ~2 ulp); arguments are <= 0 here
-__device__ __forceinline__ float ex2_approx(float x) {
-  float y;
-  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
-  return y;
-}
-
 // softmax of head (2 * pair + h) over the row's own key block -> P tile h
 __device__ void softmax_head(Pipe& P, int nk) {
   const int blk = P.r / BLK;

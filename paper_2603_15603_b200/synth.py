@@ -342,10 +342,15 @@ def decoder_weight_plan(cfg):
     return plan
 
 
-def decoder_weights(cfg, seed):
+def decoder_weights(cfg, seed, encoder_only=False):
+    """Random weight table of decoder_weight_plan(cfg).  encoder_only stops
+    after the encoder entries, which come first in the plan, so the values
+    are the same as the full table's."""
     rng = np.random.default_rng(seed)
     out = {}
     for name, shape, kind, scale in decoder_weight_plan(cfg):
+        if encoder_only and not name.startswith("enc."):
+            break
         if kind == "mat":
             out[name] = (rng.standard_normal(shape) * (scale / np.sqrt(shape[0]))).astype(DTYPE)
         elif kind == "raw":
