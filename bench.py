@@ -43,6 +43,9 @@ FLOP_DEC_FRAME = 57_853_440
 BYTES_K1_FRAME = 737_280 + 304
 BYTES_LBS_MESH = 221_268 + 304 + 1_056
 FLOP_MLP_MESH = 4_909_056
+# C4 (ViT-L-sized encoder, S=384, p=16, T=576, D=1024, 24 layers), per crop:
+# 2*T*(3p^2)*D + L*(24*T*D^2 + 4*T^2*D)
+FLOP_C4_CROP = 2 * 576 * 768 * 1024 + 24 * (24 * 576 * 1024 ** 2 + 4 * 576 ** 2 * 1024)
 
 
 def parse():
@@ -58,6 +61,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-c3", action="store_true", help="skip the C3 LBS + projector microbench")
+    ap.add_argument("--no-c4", action="store_true", help="skip the C4 ViT-L-sized encoder microbench")
+    ap.add_argument("--c4-crops", type=int, default=768, help="C4: 3 crops x 256 frames")
     return ap.parse_args()
 
 
@@ -334,6 +339,9 @@ def main():
     # -- C3 microbench: LBS + projector on 4096 full-size meshes ---------------
     c3 = None if args.no_c3 else c3_microbench(torch, pipe, ctx, meshes=4096, reps=10)
 
+    # -- C4 microbench: ViT-L-sized encoder, 3 crops x 256 frames --------------
+    c4 = None if args.no_c4 else c4_microbench(torch, crops=args.c4_crops, reps=3)
+
     if rank != 0:
         if dist is not None:
             dist.destroy_process_group()
@@ -362,7 +370,7 @@ def main():
                    "precision": args.precision, "graphs": True},
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
         "clocks": clk.summary(), "p50_frame_latency_ms": lat["p50_ms"], "frame_latency": lat,
-        "stage_ms": stage_ms, "c3": c3,
+        "stage_ms": stage_ms, "c3": c3, "c4": c4,
     }
     print(json.dumps(line), flush=True)
     if dist is not None:
@@ -423,6 +431,57 @@ def c3_microbench(torch, pipe, ctx, meshes, reps):
             "meshes_per_s": meshes / (out["full"] / 1e3), "ms_full": out["full"], "ms_lbs_fk": out["lbs"],
             "lbs_achieved_gbs": lbs_gbs, "lbs_frac_of_hbm": lbs_gbs / peak,
             "lbs_algorithmic_bytes": meshes * BYTES_LBS_MESH}
+
+
+def c4_microbench(torch, crops, reps, layers=24):
+    """C4: Decoder.encode (decoder.py:231-260) at ViT-L size,
+    DecoderConfig(crop_size=384, patch=16, dim=1024, heads=16,
+    enc_layers=24), on `crops` U[0,1) crops (768 = 3 crops x 256 frames),
+    bf16 operands with fp32 accumulation on the tcgen05 path.  Tensor-bound:
+    FLOP_C4_CROP algorithmic FLOPs per crop, against the sustained bf16 peak
+    (a ~0.2 s launch sequence under the power cap)."""
+    from paper_2603_15603_b200 import decoder as dc
+    from paper_2603_15603_b200 import runtime as rt
+    from paper_2603_15603_b200 import synth
+
+    cfg = dc.DecoderConfig(crop_size=384, patch=16, dim=1024, heads=16, enc_layers=layers, body_layers=1,
+                           hand_layers=1)
+    ctx = rt.Context()
+    ctx.load_decoder(cfg, synth.decoder_weights(cfg, 40, encoder_only=True))
+    dev = torch.device("cuda", torch.cuda.current_device())
+    g = torch.Generator(device=dev)
+    g.manual_seed(0)
+    x = torch.rand((crops, 384, 384, 3), generator=g, dtype=torch.float32, device=dev)
+    out = torch.empty((crops, 576, 1024), dtype=torch.float32, device=dev)
+    prec = rt.PRECISIONS["bf16"]
+
+    def run():
+        ctx.check(ctx.lib.fsb_encode(ctx.h, rt.ptr(x), crops, rt.ptr(out), prec, ctx.stream), "c4 encode")
+
+    run()
+    torch.cuda.synchronize()
+    st = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for _ in range(reps):
+        run()
+    e1.record(st)
+    torch.cuda.synchronize()
+    ctx.check_finite("c4")
+    ms = e0.elapsed_time(e1) / reps
+    peak, src = 1396.7, "fallback"
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            peak, src = float(json.load(fh)["bf16_tflops_sustained"]), "measured sustained"
+    except (OSError, KeyError, ValueError):
+        pass
+    tf = crops * FLOP_C4_CROP / (ms / 1e3) / 1e12
+    del ctx
+    return {"workload": "C4: ViT-L-sized encoder (S=384, p=16, T=576, D=1024, 16 heads, %d layers) on %d crops "
+                        "(3 crops x %d frames), bf16 tcgen05" % (layers, crops, crops // 3),
+            "ms_per_batch": ms, "crops_per_s": crops / (ms / 1e3), "frames_per_s": crops / 3 / (ms / 1e3),
+            "achieved_tflops": tf, "peak_tflops": peak, "peak_source": src, "frac": tf / peak,
+            "algorithmic_flop_per_batch": crops * FLOP_C4_CROP}
 
 
 def attribute_stages(torch, pipe, ctx, img, kp, outs, cfg, reps):
