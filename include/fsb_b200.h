@@ -102,7 +102,9 @@ int fsb_load_projector(fsb_ctx* ctx, int n_sub, int h1, int h2, const int64_t* c
  * pipeline._box_prompt + prepare_crops (priors.py:166-230,
  * pipeline.py:295-329): images (B, H, W, 3), kp (B, 22, 2) -> boxes
  * (B, 3, 4) f64, prompt (B, 8), crops (B, 3, S, S, 3) and optional int32
- * taps (B, 3, S, S, 4) = (x0, y0, x1, y1).  Bit-exact with the reference. */
+ * taps (B, 3, S, S, 4) = (x0, y0, x1, y1).  Bit-exact with the reference.
+ * `images` and `kp` may also be pinned host memory (cudaHostAlloc /
+ * torch pin_memory): K1 then reads only the crop footprints over PCIe. */
 int fsb_boxes_crops(fsb_ctx* ctx, const float* images, int B, int H, int W, const float* kp, double alpha, int S,
                     double* boxes, float* prompt, float* crops, int32_t* taps, void* stream);
 /* priors._body_box_from_keypoints (priors.py:166-176): kp (n, 22, 2) ->
@@ -161,6 +163,10 @@ int fsb_render(fsb_ctx* ctx, const void* scenes, int B, int H, int W, float* out
 /* reads (and optionally clears) the device non-finite flag; synchronises */
 int fsb_nonfinite(fsb_ctx* ctx, int* flag, int reset);
 int fsb_counters(const fsb_ctx* ctx, fsb_counters_t* out);
+/* bytes of frame data the crop gather (K1) has read from pinned host frames
+ * since the last reset, i.e. the bytes that crossed PCIe (only the crop
+ * footprints are read; HBM-resident frames are not counted); synchronises */
+int fsb_input_bytes(fsb_ctx* ctx, int64_t* total, int reset);
 /* number of kernels this context launched (graph replays count their nodes) */
 int64_t fsb_kernel_launches(const fsb_ctx* ctx);
 /* tcgen05 self-test: C (128 x N) f32 = A (128 x K, bf16 row-major) * B^T,

@@ -16,8 +16,9 @@
 
 // ---- kernels (other translation units) ------------------------------------
 cudaError_t launch_boxes_crops(const float* images, const float* kps, int B, int H, int W, int S, double alpha,
-                               double* boxes, float* prompt, float* crops, int32_t* taps, int* nonfinite,
-                               cudaStream_t st);
+                               bool host_frames, double* boxes, float* prompt, float* crops, int32_t* taps,
+                               int* nonfinite, unsigned long long* bytes_in, cudaStream_t st);
+cudaError_t init_attrs_crops();
 cudaError_t launch_bilinear(const float* img, int H, int W, int C, const float* grid, int64_t n, float* out,
                             int* nonfinite, cudaStream_t st);
 cudaError_t launch_encoder_f32(const float* crops, int ncrops, const EncW& w, float* feats, int* nonfinite,
@@ -105,6 +106,7 @@ struct fsb_ctx {
   int device = 0;
   std::string err;
   int* d_flag = nullptr;
+  unsigned long long* d_bytes_in = nullptr;  // frame bytes K1 read (HBM or, for host frames, PCIe)
   fsb_counters_t counters{};
   int64_t launches = 0;
   // decoder
@@ -310,11 +312,13 @@ int fsb_ctx_create(int device, fsb_ctx** out) {
   c->device = device;
   if (init_attrs_transformer() != cudaSuccess || init_attrs_transformer_tc() != cudaSuccess ||
       init_attrs_mlp_tc() != cudaSuccess || init_attrs_gemm_tc() != cudaSuccess ||
-      init_attrs_body() != cudaSuccess) {
+      init_attrs_body() != cudaSuccess || init_attrs_crops() != cudaSuccess) {
     delete c;
     return FSB_ERR_CUDA;
   }
-  if (cudaMalloc(&c->d_flag, sizeof(int)) != cudaSuccess || cudaMemset(c->d_flag, 0, sizeof(int)) != cudaSuccess) {
+  if (cudaMalloc(&c->d_flag, sizeof(int)) != cudaSuccess || cudaMemset(c->d_flag, 0, sizeof(int)) != cudaSuccess ||
+      cudaMalloc(&c->d_bytes_in, sizeof(unsigned long long)) != cudaSuccess ||
+      cudaMemset(c->d_bytes_in, 0, sizeof(unsigned long long)) != cudaSuccess) {
     delete c;
     return FSB_ERR_CUDA;
   }
@@ -326,6 +330,7 @@ void fsb_ctx_destroy(fsb_ctx* c) {
   if (!c) return;
   c->drop_graphs();
   if (c->d_flag) cudaFree(c->d_flag);
+  if (c->d_bytes_in) cudaFree(c->d_bytes_in);
   delete c;
 }
 
@@ -800,8 +805,22 @@ int fsb_boxes_crops(fsb_ctx* c, const float* images, int B, int H, int W, const 
   if (S < 2 || S > 512) return fail(c, FSB_ERR_USAGE, "out_size must be in [2, 512]");
   if (!(alpha > 0)) return fail(c, FSB_ERR_USAGE, "alpha must be positive");
   if (!boxes || !prompt) return fail(c, FSB_ERR_USAGE, "boxes and prompt outputs are required");
-  FSB_CUDA(c, launch_boxes_crops(images, kp, B, H, W, S, alpha, boxes, prompt, crops, taps, c->d_flag,
-                                 (cudaStream_t)stream));
+  bool host_frames = false;
+  if (B > 0) {
+    // frames and keypoints may live in HBM or in pinned (mapped) host memory;
+    // pageable host memory is not reachable from the device
+    for (int i = 0; i < 2; ++i) {
+      cudaPointerAttributes at{};
+      if (cudaPointerGetAttributes(&at, i ? (const void*)kp : (const void*)images) != cudaSuccess ||
+          at.type == cudaMemoryTypeUnregistered) {
+        cudaGetLastError();
+        return fail(c, FSB_ERR_USAGE, "boxes_crops: frames/keypoints must be device or pinned host memory");
+      }
+      if (i == 0) host_frames = at.type == cudaMemoryTypeHost;
+    }
+  }
+  FSB_CUDA(c, launch_boxes_crops(images, kp, B, H, W, S, alpha, host_frames, boxes, prompt, crops, taps, c->d_flag,
+                                 c->d_bytes_in, (cudaStream_t)stream));
   c->launches += B > 0;
   return FSB_OK;
 }
@@ -1146,6 +1165,16 @@ int fsb_nonfinite(fsb_ctx* c, int* flag, int reset) {
   FSB_CUDA(c, cudaMemcpy(&h, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost));
   if (reset) FSB_CUDA(c, cudaMemset(c->d_flag, 0, sizeof(int)));
   if (flag) *flag = h;
+  return FSB_OK;
+}
+
+int fsb_input_bytes(fsb_ctx* c, int64_t* total, int reset) {
+  if (!c || !total) return FSB_ERR_USAGE;
+  unsigned long long h = 0;
+  FSB_CUDA(c, cudaDeviceSynchronize());
+  FSB_CUDA(c, cudaMemcpy(&h, c->d_bytes_in, sizeof h, cudaMemcpyDeviceToHost));
+  if (reset) FSB_CUDA(c, cudaMemset(c->d_bytes_in, 0, sizeof h));
+  *total = (int64_t)h;
   return FSB_OK;
 }
 

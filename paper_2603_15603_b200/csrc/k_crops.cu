@@ -171,6 +171,176 @@ __global__ void __launch_bounds__(256) k_boxes_crops(
   }
 }
 
+// ---------------------------------------------------------------------------
+// Row-span streaming variant (the production K1).  A CTA owns `rows_per_cta`
+// consecutive output rows of one crop and walks them in sub-bands of RB = 4
+// rows.  For each sub-band the image rows it taps (y0 / y1 of each sample
+// row, each image row once when the band's rows are contiguous) are staged
+// in shared memory over the crop's x-span only: thread 0 plans the rows and
+// issues one cp.async.bulk (TMA 1-D) copy per row into one of two buffers,
+// so sub-band k+1 is in flight while sub-band k is blended from shared
+// memory.  It serves frames in pinned host memory, read in place over PCIe
+// so only the crop footprints cross the bus (measured 49 GB/s, PCIe-bound;
+// per-tap reads of host frames reach 45 GB/s).  Frames resident in HBM use
+// the per-tap kernel above, which is faster there (10.7 us vs 25 us for 32
+// frames: L1 absorbs the tap overlap and the grid is wider).  Arithmetic is
+// identical to k_boxes_crops (bit-exact).
+// ---------------------------------------------------------------------------
+#include "tc_sm100.cuh"
+
+namespace {
+constexpr int kStreamThreads = 256;
+constexpr int kRB = 4;        // sample rows per sub-band
+constexpr int kSlots = 2 * kRB;  // image rows per sub-band buffer
+
+struct BandPlan {
+  int nrows;
+  int slot0[kRB], slot1[kRB];
+  int rowoff[kSlots];  // floats between the staged row's first vector and pixel xa
+};
+}  // namespace
+
+__global__ void __launch_bounds__(kStreamThreads) k_crops_stream(
+    const float* __restrict__ images, const float* __restrict__ kps, int B, int H, int W, int S, double alpha,
+    int64_t img_stride, int rowcap4, int rows_per_cta, double* __restrict__ boxes_out,
+    float* __restrict__ prompt_out, float* __restrict__ crops_out, int32_t* __restrict__ taps_out, int* nonfinite,
+    unsigned long long* bytes_in) {
+  extern __shared__ __align__(128) float4 bufs4[];  // 2 buffers x kSlots rows x rowcap4
+  __shared__ FrameBoxes fb;
+  __shared__ float kp_s[2 * FSB_NJ];
+  __shared__ float gx[512], gy[512];
+  __shared__ BandPlan plan[2];
+  __shared__ __align__(8) uint64_t bar[2];
+  const int f = blockIdx.z, crop = blockIdx.y;
+  const int tid = threadIdx.x;
+  const int r_begin = blockIdx.x * rows_per_cta;
+  const int r_end = min(S, r_begin + rows_per_cta);
+  if (r_begin >= S) return;
+  if (tid < 2 * FSB_NJ) kp_s[tid] = kps[(int64_t)f * 2 * FSB_NJ + tid];
+  if (tid == 0) {
+    tc::mbar_init(&bar[0], 1);
+    tc::mbar_init(&bar[1], 1);
+    tc::mbar_fence_init();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    frame_boxes(kp_s, W, H, alpha, fb);
+    if (blockIdx.x == 0 && crop == 0) {
+      for (int c = 0; c < 3; ++c)
+        for (int e = 0; e < 4; ++e) boxes_out[((int64_t)f * 3 + c) * 4 + e] = fb.box[c][e];
+      for (int e = 0; e < 8; ++e) prompt_out[(int64_t)f * 8 + e] = fb.prompt[e];
+    }
+  }
+  __syncthreads();
+  const double* bx = fb.box[crop];
+  for (int i = tid; i < S; i += kStreamThreads) gx[i] = lin_f32(bx[0], bx[2], S, i);
+  for (int i = r_begin + tid; i < r_end; i += kStreamThreads) gy[i] = lin_f32(bx[1], bx[3], S, i);
+  __syncthreads();
+  if (crops_out == nullptr && taps_out == nullptr) return;
+  const float wmax = (float)(W - 1), hmax = (float)(H - 1);
+  const int nsub = (r_end - r_begin + kRB - 1) / kRB;
+  const int rowcap = rowcap4 * 4;
+  // x-span of the crop: taps of column 0 to column S-1 (the grid is monotone)
+  const int xlo = (int)floorf(fminf(fmaxf(gx[0], 0.0f), wmax));
+  const int xhi = min((int)floorf(fminf(fmaxf(gx[S - 1], 0.0f), wmax)) + 1, W - 1);
+  const int span = (xhi - xlo + 1) * 3;
+  const int64_t img0 = (int64_t)f * img_stride;
+  unsigned long long bytes = 0;  // thread 0 only
+
+  // thread 0: choose the image rows of sub-band k and start staging them
+  auto plan_band = [&](int k) {
+    const int b = k & 1;
+    BandPlan& pl = plan[b];
+    const int r0 = r_begin + k * kRB, nr = min(kRB, r_end - r0);
+    int y0s[kRB], y1s[kRB];
+    for (int i = 0; i < nr; ++i) {
+      const int y0 = (int)floorf(fminf(fmaxf(gy[r0 + i], 0.0f), hmax));
+      y0s[i] = y0;
+      y1s[i] = min(y0 + 1, H - 1);
+    }
+    const int ymin = y0s[0], ymax = y1s[nr - 1];
+    bool contiguous = ymax >= ymin && ymax - ymin + 1 <= kSlots;
+    for (int i = 0; i < nr; ++i) contiguous = contiguous && y0s[i] >= ymin && y1s[i] <= ymax;
+    int ys[kSlots];
+    int n = 0;
+    if (contiguous) {  // each image row of the band once
+      for (int y = ymin; y <= ymax; ++y) ys[n++] = y;
+      for (int i = 0; i < nr; ++i) {
+        pl.slot0[i] = y0s[i] - ymin;
+        pl.slot1[i] = y1s[i] - ymin;
+      }
+    } else {
+      for (int i = 0; i < nr; ++i) {
+        ys[n] = y0s[i];
+        pl.slot0[i] = n++;
+        ys[n] = y1s[i];
+        pl.slot1[i] = n++;
+      }
+    }
+    pl.nrows = n;
+    uint32_t tx = 0;
+    int64_t v0s[kSlots];
+    int nvs[kSlots];
+    for (int sl = 0; sl < n; ++sl) {
+      const int64_t e0 = img0 + ((int64_t)ys[sl] * W + xlo) * 3;  // first float of the span
+      const int64_t v0 = e0 >> 2, v1 = (e0 + span + 3) >> 2;
+      pl.rowoff[sl] = (int)(e0 - 4 * v0);
+      v0s[sl] = v0;
+      nvs[sl] = (int)(v1 - v0);
+      tx += (uint32_t)(v1 - v0) * 16u;
+    }
+    bytes += tx;
+    tc::mbar_expect_tx(&bar[b], tx);
+    for (int sl = 0; sl < n; ++sl)
+      tc::bulk_g2s(bufs4 + (b * kSlots + sl) * rowcap4, reinterpret_cast<const float4*>(images) + v0s[sl],
+                   (uint32_t)nvs[sl] * 16u, &bar[b]);
+  };
+
+  if (tid == 0) {
+    plan_band(0);
+    if (nsub > 1) plan_band(1);
+  }
+  __syncthreads();
+  for (int k = 0; k < nsub; ++k) {
+    const int b = k & 1;
+    tc::mbar_wait(&bar[b], (uint32_t)((k >> 1) & 1));
+    const BandPlan& pl = plan[b];
+    const float* rows = reinterpret_cast<const float*>(bufs4) + (size_t)b * kSlots * rowcap;
+    const int r0 = r_begin + k * kRB, nr = min(kRB, r_end - r0);
+    for (int p = tid; p < nr * S; p += kStreamThreads) {
+      const int i = p / S, c = p - i * S, r = r0 + i;
+      const float x = fminf(fmaxf(gx[c], 0.0f), wmax);
+      const float y = fminf(fmaxf(gy[r], 0.0f), hmax);
+      const int x0 = (int)floorf(x), y0 = (int)floorf(y);
+      const int x1 = min(x0 + 1, W - 1), y1 = min(y0 + 1, H - 1);
+      const float fx = __fsub_rn(x, (float)x0), fy = __fsub_rn(y, (float)y0);
+      const float ofx = __fsub_rn(1.0f, fx), ofy = __fsub_rn(1.0f, fy);
+      const int s0 = pl.slot0[i], s1 = pl.slot1[i];
+      const float* ra = rows + s0 * rowcap + pl.rowoff[s0] - xlo * 3;
+      const float* rb = rows + s1 * rowcap + pl.rowoff[s1] - xlo * 3;
+      const int64_t o = ((((int64_t)f * 3 + crop) * S + r) * S + c);
+      if (taps_out != nullptr) {
+        int32_t* t = taps_out + o * 4;
+        t[0] = x0; t[1] = y0; t[2] = x1; t[3] = y1;
+      }
+      if (crops_out != nullptr) {
+#pragma unroll
+        for (int ch = 0; ch < 3; ++ch) {
+          const float a = ra[x0 * 3 + ch], bb = ra[x1 * 3 + ch], cc = rb[x0 * 3 + ch], d = rb[x1 * 3 + ch];
+          const float top = __fadd_rn(__fmul_rn(a, ofx), __fmul_rn(bb, fx));
+          const float bot = __fadd_rn(__fmul_rn(cc, ofx), __fmul_rn(d, fx));
+          const float v = __fadd_rn(__fmul_rn(top, ofy), __fmul_rn(bot, fy));
+          flag_nonfinite(nonfinite, v);
+          crops_out[o * 3 + ch] = v;
+        }
+      }
+    }
+    __syncthreads();  // buffer b and its plan are free again
+    if (tid == 0 && k + 2 < nsub) plan_band(k + 2);
+  }
+  if (tid == 0 && bytes_in != nullptr) atomicAdd(bytes_in, bytes);
+}
+
 // Stand-alone numkit.bilinear_sample (numkit.py:136-154): image (H, W, C),
 // grid (n, 2) of (x, y) -> out (n, C).  One thread per sample point.
 __global__ void k_bilinear(const float* __restrict__ img, int H, int W, int C, const float* __restrict__ grid,
@@ -194,14 +364,39 @@ __global__ void k_bilinear(const float* __restrict__ img, int H, int W, int C, c
   }
 }
 
+static size_t stream_smem(int rowcap4) { return (size_t)2 * kSlots * rowcap4 * sizeof(float4); }
+constexpr size_t kStreamSmemCap = 120 * 1024;
+
+cudaError_t init_attrs_crops() {
+  return cudaFuncSetAttribute(k_crops_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kStreamSmemCap);
+}
+
+// host_frames: `images` is pinned (mapped) host memory; bytes_in (nullable)
+// then accumulates the bytes K1 read over PCIe
 cudaError_t launch_boxes_crops(const float* images, const float* kps, int B, int H, int W, int S, double alpha,
-                               double* boxes, float* prompt, float* crops, int32_t* taps, int* nonfinite,
-                               cudaStream_t st) {
+                               bool host_frames, double* boxes, float* prompt, float* crops, int32_t* taps,
+                               int* nonfinite, unsigned long long* bytes_in, cudaStream_t st) {
   if (B == 0) return cudaSuccess;
   if (S < 2 || S > 512) return cudaErrorInvalidValue;
-  dim3 grid((S + kRowsPerCTA - 1) / kRowsPerCTA, 3, B);
-  k_boxes_crops<<<grid, 256, 0, st>>>(images, kps, B, H, W, S, alpha, (int64_t)H * W * 3, boxes, prompt, crops,
-                                      taps, nonfinite);
+  const int64_t stride = (int64_t)H * W * 3;
+  const int rowcap4 = (W * 3 + 7) / 4 + 1;
+  const bool aligned = (reinterpret_cast<uintptr_t>(images) & 15u) == 0;
+  if (host_frames && aligned && stream_smem(rowcap4) <= kStreamSmemCap) {
+    // enough CTAs for ~2 per SM: bands of rows_per_cta (a multiple of kRB)
+    const int nsub_total = (S + kRB - 1) / kRB;
+    int bands = (296 + 3 * B - 1) / (3 * B);
+    bands = max(1, min(bands, nsub_total));
+    const int rows_per_cta = ((nsub_total + bands - 1) / bands) * kRB;
+    bands = (S + rows_per_cta - 1) / rows_per_cta;
+    dim3 grid(bands, 3, B);
+    k_crops_stream<<<grid, kStreamThreads, stream_smem(rowcap4), st>>>(
+        images, kps, B, H, W, S, alpha, stride, rowcap4, rows_per_cta, boxes, prompt, crops, taps, nonfinite,
+        bytes_in);
+  } else {  // HBM-resident (or very wide / unaligned host) frames: per-tap reads
+    dim3 grid((S + kRowsPerCTA - 1) / kRowsPerCTA, 3, B);
+    k_boxes_crops<<<grid, 256, 0, st>>>(images, kps, B, H, W, S, alpha, stride, boxes, prompt, crops, taps,
+                                        nonfinite);
+  }
   return cudaGetLastError();
 }
 

@@ -293,8 +293,9 @@ class Pipeline:
     # -- batched entry -------------------------------------------------------
     def run_batch(self, images, keypoints, config=None, outputs=None, precision=None, sync=True):
         """B frames in one call.  images (B, H, W, 3) float32, keypoints
-        (B, 22, 2) float32 (the stub detector's sigma = 0 keypoints), numpy or
-        CUDA tensors.  Returns a dict of CUDA tensors: boxes, prompt,
+        (B, 22, 2) float32 (the stub detector's sigma = 0 keypoints), numpy,
+        CUDA tensors or pinned host tensors (read in place: only the crop
+        footprints cross PCIe).  Returns a dict of CUDA tensors: boxes, prompt,
         body_params, body_cam, hand_rots, merged and, with the SMPL tail,
         v_mhr, theta, j_smpl.  Rows equal per-frame `run` results."""
         cfg = config if config is not None else fast_config()
@@ -303,8 +304,8 @@ class Pipeline:
             raise UsageError("run_batch takes detector keypoints directly; add noise before calling")
         ctx = self.context()
         torch = ctx.torch
-        img, _ = runtime.to_device(images, torch.float32, torch, self.device)
-        kp, _ = runtime.to_device(keypoints, torch.float32, torch, self.device)
+        img, _ = runtime.frame_source(images, torch.float32, torch, self.device)
+        kp, _ = runtime.frame_source(keypoints, torch.float32, torch, self.device)
         if img.ndim != 4 or img.shape[3] != 3:
             raise ShapeError("images must be (B, H, W, 3), got %r" % (tuple(img.shape),))
         b, h, w = img.shape[:3]
@@ -355,11 +356,11 @@ class Pipeline:
         s = self.crop_size
         crops = out.get("crops")
         if crops is None:
-            crops = torch.empty((b, 3, s, s, 3), dtype=torch.float32, device=img.device)
+            crops = torch.empty((b, 3, s, s, 3), dtype=torch.float32, device=torch.device("cuda", self.device))
         feats = out.get("feats")
         if feats is None:
             feats = torch.empty((b, 3, self.decoder.n_tokens, self.decoder.config.dim), dtype=torch.float32,
-                                device=img.device)
+                                device=torch.device("cuda", self.device))
         ctx.check(ctx.lib.fsb_boxes_crops(ctx.h, runtime.ptr(img), b, h, w, runtime.ptr(kp), float(cfg.alpha), s,
                                           runtime.ptr(out["boxes"]), runtime.ptr(out["prompt"]), runtime.ptr(crops),
                                           None, ctx.stream), "boxes_crops")

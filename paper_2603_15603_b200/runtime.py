@@ -76,6 +76,7 @@ _SIGS = {
     "fsb_render": (_i, [_p, _p, _i, _i, _i, _p, _p]),
     "fsb_nonfinite": (_i, [_p, ctypes.POINTER(_i), _i]),
     "fsb_counters": (_i, [_p, ctypes.POINTER(CountersC)]),
+    "fsb_input_bytes": (_i, [_p, ctypes.POINTER(ctypes.c_int64), _i]),
     "fsb_kernel_launches": (_i64, [_p]),
     "fsb_selftest_umma": (_i, [_p, _p, _p, _i, _i, _p, _p]),
 }
@@ -195,6 +196,12 @@ class Context:
         self.check(self.lib.fsb_counters(self.h, ctypes.byref(c)))
         return {f: int(getattr(c, f)) for f, _ in CountersC._fields_}
 
+    def input_bytes(self, reset=True):
+        """Frame bytes the crop gather read since the last reset (synchronises)."""
+        n = ctypes.c_int64(0)
+        self.check(self.lib.fsb_input_bytes(self.h, ctypes.byref(n), int(reset)), "input_bytes")
+        return int(n.value)
+
     def reserve(self, frames):
         self.check(self.lib.fsb_reserve(self.h, int(frames)), "reserve")
 
@@ -258,6 +265,17 @@ def to_device(x, dtype, torch, device=None):
     a = np.ascontiguousarray(x, dtype={torch.float32: np.float32, torch.float64: np.float64,
                                        torch.int32: np.int32, torch.int64: np.int64}[dtype])
     return torch.from_numpy(a).to(torch.device("cuda", device), non_blocking=False), True
+
+
+def frame_source(x, dtype, torch, device=None):
+    """Like to_device, but a pinned (page-locked) host tensor of the right
+    dtype is passed through as-is: the crop gather reads only the crop
+    footprints of such frames in place over PCIe instead of copying whole
+    frames to HBM first."""
+    if (isinstance(x, torch.Tensor) and x.device.type == "cpu" and x.dtype == dtype and x.is_contiguous()
+            and x.is_pinned()):
+        return x, False
+    return to_device(x, dtype, torch, device)
 
 
 def out_like(t, was_numpy):

@@ -90,6 +90,89 @@ def test_boxes_crops_bitexact(torch, pipe, frames, golden):
     assert np.array_equal(prompt, golden["prompt"][:b])
 
 
+def _gather(torch, ctx, imgs, kps, S=64, host=False):
+    """fsb_boxes_crops on device (or pinned host) frames -> numpy outputs."""
+    from paper_2603_15603_b200 import runtime
+
+    b, h, w = imgs.shape[:3]
+    if host:
+        dimg = torch.from_numpy(np.ascontiguousarray(imgs)).pin_memory()
+        dkp = torch.from_numpy(np.ascontiguousarray(kps)).pin_memory()
+    else:
+        dimg = torch.from_numpy(np.ascontiguousarray(imgs)).cuda()
+        dkp = torch.from_numpy(np.ascontiguousarray(kps)).cuda()
+    boxes = torch.empty((b, 3, 4), dtype=torch.float64, device="cuda")
+    prompt = torch.empty((b, 8), dtype=torch.float32, device="cuda")
+    crops = torch.empty((b, 3, S, S, 3), dtype=torch.float32, device="cuda")
+    ctx.input_bytes(reset=True)
+    ctx.check(ctx.lib.fsb_boxes_crops(ctx.h, runtime.ptr(dimg), b, h, w, runtime.ptr(dkp), 3.0, S,
+                                      runtime.ptr(boxes), runtime.ptr(prompt), runtime.ptr(crops), None,
+                                      ctx.stream))
+    nbytes = ctx.input_bytes(reset=True)
+    return boxes.cpu().numpy(), prompt.cpu().numpy(), crops.cpu().numpy(), nbytes
+
+
+def test_boxes_crops_host_frames(torch, pipe, frames):
+    """Frames in pinned host memory are gathered in place (only the crop
+    footprints cross PCIe) with bit-identical results."""
+    ctx = _ctx(pipe)
+    imgs = np.stack([f[0] for f in frames])
+    kps = np.stack([f[1] for f in frames])
+    bd, pd, cd, nd = _gather(torch, ctx, imgs, kps)
+    bh, ph, ch, nh = _gather(torch, ctx, imgs, kps, host=True)
+    assert np.array_equal(bd, bh) and np.array_equal(pd, ph) and np.array_equal(cd, ch)
+    assert nd == 0 and 0 < nh < imgs.nbytes // 2, (nd, nh, imgs.nbytes)  # only host reads are counted
+    for i in range(len(frames)):
+        assert np.array_equal(ch[i], orc.frame_crops(imgs[i], kps[i], 64)[3])
+
+
+def test_boxes_crops_host_frames_through_run_batch(torch, pipe, frames):
+    ctx = _ctx(pipe)
+    imgs = np.stack([f[0] for f in frames[:4]])
+    kps = np.stack([f[1] for f in frames[:4]])
+    dev = pipe.run_batch(imgs, kps)
+    host = pipe.run_batch(torch.from_numpy(imgs).pin_memory(), torch.from_numpy(kps).pin_memory())
+    for k in ("boxes", "merged", "theta", "j_smpl"):
+        assert torch.equal(dev[k], host[k]), k
+    ctx.input_bytes(reset=True)
+
+
+def test_pageable_host_frames_rejected(torch, pipe, frames):
+    from paper_2603_15603_b200 import runtime
+    from paper_2603_15603_b200.numkit import UsageError
+
+    ctx = _ctx(pipe)
+    img = torch.from_numpy(frames[0][0][None].copy())  # pageable
+    kp = torch.from_numpy(frames[0][1][None].copy()).cuda()
+    boxes = torch.empty((1, 3, 4), dtype=torch.float64, device="cuda")
+    prompt = torch.empty((1, 8), device="cuda")
+    with pytest.raises(UsageError):
+        ctx.check(ctx.lib.fsb_boxes_crops(ctx.h, runtime.ptr(img), 1, 512, 512, runtime.ptr(kp), 3.0, 64,
+                                          runtime.ptr(boxes), runtime.ptr(prompt), None, None, ctx.stream))
+
+
+@pytest.mark.parametrize("h,w,S", [(97, 130, 64), (240, 321, 48), (64, 1500, 64), (48, 9001, 32), (512, 512, 7)])
+def test_boxes_crops_odd_and_wide_frames(torch, pipe, golden, h, w, S):
+    """Odd widths (rows not 16-byte aligned), frames wider than the staged
+    path's shared-memory rows (per-tap path), tiny and non-multiple-of-4
+    crop sizes; keypoints from the stress set squeezed into the frame."""
+    ctx = _ctx(pipe)
+    rng = np.random.default_rng(h * w + S)
+    n = 6
+    imgs = rng.random((n, h, w, 3)).astype(np.float32)
+    skp = np.asarray(golden["stress_kp"][:n], np.float32)
+    kps = (skp / np.float32(512.0) * np.array([w, h], np.float32)).astype(np.float32)
+    kps = np.clip(kps, 0, np.array([w - 1, h - 1], np.float32)).astype(np.float32)
+    for host in (False, True):
+        boxes, prompt, crops, _ = _gather(torch, ctx, imgs, kps, S=S, host=host)
+        for i in range(n):
+            bb, hands, pr, cr = orc.frame_crops(imgs[i], kps[i], S)
+            assert np.array_equal(boxes[i, 0], np.array(bb))
+            assert np.array_equal(boxes[i, 1:], np.array(hands))
+            assert np.array_equal(prompt[i], pr)
+            assert np.array_equal(crops[i], cr), (i, host)
+
+
 def test_box_goldens_all_scenes_and_stress(torch, golden):
     from paper_2603_15603_b200 import priors as pr
 
