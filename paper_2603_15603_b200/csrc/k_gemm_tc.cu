@@ -2,11 +2,14 @@
 //   C[M, N] = A[M, K] . W[N, K]^T  (+ fused epilogue)
 // A and W are row-major bf16 (K contiguous, i.e. both operands K-major).
 //
-// One CTA computes a 128 x BN tile.  Warp 0 is the TMA producer (128-byte
-// swizzled boxes of 64 K-elements), warp 1 issues tcgen05.mma from one lane
-// into a TMEM accumulator, warps 2-5 drain TMEM through the epilogue; a
-// STAGES-deep ring of full/empty mbarriers keeps TMA, MMA and the previous
-// tile's epilogue overlapped.  Epilogues (decoder.py:247-257 semantics):
+// Persistent kernel: one CTA per SM walks the 128 x BN output tiles
+// (N-tile fastest, so CTAs running at the same time share A tiles in L2).
+// Warp 0 is the TMA producer (128-byte swizzled boxes of 64 K-elements),
+// warp 1 issues tcgen05.mma from one lane, warps 2-5 drain TMEM through the
+// epilogue.  A STAGES-deep ring of full/empty mbarriers feeds the tensor
+// core, and the accumulator is double-buffered in TMEM (2 x BN columns):
+// the epilogue of tile i runs while the MMAs of tile i+1 accumulate into the
+// other buffer.  Epilogues (decoder.py:247-257 semantics):
 //   EPI_BIAS_BF16   out_bf16 = acc + bias                       (Q|K|V)
 //   EPI_RELU_BF16   out_bf16 = relu(acc + bias)                 (MLP W1)
 //   EPI_RESID_F32   x_f32   += acc + bias                       (Wo, W2)
@@ -23,6 +26,44 @@
 namespace {
 constexpr int BM = 128, BK = 64, STAGES = 4;
 constexpr int GEMM_THREADS = 192;
+constexpr int EPI_WARPS = 4;
+}
+
+template <int BN>
+__device__ __forceinline__ void gemm_epilogue_chunk(const GemmEpi& epi, int row, int col, const float* v) {
+  // 32 consecutive columns [col, col + 32) of one row
+  float b[32];
+#pragma unroll
+  for (int i = 0; i < 32; i += 4) {
+    const float4 q = __ldg(reinterpret_cast<const float4*>(epi.bias + col + i));
+    b[i] = v[i] + q.x; b[i + 1] = v[i + 1] + q.y; b[i + 2] = v[i + 2] + q.z; b[i + 3] = v[i + 3] + q.w;
+  }
+  if (epi.kind == EPI_BIAS_BF16 || epi.kind == EPI_RELU_BF16) {
+    if (epi.kind == EPI_RELU_BF16)
+#pragma unroll
+      for (int i = 0; i < 32; ++i) b[i] = fmaxf(b[i], 0.0f);
+    uint4* dst = reinterpret_cast<uint4*>(epi.out_bf16 + (size_t)row * epi.ldo + col);
+#pragma unroll
+    for (int g = 0; g < 4; ++g)
+      dst[g] = make_uint4(tc::pack_bf16(b[8 * g], b[8 * g + 1]), tc::pack_bf16(b[8 * g + 2], b[8 * g + 3]),
+                          tc::pack_bf16(b[8 * g + 4], b[8 * g + 5]), tc::pack_bf16(b[8 * g + 6], b[8 * g + 7]));
+  } else {
+    float4* x = reinterpret_cast<float4*>(epi.x_f32 + (size_t)row * epi.ldo + col);
+    float4 r[8];
+    if (epi.kind == EPI_EMBED_F32) {
+      const float4* p = reinterpret_cast<const float4*>(epi.pos + (size_t)(row % epi.T) * epi.ldo + col);
+#pragma unroll
+      for (int g = 0; g < 8; ++g) r[g] = __ldg(p + g);
+    } else {
+#pragma unroll
+      for (int g = 0; g < 8; ++g) r[g] = x[g];
+    }
+#pragma unroll
+    for (int g = 0; g < 8; ++g) {
+      r[g].x += b[4 * g]; r[g].y += b[4 * g + 1]; r[g].z += b[4 * g + 2]; r[g].w += b[4 * g + 3];
+      x[g] = r[g];
+    }
+  }
 }
 
 template <int BN>
@@ -33,22 +74,27 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   // 1024-byte alignment for the 128B swizzle atoms
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   constexpr uint32_t A_BYTES = BM * BK * 2, B_BYTES = BN * BK * 2, STAGE_BYTES = A_BYTES + B_BYTES;
-  __shared__ uint64_t full[STAGES], empty[STAGES], done;
+  constexpr uint32_t TMEM_COLS = 2 * BN;  // two accumulator buffers
+  __shared__ uint64_t full[STAGES], empty[STAGES], acc_full[2], acc_empty[2];
   __shared__ uint32_t tmem_base;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
   const int nk = (K + BK - 1) / BK;
+  const int ntn = (N + BN - 1) / BN, ntm = (M + BM - 1) / BM;
+  const int ntiles = ntm * ntn;
   if (threadIdx.x == 0) {
     for (int s = 0; s < STAGES; ++s) {
       tc::mbar_init(&full[s], 1);
       tc::mbar_init(&empty[s], 1);
     }
-    tc::mbar_init(&done, 1);
+    for (int b = 0; b < 2; ++b) {
+      tc::mbar_init(&acc_full[b], 1);
+      tc::mbar_init(&acc_empty[b], EPI_WARPS);
+    }
     tc::mbar_fence_init();
     tc::prefetch_tmap(&tmA);
     tc::prefetch_tmap(&tmB);
   }
-  if (warp == 1) tc::tmem_alloc(&tmem_base, BN < 32 ? 32 : BN);
+  if (warp == 1) tc::tmem_alloc(&tmem_base, TMEM_COLS);
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
@@ -56,80 +102,68 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 
   if (warp == 0 && lane == 0) {
     // TMA producer
-    for (int kb = 0; kb < nk; ++kb) {
-      const int s = kb % STAGES;
-      if (kb >= STAGES) tc::mbar_wait(&empty[s], (uint32_t)(((kb / STAGES) - 1) & 1));
-      uint8_t* sa = smem + s * STAGE_BYTES;
-      tc::mbar_expect_tx(&full[s], STAGE_BYTES);
-      tc::tma_load_2d(sa, &tmA, kb * BK, m0, &full[s]);
-      tc::tma_load_2d(sa + A_BYTES, &tmB, kb * BK, n0, &full[s]);
+    int it = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      const int m0 = (t / ntn) * BM, n0 = (t % ntn) * BN;
+      for (int kb = 0; kb < nk; ++kb, ++it) {
+        const int s = it % STAGES;
+        if (it >= STAGES) tc::mbar_wait(&empty[s], (uint32_t)(((it / STAGES) - 1) & 1));
+        uint8_t* sa = smem + s * STAGE_BYTES;
+        tc::mbar_expect_tx(&full[s], STAGE_BYTES);
+        tc::tma_load_2d(sa, &tmA, kb * BK, m0, &full[s]);
+        tc::tma_load_2d(sa + A_BYTES, &tmB, kb * BK, n0, &full[s]);
+      }
     }
   } else if (warp == 1 && lane == 0) {
     // MMA issuer
     const uint32_t idesc = tc::idesc_bf16(BM, BN);
     const uint32_t sbase = tc::smem_u32(smem);
-    for (int kb = 0; kb < nk; ++kb) {
-      const int s = kb % STAGES;
-      tc::mbar_wait(&full[s], (uint32_t)((kb / STAGES) & 1));
+    int it = 0, tc_count = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tc_count) {
+      const int buf = tc_count & 1;
+      if (tc_count >= 2) tc::mbar_wait(&acc_empty[buf], (uint32_t)(((tc_count >> 1) - 1) & 1));
       tc::fence_after();
-      const uint32_t a = sbase + s * STAGE_BYTES, b = a + A_BYTES;
+      const uint32_t acc = tmem + (uint32_t)(buf * BN);
+      for (int kb = 0; kb < nk; ++kb, ++it) {
+        const int s = it % STAGES;
+        tc::mbar_wait(&full[s], (uint32_t)((it / STAGES) & 1));
+        tc::fence_after();
+        const uint32_t a = sbase + s * STAGE_BYTES, b = a + A_BYTES;
 #pragma unroll
-      for (int k = 0; k < BK / 16; ++k)
-        tc::mma_bf16(tmem, tc::sw128_kmajor_desc(a + 32 * k), tc::sw128_kmajor_desc(b + 32 * k), idesc,
-                     (kb | k) != 0);
-      tc::mma_commit(&empty[s]);  // frees the stage once these MMAs have read it
+        for (int k = 0; k < BK / 16; ++k)
+          tc::mma_bf16(acc, tc::sw128_kmajor_desc(a + 32 * k), tc::sw128_kmajor_desc(b + 32 * k), idesc,
+                       (kb | k) != 0);
+        tc::mma_commit(&empty[s]);  // frees the stage once these MMAs have read it
+      }
+      tc::mma_commit(&acc_full[buf]);  // accumulator of this tile complete
     }
-    tc::mma_commit(&done);
   } else if (warp >= 2) {
     // epilogue: warp w reads TMEM lanes 32 * (w % 4) .. +31 (rows of the tile)
-    tc::mbar_wait(&done, 0);
-    tc::fence_after();
     const int quad = warp % 4;
-    const int row = m0 + quad * 32 + lane;
-    const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16);
+    int tc_count = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tc_count) {
+      const int buf = tc_count & 1;
+      const int m0 = (t / ntn) * BM, n0 = (t % ntn) * BN;
+      tc::mbar_wait(&acc_full[buf], (uint32_t)((tc_count >> 1) & 1));
+      tc::fence_after();
+      const int row = m0 + quad * 32 + lane;
+      const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(buf * BN);
 #pragma unroll 1
-    for (int c = 0; c < BN; c += 16) {
-      float v[16];
-      tc::tmem_ld16(taddr + c, v);
-      const int col = n0 + c;
-      if (row >= M || col >= N) continue;
-#pragma unroll
-      for (int i = 0; i < 16; ++i) v[i] += __ldg(epi.bias + col + i);
-      if (epi.kind == EPI_BIAS_BF16 || epi.kind == EPI_RELU_BF16) {
-        if (epi.kind == EPI_RELU_BF16)
-#pragma unroll
-          for (int i = 0; i < 16; ++i) v[i] = fmaxf(v[i], 0.0f);
-        uint4 u0, u1;
-        u0.x = tc::pack_bf16(v[0], v[1]); u0.y = tc::pack_bf16(v[2], v[3]);
-        u0.z = tc::pack_bf16(v[4], v[5]); u0.w = tc::pack_bf16(v[6], v[7]);
-        u1.x = tc::pack_bf16(v[8], v[9]); u1.y = tc::pack_bf16(v[10], v[11]);
-        u1.z = tc::pack_bf16(v[12], v[13]); u1.w = tc::pack_bf16(v[14], v[15]);
-        uint4* dst = reinterpret_cast<uint4*>(epi.out_bf16 + (size_t)row * epi.ldo + col);
-        dst[0] = u0;
-        dst[1] = u1;
-      } else {
-        float* x = epi.x_f32 + (size_t)row * epi.ldo + col;
-        if (epi.kind == EPI_EMBED_F32) {
-          const float* p = epi.pos + (size_t)(row % epi.T) * N + col;
-#pragma unroll
-          for (int i = 0; i < 16; i += 4) {
-            const float4 q = __ldg(reinterpret_cast<const float4*>(p + i));
-            *reinterpret_cast<float4*>(x + i) = make_float4(v[i] + q.x, v[i + 1] + q.y, v[i + 2] + q.z, v[i + 3] + q.w);
-          }
-        } else {
-#pragma unroll
-          for (int i = 0; i < 16; i += 4) {
-            float4 r = *reinterpret_cast<float4*>(x + i);
-            r.x += v[i]; r.y += v[i + 1]; r.z += v[i + 2]; r.w += v[i + 3];
-            *reinterpret_cast<float4*>(x + i) = r;
-          }
-        }
+      for (int c = 0; c < BN; c += 32) {
+        float v[32];
+        tc::tmem_ld32(taddr + c, v);
+        const int col = n0 + c;
+        if (row < M && col < N) gemm_epilogue_chunk<BN>(epi, row, col, v);
       }
+      // this warp's TMEM reads are complete: hand the buffer back to the MMA warp
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&acc_empty[buf]);
     }
   }
   tc::fence_before();
   __syncthreads();
-  if (warp == 1) tc::tmem_dealloc(tmem, BN < 32 ? 32 : BN);
+  if (warp == 1) tc::tmem_dealloc(tmem, TMEM_COLS);
 }
 
 // ---------------------------------------------------------------------------
@@ -174,12 +208,12 @@ cudaError_t init_attrs_gemm_tc() {
   return e;
 }
 
-// A (M x K, lda), W (N x K, ldw): bf16 row-major.  N must be a multiple of 16,
+// A (M x K, lda), W (N x K, ldw): bf16 row-major.  N must be a multiple of 32,
 // K a multiple of 8 (16-byte TMA strides).
 cudaError_t launch_gemm_tc(const __nv_bfloat16* A, int lda, const __nv_bfloat16* W, int ldw, int M, int N, int K,
                            const GemmEpi& epi, cudaStream_t st) {
   if (M == 0 || N == 0) return cudaSuccess;
-  if (N % 16 || K % 8 || lda % 8 || ldw % 8) return cudaErrorInvalidValue;
+  if (N % 32 || K % 8 || lda % 8 || ldw % 8) return cudaErrorInvalidValue;
   static bool attrs = false;
   if (!attrs) {
     cudaError_t e = init_attrs_gemm_tc();
@@ -190,7 +224,14 @@ cudaError_t launch_gemm_tc(const __nv_bfloat16* A, int lda, const __nv_bfloat16*
   const int BN = (N % 256 == 0) ? 256 : 128;
   if (!make_tmap_bf16(&ta, A, M, K, lda, BM) || !make_tmap_bf16(&tb, W, N, K, ldw, BN))
     return cudaErrorInvalidValue;
-  dim3 grid((N + BN - 1) / BN, (M + BM - 1) / BM);
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = 148;
+  }
+  const int64_t tiles = (int64_t)((N + BN - 1) / BN) * ((M + BM - 1) / BM);
+  const dim3 grid((unsigned)(tiles < sms ? tiles : sms));  // persistent: one CTA per SM
   if (BN == 256)
     k_gemm_tc<256><<<grid, GEMM_THREADS, gemm_smem<256>(), st>>>(ta, tb, M, N, K, epi);
   else

@@ -15,7 +15,8 @@ def _bf16(rng, shape, scale=1.0):
 
 
 @pytest.mark.parametrize("m,n,k,kind", [(300, 256, 512, 0), (128, 384, 64, 1), (700, 1024, 1024, 2),
-                                        (576 * 2, 1024, 768, 3)])
+                                        (576 * 2, 1024, 768, 3), (20000, 768, 128, 2), (5000, 3072, 64, 0),
+                                        (3000, 96, 256, 1)])
 def test_tma_gemm(m, n, k, kind):
     """TMA (128B swizzle) + tcgen05 GEMM with each fused epilogue."""
     import ctypes
