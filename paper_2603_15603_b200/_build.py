@@ -28,6 +28,10 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxe
          "-Xptxas", "-warn-spills", "-I", os.path.join(ROOT, "include")]
 if os.environ.get("FSB_PROFILE"):  # cycle-attribution counters in the tcgen05 kernels
     FLAGS.append("-DFSB_PROFILE")
+if os.environ.get("FSB_EXTRA_FLAGS"):  # experiments: extra -D flags
+    FLAGS.extend(os.environ["FSB_EXTRA_FLAGS"].split())
+if os.environ.get("FSB_HANG_DEBUG"):  # mbarrier waits time out and report instead of hanging
+    FLAGS.append("-DFSB_HANG_DEBUG")
 
 
 def _sources():

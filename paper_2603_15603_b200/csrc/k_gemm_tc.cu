@@ -100,22 +100,25 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   tc::fence_after();
   const uint32_t tmem = tmem_base;
 
-  if (warp == 0 && lane == 0) {
-    // TMA producer
+  if (warp == 0) {
+    // TMA producer: the whole warp walks the schedule, lane 0 issues
     int it = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
       const int m0 = (t / ntn) * BM, n0 = (t % ntn) * BN;
       for (int kb = 0; kb < nk; ++kb, ++it) {
         const int s = it % STAGES;
         if (it >= STAGES) tc::mbar_wait(&empty[s], (uint32_t)(((it / STAGES) - 1) & 1));
-        uint8_t* sa = smem + s * STAGE_BYTES;
-        tc::mbar_expect_tx(&full[s], STAGE_BYTES);
-        tc::tma_load_2d(sa, &tmA, kb * BK, m0, &full[s]);
-        tc::tma_load_2d(sa + A_BYTES, &tmB, kb * BK, n0, &full[s]);
+        if (lane == 0) {
+          uint8_t* sa = smem + s * STAGE_BYTES;
+          tc::mbar_expect_tx(&full[s], STAGE_BYTES);
+          tc::tma_load_2d(sa, &tmA, kb * BK, m0, &full[s]);
+          tc::tma_load_2d(sa + A_BYTES, &tmB, kb * BK, n0, &full[s]);
+        }
+        __syncwarp();
       }
     }
-  } else if (warp == 1 && lane == 0) {
-    // MMA issuer
+  } else if (warp == 1) {
+    // MMA issuer: the whole warp walks the schedule, lane 0 issues
     const uint32_t idesc = tc::idesc_bf16(BM, BN);
     const uint32_t sbase = tc::smem_u32(smem);
     int it = 0, tc_count = 0;
@@ -128,14 +131,18 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         const int s = it % STAGES;
         tc::mbar_wait(&full[s], (uint32_t)((it / STAGES) & 1));
         tc::fence_after();
-        const uint32_t a = sbase + s * STAGE_BYTES, b = a + A_BYTES;
+        if (lane == 0) {
+          const uint32_t a = sbase + s * STAGE_BYTES, b = a + A_BYTES;
 #pragma unroll
-        for (int k = 0; k < BK / 16; ++k)
-          tc::mma_bf16(acc, tc::sw128_kmajor_desc(a + 32 * k), tc::sw128_kmajor_desc(b + 32 * k), idesc,
-                       (kb | k) != 0);
-        tc::mma_commit(&empty[s]);  // frees the stage once these MMAs have read it
+          for (int k = 0; k < BK / 16; ++k)
+            tc::mma_bf16(acc, tc::sw128_kmajor_desc(a + 32 * k), tc::sw128_kmajor_desc(b + 32 * k), idesc,
+                         (kb | k) != 0);
+          tc::mma_commit(&empty[s]);  // frees the stage once these MMAs have read it
+        }
+        __syncwarp();
       }
-      tc::mma_commit(&acc_full[buf]);  // accumulator of this tile complete
+      if (lane == 0) tc::mma_commit(&acc_full[buf]);  // accumulator of this tile complete
+      __syncwarp();
     }
   } else if (warp >= 2) {
     // epilogue: warp w reads TMEM lanes 32 * (w % 4) .. +31 (rows of the tile)

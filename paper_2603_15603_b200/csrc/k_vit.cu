@@ -101,139 +101,190 @@ __global__ void k_layernorm(const float* __restrict__ x, int rows, int D, const 
 
 // ---------------------------------------------------------------------------
 // Flash attention on tcgen05 for head dim 64 (Decoder._attention,
-// decoder.py:172-203, one crop's tokens attend to each other).
+// decoder.py:172-203: one crop's tokens attend to each other).
 //
-// CTA = (128-query tile, head, crop), 128 threads, one query row per thread.
-// Thread 0 drives TMA and the tensor core; everyone does the softmax.
-//   S  = Q K^T      Q, K: TMA SW128 K-major boxes of the qkv matrix   TMEM [0,128)
-//   P  = exp2(S*c - m) -> bf16, written to smem (no-swizzle K-major)
-//   O' = P V        V: the same TMA box read MN-major                  TMEM [128,192)
-//   O  = O * alpha + O'  in registers (online softmax), / l at the end.
-// K chunks of 128 keys are double-buffered (the TMA of chunk j+1 runs under
-// the MMAs and softmax of chunk j); V is single-buffered and refilled as soon
-// as the P.V MMA of chunk j has consumed it (96 KB smem: two CTAs per SM).
+// CTA = one 128-query tile of one (crop, head), 4 warps, one query row per
+// thread; thread 0 also drives TMA and the tensor core.  Two CTAs share an
+// SM (TMEM 256 columns and 112 KB of shared memory each).
+// TMEM: two S buffers (128 x 64 fp32 scores) and O (128 x 64 fp32).
+// Per chunk j of 64 keys:
+//   (1) thread 0 issues S(j+1) = Q K_{j+1}^T into the other S buffer, so the
+//       next scores are computed while (2) the CTA runs the softmax of chunk
+//       j: P = exp2(S c - m) -> bf16 tile in shared memory;
+//   (3) thread 0 issues O += P V_j and refills the K|V ring (4 chunks deep,
+//       TMA 128-byte-swizzled boxes straight from the qkv matrix; V is read
+//       MN-major from the same layout).
+// The running max is rescaled lazily: O and l are corrected in TMEM only
+// when the max grows by more than 2^8 (P stays <= 256; O / l is exact).
 // Keys past T are masked to -inf; query rows past T compute on the next
 // crop's rows and are not stored.
-constexpr int AT_THREADS = 128;
-constexpr uint32_t AT_Q = 0, AT_K = 16384, AT_V = 49152, AT_P = 65536, AT_SMEM = 65536 + 32768;
+constexpr int FA_THREADS = 128, FA_KC = 64, FA_RING = 4;
+constexpr uint32_t FA_Q = 0;                        // 16 KB
+constexpr uint32_t FA_KV = 16384;                   // FA_RING x (K 8 KB | V 8 KB)
+constexpr uint32_t FA_P = FA_KV + FA_RING * 16384;  // 16 KB
+constexpr uint32_t FA_SMEM = FA_P + 16384;
+constexpr float FA_RESCALE = 8.0f;  // log2 units
 
-__global__ void __launch_bounds__(AT_THREADS, 2)
-    k_attn_tc(const __grid_constant__ CUtensorMap tm, int T, int D, float scale, __nv_bfloat16* __restrict__ ctx) {
+__global__ void __launch_bounds__(FA_THREADS, 2)
+    k_attn_tc(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtensorMap tmkv, int T, int D,
+              float scale, __nv_bfloat16* __restrict__ ctx) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ uint64_t bar_ld[2], bar_v, bar_s, bar_o;
+  __shared__ uint64_t q_full, kv_full[FA_RING], s_full[2], o_full[2];
   __shared__ uint32_t tbase;
   const int qt = blockIdx.x, h = blockIdx.y, crop = blockIdx.z;
-  const int tid = threadIdx.x, warp = tid / 32;
+  const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
   const int row0 = crop * T;
-  const int nch = (T + 127) / 128;
-  if (tid == 0) {
-    tc::mbar_init(&bar_ld[0], 1);
-    tc::mbar_init(&bar_ld[1], 1);
-    tc::mbar_init(&bar_v, 1);
-    tc::mbar_init(&bar_s, 1);
-    tc::mbar_init(&bar_o, 1);
+  const int nch = (T + FA_KC - 1) / FA_KC;
+  const bool issuer = tid == 0;
+  if (issuer) {
+    tc::mbar_init(&q_full, 1);
+    for (int i = 0; i < FA_RING; ++i) tc::mbar_init(&kv_full[i], 1);
+    for (int b = 0; b < 2; ++b) {
+      tc::mbar_init(&s_full[b], 1);
+      tc::mbar_init(&o_full[b], 1);  // P(j).V(j) done, j & 1 == b
+    }
     tc::mbar_fence_init();
-    tc::prefetch_tmap(&tm);
+    tc::prefetch_tmap(&tmq);
+    tc::prefetch_tmap(&tmkv);
   }
   if (warp == 0) tc::tmem_alloc(&tbase, 256);
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
-  const uint32_t tS = tbase, tO = tbase + 128;
-  const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+  // TMEM columns: S buffer b at 64 b; O at 128
   const uint32_t sbase = tc::smem_u32(sm);
-  if (tid == 0) {
-    tc::mbar_expect_tx(&bar_ld[0], 2 * 16384);
-    tc::tma_load_2d(sm + AT_Q, &tm, h * 64, row0 + qt * 128, &bar_ld[0]);
-    tc::tma_load_2d(sm + AT_K, &tm, D + h * 64, row0, &bar_ld[0]);
-    tc::mbar_expect_tx(&bar_v, 16384);
-    tc::tma_load_2d(sm + AT_V, &tm, 2 * D + h * 64, row0, &bar_v);
-  }
-  float o[64];
-#pragma unroll
-  for (int d = 0; d < 64; ++d) o[d] = 0.0f;
-  float m = -1e30f, l = 0.0f;
-  const float c2 = scale * 1.4426950408889634f;
-  uint8_t* prow = sm + AT_P + (tid >> 3) * 2048 + (tid & 7) * 16;
-
-  for (int j = 0; j < nch; ++j) {
-    const int b = j & 1;
-    if (tid == 0) {
-      if (j + 1 < nch) {
-        tc::mbar_expect_tx(&bar_ld[b ^ 1], 16384);
-        tc::tma_load_2d(sm + AT_K + (b ^ 1) * 16384, &tm, D + h * 64, row0 + (j + 1) * 128, &bar_ld[b ^ 1]);
-      }
-      tc::mbar_wait(&bar_ld[b], (uint32_t)((j >> 1) & 1));
-      tc::fence_after();
-      const uint32_t q = sbase + AT_Q, k = sbase + AT_K + b * 16384;
-      const uint32_t id = tc::idesc_bf16(128, 128);
-#pragma unroll
-      for (int kk = 0; kk < 4; ++kk)
-        tc::mma_bf16(tS, tc::sw128_kmajor_desc(q + 32 * kk), tc::sw128_kmajor_desc(k + 32 * kk), id, kk > 0);
-      tc::mma_commit(&bar_s);
-    }
-    tc::mbar_wait(&bar_s, (uint32_t)(j & 1));
+  const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+  const uint32_t tO = tbase + 128;
+  const uint32_t id_s = tc::idesc_bf16(128, FA_KC), id_o = tc::idesc_bf16_bmn(128, 64);
+  auto load_kv = [&](int j) {
+    const int b = j % FA_RING;
+    tc::mbar_expect_tx(&kv_full[b], 16384u);
+    tc::tma_load_2d(sm + FA_KV + b * 16384, &tmkv, D + h * 64, row0 + j * FA_KC, &kv_full[b]);
+    tc::tma_load_2d(sm + FA_KV + b * 16384 + 8192, &tmkv, 2 * D + h * 64, row0 + j * FA_KC, &kv_full[b]);
+  };
+  auto issue_s = [&](int j) {  // S(j) -> S buffer j & 1
+    const int b = j % FA_RING;
+    tc::mbar_wait(&kv_full[b], (uint32_t)((j / FA_RING) & 1));
     tc::fence_after();
-    float s[128];
-    tc::tmem_ld64(tS + lane_off, s);
-    tc::tmem_ld64(tS + lane_off + 64, s + 64);
-    const int kvalid = T - j * 128;
-    float mx = m;
+    const uint32_t k = sbase + FA_KV + b * 16384;
 #pragma unroll
-    for (int i = 0; i < 128; ++i) {
-      s[i] = (i < kvalid) ? s[i] * c2 : -INFINITY;
-      mx = fmaxf(mx, s[i]);
+    for (int kk = 0; kk < 4; ++kk)
+      tc::mma_bf16(tbase + 64 * (j & 1), tc::sw128_kmajor_desc(sbase + FA_Q + 32 * kk),
+                   tc::sw128_kmajor_desc(k + 32 * kk), id_s, kk > 0);
+    tc::mma_commit(&s_full[j & 1]);
+  };
+  if (issuer) {
+    tc::mbar_expect_tx(&q_full, 16384u);
+    tc::tma_load_2d(sm + FA_Q, &tmq, h * 64, row0 + qt * 128, &q_full);
+    for (int j = 0; j < FA_RING && j < nch; ++j) load_kv(j);
+    tc::mbar_wait(&q_full, 0);
+    issue_s(0);
+  }
+  uint8_t* prow0 = sm + FA_P + (tid >> 3) * (FA_KC * 16) + (tid & 7) * 16;
+  const float c2 = scale * 1.4426950408889634f;
+  float m = -INFINITY, l = 0.0f;
+  for (int j = 0; j < nch; ++j) {
+    // (1) scores of the next chunk into the other S buffer (its previous
+    // contents, S(j-1), were read before the barrier that ended chunk j-1)
+    if (issuer && j + 1 < nch) issue_s(j + 1);
+    // (2) softmax of chunk j
+    tc::mbar_wait(&s_full[j & 1], (uint32_t)((j >> 1) & 1));
+    tc::fence_after();
+    float s[FA_KC];
+    tc::tmem_ld64(tbase + 64 * (j & 1) + lane_off, s);
+    const int kvalid = T - j * FA_KC;
+    if (kvalid < FA_KC) {
+#pragma unroll
+      for (int i = 0; i < FA_KC; ++i)
+        if (i >= kvalid) s[i] = -INFINITY;
     }
-    const float alpha = ex2_approx(m - mx);
-    m = mx;
-    float sum = 0.0f;
+    float m4[4] = {s[0], s[1], s[2], s[3]};
 #pragma unroll
-    for (int g = 0; g < 16; ++g) {
+    for (int i = 4; i < FA_KC; ++i) m4[i & 3] = fmaxf(m4[i & 3], s[i]);
+    const float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])) * c2;
+    if (j == 0) {
+      m = mx;
+    } else {
+      // lazy rescale: rows whose max grew by > 2^8 move to the new max.
+      // TMEM accesses are warp-collective: the whole warp takes the branch
+      // if any of its rows needs it (alpha = 1 elsewhere).
+      const bool need = mx > m + FA_RESCALE;
+      if (__any_sync(0xffffffffu, need)) {
+        const float alpha = need ? ex2_approx(m - mx) : 1.0f;
+        // O stable: P(j-1).V(j-1) (and everything before it) done
+        tc::mbar_wait(&o_full[(j - 1) & 1], (uint32_t)(((j - 1) >> 1) & 1));
+        tc::fence_after();
+#pragma unroll 1
+        for (int c = 0; c < 64; c += 8) {
+          float o[8];
+          tc::tmem_ld8(tO + lane_off + c, o);
+#pragma unroll
+          for (int d = 0; d < 8; ++d) o[d] *= alpha;
+          tc::tmem_st8(tO + lane_off + c, o);
+        }
+        l *= alpha;
+        if (need) m = mx;
+      }
+    }
+    if (j >= 1) {
+      // the P tile was last read by P(j-1).V(j-1).  The two o_full barriers
+      // alternate, and each is waited once per phase in order.
+      tc::mbar_wait(&o_full[(j - 1) & 1], (uint32_t)(((j - 1) >> 1) & 1));
+      tc::fence_after();
+    }
+    uint8_t* prow = prow0;
+    const float nm = -m;
+    float sum4[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+    for (int q = 0; q < FA_KC / 8; ++q) {
       uint32_t w[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
-        __nv_bfloat162 pb = __floats2bfloat162_rn(ex2_approx(s[8 * g + 2 * i] - mx), ex2_approx(s[8 * g + 2 * i + 1] - mx));
-        const float2 pf = __bfloat1622float2(pb);
-        sum += pf.x + pf.y;
-        w[i] = *reinterpret_cast<uint32_t*>(&pb);
+        const float p0 = ex2_approx(fmaf(s[8 * q + 2 * i], c2, nm));
+        const float p1 = ex2_approx(fmaf(s[8 * q + 2 * i + 1], c2, nm));
+        sum4[i] += p0 + p1;
+        w[i] = tc::pack_bf16(p0, p1);
       }
-      *reinterpret_cast<uint4*>(prow + g * 128) = make_uint4(w[0], w[1], w[2], w[3]);
+      *reinterpret_cast<uint4*>(prow + q * 128) = make_uint4(w[0], w[1], w[2], w[3]);
     }
-    l = l * alpha + sum;
+    l += (sum4[0] + sum4[1]) + (sum4[2] + sum4[3]);
     tc::fence_async_smem();
     tc::fence_before();
-    __syncthreads();
-    if (tid == 0) {
-      tc::mbar_wait(&bar_v, (uint32_t)(j & 1));
+    __syncthreads();  // P tile written, S(j) read and O rescaled by every row
+    // (3) O += P V_j; the K|V slot of chunk j is refilled with chunk j + RING
+    // once this P.V has consumed it
+    if (issuer) {
       tc::fence_after();
-      const uint32_t p = sbase + AT_P, v = sbase + AT_V;
-      const uint32_t id = tc::idesc_bf16_bmn(128, 64);
+      const int b = j % FA_RING;
+      const uint32_t v = sbase + FA_KV + b * 16384 + 8192;
+      const uint32_t p_addr = sbase + FA_P;
 #pragma unroll
-      for (int kk = 0; kk < 8; ++kk)
-        tc::mma_bf16(tO, tc::kmajor_desc(p, 128, kk * 16), tc::sw128_mnmajor_desc(v + kk * 2048, 8192), id, kk > 0);
-      tc::mma_commit(&bar_o);
+      for (int kk = 0; kk < FA_KC / 16; ++kk)
+        tc::mma_bf16(tO, tc::kmajor_desc(p_addr, FA_KC, kk * 16), tc::sw128_mnmajor_desc(v + kk * 2048, 8192), id_o,
+                     (j | kk) != 0);
+      tc::mma_commit(&o_full[j & 1]);
     }
-    tc::mbar_wait(&bar_o, (uint32_t)(j & 1));
-    tc::fence_after();
-    if (tid == 0 && j + 1 < nch) {  // V of chunk j has been consumed
-      tc::mbar_expect_tx(&bar_v, 16384);
-      tc::tma_load_2d(sm + AT_V, &tm, 2 * D + h * 64, row0 + (j + 1) * 128, &bar_v);
-    }
-    float pv[64];
-    tc::tmem_ld64(tO + lane_off, pv);
-#pragma unroll
-    for (int d = 0; d < 64; ++d) o[d] = fmaf(o[d], alpha, pv[d]);
+    // refill: P(j-1).V(j-1) completed (observed above), so the slot of
+    // chunk j-1 takes chunk j-1+RING
+    if (issuer && j >= 1 && j - 1 + FA_RING < nch) load_kv(j - 1 + FA_RING);
   }
+  tc::mbar_wait(&o_full[(nch - 1) & 1], (uint32_t)(((nch - 1) >> 1) & 1));
+  tc::fence_after();
   const int qrow = qt * 128 + tid;
-  if (qrow < T) {
-    const float inv = 1.0f / l;
-    uint4* dst = reinterpret_cast<uint4*>(ctx + (size_t)(row0 + qrow) * D + h * 64);
+  const float inv = 1.0f / l;
 #pragma unroll
-    for (int g = 0; g < 8; ++g) {
-      const float* e = o + 8 * g;
-      dst[g] = make_uint4(tc::pack_bf16(e[0] * inv, e[1] * inv), tc::pack_bf16(e[2] * inv, e[3] * inv),
-                          tc::pack_bf16(e[4] * inv, e[5] * inv), tc::pack_bf16(e[6] * inv, e[7] * inv));
+  for (int half = 0; half < 2; ++half) {
+    float o[32];
+    tc::tmem_ld32(tO + lane_off + 32 * half, o);
+    if (qrow < T) {
+      uint4* dst = reinterpret_cast<uint4*>(ctx + (size_t)(row0 + qrow) * D + h * 64 + 32 * half);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float* e = o + 8 * q;
+        dst[q] = make_uint4(tc::pack_bf16(e[0] * inv, e[1] * inv), tc::pack_bf16(e[2] * inv, e[3] * inv),
+                            tc::pack_bf16(e[4] * inv, e[5] * inv), tc::pack_bf16(e[6] * inv, e[7] * inv));
+      }
     }
   }
   tc::fence_before();
@@ -256,15 +307,16 @@ cudaError_t layernorm(const float* x, int rows, int D, const float* g, const flo
 cudaError_t attention(const __nv_bfloat16* qkv, int crops, int T, int D, int H, __nv_bfloat16* ctx, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(k_attn_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)AT_SMEM + 1024);
+    cudaError_t e = cudaFuncSetAttribute(k_attn_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)FA_SMEM + 1024);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  CUtensorMap tm;
-  if (!make_tmap_bf16(&tm, qkv, (uint64_t)crops * T, 3 * (uint64_t)D, 3 * (uint64_t)D, 128))
+  CUtensorMap tmq, tmkv;
+  if (!make_tmap_bf16(&tmq, qkv, (uint64_t)crops * T, 3 * (uint64_t)D, 3 * (uint64_t)D, 128) ||
+      !make_tmap_bf16(&tmkv, qkv, (uint64_t)crops * T, 3 * (uint64_t)D, 3 * (uint64_t)D, FA_KC))
     return cudaErrorInvalidValue;
   dim3 grid(ceil_div(T, 128), H, crops);
-  k_attn_tc<<<grid, AT_THREADS, AT_SMEM + 1024, st>>>(tm, T, D, 1.0f / sqrtf((float)(D / H)), ctx);
+  k_attn_tc<<<grid, FA_THREADS, FA_SMEM + 1024, st>>>(tmq, tmkv, T, D, 1.0f / sqrtf((float)(D / H)), ctx);
   return cudaGetLastError();
 }
 
