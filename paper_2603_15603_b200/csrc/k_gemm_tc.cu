@@ -5,8 +5,9 @@
 // Persistent kernel: one CTA per SM walks the 128 x BN output tiles
 // (N-tile fastest, so CTAs running at the same time share A tiles in L2).
 // Warp 0 is the TMA producer (128-byte swizzled boxes of 64 K-elements),
-// warp 1 issues tcgen05.mma from one lane, warps 2-5 drain TMEM through the
-// epilogue.  A STAGES-deep ring of full/empty mbarriers feeds the tensor
+// warp 1 issues tcgen05.mma from one lane, warps 2-9 drain TMEM through the
+// epilogue (two warps per TMEM lane quadrant, each on half the columns; the
+// fp32 residual rows are fetched one chunk ahead).  A STAGES-deep ring of full/empty mbarriers feeds the tensor
 // core, and the accumulator is double-buffered in TMEM (2 x BN columns):
 // the epilogue of tile i runs while the MMAs of tile i+1 accumulate into the
 // other buffer.  Epilogues (decoder.py:247-257 semantics):
@@ -25,13 +26,25 @@
 
 namespace {
 constexpr int BM = 128, BK = 64, STAGES = 4;
-constexpr int GEMM_THREADS = 192;
-constexpr int EPI_WARPS = 4;
+constexpr int EPI_WARPS = 8;  // two per TMEM lane quadrant, each on half the columns
+constexpr int GEMM_THREADS = 64 + 32 * EPI_WARPS;
 }
 
-template <int BN>
-__device__ __forceinline__ void gemm_epilogue_chunk(const GemmEpi& epi, int row, int col, const float* v) {
-  // 32 consecutive columns [col, col + 32) of one row
+// 32 consecutive columns [col, col + 32) of one row.  `r` holds the
+// residual / position rows of the chunk, loaded before the TMEM read.
+__device__ __forceinline__ void gemm_epi_prefetch(const GemmEpi& epi, int row, int col, float4* r) {
+  if (epi.kind == EPI_RESID_F32) {
+    const float4* x = reinterpret_cast<const float4*>(epi.x_f32 + (size_t)row * epi.ldo + col);
+#pragma unroll
+    for (int g = 0; g < 8; ++g) r[g] = x[g];
+  } else if (epi.kind == EPI_EMBED_F32) {
+    const float4* p = reinterpret_cast<const float4*>(epi.pos + (size_t)(row % epi.T) * epi.ldo + col);
+#pragma unroll
+    for (int g = 0; g < 8; ++g) r[g] = __ldg(p + g);
+  }
+}
+
+__device__ __forceinline__ void gemm_epi_store(const GemmEpi& epi, int row, int col, const float* v, float4* r) {
   float b[32];
 #pragma unroll
   for (int i = 0; i < 32; i += 4) {
@@ -49,15 +62,6 @@ __device__ __forceinline__ void gemm_epilogue_chunk(const GemmEpi& epi, int row,
                           tc::pack_bf16(b[8 * g + 4], b[8 * g + 5]), tc::pack_bf16(b[8 * g + 6], b[8 * g + 7]));
   } else {
     float4* x = reinterpret_cast<float4*>(epi.x_f32 + (size_t)row * epi.ldo + col);
-    float4 r[8];
-    if (epi.kind == EPI_EMBED_F32) {
-      const float4* p = reinterpret_cast<const float4*>(epi.pos + (size_t)(row % epi.T) * epi.ldo + col);
-#pragma unroll
-      for (int g = 0; g < 8; ++g) r[g] = __ldg(p + g);
-    } else {
-#pragma unroll
-      for (int g = 0; g < 8; ++g) r[g] = x[g];
-    }
 #pragma unroll
     for (int g = 0; g < 8; ++g) {
       r[g].x += b[4 * g]; r[g].y += b[4 * g + 1]; r[g].z += b[4 * g + 2]; r[g].w += b[4 * g + 3];
@@ -145,22 +149,31 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       __syncwarp();
     }
   } else if (warp >= 2) {
-    // epilogue: warp w reads TMEM lanes 32 * (w % 4) .. +31 (rows of the tile)
-    const int quad = warp % 4;
+    // epilogue: warp w reads TMEM lanes 32 * (w % 4) .. +31 (rows of the
+    // tile); warps w and w + 4 split the columns
+    const int quad = warp % 4, half = (warp - 2) / 4;
+    constexpr int HALF = BN / 2;
     int tc_count = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tc_count) {
       const int buf = tc_count & 1;
       const int m0 = (t / ntn) * BM, n0 = (t % ntn) * BN;
+      const int row = m0 + quad * 32 + lane;
+      const bool rok = row < M;
+      const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(buf * BN + half * HALF);
+      float4 r[8];
+      // the first residual chunk is fetched before waiting for the MMAs
+      if (rok && n0 + half * HALF < N) gemm_epi_prefetch(epi, row, n0 + half * HALF, r);
       tc::mbar_wait(&acc_full[buf], (uint32_t)((tc_count >> 1) & 1));
       tc::fence_after();
-      const int row = m0 + quad * 32 + lane;
-      const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(buf * BN);
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
+      for (int c = 0; c < HALF; c += 32) {
         float v[32];
         tc::tmem_ld32(taddr + c, v);
-        const int col = n0 + c;
-        if (row < M && col < N) gemm_epilogue_chunk<BN>(epi, row, col, v);
+        const int col = n0 + half * HALF + c;
+        if (rok && col < N) {
+          gemm_epi_store(epi, row, col, v, r);
+          if (c + 32 < HALF && col + 32 < N) gemm_epi_prefetch(epi, row, col + 32, r);
+        }
       }
       // this warp's TMEM reads are complete: hand the buffer back to the MMA warp
       tc::fence_before();

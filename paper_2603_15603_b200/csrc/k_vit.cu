@@ -51,10 +51,9 @@ __global__ void k_patchify(const float* __restrict__ crops, int n, int S, int p,
 // ---------------------------------------------------------------------------
 // LayerNorm (numkit.py:198-202, eps 1e-5): one warp per row, the row held in
 // registers (D <= 2048, D % 128 == 0), two-pass mean / variance.
-template <bool OUT_BF16>
+template <bool OUT_BF16, int MAXV>  // MAXV: float4 per lane (D / 128 when it is a power of two)
 __global__ void k_layernorm(const float* __restrict__ x, int rows, int D, const float* __restrict__ g,
                             const float* __restrict__ b, void* __restrict__ out, int* nonfinite) {
-  constexpr int MAXV = 16;  // float4 per lane
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) / 32, lane = threadIdx.x % 32;
   if (warp >= rows) return;
   const int nv = D / 128;
@@ -294,13 +293,25 @@ __global__ void __launch_bounds__(FA_THREADS, 2)
 
 inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
 
+template <bool OUT_BF16>
+static void layernorm_launch(const float* x, int rows, int D, const float* g, const float* b, void* out,
+                             int* nonfinite, cudaStream_t st) {
+  const int blocks = ceil_div(rows, 8);
+  switch (D / 128) {
+    case 8: k_layernorm<OUT_BF16, 8><<<blocks, 256, 0, st>>>(x, rows, D, g, b, out, nonfinite); break;
+    case 4: k_layernorm<OUT_BF16, 4><<<blocks, 256, 0, st>>>(x, rows, D, g, b, out, nonfinite); break;
+    case 2: k_layernorm<OUT_BF16, 2><<<blocks, 256, 0, st>>>(x, rows, D, g, b, out, nonfinite); break;
+    case 1: k_layernorm<OUT_BF16, 1><<<blocks, 256, 0, st>>>(x, rows, D, g, b, out, nonfinite); break;
+    default: k_layernorm<OUT_BF16, 16><<<blocks, 256, 0, st>>>(x, rows, D, g, b, out, nonfinite); break;
+  }
+}
+
 cudaError_t layernorm(const float* x, int rows, int D, const float* g, const float* b, void* out, bool bf16,
                       int* nonfinite, cudaStream_t st) {
-  const int blocks = ceil_div(rows, 8);
   if (bf16)
-    k_layernorm<true><<<blocks, 256, 0, st>>>(x, rows, D, g, b, out, nonfinite);
+    layernorm_launch<true>(x, rows, D, g, b, out, nonfinite, st);
   else
-    k_layernorm<false><<<blocks, 256, 0, st>>>(x, rows, D, g, b, out, nonfinite);
+    layernorm_launch<false>(x, rows, D, g, b, out, nonfinite, st);
   return cudaGetLastError();
 }
 
