@@ -60,6 +60,8 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--streams", type=int, default=3,
+                    help="in-flight batches per GPU: independent pipeline contexts on their own streams")
     ap.add_argument("--no-c3", action="store_true", help="skip the C3 LBS + projector microbench")
     ap.add_argument("--no-c4", action="store_true", help="skip the C4 ViT-L-sized encoder microbench")
     ap.add_argument("--c4-crops", type=int, default=768, help="C4: 3 crops x 256 frames")
@@ -166,6 +168,20 @@ def build_models(precision):
     dec = dc.Decoder(smpl, dc.DecoderConfig(), seed=40)
     proj = pj.init_projector(pj.make_subsample(6890, 1500), (512, 256), seed=0)
     return pl.Pipeline(dec, mhr=mhr, bmap=gt, projector=proj, precision=precision), (mhr, smpl, gt, dec, proj)
+
+
+def extra_pipelines(pipe, n, precision):
+    """n more pipeline instances over the same models, each with its own
+    fsb context (weights, workspace, CUDA graphs): one per in-flight batch
+    (pipelines are not shared between concurrent users)."""
+    from paper_2603_15603_b200 import decoder as dc
+    from paper_2603_15603_b200 import pipeline as pl
+
+    out = []
+    for _ in range(n):
+        d = dc.Decoder(pipe.decoder.template, pipe.decoder.config, seed=40)
+        out.append(pl.Pipeline(d, mhr=pipe.mhr, bmap=pipe.bmap, projector=pipe.projector, precision=precision))
+    return out
 
 
 def make_scenes(smpl, seeds):
@@ -278,45 +294,58 @@ def main():
     images = pr.render_scenes(scenes)                      # (bank, 512, 512, 3) resident in HBM
     kps = torch.from_numpy(np.stack([s.keypoints2d for s in scenes])).to(dev)
     nslot = bank // B
-    outs = pipe.allocate_outputs(B, tail=True)
-    cfg = None
+    S = max(1, args.streams)
+    pipes = [pipe] + extra_pipelines(pipe, S - 1, args.precision)
+    for p_ in pipes[1:]:
+        p_.context().reserve(max(B, 1))
+    streams = [torch.cuda.current_stream()] + [torch.cuda.Stream(device=dev) for _ in range(S - 1)]
+    outs_s = [p_.allocate_outputs(B, tail=True) for p_ in pipes]
+    outs = outs_s[0]
     from paper_2603_15603_b200 import pipeline as pl
 
     cfg = pl.fast_config()
     gathered = None
     if dist is not None:
-        gathered = torch.empty((world * B, 76 + 66), dtype=torch.float32, device=dev)
-        packed = torch.empty((B, 76 + 66), dtype=torch.float32, device=dev)
+        gathered = [torch.empty((world * B, 76 + 66), dtype=torch.float32, device=dev) for _ in range(S)]
+        packed = [torch.empty((B, 76 + 66), dtype=torch.float32, device=dev) for _ in range(S)]
 
     def step(i):
-        s = i % nslot
-        pipe.launch(images[s * B:(s + 1) * B], kps[s * B:(s + 1) * B], outs, cfg)
-        if dist is not None:
-            packed[:, :76].copy_(outs["theta"])
-            packed[:, 76:].copy_(outs["j_smpl"].reshape(B, 66))
-            dist.all_gather_into_tensor(gathered, packed)
+        j, s = i % S, i % nslot
+        with torch.cuda.stream(streams[j]):
+            pipes[j].launch(images[s * B:(s + 1) * B], kps[s * B:(s + 1) * B], outs_s[j], cfg)
+            if dist is not None:
+                packed[j][:, :76].copy_(outs_s[j]["theta"])
+                packed[j][:, 76:].copy_(outs_s[j]["j_smpl"].reshape(B, 66))
+                dist.all_gather_into_tensor(gathered[j], packed[j])
 
     def barrier():
         if dist is not None:
             dist.barrier()
         torch.cuda.synchronize()
 
-    # warm-up (captures one graph per input slot)
-    for i in range(max(args.warmup, 3, nslot)):
+    # warm-up (captures one graph per input slot and stream)
+    for i in range(max(args.warmup, 3, nslot * S)):
         step(i)
-    ctx.check_finite("bench warm-up")
+    for p_ in pipes:
+        p_.context().check_finite("bench warm-up")
     barrier()
-    launches0 = ctx.launches()
-    st = torch.cuda.current_stream()
+    launches0 = sum(p_.context().launches() for p_ in pipes)
+    st = streams[0]
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    joins = [torch.cuda.Event() for _ in range(S)]
     with ClockSampler(local) as clk:
         barrier()
         e0.record(st)
+        for q in streams[1:]:
+            q.wait_event(e0)
         for i in range(args.steps):
             step(i)
+        for j in range(1, S):
+            joins[j].record(streams[j])
+            st.wait_event(joins[j])
         e1.record(st)
         barrier()
-    launches = ctx.launches() - launches0
+    launches = sum(p_.context().launches() for p_ in pipes) - launches0
     ms = e0.elapsed_time(e1)
     t_max = torch.tensor([ms], dtype=torch.float64, device=dev)
     if dist is not None:
@@ -324,7 +353,10 @@ def main():
     ms = float(t_max.item())
     frames_total = world * B * args.steps
     value = frames_total / (ms / 1e3)
-    ctx.check_finite("bench")
+    for p_ in pipes:
+        p_.context().check_finite("bench")
+    # the concurrent batches computed what one pipeline computes alone
+    verified = verify_streams(torch, pipes, outs_s, images, kps, cfg, B, args.steps, nslot, S)
 
     # -- per-stage attribution (graphs off, CUDA events between stages) -------
     stage_ms = attribute_stages(torch, pipe, ctx, images[:B], kps[:B], outs, cfg, reps=20)
@@ -333,7 +365,7 @@ def main():
     lat = frame_latency(torch, pipe, images, kps, cfg, reps=200)
 
     # -- end-to-end through the public API with host buffers -------------------
-    e2e = None if args.no_e2e else end_to_end(torch, pipe, images, kps, cfg, B, args.steps, args.warmup, dist,
+    e2e = None if args.no_e2e else end_to_end(torch, pipes, images, kps, cfg, B, args.steps, args.warmup, dist,
                                               world)
     e2e_copy = None if args.no_e2e else end_to_end_full_copy(torch, pipe, images, kps, cfg, B, args.steps,
                                                              args.warmup, dist, world)
@@ -369,7 +401,8 @@ def main():
                    if world > 1 else "single GPU",
                    "l2": "inputs cycle through a %d-frame bank (%.0f MB in HBM) > 126 MB L2" %
                          (bank, bank * 512 * 512 * 12 / 1e6),
-                   "precision": args.precision, "graphs": True},
+                   "precision": args.precision, "graphs": True,
+                   "in_flight_batches": S, "concurrent_outputs_match_single_stream": verified},
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "e2e_full_frame_copy": e2e_copy,
         "gpu_launches": launches,
         "clocks": clk.summary(), "p50_frame_latency_ms": lat["p50_ms"], "frame_latency": lat,
@@ -603,7 +636,25 @@ def frame_latency(torch, pipe, images, kps, cfg, reps):
     return {"p50_ms": ts[len(ts) // 2], "p95_ms": ts[int(len(ts) * 0.95)], "reps": reps, "batch": 1}
 
 
-def end_to_end(torch, pipe, images, kps, cfg, B, steps, warmup, dist, world):
+def verify_streams(torch, pipes, outs_s, images, kps, cfg, B, steps, nslot, S):
+    """Re-run the last step of every stream alone on pipeline 0 and compare
+    bit for bit with what the concurrent run produced."""
+    torch.cuda.synchronize()
+    ref = pipes[0].allocate_outputs(B, tail=True)
+    ok = True
+    for j in range(S):
+        last = max(i for i in range(steps) if i % S == j) if steps > j else None
+        if last is None:
+            continue
+        s = last % nslot
+        got = {k: outs_s[j][k].clone() for k in ("merged", "theta", "j_smpl")}
+        pipes[0].launch(images[s * B:(s + 1) * B], kps[s * B:(s + 1) * B], ref, cfg)
+        torch.cuda.synchronize()
+        ok = ok and all(torch.equal(got[k], ref[k]) for k in got)
+    return bool(ok)
+
+
+def end_to_end(torch, pipes, images, kps, cfg, B, steps, warmup, dist, world):
     """Pipeline.run_batch on frames that live in pinned host memory (the
     reference's images are host float32 arrays).  K1 reads each frame in
     place over PCIe -- only the crop footprints (the rows and x-spans the
@@ -611,22 +662,26 @@ def end_to_end(torch, pipe, images, kps, cfg, B, steps, warmup, dist, world):
     H2D copy; steps alternate between two streams so one batch's gather
     overlaps the previous batch's compute.  Every step ends with a D2H read
     of merged/theta/j_smpl into pinned host buffers.  h2d_bytes_per_step is
-    counted on the device by K1 (fsb_input_bytes) plus the keypoints."""
-    ctx = pipe.context()
+    counted on the device by K1 (fsb_input_bytes) plus the keypoints.  Each
+    stream drives its own pipeline context (own workspace and graphs)."""
+    pipes = list(pipes[:2])
+    if len(pipes) < 2:
+        pipes += extra_pipelines(pipes[0], 1, pipes[0].precision)
+    ctxs = [p_.context() for p_ in pipes]
     dev = images.device
     nhost = min(images.shape[0], 4 * B)
     h_img = images[:nhost].cpu().pin_memory()
     h_kp = kps[:nhost].cpu().pin_memory()
     nslot = nhost // B
     streams = [torch.cuda.Stream(device=dev) for _ in range(2)]
-    outs = [pipe.allocate_outputs(B, tail=True) for _ in range(2)]
+    outs = [pipes[j].allocate_outputs(B, tail=True) for j in range(2)]
     h_out = [{k: torch.empty(outs[0][k].shape, dtype=torch.float32).pin_memory()
               for k in ("merged", "theta", "j_smpl")} for _ in range(2)]
 
     def run(i):
         j, s = i % 2, i % nslot
         with torch.cuda.stream(streams[j]):
-            pipe.run_batch(h_img[s * B:(s + 1) * B], h_kp[s * B:(s + 1) * B], cfg, outputs=outs[j], sync=False)
+            pipes[j].run_batch(h_img[s * B:(s + 1) * B], h_kp[s * B:(s + 1) * B], cfg, outputs=outs[j], sync=False)
             for k in ("merged", "theta", "j_smpl"):
                 h_out[j][k].copy_(outs[j][k], non_blocking=True)
 
@@ -635,7 +690,8 @@ def end_to_end(torch, pipe, images, kps, cfg, B, steps, warmup, dist, world):
     torch.cuda.synchronize()
     if dist is not None:
         dist.barrier()
-    ctx.input_bytes(reset=True)
+    for c in ctxs:
+        c.input_bytes(reset=True)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     tail = [torch.cuda.Event() for _ in range(2)]
     e0.record(streams[0])
@@ -648,7 +704,17 @@ def end_to_end(torch, pipe, images, kps, cfg, B, steps, warmup, dist, world):
     e1.record(streams[0])
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
-    frame_bytes = ctx.input_bytes(reset=True)
+    frame_bytes = sum(c.input_bytes(reset=True) for c in ctxs)
+    # the host-side results of the last step of each stream equal a fresh
+    # device-frame run of the same frames
+    ok = True
+    ref = pipes[0].allocate_outputs(B, tail=True)
+    for j in range(2):
+        last = max(i for i in range(steps) if i % 2 == j)
+        s = last % nslot
+        pipes[0].launch(images[s * B:(s + 1) * B], kps[s * B:(s + 1) * B], ref, cfg)
+        torch.cuda.synchronize()
+        ok = ok and all(torch.equal(h_out[j][k], ref[k].cpu()) for k in ("merged", "theta", "j_smpl"))
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if dist is not None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -660,7 +726,7 @@ def end_to_end(torch, pipe, images, kps, cfg, B, steps, warmup, dist, world):
             "d2h_bytes_per_step": d2h_b, "ms_per_step": ms / steps,
             "api": "Pipeline.run_batch on pinned host frames (K1 gathers the crop footprints over PCIe in "
                    "place; two streams)",
-            "h2d_fraction_of_frames": h2d_b / full}
+            "h2d_fraction_of_frames": h2d_b / full, "outputs_verified": bool(ok)}
 
 
 def end_to_end_full_copy(torch, pipe, images, kps, cfg, B, steps, warmup, dist, world):
