@@ -285,6 +285,20 @@ def test_fk_and_skin_fp32(torch, full_models, golden):
     assert rel_err(vs, orc.skin_batch(smpl, poses[:4])) <= FP32_TOL
 
 
+def test_skin_many_meshes(torch, full_models):
+    """Several 32-mesh groups, an odd mesh count and a partial last vertex
+    tile (18,439 = 576 x 32 + 7) through the warp-tile LBS kernel."""
+    from paper_2603_15603_b200 import bodymodel as bm
+
+    mhr, smpl, _ = full_models
+    poses = _c3_poses(71)
+    v = bm.skin_batch(mhr, poses)
+    pick = [0, 1, 31, 32, 33, 63, 64, 70]
+    assert rel_err(v[pick], orc.skin_batch(mhr, poses[pick])) <= FP32_TOL
+    vs = bm.skin_batch(smpl, poses[:35])
+    assert rel_err(vs[[0, 33, 34]], orc.skin_batch(smpl, poses[[0, 33, 34]])) <= FP32_TOL
+
+
 def test_projector_fp32(torch, full_models, full_projector, golden):
     from paper_2603_15603_b200 import projection as pj
 
