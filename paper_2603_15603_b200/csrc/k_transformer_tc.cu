@@ -61,7 +61,7 @@ struct Shared {
 // cycle attribution of CTA 0 / thread 0 (build with FSB_PROFILE=1):
 // [0] total, [1] MMA waits, [2] weight waits, [3] issue barriers,
 // [4] row-exchange barriers
-__device__ unsigned long long g_tc_prof[2][2][8];  // [role][thread 0 | thread 255][counter]
+__device__ unsigned long long g_tc_prof[2][2][12];  // [role][thread 0 | thread 255][counter]
 #define PROF_T0() const long long prof_t0_ = clock64()
 #define PROF_ADD(i) (prof[i] += clock64() - prof_t0_)
 #else
@@ -79,7 +79,7 @@ struct Pipe {
   int wload, wuse, xc, pload, puse;
   int tid, r, h;
 #ifdef FSB_PROFILE
-  long long prof[8];
+  long long prof[12];
 #endif
 
   // per-layer parameter block ring (TCP_* layout): thread 0 issues, every
@@ -249,72 +249,86 @@ __device__ void drain_kv(Pipe& P, uint32_t kcol, const float* bk, const float* b
   }
 }
 
-// softmax of head (2 * pair + h) over the row's own key block -> P tile h
-__device__ void softmax_head(Pipe& P, int nk) {
+// softmax of head (pair + 2 h) over the first NK keys of the row's own key
+// block -> P tile h, unnormalised (the context is scaled by the returned
+// 1 / sum after P.V: 16 multiplies instead of 64).  NK is the number of
+// valid keys (64 for encoder self-attention and cross-attention, 51 body
+// tokens, 4 hand tokens), so masking is resolved at compile time.
+template <int NK>
+__device__ float softmax_head(Pipe& P) {
+  static_assert(NK >= 1 && NK <= 64, "keys per block");
+  constexpr int NL = NK <= 16 ? 16 : (NK <= 32 ? 32 : 64);  // TMEM columns loaded
   const int blk = P.r / BLK;
   float s[64];
-  tc::tmem_ld64(P.lane_addr(T_GEN + 128 * P.h + 64 * blk), s);
-  float m8[8];
+  const uint32_t ta = P.lane_addr(T_GEN + 128 * P.h + 64 * blk);
+  if (NL == 64) tc::tmem_ld64(ta, s);
+  else if (NL == 32) tmem_ld32(ta, s);
+  else tc::tmem_ld16(ta, s);
+  float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-  for (int i = 0; i < 8; ++i) m8[i] = -INFINITY;
+  for (int k = 0; k < NK; ++k) m4[k & 3] = fmaxf(m4[k & 3], s[k]);
   constexpr float kScale = 0.25f * 1.4426950408889634f;  // f32(1/sqrt(16)) * log2(e)
+  const float nms = -fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])) * kScale;
+  float p4[4] = {0.0f, 0.0f, 0.0f, 0.0f};
 #pragma unroll
-  for (int k = 0; k < 64; ++k) {
-    s[k] = (k < nk) ? s[k] * kScale : -INFINITY;
-    m8[k & 7] = fmaxf(m8[k & 7], s[k]);
+  for (int k = 0; k < NK; ++k) {
+    s[k] = ex2_approx(fmaf(s[k], kScale, nms));
+    p4[k & 3] += s[k];
   }
-  const float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])), fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
-  float p8[8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i) p8[i] = 0.0f;
-#pragma unroll
-  for (int k = 0; k < 64; ++k) {
-    s[k] = (k < nk) ? ex2_approx(s[k] - mx) : 0.0f;
-    p8[k & 7] += s[k];
-  }
-  const float inv = 1.0f / (((p8[0] + p8[1]) + (p8[2] + p8[3])) + ((p8[4] + p8[5]) + (p8[6] + p8[7])));
   uint8_t* tp = P.smem + S_HP + P.h * 32768;
 #pragma unroll
   for (int q = 0; q < 8; ++q) {
-    float v[8];
+    if (8 * q < NK) {
+      float v[8];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) v[i] = s[8 * q + i] * inv;
-    st_row8(tp, P.r, 64 * blk + 8 * q, 128, v);
+      for (int i = 0; i < 8; ++i) v[i] = (8 * q + i < NK) ? s[8 * q + i] : 0.0f;
+      st_row8(tp, P.r, 64 * blk + 8 * q, 128, v);
+    } else {
+      st_row_zero8(tp, P.r, 64 * blk + 8 * q, 128);
+    }
     st_row_zero8(tp, P.r, 64 * (1 - blk) + 8 * q, 128);
   }
+  return 1.0f / ((p4[0] + p4[1]) + (p4[2] + p4[3]));
 }
 
 // the four heads of one attention given sQ / sK / sVt; the context is
-// written as bf16 straight into the A tile of the output projection
-__device__ void attn_core(Pipe& P, int nk) {
+// written as bf16 straight into the A tile of the output projection.
+// Pair p of the two passes runs heads p (threads h = 0) and p + 2
+// (threads h = 1), so each thread ends up owning the softmax sums of the
+// two heads whose context columns [32 h, 32 h + 32) it holds.
+template <int NK>
+__device__ void attn_core(Pipe& P) {
   const uint32_t sq = P.sbase + S_Q, sk = P.sbase + S_K, sv = P.sbase + S_VT, sp = P.sbase + S_HP;
   const uint32_t id_s = tc::idesc_bf16(128, 128), id_o = tc::idesc_bf16(128, 16);
   P.before_issue();
   if (P.tid == 0)
     for (int j = 0; j < 2; ++j)
-      tc::mma_bf16(P.tmem + T_GEN + 128 * j, tc::kmajor_desc(sq + j * 4096, DH, 0),
-                   tc::kmajor_desc(sk + j * 4096, DH, 0), id_s, false);
+      tc::mma_bf16(P.tmem + T_GEN + 128 * j, tc::kmajor_desc(sq + (2 * j) * 4096, DH, 0),
+                   tc::kmajor_desc(sk + (2 * j) * 4096, DH, 0), id_s, false);
   P.commit_wait();
+  float inv[2];
 #pragma unroll 1
   for (int pair = 0; pair < 2; ++pair) {
-    softmax_head(P, nk);
+    inv[pair] = softmax_head<NK>(P);
     P.before_issue();
     if (P.tid == 0) {
       for (int j = 0; j < 2; ++j) {
-        const int hd = 2 * pair + j;
+        const int hd = pair + 2 * j;
         for (int k = 0; k < 128; k += 16)
           tc::mma_bf16(P.tmem + T_O + 16 * hd, tc::kmajor_desc(sp + j * 32768, 128, k),
                        tc::kmajor_desc(sv + hd * 4096, 128, k), id_o, k > 0);
       }
       if (pair == 0)
         for (int j = 0; j < 2; ++j)
-          tc::mma_bf16(P.tmem + T_GEN + 128 * j, tc::kmajor_desc(sq + (2 + j) * 4096, DH, 0),
-                       tc::kmajor_desc(sk + (2 + j) * 4096, DH, 0), id_s, false);
+          tc::mma_bf16(P.tmem + T_GEN + 128 * j, tc::kmajor_desc(sq + (1 + 2 * j) * 4096, DH, 0),
+                       tc::kmajor_desc(sk + (1 + 2 * j) * 4096, DH, 0), id_s, false);
     }
     P.commit_wait();
   }
   float ctx[HC];
   tmem_ld32(P.lane_addr(T_O + HC * P.h), ctx);
+#pragma unroll
+  for (int c = 0; c < HC; ++c) ctx[c] *= inv[c / 16];
 #pragma unroll
   for (int q = 0; q < HC; q += 8) st_row8(P.smem + S_A, P.r, HC * P.h + q, D, ctx + q);
 }
@@ -337,7 +351,8 @@ __device__ void out_proj(Pipe& P, const float* bo, float* x, bool valid) {
 // memory (LayerNorm affine and biases); the weight images come from the ring.
 
 // self attention: x += MHA(LN(x + pos))  (decoder.py:214-218)
-__device__ void self_attn(Pipe& P, const float* prm, float* x, const float* pos, int nk, bool valid) {
+template <int NK>
+__device__ void self_attn(Pipe& P, const float* prm, float* x, const float* pos, bool valid) {
   float a[HC];
 #pragma unroll
   for (int c = 0; c < HC; ++c) a[c] = x[c] + pos[c];
@@ -349,7 +364,7 @@ __device__ void self_attn(Pipe& P, const float* prm, float* x, const float* pos,
   P.commit_wait();
   drain_q(P, T_GEN, prm + TCP_S_BQKV);
   drain_kv(P, T_GEN + 64, prm + TCP_S_BQKV + 64, prm + TCP_S_BQKV + 128);
-  attn_core(P, nk);
+  attn_core<NK>(P);
   out_proj(P, prm + TCP_S_BO, x, valid);
 }
 
@@ -375,7 +390,7 @@ __device__ void cross_attn(Pipe& P, const float* prm, float* x, const float* fro
   P.prefetch();
   P.commit_wait();
   drain_q(P, T_GEN, prm + TCP_C_BQKV);
-  attn_core(P, BLK);
+  attn_core<BLK>(P);
   out_proj(P, prm + TCP_C_BO, x, valid);
 }
 
@@ -424,7 +439,7 @@ __device__ void setup(Pipe& P, Shared& sh, uint8_t* smem) {
   P.pload = 0;
   P.puse = 0;
 #ifdef FSB_PROFILE
-  for (int i = 0; i < 8; ++i) P.prof[i] = 0;
+  for (int i = 0; i < 12; ++i) P.prof[i] = 0;
   P.prof[0] = -clock64();
 #endif
   if (P.tid == 0) {
@@ -450,7 +465,7 @@ __device__ void teardown(Pipe& P, int role) {
 #ifdef FSB_PROFILE
   P.prof[0] += clock64();
   if ((P.tid == 0 || P.tid == NTH - 1) && blockIdx.x == 0)
-    for (int i = 0; i < 8; ++i) g_tc_prof[role][P.tid ? 1 : 0][i] = (unsigned long long)P.prof[i];
+    for (int i = 0; i < 12; ++i) g_tc_prof[role][P.tid ? 1 : 0][i] = (unsigned long long)P.prof[i];
 #else
   (void)role;
 #endif
@@ -526,7 +541,7 @@ __global__ void __launch_bounds__(NTH, 1) k_encoder_tc(const float* __restrict__
     const float* prm = P.pacquire();
     __syncthreads();  // every thread is past layer l - 1: its slot may be refilled
     if (l + 1 < w.layers) P.pprefetch(w.tc_params[l + 1]);
-    self_attn(P, prm, x, zero, BLK, valid);
+    self_attn<BLK>(P, prm, x, zero, valid);
     mlp(P, prm, x, valid);
   }
   float y[HC];
@@ -688,7 +703,14 @@ __global__ void __launch_bounds__(NTH, 1) k_decoders_tc(DecodeArgs a, BodyW bw, 
   }
   __syncthreads();
 
+#ifdef FSB_PROFILE
+  P.prof[8] += clock64() + P.prof[0];  // setup: kernel start (prof[0] = -start) -> layer loop
+  long long tpos;
+#endif
   for (int l = 0; l < layers; ++l) {
+#ifdef FSB_PROFILE
+    tpos = clock64();
+#endif
     // positional terms of the self-attention input (decoder.py:300-303, :397-398)
     if (body) {
       const bool pr2 = rb >= 5 && rb < 27, pr3 = rb >= 27 && rb < 49;
@@ -727,16 +749,42 @@ __global__ void __launch_bounds__(NTH, 1) k_decoders_tc(DecodeArgs a, BodyW bw, 
     const float* prm = P.pacquire();
     __syncthreads();  // every thread is past layer l - 1: its slot may be refilled
     if (l + 1 < layers) P.pprefetch(body ? bw.tc_params[l + 1] : hw.tc_params[l + 1]);
-    self_attn(P, prm, x, pos, nrows, valid);
+#ifdef FSB_PROFILE
+    long long ts0 = clock64();
+    P.prof[9] += ts0 - tpos;
+#endif
+    if (body)
+      self_attn<51>(P, prm, x, pos, valid);
+    else
+      self_attn<4>(P, prm, x, pos, valid);
+#ifdef FSB_PROFILE
+    long long ts1 = clock64();
+    P.prof[5] += ts1 - ts0;
+#endif
     cross_attn(P, prm, x, frow, valid);
+#ifdef FSB_PROFILE
+    long long ts2 = clock64();
+    P.prof[6] += ts2 - ts1;
+#endif
     mlp(P, prm, x, valid);
+#ifdef FSB_PROFILE
+    long long ts3 = clock64();
+    P.prof[7] += ts3 - ts2;
+#endif
     const unsigned sel = body ? a.body_sel : a.hand_sel;
     if ((sel >> l) & 1u) {
       if (body) {
         // intermediate prediction: heads -> FK -> kp2d / centred joints
         body_heads(P, bx, bw, x);
+#ifdef FSB_PROFILE
+        long long th = clock64();
+        P.prof[10] += th - ts3;
+#endif
         if (t < 64) fk_warp(bx.params[t / 32], bw.joints_rest, bx.fk[t / 32], t % 32);
         __syncthreads();
+#ifdef FSB_PROFILE
+        P.prof[11] += clock64() - th;
+#endif
         if (t < 2 * FSB_NJ) {
           const int b = t / FSB_NJ, j = t % FSB_NJ;
           bx.kp2d[b][2 * j] = bx.cam[b][0] * bx.fk[b].tw[j][0] + bx.cam[b][1];
@@ -775,6 +823,9 @@ __global__ void __launch_bounds__(NTH, 1) k_decoders_tc(DecodeArgs a, BodyW bw, 
       }
     }
   }
+#ifdef FSB_PROFILE
+  long long tfin = clock64();
+#endif
   // final heads and outputs
   if (body) {
     body_heads(P, bx, bw, x);
@@ -801,15 +852,18 @@ __global__ void __launch_bounds__(NTH, 1) k_decoders_tc(DecodeArgs a, BodyW bw, 
       }
     }
   }
+#ifdef FSB_PROFILE
+  P.prof[8] += clock64() - tfin;
+#endif
   teardown(P, 1);
 }
 
 // debug export of the FSB_PROFILE cycle counters (not part of the public ABI)
 extern "C" int fsb_debug_tc_profile(unsigned long long* out32) {
 #ifdef FSB_PROFILE
-  return cudaMemcpyFromSymbol(out32, g_tc_prof, sizeof(unsigned long long) * 32) == cudaSuccess ? 0 : 4;
+  return cudaMemcpyFromSymbol(out32, g_tc_prof, sizeof(unsigned long long) * 48) == cudaSuccess ? 0 : 4;
 #else
-  for (int i = 0; i < 32; ++i) out32[i] = 0;
+  for (int i = 0; i < 48; ++i) out32[i] = 0;
   return 3;
 #endif
 }
