@@ -49,6 +49,9 @@ struct FKOut {
   float at[FSB_NJ][3];
 };
 
+// FAST: MUFU sine/cosine and approximate division (bf16-mode kernels, where
+// the bar is MPJPE <= 0.5 mm; abs error of __sinf/__cosf ~1e-6 for |x| < pi).
+template <bool FAST = false>
 __device__ __forceinline__ void rodrigues3(float wx, float wy, float wz, float* r) {
   const float t2 = __fadd_rn(__fadd_rn(__fmul_rn(wx, wx), __fmul_rn(wy, wy)), __fmul_rn(wz, wz));
   const bool small = t2 < 1e-12f;
@@ -59,9 +62,15 @@ __device__ __forceinline__ void rodrigues3(float wx, float wy, float wz, float* 
   } else {
     const float th = sqrtf(t2);
     float sn, cs;
-    sincosf(th, &sn, &cs);
-    s = sn / th;
-    c = (1.0f - cs) / t2;
+    if (FAST) {
+      __sincosf(th, &sn, &cs);
+      s = __fdividef(sn, th);
+      c = __fdividef(1.0f - cs, t2);
+    } else {
+      sincosf(th, &sn, &cs);
+      s = sn / th;
+      c = (1.0f - cs) / t2;
+    }
   }
   r[0] = 1.0f - (wy * wy + wz * wz) * c;
   r[1] = wx * wy * c - wz * s;
@@ -83,12 +92,13 @@ __constant__ __device__ static const int8_t kDepth[FSB_NJ] = {0, 1, 2, 3, 4, 5, 
 // Lane j owns joint j: Rodrigues in parallel, then the chain is composed one
 // tree level at a time (8 levels instead of 22 serial joints), each joint
 // with the reference's fixed three-term accumulation order.
+template <bool FAST = false>
 __device__ __forceinline__ void fk_warp(const float* pose, const float* grest, FKOut& o, int lane) {
   const int j = lane;
   const int p = j < FSB_NJ ? kParents[j] : -1;
   float loc[9], tl[3], g[3];
   if (j < FSB_NJ) {
-    rodrigues3(pose[3 * j], pose[3 * j + 1], pose[3 * j + 2], loc);
+    rodrigues3<FAST>(pose[3 * j], pose[3 * j + 1], pose[3 * j + 2], loc);
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
       g[a] = grest[3 * j + a];
@@ -105,13 +115,17 @@ __device__ __forceinline__ void fk_warp(const float* pose, const float* grest, F
 #pragma unroll 1
   for (int lvl = 1; lvl < 8; ++lvl) {
     if (j < FSB_NJ && kDepth[j] == lvl) {
-      const float* rp = o.rw[p];
+      float rp[9], tp[3];
+#pragma unroll
+      for (int e = 0; e < 9; ++e) rp[e] = o.rw[p][e];
+#pragma unroll
+      for (int a = 0; a < 3; ++a) tp[a] = o.tw[p][a];
 #pragma unroll
       for (int a = 0; a < 3; ++a) {
 #pragma unroll
         for (int b = 0; b < 3; ++b)
           o.rw[j][3 * a + b] = rp[3 * a] * loc[b] + rp[3 * a + 1] * loc[3 + b] + rp[3 * a + 2] * loc[6 + b];
-        o.tw[j][a] = (rp[3 * a] * tl[0] + rp[3 * a + 1] * tl[1] + rp[3 * a + 2] * tl[2]) + o.tw[p][a];
+        o.tw[j][a] = (rp[3 * a] * tl[0] + rp[3 * a + 1] * tl[1] + rp[3 * a + 2] * tl[2]) + tp[a];
       }
     }
     __syncwarp();

@@ -711,39 +711,60 @@ __global__ void __launch_bounds__(NTH, 1) k_decoders_tc(DecodeArgs a, BodyW bw, 
 #ifdef FSB_PROFILE
     tpos = clock64();
 #endif
-    // positional terms of the self-attention input (decoder.py:300-303, :397-398)
-    if (body) {
-      const bool pr2 = rb >= 5 && rb < 27, pr3 = rb >= 27 && rb < 49;
+    // positional terms of the self-attention input (decoder.py:300-303,
+    // :397-398).  They change only when a prediction has been made, so they
+    // are kept in registers and recomputed at layer 0 and after each
+    // selected layer, with 16-byte loads of this thread's 32 columns.
+    const unsigned psel = body ? a.body_sel : a.hand_sel;
+    if (l == 0 || ((psel >> (l - 1)) & 1u)) {
 #pragma unroll
-      for (int i = 0; i < HC; ++i) {
-        const int c = c0 + i;
-        float v = 0.0f;
-        if (valid && pr2) {
-          const int j = rb - 5;
-          v = bx.pred[blk] ? fmaf(bx.kp2d[blk][2 * j + 1], __ldg(bw.phi2d_w + D + c),
-                                  bx.kp2d[blk][2 * j] * __ldg(bw.phi2d_w + c)) + __ldg(bw.phi2d_b + c)
-                           : __ldg(bw.p2d_init + j * D + c);
-        } else if (valid && pr3) {
-          const int j = rb - 27;
-          v = bx.pred[blk] ? fmaf(bx.jc[blk][3 * j + 2], __ldg(bw.phi3d_w + 2 * D + c),
-                                  fmaf(bx.jc[blk][3 * j + 1], __ldg(bw.phi3d_w + D + c),
-                                       bx.jc[blk][3 * j] * __ldg(bw.phi3d_w + c))) + __ldg(bw.phi3d_b + c)
-                           : __ldg(bw.p3d_init + j * D + c);
+      for (int i = 0; i < HC; ++i) pos[i] = 0.0f;
+      int j = -1, kind = 0;  // kind 1: 2-D keypoint row, 2: 3-D joint row
+      if (valid) {
+        if (body) {
+          if (rb >= 5 && rb < 27) j = rb - 5, kind = 1;
+          else if (rb >= 27 && rb < 49) j = rb - 27, kind = 2;
+        } else if (rb >= 1) {
+          j = rb - 1, kind = 1;
         }
-        pos[i] = v;
       }
-    } else {
+      const int pred = body ? bx.pred[blk] : hx.pred[blk];
+      if (kind != 0 && !pred) {
+        const float* init = body ? (kind == 1 ? bw.p2d_init : bw.p3d_init) : hw.p_init;
+        const float4* src = reinterpret_cast<const float4*>(init + j * D + c0);
 #pragma unroll
-      for (int i = 0; i < HC; ++i) {
-        const int c = c0 + i;
-        float v = 0.0f;
-        if (valid && rb >= 1) {
-          const int j = rb - 1;
-          v = hx.pred[blk] ? fmaf(hx.pts[blk][2 * j + 1], __ldg(hw.phi2d_w + D + c),
-                                  hx.pts[blk][2 * j] * __ldg(hw.phi2d_w + c)) + __ldg(hw.phi2d_b + c)
-                           : __ldg(hw.p_init + j * D + c);
+        for (int q = 0; q < HC / 4; ++q) {
+          const float4 v = __ldg(src + q);
+          pos[4 * q] = v.x; pos[4 * q + 1] = v.y; pos[4 * q + 2] = v.z; pos[4 * q + 3] = v.w;
         }
-        pos[i] = v;
+      } else if (kind == 1) {
+        const float* w = body ? bw.phi2d_w : hw.phi2d_w;
+        const float* bb = body ? bw.phi2d_b : hw.phi2d_b;
+        const float k0 = body ? bx.kp2d[blk][2 * j] : hx.pts[blk][2 * j];
+        const float k1 = body ? bx.kp2d[blk][2 * j + 1] : hx.pts[blk][2 * j + 1];
+#pragma unroll
+        for (int q = 0; q < HC / 4; ++q) {
+          const float4 w0 = __ldg(reinterpret_cast<const float4*>(w + c0) + q);
+          const float4 w1 = __ldg(reinterpret_cast<const float4*>(w + D + c0) + q);
+          const float4 b4 = __ldg(reinterpret_cast<const float4*>(bb + c0) + q);
+          pos[4 * q] = fmaf(k1, w1.x, k0 * w0.x) + b4.x;
+          pos[4 * q + 1] = fmaf(k1, w1.y, k0 * w0.y) + b4.y;
+          pos[4 * q + 2] = fmaf(k1, w1.z, k0 * w0.z) + b4.z;
+          pos[4 * q + 3] = fmaf(k1, w1.w, k0 * w0.w) + b4.w;
+        }
+      } else if (kind == 2) {
+        const float g0 = bx.jc[blk][3 * j], g1 = bx.jc[blk][3 * j + 1], g2 = bx.jc[blk][3 * j + 2];
+#pragma unroll
+        for (int q = 0; q < HC / 4; ++q) {
+          const float4 w0 = __ldg(reinterpret_cast<const float4*>(bw.phi3d_w + c0) + q);
+          const float4 w1 = __ldg(reinterpret_cast<const float4*>(bw.phi3d_w + D + c0) + q);
+          const float4 w2 = __ldg(reinterpret_cast<const float4*>(bw.phi3d_w + 2 * D + c0) + q);
+          const float4 b4 = __ldg(reinterpret_cast<const float4*>(bw.phi3d_b + c0) + q);
+          pos[4 * q] = fmaf(g2, w2.x, fmaf(g1, w1.x, g0 * w0.x)) + b4.x;
+          pos[4 * q + 1] = fmaf(g2, w2.y, fmaf(g1, w1.y, g0 * w0.y)) + b4.y;
+          pos[4 * q + 2] = fmaf(g2, w2.z, fmaf(g1, w1.z, g0 * w0.z)) + b4.z;
+          pos[4 * q + 3] = fmaf(g2, w2.w, fmaf(g1, w1.w, g0 * w0.w)) + b4.w;
+        }
       }
     }
     const float* prm = P.pacquire();
@@ -780,7 +801,7 @@ __global__ void __launch_bounds__(NTH, 1) k_decoders_tc(DecodeArgs a, BodyW bw, 
         long long th = clock64();
         P.prof[10] += th - ts3;
 #endif
-        if (t < 64) fk_warp(bx.params[t / 32], bw.joints_rest, bx.fk[t / 32], t % 32);
+        if (t < 64) fk_warp<true>(bx.params[t / 32], bw.joints_rest, bx.fk[t / 32], t % 32);
         __syncthreads();
 #ifdef FSB_PROFILE
         P.prof[11] += clock64() - th;
@@ -808,7 +829,7 @@ __global__ void __launch_bounds__(NTH, 1) k_decoders_tc(DecodeArgs a, BodyW bw, 
         if (t < 2) {
           const float* rc = hx.rc[t];
           float R[9];
-          rodrigues3(rc[0], rc[1], rc[2], R);
+          rodrigues3<true>(rc[0], rc[1], rc[2], R);
           for (int i = 0; i < 3; ++i) {
             float q[2];
             for (int ax = 0; ax < 2; ++ax)
