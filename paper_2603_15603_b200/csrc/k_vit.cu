@@ -102,22 +102,23 @@ __global__ void k_layernorm(const float* __restrict__ x, int rows, int D, const 
 // Flash attention on tcgen05 for head dim 64 (Decoder._attention,
 // decoder.py:172-203: one crop's tokens attend to each other).
 //
-// CTA = one 128-query tile of one (crop, head), 4 warps, one query row per
-// thread; thread 0 also drives TMA and the tensor core.  Two CTAs share an
-// SM (TMEM 256 columns and 112 KB of shared memory each).
+// CTA = one 128-query tile of one (crop, head); two CTAs share an SM (TMEM
+// 256 columns and 96 KB of shared memory each).  5 warps:
+//   warps 0-3  softmax, one query row per thread
+//   warp 4     TMA (Q once, K|V chunks of 64 keys through a 4-deep ring)
+//              and the tcgen05 issue, one elected lane
 // TMEM: two S buffers (128 x 64 fp32 scores) and O (128 x 64 fp32).
-// Per chunk j of 64 keys:
-//   (1) thread 0 issues S(j+1) = Q K_{j+1}^T into the other S buffer, so the
-//       next scores are computed while (2) the CTA runs the softmax of chunk
-//       j: P = exp2(S c - m) -> bf16 tile in shared memory;
-//   (3) thread 0 issues O += P V_j and refills the K|V ring (4 chunks deep,
-//       TMA 128-byte-swizzled boxes straight from the qkv matrix; V is read
-//       MN-major from the same layout).
-// The running max is rescaled lazily: O and l are corrected in TMEM only
-// when the max grows by more than 2^8 (P stays <= 256; O / l is exact).
-// Keys past T are masked to -inf; query rows past T compute on the next
-// crop's rows and are not stored.
-constexpr int FA_THREADS = 128, FA_KC = 64, FA_RING = 4;
+// The issue warp runs one chunk ahead: S(j+1) = Q K_{j+1}^T is issued as
+// soon as the softmax has released S(j-1), so the scores of chunk j+1 are
+// ready when the softmax of chunk j ends; P(j) = exp2(S c - m) is written
+// as a bf16 tile to shared memory and O += P(j) V_j is issued when all four
+// softmax warps have arrived.  The softmax warps only synchronise through
+// mbarriers (no CTA-wide barrier per chunk).  The running max is rescaled
+// lazily: O and l are corrected in TMEM only when the max grows by more
+// than 2^8 (P stays <= 256; O / l is exact).  Keys past T are masked to
+// -inf; query rows past T compute on the next crop's rows and are not
+// stored.
+constexpr int FA_THREADS = 160, FA_KC = 64, FA_RING = 4;
 constexpr uint32_t FA_Q = 0;                        // 16 KB
 constexpr uint32_t FA_KV = 16384;                   // FA_RING x (K 8 KB | V 8 KB)
 constexpr uint32_t FA_P = FA_KV + FA_RING * 16384;  // 16 KB
@@ -129,20 +130,20 @@ __global__ void __launch_bounds__(FA_THREADS, 2)
               float scale, __nv_bfloat16* __restrict__ ctx) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ uint64_t q_full, kv_full[FA_RING], s_full[2], o_full[2];
+  __shared__ uint64_t q_full, kv_full[FA_RING], s_full[2], p_full, o_full[2];
   __shared__ uint32_t tbase;
   const int qt = blockIdx.x, h = blockIdx.y, crop = blockIdx.z;
   const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
   const int row0 = crop * T;
   const int nch = (T + FA_KC - 1) / FA_KC;
-  const bool issuer = tid == 0;
-  if (issuer) {
+  if (tid == 0) {
     tc::mbar_init(&q_full, 1);
     for (int i = 0; i < FA_RING; ++i) tc::mbar_init(&kv_full[i], 1);
     for (int b = 0; b < 2; ++b) {
       tc::mbar_init(&s_full[b], 1);
       tc::mbar_init(&o_full[b], 1);  // P(j).V(j) done, j & 1 == b
     }
+    tc::mbar_init(&p_full, 4);  // the four softmax warps wrote P(j)
     tc::mbar_fence_init();
     tc::prefetch_tmap(&tmq);
     tc::prefetch_tmap(&tmkv);
@@ -153,136 +154,149 @@ __global__ void __launch_bounds__(FA_THREADS, 2)
   tc::fence_after();
   // TMEM columns: S buffer b at 64 b; O at 128
   const uint32_t sbase = tc::smem_u32(sm);
-  const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
   const uint32_t tO = tbase + 128;
-  const uint32_t id_s = tc::idesc_bf16(128, FA_KC), id_o = tc::idesc_bf16_bmn(128, 64);
-  auto load_kv = [&](int j) {
-    const int b = j % FA_RING;
-    tc::mbar_expect_tx(&kv_full[b], 16384u);
-    tc::tma_load_2d(sm + FA_KV + b * 16384, &tmkv, D + h * 64, row0 + j * FA_KC, &kv_full[b]);
-    tc::tma_load_2d(sm + FA_KV + b * 16384 + 8192, &tmkv, 2 * D + h * 64, row0 + j * FA_KC, &kv_full[b]);
-  };
-  auto issue_s = [&](int j) {  // S(j) -> S buffer j & 1
-    const int b = j % FA_RING;
-    tc::mbar_wait(&kv_full[b], (uint32_t)((j / FA_RING) & 1));
-    tc::fence_after();
-    const uint32_t k = sbase + FA_KV + b * 16384;
+
+  if (warp == 4) {
+    // TMA + MMA issue: the whole warp walks the schedule, lane 0 issues
+    const bool leader = lane == 0;
+    const uint32_t id_s = tc::idesc_bf16(128, FA_KC), id_o = tc::idesc_bf16_bmn(128, 64);
+    auto load_kv = [&](int j) {
+      const int b = j % FA_RING;
+      if (leader) {
+        tc::mbar_expect_tx(&kv_full[b], 16384u);
+        tc::tma_load_2d(sm + FA_KV + b * 16384, &tmkv, D + h * 64, row0 + j * FA_KC, &kv_full[b]);
+        tc::tma_load_2d(sm + FA_KV + b * 16384 + 8192, &tmkv, 2 * D + h * 64, row0 + j * FA_KC, &kv_full[b]);
+      }
+      __syncwarp();
+    };
+    auto issue_s = [&](int j) {  // S(j) -> S buffer j & 1
+      const int b = j % FA_RING;
+      tc::mbar_wait(&kv_full[b], (uint32_t)((j / FA_RING) & 1));
+      tc::fence_after();
+      if (leader) {
+        const uint32_t k = sbase + FA_KV + b * 16384;
 #pragma unroll
-    for (int kk = 0; kk < 4; ++kk)
-      tc::mma_bf16(tbase + 64 * (j & 1), tc::sw128_kmajor_desc(sbase + FA_Q + 32 * kk),
-                   tc::sw128_kmajor_desc(k + 32 * kk), id_s, kk > 0);
-    tc::mma_commit(&s_full[j & 1]);
-  };
-  if (issuer) {
-    tc::mbar_expect_tx(&q_full, 16384u);
-    tc::tma_load_2d(sm + FA_Q, &tmq, h * 64, row0 + qt * 128, &q_full);
+        for (int kk = 0; kk < 4; ++kk)
+          tc::mma_bf16(tbase + 64 * (j & 1), tc::sw128_kmajor_desc(sbase + FA_Q + 32 * kk),
+                       tc::sw128_kmajor_desc(k + 32 * kk), id_s, kk > 0);
+        tc::mma_commit(&s_full[j & 1]);
+      }
+      __syncwarp();
+    };
+    if (leader) {
+      tc::mbar_expect_tx(&q_full, 16384u);
+      tc::tma_load_2d(sm + FA_Q, &tmq, h * 64, row0 + qt * 128, &q_full);
+    }
+    __syncwarp();
     for (int j = 0; j < FA_RING && j < nch; ++j) load_kv(j);
     tc::mbar_wait(&q_full, 0);
     issue_s(0);
-  }
-  uint8_t* prow0 = sm + FA_P + (tid >> 3) * (FA_KC * 16) + (tid & 7) * 16;
-  const float c2 = scale * 1.4426950408889634f;
-  float m = -INFINITY, l = 0.0f;
-  for (int j = 0; j < nch; ++j) {
-    // (1) scores of the next chunk into the other S buffer (its previous
-    // contents, S(j-1), were read before the barrier that ended chunk j-1)
-    if (issuer && j + 1 < nch) issue_s(j + 1);
-    // (2) softmax of chunk j
-    tc::mbar_wait(&s_full[j & 1], (uint32_t)((j >> 1) & 1));
-    tc::fence_after();
-    float s[FA_KC];
-    tc::tmem_ld64(tbase + 64 * (j & 1) + lane_off, s);
-    const int kvalid = T - j * FA_KC;
-    if (kvalid < FA_KC) {
+    for (int j = 0; j < nch; ++j) {
+      // S(j+1): its buffer held S(j-1), released with P(j-1) (waited below
+      // in the previous iteration)
+      if (j + 1 < nch) issue_s(j + 1);
+      // O += P(j) V_j once the four softmax warps have written P(j)
+      tc::mbar_wait(&p_full, (uint32_t)(j & 1));
+      tc::fence_after();
+      if (leader) {
+        const uint32_t v = sbase + FA_KV + (j % FA_RING) * 16384 + 8192;
 #pragma unroll
-      for (int i = 0; i < FA_KC; ++i)
-        if (i >= kvalid) s[i] = -INFINITY;
+        for (int kk = 0; kk < FA_KC / 16; ++kk)
+          tc::mma_bf16(tO, tc::kmajor_desc(sbase + FA_P, FA_KC, kk * 16), tc::sw128_mnmajor_desc(v + kk * 2048, 8192),
+                       id_o, (j | kk) != 0);
+        tc::mma_commit(&o_full[j & 1]);
+      }
+      __syncwarp();
+      // refill the slot of chunk j-1 with chunk j-1+RING once P(j-1).V(j-1)
+      // is done (o_full phases are waited in order)
+      if (j >= 1 && j - 1 + FA_RING < nch) {
+        tc::mbar_wait(&o_full[(j - 1) & 1], (uint32_t)(((j - 1) >> 1) & 1));
+        load_kv(j - 1 + FA_RING);
+      }
     }
-    float m4[4] = {s[0], s[1], s[2], s[3]};
+  } else {
+    // softmax: query row r = tid of the tile
+    const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
+    uint8_t* prow = sm + FA_P + (tid >> 3) * (FA_KC * 16) + (tid & 7) * 16;
+    const float c2 = scale * 1.4426950408889634f;
+    float m = -INFINITY, l = 0.0f;
+    for (int j = 0; j < nch; ++j) {
+      tc::mbar_wait(&s_full[j & 1], (uint32_t)((j >> 1) & 1));
+      tc::fence_after();
+      float s[FA_KC];
+      tc::tmem_ld64(tbase + 64 * (j & 1) + lane_off, s);
+      const int kvalid = T - j * FA_KC;
+      if (kvalid < FA_KC) {
 #pragma unroll
-    for (int i = 4; i < FA_KC; ++i) m4[i & 3] = fmaxf(m4[i & 3], s[i]);
-    const float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])) * c2;
-    if (j == 0) {
-      m = mx;
-    } else {
-      // lazy rescale: rows whose max grew by > 2^8 move to the new max.
-      // TMEM accesses are warp-collective: the whole warp takes the branch
-      // if any of its rows needs it (alpha = 1 elsewhere).
-      const bool need = mx > m + FA_RESCALE;
-      if (__any_sync(0xffffffffu, need)) {
-        const float alpha = need ? ex2_approx(m - mx) : 1.0f;
-        // O stable: P(j-1).V(j-1) (and everything before it) done
+        for (int i = 0; i < FA_KC; ++i)
+          if (i >= kvalid) s[i] = -INFINITY;
+      }
+      float m4[4] = {s[0], s[1], s[2], s[3]};
+#pragma unroll
+      for (int i = 4; i < FA_KC; ++i) m4[i & 3] = fmaxf(m4[i & 3], s[i]);
+      const float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])) * c2;
+      if (j > 0) {
+        // P(j-1).V(j-1) done: O is stable and the P tile is free
         tc::mbar_wait(&o_full[(j - 1) & 1], (uint32_t)(((j - 1) >> 1) & 1));
         tc::fence_after();
+      }
+      if (j == 0) {
+        m = mx;
+      } else {
+        // lazy rescale: rows whose max grew by > 2^8 move to the new max.
+        // TMEM accesses are warp-collective: the whole warp takes the branch
+        // if any of its rows needs it (alpha = 1 elsewhere).
+        const bool need = mx > m + FA_RESCALE;
+        if (__any_sync(0xffffffffu, need)) {
+          const float alpha = need ? ex2_approx(m - mx) : 1.0f;
 #pragma unroll 1
-        for (int c = 0; c < 64; c += 8) {
-          float o[8];
-          tc::tmem_ld8(tO + lane_off + c, o);
+          for (int c = 0; c < 64; c += 8) {
+            float o[8];
+            tc::tmem_ld8(tO + lane_off + c, o);
 #pragma unroll
-          for (int d = 0; d < 8; ++d) o[d] *= alpha;
-          tc::tmem_st8(tO + lane_off + c, o);
+            for (int d = 0; d < 8; ++d) o[d] *= alpha;
+            tc::tmem_st8(tO + lane_off + c, o);
+          }
+          l *= alpha;
+          if (need) m = mx;
         }
-        l *= alpha;
-        if (need) m = mx;
       }
-    }
-    if (j >= 1) {
-      // the P tile was last read by P(j-1).V(j-1).  The two o_full barriers
-      // alternate, and each is waited once per phase in order.
-      tc::mbar_wait(&o_full[(j - 1) & 1], (uint32_t)(((j - 1) >> 1) & 1));
-      tc::fence_after();
-    }
-    uint8_t* prow = prow0;
-    const float nm = -m;
-    float sum4[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+      const float nm = -m;
+      float sum4[4] = {0.0f, 0.0f, 0.0f, 0.0f};
 #pragma unroll
-    for (int q = 0; q < FA_KC / 8; ++q) {
-      uint32_t w[4];
+      for (int q = 0; q < FA_KC / 8; ++q) {
+        uint32_t w[4];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        const float p0 = ex2_approx(fmaf(s[8 * q + 2 * i], c2, nm));
-        const float p1 = ex2_approx(fmaf(s[8 * q + 2 * i + 1], c2, nm));
-        sum4[i] += p0 + p1;
-        w[i] = tc::pack_bf16(p0, p1);
+        for (int i = 0; i < 4; ++i) {
+          const float p0 = ex2_approx(fmaf(s[8 * q + 2 * i], c2, nm));
+          const float p1 = ex2_approx(fmaf(s[8 * q + 2 * i + 1], c2, nm));
+          sum4[i] += p0 + p1;
+          w[i] = tc::pack_bf16(p0, p1);
+        }
+        *reinterpret_cast<uint4*>(prow + q * 128) = make_uint4(w[0], w[1], w[2], w[3]);
       }
-      *reinterpret_cast<uint4*>(prow + q * 128) = make_uint4(w[0], w[1], w[2], w[3]);
+      l += (sum4[0] + sum4[1]) + (sum4[2] + sum4[3]);
+      tc::fence_async_smem();  // P visible to the tensor core
+      tc::fence_before();      // S(j) reads and the O rescale ordered before the arrive
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&p_full);
     }
-    l += (sum4[0] + sum4[1]) + (sum4[2] + sum4[3]);
-    tc::fence_async_smem();
-    tc::fence_before();
-    __syncthreads();  // P tile written, S(j) read and O rescaled by every row
-    // (3) O += P V_j; the K|V slot of chunk j is refilled with chunk j + RING
-    // once this P.V has consumed it
-    if (issuer) {
-      tc::fence_after();
-      const int b = j % FA_RING;
-      const uint32_t v = sbase + FA_KV + b * 16384 + 8192;
-      const uint32_t p_addr = sbase + FA_P;
+    tc::mbar_wait(&o_full[(nch - 1) & 1], (uint32_t)(((nch - 1) >> 1) & 1));
+    tc::fence_after();
+    const int qrow = qt * 128 + tid;
+    const float inv = 1.0f / l;
 #pragma unroll
-      for (int kk = 0; kk < FA_KC / 16; ++kk)
-        tc::mma_bf16(tO, tc::kmajor_desc(p_addr, FA_KC, kk * 16), tc::sw128_mnmajor_desc(v + kk * 2048, 8192), id_o,
-                     (j | kk) != 0);
-      tc::mma_commit(&o_full[j & 1]);
-    }
-    // refill: P(j-1).V(j-1) completed (observed above), so the slot of
-    // chunk j-1 takes chunk j-1+RING
-    if (issuer && j >= 1 && j - 1 + FA_RING < nch) load_kv(j - 1 + FA_RING);
-  }
-  tc::mbar_wait(&o_full[(nch - 1) & 1], (uint32_t)(((nch - 1) >> 1) & 1));
-  tc::fence_after();
-  const int qrow = qt * 128 + tid;
-  const float inv = 1.0f / l;
+    for (int half = 0; half < 2; ++half) {
+      float o[32];
+      tc::tmem_ld32(tO + lane_off + 32 * half, o);
+      if (qrow < T) {
+        uint4* dst = reinterpret_cast<uint4*>(ctx + (size_t)(row0 + qrow) * D + h * 64 + 32 * half);
 #pragma unroll
-  for (int half = 0; half < 2; ++half) {
-    float o[32];
-    tc::tmem_ld32(tO + lane_off + 32 * half, o);
-    if (qrow < T) {
-      uint4* dst = reinterpret_cast<uint4*>(ctx + (size_t)(row0 + qrow) * D + h * 64 + 32 * half);
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const float* e = o + 8 * q;
-        dst[q] = make_uint4(tc::pack_bf16(e[0] * inv, e[1] * inv), tc::pack_bf16(e[2] * inv, e[3] * inv),
-                            tc::pack_bf16(e[4] * inv, e[5] * inv), tc::pack_bf16(e[6] * inv, e[7] * inv));
+        for (int q = 0; q < 4; ++q) {
+          const float* e = o + 8 * q;
+          dst[q] = make_uint4(tc::pack_bf16(e[0] * inv, e[1] * inv), tc::pack_bf16(e[2] * inv, e[3] * inv),
+                              tc::pack_bf16(e[4] * inv, e[5] * inv), tc::pack_bf16(e[6] * inv, e[7] * inv));
+        }
       }
     }
   }
