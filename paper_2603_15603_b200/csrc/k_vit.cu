@@ -102,35 +102,36 @@ __global__ void k_layernorm(const float* __restrict__ x, int rows, int D, const 
 // Flash attention on tcgen05 for head dim 64 (Decoder._attention,
 // decoder.py:172-203: one crop's tokens attend to each other).
 //
-// CTA = one 128-query tile of one (crop, head); two CTAs share an SM (TMEM
-// 256 columns and 96 KB of shared memory each).  5 warps:
+// CTA = one 128-query tile of one (crop, head); three CTAs share an SM
+// (TMEM 128 columns and 72 KB of shared memory each).  5 warps:
 //   warps 0-3  softmax, one query row per thread
-//   warp 4     TMA (Q once, K|V chunks of 64 keys through a 4-deep ring)
-//              and the tcgen05 issue, one elected lane
-// TMEM: two S buffers (128 x 64 fp32 scores) and O (128 x 64 fp32).
-// The issue warp runs one chunk ahead: S(j+1) = Q K_{j+1}^T is issued as
-// soon as the softmax has released S(j-1), so the scores of chunk j+1 are
-// ready when the softmax of chunk j ends; P(j) = exp2(S c - m) is written
-// as a bf16 tile to shared memory and O += P(j) V_j is issued when all four
-// softmax warps have arrived.  The softmax warps only synchronise through
-// mbarriers (no CTA-wide barrier per chunk).  The running max is rescaled
-// lazily: O and l are corrected in TMEM only when the max grows by more
-// than 2^8 (P stays <= 256; O / l is exact).  Keys past T are masked to
-// -inf; query rows past T compute on the next crop's rows and are not
-// stored.
-constexpr int FA_THREADS = 160, FA_KC = 64, FA_RING = 4;
-constexpr uint32_t FA_Q = 0;                        // 16 KB
-constexpr uint32_t FA_KV = 16384;                   // FA_RING x (K 8 KB | V 8 KB)
-constexpr uint32_t FA_P = FA_KV + FA_RING * 16384;  // 16 KB
+//   warp 4     TMA (Q once; K chunks of 64 keys through a 2-deep ring, V
+//              chunks through a 3-deep ring) and the tcgen05 issue, one
+//              elected lane
+// TMEM: S (128 x 64 fp32 scores) and O (128 x 64 fp32).
+// The issue warp starts S(j+1) = Q K_{j+1}^T as soon as the softmax warps
+// have copied S(j) into registers, so the tensor core works under the
+// softmax of chunk j; P(j) = exp2(S c - m) is written as a bf16 tile to
+// shared memory and O += P(j) V_j is issued when all four softmax warps
+// have arrived.  The softmax warps only synchronise through mbarriers (no
+// CTA-wide barrier per chunk).  The running max is rescaled lazily: O and l
+// are corrected in TMEM only when the max grows by more than 2^8 (P stays
+// <= 256; O / l is exact).  Keys past T are masked to -inf; query rows
+// past T compute on the next crop's rows and are not stored.
+constexpr int FA_THREADS = 160, FA_KC = 64, FA_KR = 2, FA_VR = 3;
+constexpr uint32_t FA_Q = 0;                      // 16 KB
+constexpr uint32_t FA_K = 16384;                  // FA_KR x 8 KB
+constexpr uint32_t FA_V = FA_K + FA_KR * 8192;    // FA_VR x 8 KB
+constexpr uint32_t FA_P = FA_V + FA_VR * 8192;    // 16 KB
 constexpr uint32_t FA_SMEM = FA_P + 16384;
 constexpr float FA_RESCALE = 8.0f;  // log2 units
 
-__global__ void __launch_bounds__(FA_THREADS, 2)
+__global__ void __launch_bounds__(FA_THREADS, 3)
     k_attn_tc(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtensorMap tmkv, int T, int D,
               float scale, __nv_bfloat16* __restrict__ ctx) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ uint64_t q_full, kv_full[FA_RING], s_full[2], p_full, o_full[2];
+  __shared__ uint64_t q_full, k_full[FA_KR], v_full[FA_VR], s_full, s_free, p_full, o_full[2];
   __shared__ uint32_t tbase;
   const int qt = blockIdx.x, h = blockIdx.y, crop = blockIdx.z;
   const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
@@ -138,48 +139,55 @@ __global__ void __launch_bounds__(FA_THREADS, 2)
   const int nch = (T + FA_KC - 1) / FA_KC;
   if (tid == 0) {
     tc::mbar_init(&q_full, 1);
-    for (int i = 0; i < FA_RING; ++i) tc::mbar_init(&kv_full[i], 1);
-    for (int b = 0; b < 2; ++b) {
-      tc::mbar_init(&s_full[b], 1);
-      tc::mbar_init(&o_full[b], 1);  // P(j).V(j) done, j & 1 == b
-    }
+    for (int i = 0; i < FA_KR; ++i) tc::mbar_init(&k_full[i], 1);
+    for (int i = 0; i < FA_VR; ++i) tc::mbar_init(&v_full[i], 1);
+    tc::mbar_init(&s_full, 1);
+    tc::mbar_init(&s_free, 4);  // the four softmax warps copied S(j)
     tc::mbar_init(&p_full, 4);  // the four softmax warps wrote P(j)
+    tc::mbar_init(&o_full[0], 1);  // P(j).V(j) done, j & 1 == b
+    tc::mbar_init(&o_full[1], 1);
     tc::mbar_fence_init();
     tc::prefetch_tmap(&tmq);
     tc::prefetch_tmap(&tmkv);
   }
-  if (warp == 0) tc::tmem_alloc(&tbase, 256);
+  if (warp == 0) tc::tmem_alloc(&tbase, 128);
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
-  // TMEM columns: S buffer b at 64 b; O at 128
+  // TMEM columns: S at 0; O at 64
   const uint32_t sbase = tc::smem_u32(sm);
-  const uint32_t tO = tbase + 128;
+  const uint32_t tO = tbase + 64;
 
   if (warp == 4) {
     // TMA + MMA issue: the whole warp walks the schedule, lane 0 issues
     const bool leader = lane == 0;
     const uint32_t id_s = tc::idesc_bf16(128, FA_KC), id_o = tc::idesc_bf16_bmn(128, 64);
-    auto load_kv = [&](int j) {
-      const int b = j % FA_RING;
+    auto load_k = [&](int j) {
+      const int b = j % FA_KR;
       if (leader) {
-        tc::mbar_expect_tx(&kv_full[b], 16384u);
-        tc::tma_load_2d(sm + FA_KV + b * 16384, &tmkv, D + h * 64, row0 + j * FA_KC, &kv_full[b]);
-        tc::tma_load_2d(sm + FA_KV + b * 16384 + 8192, &tmkv, 2 * D + h * 64, row0 + j * FA_KC, &kv_full[b]);
+        tc::mbar_expect_tx(&k_full[b], 8192u);
+        tc::tma_load_2d(sm + FA_K + b * 8192, &tmkv, D + h * 64, row0 + j * FA_KC, &k_full[b]);
       }
       __syncwarp();
     };
-    auto issue_s = [&](int j) {  // S(j) -> S buffer j & 1
-      const int b = j % FA_RING;
-      tc::mbar_wait(&kv_full[b], (uint32_t)((j / FA_RING) & 1));
+    auto load_v = [&](int j) {
+      const int b = j % FA_VR;
+      if (leader) {
+        tc::mbar_expect_tx(&v_full[b], 8192u);
+        tc::tma_load_2d(sm + FA_V + b * 8192, &tmkv, 2 * D + h * 64, row0 + j * FA_KC, &v_full[b]);
+      }
+      __syncwarp();
+    };
+    auto issue_s = [&](int j) {
+      tc::mbar_wait(&k_full[j % FA_KR], (uint32_t)((j / FA_KR) & 1));
       tc::fence_after();
       if (leader) {
-        const uint32_t k = sbase + FA_KV + b * 16384;
+        const uint32_t k = sbase + FA_K + (j % FA_KR) * 8192;
 #pragma unroll
         for (int kk = 0; kk < 4; ++kk)
-          tc::mma_bf16(tbase + 64 * (j & 1), tc::sw128_kmajor_desc(sbase + FA_Q + 32 * kk),
-                       tc::sw128_kmajor_desc(k + 32 * kk), id_s, kk > 0);
-        tc::mma_commit(&s_full[j & 1]);
+          tc::mma_bf16(tbase, tc::sw128_kmajor_desc(sbase + FA_Q + 32 * kk), tc::sw128_kmajor_desc(k + 32 * kk), id_s,
+                       kk > 0);
+        tc::mma_commit(&s_full);
       }
       __syncwarp();
     };
@@ -188,18 +196,25 @@ __global__ void __launch_bounds__(FA_THREADS, 2)
       tc::tma_load_2d(sm + FA_Q, &tmq, h * 64, row0 + qt * 128, &q_full);
     }
     __syncwarp();
-    for (int j = 0; j < FA_RING && j < nch; ++j) load_kv(j);
+    for (int j = 0; j < FA_KR && j < nch; ++j) load_k(j);
+    for (int j = 0; j < FA_VR && j < nch; ++j) load_v(j);
     tc::mbar_wait(&q_full, 0);
     issue_s(0);
     for (int j = 0; j < nch; ++j) {
-      // S(j+1): its buffer held S(j-1), released with P(j-1) (waited below
-      // in the previous iteration)
-      if (j + 1 < nch) issue_s(j + 1);
+      if (j + 1 < nch) {
+        // S(j+1) once the softmax warps hold S(j) in registers; S(j) has
+        // completed, so its K slot takes chunk j+2
+        tc::mbar_wait(&s_free, (uint32_t)(j & 1));
+        tc::fence_after();
+        issue_s(j + 1);
+        if (j + 2 < nch) load_k(j + 2);
+      }
       // O += P(j) V_j once the four softmax warps have written P(j)
       tc::mbar_wait(&p_full, (uint32_t)(j & 1));
+      tc::mbar_wait(&v_full[j % FA_VR], (uint32_t)((j / FA_VR) & 1));
       tc::fence_after();
       if (leader) {
-        const uint32_t v = sbase + FA_KV + (j % FA_RING) * 16384 + 8192;
+        const uint32_t v = sbase + FA_V + (j % FA_VR) * 8192;
 #pragma unroll
         for (int kk = 0; kk < FA_KC / 16; ++kk)
           tc::mma_bf16(tO, tc::kmajor_desc(sbase + FA_P, FA_KC, kk * 16), tc::sw128_mnmajor_desc(v + kk * 2048, 8192),
@@ -207,11 +222,11 @@ __global__ void __launch_bounds__(FA_THREADS, 2)
         tc::mma_commit(&o_full[j & 1]);
       }
       __syncwarp();
-      // refill the slot of chunk j-1 with chunk j-1+RING once P(j-1).V(j-1)
-      // is done (o_full phases are waited in order)
-      if (j >= 1 && j - 1 + FA_RING < nch) {
+      // V slot of chunk j-1 takes chunk j-1+VR once P(j-1).V(j-1) is done
+      // (o_full phases are waited in order)
+      if (j >= 1 && j - 1 + FA_VR < nch) {
         tc::mbar_wait(&o_full[(j - 1) & 1], (uint32_t)(((j - 1) >> 1) & 1));
-        load_kv(j - 1 + FA_RING);
+        load_v(j - 1 + FA_VR);
       }
     }
   } else {
@@ -221,10 +236,13 @@ __global__ void __launch_bounds__(FA_THREADS, 2)
     const float c2 = scale * 1.4426950408889634f;
     float m = -INFINITY, l = 0.0f;
     for (int j = 0; j < nch; ++j) {
-      tc::mbar_wait(&s_full[j & 1], (uint32_t)((j >> 1) & 1));
+      tc::mbar_wait(&s_full, (uint32_t)(j & 1));
       tc::fence_after();
       float s[FA_KC];
-      tc::tmem_ld64(tbase + 64 * (j & 1) + lane_off, s);
+      tc::tmem_ld64(tbase + lane_off, s);
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&s_free);  // S may be overwritten by S(j+1)
       const int kvalid = T - j * FA_KC;
       if (kvalid < FA_KC) {
 #pragma unroll
@@ -302,7 +320,7 @@ __global__ void __launch_bounds__(FA_THREADS, 2)
   }
   tc::fence_before();
   __syncthreads();
-  if (warp == 0) tc::tmem_dealloc(tbase, 256);
+  if (warp == 0) tc::tmem_dealloc(tbase, 128);
 }
 
 inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
