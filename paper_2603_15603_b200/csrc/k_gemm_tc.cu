@@ -6,8 +6,8 @@
 // (N-tile fastest, so CTAs running at the same time share A tiles in L2).
 // Warp 0 is the TMA producer (128-byte swizzled boxes of 64 K-elements),
 // warp 1 issues tcgen05.mma from one lane, warps 2-9 drain TMEM through the
-// epilogue (two warps per TMEM lane quadrant, each on half the columns; the
-// fp32 residual rows are fetched one chunk ahead).  A STAGES-deep ring of full/empty mbarriers feeds the tensor
+// epilogue (two warps per TMEM lane quadrant, each on half the columns;
+// 32-row blocks staged in swizzled shared memory and moved by TMA).  A STAGES-deep ring of full/empty mbarriers feeds the tensor
 // core, and the accumulator is double-buffered in TMEM (2 x BN columns):
 // the epilogue of tile i runs while the MMAs of tile i+1 accumulate into the
 // other buffer.  Epilogues (decoder.py:247-257 semantics):
@@ -25,61 +25,25 @@
 #include "gemm_tc.h"
 
 namespace {
-constexpr int BM = 128, BK = 64, STAGES = 4;
+constexpr int BM = 128, BK = 64, STAGES = 3;
+constexpr uint32_t EPI_BUF = 4096;  // per-warp staging buffer: 32 rows x 128 B, 128-byte swizzle
 constexpr int EPI_WARPS = 8;  // two per TMEM lane quadrant, each on half the columns
 constexpr int GEMM_THREADS = 64 + 32 * EPI_WARPS;
 }
 
-// 32 consecutive columns [col, col + 32) of one row.  `r` holds the
-// residual / position rows of the chunk, loaded before the TMEM read.
-__device__ __forceinline__ void gemm_epi_prefetch(const GemmEpi& epi, int row, int col, float4* r) {
-  if (epi.kind == EPI_RESID_F32) {
-    const float4* x = reinterpret_cast<const float4*>(epi.x_f32 + (size_t)row * epi.ldo + col);
-#pragma unroll
-    for (int g = 0; g < 8; ++g) r[g] = x[g];
-  } else if (epi.kind == EPI_EMBED_F32) {
-    const float4* p = reinterpret_cast<const float4*>(epi.pos + (size_t)(row % epi.T) * epi.ldo + col);
-#pragma unroll
-    for (int g = 0; g < 8; ++g) r[g] = __ldg(p + g);
-  }
-}
-
-__device__ __forceinline__ void gemm_epi_store(const GemmEpi& epi, int row, int col, const float* v, float4* r) {
-  float b[32];
-#pragma unroll
-  for (int i = 0; i < 32; i += 4) {
-    const float4 q = __ldg(reinterpret_cast<const float4*>(epi.bias + col + i));
-    b[i] = v[i] + q.x; b[i + 1] = v[i + 1] + q.y; b[i + 2] = v[i + 2] + q.z; b[i + 3] = v[i + 3] + q.w;
-  }
-  if (epi.kind == EPI_BIAS_BF16 || epi.kind == EPI_RELU_BF16) {
-    if (epi.kind == EPI_RELU_BF16)
-#pragma unroll
-      for (int i = 0; i < 32; ++i) b[i] = fmaxf(b[i], 0.0f);
-    uint4* dst = reinterpret_cast<uint4*>(epi.out_bf16 + (size_t)row * epi.ldo + col);
-#pragma unroll
-    for (int g = 0; g < 4; ++g)
-      dst[g] = make_uint4(tc::pack_bf16(b[8 * g], b[8 * g + 1]), tc::pack_bf16(b[8 * g + 2], b[8 * g + 3]),
-                          tc::pack_bf16(b[8 * g + 4], b[8 * g + 5]), tc::pack_bf16(b[8 * g + 6], b[8 * g + 7]));
-  } else {
-    float4* x = reinterpret_cast<float4*>(epi.x_f32 + (size_t)row * epi.ldo + col);
-#pragma unroll
-    for (int g = 0; g < 8; ++g) {
-      r[g].x += b[4 * g]; r[g].y += b[4 * g + 1]; r[g].z += b[4 * g + 2]; r[g].w += b[4 * g + 3];
-      x[g] = r[g];
-    }
-  }
-}
+// 128-byte-swizzled staging row: 16-byte chunk q of row r
+__device__ __forceinline__ uint32_t sw128_off(int r, int q) { return (uint32_t)(r * 128 + ((q ^ (r & 7)) << 4)); }
 
 template <int BN>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
-    k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int M, int N, int K,
-              GemmEpi epi) {
+    k_gemm_tc(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+              const __grid_constant__ CUtensorMap tmC, int M, int N, int K, GemmEpi epi) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1024-byte alignment for the 128B swizzle atoms
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   constexpr uint32_t A_BYTES = BM * BK * 2, B_BYTES = BN * BK * 2, STAGE_BYTES = A_BYTES + B_BYTES;
   constexpr uint32_t TMEM_COLS = 2 * BN;  // two accumulator buffers
-  __shared__ uint64_t full[STAGES], empty[STAGES], acc_full[2], acc_empty[2];
+  __shared__ uint64_t full[STAGES], empty[STAGES], acc_full[2], acc_empty[2], xbar[EPI_WARPS][2];
   __shared__ uint32_t tmem_base;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int nk = (K + BK - 1) / BK;
@@ -93,10 +57,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     for (int b = 0; b < 2; ++b) {
       tc::mbar_init(&acc_full[b], 1);
       tc::mbar_init(&acc_empty[b], EPI_WARPS);
+      for (int w = 0; w < EPI_WARPS; ++w) tc::mbar_init(&xbar[w][b], 1);
     }
     tc::mbar_fence_init();
     tc::prefetch_tmap(&tmA);
     tc::prefetch_tmap(&tmB);
+    tc::prefetch_tmap(&tmC);
   }
   if (warp == 1) tc::tmem_alloc(&tmem_base, TMEM_COLS);
   tc::fence_before();
@@ -150,36 +116,112 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
   } else if (warp >= 2) {
     // epilogue: warp w reads TMEM lanes 32 * (w % 4) .. +31 (rows of the
-    // tile); warps w and w + 4 split the columns
-    const int quad = warp % 4, half = (warp - 2) / 4;
+    // tile); warps w and w + 4 split the columns.  Each warp stages 32-row
+    // blocks (128-byte rows: 32 fp32 or 64 bf16 columns) in two swizzled
+    // shared-memory buffers and moves them with TMA: fp32 residual blocks
+    // are TMA-loaded, updated in shared memory and TMA-stored; bf16 blocks
+    // are written to shared memory and TMA-stored.  Global traffic is thus
+    // whole 128-byte rows, issued by the TMA engine.
+    const int ew = warp - 2, quad = warp % 4, half = ew / 4;
     constexpr int HALF = BN / 2;
-    int tc_count = 0;
+    uint8_t* stg = smem + STAGES * STAGE_BYTES + ew * 2 * EPI_BUF;
+    const bool f32 = epi.kind == EPI_RESID_F32 || epi.kind == EPI_EMBED_F32;
+    const bool resid = epi.kind == EPI_RESID_F32;
+    const int CB = f32 ? 32 : 64;  // columns per staged block
+    int tc_count = 0, nblk = 0;    // nblk: blocks staged by this warp so far
+    uint32_t xph[2] = {0u, 0u};
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tc_count) {
       const int buf = tc_count & 1;
       const int m0 = (t / ntn) * BM, n0 = (t % ntn) * BN;
-      const int row = m0 + quad * 32 + lane;
-      const bool rok = row < M;
+      const int r0 = m0 + quad * 32, row = r0 + lane;
+      const int cbase = n0 + half * HALF;
       const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(buf * BN + half * HALF);
-      float4 r[8];
-      // the first residual chunk is fetched before waiting for the MMAs
-      if (rok && n0 + half * HALF < N) gemm_epi_prefetch(epi, row, n0 + half * HALF, r);
+      const int nb = HALF / CB;
+      // residual blocks of this tile: the first two are fetched before the
+      // MMAs finish (their staging buffers are free once earlier stores
+      // have read them)
+      auto fetch = [&](int k) {
+        const int sb = (nblk + k) & 1;
+        if (lane == 0) {
+          tc::bulk_wait_read0();
+          tc::mbar_expect_tx(&xbar[ew][sb], EPI_BUF);
+          tc::tma_load_2d(stg + sb * EPI_BUF, &tmC, cbase + k * CB, r0, &xbar[ew][sb]);
+        }
+      };
+      if (resid && r0 < M) {
+        fetch(0);
+        if (nb > 1) fetch(1);
+      }
       tc::mbar_wait(&acc_full[buf], (uint32_t)((tc_count >> 1) & 1));
       tc::fence_after();
-#pragma unroll 1
-      for (int c = 0; c < HALF; c += 32) {
-        float v[32];
-        tc::tmem_ld32(taddr + c, v);
-        const int col = n0 + half * HALF + c;
-        if (rok && col < N) {
-          gemm_epi_store(epi, row, col, v, r);
-          if (c + 32 < HALF && col + 32 < N) gemm_epi_prefetch(epi, row, col + 32, r);
+      for (int k = 0; k < nb; ++k) {
+        const int sb = (nblk + k) & 1;
+        uint8_t* sbuf = stg + sb * EPI_BUF;
+        const int col = cbase + k * CB;
+        float v[64];
+        tc::tmem_ld32(taddr + k * CB, v);
+        if (!f32) tc::tmem_ld32(taddr + k * CB + 32, v + 32);
+        if (k + 1 == nb) {
+          // last TMEM read of this tile by this warp: release the buffer
+          tc::fence_before();
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive(&acc_empty[buf]);
         }
+        if (r0 >= M || col >= N) continue;  // warp-uniform
+#pragma unroll
+        for (int i = 0; i < 32; i += 4) {  // + bias (same columns for every lane)
+          const float4 q = __ldg(reinterpret_cast<const float4*>(epi.bias + col + i));
+          v[i] += q.x; v[i + 1] += q.y; v[i + 2] += q.z; v[i + 3] += q.w;
+        }
+        if (!f32) {
+          if (col + 32 < N)  // N is a multiple of 32; the TMA store clips columns >= N
+#pragma unroll
+            for (int i = 32; i < 64; i += 4) {
+              const float4 q = __ldg(reinterpret_cast<const float4*>(epi.bias + col + i));
+              v[i] += q.x; v[i + 1] += q.y; v[i + 2] += q.z; v[i + 3] += q.w;
+            }
+          if (epi.kind == EPI_RELU_BF16)
+#pragma unroll
+            for (int i = 0; i < 64; ++i) v[i] = fmaxf(v[i], 0.0f);
+          if (lane == 0) tc::bulk_wait_read0();  // the store that last used this buffer has read it
+          __syncwarp();
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            *reinterpret_cast<uint4*>(sbuf + sw128_off(lane, q)) =
+                make_uint4(tc::pack_bf16(v[8 * q], v[8 * q + 1]), tc::pack_bf16(v[8 * q + 2], v[8 * q + 3]),
+                           tc::pack_bf16(v[8 * q + 4], v[8 * q + 5]), tc::pack_bf16(v[8 * q + 6], v[8 * q + 7]));
+        } else if (resid) {
+          tc::mbar_wait(&xbar[ew][sb], xph[sb]);
+          xph[sb] ^= 1u;
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            float4* p = reinterpret_cast<float4*>(sbuf + sw128_off(lane, q));
+            float4 x = *p;
+            x.x += v[4 * q]; x.y += v[4 * q + 1]; x.z += v[4 * q + 2]; x.w += v[4 * q + 3];
+            *p = x;
+          }
+        } else {  // EPI_EMBED_F32: x = (acc + bias) + pos[row % T]
+          if (lane == 0) tc::bulk_wait_read0();
+          __syncwarp();
+          const float4* pr = reinterpret_cast<const float4*>(epi.pos + (size_t)(row % epi.T) * epi.ldo + col);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const float4 pp = __ldg(pr + q);
+            *reinterpret_cast<float4*>(sbuf + sw128_off(lane, q)) =
+                make_float4(v[4 * q] + pp.x, v[4 * q + 1] + pp.y, v[4 * q + 2] + pp.z, v[4 * q + 3] + pp.w);
+          }
+        }
+        tc::fence_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tc::tma_store_2d(&tmC, col, r0, sbuf);
+          tc::bulk_commit();
+        }
+        if (resid && k + 2 < nb) fetch(k + 2);
       }
-      // this warp's TMEM reads are complete: hand the buffer back to the MMA warp
-      tc::fence_before();
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(&acc_empty[buf]);
+      nblk += nb;
     }
+    if (lane == 0) tc::bulk_wait0();  // stores complete before the CTA exits
   }
   tc::fence_before();
   __syncthreads();
@@ -215,9 +257,24 @@ bool make_tmap_bf16(CUtensorMap* map, const void* base, uint64_t rows, uint64_t 
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// row-major fp32 matrix as a 2-D tensor map with (box_rows x 32)-element
+// boxes (128-byte rows), 128-byte swizzle
+static bool make_tmap_f32(CUtensorMap* map, const void* base, uint64_t rows, uint64_t cols, uint64_t ld,
+                          uint32_t box_rows) {
+  auto enc = tmap_encoder();
+  if (!enc) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {ld * 4};
+  cuuint32_t box[2] = {32, box_rows};
+  cuuint32_t es[2] = {1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<void*>(base), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 template <int BN>
 static constexpr size_t gemm_smem() {
-  return (size_t)STAGES * (BM * BK * 2 + BN * BK * 2) + 1024;
+  return (size_t)STAGES * (BM * BK * 2 + BN * BK * 2) + (size_t)EPI_WARPS * 2 * EPI_BUF + 1024;
 }
 
 cudaError_t init_attrs_gemm_tc() {
@@ -240,9 +297,13 @@ cudaError_t launch_gemm_tc(const __nv_bfloat16* A, int lda, const __nv_bfloat16*
     if (e != cudaSuccess) return e;
     attrs = true;
   }
-  CUtensorMap ta, tb;
+  CUtensorMap ta, tb, tc_;
   const int BN = (N % 256 == 0) ? 256 : 128;
   if (!make_tmap_bf16(&ta, A, M, K, lda, BM) || !make_tmap_bf16(&tb, W, N, K, ldw, BN))
+    return cudaErrorInvalidValue;
+  // epilogue blocks: 32 rows x 128 bytes (fp32: 32 columns, bf16: 64)
+  const bool f32 = epi.kind == EPI_RESID_F32 || epi.kind == EPI_EMBED_F32;
+  if (f32 ? !make_tmap_f32(&tc_, epi.x_f32, M, N, epi.ldo, 32) : !make_tmap_bf16(&tc_, epi.out_bf16, M, N, epi.ldo, 32))
     return cudaErrorInvalidValue;
   static int sms = 0;
   if (sms == 0) {
@@ -253,9 +314,9 @@ cudaError_t launch_gemm_tc(const __nv_bfloat16* A, int lda, const __nv_bfloat16*
   const int64_t tiles = (int64_t)((N + BN - 1) / BN) * ((M + BM - 1) / BM);
   const dim3 grid((unsigned)(tiles < sms ? tiles : sms));  // persistent: one CTA per SM
   if (BN == 256)
-    k_gemm_tc<256><<<grid, GEMM_THREADS, gemm_smem<256>(), st>>>(ta, tb, M, N, K, epi);
+    k_gemm_tc<256><<<grid, GEMM_THREADS, gemm_smem<256>(), st>>>(ta, tb, tc_, M, N, K, epi);
   else
-    k_gemm_tc<128><<<grid, GEMM_THREADS, gemm_smem<128>(), st>>>(ta, tb, M, N, K, epi);
+    k_gemm_tc<128><<<grid, GEMM_THREADS, gemm_smem<128>(), st>>>(ta, tb, tc_, M, N, K, epi);
   return cudaGetLastError();
 }
 
