@@ -25,9 +25,15 @@
 #include "gemm_tc.h"
 
 namespace {
-constexpr int BM = 128, BK = 64, STAGES = 3;
+#ifndef GEMM_STAGES
+#define GEMM_STAGES 4
+#endif
+#ifndef GEMM_EPI_WARPS
+#define GEMM_EPI_WARPS 4
+#endif
+constexpr int BM = 128, BK = 64, STAGES = GEMM_STAGES;
 constexpr uint32_t EPI_BUF = 4096;  // per-warp staging buffer: 32 rows x 128 B, 128-byte swizzle
-constexpr int EPI_WARPS = 8;  // two per TMEM lane quadrant, each on half the columns
+constexpr int EPI_WARPS = GEMM_EPI_WARPS;  // 4: one per TMEM lane quadrant; 8: two, each on half the columns
 constexpr int GEMM_THREADS = 64 + 32 * EPI_WARPS;
 }
 
@@ -123,7 +129,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     // are written to shared memory and TMA-stored.  Global traffic is thus
     // whole 128-byte rows, issued by the TMA engine.
     const int ew = warp - 2, quad = warp % 4, half = ew / 4;
-    constexpr int HALF = BN / 2;
+    constexpr int HALF = BN / (EPI_WARPS / 4);
     uint8_t* stg = smem + STAGES * STAGE_BYTES + ew * 2 * EPI_BUF;
     const bool f32 = epi.kind == EPI_RESID_F32 || epi.kind == EPI_EMBED_F32;
     const bool resid = epi.kind == EPI_RESID_F32;
