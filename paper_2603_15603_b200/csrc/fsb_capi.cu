@@ -177,7 +177,10 @@ bool default_model(const fsb_decoder_config& c) {
          c.body_layers <= 8 && c.hand_layers <= 8;
 }
 
-constexpr int kVitChunk = 128;  // crops per large-config encoder pass
+#ifndef FSB_VIT_CHUNK
+#define FSB_VIT_CHUNK 256
+#endif
+constexpr int kVitChunk = FSB_VIT_CHUNK;  // crops per large-config encoder pass
 
 int layer_count(uint32_t sel) { return __builtin_popcount(sel); }
 
