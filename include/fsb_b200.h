@@ -154,6 +154,13 @@ int fsb_frame_batch(fsb_ctx* ctx, const float* images, int B, int H, int W, cons
                     uint32_t body_sel, uint32_t hand_sel, int precision, const fsb_frame_outputs* out,
                     void* stream);
 
+/* projection.denoise (projection.py:684-697): poses (B, 63) body-pose
+ * parameters -> out (B, 63) = x + relu(x W1 + b1) W2 + b2, W1 (63, hidden),
+ * W2 (hidden, 63), hidden <= 128; bit-identical to the reference's
+ * numkit.matmul order */
+int fsb_denoise(fsb_ctx* ctx, const float* poses, int B, const float* w1, const float* b1, const float* w2,
+                const float* b2, int hidden, float* out, void* stream);
+
 /* priors.render_scene (priors.py:237-252) for B scenes: `scenes` is a
  * device array of 464-byte records {float kp[44]; float half_color[66];
  * float inv_two_sigma2; float pad; double gdir[2]} -> (B, H, W, 3) f32 */

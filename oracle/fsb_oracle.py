@@ -463,3 +463,18 @@ def frame_to_smpl(image, kp, W, cfg, mhr, smpl, bmap, pw, trace=None):
     return dict(body_box=b, hand_boxes=hands, prompt=prompt, crops=crops,
                 feats=feats, body_params=params, body_cam=cam, hand_rots=rots,
                 merged=merged, v_mhr=v_mhr[0], theta=theta[0], j_smpl=j_smpl[0])
+
+
+# ---------------------------------------------------------------------------
+# kinematic-prior denoiser (projection.py:684-697)
+
+
+def denoise(w1, b1, w2, b2, x):
+    """projection._denoise_forward (projection.py:684-686):
+    x + (matmul(relu(matmul(x, w1) + b1), w2) + b2), numkit.matmul order."""
+    x = np.asarray(x, F32)
+    single = x.ndim == 1
+    x2 = x[None] if single else x
+    h = np.maximum(mm(x2, w1) + np.asarray(b1, F32), F32(0.0))
+    out = x2 + (mm(h, w2) + np.asarray(b2, F32))
+    return out[0] if single else out

@@ -45,6 +45,8 @@ cudaError_t launch_crop_grid(const double* boxes, int n, int S, float* out, cuda
 cudaError_t launch_bridge(const float* V, int B, int nv, const int32_t* corners, const float* w, int nt, float* out,
                           cudaStream_t st);
 cudaError_t launch_render(const void* scenes, int B, int H, int W, float* out, cudaStream_t st);
+cudaError_t launch_denoise(const float* x, int B, const float* w1, const float* b1, const float* w2, const float* b2,
+                           int H, float* out, int* nonfinite, cudaStream_t st);
 cudaError_t init_attrs_transformer();
 cudaError_t init_attrs_transformer_tc();
 cudaError_t init_attrs_mlp_tc();
@@ -1152,6 +1154,15 @@ int fsb_frame_batch(fsb_ctx* c, const float* images, int B, int H, int W, const 
   c->counters.fk += (int64_t)B * (nb + 2 * nh);
   c->counters.project += (int64_t)B * (nb + 2 * nh);
   c->counters.intermediate += (int64_t)B * nb;
+  return FSB_OK;
+}
+
+int fsb_denoise(fsb_ctx* c, const float* poses, int B, const float* w1, const float* b1, const float* w2,
+                const float* b2, int hidden, float* out, void* stream) {
+  if (B < 0) return fail(c, FSB_ERR_SHAPE, "denoise: negative batch");
+  if (hidden <= 0 || hidden > 128) return fail(c, FSB_ERR_USAGE, "denoise: hidden width %d not in [1, 128]", hidden);
+  FSB_CUDA(c, launch_denoise(poses, B, w1, b1, w2, b2, hidden, out, c->d_flag, (cudaStream_t)stream));
+  c->launches += B > 0;
   return FSB_OK;
 }
 

@@ -1,0 +1,52 @@
+// projection.denoise (reference projection.py:684-697, _denoise_forward
+// :684-686): out = x + (relu(x W1 + b1) W2 + b2) on (B, 63) body poses, the
+// kinematic-prior residual MLP.
+//
+// One warp per pose.  Both matrix products follow numkit.matmul
+// (numkit.py:78-90): every dot product is a left-to-right sum from +0 with a
+// separately rounded product and add, so the result is bit-identical to the
+// reference; lane j owns hidden units j, j + 32, ..., lanes own outputs
+// m = lane and m = lane + 32.  Weights are read from global memory (L2
+// resident, 16 KB at the default width).
+#include "fsb_common.cuh"
+
+namespace {
+constexpr int kDnWarps = 4;
+constexpr int kDnMaxHidden = 128;
+constexpr int kDnIn = 63;
+}  // namespace
+
+__global__ void __launch_bounds__(32 * kDnWarps) k_denoise(const float* __restrict__ x, int B, const float* __restrict__ w1,
+                                                          const float* __restrict__ b1, const float* __restrict__ w2,
+                                                          const float* __restrict__ b2, int H, float* __restrict__ out,
+                                                          int* nonfinite) {
+  __shared__ float xs[kDnWarps][64];
+  __shared__ float hs[kDnWarps][kDnMaxHidden];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int b = blockIdx.x * kDnWarps + warp;
+  if (b >= B) return;  // warp-uniform
+  const float* xb = x + (int64_t)b * kDnIn;
+  for (int k = lane; k < kDnIn; k += 32) xs[warp][k] = xb[k];
+  __syncwarp();
+  for (int j = lane; j < H; j += 32) {
+    float acc = 0.0f;
+    for (int k = 0; k < kDnIn; ++k) acc = __fadd_rn(acc, __fmul_rn(xs[warp][k], __ldg(w1 + (int64_t)k * H + j)));
+    hs[warp][j] = fmaxf(__fadd_rn(acc, __ldg(b1 + j)), 0.0f);
+  }
+  __syncwarp();
+  for (int m = lane; m < kDnIn; m += 32) {
+    float acc = 0.0f;
+    for (int j = 0; j < H; ++j) acc = __fadd_rn(acc, __fmul_rn(hs[warp][j], __ldg(w2 + (int64_t)j * kDnIn + m)));
+    const float v = __fadd_rn(xs[warp][m], __fadd_rn(acc, __ldg(b2 + m)));
+    flag_nonfinite(nonfinite, v);
+    out[(int64_t)b * kDnIn + m] = v;
+  }
+}
+
+cudaError_t launch_denoise(const float* x, int B, const float* w1, const float* b1, const float* w2, const float* b2,
+                           int H, float* out, int* nonfinite, cudaStream_t st) {
+  if (B == 0) return cudaSuccess;
+  if (H <= 0 || H > kDnMaxHidden) return cudaErrorInvalidValue;
+  k_denoise<<<(B + kDnWarps - 1) / kDnWarps, 32 * kDnWarps, 0, st>>>(x, B, w1, b1, w2, b2, H, out, nonfinite);
+  return cudaGetLastError();
+}

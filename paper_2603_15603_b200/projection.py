@@ -129,3 +129,44 @@ def project_forward(v, bmap, weights, subsample=None):
     if subsample is not None and not np.array_equal(np.asarray(subsample), weights.subsample):
         weights = ProjectorWeights(**{**weights.__dict__, "subsample": np.asarray(subsample, np.int64)})
     return _project(a[None], bmap, weights, "fp32")[0]
+
+
+# ---------------------------------------------------------------------------
+# kinematic-prior denoiser
+
+
+@dataclass
+class DenoiserWeights:
+    """(projection.py:669-674): W1 (63, hidden), b1, W2 (hidden, 63), b2."""
+
+    w1: np.ndarray
+    b1: np.ndarray
+    w2: np.ndarray
+    b2: np.ndarray
+
+
+def denoise(weights, pose):
+    """Nudge a (possibly noisy) body pose toward the training manifold
+    (projection.py:689-697): x + (relu(x W1 + b1) W2 + b2) on (63,) or
+    (B, 63) poses, on the GPU (k_denoise, bit-identical to the reference's
+    numkit.matmul order).  numpy in -> numpy out; CUDA tensors stay on the
+    device."""
+    torch = runtime._torch()
+    ctx = runtime.default_context()
+    was_np = not isinstance(pose, torch.Tensor)
+    p = np.asarray(pose, DTYPE) if was_np else pose
+    single = p.ndim == 1
+    if p.ndim not in (1, 2) or p.shape[-1] != 63:
+        raise ShapeError("denoise expects (..., 63) body poses")
+    x, _ = runtime.to_device(p[None] if single else p, torch.float32, torch)
+    h = int(np.asarray(weights.w1).shape[1])
+    if np.asarray(weights.w1).shape != (63, h) or np.asarray(weights.w2).shape != (h, 63):
+        raise ShapeError("denoiser weights must be (63, h) and (h, 63)")
+    dev = [runtime.to_device(np.ascontiguousarray(a, DTYPE), torch.float32, torch)[0]
+           for a in (weights.w1, weights.b1, weights.w2, weights.b2)]
+    out = torch.empty_like(x)
+    ctx.check(ctx.lib.fsb_denoise(ctx.h, runtime.ptr(x), x.shape[0], *[runtime.ptr(t) for t in dev], h,
+                                  runtime.ptr(out), ctx.stream), "denoise")
+    ctx.check_finite("denoise")
+    res = out[0] if single else out
+    return res.cpu().numpy() if was_np else res

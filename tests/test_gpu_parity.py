@@ -370,3 +370,18 @@ def test_nonfinite_image_raises(torch, pipe, frames):
     imgs[1, :, :, :] = np.nan
     with pytest.raises(nk.NumericError):
         pipe.run_batch(imgs, kps)
+
+
+def test_denoise_bitexact_vs_reference_golden(torch):
+    """projection.denoise on the GPU equals the reference's output bit for bit
+    (tools/make_golden_denoise.py), batched and single-pose."""
+    import os
+
+    from paper_2603_15603_b200 import projection as pj
+
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "denoise.npz"))
+    w = pj.DenoiserWeights(g["w1"], g["b1"], g["w2"], g["b2"])
+    assert np.array_equal(pj.denoise(w, g["x"]), g["out"])
+    assert np.array_equal(pj.denoise(w, g["x"][3]), g["out3"])
+    with pytest.raises(ValueError):
+        pj.denoise(w, g["x"][:, :60])

@@ -171,3 +171,16 @@ def test_known_answers():
     im = np.arange(12, dtype=np.float32).reshape(2, 2, 3)
     out = orc.bilinear_sample(im, np.array([[-5.0, -5.0], [9.0, 9.0]], np.float32))
     assert np.array_equal(out, np.stack([im[0, 0], im[1, 1]]))
+
+
+def test_denoise_oracle_matches_reference_golden():
+    """oracle.denoise against the reference's own projection.denoise
+    (tools/make_golden_denoise.py), bit for bit."""
+    import os
+
+    import oracle as orc
+
+    g = np.load(os.path.join(os.path.dirname(__file__), "golden", "denoise.npz"))
+    out = orc.denoise(g["w1"], g["b1"], g["w2"], g["b2"], g["x"])
+    assert np.array_equal(out, g["out"])
+    assert np.array_equal(orc.denoise(g["w1"], g["b1"], g["w2"], g["b2"], g["x"][3]), g["out3"])
