@@ -135,3 +135,40 @@ def skin_batch(template, pose_vecs, correctives=False, use_kernel=None):
 
 def skin(template, pose, correctives=False, use_kernel=True):
     return skin_batch(template, pose.as_vector()[None, :], correctives=correctives)[0]
+
+
+# ---------------------------------------------------------------------------
+# template files (bodymodel.py:655-688): float arrays as FSB1, name, parents
+# and faces in a JSON sidecar
+
+_FLOAT_FIELDS = ("vertices_rest", "joints_rest", "skin_weights", "shape_basis", "corrective_basis",
+                 "corrective_gate")
+
+
+def save_template(template, dirpath):
+    import json
+    import os
+
+    from .numkit import write_fsb1
+
+    os.makedirs(dirpath, exist_ok=True)
+    for name in _FLOAT_FIELDS:
+        write_fsb1(os.path.join(dirpath, name + ".fsb1"), getattr(template, name))
+    with open(os.path.join(dirpath, "meta.json"), "w") as fh:
+        json.dump({"name": template.name, "parents": np.asarray(template.parents).tolist(),
+                   "faces": np.asarray(template.faces).tolist()}, fh)
+
+
+def load_template(dirpath):
+    import json
+    import os
+
+    from .numkit import read_fsb1
+
+    with open(os.path.join(dirpath, "meta.json")) as fh:
+        meta = json.load(fh)
+    arrays = {name: read_fsb1(os.path.join(dirpath, name + ".fsb1")) for name in _FLOAT_FIELDS}
+    t = BodyTemplate(name=meta["name"], faces=np.asarray(meta["faces"], dtype=np.int64),
+                     parents=np.asarray(meta["parents"], dtype=np.int64), **arrays)
+    validate_template(t)
+    return t

@@ -170,3 +170,111 @@ def denoise(weights, pose):
     ctx.check_finite("denoise")
     res = out[0] if single else out
     return res.cpu().numpy() if was_np else res
+
+
+# ---------------------------------------------------------------------------
+# on-disk formats: FSB1 arrays plus a JSON manifest,
+# the same files the reference writes (projection.py:793-874), so weights
+# trained with the reference load into the GPU path and vice versa.
+
+_PROJECTOR_ARRAYS = ("w1", "b1", "w2", "b2", "w3", "b3")
+_DENOISER_ARRAYS = ("w1", "b1", "w2", "b2")
+
+
+def _manifest(path):
+    import json
+    import os
+
+    with open(os.path.join(path, "manifest.json")) as fh:
+        return json.load(fh)
+
+
+def _write_manifest(path, obj):
+    import json
+    import os
+
+    with open(os.path.join(path, "manifest.json"), "w") as fh:
+        json.dump(obj, fh, indent=1)
+
+
+def save_projector(path, weights):
+    """(projection.py:797-806): <name>.fsb1 per layer array; the manifest
+    holds the kind, hidden widths and the subsample indices."""
+    import os
+
+    from .numkit import write_fsb1
+
+    os.makedirs(path, exist_ok=True)
+    for name in _PROJECTOR_ARRAYS:
+        write_fsb1(os.path.join(path, name + ".fsb1"), getattr(weights, name))
+    _write_manifest(path, {"kind": "projector",
+                           "hidden": [int(weights.w1.shape[1]), int(weights.w2.shape[1])],
+                           "subsample": [int(i) for i in weights.subsample]})
+
+
+def load_projector(path):
+    """(projection.py:809-819)"""
+    import os
+
+    from .numkit import read_fsb1
+
+    man = _manifest(path)
+    if man.get("kind") != "projector":
+        raise UsageError("%s does not hold projector weights" % path)
+    arrs = {name: read_fsb1(os.path.join(path, name + ".fsb1")) for name in _PROJECTOR_ARRAYS}
+    return ProjectorWeights(subsample=np.asarray(man["subsample"], np.int64), mask=_output_mask(), **arrs)
+
+
+def save_denoiser(path, weights):
+    """(projection.py:822-827)"""
+    import os
+
+    from .numkit import write_fsb1
+
+    os.makedirs(path, exist_ok=True)
+    for name in _DENOISER_ARRAYS:
+        write_fsb1(os.path.join(path, name + ".fsb1"), getattr(weights, name))
+    _write_manifest(path, {"kind": "denoiser", "hidden": int(weights.w1.shape[1])})
+
+
+def load_denoiser(path):
+    """(projection.py:830-837)"""
+    import os
+
+    from .numkit import read_fsb1
+
+    if _manifest(path).get("kind") != "denoiser":
+        raise UsageError("%s does not hold denoiser weights" % path)
+    return DenoiserWeights(**{name: read_fsb1(os.path.join(path, name + ".fsb1")) for name in _DENOISER_ARRAYS})
+
+
+def save_bary_map(path, bmap):
+    """(projection.py:840-856): face ids and corner ids go through FSB1's
+    float32 payload (exact below 2^24)."""
+    import os
+
+    from .numkit import write_fsb1
+
+    if bmap.corners is None:
+        raise UsageError("refusing to store a BaryMap without corner indices")
+    os.makedirs(path, exist_ok=True)
+    write_fsb1(os.path.join(path, "face_index.fsb1"), np.asarray(bmap.face_index).astype(np.int64))
+    write_fsb1(os.path.join(path, "weights.fsb1"), bmap.weights)
+    write_fsb1(os.path.join(path, "corners.fsb1"), np.asarray(bmap.corners).astype(np.int64))
+    _write_manifest(path, {"kind": "bary_map", "targets": int(np.asarray(bmap.face_index).shape[0]),
+                           "degenerate_targets": [int(i) for i in bmap.degenerate_targets]})
+
+
+def load_bary_map(path):
+    """(projection.py:859-874)"""
+    import os
+
+    from .numkit import read_fsb1
+
+    man = _manifest(path)
+    if man.get("kind") != "bary_map":
+        raise UsageError("%s does not hold a barycentric map" % path)
+    return BaryMap(face_index=read_fsb1(os.path.join(path, "face_index.fsb1")).astype(np.int64),
+                   weights=read_fsb1(os.path.join(path, "weights.fsb1")),
+                   corners=read_fsb1(os.path.join(path, "corners.fsb1")).astype(np.int64),
+                   degenerate_targets=np.asarray(man["degenerate_targets"], dtype=np.int64))
