@@ -154,6 +154,19 @@ int fsb_frame_batch(fsb_ctx* ctx, const float* images, int B, int H, int W, cons
                     uint32_t body_sel, uint32_t hand_sel, int precision, const fsb_frame_outputs* out,
                     void* stream);
 
+/* projection.fit_batch (projection.py:321-370): `steps` Adam iterations of
+ * the fit objective (_fit_terms :266-287) per mesh against the bridged
+ * targets (B, nv, 3) on the template loaded in the FSB_SMPL slot, from init
+ * (B, 76) or the rest pose (NULL); analytic gradient.  scratch: B*nv*6
+ * floats.  Outputs: best_params (B, 76), vertex_error (B,) f64 mean vertex
+ * gap of the best iterate, err_curve (B, steps + 1) f64 best-so-far gap per
+ * evaluated iterate (the reference's curve is its mean over the batch);
+ * grad0 (B, 76), nullable: the objective's gradient at init
+ * (projection.fit_objective_grad, :303-309). */
+int fsb_fit_batch(fsb_ctx* ctx, const float* target, int B, int nv, const float* init, int steps, double lr,
+                  float lambda_pose, float lambda_shape, float* scratch, float* best_params, double* vertex_error,
+                  double* err_curve, float* grad0, void* stream);
+
 /* projection.denoise (projection.py:684-697): poses (B, 63) body-pose
  * parameters -> out (B, 63) = x + relu(x W1 + b1) W2 + b2, W1 (63, hidden),
  * W2 (hidden, 63), hidden <= 128; bit-identical to the reference's

@@ -45,6 +45,9 @@ cudaError_t launch_crop_grid(const double* boxes, int n, int S, float* out, cuda
 cudaError_t launch_bridge(const float* V, int B, int nv, const int32_t* corners, const float* w, int nt, float* out,
                           cudaStream_t st);
 cudaError_t launch_render(const void* scenes, int B, int H, int W, float* out, cudaStream_t st);
+cudaError_t launch_fit(const TemplateDev& t, const float* target, int B, const float* init, int steps, double lr,
+                       float lambda_pose, float lambda_shape, float* scratch, float* best, double* err, double* curve,
+                       float* grad0, int* nonfinite, cudaStream_t st);
 cudaError_t launch_denoise(const float* x, int B, const float* w1, const float* b1, const float* w2, const float* b2,
                            int H, float* out, int* nonfinite, cudaStream_t st);
 cudaError_t init_attrs_transformer();
@@ -709,6 +712,20 @@ int fsb_load_template(fsb_ctx* c, int which, int nv, const float* v_rest, const 
       memcpy(&r[34 + NZ + z], &jid, 4);
     }
   }
+  // skin weights by joint (CSR) for the iterative fit
+  std::vector<int> joff(FSB_NJ + 1, 0), jv;
+  std::vector<float> jw;
+  for (int j = 0; j < FSB_NJ; ++j) {
+    joff[j] = (int)jv.size();
+    for (int v = 0; v < nv; ++v) {
+      const float w = skin_weights[(size_t)v * FSB_NJ + j];
+      if (w != 0.0f) {
+        jv.push_back(v);
+        jw.push_back(w);
+      }
+    }
+  }
+  joff[FSB_NJ] = (int)jv.size();
   Packer pk;
   const size_t o_v = pk.add(v_rest, (size_t)nv * 12);
   const size_t o_s = pk.add(shape_basis, (size_t)nv * 30 * 4);
@@ -716,6 +733,9 @@ int fsb_load_template(fsb_ctx* c, int which, int nv, const float* v_rest, const 
   const size_t o_w = pk.add(sw.data(), sw.size() * 4);
   const size_t o_g = pk.add(joints_rest, FSB_NJ * 12);
   const size_t o_r = pk.add(rec.data(), rec.size() * 4);
+  const size_t o_jo = pk.add(joff.data(), joff.size() * 4);
+  const size_t o_jv = pk.add(jv.data(), jv.size() * 4 + 4);
+  const size_t o_jw = pk.add(jw.data(), jw.size() * 4 + 4);
   DevMem& m = c->tmpl_mem[which];
   FSB_CUDA(c, m.alloc(pk.host.size()));
   FSB_CUDA(c, cudaMemcpy(m.p, pk.host.data(), pk.host.size(), cudaMemcpyHostToDevice));
@@ -729,6 +749,9 @@ int fsb_load_template(fsb_ctx* c, int which, int nv, const float* v_rest, const 
   t.skin_w = reinterpret_cast<const float*>(base + o_w);
   t.joints_rest = reinterpret_cast<const float*>(base + o_g);
   t.rec = reinterpret_cast<const float*>(base + o_r);
+  t.joint_off = reinterpret_cast<const int*>(base + o_jo);
+  t.joint_v = reinterpret_cast<const int*>(base + o_jv);
+  t.joint_w = reinterpret_cast<const float*>(base + o_jw);
   c->has_tmpl[which] = true;
   if (which == FSB_SMPL) c->body.joints_rest = t.joints_rest;
   c->drop_graphs();
@@ -1154,6 +1177,21 @@ int fsb_frame_batch(fsb_ctx* c, const float* images, int B, int H, int W, const 
   c->counters.fk += (int64_t)B * (nb + 2 * nh);
   c->counters.project += (int64_t)B * (nb + 2 * nh);
   c->counters.intermediate += (int64_t)B * nb;
+  return FSB_OK;
+}
+
+int fsb_fit_batch(fsb_ctx* c, const float* target, int B, int nv, const float* init, int steps, double lr,
+                  float lambda_pose, float lambda_shape, float* scratch, float* best_params, double* vertex_error,
+                  double* err_curve, float* grad0, void* stream) {
+  if (!c->has_tmpl[FSB_SMPL]) return fail(c, FSB_ERR_USAGE, "fit_batch: no target template loaded (FSB_SMPL slot)");
+  const TemplateDev& t = c->tmpl[FSB_SMPL];
+  if (B < 0 || nv != t.nv) return fail(c, FSB_ERR_SHAPE, "fit_batch: targets have %d vertices, template %d", nv, t.nv);
+  if (steps < 1) return fail(c, FSB_ERR_USAGE, "FitConfig.steps must be at least 1");
+  if (!scratch || !best_params || !vertex_error || !err_curve)
+    return fail(c, FSB_ERR_USAGE, "fit_batch: scratch and outputs are required");
+  FSB_CUDA(c, launch_fit(t, target, B, init, steps, lr, lambda_pose, lambda_shape, scratch, best_params, vertex_error,
+                         err_curve, grad0, c->d_flag, (cudaStream_t)stream));
+  c->launches += B > 0;
   return FSB_OK;
 }
 

@@ -128,6 +128,10 @@ struct TemplateDev {
   const int16_t* skin_j;     // (nv, nnz) joint ids, ascending, padded with 0
   const float* skin_w;       // (nv, nnz) weights, padded with 0
   const float* joints_rest;  // (22, 3)
+  // skin weights by joint (CSR) for the fit's dL/dA reduction (k_fit.cu)
+  const int* joint_off;      // (23)
+  const int* joint_v;        // vertex ids
+  const float* joint_w;      // weights
 };
 
 // barycentric map + projector

@@ -278,3 +278,102 @@ def load_bary_map(path):
                    weights=read_fsb1(os.path.join(path, "weights.fsb1")),
                    corners=read_fsb1(os.path.join(path, "corners.fsb1")).astype(np.int64),
                    degenerate_targets=np.asarray(man["degenerate_targets"], dtype=np.int64))
+
+
+# ---------------------------------------------------------------------------
+# iterative fit: the reference's slow conversion
+# baseline (projection.py:211-370), on the GPU (k_fit.cu)
+
+
+@dataclass
+class FitConfig:
+    """(projection.py:211-219)"""
+
+    steps: int = 300
+    lr: float = 0.05
+    lambda_pose: float = 1e-3
+    lambda_shape: float = 1e-2
+
+    def __post_init__(self):
+        if self.steps < 1:
+            raise UsageError("FitConfig.steps must be at least 1")
+
+
+@dataclass
+class FitBatchResult:
+    """(projection.py:222-226)"""
+
+    params: np.ndarray
+    vertex_error: np.ndarray
+    curve: np.ndarray
+
+
+_FIT_CTX = {}
+
+
+def _fit_context(target):
+    """A device context holding `target` in its SMPL slot (cached per template)."""
+    key = id(target)
+    hit = _FIT_CTX.get(key)
+    if hit is not None and hit[0] is target:
+        return hit[1]
+    ctx = runtime.Context()
+    ctx.load_template(runtime.FSB_SMPL, target)
+    _FIT_CTX[key] = (target, ctx)
+    return ctx
+
+
+def _fit(v_src, bmap, target, cfg, init, want_grad):
+    torch = runtime._torch()
+    v = np.asarray(v_src, DTYPE) if not isinstance(v_src, torch.Tensor) else v_src
+    if v.ndim != 3 or v.shape[-1] != 3:
+        raise ShapeError("fit_batch expects (B, Nv, 3) meshes, got %r" % (tuple(v.shape),))
+    b = int(v.shape[0])
+    v_t = bridge(v, bmap)
+    v_t = v_t if isinstance(v_t, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(v_t))
+    v_t = v_t.to(device=torch.device("cuda", torch.cuda.current_device()), dtype=torch.float32).contiguous()
+    if not bool(torch.isfinite(v_t).all()):
+        from .numkit import NumericError
+
+        raise NumericError("fit target meshes contain non-finite values")
+    init_t = None
+    if init is not None:
+        init_np = np.array(init, dtype=DTYPE, copy=True)
+        if init_np.shape != (b, PARAM_DIM):
+            raise ShapeError("init must be (B, %d), got %r" % (PARAM_DIM, init_np.shape))
+        init_t = torch.from_numpy(init_np).cuda()
+    ctx = _fit_context(target)
+    nv = int(v_t.shape[1])
+    dev = v_t.device
+    scratch = torch.empty((b, nv, 6), dtype=torch.float32, device=dev)
+    best = torch.empty((b, PARAM_DIM), dtype=torch.float32, device=dev)
+    err = torch.empty((b,), dtype=torch.float64, device=dev)
+    curve = torch.empty((b, cfg.steps + 1), dtype=torch.float64, device=dev)
+    grad = torch.empty((b, PARAM_DIM), dtype=torch.float32, device=dev) if want_grad else None
+    ctx.check(ctx.lib.fsb_fit_batch(ctx.h, runtime.ptr(v_t), b, nv, runtime.ptr(init_t), int(cfg.steps),
+                                    float(cfg.lr), float(cfg.lambda_pose), float(cfg.lambda_shape),
+                                    runtime.ptr(scratch), runtime.ptr(best), runtime.ptr(err), runtime.ptr(curve),
+                                    runtime.ptr(grad), ctx.stream), "fit_batch")
+    ctx.check_finite("fit_batch")
+    return best, err, curve, grad
+
+
+def fit_batch(v_src, bmap, target, cfg=None, init=None):
+    """Fit target-body parameters to bridged source meshes (projection.py:
+    321-370): Adam with cosine-decayed steps on the squared vertex gap plus
+    pose/shape penalties, best iterate per mesh kept.  curve[k] is the mean
+    over the batch of the best-so-far vertex gap after iterate k."""
+    cfg = cfg or FitConfig()
+    best, err, curve, _ = _fit(v_src, bmap, target, cfg, init, False)
+    return FitBatchResult(params=best.cpu().numpy(), vertex_error=err.cpu().numpy(),
+                          curve=curve.mean(dim=0).cpu().numpy())
+
+
+def fit_objective_grad(theta, v_src, bmap, target, cfg=None):
+    """Gradient of the fit objective at theta (B, 76) for the bridged
+    targets of v_src (the reference's fit_objective_grad, :303-309, takes the
+    bridged targets directly)."""
+    cfg = cfg or FitConfig()
+    _, _, _, grad = _fit(v_src, bmap, target, FitConfig(steps=1, lr=cfg.lr, lambda_pose=cfg.lambda_pose,
+                                                        lambda_shape=cfg.lambda_shape), theta, True)
+    return grad.cpu().numpy()
