@@ -167,6 +167,15 @@ int fsb_fit_batch(fsb_ctx* ctx, const float* target, int B, int nv, const float*
                   float lambda_pose, float lambda_shape, float* scratch, float* best_params, double* vertex_error,
                   double* err_curve, float* grad0, void* stream);
 
+/* projection.bary_map_from_arrays (projection.py:96-177): device float64
+ * source vertices (nv, 3), int64 faces (F, 3) and float64 targets (nt, 3) ->
+ * degenerate (F) u8 face flags, face_index (nt) int64, weights (nt, 3) f32;
+ * bit-identical to the reference (same float64 operation order, first
+ * minimum on ties) */
+int fsb_bary_map(fsb_ctx* ctx, const double* src_verts, int nv, const int64_t* src_faces, int F,
+                 const double* tgt_verts, int nt, uint8_t* degenerate, int64_t* face_index, float* weights,
+                 void* stream);
+
 /* projection.denoise (projection.py:684-697): poses (B, 63) body-pose
  * parameters -> out (B, 63) = x + relu(x W1 + b1) W2 + b2, W1 (63, hidden),
  * W2 (hidden, 63), hidden <= 128; bit-identical to the reference's

@@ -48,6 +48,8 @@ cudaError_t launch_render(const void* scenes, int B, int H, int W, float* out, c
 cudaError_t launch_fit(const TemplateDev& t, const float* target, int B, const float* init, int steps, double lr,
                        float lambda_pose, float lambda_shape, float* scratch, float* best, double* err, double* curve,
                        float* grad0, int* nonfinite, cudaStream_t st);
+cudaError_t launch_bary(const double* verts, const int64_t* faces, int F, const double* tgts, int nt, uint8_t* degen,
+                        int64_t* face_out, float* w_out, cudaStream_t st);
 cudaError_t launch_denoise(const float* x, int B, const float* w1, const float* b1, const float* w2, const float* b2,
                            int H, float* out, int* nonfinite, cudaStream_t st);
 cudaError_t init_attrs_transformer();
@@ -1192,6 +1194,16 @@ int fsb_fit_batch(fsb_ctx* c, const float* target, int B, int nv, const float* i
   FSB_CUDA(c, launch_fit(t, target, B, init, steps, lr, lambda_pose, lambda_shape, scratch, best_params, vertex_error,
                          err_curve, grad0, c->d_flag, (cudaStream_t)stream));
   c->launches += B > 0;
+  return FSB_OK;
+}
+
+int fsb_bary_map(fsb_ctx* c, const double* src_verts, int nv, const int64_t* src_faces, int F, const double* tgt_verts,
+                 int nt, uint8_t* degenerate, int64_t* face_index, float* weights, void* stream) {
+  if (nv <= 0 || F <= 0 || nt < 0) return fail(c, FSB_ERR_SHAPE, "bary_map: bad shapes");
+  if (!degenerate || !face_index || !weights) return fail(c, FSB_ERR_USAGE, "bary_map: outputs are required");
+  FSB_CUDA(c, launch_bary(src_verts, src_faces, F, tgt_verts, nt, degenerate, face_index, weights,
+                          (cudaStream_t)stream));
+  c->launches += 2 * (nt > 0);
   return FSB_OK;
 }
 

@@ -377,3 +377,46 @@ def fit_objective_grad(theta, v_src, bmap, target, cfg=None):
     _, _, _, grad = _fit(v_src, bmap, target, FitConfig(steps=1, lr=cfg.lr, lambda_pose=cfg.lambda_pose,
                                                         lambda_shape=cfg.lambda_shape), theta, True)
     return grad.cpu().numpy()
+
+
+# ---------------------------------------------------------------------------
+# closest-point barycentric attachment, on the GPU
+
+
+def bary_map_from_arrays(src_verts, src_faces, tgt_verts, chunk=64):
+    """Attach each target point to the closest point on the source surface
+    (projection.py:96-177): float64 over every (target, face) pair, ties to
+    the lowest face index, zero-area faces projected onto their longest
+    edge; bit-identical to the reference (k_bary.cu).  `chunk` is accepted
+    for signature compatibility (the GPU search is not chunked)."""
+    torch = runtime._torch()
+    ctx = runtime.default_context()
+    verts = np.ascontiguousarray(src_verts, np.float64)
+    faces = np.ascontiguousarray(src_faces, np.int64)
+    tgts = np.ascontiguousarray(tgt_verts, np.float64)
+    if verts.ndim != 2 or verts.shape[1] != 3:
+        raise ShapeError("source vertices must be (Nv, 3)")
+    if faces.ndim != 2 or faces.shape[1] != 3:
+        raise ShapeError("source faces must be (F, 3)")
+    if tgts.ndim != 2 or tgts.shape[1] != 3:
+        raise ShapeError("target vertices must be (Nt, 3)")
+    dev = torch.device("cuda", torch.cuda.current_device())
+    dv = torch.from_numpy(verts).to(dev)
+    df = torch.from_numpy(faces).to(dev)
+    dt = torch.from_numpy(tgts).to(dev)
+    degen = torch.empty((faces.shape[0],), dtype=torch.uint8, device=dev)
+    fidx = torch.empty((tgts.shape[0],), dtype=torch.int64, device=dev)
+    w = torch.empty((tgts.shape[0], 3), dtype=torch.float32, device=dev)
+    ctx.check(ctx.lib.fsb_bary_map(ctx.h, runtime.ptr(dv), verts.shape[0], runtime.ptr(df), faces.shape[0],
+                                   runtime.ptr(dt), tgts.shape[0], runtime.ptr(degen), runtime.ptr(fidx),
+                                   runtime.ptr(w), ctx.stream), "bary_map")
+    face_out = fidx.cpu().numpy()
+    deg = degen.cpu().numpy().astype(bool)
+    return BaryMap(face_index=face_out, weights=w.cpu().numpy(), corners=faces[face_out],
+                   degenerate_targets=np.nonzero(deg[face_out])[0].astype(np.int64))
+
+
+def precompute_bary(source, target, chunk=64):
+    """Rest-pose attachment of every target vertex onto the source surface
+    (projection.py:180-184)."""
+    return bary_map_from_arrays(source.vertices_rest, source.faces, target.vertices_rest, chunk=chunk)

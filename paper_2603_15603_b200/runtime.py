@@ -78,6 +78,7 @@ _SIGS = {
     "fsb_counters": (_i, [_p, ctypes.POINTER(CountersC)]),
     "fsb_input_bytes": (_i, [_p, ctypes.POINTER(ctypes.c_int64), _i]),
     "fsb_denoise": (_i, [_p, _p, _i, _p, _p, _p, _p, _i, _p, _p]),
+    "fsb_bary_map": (_i, [_p, _p, _i, _p, _i, _p, _i, _p, _p, _p, _p]),
     "fsb_fit_batch": (_i, [_p, _p, _i, _i, _p, _i, _d, ctypes.c_float, ctypes.c_float, _p, _p, _p, _p, _p, _p]),
     "fsb_kernel_launches": (_i64, [_p]),
     "fsb_selftest_umma": (_i, [_p, _p, _p, _i, _i, _p, _p]),
