@@ -64,6 +64,7 @@ def parse():
                     help="in-flight batches per GPU: independent pipeline contexts on their own streams")
     ap.add_argument("--no-c3", action="store_true", help="skip the C3 LBS + projector microbench")
     ap.add_argument("--no-c4", action="store_true", help="skip the C4 ViT-L-sized encoder microbench")
+    ap.add_argument("--no-fit", action="store_true", help="skip the iterative-fit conversion microbench")
     ap.add_argument("--c4-crops", type=int, default=768, help="C4: 3 crops x 256 frames")
     return ap.parse_args()
 
@@ -373,6 +374,10 @@ def main():
     # -- C3 microbench: LBS + projector on 4096 full-size meshes ---------------
     c3 = None if args.no_c3 else c3_microbench(torch, pipe, ctx, meshes=4096, reps=10)
 
+    # -- conversion: iterative fit (the paper's slow baseline) vs projector ----
+    conv = None if args.no_fit else fit_microbench(torch, pipe, meshes=148, steps=300,
+                                                   projector_meshes_per_s=(c3 or {}).get("meshes_per_s"))
+
     # -- C4 microbench: ViT-L-sized encoder, 3 crops x 256 frames --------------
     c4 = None if args.no_c4 else c4_microbench(torch, crops=args.c4_crops, reps=3)
 
@@ -406,7 +411,7 @@ def main():
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "e2e_full_frame_copy": e2e_copy,
         "gpu_launches": launches,
         "clocks": clk.summary(), "p50_frame_latency_ms": lat["p50_ms"], "frame_latency": lat,
-        "stage_ms": stage_ms, "c3": c3, "c4": c4,
+        "stage_ms": stage_ms, "c3": c3, "c4": c4, "conversion": conv,
     }
     print(json.dumps(line), flush=True)
     if dist is not None:
@@ -467,6 +472,38 @@ def c3_microbench(torch, pipe, ctx, meshes, reps):
             "meshes_per_s": meshes / (out["full"] / 1e3), "ms_full": out["full"], "ms_lbs_fk": out["lbs"],
             "lbs_achieved_gbs": lbs_gbs, "lbs_frac_of_hbm": lbs_gbs / peak,
             "lbs_algorithmic_bytes": meshes * BYTES_LBS_MESH}
+
+
+def fit_microbench(torch, pipe, meshes, steps, projector_meshes_per_s=None):
+    """MHR -> SMPL conversion two ways on full-size meshes (PAPER.md:500-504's
+    comparison): projection.fit_batch (`steps` Adam iterations per mesh,
+    projection.py:321-370, one CTA per mesh on the GPU) against the
+    feed-forward projector (the C3 number)."""
+    from paper_2603_15603_b200 import bodymodel as bm
+    from paper_2603_15603_b200 import projection as pj
+
+    rng = np.random.default_rng(3)
+    p = np.zeros((meshes, 76), np.float32)
+    p[:, :66] = rng.normal(0.0, 0.2, size=(meshes, 66))
+    p[:, 66:] = rng.normal(0.0, 0.45, size=(meshes, 10))
+    p[:, 51:54] = 0.0
+    p[:, 63:66] = 0.0
+    dev = torch.device("cuda", torch.cuda.current_device())
+    v = bm.skin_batch(pipe.mhr, torch.from_numpy(p).to(dev))
+    pj.fit_batch(v[:2], pipe.bmap, pipe.decoder.template, pj.FitConfig(steps=3))
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    res = pj.fit_batch(v, pipe.bmap, pipe.decoder.template, pj.FitConfig(steps=steps))
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    out = {"workload": "fit_batch: %d full-size MHR meshes -> SMPL, %d Adam steps each (GPU)" % (meshes, steps),
+           "ms": ms, "fit_meshes_per_s": meshes / (ms / 1e3), "mean_vertex_gap": float(res.vertex_error.mean())}
+    if projector_meshes_per_s:
+        out["projector_meshes_per_s"] = projector_meshes_per_s
+        out["projector_over_fit"] = projector_meshes_per_s / out["fit_meshes_per_s"]
+    return out
 
 
 def c4_microbench(torch, crops, reps, layers=24):
