@@ -49,7 +49,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   constexpr uint32_t A_BYTES = BM * BK * 2, B_BYTES = BN * BK * 2, STAGE_BYTES = A_BYTES + B_BYTES;
   constexpr uint32_t TMEM_COLS = 2 * BN;  // two accumulator buffers
-  __shared__ uint64_t full[STAGES], empty[STAGES], acc_full[2], acc_empty[2], xbar[EPI_WARPS][2];
+  __shared__ uint64_t full[STAGES], empty[STAGES], acc_full[2], acc_empty[2], xbar[2 * EPI_WARPS];
   __shared__ uint32_t tmem_base;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int nk = (K + BK - 1) / BK;
@@ -63,8 +63,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     for (int b = 0; b < 2; ++b) {
       tc::mbar_init(&acc_full[b], 1);
       tc::mbar_init(&acc_empty[b], EPI_WARPS);
-      for (int w = 0; w < EPI_WARPS; ++w) tc::mbar_init(&xbar[w][b], 1);
     }
+    for (int i = 0; i < 2 * EPI_WARPS; ++i) tc::mbar_init(&xbar[i], 1);
     tc::mbar_fence_init();
     tc::prefetch_tmap(&tmA);
     tc::prefetch_tmap(&tmB);
@@ -150,8 +150,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         const int sb = (nblk + k) & 1;
         if (lane == 0) {
           tc::bulk_wait_read0();
-          tc::mbar_expect_tx(&xbar[ew][sb], EPI_BUF);
-          tc::tma_load_2d(stg + sb * EPI_BUF, &tmC, cbase + k * CB, r0, &xbar[ew][sb]);
+          tc::mbar_expect_tx(&xbar[2 * ew + sb], EPI_BUF);
+          tc::tma_load_2d(stg + sb * EPI_BUF, &tmC, cbase + k * CB, r0, &xbar[2 * ew + sb]);
         }
       };
       if (resid && r0 < M) {
@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                 make_uint4(tc::pack_bf16(v[8 * q], v[8 * q + 1]), tc::pack_bf16(v[8 * q + 2], v[8 * q + 3]),
                            tc::pack_bf16(v[8 * q + 4], v[8 * q + 5]), tc::pack_bf16(v[8 * q + 6], v[8 * q + 7]));
         } else if (resid) {
-          tc::mbar_wait(&xbar[ew][sb], xph[sb]);
+          tc::mbar_wait(&xbar[2 * ew + sb], xph[sb]);
           xph[sb] ^= 1u;
 #pragma unroll
           for (int q = 0; q < 8; ++q) {

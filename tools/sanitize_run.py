@@ -1,0 +1,64 @@
+"""Small invocation of every kernel family for compute-sanitizer:
+    compute-sanitizer --tool memcheck python tools/sanitize_run.py
+(K1 device + host frames, K2/K3 fp32 + bf16, K4 tail, C4 GEMM + attention +
+LayerNorm, denoise, fit, barycentric search)."""
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+if __name__ == "__main__":
+    import torch
+
+    from paper_2603_15603_b200 import decoder as dc
+    from paper_2603_15603_b200 import pipeline as pl
+    from paper_2603_15603_b200 import projection as pj
+    from paper_2603_15603_b200 import runtime as rt
+    from paper_2603_15603_b200 import synth
+
+    mhr, smpl, gt = synth.make_toy_models(0, 1200, 600)
+    proj = pj.init_projector(pj.make_subsample(600, 150), (64, 32), seed=0)
+    scenes = [synth.random_scene(np.random.default_rng(5000 + i), smpl, (512, 512)) for i in range(3)]
+    imgs = np.stack([synth.render_scene(s, smpl) for s in scenes])
+    kps = np.stack([s.keypoints2d for s in scenes])
+    for prec in ("fp32", "bf16"):
+        pipe = pl.Pipeline(dc.Decoder(smpl, dc.DecoderConfig(), seed=40), mhr=mhr, bmap=gt, projector=proj,
+                           precision=prec)
+        pipe.context().set_graphs(False)
+        out = pipe.run_batch(imgs, kps)
+        out = pipe.run_batch(torch.from_numpy(imgs).pin_memory(), torch.from_numpy(kps).pin_memory())
+        torch.cuda.synchronize()
+        print(prec, "frame batch ok", out["theta"].shape)
+    # C4 pipeline: 2 layers, 2 crops (SANITIZE_ATTN_ONLY=1: the attention
+    # kernel alone, without the GEMMs)
+    if os.environ.get("SANITIZE_ATTN_ONLY"):
+        import ctypes
+
+        lib = ctypes.CDLL(rt.LIB_PATH)
+        P = ctypes.c_void_p
+        lib.fsb_debug_attention.argtypes = [P, ctypes.c_int, ctypes.c_int, ctypes.c_int, ctypes.c_int, P, P]
+        q = (torch.randn((2 * 576, 3 * 256), device="cuda") * 0.5).to(torch.bfloat16)
+        o = torch.empty((2 * 576, 256), dtype=torch.bfloat16, device="cuda")
+        assert lib.fsb_debug_attention(q.data_ptr(), 2, 576, 256, 4, o.data_ptr(),
+                                       torch.cuda.current_stream().cuda_stream) == 0
+        torch.cuda.synchronize()
+        print("attention ok")
+    cfg = dc.DecoderConfig(crop_size=384, patch=16, dim=1024, heads=16, enc_layers=2, body_layers=1, hand_layers=1)
+    ctx = rt.Context()
+    ctx.load_decoder(cfg, synth.decoder_weights(cfg, 40, encoder_only=True))
+    x = torch.rand((2, 384, 384, 3), device="cuda")
+    f = torch.empty((2, 576, 1024), device="cuda")
+    if not os.environ.get("SANITIZE_ATTN_ONLY"):
+        ctx.check(ctx.lib.fsb_encode(ctx.h, rt.ptr(x), 2, rt.ptr(f), rt.PRECISIONS["bf16"], ctx.stream))
+        torch.cuda.synchronize()
+        print("vit ok")
+    w = pj.DenoiserWeights(*(np.random.default_rng(1).normal(size=s).astype(np.float32) * 0.1
+                             for s in ((63, 32), (32,), (32, 63), (63,))))
+    pj.denoise(w, np.zeros((5, 63), np.float32))
+    v = np.stack([mhr.vertices_rest] * 2)
+    pj.fit_batch(v, gt, smpl, pj.FitConfig(steps=3))
+    pj.precompute_bary(mhr, smpl)
+    torch.cuda.synchronize()
+    print("aux ok")
