@@ -65,6 +65,8 @@ def parse():
     ap.add_argument("--no-c3", action="store_true", help="skip the C3 LBS + projector microbench")
     ap.add_argument("--no-c4", action="store_true", help="skip the C4 ViT-L-sized encoder microbench")
     ap.add_argument("--no-fit", action="store_true", help="skip the iterative-fit conversion microbench")
+    ap.add_argument("--stream-frames", type=int, default=8192,
+                    help="C5: frames of the synthetic video stream sharded across the ranks (0: skip)")
     ap.add_argument("--c4-crops", type=int, default=768, help="C4: 3 crops x 256 frames")
     return ap.parse_args()
 
@@ -359,6 +361,10 @@ def main():
     # the concurrent batches computed what one pipeline computes alone
     verified = verify_streams(torch, pipes, outs_s, images, kps, cfg, B, args.steps, nslot, S)
 
+    # -- C5: an 8192-frame stream sharded across the ranks, one NCCL gather ----
+    c5 = None if args.stream_frames <= 0 else stream_run(torch, pipes, streams, images, kps, cfg, B, dist, world,
+                                                          rank, args.stream_frames)
+
     # -- per-stage attribution (graphs off, CUDA events between stages) -------
     stage_ms = attribute_stages(torch, pipe, ctx, images[:B], kps[:B], outs, cfg, reps=20)
 
@@ -411,7 +417,7 @@ def main():
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "e2e_full_frame_copy": e2e_copy,
         "gpu_launches": launches,
         "clocks": clk.summary(), "p50_frame_latency_ms": lat["p50_ms"], "frame_latency": lat,
-        "stage_ms": stage_ms, "c3": c3, "c4": c4, "conversion": conv,
+        "stage_ms": stage_ms, "c3": c3, "c4": c4, "c5": c5, "conversion": conv,
     }
     print(json.dumps(line), flush=True)
     if dist is not None:
@@ -671,6 +677,73 @@ def frame_latency(torch, pipe, images, kps, cfg, reps):
         ts.append(a.elapsed_time(b))
     ts.sort()
     return {"p50_ms": ts[len(ts) // 2], "p95_ms": ts[int(len(ts) * 0.95)], "reps": reps, "batch": 1}
+
+
+def stream_run(torch, pipes, streams, images, kps, cfg, B, dist, world, rank, total):
+    """C5: a stream of `total` synthetic frames, rank r taking
+    the contiguous block [r*total/G, (r+1)*total/G) (frame i is bank frame
+    i % bank), batches of B spread over the in-flight pipelines, the SMPL
+    outputs (theta + joints, 142 floats per frame) collected per rank and
+    all-gathered over NCCL once at the end.  Strong scaling: frames/s of the
+    whole stream, first frame to gathered result, max over ranks."""
+    lo, hi = shard_bounds(total, rank, world)
+    n = hi - lo
+    dev = images.device
+    bank = images.shape[0]
+    res = torch.empty((max(n, 1), 142), dtype=torch.float32, device=dev)
+    S = len(pipes)
+    outs = [p_.allocate_outputs(B, tail=True) for p_ in pipes]
+    gathered = torch.empty((world * max(n, 1), 142), dtype=torch.float32, device=dev) if dist is not None else None
+
+    def batch(k, f0, nb):
+        j = k % S
+        with torch.cuda.stream(streams[j]):
+            s0 = f0 % bank
+            if s0 + nb <= bank:
+                img, kp = images[s0:s0 + nb], kps[s0:s0 + nb]
+            else:
+                idx = torch.arange(f0, f0 + nb, device=dev) % bank
+                img, kp = images[idx], kps[idx]
+            o = outs[j] if nb == B else pipes[j].allocate_outputs(nb, tail=True)
+            pipes[j].launch(img, kp, o, cfg)
+            r = f0 - lo
+            res[r:r + nb, :76].copy_(o["theta"])
+            res[r:r + nb, 76:].copy_(o["j_smpl"].reshape(nb, 66))
+
+    # warm-up pass over a few batches (graphs for every stream)
+    for k in range(2 * S):
+        batch(k, lo, min(B, n))
+    torch.cuda.synchronize()
+    if dist is not None:
+        dist.barrier()
+    st = streams[0]
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    for q in streams[1:]:
+        q.wait_event(e0)
+    k = 0
+    for f0 in range(lo, hi, B):
+        batch(k, f0, min(B, hi - f0))
+        k += 1
+    for q in streams[1:]:
+        ev = torch.cuda.Event()
+        ev.record(q)
+        st.wait_event(ev)
+    if dist is not None:
+        with torch.cuda.stream(st):
+            dist.all_gather_into_tensor(gathered, res)
+    e1.record(st)
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    return {"workload": "C5: %d-frame synthetic stream sharded over %d GPU(s) (%d frames on this rank), batches of %d "
+                        "on %d in-flight pipelines, one all-gather of the SMPL outputs (theta + joints)"
+                        % (total, world, n, B, S),
+            "ms": ms, "frames_per_s": total / (ms / 1e3), "scaling": "strong",
+            "gathered_bytes_per_rank": int(n * 142 * 4)}
 
 
 def verify_streams(torch, pipes, outs_s, images, kps, cfg, B, steps, nslot, S):
