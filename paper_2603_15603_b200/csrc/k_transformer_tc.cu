@@ -61,7 +61,7 @@ struct Shared {
 // cycle attribution of CTA 0 / thread 0 (build with FSB_PROFILE=1):
 // [0] total, [1] MMA waits, [2] weight waits, [3] issue barriers,
 // [4] row-exchange barriers
-__device__ unsigned long long g_tc_prof[2][2][12];  // [role][thread 0 | thread 255][counter]
+__device__ unsigned long long g_tc_prof[2][2][16];  // [role][thread 0 | thread 255][counter]
 #define PROF_T0() const long long prof_t0_ = clock64()
 #define PROF_ADD(i) (prof[i] += clock64() - prof_t0_)
 #else
@@ -79,7 +79,7 @@ struct Pipe {
   int wload, wuse, xc, pload, puse;
   int tid, r, h;
 #ifdef FSB_PROFILE
-  long long prof[12];
+  long long prof[16];
 #endif
 
   // per-layer parameter block ring (TCP_* layout): thread 0 issues, every
@@ -356,15 +356,33 @@ __device__ void self_attn(Pipe& P, const float* prm, float* x, const float* pos,
   float a[HC];
 #pragma unroll
   for (int c = 0; c < HC; ++c) a[c] = x[c] + pos[c];
+#ifdef FSB_PROFILE
+  long long q0 = clock64();
+#endif
   ln_half_to_tile(P, a, prm + TCP_S_LN_G, prm + TCP_S_LN_B);
+#ifdef FSB_PROFILE
+  long long q1 = clock64();
+  P.prof[12] += q1 - q0;
+#endif
   const uint32_t wq = P.acquire();
   P.before_issue();
   if (P.tid == 0) gemm(P.sbase + S_A, D, wq, 3 * D, T_GEN, P.tmem);
   P.prefetch();
   P.commit_wait();
+#ifdef FSB_PROFILE
+  long long q2 = clock64();
+  P.prof[13] += q2 - q1;
+#endif
   drain_q(P, T_GEN, prm + TCP_S_BQKV);
   drain_kv(P, T_GEN + 64, prm + TCP_S_BQKV + 64, prm + TCP_S_BQKV + 128);
+#ifdef FSB_PROFILE
+  long long q3 = clock64();
+  P.prof[14] += q3 - q2;
+#endif
   attn_core<NK>(P);
+#ifdef FSB_PROFILE
+  P.prof[15] += clock64() - q3;
+#endif
   out_proj(P, prm + TCP_S_BO, x, valid);
 }
 
@@ -439,7 +457,7 @@ __device__ void setup(Pipe& P, Shared& sh, uint8_t* smem) {
   P.pload = 0;
   P.puse = 0;
 #ifdef FSB_PROFILE
-  for (int i = 0; i < 12; ++i) P.prof[i] = 0;
+  for (int i = 0; i < 16; ++i) P.prof[i] = 0;
   P.prof[0] = -clock64();
 #endif
   if (P.tid == 0) {
@@ -465,7 +483,7 @@ __device__ void teardown(Pipe& P, int role) {
 #ifdef FSB_PROFILE
   P.prof[0] += clock64();
   if ((P.tid == 0 || P.tid == NTH - 1) && blockIdx.x == 0)
-    for (int i = 0; i < 12; ++i) g_tc_prof[role][P.tid ? 1 : 0][i] = (unsigned long long)P.prof[i];
+    for (int i = 0; i < 16; ++i) g_tc_prof[role][P.tid ? 1 : 0][i] = (unsigned long long)P.prof[i];
 #else
   (void)role;
 #endif
@@ -882,9 +900,9 @@ __global__ void __launch_bounds__(NTH, 1) k_decoders_tc(DecodeArgs a, BodyW bw, 
 // debug export of the FSB_PROFILE cycle counters (not part of the public ABI)
 extern "C" int fsb_debug_tc_profile(unsigned long long* out32) {
 #ifdef FSB_PROFILE
-  return cudaMemcpyFromSymbol(out32, g_tc_prof, sizeof(unsigned long long) * 48) == cudaSuccess ? 0 : 4;
+  return cudaMemcpyFromSymbol(out32, g_tc_prof, sizeof(unsigned long long) * 64) == cudaSuccess ? 0 : 4;
 #else
-  for (int i = 0; i < 48; ++i) out32[i] = 0;
+  for (int i = 0; i < 64; ++i) out32[i] = 0;
   return 3;
 #endif
 }

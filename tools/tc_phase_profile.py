@@ -31,12 +31,12 @@ def main():
         pipe.launch(images, kps, outs, pl.fast_config())
     torch.cuda.synchronize()
     lib = ctypes.CDLL(runtime.LIB_PATH)
-    buf = (ctypes.c_ulonglong * 48)()
+    buf = (ctypes.c_ulonglong * 64)()
     rc = lib.fsb_debug_tc_profile(buf)
     names = ["total", "mma_wait", "weight_wait", "issue_bar", "xch_bar"]
     for role, tag in ((0, "encoder"), (1, "decoder")):
         for th, tname in ((0, "t0"), (1, "t255")):
-            v = [buf[role * 24 + th * 12 + i] for i in range(12)]
+            v = [buf[role * 32 + th * 16 + i] for i in range(16)]
             rest = v[0] - sum(v[1:5])
             print(tag, tname, "rc", rc,
                   " ".join("%s=%d(%.1f%%)" % (n, x, 100.0 * x / max(v[0], 1)) for n, x in zip(names, v)),
@@ -45,6 +45,8 @@ def main():
                 other = v[0] - v[5] - v[6] - v[7]
                 print("   sub-layers: self=%d cross=%d mlp=%d other=%d [setup+final=%d pos+params=%d heads=%d fk=%d]"
                       % (v[5], v[6], v[7], other, v[8], v[9], v[10], v[11]))
+            print("   self-attn: LN=%d QKV gemm+wait=%d drains=%d attn_core=%d out_proj=%d"
+                  % (v[12], v[13], v[14], v[15], v[5] - v[12] - v[13] - v[14] - v[15]))
 
 
 if __name__ == "__main__":
