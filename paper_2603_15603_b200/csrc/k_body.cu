@@ -133,12 +133,18 @@ __global__ void __launch_bounds__(kLbsThreads) k_lbs(TemplateDev t, const float*
   const int m0 = blockIdx.y * kLbsMeshes;
   const int nm = min(kLbsMeshes, B - m0);
   const int npair = (nm + 1) / 2;
-  for (int i = threadIdx.x; i < npair * 2 * FSB_NJ * 12; i += kLbsThreads) {
-    const int pr = i / (2 * FSB_NJ * 12), rem = i % (2 * FSB_NJ * 12), half = rem / (FSB_NJ * 12),
-              e = rem % (FSB_NJ * 12);
-    const int m = 2 * pr + half;
-    const float v = m < nm ? rel[(int64_t)(m0 + m) * FSB_NJ * 12 + e] : 0.0f;
-    reinterpret_cast<float*>(&A2[pr][e])[half] = v;
+  // stage the pairs' transforms interleaved as float2: one float4 of each
+  // mesh in, two float4 (a0 b0 a1 b1 | a2 b2 a3 b3) out
+  constexpr int Q4 = FSB_NJ * 12 / 4;  // float4 per mesh
+  for (int i = threadIdx.x; i < npair * Q4; i += kLbsThreads) {
+    const int pr = i / Q4, q = i - pr * Q4;
+    const int ma = 2 * pr, mb = ma + 1;
+    const float4 zero4 = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+    const float4 va = ma < nm ? __ldg(reinterpret_cast<const float4*>(rel + (int64_t)(m0 + ma) * FSB_NJ * 12) + q) : zero4;
+    const float4 vb = mb < nm ? __ldg(reinterpret_cast<const float4*>(rel + (int64_t)(m0 + mb) * FSB_NJ * 12) + q) : zero4;
+    float4* dst = reinterpret_cast<float4*>(&A2[pr][4 * q]);
+    dst[0] = make_float4(va.x, vb.x, va.y, vb.y);
+    dst[1] = make_float4(va.z, vb.z, va.w, vb.w);
   }
   for (int i = threadIdx.x; i < npair * 2 * 10; i += kLbsThreads) {
     const int pr = i / 20, half = (i / 10) % 2, k = i % 10, m = 2 * pr + half;
