@@ -116,110 +116,148 @@ __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
 
 constexpr int kLbsThreads = 256;
 constexpr int kLbsVPT = 2;      // consecutive vertices per thread (float2 stores)
-constexpr int kLbsMeshes = 32;  // meshes per CTA (template reuse factor), as 16 pairs
+constexpr int kLbsMeshes = 32;  // meshes per group, as 16 pairs
+constexpr int kLbsGroupCTAs = 8;  // CTAs along the mesh axis (each walks groups y, y + 8, ...)
 
-// LBS of a vertex tile for up to 32 meshes.  Each thread keeps its two
-// vertices' template records in registers and walks the meshes two at a
-// time: the per-mesh transforms and shape coefficients of a mesh pair are
-// interleaved in shared memory as float2, so every multiply-add of the blend,
-// shape offset and apply is one FFMA2 serving both meshes.
-// grid: (ceil(nv / 512), ceil(B / 32))
+// LBS of a vertex tile for a run of 32-mesh groups.  Each thread keeps its
+// two vertices' template records in registers for the whole run and walks
+// the meshes two at a time: the per-mesh transforms and shape coefficients
+// of a mesh pair are interleaved in shared memory as float2, so every
+// multiply-add of the blend, shape offset and apply is one FFMA2 serving
+// both meshes.  The next group's transforms are copied in with cp.async
+// (4-byte scatter into the interleaved layout) while the current group is
+// computed: two shared-memory buffers.
+// grid: (ceil(nv / 512), min(groups, kLbsGroupCTAs)); group g of CTA y is
+// y, y + gridDim.y, ...
+struct LbsStage {
+  float2 A2[kLbsMeshes / 2][FSB_NJ * 12];
+  float2 S2[kLbsMeshes / 2][10];
+};
+
+__device__ __forceinline__ void cp_async4(void* dst, const void* src, bool valid) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(tc::smem_u32(dst)), "l"(src),
+               "r"(valid ? 4 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait0() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+
+// copy group g's transforms and shape coefficients into `st` (zero beyond B)
+__device__ __forceinline__ void lbs_stage(LbsStage& st, const float* __restrict__ rel, const float* __restrict__ poses,
+                                          int ld_pose, int B, int g) {
+  const int m0 = g * kLbsMeshes;
+  constexpr int PAIR = 2 * FSB_NJ * 12;  // floats per interleaved pair
+  for (int pr = 0; pr < kLbsMeshes / 2; ++pr) {
+    float* dst = reinterpret_cast<float*>(st.A2[pr]);
+    for (int j = threadIdx.x; j < PAIR; j += kLbsThreads) {
+      const int e = j >> 1, m = m0 + 2 * pr + (j & 1);
+      const bool ok = m < B;
+      cp_async4(dst + j, rel + (int64_t)(ok ? m : 0) * FSB_NJ * 12 + e, ok);
+    }
+  }
+  for (int j = threadIdx.x; j < kLbsMeshes * 10; j += kLbsThreads) {
+    const int pr = j / 20, half = (j / 10) & 1, k = j % 10, m = m0 + 2 * pr + half;
+    const bool ok = m < B;
+    cp_async4(reinterpret_cast<float*>(&st.S2[pr][k]) + half, poses + (int64_t)(ok ? m : 0) * ld_pose + 66 + k, ok);
+  }
+}
+
 template <int NZ>
-__global__ void __launch_bounds__(kLbsThreads) k_lbs(TemplateDev t, const float* __restrict__ rel,
-                                                     const float* __restrict__ poses, int ld_pose, int B,
-                                                     float* __restrict__ verts, int* nonfinite) {
-  __shared__ __align__(16) float2 A2[kLbsMeshes / 2][FSB_NJ * 12];
-  __shared__ __align__(16) float2 S2[kLbsMeshes / 2][10];
-  const int m0 = blockIdx.y * kLbsMeshes;
-  const int nm = min(kLbsMeshes, B - m0);
-  const int npair = (nm + 1) / 2;
-  // stage the pairs' transforms interleaved as float2: one float4 of each
-  // mesh in, two float4 (a0 b0 a1 b1 | a2 b2 a3 b3) out
-  constexpr int Q4 = FSB_NJ * 12 / 4;  // float4 per mesh
-  for (int i = threadIdx.x; i < npair * Q4; i += kLbsThreads) {
-    const int pr = i / Q4, q = i - pr * Q4;
-    const int ma = 2 * pr, mb = ma + 1;
-    const float4 zero4 = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-    const float4 va = ma < nm ? __ldg(reinterpret_cast<const float4*>(rel + (int64_t)(m0 + ma) * FSB_NJ * 12) + q) : zero4;
-    const float4 vb = mb < nm ? __ldg(reinterpret_cast<const float4*>(rel + (int64_t)(m0 + mb) * FSB_NJ * 12) + q) : zero4;
-    float4* dst = reinterpret_cast<float4*>(&A2[pr][4 * q]);
-    dst[0] = make_float4(va.x, vb.x, va.y, vb.y);
-    dst[1] = make_float4(va.z, vb.z, va.w, vb.w);
-  }
-  for (int i = threadIdx.x; i < npair * 2 * 10; i += kLbsThreads) {
-    const int pr = i / 20, half = (i / 10) % 2, k = i % 10, m = 2 * pr + half;
-    reinterpret_cast<float*>(&S2[pr][k])[half] = m < nm ? poses[(int64_t)(m0 + m) * ld_pose + 66 + k] : 0.0f;
-  }
+__global__ void __launch_bounds__(kLbsThreads, 2) k_lbs(TemplateDev t, const float* __restrict__ rel,
+                                                        const float* __restrict__ poses, int ld_pose, int B,
+                                                        float* __restrict__ verts, int* nonfinite) {
+  extern __shared__ __align__(16) uint8_t lbs_smem[];
+  LbsStage* stage = reinterpret_cast<LbsStage*>(lbs_smem);
+  const int ngroups = (B + kLbsMeshes - 1) / kLbsMeshes;
+  int g = blockIdx.y;
+  if (g >= ngroups) return;  // CTA-uniform
+  lbs_stage(stage[0], rel, poses, ld_pose, B, g);
+  cp_async_commit();
   VertexTmpl<NZ> vt[kLbsVPT];
   const int v0 = (blockIdx.x * kLbsThreads + threadIdx.x) * kLbsVPT;
 #pragma unroll
   for (int q = 0; q < kLbsVPT; ++q)
     if (v0 + q < t.nv) vt[q].load(t, v0 + q);
-  __syncthreads();
-  if (v0 >= t.nv) return;
+  const bool live = v0 < t.nv;
   const bool both = v0 + 1 < t.nv;
   float2 chk = make_float2(0.0f, 0.0f);
   const float2 one2 = make_float2(1.0f, 1.0f);
-  for (int pr = 0; pr < npair; ++pr) {
-    float2 sh[10];
+  for (int it = 0; g < ngroups; g += gridDim.y, ++it) {
+    const int gn = g + gridDim.y;
+    if (gn < ngroups) lbs_stage(stage[(it + 1) & 1], rel, poses, ld_pose, B, gn);
+    cp_async_commit();
+    cp_async_wait1();  // this group's copies have landed
+    __syncthreads();
+    const LbsStage& st = stage[it & 1];
+    const int m0 = g * kLbsMeshes;
+    const int nm = min(kLbsMeshes, B - m0);
+    const int npair = (nm + 1) / 2;
+    if (live) {
+      for (int pr = 0; pr < npair; ++pr) {
+        float2 sh[10];
 #pragma unroll
-    for (int k = 0; k < 10; ++k) sh[k] = S2[pr][k];
-    float2 o[kLbsVPT][3];
+        for (int k = 0; k < 10; ++k) sh[k] = st.S2[pr][k];
+        float2 o[kLbsVPT][3];
 #pragma unroll
-    for (int q = 0; q < kLbsVPT; ++q) {
-      const VertexTmpl<NZ>& V = vt[q];
-      float2 T[12];
+        for (int q = 0; q < kLbsVPT; ++q) {
+          const VertexTmpl<NZ>& V = vt[q];
+          float2 T[12];
 #pragma unroll
-      for (int e = 0; e < 12; ++e) T[e] = make_float2(0.0f, 0.0f);
+          for (int e = 0; e < 12; ++e) T[e] = make_float2(0.0f, 0.0f);
 #pragma unroll
-      for (int z = 0; z < NZ; ++z) {
-        const float2 wz = make_float2(V.w[z], V.w[z]);
-        const float4* row = reinterpret_cast<const float4*>(&A2[pr][12 * V.j[z]]);
+          for (int z = 0; z < NZ; ++z) {
+            const float2 wz = make_float2(V.w[z], V.w[z]);
+            const float4* row = reinterpret_cast<const float4*>(&st.A2[pr][12 * V.j[z]]);
 #pragma unroll
-        for (int e2 = 0; e2 < 6; ++e2) {
-          const float4 r = row[e2];
-          T[2 * e2] = ffma2(wz, make_float2(r.x, r.y), T[2 * e2]);
-          T[2 * e2 + 1] = ffma2(wz, make_float2(r.z, r.w), T[2 * e2 + 1]);
+            for (int e2 = 0; e2 < 6; ++e2) {
+              const float4 r = row[e2];
+              T[2 * e2] = ffma2(wz, make_float2(r.x, r.y), T[2 * e2]);
+              T[2 * e2 + 1] = ffma2(wz, make_float2(r.z, r.w), T[2 * e2 + 1]);
+            }
+          }
+          float2 vs[3];
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            float2 acc = make_float2(0.0f, 0.0f);
+#pragma unroll
+            for (int k = 0; k < 10; ++k) acc = ffma2(make_float2(V.sb[10 * c + k], V.sb[10 * c + k]), sh[k], acc);
+            vs[c] = ffma2(acc, one2, make_float2(V.vr[c], V.vr[c]));
+          }
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            float2 acc = ffma2(T[4 * a], vs[0], T[4 * a + 3]);
+            acc = ffma2(T[4 * a + 1], vs[1], acc);
+            o[q][a] = ffma2(T[4 * a + 2], vs[2], acc);
+            if (q == 0 || both) chk = ffma2(o[q][a], one2, chk);
+          }
+        }
+        // mesh 2 pr (.x lanes) and 2 pr + 1 (.y lanes): 6 floats each; 8-byte
+        // vector stores when the mesh base keeps them aligned (odd nv, odd
+        // mesh: scalar stores)
+        const int m = m0 + 2 * pr;
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+          if (2 * pr + half >= nm) break;
+          float* d = verts + ((int64_t)(m + half) * t.nv + v0) * 3;
+          const float f[6] = {half ? o[0][0].y : o[0][0].x, half ? o[0][1].y : o[0][1].x,
+                              half ? o[0][2].y : o[0][2].x, half ? o[1][0].y : o[1][0].x,
+                              half ? o[1][1].y : o[1][1].x, half ? o[1][2].y : o[1][2].x};
+          if (both && ((reinterpret_cast<uintptr_t>(d) & 7) == 0)) {
+            __stcs(reinterpret_cast<float2*>(d), make_float2(f[0], f[1]));
+            __stcs(reinterpret_cast<float2*>(d + 2), make_float2(f[2], f[3]));
+            __stcs(reinterpret_cast<float2*>(d + 4), make_float2(f[4], f[5]));
+          } else {
+            const int n = both ? 6 : 3;
+            for (int i = 0; i < n; ++i) __stcs(d + i, f[i]);
+          }
         }
       }
-      float2 vs[3];
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        float2 acc = make_float2(0.0f, 0.0f);
-#pragma unroll
-        for (int k = 0; k < 10; ++k) acc = ffma2(make_float2(V.sb[10 * c + k], V.sb[10 * c + k]), sh[k], acc);
-        vs[c] = ffma2(acc, one2, make_float2(V.vr[c], V.vr[c]));
-      }
-#pragma unroll
-      for (int a = 0; a < 3; ++a) {
-        float2 acc = ffma2(T[4 * a], vs[0], T[4 * a + 3]);
-        acc = ffma2(T[4 * a + 1], vs[1], acc);
-        o[q][a] = ffma2(T[4 * a + 2], vs[2], acc);
-        if (q == 0 || both) chk = ffma2(o[q][a], one2, chk);
-      }
     }
-    // mesh 2 pr (.x lanes) and 2 pr + 1 (.y lanes): 6 floats each; 8-byte
-    // vector stores when the mesh base keeps them aligned (odd nv, odd mesh:
-    // scalar stores)
-    const int m = m0 + 2 * pr;
-#pragma unroll
-    for (int half = 0; half < 2; ++half) {
-      if (2 * pr + half >= nm) break;
-      float* d = verts + ((int64_t)(m + half) * t.nv + v0) * 3;
-      const float f[6] = {half ? o[0][0].y : o[0][0].x, half ? o[0][1].y : o[0][1].x,
-                          half ? o[0][2].y : o[0][2].x, half ? o[1][0].y : o[1][0].x,
-                          half ? o[1][1].y : o[1][1].x, half ? o[1][2].y : o[1][2].x};
-      if (both && ((reinterpret_cast<uintptr_t>(d) & 7) == 0)) {
-        __stcs(reinterpret_cast<float2*>(d), make_float2(f[0], f[1]));
-        __stcs(reinterpret_cast<float2*>(d + 2), make_float2(f[2], f[3]));
-        __stcs(reinterpret_cast<float2*>(d + 4), make_float2(f[4], f[5]));
-      } else {
-        const int n = both ? 6 : 3;
-        for (int i = 0; i < n; ++i) __stcs(d + i, f[i]);
-      }
-    }
+    __syncthreads();  // buffer it & 1 is refilled two groups later
   }
-  if (nonfinite != nullptr && !(isfinite(chk.x) && isfinite(chk.y))) atomicOr(nonfinite, 1);
+  cp_async_wait0();
+  if (live && nonfinite != nullptr && !(isfinite(chk.x) && isfinite(chk.y))) atomicOr(nonfinite, 1);
 }
 
 // ---------------------------------------------------------------------------
@@ -432,17 +470,26 @@ cudaError_t launch_fk(const float* poses, int ld_pose, int B, const float* grest
 cudaError_t launch_lbs(const TemplateDev& t, const float* rel, const float* poses, int ld_pose, int B, float* verts,
                        int* nonfinite, cudaStream_t st) {
   if (B == 0) return cudaSuccess;
-  dim3 grid((t.nv + kLbsThreads * kLbsVPT - 1) / (kLbsThreads * kLbsVPT), (B + kLbsMeshes - 1) / kLbsMeshes);
+  const int ngroups = (B + kLbsMeshes - 1) / kLbsMeshes;
+  dim3 grid((t.nv + kLbsThreads * kLbsVPT - 1) / (kLbsThreads * kLbsVPT),
+            ngroups < kLbsGroupCTAs ? ngroups : kLbsGroupCTAs);
+  const size_t smem = 2 * sizeof(LbsStage);
   switch (t.nnz) {
-    case 2: k_lbs<2><<<grid, kLbsThreads, 0, st>>>(t, rel, poses, ld_pose, B, verts, nonfinite); break;
-    case 4: k_lbs<4><<<grid, kLbsThreads, 0, st>>>(t, rel, poses, ld_pose, B, verts, nonfinite); break;
-    case 8: k_lbs<8><<<grid, kLbsThreads, 0, st>>>(t, rel, poses, ld_pose, B, verts, nonfinite); break;
+    case 2: k_lbs<2><<<grid, kLbsThreads, smem, st>>>(t, rel, poses, ld_pose, B, verts, nonfinite); break;
+    case 4: k_lbs<4><<<grid, kLbsThreads, smem, st>>>(t, rel, poses, ld_pose, B, verts, nonfinite); break;
+    case 8: k_lbs<8><<<grid, kLbsThreads, smem, st>>>(t, rel, poses, ld_pose, B, verts, nonfinite); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
 }
 
-cudaError_t init_attrs_body() { return cudaSuccess; }
+cudaError_t init_attrs_body() {
+  const int smem = (int)(2 * sizeof(LbsStage));
+  cudaError_t e = cudaFuncSetAttribute(k_lbs<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_lbs<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_lbs<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  return e;
+}
 
 static inline int proj_threads(const ProjectorDev& p) {
   const int per = (p.n_sub + kProjChunks - 1) / kProjChunks;

@@ -255,7 +255,7 @@ __device__ void drain_kv(Pipe& P, uint32_t kcol, const float* bk, const float* b
 // valid keys (64 for encoder self-attention and cross-attention, 51 body
 // tokens, 4 hand tokens), so masking is resolved at compile time.
 template <int NK>
-__device__ float softmax_head(Pipe& P) {
+__device__ float softmax_head(Pipe& P, bool active = true) {
   static_assert(NK >= 1 && NK <= 64, "keys per block");
   constexpr int NL = NK <= 16 ? 16 : (NK <= 32 ? 32 : 64);  // TMEM columns loaded
   const int blk = P.r / BLK;
@@ -264,6 +264,11 @@ __device__ float softmax_head(Pipe& P) {
   if (NL == 64) tc::tmem_ld64(ta, s);
   else if (NL == 32) tmem_ld32(ta, s);
   else tc::tmem_ld16(ta, s);
+  if (!active) {  // a row outside this round: P row of zeros
+#pragma unroll
+    for (int q = 0; q < 16; ++q) st_row_zero8(P.smem + S_HP + P.h * 32768, P.r, 8 * q, 128);
+    return 0.0f;
+  }
   float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
   for (int k = 0; k < NK; ++k) m4[k & 3] = fmaxf(m4[k & 3], s[k]);
@@ -291,13 +296,58 @@ __device__ float softmax_head(Pipe& P) {
   return 1.0f / ((p4[0] + p4[1]) + (p4[2] + p4[3]));
 }
 
+// softmax of head (pair + 2 h) for hand tiles: every hand's four token rows
+// [4 g, 4 g + 4) attend to the same four keys (decoder.py:393-398), so a
+// warp's 32 rows need the 32 key columns of its own lane quadrant; the
+// row's four are picked out of them.  Same arithmetic as softmax_head<4>.
+__device__ float softmax_group4(Pipe& P) {
+  float s[32];
+  tmem_ld32(P.lane_addr(T_GEN + 128 * P.h + 32 * (P.r >> 5)), s);
+  const int g = (P.r & 31) >> 2;
+  float a[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    a[k] = s[k];
+#pragma unroll
+    for (int gg = 1; gg < 8; ++gg) a[k] = g == gg ? s[4 * gg + k] : a[k];
+  }
+  constexpr float kScale = 0.25f * 1.4426950408889634f;
+  const float nms = -fmaxf(fmaxf(a[0], a[1]), fmaxf(a[2], a[3])) * kScale;
+  float e[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) e[k] = ex2_approx(fmaf(a[k], kScale, nms));
+  uint8_t* tp = P.smem + S_HP + P.h * 32768;
+  const int qk = P.r >> 3;               // 8-column chunk holding the group's keys
+  const bool hi = ((P.r >> 2) & 1) != 0;  // keys in its upper half
+#pragma unroll
+  for (int q = 0; q < 16; ++q) {
+    if (q == qk) {
+      float v[8];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        v[k] = hi ? 0.0f : e[k];
+        v[4 + k] = hi ? e[k] : 0.0f;
+      }
+      st_row8(tp, P.r, 8 * q, 128, v);
+    } else {
+      st_row_zero8(tp, P.r, 8 * q, 128);
+    }
+  }
+  return 1.0f / ((e[0] + e[1]) + (e[2] + e[3]));
+}
+
 // the four heads of one attention given sQ / sK / sVt; the context is
 // written as bf16 straight into the A tile of the output projection.
 // Pair p of the two passes runs heads p (threads h = 0) and p + 2
 // (threads h = 1), so each thread ends up owning the softmax sums of the
 // two heads whose context columns [32 h, 32 h + 32) it holds.
-template <int NK>
-__device__ void attn_core(Pipe& P) {
+// One round: S = Q K^T, softmax, O (+)= P V.  Rows with active == false
+// contribute a zero P row, so several rounds over different key sets (the
+// hand tiles' cross attention) accumulate into one context; inv keeps the
+// 1 / sum of the round in which the row was active.  G4: grouped hand
+// self-attention (softmax_group4).
+template <int NK, bool G4 = false>
+__device__ void attn_round(Pipe& P, bool active, bool accumulate, float* inv) {
   const uint32_t sq = P.sbase + S_Q, sk = P.sbase + S_K, sv = P.sbase + S_VT, sp = P.sbase + S_HP;
   const uint32_t id_s = tc::idesc_bf16(128, 128), id_o = tc::idesc_bf16(128, 16);
   P.before_issue();
@@ -306,17 +356,17 @@ __device__ void attn_core(Pipe& P) {
       tc::mma_bf16(P.tmem + T_GEN + 128 * j, tc::kmajor_desc(sq + (2 * j) * 4096, DH, 0),
                    tc::kmajor_desc(sk + (2 * j) * 4096, DH, 0), id_s, false);
   P.commit_wait();
-  float inv[2];
 #pragma unroll 1
   for (int pair = 0; pair < 2; ++pair) {
-    inv[pair] = softmax_head<NK>(P);
+    const float iv = G4 ? softmax_group4(P) : softmax_head<NK>(P, active);
+    if (active) inv[pair] = iv;
     P.before_issue();
     if (P.tid == 0) {
       for (int j = 0; j < 2; ++j) {
         const int hd = pair + 2 * j;
         for (int k = 0; k < 128; k += 16)
           tc::mma_bf16(P.tmem + T_O + 16 * hd, tc::kmajor_desc(sp + j * 32768, 128, k),
-                       tc::kmajor_desc(sv + hd * 4096, 128, k), id_o, k > 0);
+                       tc::kmajor_desc(sv + hd * 4096, 128, k), id_o, accumulate || k > 0);
       }
       if (pair == 0)
         for (int j = 0; j < 2; ++j)
@@ -325,12 +375,23 @@ __device__ void attn_core(Pipe& P) {
     }
     P.commit_wait();
   }
+}
+
+// context (scaled by the deferred 1 / sum) as bf16 into the A tile
+__device__ void attn_ctx(Pipe& P, const float* inv) {
   float ctx[HC];
   tmem_ld32(P.lane_addr(T_O + HC * P.h), ctx);
 #pragma unroll
   for (int c = 0; c < HC; ++c) ctx[c] *= inv[c / 16];
 #pragma unroll
   for (int q = 0; q < HC; q += 8) st_row8(P.smem + S_A, P.r, HC * P.h + q, D, ctx + q);
+}
+
+template <int NK, bool G4 = false>
+__device__ void attn_core(Pipe& P) {
+  float inv[2];
+  attn_round<NK, G4>(P, true, false, inv);
+  attn_ctx(P, inv);
 }
 
 // x += Wo . ctx + bo for valid rows (ctx already in the A tile)
@@ -351,7 +412,7 @@ __device__ void out_proj(Pipe& P, const float* bo, float* x, bool valid) {
 // memory (LayerNorm affine and biases); the weight images come from the ring.
 
 // self attention: x += MHA(LN(x + pos))  (decoder.py:214-218)
-template <int NK>
+template <int NK, bool G4 = false>
 __device__ void self_attn(Pipe& P, const float* prm, float* x, const float* pos, bool valid) {
   float a[HC];
 #pragma unroll
@@ -379,7 +440,7 @@ __device__ void self_attn(Pipe& P, const float* prm, float* x, const float* pos,
   long long q3 = clock64();
   P.prof[14] += q3 - q2;
 #endif
-  attn_core<NK>(P);
+  attn_core<NK, G4>(P);
 #ifdef FSB_PROFILE
   P.prof[15] += clock64() - q3;
 #endif
@@ -409,6 +470,54 @@ __device__ void cross_attn(Pipe& P, const float* prm, float* x, const float* fro
   P.commit_wait();
   drain_q(P, T_GEN, prm + TCP_C_BQKV);
   attn_core<BLK>(P);
+  out_proj(P, prm + TCP_C_BO, x, valid);
+}
+
+// cross attention of a hand tile (decoder.py:220-227 per hand): the queries
+// once, then one round per pair of hand slots (2c, 2c + 1): LN_kv of their
+// two crops' feature rows (block b of the 128 rows = slot 2c + b), K | V,
+// and an attention round in which only the slots' token rows are active.
+// Weight images in order t_q, t_kv (kept in its ring slot for all rounds),
+// t_o.
+__device__ void cross_attn_hands(Pipe& P, const float* prm, float* x, const DecodeArgs& a, int hand0, int nslots,
+                                 bool valid) {
+  ln_half_to_tile(P, x, prm + TCP_C_LNQ_G, prm + TCP_C_LNQ_B);
+  const uint32_t wq = P.acquire();
+  P.before_issue();
+  if (P.tid == 0) gemm(P.sbase + S_A, D, wq, D, T_GEN, P.tmem);
+  P.prefetch();
+  P.commit_wait();
+  drain_q(P, T_GEN, prm + TCP_C_BQKV);
+  const uint32_t wkv = P.acquire();
+  const int blk = P.r / BLK, rb = P.r % BLK;
+  const int nr = (nslots + 1) / 2;
+  float inv[2] = {0.0f, 0.0f};
+#pragma unroll 1
+  for (int c = 0; c < nr; ++c) {
+    const int slot = 2 * c + blk;
+    float f[HC];
+    if (slot < nslots) {
+      const int u = hand0 + slot;
+      const int crop = a.hand_feat_first + (u / 2) * a.body_feat_stride + (u % 2);
+      const float* frow = a.feats + ((int64_t)crop * 64 + rb) * D + HC * P.h;
+#pragma unroll
+      for (int q = 0; q < HC; q += 4) {
+        const float4 v = __ldg(reinterpret_cast<const float4*>(frow + q));
+        f[q] = v.x; f[q + 1] = v.y; f[q + 2] = v.z; f[q + 3] = v.w;
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < HC; ++q) f[q] = 0.0f;
+    }
+    ln_half_to_tile(P, f, prm + TCP_C_LNKV_G, prm + TCP_C_LNKV_B);
+    P.before_issue();
+    if (P.tid == 0) gemm(P.sbase + S_A, D, wkv, 2 * D, T_KV, P.tmem);
+    if (c == 0) P.prefetch();  // t_o into the slot t_q has left
+    P.commit_wait();
+    drain_kv(P, T_KV, prm + TCP_C_BQKV + 64, prm + TCP_C_BQKV + 128);
+    attn_round<BLK>(P, (rb >> 2) == c, c > 0, inv);
+  }
+  attn_ctx(P, inv);
   out_proj(P, prm + TCP_C_BO, x, valid);
 }
 
@@ -591,11 +700,19 @@ struct BodyAux {  // fp32 scratch per block
   FKOut fk[2];
   float boxtok[2][4 * D];
 };
+// Hand tiles hold kHandsPerCta hands: slot i sits in row block i % 2, rows
+// 64 (i % 2) + 4 (i / 2) + token, so the two slots of a cross-attention
+// round (2c, 2c + 1) use key blocks 0 and 1 and every warp sees one.
+#ifndef FSB_HANDS_PER_CTA
+#define FSB_HANDS_PER_CTA 8
+#endif
+constexpr int kHandsPerCta = FSB_HANDS_PER_CTA;
+static_assert(kHandsPerCta >= 2 && kHandsPerCta <= 32 && kHandsPerCta % 2 == 0, "hand slots per tile");
 struct HandAux {
-  float t0[2][D];
-  float rc[2][8];   // rots[3], cams[3]
-  float pts[2][6];  // 3 x (x, y) projected canonical points
-  int pred[2];
+  float t0[kHandsPerCta][D];
+  float rc[kHandsPerCta][8];   // rots[3], cams[3]
+  float pts[kHandsPerCta][6];  // 3 x (x, y) projected canonical points
+  int pred;
 };
 static_assert(sizeof(BodyAux) <= 16384 && sizeof(HandAux) <= 16384, "aux scratch");
 
@@ -627,16 +744,16 @@ __device__ void body_heads(Pipe& P, BodyAux& ax, const BodyW& w, const float* x)
   __syncthreads();
 }
 
-// LN(token 0) -> hand rotation / camera of both blocks (decoder.py:384-391)
+// LN(token 0) -> hand rotation / camera of every slot (decoder.py:384-391)
 __device__ void hand_heads(Pipe& P, HandAux& ax, const HandW& w, const float* x) {
   float y[HC];
   ln_half(P, x, w.norm_g, w.norm_b, y);
-  const int blk = P.r / BLK;
-  if (P.r % BLK == 0)
+  const int slot = 2 * ((P.r % BLK) >> 2) + P.r / BLK;
+  if ((P.r & 3) == 0 && slot < kHandsPerCta)
 #pragma unroll
-    for (int c = 0; c < HC; ++c) ax.t0[blk][HC * P.h + c] = y[c];
+    for (int c = 0; c < HC; ++c) ax.t0[slot][HC * P.h + c] = y[c];
   __syncthreads();
-  if (P.tid < 12) {
+  if (P.tid < 6 * kHandsPerCta) {
     const int b = P.tid / 6, o = P.tid % 6;
     const float* W = o < 3 ? w.head_rot_w : w.head_cam_w;
     float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
@@ -662,8 +779,13 @@ __global__ void __launch_bounds__(NTH, 1) k_decoders_tc(DecodeArgs a, BodyW bw, 
       const MlpW& m = body ? bw.mlp[l] : hw.mlp[l];
       sh.wptr[n] = s.t_qkv; sh.wbytes[n++] = 3 * D * D * 2;
       sh.wptr[n] = s.t_o;   sh.wbytes[n++] = D * D * 2;
-      sh.wptr[n] = c.t_kv;  sh.wbytes[n++] = 2 * D * D * 2;
-      sh.wptr[n] = c.t_q;   sh.wbytes[n++] = D * D * 2;
+      if (body) {
+        sh.wptr[n] = c.t_kv;  sh.wbytes[n++] = 2 * D * D * 2;
+        sh.wptr[n] = c.t_q;   sh.wbytes[n++] = D * D * 2;
+      } else {  // cross_attn_hands: queries first
+        sh.wptr[n] = c.t_q;   sh.wbytes[n++] = D * D * 2;
+        sh.wptr[n] = c.t_kv;  sh.wbytes[n++] = 2 * D * D * 2;
+      }
       sh.wptr[n] = c.t_o;   sh.wbytes[n++] = D * D * 2;
       sh.wptr[n] = m.t_w1;  sh.wbytes[n++] = 4 * D * D * 2;
       sh.wptr[n] = m.t_w2;  sh.wbytes[n++] = 4 * D * D * 2;
@@ -674,22 +796,18 @@ __global__ void __launch_bounds__(NTH, 1) k_decoders_tc(DecodeArgs a, BodyW bw, 
   Pipe P;
   setup(P, sh, smem);
   if (layers > 0) P.pprefetch(body ? bw.tc_params[0] : hw.tc_params[0]);
-  const int r = P.r, blk = r / BLK, rb = r % BLK, c0 = HC * P.h;
-  const int unit = body ? 2 * blockIdx.x + blk : 2 * (blockIdx.x - nbc) + blk;  // frame or hand index
-  const int nunit = body ? a.nbody : a.nhand;
-  const bool uvalid = unit < nunit;
-  const int nrows = body ? 51 : 4;
-  const bool valid = uvalid && rb < nrows;
+  const int r = P.r, blk = r / BLK, c0 = HC * P.h;
+  // body: frame 2 x + blk, token rb; hand: slot hs = 2 (r % 64 / 4) + blk, token rb
+  const int hand0 = kHandsPerCta * ((int)blockIdx.x - nbc);
+  const int nslots = body ? 0 : min(kHandsPerCta, a.nhand - hand0);
+  const int hs = 2 * ((r % BLK) >> 2) + blk;
+  const int rb = body ? r % BLK : (r & 3);
+  const bool valid = body ? (2 * (int)blockIdx.x + blk < a.nbody && rb < 51) : hs < nslots;
+  const int unit = body ? 2 * blockIdx.x + blk : 0;  // frame index (body tiles)
 
-  // feature row of this thread for cross attention
-  int crop;
-  if (body) {
-    crop = (uvalid ? unit : 0) * a.body_feat_stride;
-  } else {
-    const int hnd = uvalid ? unit : 0;
-    crop = a.hand_feat_first + (hnd / 2) * a.body_feat_stride + (hnd % 2);
-  }
-  const float* frow = a.feats + ((int64_t)crop * 64 + rb) * D;
+  // feature row of this thread for the body's cross attention
+  const int crop = (body && unit < a.nbody ? unit : 0) * a.body_feat_stride;
+  const float* frow = a.feats + ((int64_t)crop * 64 + (r % BLK)) * D;
 
   float x[HC], pos[HC];
   BodyAux& bx = *reinterpret_cast<BodyAux*>(smem + S_AUX);
@@ -717,7 +835,7 @@ __global__ void __launch_bounds__(NTH, 1) k_decoders_tc(DecodeArgs a, BodyW bw, 
   } else {
 #pragma unroll
     for (int c = 0; c < HC; ++c) x[c] = valid ? __ldg(hw.token_init + rb * D + c0 + c) : 0.0f;
-    if (t < 2) hx.pred[t] = 0;
+    if (t == 0) hx.pred = 0;
   }
   __syncthreads();
 
@@ -746,7 +864,7 @@ __global__ void __launch_bounds__(NTH, 1) k_decoders_tc(DecodeArgs a, BodyW bw, 
           j = rb - 1, kind = 1;
         }
       }
-      const int pred = body ? bx.pred[blk] : hx.pred[blk];
+      const int pred = body ? bx.pred[blk] : hx.pred;
       if (kind != 0 && !pred) {
         const float* init = body ? (kind == 1 ? bw.p2d_init : bw.p3d_init) : hw.p_init;
         const float4* src = reinterpret_cast<const float4*>(init + j * D + c0);
@@ -758,8 +876,8 @@ __global__ void __launch_bounds__(NTH, 1) k_decoders_tc(DecodeArgs a, BodyW bw, 
       } else if (kind == 1) {
         const float* w = body ? bw.phi2d_w : hw.phi2d_w;
         const float* bb = body ? bw.phi2d_b : hw.phi2d_b;
-        const float k0 = body ? bx.kp2d[blk][2 * j] : hx.pts[blk][2 * j];
-        const float k1 = body ? bx.kp2d[blk][2 * j + 1] : hx.pts[blk][2 * j + 1];
+        const float k0 = body ? bx.kp2d[blk][2 * j] : hx.pts[hs][2 * j];
+        const float k1 = body ? bx.kp2d[blk][2 * j + 1] : hx.pts[hs][2 * j + 1];
 #pragma unroll
         for (int q = 0; q < HC / 4; ++q) {
           const float4 w0 = __ldg(reinterpret_cast<const float4*>(w + c0) + q);
@@ -795,12 +913,15 @@ __global__ void __launch_bounds__(NTH, 1) k_decoders_tc(DecodeArgs a, BodyW bw, 
     if (body)
       self_attn<51>(P, prm, x, pos, valid);
     else
-      self_attn<4>(P, prm, x, pos, valid);
+      self_attn<4, true>(P, prm, x, pos, valid);
 #ifdef FSB_PROFILE
     long long ts1 = clock64();
     P.prof[5] += ts1 - ts0;
 #endif
-    cross_attn(P, prm, x, frow, valid);
+    if (body)
+      cross_attn(P, prm, x, frow, valid);
+    else
+      cross_attn_hands(P, prm, x, a, hand0, nslots, valid);
 #ifdef FSB_PROFILE
     long long ts2 = clock64();
     P.prof[6] += ts2 - ts1;
@@ -844,7 +965,7 @@ __global__ void __launch_bounds__(NTH, 1) k_decoders_tc(DecodeArgs a, BodyW bw, 
       } else {
         // canonical points through the predicted rotation (decoder.py:399-409)
         hand_heads(P, hx, hw, x);
-        if (t < 2) {
+        if (t < kHandsPerCta) {
           const float* rc = hx.rc[t];
           float R[9];
           rodrigues3<true>(rc[0], rc[1], rc[2], R);
@@ -856,8 +977,8 @@ __global__ void __launch_bounds__(NTH, 1) k_decoders_tc(DecodeArgs a, BodyW bw, 
             hx.pts[t][2 * i] = rc[3] * q[0] + rc[4];
             hx.pts[t][2 * i + 1] = rc[3] * q[1] + rc[5];
           }
-          hx.pred[t] = 1;
         }
+        if (t == 0) hx.pred = 1;
         __syncthreads();
       }
     }
@@ -881,9 +1002,9 @@ __global__ void __launch_bounds__(NTH, 1) k_decoders_tc(DecodeArgs a, BodyW bw, 
     }
   } else {
     hand_heads(P, hx, hw, x);
-    if (t < 6) {
-      const int b = t / 3, o = t % 3, u = 2 * (blockIdx.x - nbc) + b;
-      if (u < a.nhand) {
+    if (t < 3 * kHandsPerCta) {
+      const int b = t / 3, o = t % 3, u = hand0 + b;
+      if (b < nslots) {
         const float v = hx.rc[b][o];
         flag_nonfinite(a.nonfinite, v);
         a.hand_rots[(int64_t)u * 3 + o] = v;
@@ -921,7 +1042,7 @@ cudaError_t launch_encoder_tc(const float* crops, int ncrops, const EncW& w, flo
 }
 
 cudaError_t launch_decoders_tc(const DecodeArgs& a, const BodyW& bw, const HandW& hw, cudaStream_t st) {
-  const int n = (a.nbody + 1) / 2 + (a.nhand + 1) / 2;
+  const int n = (a.nbody + 1) / 2 + (a.nhand + kHandsPerCta - 1) / kHandsPerCta;
   if (n == 0) return cudaSuccess;
   k_decoders_tc<<<n, NTH, SMEM_TC, st>>>(a, bw, hw);
   return cudaGetLastError();

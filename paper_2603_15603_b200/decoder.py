@@ -76,8 +76,58 @@ def selection_mask(selection, layers, what="selection"):
     return m, len(sel)
 
 
+class WeightTable(dict):
+    """The decoder's name -> array table.  Counts its own mutations so the
+    per-batch "has the table changed since upload" check is O(1)."""
+
+    version = 0
+
+    def _touch(self):
+        self.version += 1
+
+    def __setitem__(self, k, v):
+        super().__setitem__(k, v)
+        self._touch()
+
+    def __delitem__(self, k):
+        super().__delitem__(k)
+        self._touch()
+
+    def update(self, *a, **kw):
+        super().update(*a, **kw)
+        self._touch()
+
+    def pop(self, *a):
+        self._touch()
+        return super().pop(*a)
+
+    def popitem(self):
+        self._touch()
+        return super().popitem()
+
+    def clear(self):
+        super().clear()
+        self._touch()
+
+    def setdefault(self, k, v=None):
+        self._touch()
+        return super().setdefault(k, v)
+
+    def __ior__(self, other):
+        self.update(other)
+        return self
+
+
 class Decoder:
     """Frozen encoder plus body/hand decoders sharing one weight table."""
+
+    @property
+    def weights(self):
+        return self._weights
+
+    @weights.setter
+    def weights(self, table):
+        self._weights = table if isinstance(table, WeightTable) else WeightTable(table)
 
     def __init__(self, template, config=None, seed=40):
         self.template = template
@@ -91,7 +141,8 @@ class Decoder:
     def context(self, device=None):
         """The fsb_ctx holding this decoder's weights (uploaded lazily; a
         changed weight table is re-uploaded)."""
-        stamp = tuple((k, id(v)) for k, v in sorted(self.weights.items()))
+        w = self._weights
+        stamp = (id(w), w.version)  # O(1): the launch path calls this every batch
         if self._ctx is None:
             self._ctx = runtime.Context(device)
         if self._uploaded != stamp:
