@@ -64,6 +64,10 @@ struct VertexTmpl {
       const float4 x = __ldg(src + q);
       f[4 * q] = x.x; f[4 * q + 1] = x.y; f[4 * q + 2] = x.z; f[4 * q + 3] = x.w;
     }
+    unpack(f);
+  }
+  // from a record already in registers / shared memory
+  __device__ void unpack(const float* f) {
 #pragma unroll
     for (int c = 0; c < 3; ++c) vr[c] = f[c];
 #pragma unroll
@@ -354,18 +358,80 @@ __global__ void k_proj_center(float* __restrict__ sub, const float* __restrict__
   }
 }
 
+// Re-skinned projector inputs for a group of kProjMeshes meshes: the three
+// corner records of this thread's target are read from the template once
+// and applied to every mesh of the group (the transforms and shape
+// coefficients of the group are staged in shared memory), so a batch of 32
+// meshes is 32 CTAs instead of 256.  Same per-target arithmetic and the same
+// per-chunk partial-sum order as proj_inputs_cta.
+constexpr int kProjMeshes = 8;
+
 template <int NZ>
 __global__ void __launch_bounds__(256) k_proj_inputs(TemplateDev t, ProjectorDev p, const float* __restrict__ rel,
-                                                     const float* __restrict__ poses, int ld_pose,
+                                                     const float* __restrict__ poses, int ld_pose, int B,
                                                      float* __restrict__ sub, float* __restrict__ psum) {
-  __shared__ __align__(16) float sm[336];
-  float* A = sm;          // 264
-  float* shp = sm + 264;  // 10
-  const int b = blockIdx.x, tid = threadIdx.x;
-  for (int i = tid; i < FSB_NJ * 12; i += blockDim.x) A[i] = rel[(int64_t)b * FSB_NJ * 12 + i];
-  if (tid < 10) shp[tid] = poses[(int64_t)b * ld_pose + 66 + tid];
+  constexpr int RS = vertex_record_floats(NZ);
+  __shared__ __align__(16) float A[kProjMeshes][FSB_NJ * 12];
+  __shared__ float shp[kProjMeshes][10];
+  __shared__ float v0[kProjMeshes][3];
+  __shared__ float rec0[RS];  // template record of vertex 0
+  __shared__ float red[kProjMeshes][32][3];
+  const int m0 = blockIdx.y * kProjMeshes, nm = min(kProjMeshes, B - m0);
+  const int chunk = blockIdx.x, tid = threadIdx.x;
+  for (int i = tid; i < nm * FSB_NJ * 12; i += blockDim.x)
+    (&A[0][0])[i] = rel[(int64_t)m0 * FSB_NJ * 12 + i];
+  for (int i = tid; i < nm * 10; i += blockDim.x) shp[i / 10][i % 10] = poses[(int64_t)(m0 + i / 10) * ld_pose + 66 + i % 10];
+  for (int i = tid; i < RS; i += blockDim.x) rec0[i] = __ldg(t.rec + i);
+  const int per = (p.n_sub + kProjChunks - 1) / kProjChunks;
+  const int i = chunk * per + tid;
+  const bool act = tid < per && i < p.n_sub;
+  VertexTmpl<NZ> vt[3];
+  float wc[3];
+  if (act)
+#pragma unroll
+    for (int c = 0; c < 3; ++c) {
+      vt[c].load(t, p.corners[3 * i + c]);
+      wc[c] = p.bw[3 * i + c];
+    }
   __syncthreads();
-  proj_inputs_cta(SkinSource<NZ>{t, A, shp}, p, sm, b, blockIdx.y, sub, psum);
+  if (tid < nm) {
+    VertexTmpl<NZ> r0;
+    r0.unpack(rec0);
+    r0.apply(A[tid], shp[tid], v0[tid]);
+  }
+  __syncthreads();
+  // per-mesh sums are reduced after the loop (independent shuffle chains)
+  float acc[kProjMeshes][3];
+#pragma unroll
+  for (int m = 0; m < kProjMeshes; ++m) {
+    acc[m][0] = acc[m][1] = acc[m][2] = 0.0f;
+    if (act && m < nm) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        float o[3];
+        vt[c].apply(A[m], shp[m], o);
+#pragma unroll
+        for (int a = 0; a < 3; ++a) acc[m][a] = fmaf(wc[c], o[a] - v0[m][a], acc[m][a]);
+      }
+#pragma unroll
+      for (int a = 0; a < 3; ++a) sub[((int64_t)(m0 + m) * p.n_sub + i) * 3 + a] = acc[m][a];
+    }
+  }
+  const int warp = tid / 32, lane = tid % 32;
+#pragma unroll
+  for (int m = 0; m < kProjMeshes; ++m)
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const float r = warp_sum(acc[m][a]);
+      if (lane == 0) red[m][warp][a] = r;
+    }
+  __syncthreads();
+  if (tid < 3 * nm) {
+    const int m = tid / 3, a = tid % 3;
+    float tot = 0.0f;
+    for (int w = 0; w < (int)blockDim.x / 32; ++w) tot += red[m][w][a];
+    psum[((int64_t)(m0 + m) * kProjChunks + chunk) * 3 + a] = tot;
+  }
 }
 
 __global__ void __launch_bounds__(256) k_proj_inputs_v(const float* __restrict__ V, int nv, ProjectorDev p,
@@ -510,12 +576,12 @@ cudaError_t launch_proj_inputs(const TemplateDev& t, const ProjectorDev& p, cons
                                cudaStream_t st) {
   if (B == 0) return cudaSuccess;
   const int nt = proj_threads(p);
-  if (nt > 1024) return cudaErrorInvalidValue;
-  const dim3 grid(B, kProjChunks);
+  if (nt > 256) return cudaErrorInvalidValue;  // n_sub <= 2048 (launch bounds)
+  const dim3 grid(kProjChunks, (B + kProjMeshes - 1) / kProjMeshes);
   switch (t.nnz) {
-    case 2: k_proj_inputs<2><<<grid, nt, 0, st>>>(t, p, rel, poses, ld_pose, sub, psum); break;
-    case 4: k_proj_inputs<4><<<grid, nt, 0, st>>>(t, p, rel, poses, ld_pose, sub, psum); break;
-    case 8: k_proj_inputs<8><<<grid, nt, 0, st>>>(t, p, rel, poses, ld_pose, sub, psum); break;
+    case 2: k_proj_inputs<2><<<grid, nt, 0, st>>>(t, p, rel, poses, ld_pose, B, sub, psum); break;
+    case 4: k_proj_inputs<4><<<grid, nt, 0, st>>>(t, p, rel, poses, ld_pose, B, sub, psum); break;
+    case 8: k_proj_inputs<8><<<grid, nt, 0, st>>>(t, p, rel, poses, ld_pose, B, sub, psum); break;
     default: return cudaErrorInvalidValue;
   }
   cudaError_t e = cudaGetLastError();
@@ -526,7 +592,7 @@ cudaError_t launch_proj_inputs_v(const float* V, int nv, const ProjectorDev& p, 
                                  __nv_bfloat16* xb, float* psum, cudaStream_t st) {
   if (B == 0) return cudaSuccess;
   const int nt = proj_threads(p);
-  if (nt > 1024) return cudaErrorInvalidValue;
+  if (nt > 256) return cudaErrorInvalidValue;  // n_sub <= 2048 (launch bounds)
   k_proj_inputs_v<<<dim3(B, kProjChunks), nt, 0, st>>>(V, nv, p, sub, psum);
   cudaError_t e = cudaGetLastError();
   return e != cudaSuccess ? e : launch_proj_center(p, B, sub, psum, f32, xb, st);

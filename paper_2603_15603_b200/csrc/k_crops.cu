@@ -108,27 +108,33 @@ constexpr int kRowsPerCTA = 16;
 }  // namespace
 
 // grid: (S / kRowsPerCTA, 3, B); block: 256 threads
+// Boxes and prompt of every frame, one thread per frame (the serial float
+// sums of the reference), ahead of the gather CTAs that read them.
+__global__ void k_frame_boxes(const float* __restrict__ kps, int B, int W, int H, double alpha,
+                              double* __restrict__ boxes_out, float* __restrict__ prompt_out) {
+  const int f = blockIdx.x * blockDim.x + threadIdx.x;
+  if (f >= B) return;
+  float kp[2 * FSB_NJ];
+#pragma unroll
+  for (int i = 0; i < 2 * FSB_NJ; ++i) kp[i] = kps[(int64_t)f * 2 * FSB_NJ + i];
+  FrameBoxes fb;
+  frame_boxes(kp, W, H, alpha, fb);
+  for (int c = 0; c < 3; ++c)
+    for (int e = 0; e < 4; ++e) boxes_out[((int64_t)f * 3 + c) * 4 + e] = fb.box[c][e];
+  for (int e = 0; e < 8; ++e) prompt_out[(int64_t)f * 8 + e] = fb.prompt[e];
+}
+
 __global__ void __launch_bounds__(256) k_boxes_crops(
     const float* __restrict__ images, const float* __restrict__ kps, int B, int H, int W, int S,
     double alpha, int64_t img_stride, double* __restrict__ boxes_out, float* __restrict__ prompt_out,
     float* __restrict__ crops_out, int32_t* __restrict__ taps_out, int* nonfinite) {
-  __shared__ FrameBoxes fb;
-  __shared__ float kp_s[2 * FSB_NJ];
+  __shared__ double bx[4];
   __shared__ float gx[512], gy[512];  // S <= 512 (checked by the launcher)
   const int f = blockIdx.z, crop = blockIdx.y, band = blockIdx.x;
   const int tid = threadIdx.x;
-  if (tid < 2 * FSB_NJ) kp_s[tid] = kps[(int64_t)f * 2 * FSB_NJ + tid];
+  // the frame's boxes come from k_frame_boxes (same stream, launched first)
+  if (tid < 4) bx[tid] = boxes_out[((int64_t)f * 3 + crop) * 4 + tid];
   __syncthreads();
-  if (tid == 0) {
-    frame_boxes(kp_s, W, H, alpha, fb);
-    if (band == 0 && crop == 0) {
-      for (int c = 0; c < 3; ++c)
-        for (int e = 0; e < 4; ++e) boxes_out[((int64_t)f * 3 + c) * 4 + e] = fb.box[c][e];
-      for (int e = 0; e < 8; ++e) prompt_out[(int64_t)f * 8 + e] = fb.prompt[e];
-    }
-  }
-  __syncthreads();
-  const double* bx = fb.box[crop];
   for (int i = tid; i < S; i += blockDim.x) {
     gx[i] = lin_f32(bx[0], bx[2], S, i);
     gy[i] = lin_f32(bx[1], bx[3], S, i);
@@ -393,6 +399,7 @@ cudaError_t launch_boxes_crops(const float* images, const float* kps, int B, int
         images, kps, B, H, W, S, alpha, stride, rowcap4, rows_per_cta, boxes, prompt, crops, taps, nonfinite,
         bytes_in);
   } else {  // HBM-resident (or very wide / unaligned host) frames: per-tap reads
+    k_frame_boxes<<<(B + 63) / 64, 64, 0, st>>>(kps, B, W, H, alpha, boxes, prompt);
     dim3 grid((S + kRowsPerCTA - 1) / kRowsPerCTA, 3, B);
     k_boxes_crops<<<grid, 256, 0, st>>>(images, kps, B, H, W, S, alpha, stride, boxes, prompt, crops, taps,
                                         nonfinite);

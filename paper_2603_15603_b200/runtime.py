@@ -18,7 +18,7 @@ import numpy as np
 from .numkit import NumericError, ShapeError, UsageError
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "lib", "libfsb_b200.so")
+LIB_PATH = os.environ.get("FSB_LIB") or os.path.join(_PKG, "lib", "libfsb_b200.so")  # FSB_LIB: A/B builds
 
 FSB_FP32, FSB_BF16 = 0, 1
 FSB_MHR, FSB_SMPL = 0, 1
