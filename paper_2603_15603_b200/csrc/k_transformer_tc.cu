@@ -3,64 +3,82 @@
 // Same math as the fp32 kernels in k_transformer.cu (reference decoder.py:
 // encode :231-260, _attention :172-203, _mlp :205-212, decode_body
 // :284-356, decode_hand :360-410) with every GEMM on tcgen05: operands are
-// bf16 in shared memory (K-major UMMA layout, tc_sm100.cuh), accumulators
-// are fp32 in TMEM, and the LayerNorm / softmax / residual / ReLU
-// epilogues run in fp32 registers.
+// bf16 in shared memory (K-major UMMA layout, tc_sm100.cuh) or in TMEM,
+// accumulators are fp32 in TMEM, and the LayerNorm / softmax / residual /
+// ReLU epilogues run in fp32 registers.
 //
-// One CTA = 8 warps = 256 threads over 128 TMEM lanes = 128 token rows,
-// organised as two 64-row blocks: two crops (encoder), two frames' body
-// tokens (51 valid rows each) or two hands (4 valid rows each).  Row r is
-// owned by threads r and r + 128 (warps w and w + 4 read the same TMEM lane
-// quadrant): each holds 32 of the row's 64 residual-stream values in
-// registers, LayerNorm sums are combined through a double-buffered shared
-// exchange (one barrier per reduction), and in attention each of the two
-// threads runs the softmax of a different head.  Attention of the two
-// blocks is one 128 x 128 score tile whose off-diagonal block is masked to
-// zero, so P.V stays a single MMA chain.  Weights (pre-packed bf16 W^T
-// images) stream through two 32 KB slots with cp.async.bulk, one GEMM ahead.
+// A tile = 128 token rows = 128 TMEM lanes, organised as two 64-row blocks:
+// two crops (encoder), two frames' body tokens (51 valid rows each) or
+// kHandsPerCta hands (4 rows each).  One CTA runs TWO independent tiles
+// ("groups" of 8 warps, 256 threads, 256 TMEM columns each) so that one
+// group's element-wise phases overlap the other's tensor-core, TMEM and
+// barrier latencies: the decoder is a long serial chain of small GEMMs and
+// one tile alone leaves the SM mostly idle.  The groups share the weight
+// stream: pre-packed bf16 W^T images flow through a two-slot ring filled by
+// cp.async.bulk, and a slot is refilled by whichever group releases it last.
+//
+// Within a group, row r is owned by threads r and r + 128 (warps w and w + 4
+// read the same TMEM lane quadrant): each holds 32 of the row's 64
+// residual-stream values in registers; LayerNorm sums are combined through a
+// double-buffered shared exchange (one group barrier per reduction).
+// Attention runs two heads at a time: S = Q K^T for both (2 x 128 TMEM
+// columns), the softmax writes P as packed bf16 back over S, and P.V reads P
+// straight from TMEM (tcgen05.mma with A in TMEM).  The MLP hidden layer is
+// likewise packed in place and read by the second GEMM from TMEM, so no
+// 128 x 256 operand ever goes through shared memory.
 #include "fsb_common.cuh"
 #include "fsb_weights.h"
 #include "tc_sm100.cuh"
 
 namespace {
 
-constexpr int D = 64, DH = 16, NTH = 256, ROWS = 128, BLK = 64, HC = 32;  // HC: columns per thread
+constexpr int D = 64, DH = 16, GT = 256, NG = 2, NTH = NG * GT, ROWS = 128, BLK = 64, HC = 32;
 
-// shared memory map (bytes)
-constexpr uint32_t S_A = 0;         // 128 x 64 bf16 GEMM A operand           16 KB
-constexpr uint32_t S_Q = 16384;     // 4 heads x (128 x 16) queries           16 KB
-constexpr uint32_t S_K = 32768;     // 4 heads x (128 x 16) keys              16 KB
-constexpr uint32_t S_VT = 49152;    // 4 heads x (16 x 128) values^T          16 KB
-constexpr uint32_t S_HP = 65536;    // MLP hidden 128x256 | P 2x(128x128) | patches 128x192   64 KB
-constexpr uint32_t S_W = 131072;    // 2 weight slots x 32 KB
-constexpr uint32_t S_AUX = 196608;  // fp32 role scratch                      16 KB
-constexpr uint32_t S_PRM = S_AUX + 16384;  // 2 slots of the per-layer TCP_* parameter block
+// shared memory map (bytes).  Per group g at g * S_GROUP:
+constexpr uint32_t S_A = 0;       // 128 x 64 bf16 GEMM A operand / attention context    16 KB
+constexpr uint32_t S_Q = 16384;   // 4 heads x (128 x 16) queries                        16 KB
+constexpr uint32_t S_K = 32768;   // 4 heads x (128 x 16) keys                           16 KB
+constexpr uint32_t S_VT = 49152;  // 4 heads x (16 x 128) values^T                       16 KB
+constexpr uint32_t S_GROUP = 65536;
+// (encoder: the patch operand, 128 x 192 bf16 = 48 KB, spans S_A..S_K)
+// shared by both groups:
+constexpr uint32_t S_W = NG * S_GROUP;             // 2 weight slots x 32 KB
+constexpr uint32_t W_SLOT = 32768;
+constexpr uint32_t S_PRM = S_W + 2 * W_SLOT;        // 2 slots of the per-layer TCP_* parameter block
 constexpr uint32_t PRM_BYTES = TCP_FLOATS * 4;
-constexpr uint32_t SMEM_TC = S_PRM + 2 * PRM_BYTES;
-static_assert(SMEM_TC <= 227 * 1024, "shared memory budget");
+constexpr uint32_t S_AUX = S_PRM + 2 * PRM_BYTES;   // per group role scratch
+constexpr uint32_t AUX_BYTES = 7168;
+constexpr uint32_t SMEM_TC = S_AUX + NG * AUX_BYTES;
+static_assert(SMEM_TC + 6 * 1024 <= 227 * 1024, "shared memory budget");
 
-// TMEM columns
-constexpr uint32_t T_GEN = 0;   // GEMM accumulators / attention score pair
-constexpr uint32_t T_O = 256;   // attention context (4 heads x 16)
-constexpr uint32_t T_KV = 384;  // cross-attention K | V of the feature rows
+// TMEM: 512 columns, group g at 256 g.  Within a group:
+//   [0, 256)  GEMM accumulators (QKV 192, KV 128, W1 256, out 64) and the
+//             attention score pair (head j of the pair at 128 j; P packed
+//             over its first 64 columns)
+//   [64, 96)  P.V output of the pair (outside both P regions)
+constexpr uint32_t T_GEN = 0;
+constexpr uint32_t T_PV = 64;
 
 constexpr int kMaxW = 64;
 
 struct Shared {
-  uint64_t wbar[2];
-  uint64_t pbar[2];
-  uint64_t mbar;
+  uint64_t wbar[2];     // weight slot full
+  uint64_t pbar[2];     // parameter slot full
+  uint64_t mbar[NG];    // per-group MMA completion
   uint32_t tmem;
-  int nw;
+  int nw, nprm;
+  unsigned wrel[2];     // releases of each weight slot (monotonic)
+  unsigned prel[2];     // releases of each parameter slot
   const uint8_t* wptr[kMaxW];
   uint32_t wbytes[kMaxW];
-  float xch[2][2 * ROWS];  // row-reduction exchange, double buffered
+  const float* pptr[FSB_MAX_LAYERS + 8];
+  float xch[NG][2][2 * ROWS];  // row-reduction exchange, per group, double buffered
 };
 
 #ifdef FSB_PROFILE
-// cycle attribution of CTA 0 / thread 0 (build with FSB_PROFILE=1):
+// cycle attribution of CTA 0 / group 0 (build with FSB_PROFILE=1):
 // [0] total, [1] MMA waits, [2] weight waits, [3] issue barriers,
-// [4] row-exchange barriers
+// [4] row-exchange barriers, [5..] per-phase (see the kernels)
 __device__ unsigned long long g_tc_prof[2][2][16];  // [role][thread 0 | thread 255][counter]
 #define PROF_T0() const long long prof_t0_ = clock64()
 #define PROF_ADD(i) (prof[i] += clock64() - prof_t0_)
@@ -69,44 +87,30 @@ __device__ unsigned long long g_tc_prof[2][2][16];  // [role][thread 0 | thread 
 #define PROF_ADD(i)
 #endif
 
-// per-thread pipeline state (every thread tracks the same phases)
+// per-thread pipeline state (every thread of a group tracks the same phases)
 struct Pipe {
   Shared* sh;
-  uint8_t* smem;
-  uint32_t sbase;  // shared-space address of smem
-  uint32_t tmem;
+  uint8_t* smem;   // this group's region
+  uint8_t* sall;   // CTA shared base
+  uint32_t sbase;  // shared-space address of this group's region
+  uint32_t wbase;  // shared-space address of the weight ring
+  uint32_t tmem;   // this group's TMEM base
   uint32_t mphase;
-  int wload, wuse, xc, pload, puse;
-  int tid, r, h;
+  int wuse, xc, puse;
+  int g, tid, r, h;
 #ifdef FSB_PROFILE
   long long prof[16];
 #endif
 
-  // per-layer parameter block ring (TCP_* layout): thread 0 issues, every
-  // thread waits on the slot it reads
-  __device__ void pprefetch(const float* src) {
-    if (tid == 0 && src != nullptr) {
-      const int slot = pload & 1;
-      tc::mbar_expect_tx(&sh->pbar[slot], PRM_BYTES);
-      tc::bulk_g2s(smem + S_PRM + slot * PRM_BYTES, src, PRM_BYTES, &sh->pbar[slot]);
-    }
-    ++pload;
-  }
-  __device__ const float* pacquire() {
-    const int slot = puse & 1;
-    tc::mbar_wait(&sh->pbar[slot], (uint32_t)((puse >> 1) & 1));
-    ++puse;
-    return reinterpret_cast<const float*>(smem + S_PRM + slot * PRM_BYTES);
-  }
+  __device__ void sync() const { asm volatile("bar.sync %0, %1;\n" ::"r"(1 + g), "r"(GT) : "memory"); }
 
-  __device__ void prefetch() {  // next weight image into its ring slot
-    if (wload < sh->nw) {
-      if (tid == 0) {
-        const int slot = wload & 1;
-        tc::mbar_expect_tx(&sh->wbar[slot], sh->wbytes[wload]);
-        tc::bulk_g2s(smem + S_W + slot * 32768u, sh->wptr[wload], sh->wbytes[wload], &sh->wbar[slot]);
-      }
-      ++wload;
+  // weight ring: image i lives in slot i & 1.  The last of the two groups to
+  // release image i - 1 loads image i + 1 into its slot.
+  __device__ void load_image(int i) {
+    if (i < sh->nw) {
+      const int slot = i & 1;
+      tc::mbar_expect_tx(&sh->wbar[slot], sh->wbytes[i]);
+      tc::bulk_g2s(sall + S_W + slot * W_SLOT, sh->wptr[i], sh->wbytes[i], &sh->wbar[slot]);
     }
   }
   __device__ uint32_t acquire() {  // wait for the next weight image; returns its address
@@ -115,21 +119,55 @@ struct Pipe {
     tc::mbar_wait(&sh->wbar[slot], (uint32_t)((wuse >> 1) & 1));
     ++wuse;
     PROF_ADD(2);
-    return sbase + S_W + slot * 32768u;
+    return wbase + slot * W_SLOT;
   }
+  // called once per acquired image, after the GEMM that reads it has been
+  // issued: image wuse - 2's GEMM has completed by then
+  __device__ void prefetch() {
+    const int done = wuse - 2;
+    if (done >= 0 && tid == 0) {
+      const unsigned prior = atomicAdd(&sh->wrel[done & 1], 1u);
+      if ((prior % NG) == NG - 1) load_image(done + 2);
+    }
+  }
+
+  // per-layer parameter blocks: same protocol, one block per layer
+  __device__ void load_prm(int l) {
+    if (l < sh->nprm) {
+      const int slot = l & 1;
+      tc::mbar_expect_tx(&sh->pbar[slot], PRM_BYTES);
+      tc::bulk_g2s(sall + S_PRM + slot * PRM_BYTES, sh->pptr[l], PRM_BYTES, &sh->pbar[slot]);
+    }
+  }
+  __device__ const float* pacquire() {
+    const int slot = puse & 1;
+    tc::mbar_wait(&sh->pbar[slot], (uint32_t)((puse >> 1) & 1));
+    ++puse;
+    return reinterpret_cast<const float*>(sall + S_PRM + slot * PRM_BYTES);
+  }
+  // every thread of the group is past layer puse - 2 (call after a group
+  // barrier at the start of layer puse - 1)
+  __device__ void prelease() {
+    const int done = puse - 2;
+    if (done >= 0 && tid == 0) {
+      const unsigned prior = atomicAdd(&sh->prel[done & 1], 1u);
+      if ((prior % NG) == NG - 1) load_prm(done + 2);
+    }
+  }
+
   // operands written by threads -> visible to the tensor core; TMEM reads done
   __device__ void before_issue() {
     PROF_T0();
     tc::fence_async_smem();
     tc::fence_before();
-    __syncthreads();
+    sync();
     tc::fence_after();
     PROF_ADD(3);
   }
   __device__ void commit_wait() {
     PROF_T0();
-    if (tid == 0) tc::mma_commit(&sh->mbar);
-    tc::mbar_wait(&sh->mbar, mphase);
+    if (tid == 0) tc::mma_commit(&sh->mbar[g]);
+    tc::mbar_wait(&sh->mbar[g], mphase);
     mphase ^= 1u;
     tc::fence_after();
     PROF_ADD(1);
@@ -137,13 +175,13 @@ struct Pipe {
   __device__ uint32_t lane_addr(uint32_t col) const {
     return tmem + ((uint32_t)(((tid >> 5) & 3) * 32) << 16) + col;
   }
-  // sum of the two threads' partials of row r (one barrier)
+  // sum of the two threads' partials of row r (one group barrier)
   __device__ float row_total(float part) {
-    float* b = sh->xch[xc & 1];
+    float* b = sh->xch[g][xc & 1];
     ++xc;
     b[h * ROWS + r] = part;
     PROF_T0();
-    __syncthreads();
+    sync();
     PROF_ADD(4);
     return b[r] + b[ROWS + r];
   }
@@ -169,10 +207,6 @@ __device__ __forceinline__ void st_row8(uint8_t* tile, int r, int k0, int K, con
   *reinterpret_cast<uint4*>(tile + tc::kmajor_off(r, k0, K)) = u;
 }
 
-__device__ __forceinline__ void st_row_zero8(uint8_t* tile, int r, int k0, int K) {
-  *reinterpret_cast<uint4*>(tile + tc::kmajor_off(r, k0, K)) = make_uint4(0u, 0u, 0u, 0u);
-}
-
 // 32-element sum with 8 independent partial chains
 __device__ __forceinline__ float sum32(const float* v) {
   float p[8];
@@ -183,27 +217,70 @@ __device__ __forceinline__ float sum32(const float* v) {
   return ((p[0] + p[1]) + (p[2] + p[3])) + ((p[4] + p[5]) + (p[6] + p[7]));
 }
 
-// LayerNorm (numkit.py:198-202) of row r split over the thread pair: this
-// thread's 32 columns [32h, 32h + 32) normalised into y
-__device__ __forceinline__ void ln_half(Pipe& P, const float* x, const float* g, const float* b, float* y) {
-  const float mu = P.row_total(sum32(x)) * (1.0f / D);
-  float d[HC];
+// sum of squared deviations, same partial-chain order as sum32 over d[c]
+__device__ __forceinline__ float sumsq32(const float* x, float mu) {
+  float p[8];
 #pragma unroll
-  for (int c = 0; c < HC; ++c) {
-    const float e = x[c] - mu;
-    d[c] = e * e;
+  for (int i = 0; i < 8; ++i) {
+    const float e = x[i] - mu;
+    p[i] = e * e;
   }
-  const float rstd = 1.0f / sqrtf(P.row_total(sum32(d)) * (1.0f / D) + 1e-5f);
+#pragma unroll
+  for (int c = 8; c < 32; ++c) {
+    const float e = x[c] - mu;
+    p[c & 7] += e * e;
+  }
+  return ((p[0] + p[1]) + (p[2] + p[3])) + ((p[4] + p[5]) + (p[6] + p[7]));
+}
+
+// LayerNorm (numkit.py:198-202) of row r split over the thread pair: mean
+// and 1 / std of the row (this thread holds columns [32h, 32h + 32))
+__device__ __forceinline__ void ln_stats(Pipe& P, const float* x, float& mu, float& rstd) {
+  mu = P.row_total(sum32(x)) * (1.0f / D);
+  rstd = 1.0f / sqrtf(P.row_total(sumsq32(x, mu)) * (1.0f / D) + 1e-5f);
+}
+
+__device__ __forceinline__ void ln_half(Pipe& P, const float* x, const float* g, const float* b, float* y) {
+  float mu, rstd;
+  ln_stats(P, x, mu, rstd);
   const int c0 = HC * P.h;
 #pragma unroll
   for (int c = 0; c < HC; ++c) y[c] = fmaf((x[c] - mu) * rstd, g[c0 + c], b[c0 + c]);  // g, b: shared or global
 }
 
-__device__ __forceinline__ void ln_half_to_tile(Pipe& P, const float* x, const float* g, const float* b) {
-  float y[HC];
-  ln_half(P, x, g, b, y);
+// LN straight into a bf16 K-major tile, 8 columns at a time
+__device__ __forceinline__ void ln_half_to_tile(Pipe& P, const float* x, const float* g, const float* b,
+                                                uint32_t tile = S_A) {
+  float mu, rstd;
+  ln_stats(P, x, mu, rstd);
+  const int c0 = HC * P.h;
 #pragma unroll
-  for (int q = 0; q < HC; q += 8) st_row8(P.smem + S_A, P.r, HC * P.h + q, D, y + q);
+  for (int q = 0; q < HC; q += 8) {
+    float y[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) y[c] = fmaf((x[q + c] - mu) * rstd, g[c0 + q + c], b[c0 + q + c]);
+    st_row8(P.smem + tile, P.r, c0 + q, D, y);
+  }
+}
+
+// fp32 row tile over [S_Q, S_Q + 32 KB) (free between layers and before
+// the QKV GEMM): row r, 16-byte chunk q at r * 256 + 16 (q ^ (r & 7)), so a
+// warp's rows hit distinct banks.  Holds the self-attention input x + pos
+// and the residual stream across the heads / FK block, keeping both out of
+// registers (a thread has 128 of them with two groups per SM).
+__device__ __forceinline__ float4* xrow(Pipe& P, int q) {
+  return reinterpret_cast<float4*>(P.smem + S_Q + P.r * 256 + ((q ^ (P.r & 7)) << 4));
+}
+__device__ __forceinline__ void save_row(Pipe& P, const float* x) {
+#pragma unroll
+  for (int k = 0; k < 8; ++k) *xrow(P, 8 * P.h + k) = make_float4(x[4 * k], x[4 * k + 1], x[4 * k + 2], x[4 * k + 3]);
+}
+__device__ __forceinline__ void load_row(Pipe& P, float* x) {
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    const float4 v = *xrow(P, 8 * P.h + k);
+    x[4 * k] = v.x; x[4 * k + 1] = v.y; x[4 * k + 2] = v.z; x[4 * k + 3] = v.w;
+  }
 }
 
 // query columns [qcol, +64) + bias -> heads 2h, 2h+1 of the query tiles
@@ -249,60 +326,69 @@ __device__ void drain_kv(Pipe& P, uint32_t kcol, const float* bk, const float* b
   }
 }
 
+constexpr float kScale = 0.25f * 1.4426950408889634f;  // f32(1/sqrt(16)) * log2(e)
+
 // softmax of head (pair + 2 h) over the first NK keys of the row's own key
-// block -> P tile h, unnormalised (the context is scaled by the returned
-// 1 / sum after P.V: 16 multiplies instead of 64).  NK is the number of
-// valid keys (64 for encoder self-attention and cross-attention, 51 body
-// tokens, 4 hand tokens), so masking is resolved at compile time.
+// block; P (unnormalised, bf16) is packed over the head's S columns
+// [128 h, 128 h + 64): the own block's 64 keys in 32 columns, zeros for the
+// other block.  Returns 1 / sum (the context is scaled after P.V: 16
+// multiplies instead of 64).  NK: 64 (encoder self-attention, cross
+// attention), 51 (body tokens).  inactive rows write a zero P row.
 template <int NK>
 __device__ float softmax_head(Pipe& P, bool active = true) {
-  static_assert(NK >= 1 && NK <= 64, "keys per block");
-  constexpr int NL = NK <= 16 ? 16 : (NK <= 32 ? 32 : 64);  // TMEM columns loaded
+  static_assert(NK > 32 && NK <= 64, "keys per block");
   const int blk = P.r / BLK;
-  float s[64];
-  const uint32_t ta = P.lane_addr(T_GEN + 128 * P.h + 64 * blk);
-  if (NL == 64) tc::tmem_ld64(ta, s);
-  else if (NL == 32) tmem_ld32(ta, s);
-  else tc::tmem_ld16(ta, s);
-  if (!active) {  // a row outside this round: P row of zeros
-#pragma unroll
-    for (int q = 0; q < 16; ++q) st_row_zero8(P.smem + S_HP + P.h * 32768, P.r, 8 * q, 128);
-    return 0.0f;
-  }
+  const uint32_t tcol = T_GEN + 128 * P.h;
+  const uint32_t sa = P.lane_addr(tcol + 64 * blk);
+  // two passes over 32-column halves (32 live registers instead of 64):
+  // the maximum, then exponentials packed as bf16 over the half just read
+  float s[32];
   float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-  for (int k = 0; k < NK; ++k) m4[k & 3] = fmaxf(m4[k & 3], s[k]);
-  constexpr float kScale = 0.25f * 1.4426950408889634f;  // f32(1/sqrt(16)) * log2(e)
+  for (int half = 0; half < 2; ++half) {
+    tmem_ld32(sa + 32 * half, s);
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      if (32 * half + i < NK) m4[i & 3] = fmaxf(m4[i & 3], s[i]);
+  }
   const float nms = -fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])) * kScale;
   float p4[4] = {0.0f, 0.0f, 0.0f, 0.0f};
 #pragma unroll
-  for (int k = 0; k < NK; ++k) {
-    s[k] = ex2_approx(fmaf(s[k], kScale, nms));
-    p4[k & 3] += s[k];
-  }
-  uint8_t* tp = P.smem + S_HP + P.h * 32768;
+  for (int half = 0; half < 2; ++half) {
+    tmem_ld32(sa + 32 * half, s);
+    uint32_t u[16];
 #pragma unroll
-  for (int q = 0; q < 8; ++q) {
-    if (8 * q < NK) {
-      float v[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) v[i] = (8 * q + i < NK) ? s[8 * q + i] : 0.0f;
-      st_row8(tp, P.r, 64 * blk + 8 * q, 128, v);
-    } else {
-      st_row_zero8(tp, P.r, 64 * blk + 8 * q, 128);
+    for (int i = 0; i < 16; ++i) {
+      const int k = 32 * half + 2 * i;
+      float e0 = 0.0f, e1 = 0.0f;
+      if (k < NK) {
+        e0 = ex2_approx(fmaf(s[2 * i], kScale, nms));
+        p4[(2 * i) & 3] += e0;
+      }
+      if (k + 1 < NK) {
+        e1 = ex2_approx(fmaf(s[2 * i + 1], kScale, nms));
+        p4[(2 * i + 1) & 3] += e1;
+      }
+      u[i] = active ? tc::pack_bf16(e0, e1) : 0u;
     }
-    st_row_zero8(tp, P.r, 64 * (1 - blk) + 8 * q, 128);
+    tc::tmem_st16u_nowait(P.lane_addr(tcol + 32 * blk + 16 * half), u);
   }
-  return 1.0f / ((p4[0] + p4[1]) + (p4[2] + p4[3]));
+  const uint32_t z[16] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+  tc::tmem_st16u_nowait(P.lane_addr(tcol + 32 * (1 - blk)), z);
+  tc::tmem_st16u_nowait(P.lane_addr(tcol + 32 * (1 - blk) + 16), z);
+  return active ? 1.0f / ((p4[0] + p4[1]) + (p4[2] + p4[3])) : 0.0f;
 }
 
 // softmax of head (pair + 2 h) for hand tiles: every hand's four token rows
-// [4 g, 4 g + 4) attend to the same four keys (decoder.py:393-398), so a
-// warp's 32 rows need the 32 key columns of its own lane quadrant; the
-// row's four are picked out of them.  Same arithmetic as softmax_head<4>.
+// [4 g, 4 g + 4) attend to the same four keys (decoder.py:393-398).  A warp's
+// 32 rows need the 32 key columns of its own lane quadrant; the row's four
+// are picked out of them.  Same arithmetic as the NK = 4 softmax.  P: the
+// quadrant's 32 keys packed in 16 columns, zeros elsewhere.
 __device__ float softmax_group4(Pipe& P) {
+  const uint32_t tcol = T_GEN + 128 * P.h;
+  const int q = P.r >> 5;
   float s[32];
-  tmem_ld32(P.lane_addr(T_GEN + 128 * P.h + 32 * (P.r >> 5)), s);
+  tmem_ld32(P.lane_addr(tcol + 32 * q), s);
   const int g = (P.r & 31) >> 2;
   float a[4];
 #pragma unroll
@@ -311,90 +397,81 @@ __device__ float softmax_group4(Pipe& P) {
 #pragma unroll
     for (int gg = 1; gg < 8; ++gg) a[k] = g == gg ? s[4 * gg + k] : a[k];
   }
-  constexpr float kScale = 0.25f * 1.4426950408889634f;
   const float nms = -fmaxf(fmaxf(a[0], a[1]), fmaxf(a[2], a[3])) * kScale;
   float e[4];
 #pragma unroll
   for (int k = 0; k < 4; ++k) e[k] = ex2_approx(fmaf(a[k], kScale, nms));
-  uint8_t* tp = P.smem + S_HP + P.h * 32768;
-  const int qk = P.r >> 3;               // 8-column chunk holding the group's keys
-  const bool hi = ((P.r >> 2) & 1) != 0;  // keys in its upper half
+  const uint32_t lo = tc::pack_bf16(e[0], e[1]), hi = tc::pack_bf16(e[2], e[3]);
+  uint32_t u[32];
 #pragma unroll
-  for (int q = 0; q < 16; ++q) {
-    if (q == qk) {
-      float v[8];
+  for (int i = 0; i < 16; ++i) u[i] = i == 2 * g ? lo : (i == 2 * g + 1 ? hi : 0u);
+  tc::tmem_st16u_nowait(P.lane_addr(tcol + 16 * q), u);
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        v[k] = hi ? 0.0f : e[k];
-        v[4 + k] = hi ? e[k] : 0.0f;
-      }
-      st_row8(tp, P.r, 8 * q, 128, v);
-    } else {
-      st_row_zero8(tp, P.r, 8 * q, 128);
-    }
+  for (int i = 0; i < 32; ++i) u[i] = 0u;
+  // the other 48 packed columns of [tcol, tcol + 64)
+  if (q == 0) {
+    tc::tmem_st16u_nowait(P.lane_addr(tcol + 16), u);
+    tc::tmem_st32u_nowait(P.lane_addr(tcol + 32), u);
+  } else if (q == 1) {
+    tc::tmem_st16u_nowait(P.lane_addr(tcol), u);
+    tc::tmem_st32u_nowait(P.lane_addr(tcol + 32), u);
+  } else if (q == 2) {
+    tc::tmem_st32u_nowait(P.lane_addr(tcol), u);
+    tc::tmem_st16u_nowait(P.lane_addr(tcol + 48), u);
+  } else {
+    tc::tmem_st32u_nowait(P.lane_addr(tcol), u);
+    tc::tmem_st16u_nowait(P.lane_addr(tcol + 32), u);
   }
   return 1.0f / ((e[0] + e[1]) + (e[2] + e[3]));
 }
 
-// the four heads of one attention given sQ / sK / sVt; the context is
-// written as bf16 straight into the A tile of the output projection.
-// Pair p of the two passes runs heads p (threads h = 0) and p + 2
-// (threads h = 1), so each thread ends up owning the softmax sums of the
-// two heads whose context columns [32 h, 32 h + 32) it holds.
-// One round: S = Q K^T, softmax, O (+)= P V.  Rows with active == false
-// contribute a zero P row, so several rounds over different key sets (the
-// hand tiles' cross attention) accumulate into one context; inv keeps the
-// 1 / sum of the round in which the row was active.  G4: grouped hand
-// self-attention (softmax_group4).
+// Attention of the four heads given sQ / sK / sVt, two heads at a time:
+// S pair -> softmax (P packed over S) -> P.V from TMEM -> the pair's
+// context columns, scaled by 1 / sum, as bf16 into `ctx_tile` for rows with
+// active == true.  Thread h handles head (pair + 2 h) of each pair, so it
+// ends up writing context columns [32 h, 32 h + 32) (heads 2h, 2h+1).
+// Several calls with disjoint active rows and different K / V (the hand
+// tiles' cross-attention rounds) assemble one context tile.
 template <int NK, bool G4 = false>
-__device__ void attn_round(Pipe& P, bool active, bool accumulate, float* inv) {
-  const uint32_t sq = P.sbase + S_Q, sk = P.sbase + S_K, sv = P.sbase + S_VT, sp = P.sbase + S_HP;
+__device__ void attention(Pipe& P, bool active, uint32_t ctx_tile = S_A) {
+  const uint32_t sq = P.sbase + S_Q, sk = P.sbase + S_K, sv = P.sbase + S_VT;
   const uint32_t id_s = tc::idesc_bf16(128, 128), id_o = tc::idesc_bf16(128, 16);
-  P.before_issue();
-  if (P.tid == 0)
-    for (int j = 0; j < 2; ++j)
-      tc::mma_bf16(P.tmem + T_GEN + 128 * j, tc::kmajor_desc(sq + (2 * j) * 4096, DH, 0),
-                   tc::kmajor_desc(sk + (2 * j) * 4096, DH, 0), id_s, false);
-  P.commit_wait();
 #pragma unroll 1
   for (int pair = 0; pair < 2; ++pair) {
-    const float iv = G4 ? softmax_group4(P) : softmax_head<NK>(P, active);
-    if (active) inv[pair] = iv;
     P.before_issue();
-    if (P.tid == 0) {
+    if (P.tid == 0)
+      for (int j = 0; j < 2; ++j)
+        tc::mma_bf16(P.tmem + T_GEN + 128 * j, tc::kmajor_desc(sq + (pair + 2 * j) * 4096, DH, 0),
+                     tc::kmajor_desc(sk + (pair + 2 * j) * 4096, DH, 0), id_s, false);
+    P.commit_wait();
+    float inv;
+    if constexpr (G4)
+      inv = softmax_group4(P);
+    else
+      inv = softmax_head<NK>(P, active);
+    tc::tmem_wait_st();
+    P.before_issue();
+    if (P.tid == 0)
       for (int j = 0; j < 2; ++j) {
         const int hd = pair + 2 * j;
-        for (int k = 0; k < 128; k += 16)
-          tc::mma_bf16(P.tmem + T_O + 16 * hd, tc::kmajor_desc(sp + j * 32768, 128, k),
-                       tc::kmajor_desc(sv + hd * 4096, 128, k), id_o, accumulate || k > 0);
+        for (int k = 0; k < 8; ++k)
+          tc::mma_bf16_ts(P.tmem + T_PV + 16 * j, P.tmem + T_GEN + 128 * j + 8 * k,
+                          tc::kmajor_desc(sv + hd * 4096, 128, 16 * k), id_o, k > 0);
       }
-      if (pair == 0)
-        for (int j = 0; j < 2; ++j)
-          tc::mma_bf16(P.tmem + T_GEN + 128 * j, tc::kmajor_desc(sq + (1 + 2 * j) * 4096, DH, 0),
-                       tc::kmajor_desc(sk + (1 + 2 * j) * 4096, DH, 0), id_s, false);
-    }
     P.commit_wait();
+    float o[16];
+    tc::tmem_ld16(P.lane_addr(T_PV + 16 * P.h), o);
+    if (active) {
+#pragma unroll
+      for (int i = 0; i < 16; ++i) o[i] *= inv;
+      const int hd = pair + 2 * P.h;
+      st_row8(P.smem + ctx_tile, P.r, 16 * hd, D, o);
+      st_row8(P.smem + ctx_tile, P.r, 16 * hd + 8, D, o + 8);
+    }
   }
 }
 
-// context (scaled by the deferred 1 / sum) as bf16 into the A tile
-__device__ void attn_ctx(Pipe& P, const float* inv) {
-  float ctx[HC];
-  tmem_ld32(P.lane_addr(T_O + HC * P.h), ctx);
-#pragma unroll
-  for (int c = 0; c < HC; ++c) ctx[c] *= inv[c / 16];
-#pragma unroll
-  for (int q = 0; q < HC; q += 8) st_row8(P.smem + S_A, P.r, HC * P.h + q, D, ctx + q);
-}
-
-template <int NK, bool G4 = false>
-__device__ void attn_core(Pipe& P) {
-  float inv[2];
-  attn_round<NK, G4>(P, true, false, inv);
-  attn_ctx(P, inv);
-}
-
-// x += Wo . ctx + bo for valid rows (ctx already in the A tile)
+// x += Wo . ctx + bo for valid rows (ctx in the A tile)
 __device__ void out_proj(Pipe& P, const float* bo, float* x, bool valid) {
   const uint32_t w = P.acquire();
   P.before_issue();
@@ -411,16 +488,20 @@ __device__ void out_proj(Pipe& P, const float* bo, float* x, bool valid) {
 // Sub-layers.  `prm` is the layer's TCP_* parameter block staged in shared
 // memory (LayerNorm affine and biases); the weight images come from the ring.
 
-// self attention: x += MHA(LN(x + pos))  (decoder.py:214-218)
+// self attention: x += MHA(LN(a)), a = x + pos  (decoder.py:214-218)
+// (a == nullptr: a is in the fp32 row tile, written by the caller)
 template <int NK, bool G4 = false>
-__device__ void self_attn(Pipe& P, const float* prm, float* x, const float* pos, bool valid) {
-  float a[HC];
-#pragma unroll
-  for (int c = 0; c < HC; ++c) a[c] = x[c] + pos[c];
+__device__ void self_attn(Pipe& P, const float* prm, float* x, const float* a, bool valid) {
 #ifdef FSB_PROFILE
   long long q0 = clock64();
 #endif
-  ln_half_to_tile(P, a, prm + TCP_S_LN_G, prm + TCP_S_LN_B);
+  if (a != nullptr) {
+    ln_half_to_tile(P, a, prm + TCP_S_LN_G, prm + TCP_S_LN_B);
+  } else {
+    float av[HC];
+    load_row(P, av);
+    ln_half_to_tile(P, av, prm + TCP_S_LN_G, prm + TCP_S_LN_B);
+  }
 #ifdef FSB_PROFILE
   long long q1 = clock64();
   P.prof[12] += q1 - q0;
@@ -440,14 +521,16 @@ __device__ void self_attn(Pipe& P, const float* prm, float* x, const float* pos,
   long long q3 = clock64();
   P.prof[14] += q3 - q2;
 #endif
-  attn_core<NK, G4>(P);
+  attention<NK, G4>(P, true);
 #ifdef FSB_PROFILE
   P.prof[15] += clock64() - q3;
 #endif
   out_proj(P, prm + TCP_S_BO, x, valid);
 }
 
-// cross attention: x += MHA(LN_q(x), LN_kv(f))  (decoder.py:220-227)
+// cross attention: x += MHA(LN_q(x), LN_kv(f))  (decoder.py:220-227).
+// LN_kv(f) is staged in the V^T tile (free until drain_kv refills it after
+// the K | V GEMM has read it).
 __device__ void cross_attn(Pipe& P, const float* prm, float* x, const float* frow, bool valid) {
   float f[HC];
 #pragma unroll
@@ -455,13 +538,13 @@ __device__ void cross_attn(Pipe& P, const float* prm, float* x, const float* fro
     const float4 v = __ldg(reinterpret_cast<const float4*>(frow + HC * P.h + c));
     f[c] = v.x; f[c + 1] = v.y; f[c + 2] = v.z; f[c + 3] = v.w;
   }
-  ln_half_to_tile(P, f, prm + TCP_C_LNKV_G, prm + TCP_C_LNKV_B);
+  ln_half_to_tile(P, f, prm + TCP_C_LNKV_G, prm + TCP_C_LNKV_B, S_VT);
   const uint32_t wkv = P.acquire();
   P.before_issue();
-  if (P.tid == 0) gemm(P.sbase + S_A, D, wkv, 2 * D, T_KV, P.tmem);
+  if (P.tid == 0) gemm(P.sbase + S_VT, D, wkv, 2 * D, T_GEN, P.tmem);
   P.prefetch();
   P.commit_wait();
-  drain_kv(P, T_KV, prm + TCP_C_BQKV + 64, prm + TCP_C_BQKV + 128);
+  drain_kv(P, T_GEN, prm + TCP_C_BQKV + 64, prm + TCP_C_BQKV + 128);
   ln_half_to_tile(P, x, prm + TCP_C_LNQ_G, prm + TCP_C_LNQ_B);
   const uint32_t wq = P.acquire();
   P.before_issue();
@@ -469,7 +552,7 @@ __device__ void cross_attn(Pipe& P, const float* prm, float* x, const float* fro
   P.prefetch();
   P.commit_wait();
   drain_q(P, T_GEN, prm + TCP_C_BQKV);
-  attn_core<BLK>(P);
+  attention<BLK>(P, true);
   out_proj(P, prm + TCP_C_BO, x, valid);
 }
 
@@ -491,7 +574,7 @@ __device__ void cross_attn_hands(Pipe& P, const float* prm, float* x, const Deco
   const uint32_t wkv = P.acquire();
   const int blk = P.r / BLK, rb = P.r % BLK;
   const int nr = (nslots + 1) / 2;
-  float inv[2] = {0.0f, 0.0f};
+  if (nr == 0) P.prefetch();  // an empty tile still releases t_q (the other group waits for t_o)
 #pragma unroll 1
   for (int c = 0; c < nr; ++c) {
     const int slot = 2 * c + blk;
@@ -509,19 +592,22 @@ __device__ void cross_attn_hands(Pipe& P, const float* prm, float* x, const Deco
 #pragma unroll
       for (int q = 0; q < HC; ++q) f[q] = 0.0f;
     }
-    ln_half_to_tile(P, f, prm + TCP_C_LNKV_G, prm + TCP_C_LNKV_B);
+    ln_half_to_tile(P, f, prm + TCP_C_LNKV_G, prm + TCP_C_LNKV_B, S_VT);
     P.before_issue();
-    if (P.tid == 0) gemm(P.sbase + S_A, D, wkv, 2 * D, T_KV, P.tmem);
-    if (c == 0) P.prefetch();  // t_o into the slot t_q has left
+    if (P.tid == 0) gemm(P.sbase + S_VT, D, wkv, 2 * D, T_GEN, P.tmem);
+    if (c == 0) P.prefetch();  // t_q's slot may be refilled
     P.commit_wait();
-    drain_kv(P, T_KV, prm + TCP_C_BQKV + 64, prm + TCP_C_BQKV + 128);
-    attn_round<BLK>(P, (rb >> 2) == c, c > 0, inv);
+    drain_kv(P, T_GEN, prm + TCP_C_BQKV + 64, prm + TCP_C_BQKV + 128);
+    attention<BLK>(P, (rb >> 2) == c);
   }
-  attn_ctx(P, inv);
   out_proj(P, prm + TCP_C_BO, x, valid);
 }
 
-// MLP: x += W2 relu(W1 LN(x) + b1) + b2  (decoder.py:205-212)
+// MLP: x += W2 relu(W1 LN(x) + b1) + b2  (decoder.py:205-212).  The hidden
+// layer is packed as bf16 over the first half of each 64-column chunk of the
+// W1 accumulator (this thread's own chunks: no cross-thread hazard) and the
+// second GEMM reads it from TMEM in two N = 32 halves whose outputs land in
+// the chunks' free second halves: [32, 64) and [96, 128).
 __device__ void mlp(Pipe& P, const float* prm, float* x, bool valid) {
   ln_half_to_tile(P, x, prm + TCP_M_LN_G, prm + TCP_M_LN_B);
   const uint32_t w1 = P.acquire();
@@ -529,69 +615,88 @@ __device__ void mlp(Pipe& P, const float* prm, float* x, bool valid) {
   if (P.tid == 0) gemm(P.sbase + S_A, D, w1, 4 * D, T_GEN, P.tmem);
   P.prefetch();
   P.commit_wait();
-  uint8_t* th = P.smem + S_HP;
+  // 32 fp32 columns at a time: piece p of a chunk packs into [c0 + 16 p, +16),
+  // columns this thread has already read
 #pragma unroll 1
-  for (int q = 0; q < 2; ++q) {
-    const int c0 = 128 * P.h + 64 * q;
-    float v[64];
-    tc::tmem_ld64(P.lane_addr(T_GEN + c0), v);
+  for (int q = 0; q < 4; ++q) {
+    const int c0 = 128 * P.h + 64 * (q >> 1), p = q & 1;
+    float v[32];
+    tmem_ld32(P.lane_addr(T_GEN + c0 + 32 * p), v);
+    uint32_t u[16];
 #pragma unroll
-    for (int i = 0; i < 64; ++i) v[i] = fmaxf(v[i] + prm[TCP_M_B1 + c0 + i], 0.0f);
-#pragma unroll
-    for (int i = 0; i < 64; i += 8) st_row8(th, P.r, c0 + i, 4 * D, v + i);
+    for (int i = 0; i < 16; ++i)
+      u[i] = tc::pack_bf16(fmaxf(v[2 * i] + prm[TCP_M_B1 + c0 + 32 * p + 2 * i], 0.0f),
+                           fmaxf(v[2 * i + 1] + prm[TCP_M_B1 + c0 + 32 * p + 2 * i + 1], 0.0f));
+    tc::tmem_st16u_nowait(P.lane_addr(T_GEN + c0 + 16 * p), u);
   }
+  tc::tmem_wait_st();
   const uint32_t w2 = P.acquire();
   P.before_issue();
-  if (P.tid == 0) gemm(P.sbase + S_HP, 4 * D, w2, D, T_GEN, P.tmem);
+  if (P.tid == 0) {
+    const uint32_t id = tc::idesc_bf16(128, 32);
+    for (int nh = 0; nh < 2; ++nh)
+      for (int s = 0; s < 16; ++s)
+        tc::mma_bf16_ts(P.tmem + T_GEN + 32 + 64 * nh, P.tmem + T_GEN + 64 * (s >> 2) + 8 * (s & 3),
+                        tc::kmajor_desc(w2 + 16384u * nh, 4 * D, 16 * s), id, s > 0);
+  }
   P.prefetch();
   P.commit_wait();
   float v[HC];
-  tmem_ld32(P.lane_addr(T_GEN + HC * P.h), v);
+  tmem_ld32(P.lane_addr(T_GEN + 32 + 64 * P.h), v);
   if (valid)
 #pragma unroll
     for (int c = 0; c < HC; ++c) x[c] += v[c] + prm[TCP_M_B2 + HC * P.h + c];
 }
 
+// CTA setup: tables are filled by thread 0 before this is called
 __device__ void setup(Pipe& P, Shared& sh, uint8_t* smem) {
   P.sh = &sh;
-  P.smem = smem;
-  P.sbase = tc::smem_u32(smem);
-  P.tid = threadIdx.x;
-  P.r = threadIdx.x & (ROWS - 1);
-  P.h = threadIdx.x / ROWS;
+  P.sall = smem;
+  P.g = threadIdx.x / GT;
+  P.smem = smem + P.g * S_GROUP;
+  P.sbase = tc::smem_u32(P.smem);
+  P.wbase = tc::smem_u32(smem + S_W);
+  P.tid = threadIdx.x % GT;
+  P.r = P.tid & (ROWS - 1);
+  P.h = P.tid / ROWS;
   P.mphase = 0;
-  P.wload = 0;
   P.wuse = 0;
   P.xc = 0;
-  P.pload = 0;
   P.puse = 0;
 #ifdef FSB_PROFILE
   for (int i = 0; i < 16; ++i) P.prof[i] = 0;
   P.prof[0] = -clock64();
 #endif
-  if (P.tid == 0) {
-    tc::mbar_init(&sh.wbar[0], 1);
-    tc::mbar_init(&sh.wbar[1], 1);
-    tc::mbar_init(&sh.pbar[0], 1);
-    tc::mbar_init(&sh.pbar[1], 1);
-    tc::mbar_init(&sh.mbar, 1);
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&sh.wbar[i], 1);
+      tc::mbar_init(&sh.pbar[i], 1);
+      sh.wrel[i] = 0;
+      sh.prel[i] = 0;
+    }
+    for (int i = 0; i < NG; ++i) tc::mbar_init(&sh.mbar[i], 1);
     tc::mbar_fence_init();
   }
-  if (P.tid < 32) tc::tmem_alloc(&sh.tmem, 512);
+  if (threadIdx.x < 32) tc::tmem_alloc(&sh.tmem, 512);
   tc::fence_before();
   __syncthreads();
   tc::fence_after();
-  P.tmem = sh.tmem;
-  P.prefetch();
+  P.tmem = sh.tmem + 256u * (uint32_t)P.g;
+  if (threadIdx.x == 0) {
+    P.load_image(0);
+    P.load_image(1);
+    P.load_prm(0);
+    P.load_prm(1);
+  }
 }
 
 __device__ void teardown(Pipe& P, int role) {
   tc::fence_before();
   __syncthreads();
-  if (P.tid < 32) tc::tmem_dealloc(P.tmem, 512);
+  if (threadIdx.x < 32) tc::tmem_dealloc(P.sh->tmem, 512);
 #ifdef FSB_PROFILE
   P.prof[0] += clock64();
-  if ((P.tid == 0 || P.tid == NTH - 1) && blockIdx.x == 0)
+  if (P.g == 0 && (P.tid == 0 || P.tid == GT - 1) && blockIdx.x == 0)
     for (int i = 0; i < 16; ++i) g_tc_prof[role][P.tid ? 1 : 0][i] = (unsigned long long)P.prof[i];
 #else
   (void)role;
@@ -601,14 +706,14 @@ __device__ void teardown(Pipe& P, int role) {
 }  // namespace
 
 // ===========================================================================
-// encoder: grid = ceil(ncrops / 2); block f of CTA b encodes crop 2b + f
+// encoder: grid = ceil(ncrops / 4); group g, block f of CTA b encodes crop
+// 4b + 2g + f
 // ===========================================================================
 __global__ void __launch_bounds__(NTH, 1) k_encoder_tc(const float* __restrict__ crops, int ncrops, EncW w,
                                                        float* __restrict__ feats, int* nonfinite) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ Shared sh;
-  const int t = threadIdx.x;
-  if (t == 0) {
+  if (threadIdx.x == 0) {
     int n = 0;
     sh.wptr[n] = w.t_patch;
     sh.wbytes[n++] = 192 * D * 2;
@@ -619,19 +724,21 @@ __global__ void __launch_bounds__(NTH, 1) k_encoder_tc(const float* __restrict__
       sh.wptr[n] = w.mlp[l].t_w2;   sh.wbytes[n++] = 4 * D * D * 2;
     }
     sh.nw = n;
+    for (int l = 0; l < w.layers; ++l) sh.pptr[l] = w.tc_params[l];
+    sh.nprm = w.layers;
   }
   __syncthreads();
   Pipe P;
   setup(P, sh, smem);
-  if (w.layers > 0) P.pprefetch(w.tc_params[0]);
   const int blk = P.r / BLK, p = P.r % BLK;
-  const int crop = 2 * blockIdx.x + blk;
+  const int crop = 4 * blockIdx.x + 2 * P.g + blk;
   const bool valid = crop < ncrops;
 
   // patchify (decoder.py:247-248): this thread packs image rows iy in
-  // [4h, 4h + 4) of patch p into the K = 192 tile (k = iy*24 + ix*3 + c)
+  // [4h, 4h + 4) of patch p into the K = 192 tile (k = iy*24 + ix*3 + c),
+  // which spans this group's A, Q and K tiles
   {
-    uint8_t* tile = smem + S_HP;
+    uint8_t* tile = P.smem + S_A;
     const int py = p / 8, px = p % 8;
     const float* src = crops + (int64_t)(valid ? crop : 0) * 64 * 64 * 3;
 #pragma unroll 1
@@ -650,7 +757,7 @@ __global__ void __launch_bounds__(NTH, 1) k_encoder_tc(const float* __restrict__
   {
     const uint32_t wp = P.acquire();
     P.before_issue();
-    if (t == 0) gemm(P.sbase + S_HP, 192, wp, D, T_GEN, P.tmem);
+    if (P.tid == 0) gemm(P.sbase + S_A, 192, wp, D, T_GEN, P.tmem);
     P.prefetch();
     P.commit_wait();
     float v[HC];
@@ -661,14 +768,11 @@ __global__ void __launch_bounds__(NTH, 1) k_encoder_tc(const float* __restrict__
       x[i] = valid ? (v[i] + __ldg(w.patch_b + c)) + __ldg(w.pos + p * D + c) : 0.0f;
     }
   }
-  float zero[HC];
-#pragma unroll
-  for (int c = 0; c < HC; ++c) zero[c] = 0.0f;
   for (int l = 0; l < w.layers; ++l) {
     const float* prm = P.pacquire();
-    __syncthreads();  // every thread is past layer l - 1: its slot may be refilled
-    if (l + 1 < w.layers) P.pprefetch(w.tc_params[l + 1]);
-    self_attn<BLK>(P, prm, x, zero, valid);
+    P.sync();  // every thread of the group is past layer l - 1
+    P.prelease();
+    self_attn<BLK>(P, prm, x, x, valid);
     mlp(P, prm, x, valid);
   }
   float y[HC];
@@ -687,10 +791,10 @@ __global__ void __launch_bounds__(NTH, 1) k_encoder_tc(const float* __restrict__
 }
 
 // ===========================================================================
-// decoders: CTAs [0, nb) decode two frames' bodies, CTAs [nb, nb + nh) two
-// hands each.
+// decoders: CTAs [0, nbc) hold two body tiles (four frames), CTAs
+// [nbc, nbc + nhc) two hand tiles (2 kHandsPerCta hands).
 // ===========================================================================
-struct BodyAux {  // fp32 scratch per block
+struct BodyAux {  // fp32 scratch per body tile
   float t0[2][D];
   float params[2][80];
   float cam[2][4];
@@ -706,25 +810,31 @@ struct BodyAux {  // fp32 scratch per block
 #ifndef FSB_HANDS_PER_CTA
 #define FSB_HANDS_PER_CTA 8
 #endif
-constexpr int kHandsPerCta = FSB_HANDS_PER_CTA;
-static_assert(kHandsPerCta >= 2 && kHandsPerCta <= 32 && kHandsPerCta % 2 == 0, "hand slots per tile");
+constexpr int kHandsPerCta = FSB_HANDS_PER_CTA;  // per tile
+static_assert(kHandsPerCta >= 2 && kHandsPerCta <= 16 && kHandsPerCta % 2 == 0, "hand slots per tile");
 struct HandAux {
   float t0[kHandsPerCta][D];
   float rc[kHandsPerCta][8];   // rots[3], cams[3]
   float pts[kHandsPerCta][6];  // 3 x (x, y) projected canonical points
   int pred;
 };
-static_assert(sizeof(BodyAux) <= 16384 && sizeof(HandAux) <= 16384, "aux scratch");
+static_assert(sizeof(BodyAux) <= AUX_BYTES && sizeof(HandAux) <= AUX_BYTES, "aux scratch");
 
 // LN(token 0) -> head params / camera of both blocks (decoder.py:264-272)
+// (x == nullptr: the residual stream is in the fp32 row tile)
 __device__ void body_heads(Pipe& P, BodyAux& ax, const BodyW& w, const float* x) {
   float y[HC];
-  ln_half(P, x, w.norm_g, w.norm_b, y);
+  if (x != nullptr) {
+    ln_half(P, x, w.norm_g, w.norm_b, y);
+  } else {
+    load_row(P, y);
+    ln_half(P, y, w.norm_g, w.norm_b, y);
+  }
   const int blk = P.r / BLK;
   if (P.r % BLK == 0)
 #pragma unroll
     for (int c = 0; c < HC; ++c) ax.t0[blk][HC * P.h + c] = y[c];
-  __syncthreads();
+  P.sync();
   {
     const int b = P.tid / 128, o = P.tid % 128;  // one head output per thread
     if (o < 79) {
@@ -741,18 +851,23 @@ __device__ void body_heads(Pipe& P, BodyAux& ax, const BodyW& w, const float* x)
         ax.cam[b][oo] = v + __ldg(w.head_cam_b + oo);
     }
   }
-  __syncthreads();
+  P.sync();
 }
 
 // LN(token 0) -> hand rotation / camera of every slot (decoder.py:384-391)
 __device__ void hand_heads(Pipe& P, HandAux& ax, const HandW& w, const float* x) {
   float y[HC];
-  ln_half(P, x, w.norm_g, w.norm_b, y);
+  if (x != nullptr) {
+    ln_half(P, x, w.norm_g, w.norm_b, y);
+  } else {
+    load_row(P, y);
+    ln_half(P, y, w.norm_g, w.norm_b, y);
+  }
   const int slot = 2 * ((P.r % BLK) >> 2) + P.r / BLK;
   if ((P.r & 3) == 0 && slot < kHandsPerCta)
 #pragma unroll
     for (int c = 0; c < HC; ++c) ax.t0[slot][HC * P.h + c] = y[c];
-  __syncthreads();
+  P.sync();
   if (P.tid < 6 * kHandsPerCta) {
     const int b = P.tid / 6, o = P.tid % 6;
     const float* W = o < 3 ? w.head_rot_w : w.head_cam_w;
@@ -761,17 +876,17 @@ __device__ void hand_heads(Pipe& P, HandAux& ax, const HandW& w, const float* x)
     for (int k = 0; k < D; ++k) acc[k & 3] = fmaf(ax.t0[b][k], __ldg(W + k * 3 + o % 3), acc[k & 3]);
     ax.rc[b][o] = (acc[0] + acc[1]) + (acc[2] + acc[3]) + __ldg((o < 3 ? w.head_rot_b : w.head_cam_b) + o % 3);
   }
-  __syncthreads();
+  P.sync();
 }
 
 __global__ void __launch_bounds__(NTH, 1) k_decoders_tc(DecodeArgs a, BodyW bw, HandW hw) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ Shared sh;
-  const int t = threadIdx.x;
-  const int nbc = (a.nbody + 1) / 2;
+  const int nbt = (a.nbody + 1) / 2;                          // body tiles
+  const int nbc = (nbt + NG - 1) / NG;                        // body CTAs
   const bool body = (int)blockIdx.x < nbc;
   const int layers = body ? bw.layers : hw.layers;
-  if (t == 0) {
+  if (threadIdx.x == 0) {
     int n = 0;
     for (int l = 0; l < layers; ++l) {
       const AttnW& s = body ? bw.self[l] : hw.self[l];
@@ -789,34 +904,38 @@ __global__ void __launch_bounds__(NTH, 1) k_decoders_tc(DecodeArgs a, BodyW bw, 
       sh.wptr[n] = c.t_o;   sh.wbytes[n++] = D * D * 2;
       sh.wptr[n] = m.t_w1;  sh.wbytes[n++] = 4 * D * D * 2;
       sh.wptr[n] = m.t_w2;  sh.wbytes[n++] = 4 * D * D * 2;
+      sh.pptr[l] = body ? bw.tc_params[l] : hw.tc_params[l];
     }
     sh.nw = n;
+    sh.nprm = layers;
   }
   __syncthreads();
   Pipe P;
   setup(P, sh, smem);
-  if (layers > 0) P.pprefetch(body ? bw.tc_params[0] : hw.tc_params[0]);
+  const int t = P.tid;
   const int r = P.r, blk = r / BLK, c0 = HC * P.h;
-  // body: frame 2 x + blk, token rb; hand: slot hs = 2 (r % 64 / 4) + blk, token rb
-  const int hand0 = kHandsPerCta * ((int)blockIdx.x - nbc);
-  const int nslots = body ? 0 : min(kHandsPerCta, a.nhand - hand0);
+  const int tile = NG * (body ? (int)blockIdx.x : (int)blockIdx.x - nbc) + P.g;
+  // body: frame 2 tile + blk, token rb; hand: slot hs = 2 (r % 64 / 4) + blk, token rb
+  const int hand0 = kHandsPerCta * tile;
+  const int nslots = body ? 0 : max(0, min(kHandsPerCta, a.nhand - hand0));
   const int hs = 2 * ((r % BLK) >> 2) + blk;
   const int rb = body ? r % BLK : (r & 3);
-  const bool valid = body ? (2 * (int)blockIdx.x + blk < a.nbody && rb < 51) : hs < nslots;
-  const int unit = body ? 2 * blockIdx.x + blk : 0;  // frame index (body tiles)
+  const int unit = body ? 2 * tile + blk : 0;  // frame index (body tiles)
+  const bool valid = body ? (unit < a.nbody && rb < 51) : hs < nslots;
+  const int fb0 = 2 * tile;                    // first frame of a body tile
 
   // feature row of this thread for the body's cross attention
   const int crop = (body && unit < a.nbody ? unit : 0) * a.body_feat_stride;
   const float* frow = a.feats + ((int64_t)crop * 64 + (r % BLK)) * D;
 
-  float x[HC], pos[HC];
-  BodyAux& bx = *reinterpret_cast<BodyAux*>(smem + S_AUX);
-  HandAux& hx = *reinterpret_cast<HandAux*>(smem + S_AUX);
+  float x[HC];
+  BodyAux& bx = *reinterpret_cast<BodyAux*>(smem + S_AUX + P.g * AUX_BYTES);
+  HandAux& hx = *reinterpret_cast<HandAux*>(smem + S_AUX + P.g * AUX_BYTES);
   if (body) {
     // tokens = token_init, rows 1..4 += prompt_box(prompt)  (decoder.py:287-293)
     for (int i = 0; i < 2; ++i) {
       const int idx = 2 * t + i, b = idx / (4 * D), o = idx % (4 * D);
-      const int u = 2 * blockIdx.x + b;
+      const int u = fb0 + b;
       float acc = 0.0f;
       if (u < a.nbody) {
 #pragma unroll
@@ -825,7 +944,7 @@ __global__ void __launch_bounds__(NTH, 1) k_decoders_tc(DecodeArgs a, BodyW bw, 
       bx.boxtok[b][o] = acc + __ldg(bw.prompt_box_b + o);
     }
     if (t < 2) bx.pred[t] = 0;
-    __syncthreads();
+    P.sync();
 #pragma unroll
     for (int c = 0; c < HC; ++c) {
       float v = valid ? __ldg(bw.token_init + rb * D + c0 + c) : 0.0f;
@@ -837,7 +956,7 @@ __global__ void __launch_bounds__(NTH, 1) k_decoders_tc(DecodeArgs a, BodyW bw, 
     for (int c = 0; c < HC; ++c) x[c] = valid ? __ldg(hw.token_init + rb * D + c0 + c) : 0.0f;
     if (t == 0) hx.pred = 0;
   }
-  __syncthreads();
+  P.sync();
 
 #ifdef FSB_PROFILE
   P.prof[8] += clock64() + P.prof[0];  // setup: kernel start (prof[0] = -start) -> layer loop
@@ -847,14 +966,13 @@ __global__ void __launch_bounds__(NTH, 1) k_decoders_tc(DecodeArgs a, BodyW bw, 
 #ifdef FSB_PROFILE
     tpos = clock64();
 #endif
-    // positional terms of the self-attention input (decoder.py:300-303,
-    // :397-398).  They change only when a prediction has been made, so they
-    // are kept in registers and recomputed at layer 0 and after each
-    // selected layer, with 16-byte loads of this thread's 32 columns.
-    const unsigned psel = body ? a.body_sel : a.hand_sel;
-    if (l == 0 || ((psel >> (l - 1)) & 1u)) {
+    // a = x + positional term of the self-attention input (decoder.py:
+    // 300-303, :397-398), recomputed every layer from the small tables
+    // (16-byte loads of this thread's 32 columns)
+    {
+      float av[HC];
 #pragma unroll
-      for (int i = 0; i < HC; ++i) pos[i] = 0.0f;
+      for (int i = 0; i < HC; ++i) av[i] = x[i];
       int j = -1, kind = 0;  // kind 1: 2-D keypoint row, 2: 3-D joint row
       if (valid) {
         if (body) {
@@ -871,7 +989,7 @@ __global__ void __launch_bounds__(NTH, 1) k_decoders_tc(DecodeArgs a, BodyW bw, 
 #pragma unroll
         for (int q = 0; q < HC / 4; ++q) {
           const float4 v = __ldg(src + q);
-          pos[4 * q] = v.x; pos[4 * q + 1] = v.y; pos[4 * q + 2] = v.z; pos[4 * q + 3] = v.w;
+          av[4 * q] += v.x; av[4 * q + 1] += v.y; av[4 * q + 2] += v.z; av[4 * q + 3] += v.w;
         }
       } else if (kind == 1) {
         const float* w = body ? bw.phi2d_w : hw.phi2d_w;
@@ -883,10 +1001,10 @@ __global__ void __launch_bounds__(NTH, 1) k_decoders_tc(DecodeArgs a, BodyW bw, 
           const float4 w0 = __ldg(reinterpret_cast<const float4*>(w + c0) + q);
           const float4 w1 = __ldg(reinterpret_cast<const float4*>(w + D + c0) + q);
           const float4 b4 = __ldg(reinterpret_cast<const float4*>(bb + c0) + q);
-          pos[4 * q] = fmaf(k1, w1.x, k0 * w0.x) + b4.x;
-          pos[4 * q + 1] = fmaf(k1, w1.y, k0 * w0.y) + b4.y;
-          pos[4 * q + 2] = fmaf(k1, w1.z, k0 * w0.z) + b4.z;
-          pos[4 * q + 3] = fmaf(k1, w1.w, k0 * w0.w) + b4.w;
+          av[4 * q] += fmaf(k1, w1.x, k0 * w0.x) + b4.x;
+          av[4 * q + 1] += fmaf(k1, w1.y, k0 * w0.y) + b4.y;
+          av[4 * q + 2] += fmaf(k1, w1.z, k0 * w0.z) + b4.z;
+          av[4 * q + 3] += fmaf(k1, w1.w, k0 * w0.w) + b4.w;
         }
       } else if (kind == 2) {
         const float g0 = bx.jc[blk][3 * j], g1 = bx.jc[blk][3 * j + 1], g2 = bx.jc[blk][3 * j + 2];
@@ -896,24 +1014,25 @@ __global__ void __launch_bounds__(NTH, 1) k_decoders_tc(DecodeArgs a, BodyW bw, 
           const float4 w1 = __ldg(reinterpret_cast<const float4*>(bw.phi3d_w + D + c0) + q);
           const float4 w2 = __ldg(reinterpret_cast<const float4*>(bw.phi3d_w + 2 * D + c0) + q);
           const float4 b4 = __ldg(reinterpret_cast<const float4*>(bw.phi3d_b + c0) + q);
-          pos[4 * q] = fmaf(g2, w2.x, fmaf(g1, w1.x, g0 * w0.x)) + b4.x;
-          pos[4 * q + 1] = fmaf(g2, w2.y, fmaf(g1, w1.y, g0 * w0.y)) + b4.y;
-          pos[4 * q + 2] = fmaf(g2, w2.z, fmaf(g1, w1.z, g0 * w0.z)) + b4.z;
-          pos[4 * q + 3] = fmaf(g2, w2.w, fmaf(g1, w1.w, g0 * w0.w)) + b4.w;
+          av[4 * q] += fmaf(g2, w2.x, fmaf(g1, w1.x, g0 * w0.x)) + b4.x;
+          av[4 * q + 1] += fmaf(g2, w2.y, fmaf(g1, w1.y, g0 * w0.y)) + b4.y;
+          av[4 * q + 2] += fmaf(g2, w2.z, fmaf(g1, w1.z, g0 * w0.z)) + b4.z;
+          av[4 * q + 3] += fmaf(g2, w2.w, fmaf(g1, w1.w, g0 * w0.w)) + b4.w;
         }
       }
+      save_row(P, av);  // S_Q is free: the previous layer's attention is done
     }
     const float* prm = P.pacquire();
-    __syncthreads();  // every thread is past layer l - 1: its slot may be refilled
-    if (l + 1 < layers) P.pprefetch(body ? bw.tc_params[l + 1] : hw.tc_params[l + 1]);
+    P.sync();  // every thread of the group is past layer l - 1
+    P.prelease();
 #ifdef FSB_PROFILE
     long long ts0 = clock64();
     P.prof[9] += ts0 - tpos;
 #endif
     if (body)
-      self_attn<51>(P, prm, x, pos, valid);
+      self_attn<51>(P, prm, x, nullptr, valid);
     else
-      self_attn<4, true>(P, prm, x, pos, valid);
+      self_attn<4, true>(P, prm, x, nullptr, valid);
 #ifdef FSB_PROFILE
     long long ts1 = clock64();
     P.prof[5] += ts1 - ts0;
@@ -933,15 +1052,16 @@ __global__ void __launch_bounds__(NTH, 1) k_decoders_tc(DecodeArgs a, BodyW bw, 
 #endif
     const unsigned sel = body ? a.body_sel : a.hand_sel;
     if ((sel >> l) & 1u) {
+      save_row(P, x);  // the residual stream waits in shared memory across heads / FK
       if (body) {
         // intermediate prediction: heads -> FK -> kp2d / centred joints
-        body_heads(P, bx, bw, x);
+        body_heads(P, bx, bw, nullptr);
 #ifdef FSB_PROFILE
         long long th = clock64();
         P.prof[10] += th - ts3;
 #endif
         if (t < 64) fk_warp<true>(bx.params[t / 32], bw.joints_rest, bx.fk[t / 32], t % 32);
-        __syncthreads();
+        P.sync();
 #ifdef FSB_PROFILE
         P.prof[11] += clock64() - th;
 #endif
@@ -952,9 +1072,9 @@ __global__ void __launch_bounds__(NTH, 1) k_decoders_tc(DecodeArgs a, BodyW bw, 
           for (int c = 0; c < 3; ++c) bx.jc[b][3 * j + c] = bx.fk[b].tw[j][c] - bx.fk[b].tw[0][c];
         }
         if (t < 2) bx.pred[t] = 1;
-        __syncthreads();
+        P.sync();
         if (a.inter != nullptr && t < 2 * 123) {
-          const int b = t / 123, i = t % 123, u = 2 * blockIdx.x + b;
+          const int b = t / 123, i = t % 123, u = fb0 + b;
           if (u < a.nbody) {
             float* dst = a.inter + ((int64_t)u * layers + l) * (FSB_PARAM_DIM + 3 + 44);
             dst[i] = i < FSB_PARAM_DIM ? bx.params[b][i]
@@ -964,7 +1084,7 @@ __global__ void __launch_bounds__(NTH, 1) k_decoders_tc(DecodeArgs a, BodyW bw, 
         }
       } else {
         // canonical points through the predicted rotation (decoder.py:399-409)
-        hand_heads(P, hx, hw, x);
+        hand_heads(P, hx, hw, nullptr);
         if (t < kHandsPerCta) {
           const float* rc = hx.rc[t];
           float R[9];
@@ -979,8 +1099,9 @@ __global__ void __launch_bounds__(NTH, 1) k_decoders_tc(DecodeArgs a, BodyW bw, 
           }
         }
         if (t == 0) hx.pred = 1;
-        __syncthreads();
+        P.sync();
       }
+      load_row(P, x);
     }
   }
 #ifdef FSB_PROFILE
@@ -990,7 +1111,7 @@ __global__ void __launch_bounds__(NTH, 1) k_decoders_tc(DecodeArgs a, BodyW bw, 
   if (body) {
     body_heads(P, bx, bw, x);
     if (t < 2 * FSB_PARAM_DIM) {
-      const int b = t / FSB_PARAM_DIM, o = t % FSB_PARAM_DIM, u = 2 * blockIdx.x + b;
+      const int b = t / FSB_PARAM_DIM, o = t % FSB_PARAM_DIM, u = fb0 + b;
       if (u < a.nbody) {
         const float v = bx.params[b][o];
         flag_nonfinite(a.nonfinite, v);
@@ -1037,12 +1158,13 @@ cudaError_t init_attrs_transformer_tc() {
 cudaError_t launch_encoder_tc(const float* crops, int ncrops, const EncW& w, float* feats, int* nonfinite,
                               cudaStream_t st) {
   if (ncrops == 0) return cudaSuccess;
-  k_encoder_tc<<<(ncrops + 1) / 2, NTH, SMEM_TC, st>>>(crops, ncrops, w, feats, nonfinite);
+  k_encoder_tc<<<(ncrops + 2 * NG - 1) / (2 * NG), NTH, SMEM_TC, st>>>(crops, ncrops, w, feats, nonfinite);
   return cudaGetLastError();
 }
 
 cudaError_t launch_decoders_tc(const DecodeArgs& a, const BodyW& bw, const HandW& hw, cudaStream_t st) {
-  const int n = (a.nbody + 1) / 2 + (a.nhand + kHandsPerCta - 1) / kHandsPerCta;
+  const int nbt = (a.nbody + 1) / 2, nht = (a.nhand + kHandsPerCta - 1) / kHandsPerCta;
+  const int n = (nbt + NG - 1) / NG + (nht + NG - 1) / NG;
   if (n == 0) return cudaSuccess;
   k_decoders_tc<<<n, NTH, SMEM_TC, st>>>(a, bw, hw);
   return cudaGetLastError();
