@@ -298,8 +298,8 @@ __device__ void drain_q(Pipe& P, uint32_t qcol, const float* bq) {
   }
 }
 
-// key | value columns [kcol, +128) + bias -> key tiles and transposed values
-__device__ void drain_kv(Pipe& P, uint32_t kcol, const float* bk, const float* bv) {
+// key columns [kcol, +64) + bias -> key tiles (heads 2h, 2h+1)
+__device__ void drain_k(Pipe& P, uint32_t kcol, const float* bk) {
   float v[HC];
   tmem_ld32(P.lane_addr(kcol + HC * P.h), v);
 #pragma unroll
@@ -311,19 +311,36 @@ __device__ void drain_kv(Pipe& P, uint32_t kcol, const float* bk, const float* b
     st_row8(tk, P.r, 0, DH, v + 16 * j);
     st_row8(tk, P.r, 8, DH, v + 16 * j + 8);
   }
-  tmem_ld32(P.lane_addr(kcol + 64 + HC * P.h), v);
-  // V^T tile per head (16 x 128): row d, column = this row's key index
-  const uint32_t col_off = (uint32_t)(P.r >> 3) * 128u + (uint32_t)(P.r & 7) * 2u;
+}
+
+// Values arrive transposed: the K | V GEMM is also issued with the weight
+// image as the A operand and the token tile as B, so TMEM lanes 64..127 hold
+// V^T (lane 64 + d = value dim d, columns = keys).  The threads of lane
+// quadrants 2 and 3 write the per-head V^T tiles (16 x 128, K-major along
+// keys) with 16-byte stores; thread h takes keys [64 h, 64 h + 64).
+__device__ void drain_vt(Pipe& P, uint32_t vtcol, const float* bv) {
+  if (P.r < 64) return;  // warp-uniform: lane quadrants 0, 1 hold K^T
+  const int d = P.r - 64, hd = d >> 4;
+  const float b = bv[d];
+  uint8_t* tv = P.smem + S_VT + hd * 4096;
+#pragma unroll 1
+  for (int c = 0; c < 2; ++c) {
+    const int k0 = 64 * P.h + 32 * c;
+    float v[32];
+    tmem_ld32(P.lane_addr(vtcol + k0), v);
 #pragma unroll
-  for (int j = 0; j < 2; ++j) {
-    const int hd = 2 * P.h + j;
-    uint8_t* tv = P.smem + S_VT + hd * 4096 + col_off;
+    for (int i = 0; i < 32; ++i) v[i] += b;
 #pragma unroll
-    for (int d = 0; d < DH; ++d) {
-      const __nv_bfloat16 hv = __float2bfloat16_rn(v[16 * j + d] + bv[16 * hd + d]);
-      *reinterpret_cast<__nv_bfloat16*>(tv + (d >> 3) * 2048 + (d & 7) * 16) = hv;
-    }
+    for (int q = 0; q < 32; q += 8) st_row8(tv, d & 15, k0 + q, 128, v + q);
   }
+}
+
+// V^T[m][key] = sum_k W[row0 + m][k] tok[key][k] for m < 128: the weight
+// image rows [row0, row0 + 128) as A, the 128 x 64 token tile as B
+__device__ __forceinline__ void gemm_t(uint32_t w, int row0, uint32_t tok, uint32_t dcol, uint32_t tmem) {
+  const uint32_t id = tc::idesc_bf16(128, 128);
+  const uint32_t a = w + (uint32_t)(row0 / 8) * (D * 16);
+  for (int k = 0; k < D; k += 16) tc::mma_bf16(tmem + dcol, tc::kmajor_desc(a, D, k), tc::kmajor_desc(tok, D, k), id, k > 0);
 }
 
 constexpr float kScale = 0.25f * 1.4426950408889634f;  // f32(1/sqrt(16)) * log2(e)
@@ -508,7 +525,10 @@ __device__ void self_attn(Pipe& P, const float* prm, float* x, const float* a, b
 #endif
   const uint32_t wq = P.acquire();
   P.before_issue();
-  if (P.tid == 0) gemm(P.sbase + S_A, D, wq, 3 * D, T_GEN, P.tmem);
+  if (P.tid == 0) {
+    gemm(P.sbase + S_A, D, wq, 2 * D, T_GEN, P.tmem);  // Q | K
+    gemm_t(wq, D, P.sbase + S_A, T_GEN + 128, P.tmem);  // (K | V)^T: V^T in lanes 64..127
+  }
   P.prefetch();
   P.commit_wait();
 #ifdef FSB_PROFILE
@@ -516,7 +536,8 @@ __device__ void self_attn(Pipe& P, const float* prm, float* x, const float* a, b
   P.prof[13] += q2 - q1;
 #endif
   drain_q(P, T_GEN, prm + TCP_S_BQKV);
-  drain_kv(P, T_GEN + 64, prm + TCP_S_BQKV + 64, prm + TCP_S_BQKV + 128);
+  drain_k(P, T_GEN + 64, prm + TCP_S_BQKV + 64);
+  drain_vt(P, T_GEN + 128, prm + TCP_S_BQKV + 128);
 #ifdef FSB_PROFILE
   long long q3 = clock64();
   P.prof[14] += q3 - q2;
@@ -541,10 +562,14 @@ __device__ void cross_attn(Pipe& P, const float* prm, float* x, const float* fro
   ln_half_to_tile(P, f, prm + TCP_C_LNKV_G, prm + TCP_C_LNKV_B, S_VT);
   const uint32_t wkv = P.acquire();
   P.before_issue();
-  if (P.tid == 0) gemm(P.sbase + S_VT, D, wkv, 2 * D, T_GEN, P.tmem);
+  if (P.tid == 0) {
+    gemm(P.sbase + S_VT, D, wkv, D, T_GEN, P.tmem);        // K
+    gemm_t(wkv, 0, P.sbase + S_VT, T_GEN + 128, P.tmem);  // (K | V)^T
+  }
   P.prefetch();
   P.commit_wait();
-  drain_kv(P, T_GEN, prm + TCP_C_BQKV + 64, prm + TCP_C_BQKV + 128);
+  drain_k(P, T_GEN, prm + TCP_C_BQKV + 64);
+  drain_vt(P, T_GEN + 128, prm + TCP_C_BQKV + 128);
   ln_half_to_tile(P, x, prm + TCP_C_LNQ_G, prm + TCP_C_LNQ_B);
   const uint32_t wq = P.acquire();
   P.before_issue();
@@ -594,10 +619,14 @@ __device__ void cross_attn_hands(Pipe& P, const float* prm, float* x, const Deco
     }
     ln_half_to_tile(P, f, prm + TCP_C_LNKV_G, prm + TCP_C_LNKV_B, S_VT);
     P.before_issue();
-    if (P.tid == 0) gemm(P.sbase + S_VT, D, wkv, 2 * D, T_GEN, P.tmem);
+    if (P.tid == 0) {
+      gemm(P.sbase + S_VT, D, wkv, D, T_GEN, P.tmem);
+      gemm_t(wkv, 0, P.sbase + S_VT, T_GEN + 128, P.tmem);
+    }
     if (c == 0) P.prefetch();  // t_q's slot may be refilled
     P.commit_wait();
-    drain_kv(P, T_GEN, prm + TCP_C_BQKV + 64, prm + TCP_C_BQKV + 128);
+    drain_k(P, T_GEN, prm + TCP_C_BQKV + 64);
+    drain_vt(P, T_GEN + 128, prm + TCP_C_BQKV + 128);
     attention<BLK>(P, (rb >> 2) == c);
   }
   out_proj(P, prm + TCP_C_BO, x, valid);
@@ -744,11 +773,14 @@ __global__ void __launch_bounds__(NTH, 1) k_encoder_tc(const float* __restrict__
 #pragma unroll 1
     for (int iy = 4 * P.h; iy < 4 * P.h + 4; ++iy) {
       const float* row = src + ((py * 8 + iy) * 64 + px * 8) * 3;
+      float4 f4[6];
+#pragma unroll
+      for (int q = 0; q < 6; ++q)
+        f4[q] = valid ? __ldg(reinterpret_cast<const float4*>(row) + q) : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
 #pragma unroll
       for (int q = 0; q < 3; ++q) {
-        float v[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) v[i] = valid ? __ldg(row + 8 * q + i) : 0.0f;
+        const float v[8] = {f4[2 * q].x, f4[2 * q].y, f4[2 * q].z, f4[2 * q].w,
+                            f4[2 * q + 1].x, f4[2 * q + 1].y, f4[2 * q + 1].z, f4[2 * q + 1].w};
         st_row8(tile, P.r, iy * 24 + 8 * q, 192, v);
       }
     }
