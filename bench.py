@@ -764,38 +764,42 @@ def verify_streams(torch, pipes, outs_s, images, kps, cfg, B, steps, nslot, S):
     return bool(ok)
 
 
+E2E_STREAMS = int(os.environ.get("FSB_E2E_STREAMS", "6"))
+
+
 def end_to_end(torch, pipes, images, kps, cfg, B, steps, warmup, dist, world):
     """Pipeline.run_batch on frames that live in pinned host memory (the
     reference's images are host float32 arrays).  K1 reads each frame in
     place over PCIe -- only the crop footprints (the rows and x-spans the
     three crops tap) cross the bus -- so there is no separate whole-frame
-    H2D copy; steps alternate between two streams so one batch's gather
-    overlaps the previous batch's compute.  Every step ends with a D2H read
+    H2D copy; steps rotate over E2E_STREAMS streams so one batch's gather
+    overlaps the others' compute.  Every step ends with a D2H read
     of merged/theta/j_smpl into pinned host buffers.  h2d_bytes_per_step is
     counted on the device by K1 (fsb_input_bytes) plus the keypoints.  Each
     stream drives its own pipeline context (own workspace and graphs)."""
-    pipes = list(pipes[:2])
-    if len(pipes) < 2:
-        pipes += extra_pipelines(pipes[0], 1, pipes[0].precision)
+    NS = E2E_STREAMS
+    pipes = list(pipes[:NS])
+    if len(pipes) < NS:
+        pipes += extra_pipelines(pipes[0], NS - len(pipes), pipes[0].precision)
     ctxs = [p_.context() for p_ in pipes]
     dev = images.device
     nhost = min(images.shape[0], 4 * B)
     h_img = images[:nhost].cpu().pin_memory()
     h_kp = kps[:nhost].cpu().pin_memory()
     nslot = nhost // B
-    streams = [torch.cuda.Stream(device=dev) for _ in range(2)]
-    outs = [pipes[j].allocate_outputs(B, tail=True) for j in range(2)]
+    streams = [torch.cuda.Stream(device=dev) for _ in range(NS)]
+    outs = [pipes[j].allocate_outputs(B, tail=True) for j in range(NS)]
     h_out = [{k: torch.empty(outs[0][k].shape, dtype=torch.float32).pin_memory()
-              for k in ("merged", "theta", "j_smpl")} for _ in range(2)]
+              for k in ("merged", "theta", "j_smpl")} for _ in range(NS)]
 
     def run(i):
-        j, s = i % 2, i % nslot
+        j, s = i % NS, i % nslot
         with torch.cuda.stream(streams[j]):
             pipes[j].run_batch(h_img[s * B:(s + 1) * B], h_kp[s * B:(s + 1) * B], cfg, outputs=outs[j], sync=False)
             for k in ("merged", "theta", "j_smpl"):
                 h_out[j][k].copy_(outs[j][k], non_blocking=True)
 
-    for i in range(max(warmup, 2 * nslot)):
+    for i in range(max(warmup, NS * nslot)):
         run(i)
     torch.cuda.synchronize()
     if dist is not None:
@@ -803,12 +807,13 @@ def end_to_end(torch, pipes, images, kps, cfg, B, steps, warmup, dist, world):
     for c in ctxs:
         c.input_bytes(reset=True)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    tail = [torch.cuda.Event() for _ in range(2)]
+    tail = [torch.cuda.Event() for _ in range(NS)]
     e0.record(streams[0])
-    streams[1].wait_event(e0)
+    for q in streams[1:]:
+        q.wait_event(e0)
     for i in range(steps):
         run(i)
-    for j in range(2):
+    for j in range(NS):
         tail[j].record(streams[j])
         streams[0].wait_event(tail[j])
     e1.record(streams[0])
@@ -819,8 +824,8 @@ def end_to_end(torch, pipes, images, kps, cfg, B, steps, warmup, dist, world):
     # device-frame run of the same frames
     ok = True
     ref = pipes[0].allocate_outputs(B, tail=True)
-    for j in range(min(2, steps)):
-        last = max(i for i in range(steps) if i % 2 == j)
+    for j in range(min(NS, steps)):
+        last = max(i for i in range(steps) if i % NS == j)
         s = last % nslot
         pipes[0].launch(images[s * B:(s + 1) * B], kps[s * B:(s + 1) * B], ref, cfg)
         torch.cuda.synchronize()
@@ -835,7 +840,7 @@ def end_to_end(torch, pipes, images, kps, cfg, B, steps, warmup, dist, world):
     return {"value": world * B * steps / (ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d_b,
             "d2h_bytes_per_step": d2h_b, "ms_per_step": ms / steps,
             "api": "Pipeline.run_batch on pinned host frames (K1 gathers the crop footprints over PCIe in "
-                   "place; two streams)",
+                   "place; %d streams)" % NS,
             "h2d_fraction_of_frames": h2d_b / full, "outputs_verified": bool(ok)}
 
 
