@@ -22,3 +22,4 @@ echo "ncu c4 gemm rc=$?"
 timeout -s KILL 600 $NCU --set full --clock-control none --import-source on -k regex:k_attn_tc -s 1 -c 1 \
   -o gpurun_out/ncu_c4_attn -f python tools/prof_c4.py 128 2 > gpurun_out/ncu_c4_attn.log 2>&1
 echo "ncu c4 attn rc=$?"
+tools/sm_time.sh gpurun_out/sm_time.csv; echo "sm_time rc=$?"
