@@ -120,6 +120,7 @@ struct fsb_ctx {
   bool has_decoder = false;
   fsb_decoder_config cfg{};
   DevMem dec_mem;
+  DevMem tcs_mem;  // TcStream tables of the encoder, body and hand decoders
   EncW enc{};
   BodyW body{};
   HandW hand{};
@@ -662,6 +663,60 @@ int fsb_load_decoder(fsb_ctx* c, const fsb_decoder_config* cfg, int n, const cha
     fill_attn(h.cross[l], p + ".cross", true);
     fill_mlp(h.mlp[l], p + ".mlp");
     h.tc_params[l] = PT(p + ".tcp");
+  }
+  // tcgen05 weight streams in consumption order (k_transformer_tc.cu)
+  if (Dm == 64) {
+    TcStream ts[3]{};
+    auto img = [&](TcStream& t, const uint8_t* ptr, uint32_t bytes) {
+      if (t.nw < FSB_TC_MAX_IMAGES) {
+        t.wptr[t.nw] = ptr;
+        t.wbytes[t.nw] = bytes;
+      }
+      ++t.nw;
+    };
+    const uint32_t DD = 64 * 64 * 2;
+    img(ts[0], e.t_patch, 192 * 64 * 2);
+    for (int l = 0; l < e.layers; ++l) {
+      img(ts[0], e.self[l].t_qkv, 3 * DD);
+      img(ts[0], e.self[l].t_o, DD);
+      img(ts[0], e.mlp[l].t_w1, 4 * DD);
+      img(ts[0], e.mlp[l].t_w2, 4 * DD);
+      ts[0].pptr[l] = e.tc_params[l];
+    }
+    ts[0].nprm = e.layers;
+    for (int role = 0; role < 2; ++role) {
+      TcStream& t = ts[1 + role];
+      const int L = role == 0 ? b.layers : h.layers;
+      for (int l = 0; l < L; ++l) {
+        const AttnW& sa = role == 0 ? b.self[l] : h.self[l];
+        const AttnW& ca = role == 0 ? b.cross[l] : h.cross[l];
+        const MlpW& m = role == 0 ? b.mlp[l] : h.mlp[l];
+        img(t, sa.t_qkv, 3 * DD);
+        img(t, sa.t_o, DD);
+        if (role == 0) {  // body: K | V first; hands (cross_attn_hands): queries first
+          img(t, ca.t_kv, 2 * DD);
+          img(t, ca.t_q, DD);
+        } else {
+          img(t, ca.t_q, DD);
+          img(t, ca.t_kv, 2 * DD);
+        }
+        img(t, ca.t_o, DD);
+        img(t, m.t_w1, 4 * DD);
+        img(t, m.t_w2, 4 * DD);
+        t.pptr[l] = role == 0 ? b.tc_params[l] : h.tc_params[l];
+      }
+      t.nprm = L;
+    }
+    for (int i = 0; i < 3; ++i)
+      if (ts[i].nw > FSB_TC_MAX_IMAGES)
+        return fail(c, FSB_ERR_USAGE, "decoder too deep for the tcgen05 weight stream (%d images > %d)", ts[i].nw,
+                    FSB_TC_MAX_IMAGES);
+    FSB_CUDA(c, c->tcs_mem.alloc(sizeof ts));
+    FSB_CUDA(c, cudaMemcpy(c->tcs_mem.p, ts, sizeof ts, cudaMemcpyHostToDevice));
+    const TcStream* dts = static_cast<const TcStream*>(c->tcs_mem.p);
+    e.tcs = dts;
+    b.tcs = dts + 1;
+    h.tcs = dts + 2;
   }
   // the body decoder's FK uses the decoder template's rest joints; the
   // body template upload patches it in (fsb_load_template)

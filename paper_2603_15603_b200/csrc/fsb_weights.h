@@ -58,6 +58,19 @@ struct MlpW {
   const uint8_t* t_w2;  // bf16 image (D, 4D)
 };
 
+// The weight-image / parameter-block sequence one tensor-core role
+// (encoder, body decoder, hand decoder) consumes, in consumption order.
+// Built on the host at upload and copied into shared memory by each CTA with
+// a few vector loads (k_transformer_tc.cu).
+#define FSB_TC_MAX_IMAGES 64
+struct TcStream {
+  const uint8_t* wptr[FSB_TC_MAX_IMAGES];
+  uint32_t wbytes[FSB_TC_MAX_IMAGES];
+  const float* pptr[FSB_MAX_LAYERS];
+  int nw, nprm;
+  int pad[2];
+};
+
 struct EncW {
   const uint8_t* t_patch;  // bf16 image (D, p*p*3)
   const float* patch_w;  // (p*p*3, D)
@@ -69,6 +82,7 @@ struct EncW {
   AttnW self[FSB_MAX_LAYERS];
   MlpW mlp[FSB_MAX_LAYERS];
   const float* tc_params[FSB_MAX_LAYERS];  // TCP_* blocks (cross part unused)
+  const TcStream* tcs;                     // device copy of the tcgen05 weight stream
 };
 
 struct BodyW {
@@ -93,6 +107,7 @@ struct BodyW {
   AttnW cross[8];
   MlpW mlp[8];
   const float* tc_params[8];  // TCP_* blocks
+  const TcStream* tcs;        // device copy of the tcgen05 weight stream
 };
 
 struct HandW {
@@ -112,6 +127,7 @@ struct HandW {
   AttnW cross[8];
   MlpW mlp[8];
   const float* tc_params[8];  // TCP_* blocks
+  const TcStream* tcs;        // device copy of the tcgen05 weight stream
 };
 
 // floats per vertex record: rest xyz + pad, shape basis (3 x 10), nnz skin

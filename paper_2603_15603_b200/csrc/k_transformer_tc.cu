@@ -59,21 +59,17 @@ static_assert(SMEM_TC + 6 * 1024 <= 227 * 1024, "shared memory budget");
 constexpr uint32_t T_GEN = 0;
 constexpr uint32_t T_PV = 64;
 
-constexpr int kMaxW = 64;
-
-struct Shared {
+struct alignas(16) Shared {
+  TcStream tab;         // this role's weight stream (copied from global by setup)
   uint64_t wbar[2];     // weight slot full
   uint64_t pbar[2];     // parameter slot full
   uint64_t mbar[NG];    // per-group MMA completion
   uint32_t tmem;
-  int nw, nprm;
   unsigned wrel[2];     // releases of each weight slot (monotonic)
   unsigned prel[2];     // releases of each parameter slot
-  const uint8_t* wptr[kMaxW];
-  uint32_t wbytes[kMaxW];
-  const float* pptr[FSB_MAX_LAYERS + 8];
   float xch[NG][2][2 * ROWS];  // row-reduction exchange, per group, double buffered
 };
+static_assert(sizeof(TcStream) % 16 == 0, "vector copy of the weight stream table");
 
 #ifdef FSB_PROFILE
 // cycle attribution of CTA 0 / group 0 (build with FSB_PROFILE=1):
@@ -107,10 +103,10 @@ struct Pipe {
   // weight ring: image i lives in slot i & 1.  The last of the two groups to
   // release image i - 1 loads image i + 1 into its slot.
   __device__ void load_image(int i) {
-    if (i < sh->nw) {
+    if (i < sh->tab.nw) {
       const int slot = i & 1;
-      tc::mbar_expect_tx(&sh->wbar[slot], sh->wbytes[i]);
-      tc::bulk_g2s(sall + S_W + slot * W_SLOT, sh->wptr[i], sh->wbytes[i], &sh->wbar[slot]);
+      tc::mbar_expect_tx(&sh->wbar[slot], sh->tab.wbytes[i]);
+      tc::bulk_g2s(sall + S_W + slot * W_SLOT, sh->tab.wptr[i], sh->tab.wbytes[i], &sh->wbar[slot]);
     }
   }
   __device__ uint32_t acquire() {  // wait for the next weight image; returns its address
@@ -133,10 +129,10 @@ struct Pipe {
 
   // per-layer parameter blocks: same protocol, one block per layer
   __device__ void load_prm(int l) {
-    if (l < sh->nprm) {
+    if (l < sh->tab.nprm) {
       const int slot = l & 1;
       tc::mbar_expect_tx(&sh->pbar[slot], PRM_BYTES);
-      tc::bulk_g2s(sall + S_PRM + slot * PRM_BYTES, sh->pptr[l], PRM_BYTES, &sh->pbar[slot]);
+      tc::bulk_g2s(sall + S_PRM + slot * PRM_BYTES, sh->tab.pptr[l], PRM_BYTES, &sh->pbar[slot]);
     }
   }
   __device__ const float* pacquire() {
@@ -677,8 +673,14 @@ __device__ void mlp(Pipe& P, const float* prm, float* x, bool valid) {
     for (int c = 0; c < HC; ++c) x[c] += v[c] + prm[TCP_M_B2 + HC * P.h + c];
 }
 
-// CTA setup: tables are filled by thread 0 before this is called
-__device__ void setup(Pipe& P, Shared& sh, uint8_t* smem) {
+// CTA setup: copy the role's weight stream table (16-byte loads), barriers,
+// TMEM, then the first two weight images and parameter blocks in flight
+__device__ void setup(Pipe& P, Shared& sh, uint8_t* smem, const TcStream* tab) {
+  {
+    const uint4* src = reinterpret_cast<const uint4*>(tab);
+    uint4* dst = reinterpret_cast<uint4*>(&sh.tab);
+    for (int i = threadIdx.x; i < (int)(sizeof(TcStream) / 16); i += NTH) dst[i] = __ldg(src + i);
+  }
   P.sh = &sh;
   P.sall = smem;
   P.g = threadIdx.x / GT;
@@ -742,23 +744,8 @@ __global__ void __launch_bounds__(NTH, 1) k_encoder_tc(const float* __restrict__
                                                        float* __restrict__ feats, int* nonfinite) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ Shared sh;
-  if (threadIdx.x == 0) {
-    int n = 0;
-    sh.wptr[n] = w.t_patch;
-    sh.wbytes[n++] = 192 * D * 2;
-    for (int l = 0; l < w.layers; ++l) {
-      sh.wptr[n] = w.self[l].t_qkv; sh.wbytes[n++] = 3 * D * D * 2;
-      sh.wptr[n] = w.self[l].t_o;   sh.wbytes[n++] = D * D * 2;
-      sh.wptr[n] = w.mlp[l].t_w1;   sh.wbytes[n++] = 4 * D * D * 2;
-      sh.wptr[n] = w.mlp[l].t_w2;   sh.wbytes[n++] = 4 * D * D * 2;
-    }
-    sh.nw = n;
-    for (int l = 0; l < w.layers; ++l) sh.pptr[l] = w.tc_params[l];
-    sh.nprm = w.layers;
-  }
-  __syncthreads();
   Pipe P;
-  setup(P, sh, smem);
+  setup(P, sh, smem, w.tcs);
   const int blk = P.r / BLK, p = P.r % BLK;
   const int crop = 4 * blockIdx.x + 2 * P.g + blk;
   const bool valid = crop < ncrops;
@@ -918,32 +905,8 @@ __global__ void __launch_bounds__(NTH, 1) k_decoders_tc(DecodeArgs a, BodyW bw, 
   const int nbc = (nbt + NG - 1) / NG;                        // body CTAs
   const bool body = (int)blockIdx.x < nbc;
   const int layers = body ? bw.layers : hw.layers;
-  if (threadIdx.x == 0) {
-    int n = 0;
-    for (int l = 0; l < layers; ++l) {
-      const AttnW& s = body ? bw.self[l] : hw.self[l];
-      const AttnW& c = body ? bw.cross[l] : hw.cross[l];
-      const MlpW& m = body ? bw.mlp[l] : hw.mlp[l];
-      sh.wptr[n] = s.t_qkv; sh.wbytes[n++] = 3 * D * D * 2;
-      sh.wptr[n] = s.t_o;   sh.wbytes[n++] = D * D * 2;
-      if (body) {
-        sh.wptr[n] = c.t_kv;  sh.wbytes[n++] = 2 * D * D * 2;
-        sh.wptr[n] = c.t_q;   sh.wbytes[n++] = D * D * 2;
-      } else {  // cross_attn_hands: queries first
-        sh.wptr[n] = c.t_q;   sh.wbytes[n++] = D * D * 2;
-        sh.wptr[n] = c.t_kv;  sh.wbytes[n++] = 2 * D * D * 2;
-      }
-      sh.wptr[n] = c.t_o;   sh.wbytes[n++] = D * D * 2;
-      sh.wptr[n] = m.t_w1;  sh.wbytes[n++] = 4 * D * D * 2;
-      sh.wptr[n] = m.t_w2;  sh.wbytes[n++] = 4 * D * D * 2;
-      sh.pptr[l] = body ? bw.tc_params[l] : hw.tc_params[l];
-    }
-    sh.nw = n;
-    sh.nprm = layers;
-  }
-  __syncthreads();
   Pipe P;
-  setup(P, sh, smem);
+  setup(P, sh, smem, body ? bw.tcs : hw.tcs);
   const int t = P.tid;
   const int r = P.r, blk = r / BLK, c0 = HC * P.h;
   const int tile = NG * (body ? (int)blockIdx.x : (int)blockIdx.x - nbc) + P.g;
