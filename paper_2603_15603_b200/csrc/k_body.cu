@@ -185,6 +185,13 @@ __global__ void __launch_bounds__(kLbsThreads, 2) k_lbs(TemplateDev t, const flo
     if (v0 + q < t.nv) vt[q].load(t, v0 + q);
   const bool live = v0 < t.nv;
   const bool both = v0 + 1 < t.nv;
+  // per-warp output staging: the warp's 64 vertices of a mesh are 192
+  // consecutive floats in V; they leave as fully coalesced 128-byte rows
+  // (a lane's own 6 floats at a 24-byte stride would touch 3x the L2 sectors)
+  float* wout = reinterpret_cast<float*>(lbs_smem + 2 * sizeof(LbsStage)) + (threadIdx.x >> 5) * 2 * 192;
+  const int lane = threadIdx.x & 31;
+  const int vw = (blockIdx.x * kLbsThreads + (threadIdx.x & ~31)) * kLbsVPT;  // the warp's first vertex
+  const int nfw = max(0, min(32 * kLbsVPT, t.nv - vw)) * 3;                   // floats of its block
   float2 chk = make_float2(0.0f, 0.0f);
   const float2 one2 = make_float2(1.0f, 1.0f);
   for (int it = 0; g < ngroups; g += gridDim.y, ++it) {
@@ -197,7 +204,7 @@ __global__ void __launch_bounds__(kLbsThreads, 2) k_lbs(TemplateDev t, const flo
     const int m0 = g * kLbsMeshes;
     const int nm = min(kLbsMeshes, B - m0);
     const int npair = (nm + 1) / 2;
-    if (live) {
+    {
       for (int pr = 0; pr < npair; ++pr) {
         float2 sh[10];
 #pragma unroll
@@ -206,56 +213,63 @@ __global__ void __launch_bounds__(kLbsThreads, 2) k_lbs(TemplateDev t, const flo
 #pragma unroll
         for (int q = 0; q < kLbsVPT; ++q) {
           const VertexTmpl<NZ>& V = vt[q];
-          float2 T[12];
+          if (!live) {  // lanes past the last vertex stage zeros (never stored)
 #pragma unroll
-          for (int e = 0; e < 12; ++e) T[e] = make_float2(0.0f, 0.0f);
+            for (int a = 0; a < 3; ++a) o[q][a] = make_float2(0.0f, 0.0f);
+            continue;
+          }
+          // shaped rest position: v_rest + basis . shape (accumulated onto v_rest)
+          float2 vs[3];
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            float2 acc = make_float2(V.vr[c], V.vr[c]);
+#pragma unroll
+            for (int k = 0; k < 10; ++k) acc = ffma2(make_float2(V.sb[10 * c + k], V.sb[10 * c + k]), sh[k], acc);
+            vs[c] = acc;
+          }
+          // sum_z w_z (R_z vs + t_z): each joint's transform applied, then
+          // weighted (24 FFMA2 for two joints instead of blending the 3 x 4
+          // transforms first, 33)
 #pragma unroll
           for (int z = 0; z < NZ; ++z) {
             const float2 wz = make_float2(V.w[z], V.w[z]);
             const float4* row = reinterpret_cast<const float4*>(&st.A2[pr][12 * V.j[z]]);
 #pragma unroll
-            for (int e2 = 0; e2 < 6; ++e2) {
-              const float4 r = row[e2];
-              T[2 * e2] = ffma2(wz, make_float2(r.x, r.y), T[2 * e2]);
-              T[2 * e2 + 1] = ffma2(wz, make_float2(r.z, r.w), T[2 * e2 + 1]);
+            for (int a = 0; a < 3; ++a) {
+              const float4 r01 = row[2 * a], r23 = row[2 * a + 1];  // (R_a0, R_a1 | R_a2, t_a) x 2 meshes
+              float2 pa = ffma2(make_float2(r01.x, r01.y), vs[0], make_float2(r23.z, r23.w));
+              pa = ffma2(make_float2(r01.z, r01.w), vs[1], pa);
+              pa = ffma2(make_float2(r23.x, r23.y), vs[2], pa);
+              o[q][a] = ffma2(wz, pa, z == 0 ? make_float2(0.0f, 0.0f) : o[q][a]);
             }
           }
-          float2 vs[3];
 #pragma unroll
-          for (int c = 0; c < 3; ++c) {
-            float2 acc = make_float2(0.0f, 0.0f);
-#pragma unroll
-            for (int k = 0; k < 10; ++k) acc = ffma2(make_float2(V.sb[10 * c + k], V.sb[10 * c + k]), sh[k], acc);
-            vs[c] = ffma2(acc, one2, make_float2(V.vr[c], V.vr[c]));
-          }
-#pragma unroll
-          for (int a = 0; a < 3; ++a) {
-            float2 acc = ffma2(T[4 * a], vs[0], T[4 * a + 3]);
-            acc = ffma2(T[4 * a + 1], vs[1], acc);
-            o[q][a] = ffma2(T[4 * a + 2], vs[2], acc);
+          for (int a = 0; a < 3; ++a)
             if (q == 0 || both) chk = ffma2(o[q][a], one2, chk);
-          }
         }
-        // mesh 2 pr (.x lanes) and 2 pr + 1 (.y lanes): 6 floats each; 8-byte
-        // vector stores when the mesh base keeps them aligned (odd nv, odd
-        // mesh: scalar stores)
+        // mesh 2 pr (.x lanes) and 2 pr + 1 (.y lanes) through the warp's
+        // staging rows
+        float2* s0 = reinterpret_cast<float2*>(wout + lane * 6);
+        float2* s1 = reinterpret_cast<float2*>(wout + 192 + lane * 6);
+        s0[0] = make_float2(o[0][0].x, o[0][1].x);
+        s0[1] = make_float2(o[0][2].x, o[1][0].x);
+        s0[2] = make_float2(o[1][1].x, o[1][2].x);
+        s1[0] = make_float2(o[0][0].y, o[0][1].y);
+        s1[1] = make_float2(o[0][2].y, o[1][0].y);
+        s1[2] = make_float2(o[1][1].y, o[1][2].y);
+        __syncwarp();
         const int m = m0 + 2 * pr;
 #pragma unroll
         for (int half = 0; half < 2; ++half) {
           if (2 * pr + half >= nm) break;
-          float* d = verts + ((int64_t)(m + half) * t.nv + v0) * 3;
-          const float f[6] = {half ? o[0][0].y : o[0][0].x, half ? o[0][1].y : o[0][1].x,
-                              half ? o[0][2].y : o[0][2].x, half ? o[1][0].y : o[1][0].x,
-                              half ? o[1][1].y : o[1][1].x, half ? o[1][2].y : o[1][2].x};
-          if (both && ((reinterpret_cast<uintptr_t>(d) & 7) == 0)) {
-            __stcs(reinterpret_cast<float2*>(d), make_float2(f[0], f[1]));
-            __stcs(reinterpret_cast<float2*>(d + 2), make_float2(f[2], f[3]));
-            __stcs(reinterpret_cast<float2*>(d + 4), make_float2(f[4], f[5]));
-          } else {
-            const int n = both ? 6 : 3;
-            for (int i = 0; i < n; ++i) __stcs(d + i, f[i]);
+          float* d = verts + ((int64_t)(m + half) * t.nv + vw) * 3;
+#pragma unroll
+          for (int i = 0; i < 6; ++i) {
+            const int idx = 32 * i + lane;
+            if (idx < nfw) __stcs(d + idx, wout[192 * half + idx]);
           }
         }
+        __syncwarp();  // the staging rows are rewritten by the next pair
       }
     }
     __syncthreads();  // buffer it & 1 is refilled two groups later
@@ -539,7 +553,7 @@ cudaError_t launch_lbs(const TemplateDev& t, const float* rel, const float* pose
   const int ngroups = (B + kLbsMeshes - 1) / kLbsMeshes;
   dim3 grid((t.nv + kLbsThreads * kLbsVPT - 1) / (kLbsThreads * kLbsVPT),
             ngroups < kLbsGroupCTAs ? ngroups : kLbsGroupCTAs);
-  const size_t smem = 2 * sizeof(LbsStage);
+  const size_t smem = 2 * sizeof(LbsStage) + kLbsThreads / 32 * 2 * 192 * sizeof(float);
   switch (t.nnz) {
     case 2: k_lbs<2><<<grid, kLbsThreads, smem, st>>>(t, rel, poses, ld_pose, B, verts, nonfinite); break;
     case 4: k_lbs<4><<<grid, kLbsThreads, smem, st>>>(t, rel, poses, ld_pose, B, verts, nonfinite); break;
@@ -550,7 +564,7 @@ cudaError_t launch_lbs(const TemplateDev& t, const float* rel, const float* pose
 }
 
 cudaError_t init_attrs_body() {
-  const int smem = (int)(2 * sizeof(LbsStage));
+  const int smem = (int)(2 * sizeof(LbsStage) + kLbsThreads / 32 * 2 * 192 * sizeof(float));
   cudaError_t e = cudaFuncSetAttribute(k_lbs<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_lbs<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_lbs<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
