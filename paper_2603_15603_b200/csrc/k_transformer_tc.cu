@@ -75,7 +75,7 @@ static_assert(sizeof(TcStream) % 16 == 0, "vector copy of the weight stream tabl
 // cycle attribution of CTA 0 / group 0 (build with FSB_PROFILE=1):
 // [0] total, [1] MMA waits, [2] weight waits, [3] issue barriers,
 // [4] row-exchange barriers, [5..] per-phase (see the kernels)
-__device__ unsigned long long g_tc_prof[2][2][16];  // [role][thread 0 | thread 255][counter]
+__device__ unsigned long long g_tc_prof[3][2][16];  // [encoder | body | hand][thread 0 | thread 255][counter]
 #define PROF_T0() const long long prof_t0_ = clock64()
 #define PROF_ADD(i) (prof[i] += clock64() - prof_t0_)
 #else
@@ -727,7 +727,9 @@ __device__ void teardown(Pipe& P, int role) {
   if (threadIdx.x < 32) tc::tmem_dealloc(P.sh->tmem, 512);
 #ifdef FSB_PROFILE
   P.prof[0] += clock64();
-  if (P.g == 0 && (P.tid == 0 || P.tid == GT - 1) && blockIdx.x == 0)
+  // CTA 0 (encoder / body decoder) and the last CTA (hand decoder), group 0
+  const bool rec = role == 0 ? blockIdx.x == 0 : (role == 1 ? blockIdx.x == 0 : blockIdx.x == gridDim.x - 1);
+  if (P.g == 0 && (P.tid == 0 || P.tid == GT - 1) && rec)
     for (int i = 0; i < 16; ++i) g_tc_prof[role][P.tid ? 1 : 0][i] = (unsigned long long)P.prof[i];
 #else
   (void)role;
@@ -1131,15 +1133,15 @@ __global__ void __launch_bounds__(NTH, 1) k_decoders_tc(DecodeArgs a, BodyW bw, 
 #ifdef FSB_PROFILE
   P.prof[8] += clock64() - tfin;
 #endif
-  teardown(P, 1);
+  teardown(P, body ? 1 : 2);
 }
 
 // debug export of the FSB_PROFILE cycle counters (not part of the public ABI)
 extern "C" int fsb_debug_tc_profile(unsigned long long* out32) {
 #ifdef FSB_PROFILE
-  return cudaMemcpyFromSymbol(out32, g_tc_prof, sizeof(unsigned long long) * 64) == cudaSuccess ? 0 : 4;
+  return cudaMemcpyFromSymbol(out32, g_tc_prof, sizeof(unsigned long long) * 96) == cudaSuccess ? 0 : 4;
 #else
-  for (int i = 0; i < 64; ++i) out32[i] = 0;
+  for (int i = 0; i < 96; ++i) out32[i] = 0;
   return 3;
 #endif
 }

@@ -31,17 +31,17 @@ def main():
         pipe.launch(images, kps, outs, pl.fast_config())
     torch.cuda.synchronize()
     lib = ctypes.CDLL(runtime.LIB_PATH)
-    buf = (ctypes.c_ulonglong * 64)()
+    buf = (ctypes.c_ulonglong * 96)()
     rc = lib.fsb_debug_tc_profile(buf)
     names = ["total", "mma_wait", "weight_wait", "issue_bar", "xch_bar"]
-    for role, tag in ((0, "encoder"), (1, "decoder")):
+    for role, tag in ((0, "encoder"), (1, "body decoder"), (2, "hand decoder")):
         for th, tname in ((0, "t0"), (1, "t255")):
             v = [buf[role * 32 + th * 16 + i] for i in range(16)]
             rest = v[0] - sum(v[1:5])
             print(tag, tname, "rc", rc,
                   " ".join("%s=%d(%.1f%%)" % (n, x, 100.0 * x / max(v[0], 1)) for n, x in zip(names, v)),
                   "work=%d(%.1f%%)" % (rest, 100.0 * rest / max(v[0], 1)))
-            if role == 1:
+            if role >= 1:
                 other = v[0] - v[5] - v[6] - v[7]
                 print("   sub-layers: self=%d cross=%d mlp=%d other=%d [setup+final=%d pos+params=%d heads=%d fk=%d]"
                       % (v[5], v[6], v[7], other, v[8], v[9], v[10], v[11]))
