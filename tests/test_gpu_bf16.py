@@ -109,3 +109,20 @@ def test_frame_batch_bf16_mpjpe(setup, dec_weights, full_models, full_projector)
     # a frame alone equals its row in the batch
     solo = pipe.run_batch(imgs[3:4], kps[3:4])
     assert np.array_equal(solo["j_smpl"].cpu().numpy()[0], res["j_smpl"][3])
+
+
+def test_frame_batch_bf16_position_independent(setup):
+    """The same frame at different batch positions -- another body tile, block,
+    hand slot, cross-attention round and CTA group -- gives the same bits.
+    23 frames: 12 body tiles (6 CTAs), 46 hands in 12 hand tiles (6 CTAs, the
+    last tile partly empty)."""
+    pipe, frames = setup
+    idx = [i % len(frames) for i in range(23)]
+    imgs = np.stack([frames[i][0] for i in idx])
+    kps = np.stack([frames[i][1] for i in idx])
+    out = pipe.run_batch(imgs, kps)
+    res = {k: v.cpu().numpy() for k, v in out.items()}
+    for j, i in enumerate(idx):
+        if j >= len(frames):
+            for k in ("merged", "theta", "j_smpl", "v_mhr"):
+                assert np.array_equal(res[k][j], res[k][i]), (j, i, k)

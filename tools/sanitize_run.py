@@ -20,7 +20,7 @@ if __name__ == "__main__":
 
     mhr, smpl, gt = synth.make_toy_models(0, 1200, 600)
     proj = pj.init_projector(pj.make_subsample(600, 150), (64, 32), seed=0)
-    scenes = [synth.random_scene(np.random.default_rng(5000 + i), smpl, (512, 512)) for i in range(3)]
+    scenes = [synth.random_scene(np.random.default_rng(5000 + i), smpl, (512, 512)) for i in range(5)]
     imgs = np.stack([synth.render_scene(s, smpl) for s in scenes])
     kps = np.stack([s.keypoints2d for s in scenes])
     for prec in ("fp32", "bf16"):
