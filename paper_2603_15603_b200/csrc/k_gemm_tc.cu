@@ -18,6 +18,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <stdio.h>
+#include <stdlib.h>
 
 #include "fsb_common.cuh"
 #include "tc_sm100.cuh"
@@ -235,6 +236,219 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 }
 
 // ---------------------------------------------------------------------------
+// CTA-pair variant (cta_group::2): a cluster of two CTAs on one TPC computes a
+// 256 x 256 tile.  CTA r holds A rows [128 r, +128) and B rows (output
+// columns) [128 r, +128) of every stage; the leader's single MMA lane issues
+// M = 256 tcgen05.mma that read both CTAs' shared memory and accumulate into
+// both CTAs' TMEM (rows [128 r, +128) in CTA r).  Per SM and k-block this
+// moves 32 KB through shared memory instead of 48 KB (TMA writes + MMA reads
+// of a 128 x 256 single-CTA tile exceed the 128 B/clk the SM provides).
+//   full[s]     leader only: expect_tx by the leader's producer for both
+//               CTAs' bytes; both CTAs' TMA loads complete on it
+//   empty[s]    each CTA: the leader's commit multicasts to both
+//   acc_full[b] each CTA: the leader's commit multicasts to both
+//   acc_empty[b] leader only: 2 x EPI_WARPS arrivals, the peer's remote
+// The epilogue is the single-CTA one on this CTA's 128 rows.
+// ---------------------------------------------------------------------------
+#ifndef GEMM2_STAGES
+#define GEMM2_STAGES 5
+#endif
+namespace {
+constexpr int STAGES2 = GEMM2_STAGES, BN2 = 256;
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
+    k_gemm_tc2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+               const __grid_constant__ CUtensorMap tmC, int M, int N, int K, GemmEpi epi) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  constexpr uint32_t A_BYTES = BM * BK * 2, B_BYTES = (BN2 / 2) * BK * 2, STAGE_BYTES = A_BYTES + B_BYTES;
+  constexpr uint32_t TMEM_COLS = 2 * BN2;
+  __shared__ uint64_t full[STAGES2], empty[STAGES2], acc_full[2], acc_empty[2], xbar[2 * EPI_WARPS];
+  __shared__ uint32_t tmem_base;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const uint32_t rank = tc::cluster_rank();
+  const bool leader = rank == 0;
+  const int nk = (K + BK - 1) / BK;
+  const int ntn = N / BN2, ntm = (M + 2 * BM - 1) / (2 * BM);
+  const int ntiles = ntm * ntn;
+  const int cid = blockIdx.x / 2, ncl = gridDim.x / 2;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES2; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      tc::mbar_init(&acc_full[b], 1);
+      tc::mbar_init(&acc_empty[b], 2 * EPI_WARPS);
+    }
+    for (int i = 0; i < 2 * EPI_WARPS; ++i) tc::mbar_init(&xbar[i], 1);
+    tc::mbar_fence_init();
+    tc::prefetch_tmap(&tmA);
+    tc::prefetch_tmap(&tmB);
+    tc::prefetch_tmap(&tmC);
+  }
+  if (warp == 1) tc::tmem_alloc_pair(&tmem_base, TMEM_COLS);
+  tc::fence_before();
+  __syncthreads();
+  tc::cluster_sync_all();  // both CTAs' barriers initialised before any remote use
+  tc::fence_after();
+  const uint32_t tmem = tmem_base;
+
+  if (warp == 0) {
+    // TMA producer (both CTAs): this CTA's A and B halves of each stage
+    int it = 0;
+    for (int t = cid; t < ntiles; t += ncl) {
+      const int m0 = (t / ntn) * 2 * BM + (int)rank * BM, n0 = (t % ntn) * BN2 + (int)rank * (BN2 / 2);
+      for (int kb = 0; kb < nk; ++kb, ++it) {
+        const int s = it % STAGES2;
+        if (it >= STAGES2) tc::mbar_wait(&empty[s], (uint32_t)(((it / STAGES2) - 1) & 1));
+        if (lane == 0) {
+          uint8_t* sa = smem + s * STAGE_BYTES;
+          if (leader) tc::mbar_expect_tx(&full[s], 2 * STAGE_BYTES);
+          tc::tma_load_2d_pair(sa, &tmA, kb * BK, m0, &full[s]);
+          tc::tma_load_2d_pair(sa + A_BYTES, &tmB, kb * BK, n0, &full[s]);
+        }
+        __syncwarp();
+      }
+    }
+  } else if (warp == 1) {
+    if (leader) {
+      // MMA issuer (leader CTA only)
+      const uint32_t idesc = tc::idesc_bf16(2 * BM, BN2);
+      const uint32_t sbase = tc::smem_u32(smem);
+      int it = 0, tc_count = 0;
+      for (int t = cid; t < ntiles; t += ncl, ++tc_count) {
+        const int buf = tc_count & 1;
+        if (tc_count >= 2) tc::mbar_wait(&acc_empty[buf], (uint32_t)(((tc_count >> 1) - 1) & 1));
+        tc::fence_after();
+        const uint32_t acc = tmem + (uint32_t)(buf * BN2);
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const int s = it % STAGES2;
+          tc::mbar_wait(&full[s], (uint32_t)((it / STAGES2) & 1));
+          tc::fence_after();
+          if (lane == 0) {
+            const uint32_t a = sbase + s * STAGE_BYTES, b = a + A_BYTES;
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k)
+              tc::mma_bf16_pair(acc, tc::sw128_kmajor_desc(a + 32 * k), tc::sw128_kmajor_desc(b + 32 * k), idesc,
+                                (kb | k) != 0);
+            tc::mma_commit_pair(&empty[s], 0x3);  // frees the stage in both CTAs
+          }
+          __syncwarp();
+        }
+        if (lane == 0) tc::mma_commit_pair(&acc_full[buf], 0x3);  // both CTAs' accumulators complete
+        __syncwarp();
+      }
+    }
+  } else if (warp >= 2) {
+    // epilogue on this CTA's 128 rows (as in k_gemm_tc)
+    const int ew = warp - 2, quad = warp % 4, half = ew / 4;
+    constexpr int HALF = BN2 / (EPI_WARPS / 4);
+    uint8_t* stg = smem + STAGES2 * STAGE_BYTES + ew * 2 * EPI_BUF;
+    const bool f32 = epi.kind == EPI_RESID_F32 || epi.kind == EPI_EMBED_F32;
+    const bool resid = epi.kind == EPI_RESID_F32;
+    const int CB = f32 ? 32 : 64;
+    const uint32_t acc_empty_leader0 = tc::mapa_shared(&acc_empty[0], 0);
+    const uint32_t acc_empty_leader1 = tc::mapa_shared(&acc_empty[1], 0);
+    int tc_count = 0, nblk = 0;
+    uint32_t xph[2] = {0u, 0u};
+    for (int t = cid; t < ntiles; t += ncl, ++tc_count) {
+      const int buf = tc_count & 1;
+      const int m0 = (t / ntn) * 2 * BM + (int)rank * BM, n0 = (t % ntn) * BN2;
+      const int r0 = m0 + quad * 32, row = r0 + lane;
+      const int cbase = n0 + half * HALF;
+      const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(buf * BN2 + half * HALF);
+      const int nb = HALF / CB;
+      auto fetch = [&](int k) {
+        const int sb = (nblk + k) & 1;
+        if (lane == 0) {
+          tc::bulk_wait_read0();
+          tc::mbar_expect_tx(&xbar[2 * ew + sb], EPI_BUF);
+          tc::tma_load_2d(stg + sb * EPI_BUF, &tmC, cbase + k * CB, r0, &xbar[2 * ew + sb]);
+        }
+      };
+      if (resid && r0 < M) {
+        fetch(0);
+        if (nb > 1) fetch(1);
+      }
+      tc::mbar_wait(&acc_full[buf], (uint32_t)((tc_count >> 1) & 1));
+      tc::fence_after();
+      for (int k = 0; k < nb; ++k) {
+        const int sb = (nblk + k) & 1;
+        uint8_t* sbuf = stg + sb * EPI_BUF;
+        const int col = cbase + k * CB;
+        float v[64];
+        tc::tmem_ld32(taddr + k * CB, v);
+        if (!f32) tc::tmem_ld32(taddr + k * CB + 32, v + 32);
+        if (k + 1 == nb) {
+          tc::fence_before();
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive_cluster(buf ? acc_empty_leader1 : acc_empty_leader0);
+        }
+        if (r0 >= M || col >= N) continue;  // warp-uniform
+#pragma unroll
+        for (int i = 0; i < 32; i += 4) {
+          const float4 q = __ldg(reinterpret_cast<const float4*>(epi.bias + col + i));
+          v[i] += q.x; v[i + 1] += q.y; v[i + 2] += q.z; v[i + 3] += q.w;
+        }
+        if (!f32) {
+          if (col + 32 < N)
+#pragma unroll
+            for (int i = 32; i < 64; i += 4) {
+              const float4 q = __ldg(reinterpret_cast<const float4*>(epi.bias + col + i));
+              v[i] += q.x; v[i + 1] += q.y; v[i + 2] += q.z; v[i + 3] += q.w;
+            }
+          if (epi.kind == EPI_RELU_BF16)
+#pragma unroll
+            for (int i = 0; i < 64; ++i) v[i] = fmaxf(v[i], 0.0f);
+          if (lane == 0) tc::bulk_wait_read0();
+          __syncwarp();
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            *reinterpret_cast<uint4*>(sbuf + sw128_off(lane, q)) =
+                make_uint4(tc::pack_bf16(v[8 * q], v[8 * q + 1]), tc::pack_bf16(v[8 * q + 2], v[8 * q + 3]),
+                           tc::pack_bf16(v[8 * q + 4], v[8 * q + 5]), tc::pack_bf16(v[8 * q + 6], v[8 * q + 7]));
+        } else if (resid) {
+          tc::mbar_wait(&xbar[2 * ew + sb], xph[sb]);
+          xph[sb] ^= 1u;
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            float4* p = reinterpret_cast<float4*>(sbuf + sw128_off(lane, q));
+            float4 x = *p;
+            x.x += v[4 * q]; x.y += v[4 * q + 1]; x.z += v[4 * q + 2]; x.w += v[4 * q + 3];
+            *p = x;
+          }
+        } else {  // EPI_EMBED_F32
+          if (lane == 0) tc::bulk_wait_read0();
+          __syncwarp();
+          const float4* pr = reinterpret_cast<const float4*>(epi.pos + (size_t)(row % epi.T) * epi.ldo + col);
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const float4 pp = __ldg(pr + q);
+            *reinterpret_cast<float4*>(sbuf + sw128_off(lane, q)) =
+                make_float4(v[4 * q] + pp.x, v[4 * q + 1] + pp.y, v[4 * q + 2] + pp.z, v[4 * q + 3] + pp.w);
+          }
+        }
+        tc::fence_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tc::tma_store_2d(&tmC, col, r0, sbuf);
+          tc::bulk_commit();
+        }
+        if (resid && k + 2 < nb) fetch(k + 2);
+      }
+      nblk += nb;
+    }
+    if (lane == 0) tc::bulk_wait0();
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::cluster_sync_all();  // the leader's MMAs into this CTA's TMEM / from its smem are done
+  if (warp == 1) tc::tmem_dealloc_pair(tmem, TMEM_COLS);
+}
+
+// ---------------------------------------------------------------------------
 // host side: tensor maps (driver entry point through the runtime) and launch
 
 static PFN_cuTensorMapEncodeTiled_v12000 tmap_encoder() {
@@ -283,12 +497,28 @@ static constexpr size_t gemm_smem() {
   return (size_t)STAGES * (BM * BK * 2 + BN * BK * 2) + (size_t)EPI_WARPS * 2 * EPI_BUF + 1024;
 }
 
+static constexpr size_t gemm2_smem() {
+  return (size_t)STAGES2 * (BM * BK * 2 + (BN2 / 2) * BK * 2) + (size_t)EPI_WARPS * 2 * EPI_BUF + 1024;
+}
+
 cudaError_t init_attrs_gemm_tc() {
   cudaError_t e = cudaFuncSetAttribute(k_gemm_tc<256>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)gemm_smem<256>());
   if (e == cudaSuccess)
     e = cudaFuncSetAttribute(k_gemm_tc<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_smem<128>());
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(k_gemm_tc2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm2_smem());
   return e;
+}
+
+// FSB_GEMM_PAIR=0 selects the single-CTA kernel for every shape (A/B runs)
+static bool use_pair() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("FSB_GEMM_PAIR");
+    v = (e != nullptr && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
 }
 
 // A (M x K, lda), W (N x K, ldw): bf16 row-major.  N must be a multiple of 32,
@@ -305,7 +535,8 @@ cudaError_t launch_gemm_tc(const __nv_bfloat16* A, int lda, const __nv_bfloat16*
   }
   CUtensorMap ta, tb, tc_;
   const int BN = (N % 256 == 0) ? 256 : 128;
-  if (!make_tmap_bf16(&ta, A, M, K, lda, BM) || !make_tmap_bf16(&tb, W, N, K, ldw, BN))
+  const bool pair = BN == 256 && M > BM && use_pair();
+  if (!make_tmap_bf16(&ta, A, M, K, lda, BM) || !make_tmap_bf16(&tb, W, N, K, ldw, pair ? BN / 2 : BN))
     return cudaErrorInvalidValue;
   // epilogue blocks: 32 rows x 128 bytes (fp32: 32 columns, bf16: 64)
   const bool f32 = epi.kind == EPI_RESID_F32 || epi.kind == EPI_EMBED_F32;
@@ -316,6 +547,12 @@ cudaError_t launch_gemm_tc(const __nv_bfloat16* A, int lda, const __nv_bfloat16*
     int dev = 0;
     cudaGetDevice(&dev);
     if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = 148;
+  }
+  if (pair) {  // persistent clusters of two CTAs, one 256 x 256 tile at a time
+    const int64_t tiles = (int64_t)(N / BN2) * ((M + 2 * BM - 1) / (2 * BM));
+    const int64_t ncl = tiles < sms / 2 ? tiles : sms / 2;
+    k_gemm_tc2<<<dim3((unsigned)(2 * ncl)), GEMM_THREADS, gemm2_smem(), st>>>(ta, tb, tc_, M, N, K, epi);
+    return cudaGetLastError();
   }
   const int64_t tiles = (int64_t)((N + BN - 1) / BN) * ((M + BM - 1) / BM);
   const dim3 grid((unsigned)(tiles < sms ? tiles : sms));  // persistent: one CTA per SM
