@@ -253,8 +253,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 #ifndef GEMM2_STAGES
 #define GEMM2_STAGES 5
 #endif
+#ifndef GEMM2_EPI_BUFS
+#define GEMM2_EPI_BUFS 4
+#endif
 namespace {
-constexpr int STAGES2 = GEMM2_STAGES, BN2 = 256;
+constexpr int STAGES2 = GEMM2_STAGES, BN2 = 256, NBUF2 = GEMM2_EPI_BUFS;  // NBUF2: staging buffers per epilogue warp
 }
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
@@ -264,7 +267,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   constexpr uint32_t A_BYTES = BM * BK * 2, B_BYTES = (BN2 / 2) * BK * 2, STAGE_BYTES = A_BYTES + B_BYTES;
   constexpr uint32_t TMEM_COLS = 2 * BN2;
-  __shared__ uint64_t full[STAGES2], empty[STAGES2], acc_full[2], acc_empty[2], xbar[2 * EPI_WARPS];
+  __shared__ uint64_t full[STAGES2], empty[STAGES2], acc_full[2], acc_empty[2], xbar[NBUF2 * EPI_WARPS];
   __shared__ uint32_t tmem_base;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t rank = tc::cluster_rank();
@@ -282,7 +285,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
       tc::mbar_init(&acc_full[b], 1);
       tc::mbar_init(&acc_empty[b], 2 * EPI_WARPS);
     }
-    for (int i = 0; i < 2 * EPI_WARPS; ++i) tc::mbar_init(&xbar[i], 1);
+    for (int i = 0; i < NBUF2 * EPI_WARPS; ++i) tc::mbar_init(&xbar[i], 1);
     tc::mbar_fence_init();
     tc::prefetch_tmap(&tmA);
     tc::prefetch_tmap(&tmB);
@@ -345,14 +348,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
     // epilogue on this CTA's 128 rows (as in k_gemm_tc)
     const int ew = warp - 2, quad = warp % 4, half = ew / 4;
     constexpr int HALF = BN2 / (EPI_WARPS / 4);
-    uint8_t* stg = smem + STAGES2 * STAGE_BYTES + ew * 2 * EPI_BUF;
+    uint8_t* stg = smem + STAGES2 * STAGE_BYTES + ew * NBUF2 * EPI_BUF;
     const bool f32 = epi.kind == EPI_RESID_F32 || epi.kind == EPI_EMBED_F32;
     const bool resid = epi.kind == EPI_RESID_F32;
     const int CB = f32 ? 32 : 64;
     const uint32_t acc_empty_leader0 = tc::mapa_shared(&acc_empty[0], 0);
     const uint32_t acc_empty_leader1 = tc::mapa_shared(&acc_empty[1], 0);
     int tc_count = 0, nblk = 0;
-    uint32_t xph[2] = {0u, 0u};
+    uint32_t xph[NBUF2];
+#pragma unroll
+    for (int i = 0; i < NBUF2; ++i) xph[i] = 0u;
     for (int t = cid; t < ntiles; t += ncl, ++tc_count) {
       const int buf = tc_count & 1;
       const int m0 = (t / ntn) * 2 * BM + (int)rank * BM, n0 = (t % ntn) * BN2;
@@ -360,22 +365,22 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
       const int cbase = n0 + half * HALF;
       const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(buf * BN2 + half * HALF);
       const int nb = HALF / CB;
+      // residual blocks run NBUF2 ahead of their use (the epilogue of the
+      // memory-bound Wo / W2 GEMMs is bound by these loads)
       auto fetch = [&](int k) {
-        const int sb = (nblk + k) & 1;
+        const int sb = (nblk + k) % NBUF2;
         if (lane == 0) {
           tc::bulk_wait_read0();
-          tc::mbar_expect_tx(&xbar[2 * ew + sb], EPI_BUF);
-          tc::tma_load_2d(stg + sb * EPI_BUF, &tmC, cbase + k * CB, r0, &xbar[2 * ew + sb]);
+          tc::mbar_expect_tx(&xbar[NBUF2 * ew + sb], EPI_BUF);
+          tc::tma_load_2d(stg + sb * EPI_BUF, &tmC, cbase + k * CB, r0, &xbar[NBUF2 * ew + sb]);
         }
       };
-      if (resid && r0 < M) {
-        fetch(0);
-        if (nb > 1) fetch(1);
-      }
+      if (resid && r0 < M)
+        for (int k = 0; k < NBUF2 && k < nb; ++k) fetch(k);
       tc::mbar_wait(&acc_full[buf], (uint32_t)((tc_count >> 1) & 1));
       tc::fence_after();
       for (int k = 0; k < nb; ++k) {
-        const int sb = (nblk + k) & 1;
+        const int sb = (nblk + k) % NBUF2;
         uint8_t* sbuf = stg + sb * EPI_BUF;
         const int col = cbase + k * CB;
         float v[64];
@@ -410,7 +415,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
                 make_uint4(tc::pack_bf16(v[8 * q], v[8 * q + 1]), tc::pack_bf16(v[8 * q + 2], v[8 * q + 3]),
                            tc::pack_bf16(v[8 * q + 4], v[8 * q + 5]), tc::pack_bf16(v[8 * q + 6], v[8 * q + 7]));
         } else if (resid) {
-          tc::mbar_wait(&xbar[2 * ew + sb], xph[sb]);
+          tc::mbar_wait(&xbar[NBUF2 * ew + sb], xph[sb]);
           xph[sb] ^= 1u;
 #pragma unroll
           for (int q = 0; q < 8; ++q) {
@@ -436,7 +441,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
           tc::tma_store_2d(&tmC, col, r0, sbuf);
           tc::bulk_commit();
         }
-        if (resid && k + 2 < nb) fetch(k + 2);
+        if (resid && k + NBUF2 < nb) fetch(k + NBUF2);
       }
       nblk += nb;
     }
@@ -498,7 +503,7 @@ static constexpr size_t gemm_smem() {
 }
 
 static constexpr size_t gemm2_smem() {
-  return (size_t)STAGES2 * (BM * BK * 2 + (BN2 / 2) * BK * 2) + (size_t)EPI_WARPS * 2 * EPI_BUF + 1024;
+  return (size_t)STAGES2 * (BM * BK * 2 + (BN2 / 2) * BK * 2) + (size_t)EPI_WARPS * NBUF2 * EPI_BUF + 1024;
 }
 
 cudaError_t init_attrs_gemm_tc() {
