@@ -118,10 +118,23 @@ __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
   return d;
 }
 
+#ifndef FSB_LBS_VPT
+#define FSB_LBS_VPT 2
+#endif
+#ifndef FSB_LBS_MESHES
+#define FSB_LBS_MESHES 32
+#endif
+#ifndef FSB_LBS_GROUP_CTAS
+#define FSB_LBS_GROUP_CTAS 8
+#endif
+#ifndef FSB_LBS_MIN_BLOCKS
+#define FSB_LBS_MIN_BLOCKS 2
+#endif
 constexpr int kLbsThreads = 256;
-constexpr int kLbsVPT = 2;      // consecutive vertices per thread (float2 stores)
-constexpr int kLbsMeshes = 32;  // meshes per group, as 16 pairs
-constexpr int kLbsGroupCTAs = 8;  // CTAs along the mesh axis (each walks groups y, y + 8, ...)
+constexpr int kLbsVPT = FSB_LBS_VPT;            // consecutive vertices per thread
+constexpr int kLbsMeshes = FSB_LBS_MESHES;      // meshes per group, as pairs
+constexpr int kLbsGroupCTAs = FSB_LBS_GROUP_CTAS;  // CTAs along the mesh axis (each walks groups y, y + G, ...)
+constexpr int kLbsWarpFloats = 32 * kLbsVPT * 3;   // V floats of one warp's vertices of one mesh
 
 // LBS of a vertex tile for a run of 32-mesh groups.  Each thread keeps its
 // two vertices' template records in registers for the whole run and walks
@@ -168,7 +181,7 @@ __device__ __forceinline__ void lbs_stage(LbsStage& st, const float* __restrict_
 }
 
 template <int NZ>
-__global__ void __launch_bounds__(kLbsThreads, 2) k_lbs(TemplateDev t, const float* __restrict__ rel,
+__global__ void __launch_bounds__(kLbsThreads, FSB_LBS_MIN_BLOCKS) k_lbs(TemplateDev t, const float* __restrict__ rel,
                                                         const float* __restrict__ poses, int ld_pose, int B,
                                                         float* __restrict__ verts, int* nonfinite) {
   extern __shared__ __align__(16) uint8_t lbs_smem[];
@@ -184,11 +197,10 @@ __global__ void __launch_bounds__(kLbsThreads, 2) k_lbs(TemplateDev t, const flo
   for (int q = 0; q < kLbsVPT; ++q)
     if (v0 + q < t.nv) vt[q].load(t, v0 + q);
   const bool live = v0 < t.nv;
-  const bool both = v0 + 1 < t.nv;
   // per-warp output staging: the warp's 64 vertices of a mesh are 192
   // consecutive floats in V; they leave as fully coalesced 128-byte rows
   // (a lane's own 6 floats at a 24-byte stride would touch 3x the L2 sectors)
-  float* wout = reinterpret_cast<float*>(lbs_smem + 2 * sizeof(LbsStage)) + (threadIdx.x >> 5) * 2 * 192;
+  float* wout = reinterpret_cast<float*>(lbs_smem + 2 * sizeof(LbsStage)) + (threadIdx.x >> 5) * 2 * kLbsWarpFloats;
   const int lane = threadIdx.x & 31;
   const int vw = (blockIdx.x * kLbsThreads + (threadIdx.x & ~31)) * kLbsVPT;  // the warp's first vertex
   const int nfw = max(0, min(32 * kLbsVPT, t.nv - vw)) * 3;                   // floats of its block
@@ -245,18 +257,17 @@ __global__ void __launch_bounds__(kLbsThreads, 2) k_lbs(TemplateDev t, const flo
           }
 #pragma unroll
           for (int a = 0; a < 3; ++a)
-            if (q == 0 || both) chk = ffma2(o[q][a], one2, chk);
+            if (v0 + q < t.nv) chk = ffma2(o[q][a], one2, chk);
         }
         // mesh 2 pr (.x lanes) and 2 pr + 1 (.y lanes) through the warp's
         // staging rows
-        float2* s0 = reinterpret_cast<float2*>(wout + lane * 6);
-        float2* s1 = reinterpret_cast<float2*>(wout + 192 + lane * 6);
-        s0[0] = make_float2(o[0][0].x, o[0][1].x);
-        s0[1] = make_float2(o[0][2].x, o[1][0].x);
-        s0[2] = make_float2(o[1][1].x, o[1][2].x);
-        s1[0] = make_float2(o[0][0].y, o[0][1].y);
-        s1[1] = make_float2(o[0][2].y, o[1][0].y);
-        s1[2] = make_float2(o[1][1].y, o[1][2].y);
+#pragma unroll
+        for (int q = 0; q < kLbsVPT; ++q)
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            wout[(lane * kLbsVPT + q) * 3 + a] = o[q][a].x;
+            wout[kLbsWarpFloats + (lane * kLbsVPT + q) * 3 + a] = o[q][a].y;
+          }
         __syncwarp();
         const int m = m0 + 2 * pr;
 #pragma unroll
@@ -264,9 +275,9 @@ __global__ void __launch_bounds__(kLbsThreads, 2) k_lbs(TemplateDev t, const flo
           if (2 * pr + half >= nm) break;
           float* d = verts + ((int64_t)(m + half) * t.nv + vw) * 3;
 #pragma unroll
-          for (int i = 0; i < 6; ++i) {
+          for (int i = 0; i < 3 * kLbsVPT; ++i) {
             const int idx = 32 * i + lane;
-            if (idx < nfw) __stcs(d + idx, wout[192 * half + idx]);
+            if (idx < nfw) __stcs(d + idx, wout[kLbsWarpFloats * half + idx]);
           }
         }
         __syncwarp();  // the staging rows are rewritten by the next pair
@@ -553,7 +564,7 @@ cudaError_t launch_lbs(const TemplateDev& t, const float* rel, const float* pose
   const int ngroups = (B + kLbsMeshes - 1) / kLbsMeshes;
   dim3 grid((t.nv + kLbsThreads * kLbsVPT - 1) / (kLbsThreads * kLbsVPT),
             ngroups < kLbsGroupCTAs ? ngroups : kLbsGroupCTAs);
-  const size_t smem = 2 * sizeof(LbsStage) + kLbsThreads / 32 * 2 * 192 * sizeof(float);
+  const size_t smem = 2 * sizeof(LbsStage) + kLbsThreads / 32 * 2 * kLbsWarpFloats * sizeof(float);
   switch (t.nnz) {
     case 2: k_lbs<2><<<grid, kLbsThreads, smem, st>>>(t, rel, poses, ld_pose, B, verts, nonfinite); break;
     case 4: k_lbs<4><<<grid, kLbsThreads, smem, st>>>(t, rel, poses, ld_pose, B, verts, nonfinite); break;
@@ -564,7 +575,7 @@ cudaError_t launch_lbs(const TemplateDev& t, const float* rel, const float* pose
 }
 
 cudaError_t init_attrs_body() {
-  const int smem = (int)(2 * sizeof(LbsStage) + kLbsThreads / 32 * 2 * 192 * sizeof(float));
+  const int smem = (int)(2 * sizeof(LbsStage) + kLbsThreads / 32 * 2 * kLbsWarpFloats * sizeof(float));
   cudaError_t e = cudaFuncSetAttribute(k_lbs<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_lbs<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_lbs<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
