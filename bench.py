@@ -710,9 +710,16 @@ def stream_run(torch, pipes, streams, images, kps, cfg, B, dist, world, rank, to
             res[r:r + nb, :76].copy_(o["theta"])
             res[r:r + nb, 76:].copy_(o["j_smpl"].reshape(nb, 66))
 
-    # warm-up pass over a few batches (graphs for every stream)
-    for k in range(2 * S):
-        batch(k, lo, min(B, n))
+    # warm-up: every (pipeline, input slot) pair the timed pass will use
+    # gets its CUDA graph captured first -- the input ring repeats with period
+    # lcm(pipelines, bank / B) batches, as a deployment's ring of frame buffers would
+    import math
+
+    nslot = max(1, bank // B)
+    period = S * nslot // math.gcd(S, nslot)
+    for k in range(min(period, max(1, (n + B - 1) // B))):
+        f0 = lo + k * B
+        batch(k, f0, min(B, hi - f0))
     torch.cuda.synchronize()
     if dist is not None:
         dist.barrier()
