@@ -64,6 +64,10 @@ def test_tcgen05_and_bulk_copy_in_sass():
     sass = subprocess.run(["cuobjdump", "-sass", runtime.LIB_PATH], capture_output=True, text=True).stdout
     for op in ("UTCHMMA", "LDTM", "UBLKCP", "UTCBAR"):
         assert op in sass, op
+    # the CTA-pair GEMM: M = 256 MMAs across two SMs, pair TMA loads and
+    # multicast commits
+    for op in ("UTCHMMA.2CTA", "UTMALDG.2D.2CTA", "UTCBAR.2CTA.MULTICAST", "UTMASTG.2D"):
+        assert op in sass, op
 
 
 def test_product_does_not_import_oracle():
