@@ -188,10 +188,8 @@ __device__ __forceinline__ void gemm(uint32_t a, int K, uint32_t b, int N, uint3
   for (int k = 0; k < K; k += 16) tc::mma_bf16(tmem + dcol, tc::kmajor_desc(a, K, k), tc::kmajor_desc(b, K, k), id, k > 0);
 }
 
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
-  tc::tmem_ld16(taddr, v);
-  tc::tmem_ld16(taddr + 16, v + 16);
-}
+// 32 lanes x 32 columns: one tcgen05.ld, one wait
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) { tc::tmem_ld32(taddr, v); }
 
 // store 8 consecutive bf16 values of row r at column k0 of a K-major tile
 __device__ __forceinline__ void st_row8(uint8_t* tile, int r, int k0, int K, const float* v) {
