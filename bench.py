@@ -60,7 +60,7 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
-    ap.add_argument("--streams", type=int, default=12,
+    ap.add_argument("--streams", type=int, default=16,
                     help="in-flight batches per GPU: independent pipeline contexts on their own streams")
     ap.add_argument("--no-c3", action="store_true", help="skip the C3 LBS + projector microbench")
     ap.add_argument("--no-c4", action="store_true", help="skip the C4 ViT-L-sized encoder microbench")
