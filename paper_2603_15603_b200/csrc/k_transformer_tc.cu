@@ -67,6 +67,7 @@ struct alignas(16) Shared {
   uint32_t tmem;
   unsigned wrel[2];     // releases of each weight slot (monotonic)
   unsigned prel[2];     // releases of each parameter slot
+  unsigned nact;        // groups of this CTA with work (1 or 2): releases per slot reuse
   float xch[NG][2][2 * ROWS];  // row-reduction exchange, per group, double buffered
 };
 static_assert(sizeof(TcStream) % 16 == 0, "vector copy of the weight stream table");
@@ -123,7 +124,7 @@ struct Pipe {
     const int done = wuse - 2;
     if (done >= 0 && tid == 0) {
       const unsigned prior = atomicAdd(&sh->wrel[done & 1], 1u);
-      if ((prior % NG) == NG - 1) load_image(done + 2);
+      if ((prior % sh->nact) == sh->nact - 1) load_image(done + 2);
     }
   }
 
@@ -147,7 +148,7 @@ struct Pipe {
     const int done = puse - 2;
     if (done >= 0 && tid == 0) {
       const unsigned prior = atomicAdd(&sh->prel[done & 1], 1u);
-      if ((prior % NG) == NG - 1) load_prm(done + 2);
+      if ((prior % sh->nact) == sh->nact - 1) load_prm(done + 2);
     }
   }
 
@@ -673,7 +674,10 @@ __device__ void mlp(Pipe& P, const float* prm, float* x, bool valid) {
 
 // CTA setup: copy the role's weight stream table (16-byte loads), barriers,
 // TMEM, then the first two weight images and parameter blocks in flight
-__device__ void setup(Pipe& P, Shared& sh, uint8_t* smem, const TcStream* tab) {
+// nact: groups of the CTA that have work; a group without work (the second
+// tile of a CTA at the end of the batch) leaves right after setup, so the
+// other runs alone on the SM and is the only one releasing weight slots.
+__device__ void setup(Pipe& P, Shared& sh, uint8_t* smem, const TcStream* tab, unsigned nact) {
   {
     const uint4* src = reinterpret_cast<const uint4*>(tab);
     uint4* dst = reinterpret_cast<uint4*>(&sh.tab);
@@ -697,6 +701,7 @@ __device__ void setup(Pipe& P, Shared& sh, uint8_t* smem, const TcStream* tab) {
   P.prof[0] = -clock64();
 #endif
   if (threadIdx.x == 0) {
+    sh.nact = nact;
     for (int i = 0; i < 2; ++i) {
       tc::mbar_init(&sh.wbar[i], 1);
       tc::mbar_init(&sh.pbar[i], 1);
@@ -745,10 +750,14 @@ __global__ void __launch_bounds__(NTH, 1) k_encoder_tc(const float* __restrict__
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ Shared sh;
   Pipe P;
-  setup(P, sh, smem, w.tcs);
+  setup(P, sh, smem, w.tcs, 4 * (int)blockIdx.x + 2 < ncrops ? 2u : 1u);
   const int blk = P.r / BLK, p = P.r % BLK;
   const int crop = 4 * blockIdx.x + 2 * P.g + blk;
   const bool valid = crop < ncrops;
+  if (4 * (int)blockIdx.x + 2 * P.g >= ncrops) {  // no crop for this group
+    teardown(P, 0);
+    return;
+  }
 
   // patchify (decoder.py:247-248): this thread packs image rows iy in
   // [4h, 4h + 4) of patch p into the K = 192 tile (k = iy*24 + ix*3 + c),
@@ -906,7 +915,10 @@ __global__ void __launch_bounds__(NTH, 1) k_decoders_tc(DecodeArgs a, BodyW bw, 
   const bool body = (int)blockIdx.x < nbc;
   const int layers = body ? bw.layers : hw.layers;
   Pipe P;
-  setup(P, sh, smem, body ? bw.tcs : hw.tcs);
+  // groups with work in this CTA: tile 2 x + 1 exists?
+  const int tile1 = NG * (body ? (int)blockIdx.x : (int)blockIdx.x - nbc) + 1;
+  const bool has1 = body ? 2 * tile1 < a.nbody : kHandsPerCta * tile1 < a.nhand;
+  setup(P, sh, smem, body ? bw.tcs : hw.tcs, has1 ? 2u : 1u);
   const int t = P.tid;
   const int r = P.r, blk = r / BLK, c0 = HC * P.h;
   const int tile = NG * (body ? (int)blockIdx.x : (int)blockIdx.x - nbc) + P.g;
@@ -918,6 +930,10 @@ __global__ void __launch_bounds__(NTH, 1) k_decoders_tc(DecodeArgs a, BodyW bw, 
   const int unit = body ? 2 * tile + blk : 0;  // frame index (body tiles)
   const bool valid = body ? (unit < a.nbody && rb < 51) : hs < nslots;
   const int fb0 = 2 * tile;                    // first frame of a body tile
+  if (P.g == 1 && !has1) {                     // no tile for this group
+    teardown(P, body ? 1 : 2);
+    return;
+  }
 
   // feature row of this thread for the body's cross attention
   const int crop = (body && unit < a.nbody ? unit : 0) * a.body_feat_stride;
