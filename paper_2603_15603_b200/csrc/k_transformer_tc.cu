@@ -754,10 +754,8 @@ __global__ void __launch_bounds__(NTH, 1) k_encoder_tc(const float* __restrict__
   const int blk = P.r / BLK, p = P.r % BLK;
   const int crop = 4 * blockIdx.x + 2 * P.g + blk;
   const bool valid = crop < ncrops;
-  if (4 * (int)blockIdx.x + 2 * P.g >= ncrops) {  // no crop for this group
-    teardown(P, 0);
-    return;
-  }
+  // a group without a crop skips to the common teardown (one barrier site)
+  if (4 * (int)blockIdx.x + 2 * P.g < ncrops) {
 
   // patchify (decoder.py:247-248): this thread packs image rows iy in
   // [4h, 4h + 4) of patch p into the K = 192 tile (k = iy*24 + ix*3 + c),
@@ -815,6 +813,7 @@ __global__ void __launch_bounds__(NTH, 1) k_encoder_tc(const float* __restrict__
     }
     flag_nonfinite(nonfinite, bad);
   }
+  }  // group has crops
   teardown(P, 0);
 }
 
@@ -930,10 +929,8 @@ __global__ void __launch_bounds__(NTH, 1) k_decoders_tc(DecodeArgs a, BodyW bw, 
   const int unit = body ? 2 * tile + blk : 0;  // frame index (body tiles)
   const bool valid = body ? (unit < a.nbody && rb < 51) : hs < nslots;
   const int fb0 = 2 * tile;                    // first frame of a body tile
-  if (P.g == 1 && !has1) {                     // no tile for this group
-    teardown(P, body ? 1 : 2);
-    return;
-  }
+  // a group without a tile skips to the common teardown (one barrier site)
+  if (P.g == 0 || has1) {
 
   // feature row of this thread for the body's cross attention
   const int crop = (body && unit < a.nbody ? unit : 0) * a.body_feat_stride;
@@ -1147,6 +1144,7 @@ __global__ void __launch_bounds__(NTH, 1) k_decoders_tc(DecodeArgs a, BodyW bw, 
 #ifdef FSB_PROFILE
   P.prof[8] += clock64() - tfin;
 #endif
+  }  // group has a tile
   teardown(P, body ? 1 : 2);
 }
 
