@@ -346,12 +346,46 @@ constexpr float kScale = 0.25f * 1.4426950408889634f;  // f32(1/sqrt(16)) * log2
 // other block.  Returns 1 / sum (the context is scaled after P.V: 16
 // multiplies instead of 64).  NK: 64 (encoder self-attention, cross
 // attention), 51 (body tokens).  inactive rows write a zero P row.
-template <int NK>
+// ONE_PASS (the encoder, whose register budget allows 64 live scores): one
+// 64-column TMEM read instead of two passes of two 32-column reads.
+template <int NK, bool ONE_PASS = false>
 __device__ float softmax_head(Pipe& P, bool active = true) {
   static_assert(NK > 32 && NK <= 64, "keys per block");
   const int blk = P.r / BLK;
   const uint32_t tcol = T_GEN + 128 * P.h;
   const uint32_t sa = P.lane_addr(tcol + 64 * blk);
+  if constexpr (ONE_PASS) {
+    float s[64];
+    tc::tmem_ld64(sa, s);
+    float m4[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
+#pragma unroll
+    for (int i = 0; i < NK; ++i) m4[i & 3] = fmaxf(m4[i & 3], s[i]);
+    const float nms = -fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])) * kScale;
+    float p4[4] = {0.0f, 0.0f, 0.0f, 0.0f};
+#pragma unroll
+    for (int half = 0; half < 2; ++half) {
+      uint32_t u[16];
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int k = 32 * half + 2 * i;
+        float e0 = 0.0f, e1 = 0.0f;
+        if (k < NK) {
+          e0 = ex2_approx(fmaf(s[k], kScale, nms));
+          p4[k & 3] += e0;
+        }
+        if (k + 1 < NK) {
+          e1 = ex2_approx(fmaf(s[k + 1], kScale, nms));
+          p4[(k + 1) & 3] += e1;
+        }
+        u[i] = active ? tc::pack_bf16(e0, e1) : 0u;
+      }
+      tc::tmem_st16u_nowait(P.lane_addr(tcol + 32 * blk + 16 * half), u);
+    }
+    const uint32_t z[16] = {0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u, 0u};
+    tc::tmem_st16u_nowait(P.lane_addr(tcol + 32 * (1 - blk)), z);
+    tc::tmem_st16u_nowait(P.lane_addr(tcol + 32 * (1 - blk) + 16), z);
+    return active ? 1.0f / ((p4[0] + p4[1]) + (p4[2] + p4[3])) : 0.0f;
+  }
   // two passes over 32-column halves (32 live registers instead of 64):
   // the maximum, then exponentials packed as bf16 over the half just read
   float s[32];
@@ -444,7 +478,7 @@ __device__ float softmax_group4(Pipe& P) {
 // ends up writing context columns [32 h, 32 h + 32) (heads 2h, 2h+1).
 // Several calls with disjoint active rows and different K / V (the hand
 // tiles' cross-attention rounds) assemble one context tile.
-template <int NK, bool G4 = false>
+template <int NK, bool G4 = false, bool ONE_PASS = false>
 __device__ void attention(Pipe& P, bool active, uint32_t ctx_tile = S_A) {
   const uint32_t sq = P.sbase + S_Q, sk = P.sbase + S_K, sv = P.sbase + S_VT;
   const uint32_t id_s = tc::idesc_bf16(128, 128), id_o = tc::idesc_bf16(128, 16);
@@ -460,7 +494,7 @@ __device__ void attention(Pipe& P, bool active, uint32_t ctx_tile = S_A) {
     if constexpr (G4)
       inv = softmax_group4(P);
     else
-      inv = softmax_head<NK>(P, active);
+      inv = softmax_head<NK, ONE_PASS>(P, active);
     tc::tmem_wait_st();
     P.before_issue();
     if (P.tid == 0)
@@ -502,7 +536,7 @@ __device__ void out_proj(Pipe& P, const float* bo, float* x, bool valid) {
 
 // self attention: x += MHA(LN(a)), a = x + pos  (decoder.py:214-218)
 // (a == nullptr: a is in the fp32 row tile, written by the caller)
-template <int NK, bool G4 = false>
+template <int NK, bool G4 = false, bool ONE_PASS = false>
 __device__ void self_attn(Pipe& P, const float* prm, float* x, const float* a, bool valid) {
 #ifdef FSB_PROFILE
   long long q0 = clock64();
@@ -537,7 +571,7 @@ __device__ void self_attn(Pipe& P, const float* prm, float* x, const float* a, b
   long long q3 = clock64();
   P.prof[14] += q3 - q2;
 #endif
-  attention<NK, G4>(P, true);
+  attention<NK, G4, ONE_PASS>(P, true);
 #ifdef FSB_PROFILE
   P.prof[15] += clock64() - q3;
 #endif
@@ -798,7 +832,7 @@ __global__ void __launch_bounds__(NTH, 1) k_encoder_tc(const float* __restrict__
     const float* prm = P.pacquire();
     P.sync();  // every thread of the group is past layer l - 1
     P.prelease();
-    self_attn<BLK>(P, prm, x, x, valid);
+    self_attn<BLK, false, true>(P, prm, x, x, valid);
     mlp(P, prm, x, valid);
   }
   float y[HC];
