@@ -1,3 +1,4 @@
+#include <stdlib.h>
 // C ABI (include/fsb_b200.h): context, model upload/repacking, workspace,
 // stage entry points and the CUDA-graph replay of the whole frame batch.
 #include <cuda_runtime.h>
@@ -1122,8 +1123,14 @@ static int skin_project_impl(fsb_ctx* c, const float* params, int B, float* v_mh
   FSB_CUDA(c, launch_fk(params, FSB_PARAM_DIM, B, mhr.joints_rest, nullptr, c->w_rel, st));
   if (v_mhr) FSB_CUDA(c, launch_lbs(mhr, c->w_rel, params, FSB_PARAM_DIM, B, v_mhr, c->d_flag, st));
   const bool tc = mlp_tc(c, precision);
-  FSB_CUDA(c, launch_proj_inputs(mhr, c->proj, c->w_rel, params, FSB_PARAM_DIM, B, c->w_x, !tc,
-                                 tc ? c->w_xb : nullptr, c->w_psum, st));
+  if (v_mhr && getenv("FSB_PROJ_RESKIN") == nullptr) {
+    // V_mhr was just written: bridge its corner vertices (what the reference
+    // projects, projection.py:447-465) instead of re-skinning them
+    FSB_CUDA(c, launch_proj_inputs_v(v_mhr, mhr.nv, c->proj, B, c->w_x, !tc, tc ? c->w_xb : nullptr, c->w_psum, st));
+  } else {
+    FSB_CUDA(c, launch_proj_inputs(mhr, c->proj, c->w_rel, params, FSB_PARAM_DIM, B, c->w_x, !tc,
+                                   tc ? c->w_xb : nullptr, c->w_psum, st));
+  }
   c->launches += 3 + (v_mhr != nullptr);
   int rc = run_mlp(c, B, theta, precision, st);
   if (rc) return rc;

@@ -393,19 +393,17 @@ constexpr int kProjMeshes = 8;
 
 template <int NZ>
 __global__ void __launch_bounds__(256) k_proj_inputs(TemplateDev t, ProjectorDev p, const float* __restrict__ rel,
-                                                     const float* __restrict__ poses, int ld_pose, int B,
+                                                     const float* __restrict__ poses, int ld_pose, int B, int gpc,
                                                      float* __restrict__ sub, float* __restrict__ psum) {
+  // gpc groups of kProjMeshes meshes per CTA (large batches): the corner
+  // records stay in registers across the groups
   constexpr int RS = vertex_record_floats(NZ);
   __shared__ __align__(16) float A[kProjMeshes][FSB_NJ * 12];
   __shared__ float shp[kProjMeshes][10];
   __shared__ float v0[kProjMeshes][3];
   __shared__ float rec0[RS];  // template record of vertex 0
   __shared__ float red[kProjMeshes][32][3];
-  const int m0 = blockIdx.y * kProjMeshes, nm = min(kProjMeshes, B - m0);
   const int chunk = blockIdx.x, tid = threadIdx.x;
-  for (int i = tid; i < nm * FSB_NJ * 12; i += blockDim.x)
-    (&A[0][0])[i] = rel[(int64_t)m0 * FSB_NJ * 12 + i];
-  for (int i = tid; i < nm * 10; i += blockDim.x) shp[i / 10][i % 10] = poses[(int64_t)(m0 + i / 10) * ld_pose + 66 + i % 10];
   for (int i = tid; i < RS; i += blockDim.x) rec0[i] = __ldg(t.rec + i);
   const int per = (p.n_sub + kProjChunks - 1) / kProjChunks;
   const int i = chunk * per + tid;
@@ -418,44 +416,54 @@ __global__ void __launch_bounds__(256) k_proj_inputs(TemplateDev t, ProjectorDev
       vt[c].load(t, p.corners[3 * i + c]);
       wc[c] = p.bw[3 * i + c];
     }
-  __syncthreads();
-  if (tid < nm) {
-    VertexTmpl<NZ> r0;
-    r0.unpack(rec0);
-    r0.apply(A[tid], shp[tid], v0[tid]);
-  }
-  __syncthreads();
-  // per-mesh sums are reduced after the loop (independent shuffle chains)
-  float acc[kProjMeshes][3];
-#pragma unroll
-  for (int m = 0; m < kProjMeshes; ++m) {
-    acc[m][0] = acc[m][1] = acc[m][2] = 0.0f;
-    if (act && m < nm) {
-#pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        float o[3];
-        vt[c].apply(A[m], shp[m], o);
-#pragma unroll
-        for (int a = 0; a < 3; ++a) acc[m][a] = fmaf(wc[c], o[a] - v0[m][a], acc[m][a]);
-      }
-#pragma unroll
-      for (int a = 0; a < 3; ++a) sub[((int64_t)(m0 + m) * p.n_sub + i) * 3 + a] = acc[m][a];
-    }
-  }
   const int warp = tid / 32, lane = tid % 32;
-#pragma unroll
-  for (int m = 0; m < kProjMeshes; ++m)
-#pragma unroll
-    for (int a = 0; a < 3; ++a) {
-      const float r = warp_sum(acc[m][a]);
-      if (lane == 0) red[m][warp][a] = r;
+#pragma unroll 1
+  for (int gi = 0; gi < gpc; ++gi) {
+    const int m0 = ((int)blockIdx.y * gpc + gi) * kProjMeshes;
+    if (m0 >= B) break;  // CTA-uniform
+    const int nm = min(kProjMeshes, B - m0);
+    if (gi > 0) __syncthreads();  // the previous group's A / shp / red reads are done
+    for (int k = tid; k < nm * FSB_NJ * 12; k += blockDim.x) (&A[0][0])[k] = rel[(int64_t)m0 * FSB_NJ * 12 + k];
+    for (int k = tid; k < nm * 10; k += blockDim.x)
+      shp[k / 10][k % 10] = poses[(int64_t)(m0 + k / 10) * ld_pose + 66 + k % 10];
+    __syncthreads();
+    if (tid < nm) {
+      VertexTmpl<NZ> r0;
+      r0.unpack(rec0);
+      r0.apply(A[tid], shp[tid], v0[tid]);
     }
-  __syncthreads();
-  if (tid < 3 * nm) {
-    const int m = tid / 3, a = tid % 3;
-    float tot = 0.0f;
-    for (int w = 0; w < (int)blockDim.x / 32; ++w) tot += red[m][w][a];
-    psum[((int64_t)(m0 + m) * kProjChunks + chunk) * 3 + a] = tot;
+    __syncthreads();
+    // per-mesh sums are reduced after the loop (independent shuffle chains)
+    float acc[kProjMeshes][3];
+#pragma unroll
+    for (int m = 0; m < kProjMeshes; ++m) {
+      acc[m][0] = acc[m][1] = acc[m][2] = 0.0f;
+      if (act && m < nm) {
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          float o[3];
+          vt[c].apply(A[m], shp[m], o);
+#pragma unroll
+          for (int a = 0; a < 3; ++a) acc[m][a] = fmaf(wc[c], o[a] - v0[m][a], acc[m][a]);
+        }
+#pragma unroll
+        for (int a = 0; a < 3; ++a) sub[((int64_t)(m0 + m) * p.n_sub + i) * 3 + a] = acc[m][a];
+      }
+    }
+#pragma unroll
+    for (int m = 0; m < kProjMeshes; ++m)
+#pragma unroll
+      for (int a = 0; a < 3; ++a) {
+        const float r = warp_sum(acc[m][a]);
+        if (lane == 0) red[m][warp][a] = r;
+      }
+    __syncthreads();
+    if (tid < 3 * nm) {
+      const int m = tid / 3, a = tid % 3;
+      float tot = 0.0f;
+      for (int w = 0; w < (int)blockDim.x / 32; ++w) tot += red[m][w][a];
+      psum[((int64_t)(m0 + m) * kProjChunks + chunk) * 3 + a] = tot;
+    }
   }
 }
 
@@ -602,11 +610,16 @@ cudaError_t launch_proj_inputs(const TemplateDev& t, const ProjectorDev& p, cons
   if (B == 0) return cudaSuccess;
   const int nt = proj_threads(p);
   if (nt > 256) return cudaErrorInvalidValue;  // n_sub <= 2048 (launch bounds)
-  const dim3 grid(kProjChunks, (B + kProjMeshes - 1) / kProjMeshes);
+  // small batches: one group of kProjMeshes per CTA (latency); large ones
+  // (C3): 8 groups per CTA so each target's corner records are read once per
+  // 64 meshes
+  const int groups = (B + kProjMeshes - 1) / kProjMeshes;
+  const int gpc = B >= 1024 ? 8 : 1;
+  const dim3 grid(kProjChunks, (groups + gpc - 1) / gpc);
   switch (t.nnz) {
-    case 2: k_proj_inputs<2><<<grid, nt, 0, st>>>(t, p, rel, poses, ld_pose, B, sub, psum); break;
-    case 4: k_proj_inputs<4><<<grid, nt, 0, st>>>(t, p, rel, poses, ld_pose, B, sub, psum); break;
-    case 8: k_proj_inputs<8><<<grid, nt, 0, st>>>(t, p, rel, poses, ld_pose, B, sub, psum); break;
+    case 2: k_proj_inputs<2><<<grid, nt, 0, st>>>(t, p, rel, poses, ld_pose, B, gpc, sub, psum); break;
+    case 4: k_proj_inputs<4><<<grid, nt, 0, st>>>(t, p, rel, poses, ld_pose, B, gpc, sub, psum); break;
+    case 8: k_proj_inputs<8><<<grid, nt, 0, st>>>(t, p, rel, poses, ld_pose, B, gpc, sub, psum); break;
     default: return cudaErrorInvalidValue;
   }
   cudaError_t e = cudaGetLastError();
