@@ -1111,7 +1111,7 @@ int fsb_project_vertices(fsb_ctx* c, const float* v_mhr, int B, int nv, float* t
   if (rc) return rc;
   const bool tc = mlp_tc(c, precision);
   FSB_CUDA(c, launch_proj_inputs_v(v_mhr, nv, c->proj, B, c->w_x, !tc, tc ? c->w_xb : nullptr, c->w_psum, st));
-  c->launches += 2 * (B > 0);
+  c->launches += B > 0;  // bridge + centre in one kernel
   return run_mlp(c, B, theta, precision, st);
 }
 
@@ -1127,11 +1127,12 @@ static int skin_project_impl(fsb_ctx* c, const float* params, int B, float* v_mh
     // V_mhr was just written: bridge its corner vertices (what the reference
     // projects, projection.py:447-465) instead of re-skinning them
     FSB_CUDA(c, launch_proj_inputs_v(v_mhr, mhr.nv, c->proj, B, c->w_x, !tc, tc ? c->w_xb : nullptr, c->w_psum, st));
+    c->launches += 3;  // FK, LBS, bridge + centre
   } else {
     FSB_CUDA(c, launch_proj_inputs(mhr, c->proj, c->w_rel, params, FSB_PARAM_DIM, B, c->w_x, !tc,
                                    tc ? c->w_xb : nullptr, c->w_psum, st));
+    c->launches += 3 + (v_mhr != nullptr);  // FK, (LBS), re-skinned inputs, centre
   }
-  c->launches += 3 + (v_mhr != nullptr);
   int rc = run_mlp(c, B, theta, precision, st);
   if (rc) return rc;
   FSB_CUDA(c, launch_fk(theta, FSB_PARAM_DIM, B, c->tmpl[FSB_SMPL].joints_rest, j_smpl, v_smpl ? c->w_rel2 : nullptr,

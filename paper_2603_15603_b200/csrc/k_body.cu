@@ -292,76 +292,17 @@ __global__ void __launch_bounds__(kLbsThreads, FSB_LBS_MIN_BLOCKS) k_lbs(Templat
 // ---------------------------------------------------------------------------
 // projector input (projection.py:447-465): centre the source mesh on vertex
 // 0, bridge the subsampled targets through their three corners, remove the
-// subsample centroid.  The needed MHR vertices are re-skinned here from the
-// L2-resident template instead of re-read from the V_mhr stream.
-// One CTA per mesh.
+// subsample centroid.  From given vertices (V_mhr just written, or
+// project_batch's input): k_proj_inputs_vc, one CTA per mesh.  Without V_mhr
+// the needed MHR vertices are re-skinned from the L2-resident template:
+// k_proj_inputs + k_proj_center.
 // ---------------------------------------------------------------------------
 
-template <int NZ>
-__device__ __forceinline__ void skin_one(const TemplateDev& t, int v, const float* A, const float* shp, float o[3]) {
-  VertexTmpl<NZ> vt;
-  vt.load(t, v);
-  vt.apply(A, shp, o);
-}
-
-// vertex sources for the projector input: re-skin from the template, or read
-// a caller-supplied vertex tensor (project_batch on arbitrary meshes)
-template <int NZ>
-struct SkinSource {
-  TemplateDev t;
-  const float* A;
-  const float* shp;
-  __device__ void get(int v, float o[3]) const { skin_one<NZ>(t, v, A, shp, o); }
-};
-struct VertexSource {
-  const float* V;  // (nv, 3) of this mesh
-  __device__ void get(int v, float o[3]) const {
-    o[0] = V[3 * v]; o[1] = V[3 * v + 1]; o[2] = V[3 * v + 2];
-  }
-};
-
-// The targets of one mesh are spread over kProjChunks CTAs (one target per
-// thread); each CTA writes its bridged, vertex-0-centred targets and its
-// partial sum, and k_proj_center removes the centroid (partials added in
-// chunk order, so the result does not depend on the batch).
+// Re-skinned path: the targets of one mesh are spread over kProjChunks CTAs
+// (one target per thread); each CTA writes its bridged, vertex-0-centred
+// targets and its partial sum, and k_proj_center removes the centroid
+// (partials added in chunk order, so the result does not depend on the batch).
 constexpr int kProjChunks = 8;
-
-template <class Src>
-__device__ void proj_inputs_cta(const Src& src, const ProjectorDev& p, float* sm, int b, int chunk,
-                                float* __restrict__ sub, float* __restrict__ psum) {
-  float* v0 = sm + 276;   // 3
-  float* red = sm + 280;  // 3 x warps
-  const int tid = threadIdx.x;
-  const int per = (p.n_sub + kProjChunks - 1) / kProjChunks;
-  const int i = chunk * per + tid;
-  if (tid == 0) src.get(0, v0);
-  __syncthreads();
-  float acc[3] = {0.0f, 0.0f, 0.0f};
-  if (tid < per && i < p.n_sub) {
-#pragma unroll
-    for (int c = 0; c < 3; ++c) {
-      float o[3];
-      src.get(p.corners[3 * i + c], o);
-      const float wc = p.bw[3 * i + c];
-#pragma unroll
-      for (int a = 0; a < 3; ++a) acc[a] = fmaf(wc, o[a] - v0[a], acc[a]);
-    }
-#pragma unroll
-    for (int a = 0; a < 3; ++a) sub[((int64_t)b * p.n_sub + i) * 3 + a] = acc[a];
-  }
-  const int warp = tid / 32, lane = tid % 32;
-#pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    const float r = warp_sum(acc[a]);
-    if (lane == 0) red[3 * warp + a] = r;
-  }
-  __syncthreads();
-  if (tid < 3) {
-    float tot = 0.0f;
-    for (int w = 0; w < (int)blockDim.x / 32; ++w) tot += red[3 * w + tid];
-    psum[((int64_t)b * kProjChunks + chunk) * 3 + tid] = tot;
-  }
-}
 
 // x = sub - centroid (projection.py:464), as fp32 (in place) and/or as the
 // bf16 A-tile image of the tensor-core MLP (k_mlp_tc.cu)
@@ -388,7 +329,7 @@ __global__ void k_proj_center(float* __restrict__ sub, const float* __restrict__
 // and applied to every mesh of the group (the transforms and shape
 // coefficients of the group are staged in shared memory), so a batch of 32
 // meshes is 32 CTAs instead of 256.  Same per-target arithmetic and the same
-// per-chunk partial-sum order as proj_inputs_cta.
+// per-chunk partial-sum order as k_proj_center expects.
 constexpr int kProjMeshes = 8;
 
 template <int NZ>
@@ -467,11 +408,70 @@ __global__ void __launch_bounds__(256) k_proj_inputs(TemplateDev t, ProjectorDev
   }
 }
 
-__global__ void __launch_bounds__(256) k_proj_inputs_v(const float* __restrict__ V, int nv, ProjectorDev p,
-                                                       float* __restrict__ sub, float* __restrict__ psum) {
-  __shared__ __align__(16) float sm[336];
-  const int b = blockIdx.x;
-  proj_inputs_cta(VertexSource{V + (int64_t)b * nv * 3}, p, sm, b, blockIdx.y, sub, psum);
+// Projector input of one mesh per CTA from its skinned vertices
+// (projection.py:447-465): centre on vertex 0, bridge each target through
+// its three corners, remove the subsample centroid, and write x as fp32
+// and/or straight into the bf16 A-tile image of the tensor-core MLP -- the
+// centroid is a CTA reduction (fixed order, so a mesh gives the same bits
+// in any batch), no partial-sum buffer and no second kernel.
+constexpr int kProjVcThreads = 512, kProjVcPer = 4;  // targets per thread (n_sub <= 2048)
+
+__global__ void __launch_bounds__(kProjVcThreads) k_proj_inputs_vc(const float* __restrict__ V, int nv,
+                                                                   ProjectorDev p, float* __restrict__ x32,
+                                                                   __nv_bfloat16* __restrict__ xb) {
+  __shared__ float red[kProjVcThreads / 32][3];
+  __shared__ float cen[3];
+  const int b = blockIdx.x, tid = threadIdx.x;
+  const float* Vb = V + (int64_t)b * nv * 3;
+  const float o0 = __ldg(Vb), o1 = __ldg(Vb + 1), o2 = __ldg(Vb + 2);
+  float acc[kProjVcPer][3];
+  float part[3] = {0.0f, 0.0f, 0.0f};
+#pragma unroll
+  for (int q = 0; q < kProjVcPer; ++q) {
+    const int t = tid + q * kProjVcThreads;
+    acc[q][0] = acc[q][1] = acc[q][2] = 0.0f;
+    if (t < p.n_sub) {
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const float* vc = Vb + 3 * (int64_t)p.corners[3 * t + c];
+        const float wc = p.bw[3 * t + c];
+        acc[q][0] = fmaf(wc, __ldg(vc) - o0, acc[q][0]);
+        acc[q][1] = fmaf(wc, __ldg(vc + 1) - o1, acc[q][1]);
+        acc[q][2] = fmaf(wc, __ldg(vc + 2) - o2, acc[q][2]);
+      }
+#pragma unroll
+      for (int a = 0; a < 3; ++a) part[a] += acc[q][a];
+    }
+  }
+  const int warp = tid / 32, lane = tid % 32;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const float r = warp_sum(part[a]);
+    if (lane == 0) red[warp][a] = r;
+  }
+  __syncthreads();
+  if (tid < 3) {
+    float sum = 0.0f;
+    for (int w = 0; w < kProjVcThreads / 32; ++w) sum += red[w][tid];
+    cen[tid] = sum / (float)p.n_sub;
+  }
+  __syncthreads();
+  const int K = 3 * p.n_sub, KT = (K + 127) / 128;
+#pragma unroll
+  for (int q = 0; q < kProjVcPer; ++q) {
+    const int t = tid + q * kProjVcThreads;
+    if (t >= p.n_sub) break;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const float v = acc[q][a] - cen[a];
+      const int k = 3 * t + a;
+      if (x32 != nullptr) x32[(int64_t)b * K + k] = v;
+      if (xb != nullptr) {
+        const size_t tile = (size_t)(b >> 7) * KT + (k >> 7);
+        xb[tile * 16384 + tc::kmajor_off(b & 127, k & 127, 128) / 2] = __float2bfloat16_rn(v);
+      }
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -629,11 +629,10 @@ cudaError_t launch_proj_inputs(const TemplateDev& t, const ProjectorDev& p, cons
 cudaError_t launch_proj_inputs_v(const float* V, int nv, const ProjectorDev& p, int B, float* sub, bool f32,
                                  __nv_bfloat16* xb, float* psum, cudaStream_t st) {
   if (B == 0) return cudaSuccess;
-  const int nt = proj_threads(p);
-  if (nt > 256) return cudaErrorInvalidValue;  // n_sub <= 2048 (launch bounds)
-  k_proj_inputs_v<<<dim3(B, kProjChunks), nt, 0, st>>>(V, nv, p, sub, psum);
-  cudaError_t e = cudaGetLastError();
-  return e != cudaSuccess ? e : launch_proj_center(p, B, sub, psum, f32, xb, st);
+  if (p.n_sub > kProjVcThreads * kProjVcPer) return cudaErrorInvalidValue;
+  (void)psum;
+  k_proj_inputs_vc<<<B, kProjVcThreads, 0, st>>>(V, nv, p, f32 ? sub : nullptr, xb);
+  return cudaGetLastError();
 }
 
 // number of K chunks of a layer: a function of K only (batch independence);
