@@ -366,7 +366,10 @@ def main():
                                                           rank, args.stream_frames)
 
     # -- per-stage attribution (graphs off, CUDA events between stages) -------
-    stage_ms = attribute_stages(torch, pipe, ctx, images[:B], kps[:B], outs, cfg, reps=20)
+    stage_sat = {}
+    stage_ms = attribute_stages(torch, pipe, ctx, images[:B], kps[:B], outs, cfg, reps=20, saturated=16,
+                                saturated_out=stage_sat)
+    stage_sat["sum"] = round(sum(stage_sat.values()), 2)
 
     # -- p50 single-frame latency (B = 1 graph replay) -------------------------
     lat = frame_latency(torch, pipe, images, kps, cfg, reps=200)
@@ -417,7 +420,9 @@ def main():
         "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "e2e_full_frame_copy": e2e_copy,
         "gpu_launches": launches,
         "clocks": clk.summary(), "p50_frame_latency_ms": lat["p50_ms"], "frame_latency": lat,
-        "stage_ms": stage_ms, "c3": c3, "c4": c4, "c5": c5, "conversion": conv,
+        "stage_ms": stage_ms,
+        "stage_saturated_us_per_batch": stage_sat,  # 16 concurrent copies of each stage alone
+        "c3": c3, "c4": c4, "c5": c5, "conversion": conv,
     }
     print(json.dumps(line), flush=True)
     if dist is not None:
@@ -563,7 +568,7 @@ def c4_microbench(torch, crops, reps, layers=24):
             "algorithmic_flop_per_batch": crops * FLOP_C4_CROP}
 
 
-def attribute_stages(torch, pipe, ctx, img, kp, outs, cfg, reps):
+def attribute_stages(torch, pipe, ctx, img, kp, outs, cfg, reps, saturated=None, saturated_out=None):
     """Average device time of each stage kernel on one batch.  Each stage's
     launches are captured `reps` times into its own CUDA graph and the graph
     is replayed between CUDA events, so the numbers are device time, not the
@@ -594,12 +599,12 @@ def attribute_stages(torch, pipe, ctx, img, kp, outs, cfg, reps):
     def k4a():
         ctx.check(lib.fsb_skin(h, 0, rt.ptr(outs["merged"]), B, rt.ptr(outs["v_mhr"]), ctx.stream))
 
-    def k4b():
-        ctx.check(lib.fsb_skin_project(h, rt.ptr(outs["merged"]), B, None, rt.ptr(outs["theta"]),
-                                       rt.ptr(outs["j_smpl"]), None, prec, ctx.stream))
+    def k4b():  # projector input bridged from V_mhr + the MLP, as in the frame path
+        ctx.check(lib.fsb_project_vertices(h, rt.ptr(outs["v_mhr"]), B, pipe.mhr.num_vertices, rt.ptr(outs["theta"]),
+                                           prec, ctx.stream))
 
     stages = [("k1_boxes_crops", k1), ("k2_encoder", k2), ("k3_decoders", k3), ("k4_fk_lbs", k4a),
-              ("k4_proj_mlp_smplfk", k4b)]
+              ("k4_proj_mlp", k4b)]
     for _, fn in stages:  # eager warm-up (workspace allocation happens here)
         fn()
     torch.cuda.synchronize()
@@ -620,6 +625,32 @@ def attribute_stages(torch, pipe, ctx, img, kp, outs, cfg, reps):
         e1.record()
         torch.cuda.synchronize()
         out[name] = float(e0.elapsed_time(e1) / (3 * reps))
+    if saturated is not None:
+        # the same stages with `saturated` concurrent copies (forked streams in
+        # one graph): device time one batch of the stage costs when the GPU is
+        # kept full with it -- its share of the SM budget the pipeline runs on
+        n = saturated
+        for name, fn in stages:
+            branches = [torch.cuda.Stream(device=dev) for _ in range(n)]
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.stream(side):
+                with torch.cuda.graph(g, stream=side, capture_error_mode="relaxed"):
+                    for q in branches:
+                        q.wait_stream(side)
+                        with torch.cuda.stream(q):
+                            for _ in range(4):
+                                fn()
+                    for q in branches:
+                        side.wait_stream(q)
+            g.replay()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(3):
+                g.replay()
+            e1.record()
+            torch.cuda.synchronize()
+            saturated_out[name] = round(float(1e3 * e0.elapsed_time(e1) / (3 * 4 * n)), 2)
     return out
 
 
@@ -637,7 +668,7 @@ def roofline(stage_ms, B):
         "k2_encoder": ("tensor", FLOP_ENC_FRAME * B),
         "k3_decoders": ("tensor", FLOP_DEC_FRAME * B),
         "k4_fk_lbs": ("hbm", BYTES_LBS_MESH * B),
-        "k4_proj_mlp_smplfk": ("tensor", FLOP_MLP_MESH * B),
+        "k4_proj_mlp": ("tensor", FLOP_MLP_MESH * B),
     }
     dom = max(stage_ms, key=stage_ms.get)
     bound, amount = work[dom]
