@@ -385,3 +385,33 @@ def test_denoise_bitexact_vs_reference_golden(torch):
     assert np.array_equal(pj.denoise(w, g["x"][3]), g["out3"])
     with pytest.raises(ValueError):
         pj.denoise(w, g["x"][:, :60])
+
+
+@pytest.mark.parametrize("prec,n,tol", [("fp32", 40, 1e-4), ("bf16", 40, 2e-2), ("fp32", 1030, 1e-4)])
+def test_skin_project_with_and_without_vmhr(torch, pipe, full_models, full_projector, prec, n, tol):
+    """fsb_skin_project bridges the projector input from V_mhr when it is
+    produced and re-skins the corner vertices otherwise (one CTA per 8-mesh
+    group, 8 groups per CTA from 1024 meshes); both give the same theta and
+    SMPL joints within the precision's tolerance, and match the oracle."""
+    from paper_2603_15603_b200 import runtime as rt
+
+    mhr, smpl, gt = full_models
+    ctx = pipe.context()
+    ctx.reserve(n)
+    poses = torch.from_numpy(_c3_poses(n)).cuda()
+    nv = mhr.num_vertices
+    v = torch.empty((n, nv, 3), dtype=torch.float32, device="cuda")
+    th = [torch.empty((n, 76), dtype=torch.float32, device="cuda") for _ in range(2)]
+    jj = [torch.empty((n, 22, 3), dtype=torch.float32, device="cuda") for _ in range(2)]
+    p = rt.PRECISIONS[prec]
+    ctx.check(ctx.lib.fsb_skin_project(ctx.h, rt.ptr(poses), n, rt.ptr(v), rt.ptr(th[0]), rt.ptr(jj[0]), None, p,
+                                       ctx.stream))
+    ctx.check(ctx.lib.fsb_skin_project(ctx.h, rt.ptr(poses), n, None, rt.ptr(th[1]), rt.ptr(jj[1]), None, p,
+                                       ctx.stream))
+    torch.cuda.synchronize()
+    t0, t1 = th[0].cpu().numpy(), th[1].cpu().numpy()
+    assert rel_err(t1, t0) <= tol
+    assert rel_err(jj[1].cpu().numpy(), jj[0].cpu().numpy()) <= tol
+    k = min(n, 8)
+    want = orc.project_batch(orc.skin_batch(mhr, _c3_poses(k)), gt.corners, gt.weights, projector_dict(full_projector))
+    assert rel_err(t0[:k], want) <= (FP32_TOL if prec == "fp32" else 5e-2)
