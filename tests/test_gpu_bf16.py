@@ -126,3 +126,23 @@ def test_frame_batch_bf16_position_independent(setup):
         if j >= len(frames):
             for k in ("merged", "theta", "j_smpl", "v_mhr"):
                 assert np.array_equal(res[k][j], res[k][i]), (j, i, k)
+
+
+def test_decode_hand_bf16_ragged(setup, dec_weights):
+    """Seven hands: a full 4-hand tile and a 3-hand tile whose second
+    cross-attention round has one slot (odd slot count), in one CTA."""
+    from paper_2603_15603_b200 import decoder as dc
+
+    pipe, frames = setup
+    cfg = dc.DecoderConfig()
+    feats = []
+    for f in frames[:4]:
+        _, _, _, crops = orc.frame_crops(f[0], f[1], 64)
+        feats.append(orc.encode(dec_weights, cfg, crops)[1:3])
+    feats = np.concatenate(feats)[:7]
+    got = pipe.decoder.decode_hand(feats, (), precision="bf16")
+    assert rel_err(got, orc.decode_hand(dec_weights, cfg, feats, ())) <= 5e-2
+    # each hand alone gives the same bits as in the batch
+    for i in (0, 3, 6):
+        one = pipe.decoder.decode_hand(feats[i:i + 1], (), precision="bf16")
+        assert np.array_equal(one[0], got[i]), i
