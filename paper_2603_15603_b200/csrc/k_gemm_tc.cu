@@ -256,18 +256,22 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 #ifndef GEMM2_EPI_BUFS
 #define GEMM2_EPI_BUFS 4
 #endif
+#ifndef GEMM2_EPI_WARPS
+#define GEMM2_EPI_WARPS 4
+#endif
 namespace {
 constexpr int STAGES2 = GEMM2_STAGES, BN2 = 256, NBUF2 = GEMM2_EPI_BUFS;  // NBUF2: staging buffers per epilogue warp
+constexpr int EPI_WARPS2 = GEMM2_EPI_WARPS, GEMM_THREADS2 = 64 + 32 * EPI_WARPS2;
 }
 
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS2, 1)
     k_gemm_tc2(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                const __grid_constant__ CUtensorMap tmC, int M, int N, int K, GemmEpi epi) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   constexpr uint32_t A_BYTES = BM * BK * 2, B_BYTES = (BN2 / 2) * BK * 2, STAGE_BYTES = A_BYTES + B_BYTES;
   constexpr uint32_t TMEM_COLS = 2 * BN2;
-  __shared__ uint64_t full[STAGES2], empty[STAGES2], acc_full[2], acc_empty[2], xbar[NBUF2 * EPI_WARPS];
+  __shared__ uint64_t full[STAGES2], empty[STAGES2], acc_full[2], acc_empty[2], xbar[NBUF2 * EPI_WARPS2];
   __shared__ uint32_t tmem_base;
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const uint32_t rank = tc::cluster_rank();
@@ -283,9 +287,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
     }
     for (int b = 0; b < 2; ++b) {
       tc::mbar_init(&acc_full[b], 1);
-      tc::mbar_init(&acc_empty[b], 2 * EPI_WARPS);
+      tc::mbar_init(&acc_empty[b], 2 * EPI_WARPS2);
     }
-    for (int i = 0; i < NBUF2 * EPI_WARPS; ++i) tc::mbar_init(&xbar[i], 1);
+    for (int i = 0; i < NBUF2 * EPI_WARPS2; ++i) tc::mbar_init(&xbar[i], 1);
     tc::mbar_fence_init();
     tc::prefetch_tmap(&tmA);
     tc::prefetch_tmap(&tmB);
@@ -347,7 +351,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(GEMM_THREADS, 1)
   } else if (warp >= 2) {
     // epilogue on this CTA's 128 rows (as in k_gemm_tc)
     const int ew = warp - 2, quad = warp % 4, half = ew / 4;
-    constexpr int HALF = BN2 / (EPI_WARPS / 4);
+    constexpr int HALF = BN2 / (EPI_WARPS2 / 4);
     uint8_t* stg = smem + STAGES2 * STAGE_BYTES + ew * NBUF2 * EPI_BUF;
     const bool f32 = epi.kind == EPI_RESID_F32 || epi.kind == EPI_EMBED_F32;
     const bool resid = epi.kind == EPI_RESID_F32;
@@ -503,7 +507,7 @@ static constexpr size_t gemm_smem() {
 }
 
 static constexpr size_t gemm2_smem() {
-  return (size_t)STAGES2 * (BM * BK * 2 + (BN2 / 2) * BK * 2) + (size_t)EPI_WARPS * NBUF2 * EPI_BUF + 1024;
+  return (size_t)STAGES2 * (BM * BK * 2 + (BN2 / 2) * BK * 2) + (size_t)EPI_WARPS2 * NBUF2 * EPI_BUF + 1024;
 }
 
 cudaError_t init_attrs_gemm_tc() {
@@ -556,7 +560,7 @@ cudaError_t launch_gemm_tc(const __nv_bfloat16* A, int lda, const __nv_bfloat16*
   if (pair) {  // persistent clusters of two CTAs, one 256 x 256 tile at a time
     const int64_t tiles = (int64_t)(N / BN2) * ((M + 2 * BM - 1) / (2 * BM));
     const int64_t ncl = tiles < sms / 2 ? tiles : sms / 2;
-    k_gemm_tc2<<<dim3((unsigned)(2 * ncl)), GEMM_THREADS, gemm2_smem(), st>>>(ta, tb, tc_, M, N, K, epi);
+    k_gemm_tc2<<<dim3((unsigned)(2 * ncl)), GEMM_THREADS2, gemm2_smem(), st>>>(ta, tb, tc_, M, N, K, epi);
     return cudaGetLastError();
   }
   const int64_t tiles = (int64_t)((N + BN - 1) / BN) * ((M + BM - 1) / BM);
