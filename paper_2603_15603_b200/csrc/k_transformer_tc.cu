@@ -869,7 +869,7 @@ struct BodyAux {  // fp32 scratch per body tile
 // 64 (i % 2) + 4 (i / 2) + token, so the two slots of a cross-attention
 // round (2c, 2c + 1) use key blocks 0 and 1 and every warp sees one.
 #ifndef FSB_HANDS_PER_CTA
-#define FSB_HANDS_PER_CTA 4
+#define FSB_HANDS_PER_CTA 8  // 2 / 4 / 8 / 16 measured: DESIGN.md §4
 #endif
 constexpr int kHandsPerCta = FSB_HANDS_PER_CTA;  // per tile
 static_assert(kHandsPerCta >= 2 && kHandsPerCta <= 16 && kHandsPerCta % 2 == 0, "hand slots per tile");

@@ -118,20 +118,24 @@ __global__ void k_layernorm(const float* __restrict__ x, int rows, int D, const 
 // are corrected in TMEM only when the max grows by more than 2^8 (P stays
 // <= 256; O / l is exact).  Keys past T are masked to -inf; query rows
 // past T compute on the next crop's rows and are not stored.
-constexpr int FA_THREADS = 160, FA_KC = 64, FA_KR = 2, FA_VR = 3;
+#ifndef FSB_FA_PB
+#define FSB_FA_PB 1  // P tiles in shared memory: 2 lets softmax(j) run under P(j-1).V (2 CTAs per SM)
+#endif
+constexpr int FA_THREADS = 160, FA_KC = 64, FA_KR = 2, FA_VR = 3, FA_PB = FSB_FA_PB;
 constexpr uint32_t FA_Q = 0;                      // 16 KB
 constexpr uint32_t FA_K = 16384;                  // FA_KR x 8 KB
 constexpr uint32_t FA_V = FA_K + FA_KR * 8192;    // FA_VR x 8 KB
-constexpr uint32_t FA_P = FA_V + FA_VR * 8192;    // 16 KB
-constexpr uint32_t FA_SMEM = FA_P + 16384;
+constexpr uint32_t FA_P = FA_V + FA_VR * 8192;    // FA_PB x 16 KB
+constexpr uint32_t FA_SMEM = FA_P + FA_PB * 16384;
 constexpr float FA_RESCALE = 8.0f;  // log2 units
+static_assert(FA_PB == 1 || FA_PB == 2, "P buffers");
 
-__global__ void __launch_bounds__(FA_THREADS, 3)
+__global__ void __launch_bounds__(FA_THREADS, FA_PB == 1 ? 3 : 2)
     k_attn_tc(const __grid_constant__ CUtensorMap tmq, const __grid_constant__ CUtensorMap tmkv, int T, int D,
               float scale, __nv_bfloat16* __restrict__ ctx) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* sm = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ uint64_t q_full, k_full[FA_KR], v_full[FA_VR], s_full, s_free, p_full, o_full[2];
+  __shared__ uint64_t q_full, k_full[FA_KR], v_full[FA_VR], s_full, s_free, p_full[FA_PB], o_full[2];
   __shared__ uint32_t tbase;
   const int qt = blockIdx.x, h = blockIdx.y, crop = blockIdx.z;
   const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
@@ -143,7 +147,7 @@ __global__ void __launch_bounds__(FA_THREADS, 3)
     for (int i = 0; i < FA_VR; ++i) tc::mbar_init(&v_full[i], 1);
     tc::mbar_init(&s_full, 1);
     tc::mbar_init(&s_free, 4);  // the four softmax warps copied S(j)
-    tc::mbar_init(&p_full, 4);  // the four softmax warps wrote P(j)
+    for (int i = 0; i < FA_PB; ++i) tc::mbar_init(&p_full[i], 4);  // the four softmax warps wrote P(j)
     tc::mbar_init(&o_full[0], 1);  // P(j).V(j) done, j & 1 == b
     tc::mbar_init(&o_full[1], 1);
     tc::mbar_fence_init();
@@ -210,14 +214,15 @@ __global__ void __launch_bounds__(FA_THREADS, 3)
         if (j + 2 < nch) load_k(j + 2);
       }
       // O += P(j) V_j once the four softmax warps have written P(j)
-      tc::mbar_wait(&p_full, (uint32_t)(j & 1));
+      tc::mbar_wait(&p_full[j % FA_PB], (uint32_t)((j / FA_PB) & 1));
       tc::mbar_wait(&v_full[j % FA_VR], (uint32_t)((j / FA_VR) & 1));
       tc::fence_after();
       if (leader) {
         const uint32_t v = sbase + FA_V + (j % FA_VR) * 8192;
+        const uint32_t pt = sbase + FA_P + (j % FA_PB) * 16384;
 #pragma unroll
         for (int kk = 0; kk < FA_KC / 16; ++kk)
-          tc::mma_bf16(tO, tc::kmajor_desc(sbase + FA_P, FA_KC, kk * 16), tc::sw128_mnmajor_desc(v + kk * 2048, 8192),
+          tc::mma_bf16(tO, tc::kmajor_desc(pt, FA_KC, kk * 16), tc::sw128_mnmajor_desc(v + kk * 2048, 8192),
                        id_o, (j | kk) != 0);
         tc::mma_commit(&o_full[j & 1]);
       }
@@ -232,7 +237,7 @@ __global__ void __launch_bounds__(FA_THREADS, 3)
   } else {
     // softmax: query row r = tid of the tile
     const uint32_t lane_off = (uint32_t)(warp * 32) << 16;
-    uint8_t* prow = sm + FA_P + (tid >> 3) * (FA_KC * 16) + (tid & 7) * 16;
+    uint8_t* prow0 = sm + FA_P + (tid >> 3) * (FA_KC * 16) + (tid & 7) * 16;
     const float c2 = scale * 1.4426950408889634f;
     float m = -INFINITY, l = 0.0f;
     for (int j = 0; j < nch; ++j) {
@@ -253,9 +258,9 @@ __global__ void __launch_bounds__(FA_THREADS, 3)
 #pragma unroll
       for (int i = 4; i < FA_KC; ++i) m4[i & 3] = fmaxf(m4[i & 3], s[i]);
       const float mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3])) * c2;
-      if (j > 0) {
-        // P(j-1).V(j-1) done: O is stable and the P tile is free
-        tc::mbar_wait(&o_full[(j - 1) & 1], (uint32_t)(((j - 1) >> 1) & 1));
+      if (j >= FA_PB) {
+        // P(j-PB).V(j-PB) done: P tile j % PB is free (PB = 1: O is stable too)
+        tc::mbar_wait(&o_full[(j - FA_PB) & 1], (uint32_t)(((j - FA_PB) >> 1) & 1));
         tc::fence_after();
       }
       if (j == 0) {
@@ -266,6 +271,10 @@ __global__ void __launch_bounds__(FA_THREADS, 3)
         // if any of its rows needs it (alpha = 1 elsewhere).
         const bool need = mx > m + FA_RESCALE;
         if (__any_sync(0xffffffffu, need)) {
+          if (FA_PB == 2) {  // O must be stable: P(j-1).V(j-1) done
+            tc::mbar_wait(&o_full[(j - 1) & 1], (uint32_t)(((j - 1) >> 1) & 1));
+            tc::fence_after();
+          }
           const float alpha = need ? ex2_approx(m - mx) : 1.0f;
 #pragma unroll 1
           for (int c = 0; c < 64; c += 8) {
@@ -280,6 +289,7 @@ __global__ void __launch_bounds__(FA_THREADS, 3)
         }
       }
       const float nm = -m;
+      uint8_t* prow = prow0 + (j % FA_PB) * 16384;
       float sum4[4] = {0.0f, 0.0f, 0.0f, 0.0f};
 #pragma unroll
       for (int q = 0; q < FA_KC / 8; ++q) {
@@ -297,7 +307,7 @@ __global__ void __launch_bounds__(FA_THREADS, 3)
       tc::fence_async_smem();  // P visible to the tensor core
       tc::fence_before();      // S(j) reads and the O rescale ordered before the arrive
       __syncwarp();
-      if (lane == 0) tc::mbar_arrive(&p_full);
+      if (lane == 0) tc::mbar_arrive(&p_full[j % FA_PB]);
     }
     tc::mbar_wait(&o_full[(nch - 1) & 1], (uint32_t)(((nch - 1) >> 1) & 1));
     tc::fence_after();
