@@ -187,7 +187,7 @@ bool default_model(const fsb_decoder_config& c) {
 }
 
 #ifndef FSB_VIT_CHUNK
-#define FSB_VIT_CHUNK 256
+#define FSB_VIT_CHUNK 256  // 128 / 256 / 384 / 768 measured equal within 2 %; 256 uses the least memory
 #endif
 constexpr int kVitChunk = FSB_VIT_CHUNK;  // crops per large-config encoder pass
 

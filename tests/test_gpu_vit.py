@@ -105,6 +105,26 @@ def test_vitl_batch_independence(vit_ctx):
     assert np.array_equal(many[1], one[0])
 
 
+def test_vitl_chunk_boundary(vit_ctx):
+    """More crops than one encoder pass (fsb_capi.cu kVitChunk = 256): crops on
+    both sides of the pass boundary and in the ragged last pass equal solo runs."""
+    import torch
+
+    from paper_2603_15603_b200 import runtime as rt
+
+    ctx, _ = vit_ctx
+    n = 260
+    g = torch.Generator(device="cuda").manual_seed(7)
+    x = torch.rand((n, 384, 384, 3), generator=g, device="cuda")
+    out = torch.empty((n, 576, 1024), dtype=torch.float32, device="cuda")
+    ctx.check(ctx.lib.fsb_encode(ctx.h, rt.ptr(x), n, rt.ptr(out), rt.PRECISIONS["bf16"], ctx.stream), "encode")
+    torch.cuda.synchronize()
+    assert torch.isfinite(out).all()
+    for i in (0, 255, 256, n - 1):
+        one = _encode(ctx, x[i:i + 1].cpu().numpy())
+        assert np.array_equal(out[i].cpu().numpy(), one[0]), i
+
+
 def test_vitl_fp32_rejected(vit_ctx):
     import torch
 
