@@ -21,6 +21,7 @@ from __future__ import annotations
 
 import argparse
 import json
+import math
 import multiprocessing as mp
 import os
 import statistics
@@ -48,31 +49,62 @@ FLOP_MLP_MESH = 4_909_056
 FLOP_C4_CROP = 2 * 576 * 768 * 1024 + 24 * (24 * 576 * 1024 ** 2 + 4 * 576 ** 2 * 1024)
 
 
-def parse():
+def parse(argv=None):
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=2000)
-    ap.add_argument("--warmup", type=int, default=20)
-    ap.add_argument("--batch", type=int, default=32, help="frames per GPU per step (C2: 32)")
-    ap.add_argument("--bank", type=int, default=256, help="distinct frames per GPU cycled through")
+    ap.add_argument("--steps", type=int, default=40)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--batch", type=int, default=32, help="frames per batch (C2: 32)")
+    ap.add_argument("--bank", type=int, default=512,
+                    help="distinct frames per GPU cycled through (>= streams x batch: no two in-flight batches "
+                         "read the same frames)")
     ap.add_argument("--precision", default="bf16", choices=("fp32", "bf16"))
     ap.add_argument("--impl", default="ours", choices=("ours", "reference"))
     ap.add_argument("--cpu-seconds", type=float, default=12.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--streams", type=int, default=16,
-                    help="in-flight batches per GPU: independent pipeline contexts on their own streams")
+                    help="in-flight batches per GPU: pipelines sharing one uploaded model, each with its own "
+                         "context (workspace, CUDA graphs) and stream; one step = one batch on each")
     ap.add_argument("--no-c3", action="store_true", help="skip the C3 LBS + projector microbench")
     ap.add_argument("--no-c4", action="store_true", help="skip the C4 ViT-L-sized encoder microbench")
     ap.add_argument("--no-fit", action="store_true", help="skip the iterative-fit conversion microbench")
     ap.add_argument("--stream-frames", type=int, default=8192,
                     help="C5: frames of the synthetic video stream sharded across the ranks (0: skip)")
     ap.add_argument("--c4-crops", type=int, default=768, help="C4: 3 crops x 256 frames")
-    return ap.parse_args()
+    return ap.parse_args(argv)
 
 
 # ---------------------------------------------------------------------------
 # distributed plumbing
+
+
+def torchrun_argv(argv, n, port):
+    """`python bench.py --gpus N ...` without a torchrun environment re-executes
+    itself under torchrun: one process per GPU on this node (127.0.0.1)."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(n),
+            "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + list(argv)
+
+
+def maybe_spawn(args, argv):
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return
+    import socket
+
+    if args.impl == "ours":
+        import torch
+
+        have = torch.cuda.device_count()
+        if have < args.gpus:
+            sys.stderr.write("bench.py: --gpus %d but only %d CUDA device(s) visible\n" % (args.gpus, have))
+            sys.exit(2)
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = torchrun_argv(argv, args.gpus, port)
+    sys.stderr.write("bench.py: spawning %d ranks: %s\n" % (args.gpus, " ".join(cmd)))
+    sys.exit(subprocess.call(cmd))
 
 
 def dist_setup(torch, want):
@@ -83,8 +115,11 @@ def dist_setup(torch, want):
         import torch.distributed as dist
 
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("NCCL_DEBUG", "VERSION")
         torch.cuda.set_device(local)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if rank == 0:
+            sys.stderr.write("bench.py: NCCL process group, %d ranks\n" % dist.get_world_size())
         return dist, rank, ws, local
     return None, 0, 1, 0
 
@@ -99,62 +134,190 @@ def shard_bounds(n_frames, rank, world):
     return rank * n_frames // world, (rank + 1) * n_frames // world
 
 
-# ---------------------------------------------------------------------------
-# clocks during the timed region (B200_PROFILING.md)
+def gather_rows(dist, torch, rows, world):
+    """All ranks' (n, k) result rows -> (world * n, k) on every rank: NCCL
+    all_gather_into_tensor on the GPU, the list form on gloo/CPU."""
+    if dist is None:
+        return rows
+    if rows.is_cuda:
+        out = torch.empty((world * rows.shape[0],) + tuple(rows.shape[1:]), dtype=rows.dtype, device=rows.device)
+        dist.all_gather_into_tensor(out, rows)
+        return out
+    parts = [torch.empty_like(rows) for _ in range(world)]
+    dist.all_gather(parts, rows)
+    return torch.cat(parts)
 
-_REASONS = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+
+def max_over_ranks(dist, torch, ms, device):
+    t = torch.tensor([ms], dtype=torch.float64, device=device)
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+class Lanes:
+    """In-flight lanes of one rank: CUDA streams timed with CUDA events on the
+    device (cuda=True), or sequential CPU execution timed on the host (the
+    gloo tests drive the same stream/shard/gather code with a stand-in
+    pipeline)."""
+
+    def __init__(self, torch, n, device, streams=None):
+        self.torch, self.n, self.device = torch, n, device
+        self.cuda = device.type == "cuda"
+        if self.cuda:
+            self.streams = streams or ([torch.cuda.current_stream(device)] +
+                                       [torch.cuda.Stream(device=device) for _ in range(n - 1)])
+
+    def lane(self, j):
+        import contextlib
+
+        return self.torch.cuda.stream(self.streams[j]) if self.cuda else contextlib.nullcontext()
+
+    def main(self):
+        import contextlib
+
+        return self.torch.cuda.stream(self.streams[0]) if self.cuda else contextlib.nullcontext()
+
+    def start(self):
+        if self.cuda:
+            self.e0 = self.torch.cuda.Event(enable_timing=True)
+            self.e0.record(self.streams[0])
+            for q in self.streams[1:]:
+                q.wait_event(self.e0)
+        else:
+            self.t0 = time.perf_counter()
+
+    def join(self):
+        """Everything every lane enqueued so far happens before what the main
+        lane enqueues next."""
+        if self.cuda:
+            for q in self.streams[1:]:
+                ev = self.torch.cuda.Event()
+                ev.record(q)
+                self.streams[0].wait_event(ev)
+
+    def stop(self):
+        self.join()
+        if self.cuda:
+            self.e1 = self.torch.cuda.Event(enable_timing=True)
+            self.e1.record(self.streams[0])
+            self.torch.cuda.synchronize(self.device)
+            return self.e0.elapsed_time(self.e1)
+        return (time.perf_counter() - self.t0) * 1e3
+
+
+def stream_shard(lanes, launch, frames_fn, B, dist, world, rank, total, out_width=142):
+    """C5: a stream of `total` frames, rank r taking the
+    contiguous block [r*total/G, (r+1)*total/G); batches of B round-robin over
+    the lanes; each batch's SMPL outputs (theta + joints) land in the rank's
+    result rows; ONE all-gather of the rows at the end (the path's only
+    collective).  `launch(j, img, kp, nb)` enqueues a batch on lane j and
+    returns (theta (nb, 76), j_smpl (nb, 22, 3)); `frames_fn(f0, nb)` gives the
+    batch's frames.  Returns (gathered rows (total, 142), ms)."""
+    torch = lanes.torch
+    lo, hi = shard_bounds(total, rank, world)
+    n = hi - lo
+    res = torch.zeros((max(n, 1), out_width), dtype=torch.float32, device=lanes.device)
+    lanes.start()
+    k = 0
+    for f0 in range(lo, hi, B):
+        nb = min(B, hi - f0)
+        j = k % lanes.n
+        with lanes.lane(j):
+            img, kp = frames_fn(f0, nb)
+            th, jj = launch(j, img, kp, nb)
+            r = f0 - lo
+            res[r:r + nb, :76].copy_(th)
+            res[r:r + nb, 76:].copy_(jj.reshape(nb, 66))
+        k += 1
+    lanes.join()
+    with lanes.main():
+        gathered = gather_rows(dist, torch, res[:n] if n else res, world)
+    ms = lanes.stop()
+    return gathered, max_over_ranks(dist, torch, ms, lanes.device)
+
+
+# ---------------------------------------------------------------------------
+# clocks during the timed region (B200_PROFILING.md): NVML polled from a
+# thread (sub-millisecond), nvidia-smi as the fallback
+
+_REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20, "sw_power_cap": 0x4}
 
 
 class ClockSampler:
     def __init__(self, index):
         self.index = index
-        self.proc = None
-        self.lines = []
+        self.samples = []  # (sm_mhz, reasons bitmask)
+        self.max_mhz = None
+        self.stop_ev = threading.Event()
+        self.t = None
+        self.src = "nvml"
 
     def __enter__(self):
-        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
-             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-             "clocks_event_reasons.sw_power_cap")
         try:
-            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + q,
-                                          "--format=csv,noheader,nounits", "-lms", "20"],
-                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml
+
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+
+            def poll():
+                while not self.stop_ev.is_set():
+                    try:
+                        sm = pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM)
+                        rs = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                        self.samples.append((sm, rs))
+                    except pynvml.NVMLError:
+                        pass
+                    time.sleep(0.0005)
+
+            self.t = threading.Thread(target=poll, daemon=True)
             self.t.start()
-        except OSError:
-            self.proc = None
+        except Exception:  # no NVML: nvidia-smi at its 10 ms minimum
+            self.src = "nvidia-smi"
+            self._smi()
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
+    def _smi(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), "--query-gpu=" + q,
+                                          "--format=csv,noheader,nounits", "-lms", "10"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+            return
+
+        def read():
+            for line in self.proc.stdout:
+                parts = [p.strip() for p in line.split(",")]
+                try:
+                    sm, mx = float(parts[0]), float(parts[1])
+                except (ValueError, IndexError):
+                    continue
+                self.max_mhz = mx
+                bits = 0
+                for (name, bit), v in zip(_REASONS.items(), parts[2:6]):
+                    bits |= bit if v.lower() == "active" else 0
+                self.samples.append((sm, bits))
+
+        self.t = threading.Thread(target=read, daemon=True)
+        self.t.start()
 
     def __exit__(self, *a):
-        if self.proc is not None:
+        self.stop_ev.set()
+        if self.src == "nvidia-smi" and getattr(self, "proc", None) is not None:
             self.proc.terminate()
-            try:
-                self.proc.wait(timeout=5)
-            except subprocess.TimeoutExpired:
-                self.proc.kill()
+        if self.t is not None:
+            self.t.join(timeout=5)
 
-    def summary(self):
-        sm, mx, reasons = [], None, set()
-        for ln in self.lines:
-            parts = [p.strip() for p in ln.split(",")]
-            if len(parts) < 7:
-                continue
-            try:
-                s, m = float(parts[0]), float(parts[1])
-            except ValueError:
-                continue
-            mx = m
-            if s > 0.5 * m:  # under load
-                sm.append(s)
-            for name, val in zip(_REASONS, parts[3:7]):
-                if val.lower() == "active":
-                    reasons.add(name)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
-                "reasons": sorted(reasons), "samples": len(self.lines)}
+    def summary(self, samples=None):
+        samples = self.samples if samples is None else samples
+        sm = [s for s, _ in samples if self.max_mhz and s > 0.5 * self.max_mhz]
+        reasons = sorted(name for name, bit in _REASONS.items() if any(r & bit for _, r in samples))
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.max_mhz, "reasons": reasons,
+                "samples": len(samples), "source": self.src}
 
 
 # ---------------------------------------------------------------------------
@@ -173,28 +336,29 @@ def build_models(precision):
     return pl.Pipeline(dec, mhr=mhr, bmap=gt, projector=proj, precision=precision), (mhr, smpl, gt, dec, proj)
 
 
-def extra_pipelines(pipe, n, precision):
-    """n more pipeline instances over the same models, each with its own
-    fsb context (weights, workspace, CUDA graphs): one per in-flight batch
-    (pipelines are not shared between concurrent users)."""
-    from paper_2603_15603_b200 import decoder as dc
-    from paper_2603_15603_b200 import pipeline as pl
-
-    out = []
-    for _ in range(n):
-        d = dc.Decoder(pipe.decoder.template, pipe.decoder.config, seed=40)
-        out.append(pl.Pipeline(d, mhr=pipe.mhr, bmap=pipe.bmap, projector=pipe.projector, precision=precision))
-    return out
-
-
 def make_scenes(smpl, seeds):
     from paper_2603_15603_b200 import synth
 
     return [synth.random_scene(np.random.default_rng(s), smpl, (512, 512)) for s in seeds]
 
 
+def cpu_model():
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for ln in out.splitlines():
+            if ln.startswith("Model name:"):
+                return ln.split(":", 1)[1].strip()
+    except (OSError, subprocess.SubprocessError):
+        pass
+    return None
+
+
 # ---------------------------------------------------------------------------
 # CPU oracle (baseline / reference arm)
+
+PORT_NOTE = ("oracle/ restatement of the reference (numpy + the two numba kernels restated in C); in the survey "
+             "container the reference package itself ran this composition 1.3-1.8x slower per frame, so ratios "
+             "against this arm understate the gap to the reference")
 
 
 def _cpu_worker(args):
@@ -263,9 +427,9 @@ def reference_arm(args):
             "config": {"workload": "C2 frame->SMPL, 512x512 frames, default encoder/decoders, full-size "
                                    "MHR 18439 / SMPL 6890 tail (CPU oracle restatement of the reference)",
                        "frames_per_step": n},
-            "cpu_baseline": {"value": fps, "unit": UNIT, "cores": cores, "kind": "port",
+            "cpu_baseline": {"value": fps, "unit": UNIT, "cores": cores, "kind": "port", "cpu_model": cpu_model(),
                              "sample": "%d timed frames on %d host processes (one frame per process per step, %d "
-                                       "steps), p50 %.1f ms/frame" % (done, cores, steps, p50)},
+                                       "steps), p50 %.1f ms/frame; %s" % (done, cores, steps, p50, PORT_NOTE)},
             "e2e": {"value": fps, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "p50_frame_latency_ms": p50}
     print(json.dumps(line), flush=True)
@@ -275,8 +439,10 @@ def reference_arm(args):
 # the GPU arm
 
 
-def main():
-    args = parse()
+def main(argv=None):
+    argv = sys.argv[1:] if argv is None else argv
+    args = parse(argv)
+    maybe_spawn(args, argv)
     if args.impl == "reference":
         reference_arm(args)
         return
@@ -285,8 +451,10 @@ def main():
     dist, rank, world, local = dist_setup(torch, args.gpus)
     dev = torch.device("cuda", local)
     torch.cuda.set_device(dev)
+    from paper_2603_15603_b200 import pipeline as pl
     from paper_2603_15603_b200 import priors as pr
 
+    clk = ClockSampler(local).__enter__()  # whole run; the timed regions are marked below
     pipe, (mhr, smpl, gt, dec, proj) = build_models(args.precision)
     ctx = pipe.context()
     B, bank = args.batch, max(args.bank, args.batch)
@@ -298,63 +466,53 @@ def main():
     kps = torch.from_numpy(np.stack([s.keypoints2d for s in scenes])).to(dev)
     nslot = bank // B
     S = max(1, args.streams)
-    pipes = [pipe] + extra_pipelines(pipe, S - 1, args.precision)
-    for p_ in pipes[1:]:
+    pipes = [pipe] + [pipe.fork() for _ in range(S - 1)]   # one uploaded model, S contexts
+    for p_ in pipes:
         p_.context().reserve(max(B, 1))
-    streams = [torch.cuda.current_stream()] + [torch.cuda.Stream(device=dev) for _ in range(S - 1)]
+    lanes = Lanes(torch, S, dev)
     outs_s = [p_.allocate_outputs(B, tail=True) for p_ in pipes]
-    outs = outs_s[0]
-    from paper_2603_15603_b200 import pipeline as pl
-
     cfg = pl.fast_config()
-    gathered = None
-    if dist is not None:
-        gathered = [torch.empty((world * B, 76 + 66), dtype=torch.float32, device=dev) for _ in range(S)]
-        packed = [torch.empty((B, 76 + 66), dtype=torch.float32, device=dev) for _ in range(S)]
 
     def step(i):
-        j, s = i % S, i % nslot
-        with torch.cuda.stream(streams[j]):
-            pipes[j].launch(images[s * B:(s + 1) * B], kps[s * B:(s + 1) * B], outs_s[j], cfg)
-            if dist is not None:
-                packed[j][:, :76].copy_(outs_s[j]["theta"])
-                packed[j][:, 76:].copy_(outs_s[j]["j_smpl"].reshape(B, 66))
-                dist.all_gather_into_tensor(gathered[j], packed[j])
+        """One step: batch j of every in-flight pipeline (S * B frames),
+        inputs cycling through the HBM bank (larger than L2)."""
+        for j in range(S):
+            s = (i * S + j) % nslot
+            with lanes.lane(j):
+                pipes[j].launch(images[s * B:(s + 1) * B], kps[s * B:(s + 1) * B], outs_s[j], cfg)
 
     def barrier():
         if dist is not None:
             dist.barrier()
         torch.cuda.synchronize()
 
-    # warm-up (captures one graph per input slot and stream)
-    for i in range(max(args.warmup, 3, nslot * S)):
+    # warm-up: every (pipeline, input slot) pair gets its CUDA graph captured
+    period = nslot // math.gcd(nslot, S)
+    for i in range(max(args.warmup, 3, period)):
         step(i)
     for p_ in pipes:
         p_.context().check_finite("bench warm-up")
     barrier()
     launches0 = sum(p_.context().launches() for p_ in pipes)
-    st = streams[0]
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    joins = [torch.cuda.Event() for _ in range(S)]
-    with ClockSampler(local) as clk:
-        barrier()
-        e0.record(st)
-        for q in streams[1:]:
-            q.wait_event(e0)
-        for i in range(args.steps):
-            step(i)
-        for j in range(1, S):
-            joins[j].record(streams[j])
-            st.wait_event(joins[j])
-        e1.record(st)
-        barrier()
-    launches = sum(p_.context().launches() for p_ in pipes) - launches0
-    ms = e0.elapsed_time(e1)
-    t_max = torch.tensor([ms], dtype=torch.float64, device=dev)
+    n0 = len(clk.samples)
+    barrier()
+    lanes.start()
+    for i in range(args.steps):
+        step(i)
+    lanes.join()
+    # the path's only collective: the final gather of the SMPL outputs
+    # (theta + joints) of the last round, on the main lane
     if dist is not None:
-        dist.all_reduce(t_max, op=dist.ReduceOp.MAX)
-    ms = float(t_max.item())
-    frames_total = world * B * args.steps
+        with lanes.main():
+            rows = torch.cat([torch.cat([o["theta"], o["j_smpl"].reshape(B, 66)], 1) for o in outs_s])
+            gather_rows(dist, torch, rows, world)
+    ms = lanes.stop()
+    barrier()
+    timed_clocks = clk.samples[n0:]
+    launches = sum(p_.context().launches() for p_ in pipes) - launches0
+    ms = max_over_ranks(dist, torch, ms, dev)
+    frames_step = S * B
+    frames_total = world * frames_step * args.steps
     value = frames_total / (ms / 1e3)
     for p_ in pipes:
         p_.context().check_finite("bench")
@@ -362,23 +520,22 @@ def main():
     verified = verify_streams(torch, pipes, outs_s, images, kps, cfg, B, args.steps, nslot, S)
 
     # -- C5: an 8192-frame stream sharded across the ranks, one NCCL gather ----
-    c5 = None if args.stream_frames <= 0 else stream_run(torch, pipes, streams, images, kps, cfg, B, dist, world,
+    c5 = None if args.stream_frames <= 0 else stream_run(torch, pipes, lanes, images, kps, cfg, B, dist, world,
                                                           rank, args.stream_frames)
 
-    # -- per-stage attribution (graphs off, CUDA events between stages) -------
+    # -- per-stage attribution (each stage alone in a CUDA graph) -------------
     stage_sat = {}
-    stage_ms = attribute_stages(torch, pipe, ctx, images[:B], kps[:B], outs, cfg, reps=20, saturated=16,
+    stage_ms = attribute_stages(torch, pipe, ctx, images, kps, outs_s[0], cfg, reps=20, saturated=16,
                                 saturated_out=stage_sat)
     stage_sat["sum"] = round(sum(stage_sat.values()), 2)
 
-    # -- p50 single-frame latency (B = 1 graph replay) -------------------------
+    # -- p50 single-frame latency ----------------------------------------------
     lat = frame_latency(torch, pipe, images, kps, cfg, reps=200)
+    lat_api = api_latency(torch, pipe, images, scenes, cfg, reps=100)
 
     # -- end-to-end through the public API with host buffers -------------------
     e2e = None if args.no_e2e else end_to_end(torch, pipes, images, kps, cfg, B, args.steps, args.warmup, dist,
                                               world)
-    e2e_copy = None if args.no_e2e else end_to_end_full_copy(torch, pipe, images, kps, cfg, B, args.steps,
-                                                             args.warmup, dist, world)
 
     # -- C3 microbench: LBS + projector on 4096 full-size meshes ---------------
     c3 = None if args.no_c3 else c3_microbench(torch, pipe, ctx, meshes=4096, reps=10)
@@ -389,39 +546,45 @@ def main():
 
     # -- C4 microbench: ViT-L-sized encoder, 3 crops x 256 frames --------------
     c4 = None if args.no_c4 else c4_microbench(torch, crops=args.c4_crops, reps=3)
+    clk.__exit__()
 
     if rank != 0:
         if dist is not None:
             dist.destroy_process_group()
         return
-    roof = roofline(stage_ms, B)
+    roof = roofline(stage_ms, stage_sat, B)
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         n_host = min(len(scenes), 64)
         fr = images[:n_host].cpu().numpy()
         kk = kps[:n_host].cpu().numpy()
         fps, cores, done, p50c = cpu_oracle_run(fr, kk, args.cpu_seconds)
-        cpu = {"value": fps, "unit": UNIT, "cores": cores, "kind": "port",
+        cpu = {"value": fps, "unit": UNIT, "cores": cores, "kind": "port", "cpu_model": cpu_model(),
                "sample": "%d frames (C2 frame->SMPL, full-size tail) on %d host processes over ~%.0f s; "
-                         "p50 %.1f ms/frame single process" % (done, cores, args.cpu_seconds, p50c)}
+                         "p50 %.1f ms/frame single process; %s" % (done, cores, args.cpu_seconds, p50c, PORT_NOTE)}
+    clocks = clk.summary(timed_clocks)  # samples taken inside the timed region
+    clocks["whole_run"] = clk.summary()
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "f32" if args.precision == "fp32" else "bf16", "data": "synthetic",
-        "config": {"workload": "C2: %d synthetic 512x512 frames per GPU per step, body + 2 hand crops -> "
-                               "encoder -> pruned decoders -> MHR LBS (18439 v) -> projector -> SMPL FK" % B,
-                   "frames_per_gpu_per_step": B, "global_batch": B * world,
-                   "parallelism": "dp%d (frame sharding, NCCL all-gather of SMPL outputs)" % world
-                   if world > 1 else "single GPU",
+        "config": {"workload": "C2: batches of %d synthetic 512x512 frames, body + 2 hand crops -> encoder -> "
+                               "pruned decoders -> MHR LBS (18439 v) -> projector -> SMPL FK; one step = one batch "
+                               "on each of %d in-flight pipelines" % (B, S),
+                   "batch": B, "in_flight_batches": S, "frames_per_gpu_per_step": frames_step,
+                   "global_batch": frames_step * world,
+                   "parallelism": "dp%d (frame sharding, one NCCL all-gather of the SMPL outputs after the "
+                                  "timed steps)" % world if world > 1 else "single GPU",
                    "l2": "inputs cycle through a %d-frame bank (%.0f MB in HBM) > 126 MB L2" %
                          (bank, bank * 512 * 512 * 12 / 1e6),
-                   "precision": args.precision, "graphs": True,
-                   "in_flight_batches": S, "concurrent_outputs_match_single_stream": verified},
-        "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "e2e_full_frame_copy": e2e_copy,
+                   "precision": args.precision, "graphs": True, "shared_model": True,
+                   "concurrent_outputs_match_single_stream": verified},
+        "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
         "gpu_launches": launches,
-        "clocks": clk.summary(), "p50_frame_latency_ms": lat["p50_ms"], "frame_latency": lat,
+        "clocks": clocks, "p50_frame_latency_ms": lat_api["p50_ms"], "frame_latency_api": lat_api,
+        "frame_latency_device": lat,
         "stage_ms": stage_ms,
-        "stage_saturated_us_per_batch": stage_sat,  # 16 concurrent copies of each stage alone
+        "stage_saturated_us_per_batch": stage_sat,  # 16 concurrent copies of each stage alone, distinct frames
         "c3": c3, "c4": c4, "c5": c5, "conversion": conv,
     }
     print(json.dumps(line), flush=True)
@@ -568,45 +731,63 @@ def c4_microbench(torch, crops, reps, layers=24):
             "algorithmic_flop_per_batch": crops * FLOP_C4_CROP}
 
 
-def attribute_stages(torch, pipe, ctx, img, kp, outs, cfg, reps, saturated=None, saturated_out=None):
+def attribute_stages(torch, pipe, ctx, images, kps, outs, cfg, reps, saturated=None, saturated_out=None):
     """Average device time of each stage kernel on one batch.  Each stage's
     launches are captured `reps` times into its own CUDA graph and the graph
     is replayed between CUDA events, so the numbers are device time, not the
-    host's ctypes launch rate."""
+    host's ctypes launch rate.  With `saturated`, the same stage runs as
+    `saturated` concurrent copies (forked streams in one graph), each copy on
+    DISTINCT frames and its own buffers: the device time one batch of the
+    stage costs when the GPU is kept full of it."""
     from paper_2603_15603_b200 import decoder as dc
     from paper_2603_15603_b200 import runtime as rt
 
-    B = img.shape[0]
+    B = outs["merged"].shape[0]
     lib, h = ctx.lib, ctx.h
     prec = rt.PRECISIONS[pipe.precision]
-    dev = img.device
-    crops = torch.empty((B, 3, 64, 64, 3), dtype=torch.float32, device=dev)
-    feats = torch.empty((B, 3, 64, 64), dtype=torch.float32, device=dev)
+    dev = images.device
+    nv = pipe.mhr.num_vertices
     bsel, _ = dc.selection_mask(cfg.selection, 5)
+    n_copies = saturated or 1
+    nslot = images.shape[0] // B
+    bufs = []
+    for q in range(n_copies):
+        o = outs if q == 0 else {k: torch.empty_like(v) for k, v in outs.items()}
+        s = q % nslot
+        bufs.append({"img": images[s * B:(s + 1) * B], "kp": kps[s * B:(s + 1) * B], "o": o,
+                     "crops": torch.empty((B, 3, 64, 64, 3), dtype=torch.float32, device=dev),
+                     "feats": torch.empty((B, 3, 64, 64), dtype=torch.float32, device=dev)})
+    # each concurrent copy needs its own workspace: one forked context per copy
+    ctxs = [ctx] + [rt.Context(share=ctx) for _ in range(n_copies - 1)]
+    for c in ctxs:
+        c.reserve(B)
 
-    def k1():
-        ctx.check(lib.fsb_boxes_crops(h, rt.ptr(img), B, 512, 512, rt.ptr(kp), 3.0, 64, rt.ptr(outs["boxes"]),
-                                      rt.ptr(outs["prompt"]), rt.ptr(crops), None, ctx.stream))
+    def k1(c, b):
+        c.check(lib.fsb_boxes_crops(c.h, rt.ptr(b["img"]), B, 512, 512, rt.ptr(b["kp"]), 3.0, 64,
+                                    rt.ptr(b["o"]["boxes"]), rt.ptr(b["o"]["prompt"]), rt.ptr(b["crops"]), None,
+                                    c.stream))
 
-    def k2():
-        ctx.check(lib.fsb_encode(h, rt.ptr(crops), 3 * B, rt.ptr(feats), prec, ctx.stream))
+    def k2(c, b):
+        c.check(lib.fsb_encode(c.h, rt.ptr(b["crops"]), 3 * B, rt.ptr(b["feats"]), prec, c.stream))
 
-    def k3():
-        ctx.check(lib.fsb_decode_frames(h, rt.ptr(feats), B, rt.ptr(outs["prompt"]), bsel, 0,
-                                        rt.ptr(outs["body_params"]), rt.ptr(outs["body_cam"]),
-                                        rt.ptr(outs["hand_rots"]), rt.ptr(outs["merged"]), prec, ctx.stream))
+    def k3(c, b):
+        o = b["o"]
+        c.check(lib.fsb_decode_frames(c.h, rt.ptr(b["feats"]), B, rt.ptr(o["prompt"]), bsel, 0,
+                                      rt.ptr(o["body_params"]), rt.ptr(o["body_cam"]), rt.ptr(o["hand_rots"]),
+                                      rt.ptr(o["merged"]), prec, c.stream))
 
-    def k4a():
-        ctx.check(lib.fsb_skin(h, 0, rt.ptr(outs["merged"]), B, rt.ptr(outs["v_mhr"]), ctx.stream))
+    def k4a(c, b):
+        c.check(lib.fsb_skin(c.h, 0, rt.ptr(b["o"]["merged"]), B, rt.ptr(b["o"]["v_mhr"]), c.stream))
 
-    def k4b():  # projector input bridged from V_mhr + the MLP, as in the frame path
-        ctx.check(lib.fsb_project_vertices(h, rt.ptr(outs["v_mhr"]), B, pipe.mhr.num_vertices, rt.ptr(outs["theta"]),
-                                           prec, ctx.stream))
+    def k4b(c, b):  # projector input bridged from V_mhr + the MLP, as in the frame path
+        c.check(lib.fsb_project_vertices(c.h, rt.ptr(b["o"]["v_mhr"]), B, nv, rt.ptr(b["o"]["theta"]), prec,
+                                         c.stream))
 
     stages = [("k1_boxes_crops", k1), ("k2_encoder", k2), ("k3_decoders", k3), ("k4_fk_lbs", k4a),
               ("k4_proj_mlp", k4b)]
-    for _, fn in stages:  # eager warm-up (workspace allocation happens here)
-        fn()
+    for q in range(n_copies):  # eager pass: real inputs for every stage of every copy
+        for _, fn in stages:
+            fn(ctxs[q], bufs[q])
     torch.cuda.synchronize()
     out = {}
     side = torch.cuda.Stream(device=dev)
@@ -615,7 +796,7 @@ def attribute_stages(torch, pipe, ctx, img, kp, outs, cfg, reps, saturated=None,
         with torch.cuda.stream(side):
             with torch.cuda.graph(g, stream=side, capture_error_mode="relaxed"):
                 for _ in range(reps):
-                    fn()
+                    fn(ctx, bufs[0])
         g.replay()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -625,23 +806,19 @@ def attribute_stages(torch, pipe, ctx, img, kp, outs, cfg, reps, saturated=None,
         e1.record()
         torch.cuda.synchronize()
         out[name] = float(e0.elapsed_time(e1) / (3 * reps))
-    if saturated is not None:
-        # the same stages with `saturated` concurrent copies (forked streams in
-        # one graph): device time one batch of the stage costs when the GPU is
-        # kept full with it -- its share of the SM budget the pipeline runs on
-        n = saturated
+    if saturated:
+        branches = [torch.cuda.Stream(device=dev) for _ in range(n_copies)]
         for name, fn in stages:
-            branches = [torch.cuda.Stream(device=dev) for _ in range(n)]
             g = torch.cuda.CUDAGraph()
             with torch.cuda.stream(side):
                 with torch.cuda.graph(g, stream=side, capture_error_mode="relaxed"):
-                    for q in branches:
-                        q.wait_stream(side)
-                        with torch.cuda.stream(q):
+                    for q, br in enumerate(branches):
+                        br.wait_stream(side)
+                        with torch.cuda.stream(br):
                             for _ in range(4):
-                                fn()
-                    for q in branches:
-                        side.wait_stream(q)
+                                fn(ctxs[q], bufs[q])
+                    for br in branches:
+                        side.wait_stream(br)
             g.replay()
             torch.cuda.synchronize()
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -650,12 +827,11 @@ def attribute_stages(torch, pipe, ctx, img, kp, outs, cfg, reps, saturated=None,
                 g.replay()
             e1.record()
             torch.cuda.synchronize()
-            saturated_out[name] = round(float(1e3 * e0.elapsed_time(e1) / (3 * 4 * n)), 2)
+            saturated_out[name] = round(float(1e3 * e0.elapsed_time(e1) / (3 * 4 * n_copies)), 2)
     return out
 
 
-def roofline(stage_ms, B):
-    """Roofline of the dominant stage kernel against MEASURED_PEAKS.json."""
+def _peaks():
     peaks = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "src": "fallback (B200_PROFILING.md)"}
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
@@ -663,6 +839,15 @@ def roofline(stage_ms, B):
         peaks = {"hbm_gbs": float(m["hbm_gbs"]), "bf16_tflops": float(m["bf16_tflops"]), "src": "measured"}
     except (OSError, KeyError, ValueError):
         pass
+    return peaks
+
+
+def roofline(stage_ms, stage_sat, B):
+    """Roofline of the dominant stage kernel against MEASURED_PEAKS.json:
+    `achieved` from the stage's isolated launch time (one batch alone on the
+    GPU), `achieved_saturated` from its per-batch cost with 16 concurrent
+    copies (how the pipeline runs it)."""
+    peaks = _peaks()
     work = {  # name -> (bound, algorithmic units per launch, unit)
         "k1_boxes_crops": ("hbm", BYTES_K1_FRAME * B),
         "k2_encoder": ("tensor", FLOP_ENC_FRAME * B),
@@ -673,10 +858,13 @@ def roofline(stage_ms, B):
     dom = max(stage_ms, key=stage_ms.get)
     bound, amount = work[dom]
     sec = stage_ms[dom] / 1e3
+    sat_s = stage_sat.get(dom, 0.0) / 1e6
     if bound == "hbm":
-        achieved, peak, unit = amount / sec / 1e9, peaks["hbm_gbs"], "GB/s"
+        scale, peak, unit = 1e9, peaks["hbm_gbs"], "GB/s"
     else:
-        achieved, peak, unit = amount / sec / 1e12, peaks["bf16_tflops"], "TFLOP/s"
+        scale, peak, unit = 1e12, peaks["bf16_tflops"], "TFLOP/s"
+    achieved = amount / sec / scale
+    achieved_sat = amount / sat_s / scale if sat_s > 0 else None
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as fh:
@@ -687,12 +875,15 @@ def roofline(stage_ms, B):
         pass
     return {"kernel": dom, "bound": bound, "achieved": achieved, "peak": peak, "unit": unit,
             "frac": achieved / peak, "traffic": traffic, "peak_source": peaks["src"],
+            "achieved_saturated": achieved_sat, "frac_saturated": achieved_sat / peak if achieved_sat else None,
             "share_of_step": stage_ms[dom] / sum(stage_ms.values()),
+            "share_of_saturated_step": stage_sat.get(dom, 0.0) / max(stage_sat.get("sum", 0.0), 1e-9),
             "algorithmic_per_launch": amount, "launch_ms": stage_ms[dom]}
 
 
 def frame_latency(torch, pipe, images, kps, cfg, reps):
-    """p50 latency of one frame through the whole path (graph replay)."""
+    """p50 device latency of one HBM-resident frame through the whole path
+    (graph replay, CUDA events)."""
     outs = pipe.allocate_outputs(1, tail=True)
     st = torch.cuda.current_stream()
     for i in range(5):
@@ -702,99 +893,86 @@ def frame_latency(torch, pipe, images, kps, cfg, reps):
     for r in range(reps):
         a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a.record(st)
-        pipe.launch(images[0:1], kps[0:1], outs, cfg)
+        pipe.launch(images[r % 8:r % 8 + 1], kps[r % 8:r % 8 + 1], outs, cfg)
         b.record(st)
         b.synchronize()
         ts.append(a.elapsed_time(b))
     ts.sort()
-    return {"p50_ms": ts[len(ts) // 2], "p95_ms": ts[int(len(ts) * 0.95)], "reps": reps, "batch": 1}
+    return {"p50_ms": ts[len(ts) // 2], "p95_ms": ts[int(len(ts) * 0.95)], "reps": reps, "batch": 1,
+            "api": "graph replay of one HBM-resident frame (device time)"}
 
 
-def stream_run(torch, pipes, streams, images, kps, cfg, B, dist, world, rank, total):
-    """C5: a stream of `total` synthetic frames, rank r taking
-    the contiguous block [r*total/G, (r+1)*total/G) (frame i is bank frame
-    i % bank), batches of B spread over the in-flight pipelines, the SMPL
-    outputs (theta + joints, 142 floats per frame) collected per rank and
-    all-gathered over NCCL once at the end.  Strong scaling: frames/s of the
-    whole stream, first frame to gathered result, max over ranks."""
+def api_latency(torch, pipe, images, scenes, cfg, reps):
+    """p50 single-frame latency through the reference-shaped API:
+    Pipeline.run_smpl(image numpy (512, 512, 3), scene) -> host theta / SMPL
+    joints: host finiteness check, staging into pinned memory, one graph
+    replay (K1 gathers the crop footprints over PCIe), results read back.
+    Host wall clock around the call."""
+    host = [images[i].cpu().numpy() for i in range(8)]
+    for i in range(5):
+        pipe.run_smpl(host[i % 8], scenes[i % 8], cfg)
+    ts = []
+    for r in range(reps):
+        t0 = time.perf_counter()
+        pipe.run_smpl(host[r % 8], scenes[r % 8], cfg)
+        ts.append((time.perf_counter() - t0) * 1e3)
+    ts.sort()
+    return {"p50_ms": ts[len(ts) // 2], "p95_ms": ts[int(len(ts) * 0.95)], "reps": reps, "batch": 1,
+            "api": "Pipeline.run_smpl(numpy image, scene) -> numpy theta/joints (host wall clock)"}
+
+
+def stream_run(torch, pipes, lanes, images, kps, cfg, B, dist, world, rank, total):
+    """C5 on the GPU: stream_shard with the real pipelines.
+    Frame i of the stream is bank frame i % bank; batches of B spread over the
+    in-flight pipelines; the SMPL outputs all-gathered over NCCL once at the
+    end.  Strong scaling: frames/s of the whole stream, first frame to
+    gathered result, max over ranks."""
     lo, hi = shard_bounds(total, rank, world)
-    n = hi - lo
     dev = images.device
     bank = images.shape[0]
-    res = torch.empty((max(n, 1), 142), dtype=torch.float32, device=dev)
     S = len(pipes)
     outs = [p_.allocate_outputs(B, tail=True) for p_ in pipes]
-    gathered = torch.empty((world * max(n, 1), 142), dtype=torch.float32, device=dev) if dist is not None else None
 
-    def batch(k, f0, nb):
-        j = k % S
-        with torch.cuda.stream(streams[j]):
-            s0 = f0 % bank
-            if s0 + nb <= bank:
-                img, kp = images[s0:s0 + nb], kps[s0:s0 + nb]
-            else:
-                idx = torch.arange(f0, f0 + nb, device=dev) % bank
-                img, kp = images[idx], kps[idx]
-            o = outs[j] if nb == B else pipes[j].allocate_outputs(nb, tail=True)
-            pipes[j].launch(img, kp, o, cfg)
-            r = f0 - lo
-            res[r:r + nb, :76].copy_(o["theta"])
-            res[r:r + nb, 76:].copy_(o["j_smpl"].reshape(nb, 66))
+    def frames_fn(f0, nb):
+        s0 = f0 % bank
+        if s0 + nb <= bank:
+            return images[s0:s0 + nb], kps[s0:s0 + nb]
+        idx = torch.arange(f0, f0 + nb, device=dev) % bank
+        return images[idx], kps[idx]
 
-    # warm-up: every (pipeline, input slot) pair the timed pass will use
-    # gets its CUDA graph captured first -- the input ring repeats with period
-    # lcm(pipelines, bank / B) batches, as a deployment's ring of frame buffers would
-    import math
+    def launch(j, img, kp, nb):
+        o = outs[j] if nb == B else pipes[j].allocate_outputs(nb, tail=True)
+        pipes[j].launch(img, kp, o, cfg)
+        return o["theta"], o["j_smpl"]
 
+    # warm-up: every (pipeline, input slot) pair the timed pass uses gets its
+    # CUDA graph captured first (the ring of frame buffers repeats)
     nslot = max(1, bank // B)
     period = S * nslot // math.gcd(S, nslot)
+    n = hi - lo
     for k in range(min(period, max(1, (n + B - 1) // B))):
         f0 = lo + k * B
-        batch(k, f0, min(B, hi - f0))
+        with lanes.lane(k % S):
+            launch(k % S, *frames_fn(f0, min(B, hi - f0)), min(B, hi - f0))
     torch.cuda.synchronize()
     if dist is not None:
         dist.barrier()
-    st = streams[0]
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(st)
-    for q in streams[1:]:
-        q.wait_event(e0)
-    k = 0
-    for f0 in range(lo, hi, B):
-        batch(k, f0, min(B, hi - f0))
-        k += 1
-    for q in streams[1:]:
-        ev = torch.cuda.Event()
-        ev.record(q)
-        st.wait_event(ev)
-    if dist is not None:
-        with torch.cuda.stream(st):
-            dist.all_gather_into_tensor(gathered, res)
-    e1.record(st)
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1)
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if dist is not None:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
+    gathered, ms = stream_shard(lanes, launch, frames_fn, B, dist, world, rank, total)
     return {"workload": "C5: %d-frame synthetic stream sharded over %d GPU(s) (%d frames on this rank), batches of %d "
                         "on %d in-flight pipelines, one all-gather of the SMPL outputs (theta + joints)"
                         % (total, world, n, B, S),
             "ms": ms, "frames_per_s": total / (ms / 1e3), "scaling": "strong",
-            "gathered_bytes_per_rank": int(n * 142 * 4)}
+            "gathered_rows": int(gathered.shape[0]), "gathered_bytes_per_rank": int(n * 142 * 4)}
 
 
 def verify_streams(torch, pipes, outs_s, images, kps, cfg, B, steps, nslot, S):
-    """Re-run the last step of every stream alone on pipeline 0 and compare
-    bit for bit with what the concurrent run produced."""
+    """Re-run the last step's batch of every lane alone on pipeline 0 and
+    compare bit for bit with what the concurrent run produced."""
     torch.cuda.synchronize()
     ref = pipes[0].allocate_outputs(B, tail=True)
     ok = True
     for j in range(S):
-        last = max(i for i in range(steps) if i % S == j) if steps > j else None
-        if last is None:
-            continue
-        s = last % nslot
+        s = ((steps - 1) * S + j) % nslot
         got = {k: outs_s[j][k].clone() for k in ("merged", "theta", "j_smpl")}
         pipes[0].launch(images[s * B:(s + 1) * B], kps[s * B:(s + 1) * B], ref, cfg)
         torch.cuda.synchronize()
@@ -805,23 +983,41 @@ def verify_streams(torch, pipes, outs_s, images, kps, cfg, B, steps, nslot, S):
 E2E_STREAMS = int(os.environ.get("FSB_E2E_STREAMS", "6"))
 
 
+def pinned_h2d_gbs(torch, dev, nbytes=256 << 20):
+    """Measured pinned host -> HBM copy bandwidth (the e2e roofline's
+    denominator): one 256 MB cudaMemcpyAsync, best of 3."""
+    h = torch.empty(nbytes // 4, dtype=torch.float32).pin_memory()
+    d = torch.empty(nbytes // 4, dtype=torch.float32, device=dev)
+    best = 0.0
+    for _ in range(3):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        d.copy_(h, non_blocking=True)
+        e1.record()
+        torch.cuda.synchronize()
+        best = max(best, nbytes / (e0.elapsed_time(e1) / 1e3) / 1e9)
+    return best
+
+
 def end_to_end(torch, pipes, images, kps, cfg, B, steps, warmup, dist, world):
     """Pipeline.run_batch on frames that live in pinned host memory (the
     reference's images are host float32 arrays).  K1 reads each frame in
     place over PCIe -- only the crop footprints (the rows and x-spans the
     three crops tap) cross the bus -- so there is no separate whole-frame
     H2D copy; steps rotate over E2E_STREAMS streams so one batch's gather
-    overlaps the others' compute.  Every step ends with a D2H read
-    of merged/theta/j_smpl into pinned host buffers.  h2d_bytes_per_step is
-    counted on the device by K1 (fsb_input_bytes) plus the keypoints.  Each
-    stream drives its own pipeline context (own workspace and graphs)."""
+    overlaps the others' compute.  Every step ends with a D2H read of
+    merged/theta/j_smpl into pinned host buffers; after the timed region every
+    context's non-finite flag is read (NumericError contract).  The host bank
+    (every frame of the HBM bank) is several times the 126 MB L2, so the crop
+    footprints cannot be served from L2.  h2d_bytes_per_step is counted on
+    the device by K1 (fsb_input_bytes) plus the keypoints."""
     NS = E2E_STREAMS
     pipes = list(pipes[:NS])
-    if len(pipes) < NS:
-        pipes += extra_pipelines(pipes[0], NS - len(pipes), pipes[0].precision)
+    while len(pipes) < NS:
+        pipes.append(pipes[0].fork())
     ctxs = [p_.context() for p_ in pipes]
     dev = images.device
-    nhost = min(images.shape[0], 4 * B)
+    nhost = min(images.shape[0], 256)
     h_img = images[:nhost].cpu().pin_memory()
     h_kp = kps[:nhost].cpu().pin_memory()
     nslot = nhost // B
@@ -837,7 +1033,7 @@ def end_to_end(torch, pipes, images, kps, cfg, B, steps, warmup, dist, world):
             for k in ("merged", "theta", "j_smpl"):
                 h_out[j][k].copy_(outs[j][k], non_blocking=True)
 
-    for i in range(max(warmup, NS * nslot)):
+    for i in range(max(warmup, NS * nslot // math.gcd(NS, nslot))):
         run(i)
     torch.cuda.synchronize()
     if dist is not None:
@@ -849,7 +1045,8 @@ def end_to_end(torch, pipes, images, kps, cfg, B, steps, warmup, dist, world):
     e0.record(streams[0])
     for q in streams[1:]:
         q.wait_event(e0)
-    for i in range(steps):
+    n_e2e = max(steps, 2 * nslot)  # every host frame at least twice
+    for i in range(n_e2e):
         run(i)
     for j in range(NS):
         tail[j].record(streams[j])
@@ -857,92 +1054,32 @@ def end_to_end(torch, pipes, images, kps, cfg, B, steps, warmup, dist, world):
     e1.record(streams[0])
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
+    for c in ctxs:  # the reference raises NumericError on non-finite results
+        c.check_finite("e2e")
     frame_bytes = sum(c.input_bytes(reset=True) for c in ctxs)
     # the host-side results of the last step of each stream equal a fresh
     # device-frame run of the same frames
     ok = True
     ref = pipes[0].allocate_outputs(B, tail=True)
-    for j in range(min(NS, steps)):
-        last = max(i for i in range(steps) if i % NS == j)
+    for j in range(min(NS, n_e2e)):
+        last = max(i for i in range(n_e2e) if i % NS == j)
         s = last % nslot
         pipes[0].launch(images[s * B:(s + 1) * B], kps[s * B:(s + 1) * B], ref, cfg)
         torch.cuda.synchronize()
         ok = ok and all(torch.equal(h_out[j][k], ref[k].cpu()) for k in ("merged", "theta", "j_smpl"))
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if dist is not None:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
-    h2d_b = frame_bytes // steps + B * 44 * 4
+    ms = max_over_ranks(dist, torch, ms, dev)
+    h2d_b = frame_bytes // n_e2e + B * 44 * 4
     d2h_b = B * (76 + 76 + 66) * 4
     full = B * (images[0].numel() + 44) * 4
-    return {"value": world * B * steps / (ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d_b,
-            "d2h_bytes_per_step": d2h_b, "ms_per_step": ms / steps,
+    peak = pinned_h2d_gbs(torch, dev)
+    achieved = h2d_b / (ms / n_e2e / 1e3) / 1e9
+    return {"value": world * B * n_e2e / (ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d_b,
+            "d2h_bytes_per_step": d2h_b, "ms_per_step": ms / n_e2e, "steps": n_e2e, "batch": B,
             "api": "Pipeline.run_batch on pinned host frames (K1 gathers the crop footprints over PCIe in "
-                   "place; %d streams)" % NS,
-            "h2d_fraction_of_frames": h2d_b / full, "outputs_verified": bool(ok)}
-
-
-def end_to_end_full_copy(torch, pipe, images, kps, cfg, B, steps, warmup, dist, world):
-    """Variant kept for comparison: whole frames copied H2D (copy stream,
-    double-buffered) before Pipeline.run_batch on device frames."""
-    dev = images.device
-    nhost = min(images.shape[0], 4 * B)
-    h_img = images[:nhost].cpu().pin_memory()
-    h_kp = kps[:nhost].cpu().pin_memory()
-    nslot = nhost // B
-    d_img = [torch.empty((B,) + tuple(images.shape[1:]), dtype=torch.float32, device=dev) for _ in range(2)]
-    d_kp = [torch.empty((B, 22, 2), dtype=torch.float32, device=dev) for _ in range(2)]
-    outs = [pipe.allocate_outputs(B, tail=True) for _ in range(2)]
-    h_out = [{k: torch.empty(outs[0][k].shape, dtype=torch.float32).pin_memory()
-              for k in ("merged", "theta", "j_smpl")} for _ in range(2)]
-    comp = torch.cuda.current_stream()
-    copy = torch.cuda.Stream(device=dev)
-    ready = [torch.cuda.Event() for _ in range(2)]
-    done = [torch.cuda.Event() for _ in range(2)]
-    for d in done:
-        d.record(comp)
-
-    def h2d(i):
-        j = i % 2
-        s = i % nslot
-        with torch.cuda.stream(copy):
-            copy.wait_event(done[j])
-            d_img[j].copy_(h_img[s * B:(s + 1) * B], non_blocking=True)
-            d_kp[j].copy_(h_kp[s * B:(s + 1) * B], non_blocking=True)
-            ready[j].record(copy)
-
-    def run(i):
-        j = i % 2
-        comp.wait_event(ready[j])
-        pipe.run_batch(d_img[j], d_kp[j], cfg, outputs=outs[j], sync=False)
-        for k in ("merged", "theta", "j_smpl"):
-            h_out[j][k].copy_(outs[j][k], non_blocking=True)
-        done[j].record(comp)
-
-    total = warmup + steps
-    h2d(0)
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    for i in range(total):
-        if i == warmup:
-            torch.cuda.synchronize()
-            if dist is not None:
-                dist.barrier()
-            e0.record(comp)
-        if i + 1 < total:
-            h2d(i + 1)
-        run(i)
-    e1.record(comp)
-    torch.cuda.synchronize()
-    ms = e0.elapsed_time(e1)
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if dist is not None:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms = float(t.item())
-    h2d_b = B * (images[0].numel() + 44) * 4
-    d2h_b = B * (76 + 76 + 66) * 4
-    return {"value": world * B * steps / (ms / 1e3), "unit": UNIT, "h2d_bytes_per_step": h2d_b,
-            "d2h_bytes_per_step": d2h_b, "ms_per_step": ms / steps,
-            "api": "Pipeline.run_batch after whole-frame H2D copies (copy stream double-buffered)"}
+                   "place; %d streams; %d-frame host bank, %.0f MB)" % (NS, nhost, nhost * 512 * 512 * 12 / 1e6),
+            "h2d_fraction_of_frames": h2d_b / full, "outputs_verified": bool(ok), "nonfinite_checked": True,
+            "roofline": {"bound": "pcie", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "peak_source": "measured pinned H2D cudaMemcpyAsync, 256 MB"}}
 
 
 if __name__ == "__main__":

@@ -74,6 +74,12 @@ typedef struct {
 
 /* ---- lifetime ---------------------------------------------------------- */
 int fsb_ctx_create(int device, fsb_ctx** out);
+/* a second context on model_owner's GPU that shares its uploaded model
+ * (decoder weights, templates, projector: one device copy) but owns its
+ * workspace, graphs, flags and counters -- one per in-flight stream
+ * (pipelines are per thread, the frozen model is not mutated).
+ * An upload through any sharing context is seen by all of them. */
+int fsb_ctx_create_shared(fsb_ctx* model_owner, fsb_ctx** out);
 void fsb_ctx_destroy(fsb_ctx* ctx);
 const char* fsb_last_error(const fsb_ctx* ctx);
 const char* fsb_build_info(void);
@@ -149,7 +155,10 @@ int fsb_project_vertices(fsb_ctx* ctx, const float* v_mhr, int B, int nv, float*
 /* fused MHR skin -> bridge -> projector -> SMPL FK from MHR parameters */
 int fsb_skin_project(fsb_ctx* ctx, const float* params, int B, float* v_mhr, float* theta, float* j_smpl,
                      float* v_smpl, int precision, void* stream);
-/* the whole frame -> SMPL path for B frames (SURVEY §3.2 composition) */
+/* the whole frame -> SMPL path for B frames (SURVEY §3.2 composition),
+ * replayed from a CUDA graph; with out->theta == out->j_smpl == NULL only the
+ * front half (boxes, crops, encode, decoders, merge: pipeline.Pipeline.run,
+ * pipeline.py:377-506) runs */
 int fsb_frame_batch(fsb_ctx* ctx, const float* images, int B, int H, int W, const float* kp, double alpha,
                     uint32_t body_sel, uint32_t hand_sel, int precision, const fsb_frame_outputs* out,
                     void* stream);
@@ -189,12 +198,15 @@ int fsb_denoise(fsb_ctx* ctx, const float* poses, int B, const float* w1, const 
 int fsb_render(fsb_ctx* ctx, const void* scenes, int B, int H, int W, float* out, void* stream);
 
 /* ---- diagnostics -------------------------------------------------------- */
-/* reads (and optionally clears) the device non-finite flag; synchronises */
+/* reads (and optionally clears) this context's non-finite flag; waits only
+ * for the work this context enqueued (an event per stream it used), never
+ * for the whole device */
 int fsb_nonfinite(fsb_ctx* ctx, int* flag, int reset);
 int fsb_counters(const fsb_ctx* ctx, fsb_counters_t* out);
 /* bytes of frame data the crop gather (K1) has read from pinned host frames
  * since the last reset, i.e. the bytes that crossed PCIe (only the crop
- * footprints are read; HBM-resident frames are not counted); synchronises */
+ * footprints are read; HBM-resident frames are not counted); waits for this
+ * context's work like fsb_nonfinite */
 int fsb_input_bytes(fsb_ctx* ctx, int64_t* total, int reset);
 /* number of kernels this context launched (graph replays count their nodes) */
 int64_t fsb_kernel_launches(const fsb_ctx* ctx);

@@ -143,7 +143,10 @@ def box_prompt(box, image_size):
 
 def frame_boxes(kp, image_size, alpha=3.0):
     """detect_stub(sigma=0) -> body box, two wrist hand boxes, prompt
-    (priors.py:179-195, pipeline.py:356-373, :318-329)."""
+    (priors.py:179-195, pipeline.py:356-373, :318-329).  detect_stub clips
+    the keypoints into the frame first (priors.py:188-190)."""
+    w, h = image_size
+    kp = np.clip(np.asarray(kp, F32), 0.0, [w - 1.0, h - 1.0]).astype(F32)
     b = body_box(kp, image_size)
     hands = [hand_box(kp[j], b, alpha, image_size) for j in WRISTS]
     return b, hands, box_prompt(b, image_size)

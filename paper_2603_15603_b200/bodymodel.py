@@ -78,17 +78,22 @@ def rodrigues(omega):
 # device templates for the functional API: one small context per template
 
 
-_TEMPLATE_CTX = {}
+_TEMPLATE_CTX = runtime.IdentityCache(cap=8)
 
 
 def _template_ctx(template):
-    key = (id(template), template.vertices_rest.ctypes.data, template.num_vertices)
-    ctx = _TEMPLATE_CTX.get(key)
-    if ctx is None:
+    """Device context holding `template`: keyed on the identity of the arrays
+    it uploaded (strong references, bounded LRU; the uploaded arrays are
+    frozen read-only, runtime.freeze)."""
+    objs = (template.vertices_rest, template.joints_rest, template.parents, template.skin_weights,
+            template.shape_basis)
+
+    def make():
         ctx = runtime.Context()
         ctx.load_template(runtime.FSB_MHR, template)
-        _TEMPLATE_CTX[key] = ctx
-    return ctx
+        return ctx
+
+    return _TEMPLATE_CTX.get(objs, int(template.num_vertices), make)
 
 
 def _poses(template, pose_vecs, torch):

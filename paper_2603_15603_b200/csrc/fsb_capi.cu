@@ -7,6 +7,7 @@
 #include <string.h>
 
 #include <map>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -110,13 +111,13 @@ struct GraphKey {
 
 }  // namespace
 
-struct fsb_ctx {
-  int device = 0;
-  std::string err;
-  int* d_flag = nullptr;
-  unsigned long long* d_bytes_in = nullptr;  // frame bytes K1 read (HBM or, for host frames, PCIe)
-  fsb_counters_t counters{};
-  int64_t launches = 0;
+// The uploaded model (decoder weights and their tcgen05 images, templates,
+// projector): read-only on the device once uploaded, so contexts created
+// with fsb_ctx_create_shared point at one copy (one per GPU) instead of one
+// per in-flight stream.  `version` counts uploads; a context whose graphs
+// and workspace were built against another version rebuilds them.
+struct fsb_model {
+  uint64_t version = 1;
   // decoder
   bool has_decoder = false;
   fsb_decoder_config cfg{};
@@ -128,8 +129,6 @@ struct fsb_ctx {
   // large-config encoder (non-default DecoderConfig, k_vit.cu)
   bool vit = false;
   VitW vitw;
-  DevMem vit_ws_mem;
-  VitWs vit_ws{};
   // templates / projector
   bool has_tmpl[2] = {false, false};
   DevMem tmpl_mem[2];
@@ -137,6 +136,26 @@ struct fsb_ctx {
   bool has_proj = false;
   DevMem proj_mem;
   ProjectorDev proj{};
+};
+
+struct fsb_ctx {
+  int device = 0;
+  std::string err;
+  int* d_flag = nullptr;
+  unsigned long long* d_bytes_in = nullptr;  // frame bytes K1 read (HBM or, for host frames, PCIe)
+  fsb_counters_t counters{};
+  int64_t launches = 0;
+  std::shared_ptr<fsb_model> mp;
+  fsb_model* m = nullptr;
+  uint64_t seen_version = 0;  // model version the workspace / graphs were built for
+  // streams this context enqueued work on (top-level calls), with an event
+  // recorded after the call: fsb_nonfinite / fsb_input_bytes wait on these
+  // instead of synchronising the whole device
+  std::vector<std::pair<cudaStream_t, cudaEvent_t>> done;
+  cudaStream_t aux = nullptr;  // private non-blocking stream for flag reads
+  // large-config encoder workspace
+  DevMem vit_ws_mem;
+  VitWs vit_ws{};
   // workspace
   int ws_frames = 0;
   DevMem ws;
@@ -199,7 +218,48 @@ bool capturing(cudaStream_t st) {
   return s != cudaStreamCaptureStatusNone;
 }
 
+// The (possibly shared) model was re-uploaded since this context built its
+// graphs and workspace: both are stale.
+void model_sync(fsb_ctx* c) {
+  if (c->seen_version == c->m->version) return;
+  c->drop_graphs();
+  c->ws_frames = 0;
+  c->vit_ws_mem.release();
+  c->vit_ws = VitWs{};
+  c->seen_version = c->m->version;
+}
+
+void model_changed(fsb_ctx* c) {
+  ++c->m->version;
+  model_sync(c);
+}
+
+// record "this context's work on `st` is enqueued up to here" (top-level,
+// non-capturing calls only; a captured graph records on its launch)
+void note_stream(fsb_ctx* c, cudaStream_t st) {
+  if (capturing(st)) return;
+  for (auto& d : c->done)
+    if (d.first == st) {
+      cudaEventRecord(d.second, st);
+      return;
+    }
+  cudaEvent_t ev = nullptr;
+  if (cudaEventCreateWithFlags(&ev, cudaEventDisableTiming) != cudaSuccess) return;
+  cudaEventRecord(ev, st);
+  c->done.push_back({st, ev});
+}
+
+// wait for this context's enqueued work only (not the whole device)
+cudaError_t wait_own_work(fsb_ctx* c) {
+  for (auto& d : c->done) {
+    cudaError_t e = cudaEventSynchronize(d.second);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
 int ensure_ws(fsb_ctx* c, int frames, cudaStream_t st) {
+  model_sync(c);
   if (frames <= c->ws_frames) return FSB_OK;
   if (capturing(st))
     return fail(c, FSB_ERR_USAGE, "workspace for %d frames not reserved before graph capture", frames);
@@ -279,12 +339,12 @@ int load_vit(fsb_ctx* c, const fsb_decoder_config& cfg, const std::map<std::stri
   if (!missing.empty()) return fail(c, FSB_ERR_SHAPE, "encoder weight table: missing or mis-sized '%s'", missing.c_str());
   c->vit_ws_mem.release();
   c->vit_ws = VitWs{};
-  FSB_CUDA(c, c->dec_mem.alloc(pk.host.size()));
-  FSB_CUDA(c, cudaMemcpy(c->dec_mem.p, pk.host.data(), pk.host.size(), cudaMemcpyHostToDevice));
-  const uint8_t* base = static_cast<const uint8_t*>(c->dec_mem.p);
+  FSB_CUDA(c, c->m->dec_mem.alloc(pk.host.size()));
+  FSB_CUDA(c, cudaMemcpy(c->m->dec_mem.p, pk.host.data(), pk.host.size(), cudaMemcpyHostToDevice));
+  const uint8_t* base = static_cast<const uint8_t*>(c->m->dec_mem.p);
   auto F = [&](const std::string& n) { return reinterpret_cast<const float*>(base + off.at(n)); };
   auto B = [&](const std::string& n) { return reinterpret_cast<const __nv_bfloat16*>(base + off.at(n)); };
-  VitW& w = c->vitw;
+  VitW& w = c->m->vitw;
   w.S = cfg.crop_size;
   w.p = p;
   w.D = D;
@@ -302,10 +362,10 @@ int load_vit(fsb_ctx* c, const fsb_decoder_config& cfg, const std::map<std::stri
                                 F(a + ".ln_b"), F(a + ".bqkv"), F(a + ".bo"), F(m + ".ln_g"), F(m + ".ln_b"),
                                 F(m + ".b1"), F(m + ".b2")});
   }
-  c->cfg = cfg;
-  c->has_decoder = true;
-  c->vit = true;
-  c->ws_frames = 0;
+  c->m->cfg = cfg;
+  c->m->has_decoder = true;
+  c->m->vit = true;
+  model_changed(c);
   return FSB_OK;
 }
 
@@ -315,13 +375,16 @@ extern "C" {
 
 const char* fsb_build_info(void) { return "fsb_b200 sm_100a (" __DATE__ ")"; }
 
-int fsb_ctx_create(int device, fsb_ctx** out) {
+static int ctx_new(int device, std::shared_ptr<fsb_model> model, fsb_ctx** out) {
   if (!out) return FSB_ERR_USAGE;
   *out = nullptr;
   cudaError_t e = cudaSetDevice(device);
   if (e != cudaSuccess) return FSB_ERR_CUDA;
   fsb_ctx* c = new fsb_ctx();
   c->device = device;
+  c->mp = model ? model : std::make_shared<fsb_model>();
+  c->m = c->mp.get();
+  c->seen_version = c->m->version;
   if (init_attrs_transformer() != cudaSuccess || init_attrs_transformer_tc() != cudaSuccess ||
       init_attrs_mlp_tc() != cudaSuccess || init_attrs_gemm_tc() != cudaSuccess ||
       init_attrs_body() != cudaSuccess || init_attrs_crops() != cudaSuccess) {
@@ -330,20 +393,30 @@ int fsb_ctx_create(int device, fsb_ctx** out) {
   }
   if (cudaMalloc(&c->d_flag, sizeof(int)) != cudaSuccess || cudaMemset(c->d_flag, 0, sizeof(int)) != cudaSuccess ||
       cudaMalloc(&c->d_bytes_in, sizeof(unsigned long long)) != cudaSuccess ||
-      cudaMemset(c->d_bytes_in, 0, sizeof(unsigned long long)) != cudaSuccess) {
-    delete c;
+      cudaMemset(c->d_bytes_in, 0, sizeof(unsigned long long)) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking) != cudaSuccess) {
+    fsb_ctx_destroy(c);
     return FSB_ERR_CUDA;
   }
   *out = c;
   return FSB_OK;
 }
 
+int fsb_ctx_create(int device, fsb_ctx** out) { return ctx_new(device, nullptr, out); }
+
+int fsb_ctx_create_shared(fsb_ctx* model_owner, fsb_ctx** out) {
+  if (!model_owner) return FSB_ERR_USAGE;
+  return ctx_new(model_owner->device, model_owner->mp, out);
+}
+
 void fsb_ctx_destroy(fsb_ctx* c) {
   if (!c) return;
   c->drop_graphs();
+  for (auto& d : c->done) cudaEventDestroy(d.second);
+  if (c->aux) cudaStreamDestroy(c->aux);
   if (c->d_flag) cudaFree(c->d_flag);
   if (c->d_bytes_in) cudaFree(c->d_bytes_in);
-  delete c;
+  delete c;  // the model is freed with its last context
 }
 
 const char* fsb_last_error(const fsb_ctx* c) { return c ? c->err.c_str() : "null context"; }
@@ -354,12 +427,13 @@ int fsb_set_graphs(fsb_ctx* c, int enabled) {
 }
 
 int fsb_reserve(fsb_ctx* c, int max_frames) {
+  model_sync(c);
   if (max_frames <= c->ws_frames) return FSB_OK;
-  const int S = c->has_decoder ? c->cfg.crop_size : 0;
-  const int T = c->has_decoder ? (S / c->cfg.patch) * (S / c->cfg.patch) : 0;
-  const int Dm = c->has_decoder ? c->cfg.dim : 0;
-  const int nsub = c->has_proj ? c->proj.n_sub : 1500;
-  const int h1 = c->has_proj ? c->proj.h1 : 512, h2 = c->has_proj ? c->proj.h2 : 256;
+  const int S = c->m->has_decoder ? c->m->cfg.crop_size : 0;
+  const int T = c->m->has_decoder ? (S / c->m->cfg.patch) * (S / c->m->cfg.patch) : 0;
+  const int Dm = c->m->has_decoder ? c->m->cfg.dim : 0;
+  const int nsub = c->m->has_proj ? c->m->proj.n_sub : 1500;
+  const int h1 = c->m->has_proj ? c->m->proj.h1 : 512, h2 = c->m->has_proj ? c->m->proj.h2 : 256;
   const size_t F = (size_t)max_frames;
   size_t off = 0;
   auto take = [&](size_t bytes) {
@@ -578,9 +652,9 @@ int fsb_load_decoder(fsb_ctx* c, const fsb_decoder_config* cfg, int n, const cha
     }
   }
   if (!ok) return fail(c, FSB_ERR_SHAPE, "decoder weight table: missing or mis-sized '%s'", missing.c_str());
-  FSB_CUDA(c, c->dec_mem.alloc(pk.host.size()));
-  FSB_CUDA(c, cudaMemcpy(c->dec_mem.p, pk.host.data(), pk.host.size(), cudaMemcpyHostToDevice));
-  const unsigned char* base = static_cast<const unsigned char*>(c->dec_mem.p);
+  FSB_CUDA(c, c->m->dec_mem.alloc(pk.host.size()));
+  FSB_CUDA(c, cudaMemcpy(c->m->dec_mem.p, pk.host.data(), pk.host.size(), cudaMemcpyHostToDevice));
+  const unsigned char* base = static_cast<const unsigned char*>(c->m->dec_mem.p);
   auto P = [&](const std::string& name) { return reinterpret_cast<const float*>(base + off.at(name)); };
   auto I = [&](const std::string& name) { return reinterpret_cast<const uint8_t*>(base + off.at(name)); };
   auto fill_attn = [&](AttnW& a, const std::string& p, bool cross) {
@@ -607,7 +681,7 @@ int fsb_load_decoder(fsb_ctx* c, const fsb_decoder_config* cfg, int n, const cha
     m.t_w1 = I(p + ".t_w1");
     m.t_w2 = I(p + ".t_w2");
   };
-  EncW& e = c->enc;
+  EncW& e = c->m->enc;
   e.t_patch = I("enc.t_patch");
   e.patch_w = P("enc.patch_w");
   e.patch_b = P("enc.patch_b");
@@ -621,7 +695,7 @@ int fsb_load_decoder(fsb_ctx* c, const fsb_decoder_config* cfg, int n, const cha
     fill_mlp(e.mlp[l], "enc.l" + std::to_string(l) + ".mlp");
     e.tc_params[l] = PT("enc.l" + std::to_string(l) + ".tcp");
   }
-  BodyW& b = c->body;
+  BodyW& b = c->m->body;
   b.token_init = P("body.token_init");
   b.p2d_init = P("body.p2d_init");
   b.p3d_init = P("body.p3d_init");
@@ -645,7 +719,7 @@ int fsb_load_decoder(fsb_ctx* c, const fsb_decoder_config* cfg, int n, const cha
     fill_mlp(b.mlp[l], p + ".mlp");
     b.tc_params[l] = PT(p + ".tcp");
   }
-  HandW& h = c->hand;
+  HandW& h = c->m->hand;
   h.token_init = P("hand.token_init");
   h.p_init = P("hand.p_init");
   h.norm_g = P("hand.norm_g");
@@ -712,20 +786,20 @@ int fsb_load_decoder(fsb_ctx* c, const fsb_decoder_config* cfg, int n, const cha
       if (ts[i].nw > FSB_TC_MAX_IMAGES)
         return fail(c, FSB_ERR_USAGE, "decoder too deep for the tcgen05 weight stream (%d images > %d)", ts[i].nw,
                     FSB_TC_MAX_IMAGES);
-    FSB_CUDA(c, c->tcs_mem.alloc(sizeof ts));
-    FSB_CUDA(c, cudaMemcpy(c->tcs_mem.p, ts, sizeof ts, cudaMemcpyHostToDevice));
-    const TcStream* dts = static_cast<const TcStream*>(c->tcs_mem.p);
+    FSB_CUDA(c, c->m->tcs_mem.alloc(sizeof ts));
+    FSB_CUDA(c, cudaMemcpy(c->m->tcs_mem.p, ts, sizeof ts, cudaMemcpyHostToDevice));
+    const TcStream* dts = static_cast<const TcStream*>(c->m->tcs_mem.p);
     e.tcs = dts;
     b.tcs = dts + 1;
     h.tcs = dts + 2;
   }
   // the body decoder's FK uses the decoder template's rest joints; the
   // body template upload patches it in (fsb_load_template)
-  c->body.joints_rest = c->has_tmpl[FSB_SMPL] ? c->tmpl[FSB_SMPL].joints_rest : nullptr;
-  c->cfg = *cfg;
-  c->has_decoder = true;
-  c->vit = false;
-  c->ws_frames = 0;  // re-reserve for the new shapes
+  c->m->body.joints_rest = c->m->has_tmpl[FSB_SMPL] ? c->m->tmpl[FSB_SMPL].joints_rest : nullptr;
+  c->m->cfg = *cfg;
+  c->m->has_decoder = true;
+  c->m->vit = false;
+  model_changed(c);
   return FSB_OK;
 }
 
@@ -794,11 +868,11 @@ int fsb_load_template(fsb_ctx* c, int which, int nv, const float* v_rest, const 
   const size_t o_jo = pk.add(joff.data(), joff.size() * 4);
   const size_t o_jv = pk.add(jv.data(), jv.size() * 4 + 4);
   const size_t o_jw = pk.add(jw.data(), jw.size() * 4 + 4);
-  DevMem& m = c->tmpl_mem[which];
+  DevMem& m = c->m->tmpl_mem[which];
   FSB_CUDA(c, m.alloc(pk.host.size()));
   FSB_CUDA(c, cudaMemcpy(m.p, pk.host.data(), pk.host.size(), cudaMemcpyHostToDevice));
   const unsigned char* base = static_cast<const unsigned char*>(m.p);
-  TemplateDev& t = c->tmpl[which];
+  TemplateDev& t = c->m->tmpl[which];
   t.nv = nv;
   t.nnz = NZ;
   t.v_rest = reinterpret_cast<const float*>(base + o_v);
@@ -810,9 +884,9 @@ int fsb_load_template(fsb_ctx* c, int which, int nv, const float* v_rest, const 
   t.joint_off = reinterpret_cast<const int*>(base + o_jo);
   t.joint_v = reinterpret_cast<const int*>(base + o_jv);
   t.joint_w = reinterpret_cast<const float*>(base + o_jw);
-  c->has_tmpl[which] = true;
-  if (which == FSB_SMPL) c->body.joints_rest = t.joints_rest;
-  c->drop_graphs();
+  c->m->has_tmpl[which] = true;
+  if (which == FSB_SMPL) c->m->body.joints_rest = t.joints_rest;
+  model_changed(c);
   return FSB_OK;
 }
 
@@ -855,10 +929,10 @@ int fsb_load_projector(fsb_ctx* c, int n_sub, int h1, int h2, const int64_t* cor
   const size_t o_i1 = pk.add(i1.data(), i1.size() * 2);
   const size_t o_i2 = pk.add(i2.data(), i2.size() * 2);
   const size_t o_i3 = pk.add(i3.data(), i3.size() * 2);
-  FSB_CUDA(c, c->proj_mem.alloc(pk.host.size()));
-  FSB_CUDA(c, cudaMemcpy(c->proj_mem.p, pk.host.data(), pk.host.size(), cudaMemcpyHostToDevice));
-  const unsigned char* base = static_cast<const unsigned char*>(c->proj_mem.p);
-  ProjectorDev& p = c->proj;
+  FSB_CUDA(c, c->m->proj_mem.alloc(pk.host.size()));
+  FSB_CUDA(c, cudaMemcpy(c->m->proj_mem.p, pk.host.data(), pk.host.size(), cudaMemcpyHostToDevice));
+  const unsigned char* base = static_cast<const unsigned char*>(c->m->proj_mem.p);
+  ProjectorDev& p = c->m->proj;
   p.n_sub = n_sub;
   p.h1 = h1;
   p.h2 = h2;
@@ -877,8 +951,8 @@ int fsb_load_projector(fsb_ctx* c, int n_sub, int h1, int h2, const int64_t* cor
   p.KT1 = (K + 127) / 128;
   p.KT2 = (h1 + 127) / 128;
   p.KT3 = (h2 + 127) / 128;
-  c->has_proj = true;
-  c->ws_frames = 0;
+  c->m->has_proj = true;
+  model_changed(c);
   return FSB_OK;
 }
 
@@ -908,6 +982,7 @@ int fsb_boxes_crops(fsb_ctx* c, const float* images, int B, int H, int W, const 
   FSB_CUDA(c, launch_boxes_crops(images, kp, B, H, W, S, alpha, host_frames, boxes, prompt, crops, taps, c->d_flag,
                                  c->d_bytes_in, (cudaStream_t)stream));
   c->launches += B > 0 ? (host_frames ? 1 : 2) : 0;  // HBM frames: k_frame_boxes + k_boxes_crops
+  note_stream(c, (cudaStream_t)stream);
   return FSB_OK;
 }
 
@@ -916,6 +991,7 @@ int fsb_bilinear(fsb_ctx* c, const float* image, int H, int W, int C, const floa
   if (H < 1 || W < 1 || C < 1 || n < 0) return fail(c, FSB_ERR_SHAPE, "bilinear: bad shapes");
   FSB_CUDA(c, launch_bilinear(image, H, W, C, grid, n, out, c->d_flag, (cudaStream_t)stream));
   c->launches += n > 0;
+  note_stream(c, (cudaStream_t)stream);
   return FSB_OK;
 }
 
@@ -923,6 +999,7 @@ int fsb_body_boxes(fsb_ctx* c, const float* kp, int n, int W, int H, double* out
   if (n < 0 || W < 2 || H < 2) return fail(c, FSB_ERR_SHAPE, "body_boxes: bad shapes");
   FSB_CUDA(c, launch_body_boxes(kp, n, W, H, out, (cudaStream_t)stream));
   c->launches += n > 0;
+  note_stream(c, (cudaStream_t)stream);
   return FSB_OK;
 }
 
@@ -931,6 +1008,7 @@ int fsb_hand_boxes(fsb_ctx* c, const double* wrists, const double* body, int n, 
   if (!(alpha > 0)) return fail(c, FSB_ERR_USAGE, "alpha must be positive");
   FSB_CUDA(c, launch_hand_boxes(wrists, body, n, alpha, W, H, out, (cudaStream_t)stream));
   c->launches += n > 0;
+  note_stream(c, (cudaStream_t)stream);
   return FSB_OK;
 }
 
@@ -938,6 +1016,7 @@ int fsb_crop_grid(fsb_ctx* c, const double* boxes, int n, int S, float* out, voi
   if (S < 2) return fail(c, FSB_ERR_USAGE, "out_size must be >= 2");
   FSB_CUDA(c, launch_crop_grid(boxes, n, S, out, (cudaStream_t)stream));
   c->launches += n > 0;
+  note_stream(c, (cudaStream_t)stream);
   return FSB_OK;
 }
 
@@ -946,13 +1025,15 @@ int fsb_bridge(fsb_ctx* c, const float* v, int B, int nv, const int32_t* corners
   if (B < 0 || nv <= 0 || nt < 0) return fail(c, FSB_ERR_SHAPE, "bridge: bad shapes");
   FSB_CUDA(c, launch_bridge(v, B, nv, corners, w, nt, out, (cudaStream_t)stream));
   c->launches += (int64_t)B * nt > 0;
+  note_stream(c, (cudaStream_t)stream);
   return FSB_OK;
 }
 
 int fsb_encode(fsb_ctx* c, const float* crops, int n, float* feats, int precision, void* stream) {
-  if (!c->has_decoder) return fail(c, FSB_ERR_USAGE, "encode: no decoder loaded");
+  if (!c->m->has_decoder) return fail(c, FSB_ERR_USAGE, "encode: no decoder loaded");
   if (precision != FSB_FP32 && precision != FSB_BF16) return fail(c, FSB_ERR_USAGE, "encode: bad precision %d", precision);
-  if (c->vit) {
+  model_sync(c);
+  if (c->m->vit) {
     if (precision != FSB_BF16)
       return fail(c, FSB_ERR_USAGE, "encode: the large-config encoder runs in bf16 only (precision='bf16')");
     if (n <= 0) return FSB_OK;
@@ -961,47 +1042,50 @@ int fsb_encode(fsb_ctx* c, const float* crops, int n, float* feats, int precisio
       if (capturing((cudaStream_t)stream))
         return fail(c, FSB_ERR_USAGE, "encode: encoder workspace for %d crops not allocated before graph capture", want);
       FSB_CUDA(c, cudaStreamSynchronize((cudaStream_t)stream));
-      FSB_CUDA(c, c->vit_ws_mem.alloc(vit_ws_bytes(c->vitw, want)));
-      vit_ws_carve(c->vitw, want, c->vit_ws_mem.p, &c->vit_ws);
+      FSB_CUDA(c, c->vit_ws_mem.alloc(vit_ws_bytes(c->m->vitw, want)));
+      vit_ws_carve(c->m->vitw, want, c->vit_ws_mem.p, &c->vit_ws);
     }
     int nl = 0;
-    FSB_CUDA(c, launch_vit_encoder(c->vitw, c->vit_ws, crops, n, feats, c->d_flag, (cudaStream_t)stream, &nl));
+    FSB_CUDA(c, launch_vit_encoder(c->m->vitw, c->vit_ws, crops, n, feats, c->d_flag, (cudaStream_t)stream, &nl));
     c->counters.encode += 1;
     c->counters.encoded_crops += n;
     c->launches += nl;
+    note_stream(c, (cudaStream_t)stream);
     return FSB_OK;
   }
-  if (!default_model(c->cfg))
+  if (!default_model(c->m->cfg))
     return fail(c, FSB_ERR_USAGE, "encode: the fused fp32 encoder supports the default DecoderConfig only");
   if (precision == FSB_BF16)
-    FSB_CUDA(c, launch_encoder_tc(crops, n, c->enc, feats, c->d_flag, (cudaStream_t)stream));
+    FSB_CUDA(c, launch_encoder_tc(crops, n, c->m->enc, feats, c->d_flag, (cudaStream_t)stream));
   else
-    FSB_CUDA(c, launch_encoder_f32(crops, n, c->enc, feats, c->d_flag, (cudaStream_t)stream));
+    FSB_CUDA(c, launch_encoder_f32(crops, n, c->m->enc, feats, c->d_flag, (cudaStream_t)stream));
   c->counters.encode += 1;
   c->counters.encoded_crops += n;
   c->launches += n > 0;
+  note_stream(c, (cudaStream_t)stream);
   return FSB_OK;
 }
 
 static int decode_common(fsb_ctx* c, DecodeArgs& a, int precision, cudaStream_t st) {
-  if (!c->has_decoder) return fail(c, FSB_ERR_USAGE, "decode: no decoder loaded");
-  if (a.nbody > 0 && !c->has_tmpl[FSB_SMPL])
+  if (!c->m->has_decoder) return fail(c, FSB_ERR_USAGE, "decode: no decoder loaded");
+  if (a.nbody > 0 && !c->m->has_tmpl[FSB_SMPL])
     return fail(c, FSB_ERR_USAGE, "decode: the body decoder needs its template (fsb_load_template SMPL)");
   if (precision != FSB_FP32 && precision != FSB_BF16) return fail(c, FSB_ERR_USAGE, "decode: bad precision %d", precision);
-  if (!default_model(c->cfg))
+  if (!default_model(c->m->cfg))
     return fail(c, FSB_ERR_USAGE, "decode: the fused fp32 decoders support the default DecoderConfig only");
-  if ((a.body_sel >> c->cfg.body_layers) != 0u || (a.hand_sel >> c->cfg.hand_layers) != 0u)
+  if ((a.body_sel >> c->m->cfg.body_layers) != 0u || (a.hand_sel >> c->m->cfg.hand_layers) != 0u)
     return fail(c, FSB_ERR_USAGE, "selection out of range");
   a.nonfinite = c->d_flag;
   if (precision == FSB_BF16)
-    FSB_CUDA(c, launch_decoders_tc(a, c->body, c->hand, st));
+    FSB_CUDA(c, launch_decoders_tc(a, c->m->body, c->m->hand, st));
   else
-    FSB_CUDA(c, launch_decoders_f32(a, c->body, c->hand, st));
+    FSB_CUDA(c, launch_decoders_f32(a, c->m->body, c->m->hand, st));
   c->launches += (a.nbody + a.nhand) > 0;
   const int nb = layer_count(a.body_sel);
   c->counters.fk += (int64_t)a.nbody * nb + (int64_t)a.nhand * layer_count(a.hand_sel);
   c->counters.project += (int64_t)a.nbody * nb + (int64_t)a.nhand * layer_count(a.hand_sel);
   c->counters.intermediate += (int64_t)a.nbody * nb;
+  note_stream(c, st);
   return FSB_OK;
 }
 
@@ -1053,21 +1137,23 @@ int fsb_decode_frames(fsb_ctx* c, const float* feats, int B, const float* prompt
 
 int fsb_fk(fsb_ctx* c, int which, const float* poses, int B, float* joints, float* rel, void* stream) {
   if (which != FSB_MHR && which != FSB_SMPL) return fail(c, FSB_ERR_USAGE, "bad template id");
-  if (!c->has_tmpl[which]) return fail(c, FSB_ERR_USAGE, "fk: template %d not loaded", which);
-  FSB_CUDA(c, launch_fk(poses, FSB_PARAM_DIM, B, c->tmpl[which].joints_rest, joints, rel, (cudaStream_t)stream));
+  if (!c->m->has_tmpl[which]) return fail(c, FSB_ERR_USAGE, "fk: template %d not loaded", which);
+  FSB_CUDA(c, launch_fk(poses, FSB_PARAM_DIM, B, c->m->tmpl[which].joints_rest, joints, rel, (cudaStream_t)stream));
   c->launches += B > 0;
+  note_stream(c, (cudaStream_t)stream);
   return FSB_OK;
 }
 
 int fsb_skin(fsb_ctx* c, int which, const float* poses, int B, float* verts, void* stream) {
   if (which != FSB_MHR && which != FSB_SMPL) return fail(c, FSB_ERR_USAGE, "bad template id");
-  if (!c->has_tmpl[which]) return fail(c, FSB_ERR_USAGE, "skin: template %d not loaded", which);
+  if (!c->m->has_tmpl[which]) return fail(c, FSB_ERR_USAGE, "skin: template %d not loaded", which);
   cudaStream_t st = (cudaStream_t)stream;
   int rc = ensure_ws(c, B, st);
   if (rc) return rc;
-  FSB_CUDA(c, launch_fk(poses, FSB_PARAM_DIM, B, c->tmpl[which].joints_rest, nullptr, c->w_rel, st));
-  FSB_CUDA(c, launch_lbs(c->tmpl[which], c->w_rel, poses, FSB_PARAM_DIM, B, verts, c->d_flag, st));
+  FSB_CUDA(c, launch_fk(poses, FSB_PARAM_DIM, B, c->m->tmpl[which].joints_rest, nullptr, c->w_rel, st));
+  FSB_CUDA(c, launch_lbs(c->m->tmpl[which], c->w_rel, poses, FSB_PARAM_DIM, B, verts, c->d_flag, st));
   c->launches += 2 * (B > 0);
+  note_stream(c, (cudaStream_t)stream);
   return FSB_OK;
 }
 
@@ -1075,10 +1161,10 @@ int fsb_skin(fsb_ctx* c, int which, const float* poses, int B, float* verts, voi
 // the K partition (and the bits of a mesh's output) never depend on B
 constexpr int kMlpGroup = 4;
 
-static bool mlp_tc(const fsb_ctx* c, int precision) { return precision == FSB_BF16 && c->proj.img_w1 != nullptr; }
+static bool mlp_tc(const fsb_ctx* c, int precision) { return precision == FSB_BF16 && c->m->proj.img_w1 != nullptr; }
 
 static int run_mlp(fsb_ctx* c, int B, float* theta, int precision, cudaStream_t st) {
-  const ProjectorDev& p = c->proj;
+  const ProjectorDev& p = c->m->proj;
   if (mlp_tc(c, precision)) {
     // relu(x W1 + b1) -> relu(h1 W2 + b2) -> (h2 W3 + b3) * mask on tcgen05;
     // each reduce writes the next layer's bf16 A-tile image
@@ -1104,42 +1190,44 @@ static int run_mlp(fsb_ctx* c, int B, float* theta, int precision, cudaStream_t 
 
 int fsb_project_vertices(fsb_ctx* c, const float* v_mhr, int B, int nv, float* theta, int precision,
                          void* stream) {
-  if (!c->has_proj) return fail(c, FSB_ERR_USAGE, "project: no projector loaded");
+  if (!c->m->has_proj) return fail(c, FSB_ERR_USAGE, "project: no projector loaded");
   if (nv <= 0) return fail(c, FSB_ERR_SHAPE, "project: bad vertex count");
   cudaStream_t st = (cudaStream_t)stream;
   int rc = ensure_ws(c, B, st);
   if (rc) return rc;
   const bool tc = mlp_tc(c, precision);
-  FSB_CUDA(c, launch_proj_inputs_v(v_mhr, nv, c->proj, B, c->w_x, !tc, tc ? c->w_xb : nullptr, c->w_psum, st));
+  FSB_CUDA(c, launch_proj_inputs_v(v_mhr, nv, c->m->proj, B, c->w_x, !tc, tc ? c->w_xb : nullptr, c->w_psum, st));
   c->launches += B > 0;  // bridge + centre in one kernel
-  return run_mlp(c, B, theta, precision, st);
+  rc = run_mlp(c, B, theta, precision, st);
+  if (rc == FSB_OK) note_stream(c, st);
+  return rc;
 }
 
 static int skin_project_impl(fsb_ctx* c, const float* params, int B, float* v_mhr, float* theta, float* j_smpl,
                              float* v_smpl, int precision, cudaStream_t st) {
-  if (!c->has_proj || !c->has_tmpl[FSB_MHR] || !c->has_tmpl[FSB_SMPL])
+  if (!c->m->has_proj || !c->m->has_tmpl[FSB_MHR] || !c->m->has_tmpl[FSB_SMPL])
     return fail(c, FSB_ERR_USAGE, "skin_project: projector or templates missing");
-  const TemplateDev& mhr = c->tmpl[FSB_MHR];
+  const TemplateDev& mhr = c->m->tmpl[FSB_MHR];
   FSB_CUDA(c, launch_fk(params, FSB_PARAM_DIM, B, mhr.joints_rest, nullptr, c->w_rel, st));
   if (v_mhr) FSB_CUDA(c, launch_lbs(mhr, c->w_rel, params, FSB_PARAM_DIM, B, v_mhr, c->d_flag, st));
   const bool tc = mlp_tc(c, precision);
   if (v_mhr && getenv("FSB_PROJ_RESKIN") == nullptr) {
     // V_mhr was just written: bridge its corner vertices (what the reference
     // projects, projection.py:447-465) instead of re-skinning them
-    FSB_CUDA(c, launch_proj_inputs_v(v_mhr, mhr.nv, c->proj, B, c->w_x, !tc, tc ? c->w_xb : nullptr, c->w_psum, st));
+    FSB_CUDA(c, launch_proj_inputs_v(v_mhr, mhr.nv, c->m->proj, B, c->w_x, !tc, tc ? c->w_xb : nullptr, c->w_psum, st));
     c->launches += 3;  // FK, LBS, bridge + centre
   } else {
-    FSB_CUDA(c, launch_proj_inputs(mhr, c->proj, c->w_rel, params, FSB_PARAM_DIM, B, c->w_x, !tc,
+    FSB_CUDA(c, launch_proj_inputs(mhr, c->m->proj, c->w_rel, params, FSB_PARAM_DIM, B, c->w_x, !tc,
                                    tc ? c->w_xb : nullptr, c->w_psum, st));
     c->launches += 3 + (v_mhr != nullptr);  // FK, (LBS), re-skinned inputs, centre
   }
   int rc = run_mlp(c, B, theta, precision, st);
   if (rc) return rc;
-  FSB_CUDA(c, launch_fk(theta, FSB_PARAM_DIM, B, c->tmpl[FSB_SMPL].joints_rest, j_smpl, v_smpl ? c->w_rel2 : nullptr,
+  FSB_CUDA(c, launch_fk(theta, FSB_PARAM_DIM, B, c->m->tmpl[FSB_SMPL].joints_rest, j_smpl, v_smpl ? c->w_rel2 : nullptr,
                         st));
   c->launches += 1;
   if (v_smpl) {
-    FSB_CUDA(c, launch_lbs(c->tmpl[FSB_SMPL], c->w_rel2, theta, FSB_PARAM_DIM, B, v_smpl, c->d_flag, st));
+    FSB_CUDA(c, launch_lbs(c->m->tmpl[FSB_SMPL], c->w_rel2, theta, FSB_PARAM_DIM, B, v_smpl, c->d_flag, st));
     c->launches += 1;
   }
   return FSB_OK;
@@ -1150,13 +1238,15 @@ int fsb_skin_project(fsb_ctx* c, const float* params, int B, float* v_mhr, float
   cudaStream_t st = (cudaStream_t)stream;
   int rc = ensure_ws(c, B, st);
   if (rc) return rc;
-  return skin_project_impl(c, params, B, v_mhr, theta, j_smpl, v_smpl, precision, st);
+  rc = skin_project_impl(c, params, B, v_mhr, theta, j_smpl, v_smpl, precision, st);
+  if (rc == FSB_OK) note_stream(c, st);
+  return rc;
 }
 
 static int frame_batch_launches(fsb_ctx* c, const float* images, int B, int H, int W, const float* kp, double alpha,
                                 uint32_t bsel, uint32_t hsel, int precision, const fsb_frame_outputs& o,
                                 cudaStream_t st) {
-  const int S = c->cfg.crop_size;
+  const int S = c->m->cfg.crop_size;
   double* boxes = o.boxes ? o.boxes : c->w_boxes;
   float* prompt = o.prompt ? o.prompt : c->w_prompt;
   float* crops = o.crops ? o.crops : c->w_crops;
@@ -1169,17 +1259,21 @@ static int frame_batch_launches(fsb_ctx* c, const float* images, int B, int H, i
   rc = fsb_encode(c, crops, 3 * B, feats, precision, st);
   if (rc) return rc;
   rc = fsb_decode_frames(c, feats, B, prompt, bsel, hsel, params, cam, rots, o.merged, precision, st);
-  if (rc) return rc;
+  if (rc || !o.theta) return rc;  // front half only (Pipeline.run without the SMPL tail)
   return skin_project_impl(c, o.merged, B, o.v_mhr, o.theta, o.j_smpl, o.v_smpl, precision, st);
 }
 
 int fsb_frame_batch(fsb_ctx* c, const float* images, int B, int H, int W, const float* kp, double alpha,
                     uint32_t body_sel, uint32_t hand_sel, int precision, const fsb_frame_outputs* out,
                     void* stream) {
-  if (!out || !out->merged || !out->theta || !out->j_smpl)
-    return fail(c, FSB_ERR_USAGE, "frame_batch: merged, theta and j_smpl outputs are required");
-  if (!c->has_decoder || !c->has_proj || !c->has_tmpl[0] || !c->has_tmpl[1])
-    return fail(c, FSB_ERR_USAGE, "frame_batch: decoder, templates and projector must be loaded");
+  if (!out || !out->merged || (!out->theta) != (!out->j_smpl))
+    return fail(c, FSB_ERR_USAGE, "frame_batch: merged is required, theta and j_smpl together or neither");
+  const bool tail = out->theta != nullptr;
+  if (!c->m->has_decoder || !c->m->has_tmpl[FSB_SMPL] || (tail && (!c->m->has_proj || !c->m->has_tmpl[FSB_MHR])))
+    return fail(c, FSB_ERR_USAGE, "frame_batch: decoder and SMPL template (and for the tail: MHR template and "
+                                  "projector) must be loaded");
+  if (!tail && (out->v_mhr || out->v_smpl))
+    return fail(c, FSB_ERR_USAGE, "frame_batch: v_mhr / v_smpl need the SMPL tail outputs");
   if (B <= 0) return FSB_OK;
   cudaStream_t st = (cudaStream_t)stream;
   int rc = ensure_ws(c, B, st);
@@ -1242,14 +1336,15 @@ int fsb_frame_batch(fsb_ctx* c, const float* images, int B, int H, int W, const 
   c->counters.fk += (int64_t)B * (nb + 2 * nh);
   c->counters.project += (int64_t)B * (nb + 2 * nh);
   c->counters.intermediate += (int64_t)B * nb;
+  note_stream(c, (cudaStream_t)stream);
   return FSB_OK;
 }
 
 int fsb_fit_batch(fsb_ctx* c, const float* target, int B, int nv, const float* init, int steps, double lr,
                   float lambda_pose, float lambda_shape, float* scratch, float* best_params, double* vertex_error,
                   double* err_curve, float* grad0, void* stream) {
-  if (!c->has_tmpl[FSB_SMPL]) return fail(c, FSB_ERR_USAGE, "fit_batch: no target template loaded (FSB_SMPL slot)");
-  const TemplateDev& t = c->tmpl[FSB_SMPL];
+  if (!c->m->has_tmpl[FSB_SMPL]) return fail(c, FSB_ERR_USAGE, "fit_batch: no target template loaded (FSB_SMPL slot)");
+  const TemplateDev& t = c->m->tmpl[FSB_SMPL];
   if (B < 0 || nv != t.nv) return fail(c, FSB_ERR_SHAPE, "fit_batch: targets have %d vertices, template %d", nv, t.nv);
   if (steps < 1) return fail(c, FSB_ERR_USAGE, "FitConfig.steps must be at least 1");
   if (!scratch || !best_params || !vertex_error || !err_curve)
@@ -1257,6 +1352,7 @@ int fsb_fit_batch(fsb_ctx* c, const float* target, int B, int nv, const float* i
   FSB_CUDA(c, launch_fit(t, target, B, init, steps, lr, lambda_pose, lambda_shape, scratch, best_params, vertex_error,
                          err_curve, grad0, c->d_flag, (cudaStream_t)stream));
   c->launches += B > 0;
+  note_stream(c, (cudaStream_t)stream);
   return FSB_OK;
 }
 
@@ -1267,6 +1363,7 @@ int fsb_bary_map(fsb_ctx* c, const double* src_verts, int nv, const int64_t* src
   FSB_CUDA(c, launch_bary(src_verts, src_faces, F, tgt_verts, nt, degenerate, face_index, weights,
                           (cudaStream_t)stream));
   c->launches += 2 * (nt > 0);
+  note_stream(c, (cudaStream_t)stream);
   return FSB_OK;
 }
 
@@ -1276,6 +1373,7 @@ int fsb_denoise(fsb_ctx* c, const float* poses, int B, const float* w1, const fl
   if (hidden <= 0 || hidden > 128) return fail(c, FSB_ERR_USAGE, "denoise: hidden width %d not in [1, 128]", hidden);
   FSB_CUDA(c, launch_denoise(poses, B, w1, b1, w2, b2, hidden, out, c->d_flag, (cudaStream_t)stream));
   c->launches += B > 0;
+  note_stream(c, (cudaStream_t)stream);
   return FSB_OK;
 }
 
@@ -1283,14 +1381,16 @@ int fsb_render(fsb_ctx* c, const void* scenes, int B, int H, int W, float* out, 
   if (B < 0 || H < 1 || W < 1) return fail(c, FSB_ERR_SHAPE, "render: bad shapes");
   FSB_CUDA(c, launch_render(scenes, B, H, W, out, (cudaStream_t)stream));
   c->launches += B > 0;
+  note_stream(c, (cudaStream_t)stream);
   return FSB_OK;
 }
 
 int fsb_nonfinite(fsb_ctx* c, int* flag, int reset) {
   int h = 0;
-  FSB_CUDA(c, cudaDeviceSynchronize());
-  FSB_CUDA(c, cudaMemcpy(&h, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost));
-  if (reset) FSB_CUDA(c, cudaMemset(c->d_flag, 0, sizeof(int)));
+  FSB_CUDA(c, wait_own_work(c));
+  FSB_CUDA(c, cudaMemcpyAsync(&h, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, c->aux));
+  if (reset) FSB_CUDA(c, cudaMemsetAsync(c->d_flag, 0, sizeof(int), c->aux));
+  FSB_CUDA(c, cudaStreamSynchronize(c->aux));
   if (flag) *flag = h;
   return FSB_OK;
 }
@@ -1298,9 +1398,10 @@ int fsb_nonfinite(fsb_ctx* c, int* flag, int reset) {
 int fsb_input_bytes(fsb_ctx* c, int64_t* total, int reset) {
   if (!c || !total) return FSB_ERR_USAGE;
   unsigned long long h = 0;
-  FSB_CUDA(c, cudaDeviceSynchronize());
-  FSB_CUDA(c, cudaMemcpy(&h, c->d_bytes_in, sizeof h, cudaMemcpyDeviceToHost));
-  if (reset) FSB_CUDA(c, cudaMemset(c->d_bytes_in, 0, sizeof h));
+  FSB_CUDA(c, wait_own_work(c));
+  FSB_CUDA(c, cudaMemcpyAsync(&h, c->d_bytes_in, sizeof h, cudaMemcpyDeviceToHost, c->aux));
+  if (reset) FSB_CUDA(c, cudaMemsetAsync(c->d_bytes_in, 0, sizeof h, c->aux));
+  FSB_CUDA(c, cudaStreamSynchronize(c->aux));
   *total = (int64_t)h;
   return FSB_OK;
 }

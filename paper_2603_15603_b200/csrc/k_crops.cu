@@ -80,6 +80,14 @@ __device__ void hand_box(double wx_f, double wy_f, const double body[4], double 
   out[3] = __dadd_rn(y0, sy);
 }
 
+// detect_stub (priors.py:188-190) clips the keypoints into the frame before
+// the body box: np.clip of float32 values against the integral bounds
+// [0, W-1] x [0, H-1] is exact in float32.  e = flat index into (22, 2).
+__device__ __forceinline__ float clip_kp(float v, int e, int W, int H) {
+  return fminf(fmaxf(v, 0.0f), (float)((e & 1) ? H - 1 : W - 1));
+}
+
+// kp: the frame's keypoints already clipped by clip_kp
 __device__ void frame_boxes(const float* kp, int W, int H, double alpha, FrameBoxes& fb) {
   body_box(kp, W, H, fb.box[0]);
   hand_box(kp[2 * 16], kp[2 * 16 + 1], fb.box[0], alpha, W, H, fb.box[1]);
@@ -116,7 +124,7 @@ __global__ void k_frame_boxes(const float* __restrict__ kps, int B, int W, int H
   if (f >= B) return;
   float kp[2 * FSB_NJ];
 #pragma unroll
-  for (int i = 0; i < 2 * FSB_NJ; ++i) kp[i] = kps[(int64_t)f * 2 * FSB_NJ + i];
+  for (int i = 0; i < 2 * FSB_NJ; ++i) kp[i] = clip_kp(kps[(int64_t)f * 2 * FSB_NJ + i], i, W, H);
   FrameBoxes fb;
   frame_boxes(kp, W, H, alpha, fb);
   for (int c = 0; c < 3; ++c)
@@ -222,7 +230,7 @@ __global__ void __launch_bounds__(kStreamThreads) k_crops_stream(
   const int r_begin = blockIdx.x * rows_per_cta;
   const int r_end = min(S, r_begin + rows_per_cta);
   if (r_begin >= S) return;
-  if (tid < 2 * FSB_NJ) kp_s[tid] = kps[(int64_t)f * 2 * FSB_NJ + tid];
+  if (tid < 2 * FSB_NJ) kp_s[tid] = clip_kp(kps[(int64_t)f * 2 * FSB_NJ + tid], tid, W, H);
   if (tid == 0) {
     tc::mbar_init(&bar[0], 1);
     tc::mbar_init(&bar[1], 1);

@@ -140,15 +140,19 @@ class Decoder:
     # -- device context ------------------------------------------------------
     def context(self, device=None):
         """The fsb_ctx holding this decoder's weights (uploaded lazily; a
-        changed weight table is re-uploaded)."""
+        changed weight table is re-uploaded).  The table is held by strong
+        reference and compared by identity plus its mutation counter (O(1):
+        the launch path calls this every batch); the uploaded arrays are
+        frozen read-only, so an in-place edit raises instead of running
+        with stale device weights."""
         w = self._weights
-        stamp = (id(w), w.version)  # O(1): the launch path calls this every batch
         if self._ctx is None:
             self._ctx = runtime.Context(device)
-        if self._uploaded != stamp:
+        up = self._uploaded
+        if up is None or up[0] is not w or up[1] != w.version:
             self._ctx.load_decoder(self.config, self.weights)
             self._ctx.load_template(runtime.FSB_SMPL, self.template)
-            self._uploaded = stamp
+            self._uploaded = (w, w.version)
         return self._ctx
 
     @property

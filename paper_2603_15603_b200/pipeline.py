@@ -277,18 +277,44 @@ class Pipeline:
             device = torch.cuda.current_device()
         self.device = device
         self.last_counters = {}
-        self._tail_loaded = None
+        self._parent = None
+        self._fork_ctx = None
+
+    def fork(self):
+        """Another pipeline over the same decoder and SMPL tail, with its own
+        device context (workspace, CUDA graphs, flags) that SHARES the
+        uploaded model: one per in-flight stream (SPEC.md:383 -- pipelines
+        are per thread; the frozen weights are not duplicated on the GPU)."""
+        p = Pipeline(self.decoder, mhr=self.mhr, bmap=self.bmap, projector=self.projector,
+                     precision=self.precision, device=self.device)
+        p._parent = self if self._parent is None else self._parent
+        return p
 
     # -- device setup ----------------------------------------------------------
-    def context(self):
-        ctx = self.decoder.context(self.device)
-        if self.mhr is not None and self._tail_loaded is not ctx:
-            if self.bmap is None or self.projector is None:
-                raise UsageError("the SMPL tail needs mhr, bmap and projector")
+    def _load_tail(self, ctx):
+        """Make sure the model context holds THIS pipeline's SMPL tail: the
+        loaded (mhr, bmap, projector) objects are recorded on the context and
+        compared by identity every call, so pipelines sharing a decoder with
+        different tails (or a reassigned pipe.projector) never run with
+        another's."""
+        if self.mhr is None:
+            return
+        if self.bmap is None or self.projector is None:
+            raise UsageError("the SMPL tail needs mhr, bmap and projector")
+        st = ctx.model_state
+        if st.get(("template", runtime.FSB_MHR)) is not self.mhr:
             ctx.load_template(runtime.FSB_MHR, self.mhr)
+        if st.get("projector", (None, None))[0] is not self.projector or st["projector"][1] is not self.bmap:
             ctx.load_projector(self.projector, self.bmap)
-            self._tail_loaded = ctx
-        return ctx
+
+    def context(self):
+        model = self.decoder.context(self.device)
+        self._load_tail(model)
+        if self._parent is None:
+            return model
+        if self._fork_ctx is None:
+            self._fork_ctx = runtime.Context(share=model)
+        return self._fork_ctx
 
     # -- batched entry -------------------------------------------------------
     def run_batch(self, images, keypoints, config=None, outputs=None, precision=None, sync=True):
@@ -340,41 +366,43 @@ class Pipeline:
         return o
 
     def launch(self, img, kp, out, cfg, precision=None):
-        """Enqueue the whole batch on the current stream (graph replay)."""
+        """Enqueue the whole batch on the current stream (one CUDA-graph
+        replay of fsb_frame_batch; without theta/j_smpl in `out` only the
+        front half -- boxes, crops, encoder, decoders, merge -- runs)."""
         ctx = self.context()
         prec = runtime.PRECISIONS[precision or self.precision]
         b, h, w = img.shape[:3]
         bsel, _ = dc.selection_mask(cfg.selection, self.decoder.config.body_layers)
         hsel, _ = dc.selection_mask(cfg.hand_selection, self.decoder.config.hand_layers, "hand selection")
-        if "theta" in out:
-            fo = runtime.FrameOutputsC(*[runtime.ptr(out.get(k)) for k, _ in runtime.FrameOutputsC._fields_])
-            ctx.check(ctx.lib.fsb_frame_batch(ctx.h, runtime.ptr(img), b, h, w, runtime.ptr(kp), float(cfg.alpha),
-                                              bsel, hsel, prec, fo, ctx.stream), "frame_batch")
-            return
-        # front half only (no SMPL tail): K1 -> K2 -> K3
-        torch = ctx.torch
-        s = self.crop_size
-        crops = out.get("crops")
-        if crops is None:
-            crops = torch.empty((b, 3, s, s, 3), dtype=torch.float32, device=torch.device("cuda", self.device))
-        feats = out.get("feats")
-        if feats is None:
-            feats = torch.empty((b, 3, self.decoder.n_tokens, self.decoder.config.dim), dtype=torch.float32,
-                                device=torch.device("cuda", self.device))
-        ctx.check(ctx.lib.fsb_boxes_crops(ctx.h, runtime.ptr(img), b, h, w, runtime.ptr(kp), float(cfg.alpha), s,
-                                          runtime.ptr(out["boxes"]), runtime.ptr(out["prompt"]), runtime.ptr(crops),
-                                          None, ctx.stream), "boxes_crops")
-        ctx.check(ctx.lib.fsb_encode(ctx.h, runtime.ptr(crops), 3 * b, runtime.ptr(feats), prec, ctx.stream),
-                  "encode")
-        ctx.check(ctx.lib.fsb_decode_frames(ctx.h, runtime.ptr(feats), b, runtime.ptr(out["prompt"]), bsel, hsel,
-                                            runtime.ptr(out["body_params"]), runtime.ptr(out["body_cam"]),
-                                            runtime.ptr(out["hand_rots"]), runtime.ptr(out["merged"]), prec,
-                                            ctx.stream), "decode_frames")
+        fo = runtime.FrameOutputsC(*[runtime.ptr(out.get(k)) for k, _ in runtime.FrameOutputsC._fields_])
+        ctx.check(ctx.lib.fsb_frame_batch(ctx.h, runtime.ptr(img), b, h, w, runtime.ptr(kp), float(cfg.alpha),
+                                          bsel, hsel, prec, fo, ctx.stream), "frame_batch")
 
     # -- one frame (reference API) ---------------------------------------------
-    def run(self, image, scene, config, plan=None):
-        """One frame -> (merged (76,), LatencyReport) (pipeline.py:377-506)."""
-        cfg = config
+    def _frame_state(self, h, w, tail):
+        """Per-pipeline single-frame buffers (allocated once per frame size):
+        a pinned staging frame that K1 gathers the crop footprints from in
+        place over PCIe, pinned keypoints, device outputs for B = 1 and pinned
+        host buffers the results are read back into."""
+        key = (h, w, tail)
+        st = getattr(self, "_fstate", None)
+        if st is not None and st["key"] == key:
+            return st
+        torch = self.context().torch
+        h_img = torch.empty((1, h, w, 3), dtype=torch.float32).pin_memory()
+        h_kp = torch.empty((1, 22, 2), dtype=torch.float32).pin_memory()
+        out = self.allocate_outputs(1, tail=tail, v_mhr=False)
+        names = ("prompt", "merged") + (("theta", "j_smpl") if tail else ())
+        host = {k: torch.empty(tuple(out[k].shape), dtype=torch.float32).pin_memory() for k in names}
+        st = {"key": key, "h_img": h_img, "img_np": h_img.numpy()[0], "h_kp": h_kp, "kp_np": h_kp.numpy()[0],
+              "out": out, "host": host, "ev": [torch.cuda.Event(enable_timing=True) for _ in range(3)]}
+        self._fstate = st
+        return st
+
+    def _run_one(self, image, scene, cfg, plan, tail):
+        """The single-frame path shared by run() and run_smpl(): host checks
+        and keypoints, one graph replay of the fused frame batch (B = 1) on
+        the pinned staging frame, one D2H read of the results."""
         _check_fast(cfg)
         if plan is None:
             plan = build_plan(cfg)
@@ -383,65 +411,70 @@ class Pipeline:
 
         allocs_before = plan.allocations
         t0 = time.perf_counter_ns()
-        image = np.ascontiguousarray(image, dtype=DTYPE)
-        check_finite(image, "bilinear_sample")
-        if cfg.noise_sigma != 0.0:
-            _, kp = pr.detect_stub(scene, cfg.noise_sigma, cfg.seed)
-            kpxy = kp.xy
-        else:
-            kpxy = np.asarray(scene.keypoints2d, DTYPE)
+        image = np.asarray(image, dtype=DTYPE)
         w, h = scene.image_size
-        if image.shape[:2] != (h, w):
+        if image.ndim != 3 or image.shape != (h, w, 3):
             raise ShapeError("image %r does not match scene size %r" % (image.shape, scene.image_size))
+        check_finite(image, "bilinear_sample")
+        with plan.stage("detect"):
+            if cfg.noise_sigma != 0.0:
+                _, kp = pr.detect_stub(scene, cfg.noise_sigma, cfg.seed)
+                kpxy = kp.xy
+            else:  # sigma = 0: the stub's clip into the frame happens in K1
+                kpxy = np.asarray(scene.keypoints2d, DTYPE)
         ctx = self.context()
         torch = ctx.torch
-        st = torch.cuda.current_stream()
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-        img = torch.from_numpy(image[None]).to(torch.device("cuda", self.device))
-        kp = torch.from_numpy(np.ascontiguousarray(kpxy[None])).to(img.device)
-        out = self._frame_bufs()
-        ev[0].record(st)
-        s = self.crop_size
-        prec = runtime.PRECISIONS[self.precision]
-        ctx.check(ctx.lib.fsb_boxes_crops(ctx.h, runtime.ptr(img), 1, h, w, runtime.ptr(kp), float(cfg.alpha), s,
-                                          runtime.ptr(out["boxes"]), runtime.ptr(out["prompt"]),
-                                          runtime.ptr(out["crops"]), None, ctx.stream), "boxes_crops")
-        ev[1].record(st)
-        ctx.check(ctx.lib.fsb_encode(ctx.h, runtime.ptr(out["crops"]), 3, runtime.ptr(out["feats"]), prec,
-                                     ctx.stream), "encode")
-        ev[2].record(st)
-        bsel, nb = dc.selection_mask(cfg.selection, self.decoder.config.body_layers)
-        hsel, nh = dc.selection_mask(cfg.hand_selection, self.decoder.config.hand_layers, "hand selection")
-        ctx.check(ctx.lib.fsb_decode_frames(ctx.h, runtime.ptr(out["feats"]), 1, runtime.ptr(out["prompt"]), bsel,
-                                            hsel, runtime.ptr(out["body_params"]), runtime.ptr(out["body_cam"]),
-                                            runtime.ptr(out["hand_rots"]), runtime.ptr(out["merged"]), prec,
-                                            ctx.stream), "decode_frames")
-        ev[3].record(st)
+        st = self._frame_state(h, w, tail)
+        np.copyto(st["img_np"], image)
+        st["kp_np"][...] = kpxy
+        stream = torch.cuda.current_stream()
+        ev = st["ev"]
+        ev[0].record(stream)
+        self.launch(st["h_img"], st["h_kp"], st["out"], cfg)
+        ev[1].record(stream)
+        for k, hb in st["host"].items():
+            hb.copy_(st["out"][k], non_blocking=True)
+        ev[2].record(stream)
+        ev[2].synchronize()
+        ctx.check_finite("run")
         prompt = plan.buffer("prompt", (dc.PROMPT_DIM,))
         merged = plan.buffer("merged", (PARAM_DIM,))
-        prompt[:] = out["prompt"][0].cpu().numpy()
-        merged[:] = out["merged"][0].cpu().numpy()
-        ctx.check_finite("run")
-        spans = [ev[i].elapsed_time(ev[i + 1]) for i in range(3)]
-        names = set(s_.name for s_ in plan.stages)
-        for (_, members), ms in zip(_STAGE_GROUPS, spans):
-            present = [m for m in members if m in names]
-            for i, m in enumerate(present):
-                plan.record(m, ms if i == len(present) - 1 else 0.0)
-        counters = {"encode": 1, "encoded_crops": 3, "fk": nb + 2 * nh, "project": nb + 2 * nh,
-                    "intermediate": nb}
+        prompt[:] = st["host"]["prompt"].numpy()[0]
+        merged[:] = st["host"]["merged"].numpy()[0]
+        # the fused graph has no stage boundaries: its device time is booked on
+        # the plan's last stage (merge); the host-side detect is timed above
+        dev_ms = ev[0].elapsed_time(ev[1])
+        names = [s_.name for s_ in plan.stages]
+        for m in names:
+            if m not in ("detect",):
+                plan.record(m, dev_ms if m == names[-1] else 0.0)
+        bsel, nb = dc.selection_mask(cfg.selection, self.decoder.config.body_layers)
+        hsel, nh = dc.selection_mask(cfg.hand_selection, self.decoder.config.hand_layers, "hand selection")
+        self.last_counters = {"encode": 1, "encoded_crops": 3, "fk": nb + 2 * nh, "project": nb + 2 * nh,
+                              "intermediate": nb}
         if plan.mode == FAST_STATIC and plan.warm and plan.allocations != allocs_before:
             raise UsageError("static plan allocated %d buffers in steady state" % (plan.allocations - allocs_before))
         plan.frame_done((time.perf_counter_ns() - t0) / 1e6)
-        self.last_counters = counters
+        return merged, plan, st
+
+    def run(self, image, scene, config, plan=None):
+        """One frame -> (merged (76,), LatencyReport) (pipeline.py:377-506).
+        `merged` aliases the plan's buffer, as in the reference."""
+        merged, plan, _ = self._run_one(image, scene, config, plan, tail=False)
         return merged, plan.latency_report()
 
-    def _frame_bufs(self):
-        bufs = getattr(self, "_fbufs", None)
-        if bufs is None:
-            bufs = self.allocate_outputs(1, tail=False, crops=True, feats=True)
-            self._fbufs = bufs
-        return bufs
+    def run_smpl(self, image, scene, config=None, plan=None):
+        """One frame through the whole SURVEY §3.2 composition (crop ->
+        encode -> decode -> MHR LBS -> projector -> SMPL FK) from a host
+        image to host results: dict(merged, theta, j_smpl) of numpy arrays
+        (copies), and the LatencyReport."""
+        if self.mhr is None:
+            raise UsageError("run_smpl needs the SMPL tail (mhr, bmap, projector)")
+        merged, plan, st = self._run_one(image, scene, config if config is not None else fast_config(), plan,
+                                         tail=True)
+        out = {"merged": merged.copy(), "theta": st["host"]["theta"].numpy()[0].copy(),
+               "j_smpl": st["host"]["j_smpl"].numpy()[0].copy()}
+        return out, plan.latency_report()
 
     def run_fast(self, image, scene, config=None):
         return self.run(image, scene, config if config is not None else fast_config())

@@ -54,18 +54,25 @@ def init_projector(subsample, hidden=(512, 256), seed=0):
                             w3=w3, b3=np.zeros(PARAM_DIM, DTYPE), subsample=idx, mask=_output_mask())
 
 
-_PROJ_CTX = {}
+_PROJ_CTX = runtime.IdentityCache(cap=8)
 
 
 def _projector_ctx(bmap, weights, nv):
-    key = (id(bmap), id(weights), nv)
-    ent = _PROJ_CTX.get(key)
-    if ent is None:
+    """Device context holding (weights, bmap): keyed on the identity of the
+    arrays it uploaded (strong references, bounded LRU) plus the subsample
+    contents, so a temporary ProjectorWeights over the same arrays (as
+    project_forward(subsample=...) builds) hits, and a different subsample
+    never reuses another's corner table."""
+    objs = (bmap.corners, bmap.weights, weights.w1, weights.b1, weights.w2, weights.b2, weights.w3, weights.b3,
+            weights.mask)
+    extra = (int(nv), np.asarray(weights.subsample, np.int64).tobytes())
+
+    def make():
         ctx = runtime.Context()
         ctx.load_projector(weights, bmap)
-        ent = (ctx, nv)
-        _PROJ_CTX[key] = ent
-    return ent[0]
+        return ctx
+
+    return _PROJ_CTX.get(objs, extra, make)
 
 
 def bridge(v_src, bmap):

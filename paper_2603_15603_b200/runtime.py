@@ -49,6 +49,7 @@ class FrameOutputsC(ctypes.Structure):
 # name -> (restype, argtypes); must match include/fsb_b200.h
 _SIGS = {
     "fsb_ctx_create": (_i, [_i, ctypes.POINTER(_p)]),
+    "fsb_ctx_create_shared": (_i, [_p, ctypes.POINTER(_p)]),
     "fsb_ctx_destroy": (None, [_p]),
     "fsb_last_error": (ctypes.c_char_p, [_p]),
     "fsb_build_info": (ctypes.c_char_p, []),
@@ -131,6 +132,42 @@ def exported_symbols():
     return sorted(_SIGS)
 
 
+def freeze(*arrays):
+    """Mark host arrays that were uploaded to the device read-only, so an
+    in-place edit (which the device copy would not see) fails loudly instead
+    of silently running with stale weights."""
+    for a in arrays:
+        if isinstance(a, np.ndarray) and a.flags.writeable:
+            try:
+                a.flags.writeable = False
+            except ValueError:
+                pass
+
+
+class IdentityCache:
+    """Small LRU of device objects keyed on the IDENTITY of host objects
+    (strong references: ids are never reused while an entry lives) plus a
+    hashable extra key.  Bounded, so temporary keys cannot leak contexts."""
+
+    def __init__(self, cap=8):
+        self.cap = cap
+        self.items = []
+
+    def get(self, objs, extra, make):
+        for i, (o, e, v) in enumerate(self.items):
+            if e == extra and len(o) == len(objs) and all(a is b for a, b in zip(o, objs)):
+                self.items.append(self.items.pop(i))
+                return v
+        v = make()
+        self.items.append((tuple(objs), extra, v))
+        if len(self.items) > self.cap:
+            self.items.pop(0)
+        return v
+
+    def clear(self):
+        self.items = []
+
+
 def _torch():
     import torch
 
@@ -151,15 +188,27 @@ _ERRORS = {1: ShapeError, 2: NumericError, 3: UsageError}
 
 
 class Context:
-    """One fsb_ctx on one GPU: uploaded models, workspace, graph cache."""
+    """One fsb_ctx on one GPU: uploaded models, workspace, graph cache.
 
-    def __init__(self, device=None):
+    Context(share=other) creates a context that shares `other`'s uploaded
+    model (one device copy of the weights, templates and projector) but owns
+    its workspace, CUDA graphs, non-finite flag and counters: one per
+    in-flight stream (fsb_ctx_create_shared)."""
+
+    def __init__(self, device=None, share=None):
         self.torch = _torch()
-        self.device = int(self.torch.cuda.current_device() if device is None else device)
         self.lib = lib()
         h = ctypes.c_void_p()
-        with self.torch.cuda.device(self.device):
-            rc = self.lib.fsb_ctx_create(self.device, ctypes.byref(h))
+        if share is not None:
+            self.device = share.device
+            with self.torch.cuda.device(self.device):
+                rc = self.lib.fsb_ctx_create_shared(share.h, ctypes.byref(h))
+            self.model_state = share.model_state  # what is loaded, shared with `share`
+        else:
+            self.device = int(self.torch.cuda.current_device() if device is None else device)
+            with self.torch.cuda.device(self.device):
+                rc = self.lib.fsb_ctx_create(self.device, ctypes.byref(h))
+            self.model_state = {}
         if rc != 0:
             raise RuntimeError("fsb_ctx_create failed (code %d)" % rc)
         self.h = h
@@ -223,6 +272,8 @@ class Context:
         cp = (ctypes.c_void_p * n)(*[a.ctypes.data for a in arrs])
         ce = (ctypes.c_int64 * n)(*[a.size for a in arrs])
         self.check(self.lib.fsb_load_decoder(self.h, ctypes.byref(c), n, cn, cp, ce), "load_decoder")
+        freeze(*[weights[k] for k in names])
+        self.model_state["decoder"] = (weights, getattr(weights, "version", None))
 
     def load_template(self, which, t):
         v = np.ascontiguousarray(t.vertices_rest, np.float32)
@@ -235,6 +286,8 @@ class Context:
         self.check(self.lib.fsb_load_template(self.h, which, v.shape[0], v.ctypes.data, g.ctypes.data,
                                               par.ctypes.data, sw.ctypes.data, sb.ctypes.data),
                    "load_template")
+        freeze(t.vertices_rest, t.joints_rest, t.parents, t.skin_weights, t.shape_basis)
+        self.model_state[("template", which)] = t
 
     def load_projector(self, weights, bmap):
         idx = np.asarray(weights.subsample, np.int64)
@@ -251,6 +304,9 @@ class Context:
         self.check(self.lib.fsb_load_projector(
             self.h, len(idx), h1, h2, corners.ctypes.data, bw.ctypes.data, w1.ctypes.data,
             *[a.ctypes.data for a in arrs]), "load_projector")
+        freeze(weights.w1, weights.b1, weights.w2, weights.b2, weights.w3, weights.b3, weights.mask,
+               weights.subsample, bmap.corners, bmap.weights)
+        self.model_state["projector"] = (weights, bmap)
 
 
 # ---------------------------------------------------------------------------

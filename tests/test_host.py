@@ -258,3 +258,81 @@ def test_gloo_two_rank_gather_of_sharded_frames():
     ids = np.arange(64, dtype=np.float32)
     assert np.array_equal(gathered, np.stack([ids * 1.5, ids + 0.25], axis=1))
     assert tmax == 2.0
+
+
+def _bench_shard_worker(rank, world, port, q):
+    """Runs bench.stream_shard -- the C5 code path bench.py drives on the GPU
+    (lanes, ragged last batch, per-rank result rows, ONE gather) -- on CPU
+    over gloo, with a stand-in pipeline whose SMPL outputs are a
+    deterministic function of the frame."""
+    import torch
+    import torch.distributed as dist
+
+    import bench
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    total, B, bank = 200, 32, 48
+    frames = torch.arange(bank, dtype=torch.float32)[:, None, None, None].expand(bank, 2, 2, 3).contiguous()
+    kps = torch.arange(bank, dtype=torch.float32)[:, None, None].expand(bank, 22, 2).contiguous()
+
+    def frames_fn(f0, nb):
+        idx = torch.arange(f0, f0 + nb) % bank
+        return frames[idx], kps[idx]
+
+    calls = []
+
+    def launch(j, img, kp, nb):  # stand-in for Pipeline.launch on lane j
+        calls.append((j, nb))
+        fid = img[:, 0, 0, 0]
+        theta = fid[:, None] * 0.5 + torch.arange(76, dtype=torch.float32)[None]
+        joints = kp[:, :, :1].expand(nb, 22, 3) + 0.25
+        return theta, joints
+
+    lanes = bench.Lanes(torch, 3, torch.device("cpu"))
+    gathered, ms = bench.stream_shard(lanes, launch, frames_fn, B, dist, world, rank, total)
+    if rank == 0:
+        q.put((gathered.numpy(), ms, calls))
+    dist.destroy_process_group()
+
+
+def test_bench_stream_shard_gloo_two_ranks():
+    import multiprocessing as mp
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_bench_shard_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    gathered, ms, calls = q.get(timeout=180)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    fid = (np.arange(200) % 48).astype(np.float32)
+    want = np.concatenate([fid[:, None] * 0.5 + np.arange(76, dtype=np.float32)[None],
+                           np.repeat(fid[:, None] + 0.25, 66, axis=1)], axis=1)
+    assert gathered.shape == (200, 142)
+    assert np.array_equal(gathered, want)
+    # rank 0 owns frames [0, 100): batches of 32, 32, 32, 4 round-robin over 3 lanes
+    assert calls == [(0, 32), (1, 32), (2, 32), (0, 4)]
+    assert ms >= 0.0
+
+
+def test_bench_self_spawns_torchrun():
+    """`bench.py --gpus N` outside torchrun re-executes itself under
+    torch.distributed.run with N ranks on 127.0.0.1."""
+    import bench
+
+    argv = bench.torchrun_argv(["--gpus", "4", "--steps", "20"], 4, 29555)
+    assert argv[1:3] == ["-m", "torch.distributed.run"]
+    assert argv[argv.index("--nproc-per-node") + 1] == "4"
+    assert argv[argv.index("--master-addr") + 1] == "127.0.0.1"
+    assert argv[-4:] == ["--gpus", "4", "--steps", "20"] and argv[-5].endswith("bench.py")
+    a = bench.parse(["--gpus", "4"])
+    assert a.gpus == 4 and a.steps >= 20 and a.warmup >= 3
