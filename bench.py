@@ -211,9 +211,10 @@ def stream_shard(lanes, launch, frames_fn, B, dist, world, rank, total, out_widt
     contiguous block [r*total/G, (r+1)*total/G); batches of B round-robin over
     the lanes; each batch's SMPL outputs (theta + joints) land in the rank's
     result rows; ONE all-gather of the rows at the end (the path's only
-    collective).  `launch(j, img, kp, nb)` enqueues a batch on lane j and
-    returns (theta (nb, 76), j_smpl (nb, 22, 3)); `frames_fn(f0, nb)` gives the
-    batch's frames.  Returns (gathered rows (total, 142), ms)."""
+    collective).  `launch(j, img, kp, nb, res, r)` enqueues a batch on lane j
+    and places its (theta (nb, 76) | joints (nb, 66)) into res[r:r + nb];
+    `frames_fn(f0, nb)` gives the batch's frames.  Returns (gathered rows
+    (total, 142), ms)."""
     torch = lanes.torch
     lo, hi = shard_bounds(total, rank, world)
     n = hi - lo
@@ -222,13 +223,8 @@ def stream_shard(lanes, launch, frames_fn, B, dist, world, rank, total, out_widt
     k = 0
     for f0 in range(lo, hi, B):
         nb = min(B, hi - f0)
-        j = k % lanes.n
-        with lanes.lane(j):
-            img, kp = frames_fn(f0, nb)
-            th, jj = launch(j, img, kp, nb)
-            r = f0 - lo
-            res[r:r + nb, :76].copy_(th)
-            res[r:r + nb, 76:].copy_(jj.reshape(nb, 66))
+        img, kp = frames_fn(f0, nb)
+        launch(k % lanes.n, img, kp, nb, res, f0 - lo)
         k += 1
     lanes.join()
     with lanes.main():
@@ -473,13 +469,18 @@ def main(argv=None):
     outs_s = [p_.allocate_outputs(B, tail=True) for p_ in pipes]
     cfg = pl.fast_config()
 
+    prepared = {}  # (lane, input slot) -> PreparedBatch (arguments bound once)
+
     def step(i):
         """One step: batch j of every in-flight pipeline (S * B frames),
         inputs cycling through the HBM bank (larger than L2)."""
         for j in range(S):
             s = (i * S + j) % nslot
-            with lanes.lane(j):
-                pipes[j].launch(images[s * B:(s + 1) * B], kps[s * B:(s + 1) * B], outs_s[j], cfg)
+            pb = prepared.get((j, s))
+            if pb is None:
+                pb = prepared[(j, s)] = pipes[j].prepare(images[s * B:(s + 1) * B], kps[s * B:(s + 1) * B],
+                                                         outs_s[j], cfg)
+            pb.launch(lanes.streams[j])
 
     def barrier():
         if dist is not None:
@@ -933,27 +934,58 @@ def stream_run(torch, pipes, lanes, images, kps, cfg, B, dist, world, rank, tota
     S = len(pipes)
     outs = [p_.allocate_outputs(B, tail=True) for p_ in pipes]
 
+    views = {}  # bank offset -> (frames, keypoints) views, built once
+
     def frames_fn(f0, nb):
         s0 = f0 % bank
         if s0 + nb <= bank:
-            return images[s0:s0 + nb], kps[s0:s0 + nb]
+            v = views.get((s0, nb))
+            if v is None:
+                v = views[(s0, nb)] = (images[s0:s0 + nb], kps[s0:s0 + nb])
+            return v
         idx = torch.arange(f0, f0 + nb, device=dev) % bank
         return images[idx], kps[idx]
 
-    def launch(j, img, kp, nb):
-        o = outs[j] if nb == B else pipes[j].allocate_outputs(nb, tail=True)
-        pipes[j].launch(img, kp, o, cfg)
-        return o["theta"], o["j_smpl"]
+    prepared = {}
+    import ctypes
+
+    cudart = ctypes.CDLL("libcudart.so.12")  # the runtime torch loaded (plumbing for the result copies)
+    cudart.cudaMemcpy2DAsync.argtypes = [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_size_t,
+                                         ctypes.c_size_t, ctypes.c_size_t, ctypes.c_int, ctypes.c_void_p]
+    D2D = 3  # cudaMemcpyDeviceToDevice
+
+    def place(st, o, nb, res, r):
+        """theta / joints of a batch into result rows r.. (two strided
+        cudaMemcpy2DAsync on the lane's stream: no torch dispatch per batch)"""
+        row = res.data_ptr() + r * 142 * 4
+        cudart.cudaMemcpy2DAsync(row, 142 * 4, o["theta"].data_ptr(), 76 * 4, 76 * 4, nb, D2D, st)
+        cudart.cudaMemcpy2DAsync(row + 76 * 4, 142 * 4, o["j_smpl"].data_ptr(), 66 * 4, 66 * 4, nb, D2D, st)
+
+    def launch(j, img, kp, nb, res, r):
+        st = lanes.streams[j]
+        if nb != B:  # the ragged last batch of a shard
+            with lanes.lane(j):
+                o = pipes[j].allocate_outputs(nb, tail=True)
+                pipes[j].launch(img, kp, o, cfg)
+        else:
+            key = (j, img.data_ptr())
+            pb = prepared.get(key)
+            if pb is None:
+                pb = prepared[key] = pipes[j].prepare(img, kp, outs[j], cfg)
+            pb.launch(st)
+            o = outs[j]
+        place(st.cuda_stream, o, nb, res, r)
 
     # warm-up: every (pipeline, input slot) pair the timed pass uses gets its
     # CUDA graph captured first (the ring of frame buffers repeats)
     nslot = max(1, bank // B)
     period = S * nslot // math.gcd(S, nslot)
     n = hi - lo
+    warm_res = torch.zeros((B, 142), dtype=torch.float32, device=dev)
     for k in range(min(period, max(1, (n + B - 1) // B))):
         f0 = lo + k * B
-        with lanes.lane(k % S):
-            launch(k % S, *frames_fn(f0, min(B, hi - f0)), min(B, hi - f0))
+        nb = min(B, hi - f0)
+        launch(k % S, *frames_fn(f0, nb), nb, warm_res, 0)
     torch.cuda.synchronize()
     if dist is not None:
         dist.barrier()

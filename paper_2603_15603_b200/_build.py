@@ -19,9 +19,9 @@ import sys
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
-OBJ = os.path.join(ROOT, "build", "obj")
+OBJ = os.environ.get("FSB_OBJ_DIR") or os.path.join(ROOT, "build", "obj")
 LIB_DIR = os.path.join(PKG, "lib")
-LIB = os.path.join(LIB_DIR, "libfsb_b200.so")
+LIB = os.environ.get("FSB_LIB_OUT") or os.path.join(LIB_DIR, "libfsb_b200.so")  # A/B variants: FSB_LIB_OUT
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",

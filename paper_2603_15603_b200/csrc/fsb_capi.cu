@@ -27,7 +27,9 @@ cudaError_t launch_encoder_f32(const float* crops, int ncrops, const EncW& w, fl
                                cudaStream_t st);
 cudaError_t launch_decoders_f32(const DecodeArgs& a, const BodyW& bw, const HandW& hw, cudaStream_t st);
 cudaError_t launch_fk(const float* poses, int ld_pose, int B, const float* grest, float* joints, float* rel,
-                      cudaStream_t st);
+                      cudaStream_t st, uint8_t* lbs_in = nullptr);
+cudaError_t launch_lbs_tc(const TemplateDev& t, const uint8_t* lbs_in, int B, float* verts, int* nonfinite,
+                          cudaStream_t st);
 cudaError_t launch_lbs(const TemplateDev& t, const float* rel, const float* poses, int ld_pose, int B, float* verts,
                        int* nonfinite, cudaStream_t st);
 cudaError_t launch_proj_inputs(const TemplateDev& t, const ProjectorDev& p, const float* rel, const float* poses,
@@ -164,6 +166,7 @@ struct fsb_ctx {
         *w_rots = nullptr, *w_rel = nullptr, *w_rel2 = nullptr, *w_x = nullptr, *w_h1 = nullptr, *w_h2 = nullptr,
         *w_theta = nullptr, *w_part = nullptr, *w_psum = nullptr;
   __nv_bfloat16* w_xb = nullptr;  // projector input as a bf16 A-tile image
+  uint8_t *w_lbsin = nullptr, *w_lbsin2 = nullptr;  // k_lbs_tc chunk records (MHR, SMPL)
   unsigned char *w_h1img = nullptr, *w_h2img = nullptr;
   // graphs
   bool graphs = true;
@@ -465,6 +468,9 @@ int fsb_reserve(fsb_ctx* c, int max_frames) {
   const int hmax = h1 > h2 ? (h1 > 76 ? h1 : 76) : (h2 > 76 ? h2 : 76);
   const size_t o_part = take(F * 16 * (size_t)hmax * 4);  // split-K partials (<= 16 chunks)
   const size_t o_psum = take(F * 8 * 3 * 4);               // projector-input centroid partials
+  const size_t lbsin_bytes = (F + FSB_LBS_N - 1) / FSB_LBS_N * (size_t)FSB_LBS_REC_BYTES;
+  const size_t o_lbsin = take(lbsin_bytes);
+  const size_t o_lbsin2 = take(lbsin_bytes);
   c->drop_graphs();
   FSB_CUDA(c, c->ws.alloc(off));
   unsigned char* b = static_cast<unsigned char*>(c->ws.p);
@@ -489,6 +495,10 @@ int fsb_reserve(fsb_ctx* c, int max_frames) {
   c->w_theta = reinterpret_cast<float*>(b + o_theta);
   c->w_part = reinterpret_cast<float*>(b + o_part);
   c->w_psum = reinterpret_cast<float*>(b + o_psum);
+  // the shape images' K padding (k >= 10) and meshes past B stay zero
+  FSB_CUDA(c, cudaMemset(b + o_lbsin, 0, o_lbsin2 - o_lbsin + lbsin_bytes));
+  c->w_lbsin = b + o_lbsin;
+  c->w_lbsin2 = b + o_lbsin2;
   c->ws_frames = max_frames;
   return FSB_OK;
 }
@@ -858,6 +868,25 @@ int fsb_load_template(fsb_ctx* c, int which, int nv, const float* v_rest, const 
     }
   }
   joff[FSB_NJ] = (int)jv.size();
+  // bf16 hi / lo images of the shape basis per 256-vertex tile (k_lbs_tc):
+  // row i of parity e is vertex 2 i + e
+  const int ntiles = (nv + FSB_LBS_TILE - 1) / FSB_LBS_TILE;
+  std::vector<uint8_t> bimg((size_t)ntiles * FSB_LBS_BASIS_BYTES, 0);
+  for (int tile = 0; tile < ntiles; ++tile)
+    for (int i = 0; i < 128; ++i)
+      for (int e = 0; e < 2; ++e) {
+        const int v = tile * FSB_LBS_TILE + 2 * i + e;
+        if (v >= nv) continue;
+        for (int cc = 0; cc < 3; ++cc)
+          for (int k = 0; k < 10; ++k) {
+            const float x = shape_basis[(size_t)v * 30 + cc * 10 + k];
+            const __nv_bfloat16 hi = __float2bfloat16_rn(x);
+            const __nv_bfloat16 lo = __float2bfloat16_rn(x - __bfloat162float(hi));
+            uint8_t* base = bimg.data() + (size_t)tile * FSB_LBS_BASIS_BYTES + tc_kmajor_off(i, k, 16);
+            memcpy(base + (e * 6 + cc) * 4096, &hi, 2);
+            memcpy(base + (e * 6 + 3 + cc) * 4096, &lo, 2);
+          }
+      }
   Packer pk;
   const size_t o_v = pk.add(v_rest, (size_t)nv * 12);
   const size_t o_s = pk.add(shape_basis, (size_t)nv * 30 * 4);
@@ -868,6 +897,7 @@ int fsb_load_template(fsb_ctx* c, int which, int nv, const float* v_rest, const 
   const size_t o_jo = pk.add(joff.data(), joff.size() * 4);
   const size_t o_jv = pk.add(jv.data(), jv.size() * 4 + 4);
   const size_t o_jw = pk.add(jw.data(), jw.size() * 4 + 4);
+  const size_t o_bi = pk.add(bimg.data(), bimg.size());
   DevMem& m = c->m->tmpl_mem[which];
   FSB_CUDA(c, m.alloc(pk.host.size()));
   FSB_CUDA(c, cudaMemcpy(m.p, pk.host.data(), pk.host.size(), cudaMemcpyHostToDevice));
@@ -884,6 +914,7 @@ int fsb_load_template(fsb_ctx* c, int which, int nv, const float* v_rest, const 
   t.joint_off = reinterpret_cast<const int*>(base + o_jo);
   t.joint_v = reinterpret_cast<const int*>(base + o_jv);
   t.joint_w = reinterpret_cast<const float*>(base + o_jw);
+  t.basis_img = base + o_bi;
   c->m->has_tmpl[which] = true;
   if (which == FSB_SMPL) c->m->body.joints_rest = t.joints_rest;
   model_changed(c);
@@ -1144,15 +1175,36 @@ int fsb_fk(fsb_ctx* c, int which, const float* poses, int B, float* joints, floa
   return FSB_OK;
 }
 
+// FK (rel transforms + the k_lbs_tc chunk records) then LBS.  FSB_LBS_SIMT=1
+// selects the all-CUDA-core k_lbs (measured alternative).
+static bool lbs_simt() {
+  static const bool v = getenv("FSB_LBS_SIMT") != nullptr;
+  return v;
+}
+
+static int fk_lbs(fsb_ctx* c, int which, const float* poses, int B, float* rel, uint8_t* lbsin, float* joints,
+                  float* verts, cudaStream_t st) {
+  const TemplateDev& t = c->m->tmpl[which];
+  const bool tc = verts != nullptr && !lbs_simt();
+  FSB_CUDA(c, launch_fk(poses, FSB_PARAM_DIM, B, t.joints_rest, joints, rel, st, tc ? lbsin : nullptr));
+  c->launches += B > 0;
+  if (verts == nullptr) return FSB_OK;
+  if (tc)
+    FSB_CUDA(c, launch_lbs_tc(t, lbsin, B, verts, c->d_flag, st));
+  else
+    FSB_CUDA(c, launch_lbs(t, rel, poses, FSB_PARAM_DIM, B, verts, c->d_flag, st));
+  c->launches += B > 0;
+  return FSB_OK;
+}
+
 int fsb_skin(fsb_ctx* c, int which, const float* poses, int B, float* verts, void* stream) {
   if (which != FSB_MHR && which != FSB_SMPL) return fail(c, FSB_ERR_USAGE, "bad template id");
   if (!c->m->has_tmpl[which]) return fail(c, FSB_ERR_USAGE, "skin: template %d not loaded", which);
   cudaStream_t st = (cudaStream_t)stream;
   int rc = ensure_ws(c, B, st);
   if (rc) return rc;
-  FSB_CUDA(c, launch_fk(poses, FSB_PARAM_DIM, B, c->m->tmpl[which].joints_rest, nullptr, c->w_rel, st));
-  FSB_CUDA(c, launch_lbs(c->m->tmpl[which], c->w_rel, poses, FSB_PARAM_DIM, B, verts, c->d_flag, st));
-  c->launches += 2 * (B > 0);
+  rc = fk_lbs(c, which, poses, B, c->w_rel, c->w_lbsin, nullptr, verts, st);
+  if (rc) return rc;
   note_stream(c, (cudaStream_t)stream);
   return FSB_OK;
 }
@@ -1208,29 +1260,22 @@ static int skin_project_impl(fsb_ctx* c, const float* params, int B, float* v_mh
   if (!c->m->has_proj || !c->m->has_tmpl[FSB_MHR] || !c->m->has_tmpl[FSB_SMPL])
     return fail(c, FSB_ERR_USAGE, "skin_project: projector or templates missing");
   const TemplateDev& mhr = c->m->tmpl[FSB_MHR];
-  FSB_CUDA(c, launch_fk(params, FSB_PARAM_DIM, B, mhr.joints_rest, nullptr, c->w_rel, st));
-  if (v_mhr) FSB_CUDA(c, launch_lbs(mhr, c->w_rel, params, FSB_PARAM_DIM, B, v_mhr, c->d_flag, st));
+  int rc = fk_lbs(c, FSB_MHR, params, B, c->w_rel, c->w_lbsin, nullptr, v_mhr, st);
+  if (rc) return rc;
   const bool tc = mlp_tc(c, precision);
   if (v_mhr && getenv("FSB_PROJ_RESKIN") == nullptr) {
     // V_mhr was just written: bridge its corner vertices (what the reference
     // projects, projection.py:447-465) instead of re-skinning them
     FSB_CUDA(c, launch_proj_inputs_v(v_mhr, mhr.nv, c->m->proj, B, c->w_x, !tc, tc ? c->w_xb : nullptr, c->w_psum, st));
-    c->launches += 3;  // FK, LBS, bridge + centre
+    c->launches += 1;  // bridge + centre
   } else {
     FSB_CUDA(c, launch_proj_inputs(mhr, c->m->proj, c->w_rel, params, FSB_PARAM_DIM, B, c->w_x, !tc,
                                    tc ? c->w_xb : nullptr, c->w_psum, st));
-    c->launches += 3 + (v_mhr != nullptr);  // FK, (LBS), re-skinned inputs, centre
+    c->launches += 2;  // re-skinned inputs, centre
   }
-  int rc = run_mlp(c, B, theta, precision, st);
+  rc = run_mlp(c, B, theta, precision, st);
   if (rc) return rc;
-  FSB_CUDA(c, launch_fk(theta, FSB_PARAM_DIM, B, c->m->tmpl[FSB_SMPL].joints_rest, j_smpl, v_smpl ? c->w_rel2 : nullptr,
-                        st));
-  c->launches += 1;
-  if (v_smpl) {
-    FSB_CUDA(c, launch_lbs(c->m->tmpl[FSB_SMPL], c->w_rel2, theta, FSB_PARAM_DIM, B, v_smpl, c->d_flag, st));
-    c->launches += 1;
-  }
-  return FSB_OK;
+  return fk_lbs(c, FSB_SMPL, theta, B, v_smpl ? c->w_rel2 : nullptr, c->w_lbsin2, j_smpl, v_smpl, st);
 }
 
 int fsb_skin_project(fsb_ctx* c, const float* params, int B, float* v_mhr, float* theta, float* j_smpl,

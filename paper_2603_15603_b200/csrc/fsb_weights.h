@@ -148,7 +148,25 @@ struct TemplateDev {
   const int* joint_off;      // (23)
   const int* joint_v;        // vertex ids
   const float* joint_w;      // weights
+  // shape basis of each 256-vertex tile as bf16 hi / lo UMMA images for the
+  // tensor-core shape blend of k_lbs_tc (k_body.cu): per tile 12 x 4 KB =
+  // [even | odd vertices][hi | lo][x, y, z], each 128 rows x K = 16 K-major
+  // (row i = vertex 2 i + parity of the tile)
+  const uint8_t* basis_img;
 };
+
+// k_lbs_tc: vertices per tile (two per TMEM lane) and meshes per chunk
+#define FSB_LBS_TILE 256
+#ifndef FSB_LBS_N
+#define FSB_LBS_N 16
+#endif
+#define FSB_LBS_BASIS_BYTES (12 * 128 * 16 * 2)
+// per-chunk record written by k_fk (lbs_in): the chunk's joint transforms
+// interleaved by mesh pairs (float2 [N/2][22 * 12]) and its shape
+// coefficients as bf16 hi / lo images (N meshes x K = 16, K-major)
+#define FSB_LBS_REC_A2 (FSB_LBS_N / 2 * 22 * 12 * 8)
+#define FSB_LBS_REC_B (FSB_LBS_N * 16 * 2)
+#define FSB_LBS_REC_BYTES (FSB_LBS_REC_A2 + 2 * FSB_LBS_REC_B)
 
 // barycentric map + projector
 struct ProjectorDev {

@@ -17,9 +17,12 @@
 // ---------------------------------------------------------------------------
 // FK: one warp per pose.  rel (B, 22, 3, 4) = [R_world | t_world - R_world g]
 // ---------------------------------------------------------------------------
+// lbs_in (nullable): the k_lbs_tc chunk records (fsb_weights.h
+// FSB_LBS_REC_*): transforms interleaved by mesh pairs and the shape
+// coefficients split into bf16 hi + lo (hi = bf16(s), lo = bf16(s - hi)).
 __global__ void __launch_bounds__(128) k_fk(const float* __restrict__ poses, int ld_pose, int B,
                                             const float* __restrict__ grest, float* __restrict__ joints,
-                                            float* __restrict__ rel) {
+                                            float* __restrict__ rel, uint8_t* __restrict__ lbs_in) {
   __shared__ FKOut fk[4];
   __shared__ float pose_s[4][66];
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
@@ -41,6 +44,27 @@ __global__ void __launch_bounds__(128) k_fk(const float* __restrict__ poses, int
         r[4 * a + 3] = fk[warp].at[j][a];
       }
     }
+    if (lbs_in != nullptr) {
+      uint8_t* rec = lbs_in + (int64_t)(b / FSB_LBS_N) * FSB_LBS_REC_BYTES;
+      const int m = b % FSB_LBS_N;
+      float* a2 = reinterpret_cast<float*>(rec) + ((m >> 1) * FSB_NJ * 12 + j * 12) * 2 + (m & 1);
+      for (int a = 0; a < 3; ++a) {
+        a2[2 * (4 * a + 0)] = fk[warp].rw[j][3 * a + 0];
+        a2[2 * (4 * a + 1)] = fk[warp].rw[j][3 * a + 1];
+        a2[2 * (4 * a + 2)] = fk[warp].rw[j][3 * a + 2];
+        a2[2 * (4 * a + 3)] = fk[warp].at[j][a];
+      }
+    }
+  }
+  if (lbs_in != nullptr && lane < 16) {  // shape coefficient k = lane (zero padding k >= 10)
+    uint8_t* rec = lbs_in + (int64_t)(b / FSB_LBS_N) * FSB_LBS_REC_BYTES;
+    const int m = b % FSB_LBS_N, k = lane;
+    const float sv = k < 10 ? poses[(int64_t)b * ld_pose + 66 + k] : 0.0f;
+    const __nv_bfloat16 hi = __float2bfloat16_rn(sv);
+    const __nv_bfloat16 lo = __float2bfloat16_rn(sv - __bfloat162float(hi));
+    const uint32_t off = tc::kmajor_off(m, k, 16);
+    *reinterpret_cast<__nv_bfloat16*>(rec + FSB_LBS_REC_A2 + off) = hi;
+    *reinterpret_cast<__nv_bfloat16*>(rec + FSB_LBS_REC_A2 + FSB_LBS_REC_B + off) = lo;
   }
 }
 
@@ -194,9 +218,28 @@ __global__ void __launch_bounds__(kLbsThreads, FSB_LBS_MIN_BLOCKS) k_lbs(Templat
   VertexTmpl<NZ> vt[kLbsVPT];
   const int v0 = (blockIdx.x * kLbsThreads + threadIdx.x) * kLbsVPT;
 #pragma unroll
-  for (int q = 0; q < kLbsVPT; ++q)
-    if (v0 + q < t.nv) vt[q].load(t, v0 + q);
+  for (int q = 0; q < kLbsVPT; ++q) {
+    if (v0 + q < t.nv) {
+      vt[q].load(t, v0 + q);
+    } else {  // past the last vertex: harmless zeros (never stored)
+#pragma unroll
+      for (int z = 0; z < NZ; ++z) vt[q].j[z] = 0, vt[q].w[z] = 0.0f;
+#pragma unroll
+      for (int c = 0; c < 3; ++c) vt[q].vr[c] = 0.0f;
+#pragma unroll
+      for (int k = 0; k < 30; ++k) vt[q].sb[k] = 0.0f;
+    }
+  }
   const bool live = v0 < t.nv;
+  // adjacent vertices of a thread mostly share their joints: where every
+  // thread of the warp does, each transform row read from shared memory
+  // serves all kLbsVPT vertices (shared-memory wavefronts bound this kernel)
+  bool same = true;
+#pragma unroll
+  for (int q = 1; q < kLbsVPT; ++q)
+#pragma unroll
+    for (int z = 0; z < NZ; ++z) same = same && vt[q].j[z] == vt[0].j[z];
+  const bool reuse = __all_sync(0xffffffffu, same);
   // per-warp output staging: the warp's 64 vertices of a mesh are 192
   // consecutive floats in V; they leave as fully coalesced 128-byte rows
   // (a lane's own 6 floats at a 24-byte stride would touch 3x the L2 sectors)
@@ -222,43 +265,59 @@ __global__ void __launch_bounds__(kLbsThreads, FSB_LBS_MIN_BLOCKS) k_lbs(Templat
 #pragma unroll
         for (int k = 0; k < 10; ++k) sh[k] = st.S2[pr][k];
         float2 o[kLbsVPT][3];
+        // shaped rest positions: v_rest + basis . shape (accumulated onto v_rest)
+        float2 vs[kLbsVPT][3];
 #pragma unroll
-        for (int q = 0; q < kLbsVPT; ++q) {
-          const VertexTmpl<NZ>& V = vt[q];
-          if (!live) {  // lanes past the last vertex stage zeros (never stored)
-#pragma unroll
-            for (int a = 0; a < 3; ++a) o[q][a] = make_float2(0.0f, 0.0f);
-            continue;
-          }
-          // shaped rest position: v_rest + basis . shape (accumulated onto v_rest)
-          float2 vs[3];
+        for (int q = 0; q < kLbsVPT; ++q)
 #pragma unroll
           for (int c = 0; c < 3; ++c) {
-            float2 acc = make_float2(V.vr[c], V.vr[c]);
+            float2 acc = make_float2(vt[q].vr[c], vt[q].vr[c]);
 #pragma unroll
-            for (int k = 0; k < 10; ++k) acc = ffma2(make_float2(V.sb[10 * c + k], V.sb[10 * c + k]), sh[k], acc);
-            vs[c] = acc;
+            for (int k = 0; k < 10; ++k)
+              acc = ffma2(make_float2(vt[q].sb[10 * c + k], vt[q].sb[10 * c + k]), sh[k], acc);
+            vs[q][c] = acc;
           }
-          // sum_z w_z (R_z vs + t_z): each joint's transform applied, then
-          // weighted (24 FFMA2 for two joints instead of blending the 3 x 4
-          // transforms first, 33)
+        // sum_z w_z (R_z vs + t_z): each joint's transform applied, then
+        // weighted (24 FFMA2 for two joints instead of blending the 3 x 4
+        // transforms first, 33)
+        if (reuse) {
 #pragma unroll
           for (int z = 0; z < NZ; ++z) {
-            const float2 wz = make_float2(V.w[z], V.w[z]);
-            const float4* row = reinterpret_cast<const float4*>(&st.A2[pr][12 * V.j[z]]);
+            const float4* row = reinterpret_cast<const float4*>(&st.A2[pr][12 * vt[0].j[z]]);
 #pragma unroll
             for (int a = 0; a < 3; ++a) {
               const float4 r01 = row[2 * a], r23 = row[2 * a + 1];  // (R_a0, R_a1 | R_a2, t_a) x 2 meshes
-              float2 pa = ffma2(make_float2(r01.x, r01.y), vs[0], make_float2(r23.z, r23.w));
-              pa = ffma2(make_float2(r01.z, r01.w), vs[1], pa);
-              pa = ffma2(make_float2(r23.x, r23.y), vs[2], pa);
-              o[q][a] = ffma2(wz, pa, z == 0 ? make_float2(0.0f, 0.0f) : o[q][a]);
+#pragma unroll
+              for (int q = 0; q < kLbsVPT; ++q) {
+                float2 pa = ffma2(make_float2(r01.x, r01.y), vs[q][0], make_float2(r23.z, r23.w));
+                pa = ffma2(make_float2(r01.z, r01.w), vs[q][1], pa);
+                pa = ffma2(make_float2(r23.x, r23.y), vs[q][2], pa);
+                o[q][a] = ffma2(make_float2(vt[q].w[z], vt[q].w[z]), pa, z == 0 ? make_float2(0.0f, 0.0f) : o[q][a]);
+              }
             }
           }
+        } else {
+#pragma unroll
+          for (int q = 0; q < kLbsVPT; ++q)
+#pragma unroll
+            for (int z = 0; z < NZ; ++z) {
+              const float2 wz = make_float2(vt[q].w[z], vt[q].w[z]);
+              const float4* row = reinterpret_cast<const float4*>(&st.A2[pr][12 * vt[q].j[z]]);
+#pragma unroll
+              for (int a = 0; a < 3; ++a) {
+                const float4 r01 = row[2 * a], r23 = row[2 * a + 1];
+                float2 pa = ffma2(make_float2(r01.x, r01.y), vs[q][0], make_float2(r23.z, r23.w));
+                pa = ffma2(make_float2(r01.z, r01.w), vs[q][1], pa);
+                pa = ffma2(make_float2(r23.x, r23.y), vs[q][2], pa);
+                o[q][a] = ffma2(wz, pa, z == 0 ? make_float2(0.0f, 0.0f) : o[q][a]);
+              }
+            }
+        }
+#pragma unroll
+        for (int q = 0; q < kLbsVPT; ++q)
 #pragma unroll
           for (int a = 0; a < 3; ++a)
             if (v0 + q < t.nv) chk = ffma2(o[q][a], one2, chk);
-        }
         // mesh 2 pr (.x lanes) and 2 pr + 1 (.y lanes) through the warp's
         // staging rows
 #pragma unroll
@@ -287,6 +346,243 @@ __global__ void __launch_bounds__(kLbsThreads, FSB_LBS_MIN_BLOCKS) k_lbs(Templat
   }
   cp_async_wait0();
   if (live && nonfinite != nullptr && !(isfinite(chk.x) && isfinite(chk.y))) atomicOr(nonfinite, 1);
+}
+
+// ---------------------------------------------------------------------------
+// k_lbs_tc: LBS with the shape blend on the tensor cores.
+//
+// The shape offsets  off[b, v, c] = sum_k basis[v, c, k] * shape[b, k]
+// (bodymodel.py:350-356; 30 of the 57 FMA pairs per vertex pair of meshes in
+// the all-CUDA-core k_lbs) form a GEMM with K = 10: per 256-vertex tile and
+// chunk of FSB_LBS_N meshes, tcgen05.mma (M = 128 rows = the tile's even or
+// odd vertices, N = meshes, K = 16 padded) computes them into TMEM with a
+// bf16 hi / lo split of both operands (hi.hi + hi.lo + lo.hi; ~2^-16
+// relative per product) and fp32 accumulation.  The CUDA cores apply the 1-2
+// weighted joint transforms (FFMA2 over mesh pairs).
+//
+// Shared-memory wavefronts, not FLOPs, bound this kernel (ncu: L1 ~80 %): a
+// thread owns two ADJACENT vertices (TMEM lane i = vertices 2i, 2i + 1), so
+// where a warp's vertex pairs share their joints (warp-uniform test, decided
+// once from the template) each transform row read from shared memory serves
+// both; the vertex rows leave through per-warp staging as coalesced stores.
+//
+// grid (vertex tiles, chunk CTAs); 256 threads: warps w and w + 4 own TMEM
+// lane quadrant w % 4 (64 vertices) and take meshes [0, N/2) and [N/2, N) of
+// each chunk.
+// Per chunk: the k_fk record (transforms + shape images, one bulk copy) lands
+// in one of two stage buffers; thread 0 issues the next chunk's MMAs into the
+// other TMEM buffer while every thread applies the current one.
+// ---------------------------------------------------------------------------
+#ifndef FSB_LBS_WARPS
+#define FSB_LBS_WARPS 8
+#endif
+constexpr int kLtWarps = FSB_LBS_WARPS;   // 8: 2 CTAs per SM; 16: 1 CTA per SM, half the chunk barriers
+constexpr int kLtThreads = 32 * kLtWarps;
+constexpr int kLtN = FSB_LBS_N;
+constexpr int kLtCols = 2 * 3 * kLtN;     // TMEM columns per chunk buffer: [even x,y,z | odd x,y,z]
+constexpr int kLtTmem = 2 * kLtCols <= 256 ? 256 : 512;  // two chunk buffers, power of two
+constexpr int kLtHalf = kLtN / (kLtWarps / 4);  // meshes per warp and chunk
+constexpr int kLtRow = 2 * 32 * 3;        // staging floats per (warp, mesh): 64 vertices
+constexpr uint32_t kLtBasis = 0;
+constexpr uint32_t kLtStage = FSB_LBS_BASIS_BYTES;
+constexpr uint32_t kLtOut = kLtStage + 2 * FSB_LBS_REC_BYTES;  // per warp: 2 meshes x kLtRow
+constexpr uint32_t kLtSmem = kLtOut + kLtWarps * 2 * kLtRow * 4;
+static_assert(2 * kLtCols <= kLtTmem, "two chunk buffers in TMEM");
+static_assert(kLtHalf % 2 == 0, "mesh pairs per warp");
+
+template <int NZ>
+__device__ __forceinline__ void lbs_apply(const float2* pairA, const int* jj, const float* w, const float2* vs,
+                                          float2* o) {
+#pragma unroll
+  for (int z = 0; z < NZ; ++z) {
+    const float2 wz = make_float2(w[z], w[z]);
+    const float4* row = reinterpret_cast<const float4*>(pairA + 12 * jj[z]);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const float4 r01 = row[2 * a], r23 = row[2 * a + 1];  // (R_a0, R_a1 | R_a2, t_a) x 2 meshes
+      float2 pa = ffma2(make_float2(r01.x, r01.y), vs[0], make_float2(r23.z, r23.w));
+      pa = ffma2(make_float2(r01.z, r01.w), vs[1], pa);
+      pa = ffma2(make_float2(r23.x, r23.y), vs[2], pa);
+      o[a] = ffma2(wz, pa, z == 0 ? make_float2(0.0f, 0.0f) : o[a]);
+    }
+  }
+}
+
+template <int NZ>
+__global__ void __launch_bounds__(kLtThreads, 512 / kLtTmem)
+    k_lbs_tc(TemplateDev t, const uint8_t* __restrict__ lbs_in, int B, float* __restrict__ verts, int* nonfinite) {
+  extern __shared__ __align__(1024) uint8_t lsm[];
+  __shared__ __align__(8) uint64_t bar_basis, bar_stage[2], bar_mma[2];
+  __shared__ uint32_t tmem_base;
+  const int nchunks = (B + kLtN - 1) / kLtN;
+  const int c0 = blockIdx.y;
+  if (c0 >= nchunks) return;  // CTA-uniform
+  const int G = gridDim.y;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int quad = warp & 3, mh = warp >> 2;  // TMEM lane quadrant, mesh slice of the chunk
+  const int vw = blockIdx.x * FSB_LBS_TILE + 64 * quad;  // the warp's first vertex
+  const int va = vw + 2 * lane;                           // this thread's vertices va, va + 1
+  if (threadIdx.x == 0) {
+    tc::mbar_init(&bar_basis, 1);
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&bar_stage[i], 1);
+      tc::mbar_init(&bar_mma[i], 1);
+    }
+    tc::mbar_fence_init();
+  }
+  if (warp == 0) tc::tmem_alloc(&tmem_base, kLtTmem);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = tmem_base;
+  auto stage_in = [&](int chunk, int buf) {
+    tc::mbar_expect_tx(&bar_stage[buf], FSB_LBS_REC_BYTES);
+    tc::bulk_g2s(lsm + kLtStage + buf * FSB_LBS_REC_BYTES, lbs_in + (int64_t)chunk * FSB_LBS_REC_BYTES,
+                 FSB_LBS_REC_BYTES, &bar_stage[buf]);
+  };
+  if (threadIdx.x == 0) {
+    tc::mbar_expect_tx(&bar_basis, FSB_LBS_BASIS_BYTES);
+    tc::bulk_g2s(lsm + kLtBasis, t.basis_img + (int64_t)blockIdx.x * FSB_LBS_BASIS_BYTES, FSB_LBS_BASIS_BYTES,
+                 &bar_basis);
+    stage_in(c0, 0);
+    if (c0 + G < nchunks) stage_in(c0 + G, 1);
+  }
+  // the two vertices' rest positions and skin weights stay in registers
+  float vr[2][3], w[2][NZ];
+  int jj[2][NZ];
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    const int v = va + e;
+    const bool live = v < t.nv;
+#pragma unroll
+    for (int z = 0; z < NZ; ++z) {
+      w[e][z] = live ? __ldg(t.skin_w + (int64_t)v * NZ + z) : 0.0f;
+      jj[e][z] = live ? (int)t.skin_j[(int64_t)v * NZ + z] : 0;
+    }
+#pragma unroll
+    for (int c = 0; c < 3; ++c) vr[e][c] = live ? __ldg(t.v_rest + (int64_t)v * 3 + c) : 0.0f;
+  }
+  // every vertex pair of the warp has one joint set: one row read serves both
+  bool same = true;
+#pragma unroll
+  for (int z = 0; z < NZ; ++z) same = same && jj[0][z] == jj[1][z];
+  const bool reuse = __all_sync(0xffffffffu, same);
+  const uint32_t sbase = tc::smem_u32(lsm);
+  auto issue = [&](int buf) {  // D[e][c] = basis(e, c) . shape^T: hi.hi + hi.lo + lo.hi
+    const uint32_t bimg = sbase + kLtStage + buf * FSB_LBS_REC_BYTES + FSB_LBS_REC_A2;
+    const uint32_t id = tc::idesc_bf16(128, kLtN);
+#pragma unroll
+    for (int e = 0; e < 2; ++e)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) {
+        const uint32_t d = tmem + buf * kLtCols + (3 * e + c) * kLtN;
+        const uint32_t ahi = sbase + kLtBasis + (e * 6 + c) * 4096, alo = ahi + 3 * 4096;
+        tc::mma_bf16(d, tc::kmajor_desc(ahi, 16, 0), tc::kmajor_desc(bimg, 16, 0), id, false);
+        tc::mma_bf16(d, tc::kmajor_desc(ahi, 16, 0), tc::kmajor_desc(bimg + FSB_LBS_REC_B, 16, 0), id, true);
+        tc::mma_bf16(d, tc::kmajor_desc(alo, 16, 0), tc::kmajor_desc(bimg, 16, 0), id, true);
+      }
+    tc::mma_commit(&bar_mma[buf]);
+  };
+  if (threadIdx.x == 0) {
+    tc::mbar_wait(&bar_basis, 0);
+    tc::mbar_wait(&bar_stage[0], 0);
+    tc::fence_after();
+    issue(0);
+  }
+  float* stg = reinterpret_cast<float*>(lsm + kLtOut) + warp * 2 * kLtRow;
+  const int nfw = max(0, min(64, t.nv - vw)) * 3;  // floats of the warp's vertex block
+  const uint32_t tl = tmem + ((uint32_t)(32 * quad) << 16);
+  float2 chk = make_float2(0.0f, 0.0f);
+  for (int it = 0, ch = c0; ch < nchunks; ++it, ch += G) {
+    const int buf = it & 1;
+    if (threadIdx.x == 0 && ch + G < nchunks) {  // next chunk's MMAs into the other buffer
+      tc::mbar_wait(&bar_stage[buf ^ 1], (uint32_t)(((it + 1) >> 1) & 1));
+      tc::fence_after();
+      issue(buf ^ 1);
+    }
+    tc::mbar_wait(&bar_mma[buf], (uint32_t)((it >> 1) & 1));
+    tc::fence_after();
+    float off[2][3][kLtHalf];
+#pragma unroll
+    for (int e = 0; e < 2; ++e)
+#pragma unroll
+      for (int c = 0; c < 3; ++c) tc::tmem_ld8(tl + buf * kLtCols + (3 * e + c) * kLtN + kLtHalf * mh, off[e][c]);
+    const float2* A2 = reinterpret_cast<const float2*>(lsm + kLtStage + buf * FSB_LBS_REC_BYTES);
+    const int m0 = ch * kLtN + kLtHalf * mh;  // first mesh of this warp's half
+    const int nm = min(kLtHalf, B - m0);
+#pragma unroll
+    for (int p = 0; p < kLtHalf / 2; ++p) {
+      if (2 * p >= nm) continue;  // warp-uniform (the last chunk of a batch)
+      const float2* pairA = A2 + (kLtHalf / 2 * mh + p) * (FSB_NJ * 12);
+      float2 vs[2][3], o[2][3];
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+#pragma unroll
+        for (int c = 0; c < 3; ++c) vs[e][c] = make_float2(vr[e][c] + off[e][c][2 * p], vr[e][c] + off[e][c][2 * p + 1]);
+      if (reuse) {  // one read of each transform row for both vertices
+#pragma unroll
+        for (int z = 0; z < NZ; ++z) {
+          const float4* row = reinterpret_cast<const float4*>(pairA + 12 * jj[0][z]);
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            const float4 r01 = row[2 * a], r23 = row[2 * a + 1];
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              float2 pa = ffma2(make_float2(r01.x, r01.y), vs[e][0], make_float2(r23.z, r23.w));
+              pa = ffma2(make_float2(r01.z, r01.w), vs[e][1], pa);
+              pa = ffma2(make_float2(r23.x, r23.y), vs[e][2], pa);
+              const float2 wz = make_float2(w[e][z], w[e][z]);
+              o[e][a] = ffma2(wz, pa, z == 0 ? make_float2(0.0f, 0.0f) : o[e][a]);
+            }
+          }
+        }
+      } else {
+        lbs_apply<NZ>(pairA, jj[0], w[0], vs[0], o[0]);
+        lbs_apply<NZ>(pairA, jj[1], w[1], vs[1], o[1]);
+      }
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+        if (va + e < t.nv)
+#pragma unroll
+          for (int a = 0; a < 3; ++a) chk = ffma2(o[e][a], make_float2(1.0f, 1.0f), chk);
+      // the warp's 64 vertices of meshes m, m + 1 leave as coalesced rows
+      // through its staging buffer (2 x 192 floats).  Measured alternatives
+      // (DESIGN.md §4): cp.async.bulk of the 16-byte-aligned interior and
+      // 1-D TMA tensor stores of 188 / 192-float boxes (a mesh row of 18,439
+      // x 12 B is 16-byte aligned only for every fourth mesh) were slower
+      // (391 / 356 us vs 271 us at C3): ~750-byte bulk stores do not keep up.
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        float* row = stg + half * kLtRow + 6 * lane;  // this lane's 6 floats (2 vertices x 3)
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          const int e = (2 * q) / 3, a = (2 * q) % 3, e1 = (2 * q + 1) / 3, a1 = (2 * q + 1) % 3;
+          *reinterpret_cast<float2*>(row + 2 * q) =
+              half ? make_float2(o[e][a].y, o[e1][a1].y) : make_float2(o[e][a].x, o[e1][a1].x);
+        }
+      }
+      __syncwarp();
+      const int m = m0 + 2 * p;
+#pragma unroll
+      for (int half = 0; half < 2; ++half) {
+        if (2 * p + half >= nm) break;
+        float* dst = verts + ((int64_t)(m + half) * t.nv + vw) * 3;
+#pragma unroll
+        for (int i = 0; i < 6; ++i) {
+          const int idx = 32 * i + lane;
+          if (idx < nfw) __stcs(dst + idx, stg[half * kLtRow + idx]);
+        }
+      }
+      __syncwarp();  // the staging rows are rewritten by the next pair
+    }
+    tc::fence_before();
+    __syncthreads();  // TMEM buffer `buf` and stage buffer `buf` are free
+    if (threadIdx.x == 0 && ch + 2 * G < nchunks) stage_in(ch + 2 * G, buf);
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc(tmem, kLtTmem);
+  if (va < t.nv && nonfinite != nullptr && !(isfinite(chk.x) && isfinite(chk.y))) atomicOr(nonfinite, 1);
 }
 
 // ---------------------------------------------------------------------------
@@ -560,9 +856,29 @@ __global__ void k_splitk_reduce(const float* __restrict__ P, int S, int M, int N
 // launchers
 // ---------------------------------------------------------------------------
 cudaError_t launch_fk(const float* poses, int ld_pose, int B, const float* grest, float* joints, float* rel,
-                      cudaStream_t st) {
+                      cudaStream_t st, uint8_t* lbs_in) {
   if (B == 0) return cudaSuccess;
-  k_fk<<<(B + 3) / 4, 128, 0, st>>>(poses, ld_pose, B, grest, joints, rel);
+  k_fk<<<(B + 3) / 4, 128, 0, st>>>(poses, ld_pose, B, grest, joints, rel, lbs_in);
+  return cudaGetLastError();
+}
+
+// grid: (vertex tiles, chunk CTAs); each chunk CTA walks chunks y, y + G, ...
+// with G chosen so the grid fills ~2 CTAs per SM
+cudaError_t launch_lbs_tc(const TemplateDev& t, const uint8_t* lbs_in, int B, float* verts, int* nonfinite,
+                          cudaStream_t st) {
+  if (B == 0) return cudaSuccess;
+  if (t.basis_img == nullptr) return cudaErrorInvalidValue;
+  const int tiles = (t.nv + FSB_LBS_TILE - 1) / FSB_LBS_TILE;
+  const int nchunks = (B + kLtN - 1) / kLtN;
+  int G = (512 / kLtTmem) * 148 / tiles;  // whole waves
+  G = G < 1 ? 1 : (G > nchunks ? nchunks : G);
+  dim3 grid(tiles, G);
+  switch (t.nnz) {
+    case 2: k_lbs_tc<2><<<grid, kLtThreads, kLtSmem, st>>>(t, lbs_in, B, verts, nonfinite); break;
+    case 4: k_lbs_tc<4><<<grid, kLtThreads, kLtSmem, st>>>(t, lbs_in, B, verts, nonfinite); break;
+    case 8: k_lbs_tc<8><<<grid, kLtThreads, kLtSmem, st>>>(t, lbs_in, B, verts, nonfinite); break;
+    default: return cudaErrorInvalidValue;
+  }
   return cudaGetLastError();
 }
 
@@ -587,6 +903,9 @@ cudaError_t init_attrs_body() {
   cudaError_t e = cudaFuncSetAttribute(k_lbs<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_lbs<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e == cudaSuccess) e = cudaFuncSetAttribute(k_lbs<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_lbs_tc<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLtSmem);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_lbs_tc<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLtSmem);
+  if (e == cudaSuccess) e = cudaFuncSetAttribute(k_lbs_tc<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kLtSmem);
   return e;
 }
 

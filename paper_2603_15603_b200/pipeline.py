@@ -378,6 +378,18 @@ class Pipeline:
         ctx.check(ctx.lib.fsb_frame_batch(ctx.h, runtime.ptr(img), b, h, w, runtime.ptr(kp), float(cfg.alpha),
                                           bsel, hsel, prec, fo, ctx.stream), "frame_batch")
 
+    def prepare(self, img, kp, out, cfg=None, precision=None):
+        """A batch whose buffers are fixed (a ring of frame slots, as a video
+        stream or the benchmark has): validates shapes once and binds the
+        ctypes arguments, so each PreparedBatch.launch() costs one C call
+        (the CUDA-graph lookup and launch) instead of rebuilding them."""
+        cfg = cfg if cfg is not None else fast_config()
+        _check_fast(cfg)
+        b, h, w = img.shape[:3]
+        if tuple(kp.shape) != (b, 22, 2) or img.ndim != 4 or img.shape[3] != 3:
+            raise ShapeError("images (B, H, W, 3) and keypoints (B, 22, 2) expected")
+        return PreparedBatch(self, img, kp, out, cfg, precision)
+
     # -- one frame (reference API) ---------------------------------------------
     def _frame_state(self, h, w, tail):
         """Per-pipeline single-frame buffers (allocated once per frame size):
@@ -481,6 +493,35 @@ class Pipeline:
 
     def run_serial(self, image, scene):
         return self.run(image, scene, serial_config())
+
+
+class PreparedBatch:
+    """Pipeline.prepare(): fsb_frame_batch with pre-bound arguments.  The
+    decoder / tail uploads are still re-checked on every launch (identity and
+    version compares), so weight edits are never missed."""
+
+    def __init__(self, pipe, img, kp, out, cfg, precision):
+        self.pipe = pipe
+        self.keep = (img, kp, out)
+        ctx = pipe.context()
+        self.lib = ctx.lib
+        b, h, w = img.shape[:3]
+        bsel, _ = dc.selection_mask(cfg.selection, pipe.decoder.config.body_layers)
+        hsel, _ = dc.selection_mask(cfg.hand_selection, pipe.decoder.config.hand_layers, "hand selection")
+        self.fo = runtime.FrameOutputsC(*[runtime.ptr(out.get(k)) for k, _ in runtime.FrameOutputsC._fields_])
+        import ctypes
+
+        self.args = (runtime.ptr(img), b, h, w, runtime.ptr(kp), float(cfg.alpha), bsel, hsel,
+                     runtime.PRECISIONS[precision or pipe.precision], ctypes.byref(self.fo))
+        self.torch = ctx.torch
+
+    def launch(self, stream=None):
+        """Enqueue on `stream` (a torch stream; default: the current one)."""
+        ctx = self.pipe.context()
+        st = (stream or self.torch.cuda.current_stream()).cuda_stream
+        rc = self.lib.fsb_frame_batch(ctx.h, *self.args, st)
+        if rc:
+            ctx.check(rc, "frame_batch")
 
 
 # ---------------------------------------------------------------------------

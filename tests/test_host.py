@@ -283,12 +283,11 @@ def _bench_shard_worker(rank, world, port, q):
 
     calls = []
 
-    def launch(j, img, kp, nb):  # stand-in for Pipeline.launch on lane j
+    def launch(j, img, kp, nb, res, r):  # stand-in for Pipeline.launch on lane j + result placement
         calls.append((j, nb))
         fid = img[:, 0, 0, 0]
-        theta = fid[:, None] * 0.5 + torch.arange(76, dtype=torch.float32)[None]
-        joints = kp[:, :, :1].expand(nb, 22, 3) + 0.25
-        return theta, joints
+        res[r:r + nb, :76] = fid[:, None] * 0.5 + torch.arange(76, dtype=torch.float32)[None]
+        res[r:r + nb, 76:] = (kp[:, :, :1].expand(nb, 22, 3) + 0.25).reshape(nb, 66)
 
     lanes = bench.Lanes(torch, 3, torch.device("cpu"))
     gathered, ms = bench.stream_shard(lanes, launch, frames_fn, B, dist, world, rank, total)
