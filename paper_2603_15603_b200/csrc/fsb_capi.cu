@@ -13,6 +13,7 @@
 
 #include "../../include/fsb_b200.h"
 #include "fsb_common.cuh"
+#include "fsb_enc_f32.h"
 #include "fsb_vit.h"
 #include "fsb_weights.h"
 
@@ -128,9 +129,14 @@ struct fsb_model {
   EncW enc{};
   BodyW body{};
   HandW hand{};
-  // large-config encoder (non-default DecoderConfig, k_vit.cu)
+  // non-default DecoderConfig: the encoder as a layer pipeline, bf16 on the
+  // tensor cores (k_vit.cu, when the shape fits it) and fp32 on the CUDA
+  // cores (k_enc_f32.cu, any shape)
   bool vit = false;
+  bool vit_tc = false;
   VitW vitw;
+  DevMem encf32_mem;
+  EncF32W encw;
   // templates / projector
   bool has_tmpl[2] = {false, false};
   DevMem tmpl_mem[2];
@@ -155,9 +161,11 @@ struct fsb_ctx {
   // instead of synchronising the whole device
   std::vector<std::pair<cudaStream_t, cudaEvent_t>> done;
   cudaStream_t aux = nullptr;  // private non-blocking stream for flag reads
-  // large-config encoder workspace
+  // large-config encoder workspaces
   DevMem vit_ws_mem;
   VitWs vit_ws{};
+  DevMem encf32_ws_mem;
+  EncF32Ws encf32_ws{};
   // workspace
   int ws_frames = 0;
   DevMem ws;
@@ -229,6 +237,8 @@ void model_sync(fsb_ctx* c) {
   c->ws_frames = 0;
   c->vit_ws_mem.release();
   c->vit_ws = VitWs{};
+  c->encf32_ws_mem.release();
+  c->encf32_ws = EncF32Ws{};
   c->seen_version = c->m->version;
 }
 
@@ -273,11 +283,22 @@ int ensure_ws(fsb_ctx* c, int frames, cudaStream_t st) {
 // q|k|v stacked to (3D x D); fp32 biases, LayerNorm affine and positions.
 // Only the encoder is device-resident for such configs;
 // the decoders stay on the default configuration.
+int load_enc_f32(fsb_ctx* c, const fsb_decoder_config& cfg,
+                 const std::map<std::string, std::pair<const float*, int64_t>>& tab);
+
 int load_vit(fsb_ctx* c, const fsb_decoder_config& cfg, const std::map<std::string, std::pair<const float*, int64_t>>& tab) {
   const int D = cfg.dim, p = cfg.patch, K0 = p * p * 3;
-  if (D % 128 || D > 2048 || D / cfg.heads != 64 || D % cfg.heads || K0 % 64)
-    return fail(c, FSB_ERR_USAGE,
-                "large-config encoder needs dim %% 128 == 0 (<= 2048), head dim 64 and patch*patch*3 %% 64 == 0");
+  // fp32 (reference precision) tables first: any shape with a supported head dim
+  int rc = load_enc_f32(c, cfg, tab);
+  if (rc) return rc;
+  c->m->vit_tc = !(D % 128 || D > 2048 || D / cfg.heads != 64 || D % cfg.heads || K0 % 64);
+  if (!c->m->vit_tc) {  // bf16 encode will raise; fp32 runs
+    c->m->vit = true;
+    c->m->cfg = cfg;
+    c->m->has_decoder = true;
+    model_changed(c);
+    return FSB_OK;
+  }
   const int np = cfg.crop_size / p, T = np * np;
   Packer pk;
   std::map<std::string, size_t> off;
@@ -369,6 +390,92 @@ int load_vit(fsb_ctx* c, const fsb_decoder_config& cfg, const std::map<std::stri
   c->m->has_decoder = true;
   c->m->vit = true;
   model_changed(c);
+  return FSB_OK;
+}
+
+// fp32 tables of a non-default encoder (k_enc_f32.cu): the reference's
+// (in, out) matrices as they are, q|k|v concatenated to (D, 3D)
+int load_enc_f32(fsb_ctx* c, const fsb_decoder_config& cfg,
+                 const std::map<std::string, std::pair<const float*, int64_t>>& tab) {
+  const int D = cfg.dim, p = cfg.patch, K0 = p * p * 3;
+  if (!enc_f32_supported(D, cfg.heads))
+    return fail(c, FSB_ERR_USAGE, "encoder head dim %d not supported (16, 32, 64 or 128)",
+                cfg.heads ? D / cfg.heads : 0);
+  const int np = cfg.crop_size / p, T = np * np;
+  Packer pk;
+  std::map<std::string, size_t> off;
+  std::string missing;
+  auto find = [&](const std::string& name, int64_t n) -> const float* {
+    auto it = tab.find(name);
+    if (it == tab.end() || it->second.second != n) {
+      if (missing.empty()) missing = name;
+      return nullptr;
+    }
+    return it->second.first;
+  };
+  auto put = [&](const std::string& name, int64_t n) {
+    const float* a = find(name, n);
+    if (a) off[name] = pk.add(a, (size_t)n * 4);
+  };
+  put("enc.patch_w", (int64_t)K0 * D);
+  put("enc.patch_b", D);
+  put("enc.pos", (int64_t)T * D);
+  put("enc.norm_g", D);
+  put("enc.norm_b", D);
+  for (int l = 0; l < cfg.enc_layers; ++l) {
+    const std::string a = "enc.l" + std::to_string(l) + ".self", m = "enc.l" + std::to_string(l) + ".mlp";
+    const float *wq = find(a + ".wq", (int64_t)D * D), *wk = find(a + ".wk", (int64_t)D * D),
+                *wv = find(a + ".wv", (int64_t)D * D);
+    const float *bq = find(a + ".bq", D), *bk = find(a + ".bk", D), *bv = find(a + ".bv", D);
+    if (wq && wk && wv && bq && bk && bv) {
+      const size_t o = pk.add(nullptr, (size_t)D * 3 * D * 4);
+      float* w = reinterpret_cast<float*>(pk.host.data() + o);
+      for (int r = 0; r < D; ++r) {
+        memcpy(w + (size_t)r * 3 * D, wq + (size_t)r * D, D * 4);
+        memcpy(w + (size_t)r * 3 * D + D, wk + (size_t)r * D, D * 4);
+        memcpy(w + (size_t)r * 3 * D + 2 * D, wv + (size_t)r * D, D * 4);
+      }
+      off[a + ".wqkv32"] = o;
+      std::vector<float> b(3 * (size_t)D);
+      memcpy(b.data(), bq, D * 4);
+      memcpy(b.data() + D, bk, D * 4);
+      memcpy(b.data() + 2 * D, bv, D * 4);
+      off[a + ".bqkv32"] = pk.add(b.data(), b.size() * 4);
+    }
+    put(a + ".wo", (int64_t)D * D);
+    put(a + ".bo", D);
+    put(a + ".ln_g", D);
+    put(a + ".ln_b", D);
+    put(m + ".ln_g", D);
+    put(m + ".ln_b", D);
+    put(m + ".w1", (int64_t)D * 4 * D);
+    put(m + ".b1", 4 * D);
+    put(m + ".w2", (int64_t)4 * D * D);
+    put(m + ".b2", D);
+  }
+  if (!missing.empty()) return fail(c, FSB_ERR_SHAPE, "encoder weight table: missing or mis-sized '%s'", missing.c_str());
+  FSB_CUDA(c, c->m->encf32_mem.alloc(pk.host.size()));
+  FSB_CUDA(c, cudaMemcpy(c->m->encf32_mem.p, pk.host.data(), pk.host.size(), cudaMemcpyHostToDevice));
+  const uint8_t* base = static_cast<const uint8_t*>(c->m->encf32_mem.p);
+  auto F = [&](const std::string& n) { return reinterpret_cast<const float*>(base + off.at(n)); };
+  EncF32W& w = c->m->encw;
+  w.S = cfg.crop_size;
+  w.p = p;
+  w.D = D;
+  w.H = cfg.heads;
+  w.T = T;
+  w.wpatch = F("enc.patch_w");
+  w.patch_b = F("enc.patch_b");
+  w.pos = F("enc.pos");
+  w.norm_g = F("enc.norm_g");
+  w.norm_b = F("enc.norm_b");
+  w.layers.clear();
+  for (int l = 0; l < cfg.enc_layers; ++l) {
+    const std::string a = "enc.l" + std::to_string(l) + ".self", m = "enc.l" + std::to_string(l) + ".mlp";
+    w.layers.push_back(EncF32Layer{F(a + ".wqkv32"), F(a + ".bqkv32"), F(a + ".wo"), F(a + ".bo"), F(a + ".ln_g"),
+                                   F(a + ".ln_b"), F(m + ".ln_g"), F(m + ".ln_b"), F(m + ".w1"), F(m + ".b1"),
+                                   F(m + ".w2"), F(m + ".b2")});
+  }
   return FSB_OK;
 }
 
@@ -1064,9 +1171,30 @@ int fsb_encode(fsb_ctx* c, const float* crops, int n, float* feats, int precisio
   if (!c->m->has_decoder) return fail(c, FSB_ERR_USAGE, "encode: no decoder loaded");
   if (precision != FSB_FP32 && precision != FSB_BF16) return fail(c, FSB_ERR_USAGE, "encode: bad precision %d", precision);
   model_sync(c);
+  if (c->m->vit && precision == FSB_FP32) {  // reference precision, any config (k_enc_f32.cu)
+    if (n <= 0) return FSB_OK;
+    constexpr int kF32Chunk = 64;
+    const int want = n < kF32Chunk ? n : kF32Chunk;
+    if (c->encf32_ws.max_crops < want) {
+      if (capturing((cudaStream_t)stream))
+        return fail(c, FSB_ERR_USAGE, "encode: encoder workspace for %d crops not allocated before graph capture", want);
+      FSB_CUDA(c, cudaStreamSynchronize((cudaStream_t)stream));
+      FSB_CUDA(c, c->encf32_ws_mem.alloc(enc_f32_ws_bytes(c->m->encw, want)));
+      enc_f32_ws_carve(c->m->encw, want, c->encf32_ws_mem.p, &c->encf32_ws);
+    }
+    int nl = 0;
+    FSB_CUDA(c, launch_enc_f32(c->m->encw, c->encf32_ws, crops, n, feats, c->d_flag, (cudaStream_t)stream, &nl));
+    c->counters.encode += 1;
+    c->counters.encoded_crops += n;
+    c->launches += nl;
+    note_stream(c, (cudaStream_t)stream);
+    return FSB_OK;
+  }
   if (c->m->vit) {
-    if (precision != FSB_BF16)
-      return fail(c, FSB_ERR_USAGE, "encode: the large-config encoder runs in bf16 only (precision='bf16')");
+    if (!c->m->vit_tc)
+      return fail(c, FSB_ERR_USAGE,
+                  "encode: the bf16 tensor-core encoder needs dim %% 128 == 0 (<= 2048), head dim 64 and "
+                  "patch*patch*3 %% 64 == 0; precision='fp32' runs any config");
     if (n <= 0) return FSB_OK;
     const int want = n < kVitChunk ? n : kVitChunk;
     if (c->vit_ws.max_crops < want) {

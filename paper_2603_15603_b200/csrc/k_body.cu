@@ -786,7 +786,7 @@ __global__ void __launch_bounds__(256) k_gemm_f32(const float* __restrict__ A, i
                                                    const float* __restrict__ W, const float* __restrict__ bias,
                                                    const float* __restrict__ mask, float* __restrict__ C, int ldc,
                                                    int M, int N, int K, int relu, int* nonfinite, int kchunk,
-                                                   float* __restrict__ P) {
+                                                   float* __restrict__ P, int accumulate = 0) {
   __shared__ __align__(16) float As[kGK][kGT + 4];
   __shared__ __align__(16) float Bs[kGK][kGT + 4];
   const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
@@ -830,10 +830,21 @@ __global__ void __launch_bounds__(256) k_gemm_f32(const float* __restrict__ A, i
       float v = acc[i][j] + bias[gn];
       if (relu) v = fmaxf(v, 0.0f);
       if (mask != nullptr) v *= mask[gn];
+      if (accumulate) v += C[(int64_t)gm * ldc + gn];  // residual stream (k_enc_f32.cu)
       flag_nonfinite(nonfinite, v);
       C[(int64_t)gm * ldc + gn] = v;
     }
   }
+}
+
+// C = act(A W + bias) (+ C): the fp32 encoder's GEMMs (large M, no split)
+cudaError_t launch_gemm_f32_acc(const float* A, int lda, const float* W, const float* bias, float* C, int ldc, int M,
+                                int N, int K, int relu, int accumulate, cudaStream_t st) {
+  if (M == 0 || N == 0) return cudaSuccess;
+  dim3 grid((N + kGT - 1) / kGT, (M + kGT - 1) / kGT, 1);
+  if (grid.y > 65535) return cudaErrorInvalidValue;
+  k_gemm_f32<<<grid, 256, 0, st>>>(A, lda, W, bias, nullptr, C, ldc, M, N, K, relu, nullptr, K, nullptr, accumulate);
+  return cudaGetLastError();
 }
 
 // C = act(sum_s P[s] + b) * mask, partials added in split order

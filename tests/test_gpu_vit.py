@@ -125,13 +125,40 @@ def test_vitl_chunk_boundary(vit_ctx):
         assert np.array_equal(out[i].cpu().numpy(), one[0]), i
 
 
-def test_vitl_fp32_rejected(vit_ctx):
+def test_vitl_fp32_reference_precision(vit_ctx, golden):
+    """precision='fp32' runs the large config on the CUDA cores in fp32
+    (k_enc_f32.cu): the reference's arithmetic type, held to the fp32 bar."""
     import torch
 
     from paper_2603_15603_b200 import runtime as rt
 
     ctx, _ = vit_ctx
-    x = torch.zeros((1, 384, 384, 3), dtype=torch.float32, device="cuda")
+    crop = np.random.default_rng(0).random((1, 384, 384, 3)).astype(np.float32)
+    x = torch.from_numpy(crop).cuda()
     out = torch.empty((1, 576, 1024), dtype=torch.float32, device="cuda")
-    rc = ctx.lib.fsb_encode(ctx.h, rt.ptr(x), 1, rt.ptr(out), rt.PRECISIONS["fp32"], ctx.stream)
-    assert rc != 0
+    ctx.check(ctx.lib.fsb_encode(ctx.h, rt.ptr(x), 1, rt.ptr(out), rt.PRECISIONS["fp32"], ctx.stream), "encode")
+    torch.cuda.synchronize()
+    got = out.cpu().numpy()[0, ::36]
+    want = golden["c4.l2.feats_rows"]
+    err = np.abs(got.astype(np.float64) - want).max() / np.abs(want).max()
+    assert err <= 1e-4, err
+
+
+@pytest.mark.parametrize("cfgkw", [dict(crop_size=32, patch=8, dim=32, heads=2, enc_layers=2),
+                                   dict(crop_size=48, patch=16, dim=96, heads=3, enc_layers=1),
+                                   dict(crop_size=64, patch=8, dim=128, heads=1, enc_layers=1)])
+def test_any_config_fp32_encoder(cfgkw):
+    """Decoder.encode at fp32 for configurations outside the fused default
+    kernels (reference decoder.py:231-260 accepts any DecoderConfig), against
+    the oracle on the same seeded weights."""
+    import oracle as orc
+    from paper_2603_15603_b200 import decoder as dc
+    from paper_2603_15603_b200 import synth
+
+    cfg = dc.DecoderConfig(body_layers=1, hand_layers=1, **cfgkw)
+    dec = dc.Decoder(synth.make_toy_models(0, 252, 168)[1], cfg, seed=40)
+    crops = np.random.default_rng(3).random((5, cfg.crop_size, cfg.crop_size, 3)).astype(np.float32)
+    got = dec.encode(crops, precision="fp32")
+    want = orc.encode(dec.weights, cfg, crops)
+    err = np.abs(got.astype(np.float64) - want).max() / np.abs(want).max()
+    assert err <= 1e-4, err
