@@ -768,8 +768,8 @@ def attribute_stages(torch, pipe, ctx, images, kps, outs, cfg, reps, saturated=N
                                     rt.ptr(b["o"]["boxes"]), rt.ptr(b["o"]["prompt"]), rt.ptr(b["crops"]), None,
                                     c.stream))
 
-    def k2(c, b):
-        c.check(lib.fsb_encode(c.h, rt.ptr(b["crops"]), 3 * B, rt.ptr(b["feats"]), prec, c.stream))
+    def k2(c, b):  # encoder + the decoders' cross-attention K / V (one launch, as in the frame path)
+        c.check(lib.fsb_encode_frames(c.h, rt.ptr(b["crops"]), B, rt.ptr(b["feats"]), prec, c.stream))
 
     def k3(c, b):
         o = b["o"]

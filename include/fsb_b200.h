@@ -140,6 +140,14 @@ int fsb_decode_body(fsb_ctx* ctx, const float* feats, int B, int feat_stride, co
 /* Decoder.decode_hand (decoder.py:360-410): feats (n, T, D) -> rots (n, 3) */
 int fsb_decode_hands(fsb_ctx* ctx, const float* feats, int n, uint32_t sel, float* rots, int precision,
                      void* stream);
+/* Decoder.encode (decoder.py:231-260) of B frames' body + hand crops
+ * (B, 3, S, S, 3) -> feats (B, 3, T, D); in bf16 mode the same launch also
+ * projects every decoder layer's cross-attention keys / values
+ * (decoder.py:220-227) into the context: fsb_decode_frames on this context
+ * with the same feats and B reads them instead of projecting them again,
+ * until the next encode on this context (fsb_frame_batch runs the pair;
+ * the feats must not be modified in between) */
+int fsb_encode_frames(fsb_ctx* ctx, const float* crops, int B, float* feats, int precision, void* stream);
 /* body + both hands of B frames in one launch, merged (decoder.py:414-422) */
 int fsb_decode_frames(fsb_ctx* ctx, const float* feats, int B, const float* prompts, uint32_t body_sel,
                       uint32_t hand_sel, float* params, float* cam, float* rots, float* merged, int precision,

@@ -65,7 +65,7 @@ cudaError_t launch_tile_layer(const uint8_t* Aimg, const uint8_t* Bimg, int KT, 
                               const float* bias, const float* mask, int relu, float* out, int ldo, uint8_t* out_img,
                               int KT_out, int* nonfinite, cudaStream_t st);
 cudaError_t launch_encoder_tc(const float* crops, int ncrops, const EncW& w, float* feats, int* nonfinite,
-                              cudaStream_t st);
+                              const KvArgs& kv, cudaStream_t st);
 cudaError_t launch_decoders_tc(const DecodeArgs& a, const BodyW& bw, const HandW& hw, cudaStream_t st);
 cudaError_t init_attrs_body();
 
@@ -125,7 +125,8 @@ struct fsb_model {
   bool has_decoder = false;
   fsb_decoder_config cfg{};
   DevMem dec_mem;
-  DevMem tcs_mem;  // TcStream tables of the encoder, body and hand decoders
+  DevMem tcs_mem;  // TcStream tables of the encoder, body and hand decoders, K / V projection
+  const TcStream* kv_tcs[2][2] = {{nullptr, nullptr}, {nullptr, nullptr}};  // [encoder + K/V | K/V only][body | hand]
   EncW enc{};
   BodyW body{};
   HandW hand{};
@@ -175,6 +176,12 @@ struct fsb_ctx {
         *w_theta = nullptr, *w_part = nullptr, *w_psum = nullptr;
   __nv_bfloat16* w_xb = nullptr;  // projector input as a bf16 A-tile image
   uint8_t *w_lbsin = nullptr, *w_lbsin2 = nullptr;  // k_lbs_tc chunk records (MHR, SMPL)
+  uint8_t *w_bkv = nullptr, *w_hkv = nullptr;  // projected cross-attention K / V (bf16 decoders)
+  // fsb_encode_frames projected K / V for (kv_feats, kv_frames):
+  // fsb_decode_frames on those features reads them instead of re-projecting
+  // until the next encode / projection on this context
+  const float* kv_feats = nullptr;
+  int kv_frames = 0;
   unsigned char *w_h1img = nullptr, *w_h2img = nullptr;
   // graphs
   bool graphs = true;
@@ -233,6 +240,7 @@ bool capturing(cudaStream_t st) {
 // graphs and workspace: both are stale.
 void model_sync(fsb_ctx* c) {
   if (c->seen_version == c->m->version) return;
+  c->kv_feats = nullptr;
   c->drop_graphs();
   c->ws_frames = 0;
   c->vit_ws_mem.release();
@@ -578,7 +586,12 @@ int fsb_reserve(fsb_ctx* c, int max_frames) {
   const size_t lbsin_bytes = (F + FSB_LBS_N - 1) / FSB_LBS_N * (size_t)FSB_LBS_REC_BYTES;
   const size_t o_lbsin = take(lbsin_bytes);
   const size_t o_lbsin2 = take(lbsin_bytes);
+  const int Lb = c->m->has_decoder ? c->m->cfg.body_layers : 0, Lh = c->m->has_decoder ? c->m->cfg.hand_layers : 0;
+  const size_t o_bkv = take((F + 1) / 2 * (size_t)Lb * FSB_KV_BODY_TILE);
+  const size_t o_hkv = take((2 * F + FSB_HANDS_PER_TILE - 1) / FSB_HANDS_PER_TILE * FSB_HANDS_PER_TILE * (size_t)Lh *
+                            FSB_KV_HAND);
   c->drop_graphs();
+  c->kv_feats = nullptr;
   FSB_CUDA(c, c->ws.alloc(off));
   unsigned char* b = static_cast<unsigned char*>(c->ws.p);
   // zero padding of the tile images (k columns past K, rows past B) must stay
@@ -606,6 +619,8 @@ int fsb_reserve(fsb_ctx* c, int max_frames) {
   FSB_CUDA(c, cudaMemset(b + o_lbsin, 0, o_lbsin2 - o_lbsin + lbsin_bytes));
   c->w_lbsin = b + o_lbsin;
   c->w_lbsin2 = b + o_lbsin2;
+  c->w_bkv = b + o_bkv;
+  c->w_hkv = b + o_hkv;
   c->ws_frames = max_frames;
   return FSB_OK;
 }
@@ -767,6 +782,46 @@ int fsb_load_decoder(fsb_ctx* c, const fsb_decoder_config* cfg, int n, const cha
       const std::string p = "hand.l" + std::to_string(l);
       ok = put_params(p + ".tcp", p + ".self", p + ".cross", p + ".mlp");
     }
+    // The K / V projection ahead of the decoders (kv_project, k_transformer_tc.cu)
+    // normalises the features once and folds each layer's LN_kv affine into
+    // its weights: LN_l(f) [Wk | Wv] + [bk | bv] = n(f) (diag(g_l) [Wk | Wv])
+    // + (b_l [Wk | Wv] + [bk | bv]).  Layers are packed in pairs: a bf16
+    // image of 256 rows (layer 2p's 128 K | V columns, then 2p + 1's) and a
+    // parameter block holding the folded biases at [0, 256).
+    for (int role = 0; ok && role < 2; ++role) {
+      const std::string rn = role == 0 ? "body" : "hand";
+      const int L = role == 0 ? cfg->body_layers : cfg->hand_layers;
+      for (int l0 = 0; ok && l0 < L; l0 += 2) {
+        const int nl = L - l0 < 2 ? L - l0 : 2;
+        std::vector<__nv_bfloat16> img((size_t)nl * 128 * Dm);
+        std::vector<float> blk(TCP_FLOATS, 0.0f);
+        for (int j = 0; ok && j < nl; ++j) {
+          const std::string p = rn + ".l" + std::to_string(l0 + j) + ".cross";
+          auto g = tab.find(p + ".lnkv_g"), be = tab.find(p + ".lnkv_b");
+          auto wk = tab.find(p + ".wk"), wv = tab.find(p + ".wv"), bk = tab.find(p + ".bk"), bv = tab.find(p + ".bv");
+          if (g == tab.end() || be == tab.end() || wk == tab.end() || wv == tab.end() || bk == tab.end() ||
+              bv == tab.end()) {
+            missing = p + " (K / V projection)";
+            ok = false;
+            break;
+          }
+          for (int n = 0; n < 2 * Dm; ++n) {
+            const float* W = n < Dm ? wk->second.first : wv->second.first;
+            const int nn = n % Dm;
+            double acc = (n < Dm ? bk->second.first : bv->second.first)[nn];
+            for (int k = 0; k < Dm; ++k) {
+              const float w = W[(size_t)k * Dm + nn];
+              img[tc_kmajor_off(128 * j + n, k, Dm) / 2] = __float2bfloat16_rn(g->second.first[k] * w);
+              acc += (double)be->second.first[k] * w;
+            }
+            blk[128 * j + n] = (float)acc;
+          }
+        }
+        if (!ok) break;
+        off[rn + ".kvimg" + std::to_string(l0 / 2)] = pk.add(img.data(), img.size() * 2);
+        off[rn + ".kvprm" + std::to_string(l0 / 2)] = pk.add(blk.data(), blk.size() * 4);
+      }
+    }
   }
   if (!ok) return fail(c, FSB_ERR_SHAPE, "decoder weight table: missing or mis-sized '%s'", missing.c_str());
   FSB_CUDA(c, c->m->dec_mem.alloc(pk.host.size()));
@@ -858,7 +913,7 @@ int fsb_load_decoder(fsb_ctx* c, const fsb_decoder_config* cfg, int n, const cha
   }
   // tcgen05 weight streams in consumption order (k_transformer_tc.cu)
   if (Dm == 64) {
-    TcStream ts[3]{};
+    TcStream ts[7]{};
     auto img = [&](TcStream& t, const uint8_t* ptr, uint32_t bytes) {
       if (t.nw < FSB_TC_MAX_IMAGES) {
         t.wptr[t.nw] = ptr;
@@ -885,21 +940,27 @@ int fsb_load_decoder(fsb_ctx* c, const fsb_decoder_config* cfg, int n, const cha
         const MlpW& m = role == 0 ? b.mlp[l] : h.mlp[l];
         img(t, sa.t_qkv, 3 * DD);
         img(t, sa.t_o, DD);
-        if (role == 0) {  // body: K | V first; hands (cross_attn_hands): queries first
-          img(t, ca.t_kv, 2 * DD);
-          img(t, ca.t_q, DD);
-        } else {
-          img(t, ca.t_q, DD);
-          img(t, ca.t_kv, 2 * DD);
-        }
+        img(t, ca.t_q, DD);  // K | V were projected ahead (kv_project)
         img(t, ca.t_o, DD);
         img(t, m.t_w1, 4 * DD);
         img(t, m.t_w2, 4 * DD);
         t.pptr[l] = role == 0 ? b.tc_params[l] : h.tc_params[l];
       }
       t.nprm = L;
+      // K / V projection streams: after the encoder's (frame encode) or
+      // alone (given features); one folded image + bias block per layer pair
+      for (int mode = 0; mode < 2; ++mode) {
+        TcStream& k = ts[3 + 2 * mode + role];
+        if (mode == 0) k = ts[0];
+        const std::string rn = role == 0 ? "body" : "hand";
+        for (int l0 = 0; l0 < L; l0 += 2) {
+          const int nl = L - l0 < 2 ? L - l0 : 2;
+          img(k, I(rn + ".kvimg" + std::to_string(l0 / 2)), (uint32_t)nl * 2 * DD);
+          k.pptr[k.nprm++] = PT(rn + ".kvprm" + std::to_string(l0 / 2));
+        }
+      }
     }
-    for (int i = 0; i < 3; ++i)
+    for (int i = 0; i < 7; ++i)
       if (ts[i].nw > FSB_TC_MAX_IMAGES)
         return fail(c, FSB_ERR_USAGE, "decoder too deep for the tcgen05 weight stream (%d images > %d)", ts[i].nw,
                     FSB_TC_MAX_IMAGES);
@@ -909,6 +970,8 @@ int fsb_load_decoder(fsb_ctx* c, const fsb_decoder_config* cfg, int n, const cha
     e.tcs = dts;
     b.tcs = dts + 1;
     h.tcs = dts + 2;
+    for (int mode = 0; mode < 2; ++mode)
+      for (int role = 0; role < 2; ++role) c->m->kv_tcs[mode][role] = dts + 3 + 2 * mode + role;
   }
   // the body decoder's FK uses the decoder template's rest joints; the
   // body template upload patches it in (fsb_load_template)
@@ -1169,6 +1232,7 @@ int fsb_bridge(fsb_ctx* c, const float* v, int B, int nv, const int32_t* corners
 
 int fsb_encode(fsb_ctx* c, const float* crops, int n, float* feats, int precision, void* stream) {
   if (!c->m->has_decoder) return fail(c, FSB_ERR_USAGE, "encode: no decoder loaded");
+  c->kv_feats = nullptr;
   if (precision != FSB_FP32 && precision != FSB_BF16) return fail(c, FSB_ERR_USAGE, "encode: bad precision %d", precision);
   model_sync(c);
   if (c->m->vit && precision == FSB_FP32) {  // reference precision, any config (k_enc_f32.cu)
@@ -1215,7 +1279,7 @@ int fsb_encode(fsb_ctx* c, const float* crops, int n, float* feats, int precisio
   if (!default_model(c->m->cfg))
     return fail(c, FSB_ERR_USAGE, "encode: the fused fp32 encoder supports the default DecoderConfig only");
   if (precision == FSB_BF16)
-    FSB_CUDA(c, launch_encoder_tc(crops, n, c->m->enc, feats, c->d_flag, (cudaStream_t)stream));
+    FSB_CUDA(c, launch_encoder_tc(crops, n, c->m->enc, feats, c->d_flag, KvArgs{}, (cudaStream_t)stream));
   else
     FSB_CUDA(c, launch_encoder_f32(crops, n, c->m->enc, feats, c->d_flag, (cudaStream_t)stream));
   c->counters.encode += 1;
@@ -1223,6 +1287,24 @@ int fsb_encode(fsb_ctx* c, const float* crops, int n, float* feats, int precisio
   c->launches += n > 0;
   note_stream(c, (cudaStream_t)stream);
   return FSB_OK;
+}
+
+// K / V projection arguments for a decode of `a` (crop mapping as DecodeArgs)
+static KvArgs kv_args(fsb_ctx* c, const DecodeArgs& a, int mode) {
+  KvArgs kv{};
+  kv.mode = mode;
+  kv.nbody = a.nbody;
+  kv.nhand = a.nhand;
+  kv.body_feat_stride = a.body_feat_stride;
+  kv.hand_feat_first = a.hand_feat_first;
+  kv.feats_in = a.feats;
+  kv.body_kv = c->w_bkv;
+  kv.hand_kv = c->w_hkv;
+  kv.tcs[0] = c->m->kv_tcs[mode - 1][0];
+  kv.tcs[1] = c->m->kv_tcs[mode - 1][1];
+  kv.layers[0] = c->m->cfg.body_layers;
+  kv.layers[1] = c->m->cfg.hand_layers;
+  return kv;
 }
 
 static int decode_common(fsb_ctx* c, DecodeArgs& a, int precision, cudaStream_t st) {
@@ -1235,6 +1317,18 @@ static int decode_common(fsb_ctx* c, DecodeArgs& a, int precision, cudaStream_t 
   if ((a.body_sel >> c->m->cfg.body_layers) != 0u || (a.hand_sel >> c->m->cfg.hand_layers) != 0u)
     return fail(c, FSB_ERR_USAGE, "selection out of range");
   a.nonfinite = c->d_flag;
+  if (precision == FSB_BF16 && a.body_kv == nullptr) {
+    // the bf16 decoders read the cross-attention K / V projected ahead:
+    // project them from the given features (k_encoder_tc mode 2)
+    const int frames = a.nbody > (a.nhand + 1) / 2 ? a.nbody : (a.nhand + 1) / 2;
+    int rc = ensure_ws(c, frames, st);
+    if (rc) return rc;
+    FSB_CUDA(c, launch_encoder_tc(nullptr, 0, c->m->enc, nullptr, c->d_flag, kv_args(c, a, 2), st));
+    c->launches += (a.nbody + a.nhand) > 0;
+    a.body_kv = c->w_bkv;
+    a.hand_kv = c->w_hkv;
+    c->kv_feats = nullptr;
+  }
   if (precision == FSB_BF16)
     FSB_CUDA(c, launch_decoders_tc(a, c->m->body, c->m->hand, st));
   else
@@ -1275,10 +1369,38 @@ int fsb_decode_hands(fsb_ctx* c, const float* feats, int n, uint32_t sel, float*
   return decode_common(c, a, precision, (cudaStream_t)stream);
 }
 
+int fsb_encode_frames(fsb_ctx* c, const float* crops, int B, float* feats, int precision, void* stream) {
+  if (precision != FSB_BF16 || c->m->vit || !c->m->has_decoder || !default_model(c->m->cfg))
+    return fsb_encode(c, crops, 3 * B, feats, precision, stream);
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = ensure_ws(c, B, st);
+  if (rc) return rc;
+  // encoder + every decoder layer's cross-attention K / V in one launch
+  // (k_encoder_tc mode 1)
+  DecodeArgs a{};
+  a.feats = feats;
+  a.nbody = B;
+  a.nhand = 2 * B;
+  a.body_feat_stride = 3;
+  a.hand_feat_first = 1;
+  FSB_CUDA(c, launch_encoder_tc(crops, 3 * B, c->m->enc, feats, c->d_flag, kv_args(c, a, 1), st));
+  c->counters.encode += 1;
+  c->counters.encoded_crops += 3 * B;
+  c->launches += B > 0;
+  c->kv_feats = feats;
+  c->kv_frames = B;
+  note_stream(c, st);
+  return FSB_OK;
+}
+
 int fsb_decode_frames(fsb_ctx* c, const float* feats, int B, const float* prompts, uint32_t body_sel,
                       uint32_t hand_sel, float* params, float* cam, float* rots, float* merged, int precision,
                       void* stream) {
   DecodeArgs a{};
+  if (precision == FSB_BF16 && c->kv_feats == feats && c->kv_frames == B && feats != nullptr) {
+    a.body_kv = c->w_bkv;  // projected by fsb_encode_frames
+    a.hand_kv = c->w_hkv;
+  }
   a.feats = feats;
   a.prompts = prompts;
   a.nbody = B;
@@ -1429,7 +1551,7 @@ static int frame_batch_launches(fsb_ctx* c, const float* images, int B, int H, i
   float* rots = o.hand_rots ? o.hand_rots : c->w_rots;
   int rc = fsb_boxes_crops(c, images, B, H, W, kp, alpha, S, boxes, prompt, crops, nullptr, st);
   if (rc) return rc;
-  rc = fsb_encode(c, crops, 3 * B, feats, precision, st);
+  rc = fsb_encode_frames(c, crops, B, feats, precision, st);
   if (rc) return rc;
   rc = fsb_decode_frames(c, feats, B, prompt, bsel, hsel, params, cam, rots, o.merged, precision, st);
   if (rc || !o.theta) return rc;  // front half only (Pipeline.run without the SMPL tail)

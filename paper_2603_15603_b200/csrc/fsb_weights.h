@@ -66,7 +66,7 @@ struct MlpW {
 struct TcStream {
   const uint8_t* wptr[FSB_TC_MAX_IMAGES];
   uint32_t wbytes[FSB_TC_MAX_IMAGES];
-  const float* pptr[FSB_MAX_LAYERS];
+  const float* pptr[FSB_MAX_LAYERS + 8];
   int nw, nprm;
   int pad[2];
 };
@@ -203,4 +203,39 @@ struct DecodeArgs {
   float* merged;            // (nbody, 76) or null: body params with hand rotations overwritten
   float* inter;             // (nbody, body_layers, 76 + 3 + 44) or null: intermediate predictions
   int* nonfinite;
+  // bf16 mode: the cross-attention keys / values of every layer, projected
+  // ahead of the decoders from the features (KvArgs below)
+  const uint8_t* body_kv;   // FSB_KV_BODY_TILE bytes per (body tile, layer)
+  const uint8_t* hand_kv;   // FSB_KV_HAND bytes per (hand, layer), 32 hands per tile
+  int hand_tiles_per_cta;   // set by the launcher
+};
+
+// Cross-attention K / V of the decoders depend only on the features
+// (decoder.py:220-227: LN_kv(f) Wk + bk, LN_kv(f) Wv + bv), so the bf16 path
+// projects them for every layer right after the encoder (k_encoder_tc, or
+// the same kernel on given features) instead of inside the decoders' serial
+// layer chain.
+//  * body tile T (frames 2T, 2T + 1), layer l: the decoder's shared-memory
+//    image of the tile's keys and values, [K: 4 heads x (128 x 16, K-major)]
+//    [V^T: 4 heads x (16 x 128 keys, K-major)], 32 KB, loaded with one bulk
+//    copy per layer;
+//  * hand tile T (hands 32 T + i), layer l: 32 key pairs s of 16 KB
+//    ([hand i][512 bytes]); in hand i's 512 bytes the 16-byte chunk
+//    q = kk 16 + kv 8 + h 4 + c (key 2 s + kk, K | V, column half h, chunk c
+//    of the half) sits at position q ^ (i & 7), so a key pair lands in shared
+//    memory with one 16 KB bulk copy and a warp's eight hands x four chunks
+//    read distinct banks.
+#define FSB_KV_BODY_TILE 32768
+#define FSB_HANDS_PER_TILE 32
+#define FSB_KV_HAND 16384
+struct KvArgs {
+  int mode;                 // 0: encode only; 1: encode frames + K / V; 2: K / V of the given features
+  int nbody, nhand;         // modes 1, 2: crops as DecodeArgs (body of frame f = f * stride, hand u =
+  int body_feat_stride;     //   first + (u / 2) * stride + u % 2)
+  int hand_feat_first;
+  const float* feats_in;    // mode 2
+  uint8_t* body_kv;
+  uint8_t* hand_kv;
+  const TcStream* tcs[2];   // body / hand: (mode 1) encoder images + the role's K | V images, (mode 2) K | V only
+  int layers[2];            // body / hand decoder layers
 };

@@ -26,6 +26,8 @@
 // straight from TMEM (tcgen05.mma with A in TMEM).  The MLP hidden layer is
 // likewise packed in place and read by the second GEMM from TMEM, so no
 // 128 x 256 operand ever goes through shared memory.
+#include <cstdlib>
+
 #include "fsb_common.cuh"
 #include "fsb_weights.h"
 #include "tc_sm100.cuh"
@@ -64,6 +66,7 @@ struct alignas(16) Shared {
   uint64_t wbar[2];     // weight slot full
   uint64_t pbar[2];     // parameter slot full
   uint64_t mbar[NG];    // per-group MMA completion
+  uint64_t kvb[NG][3];  // per-group cross-attention K / V stages (body: [0] one 32 KB image per layer)
   uint32_t tmem;
   unsigned wrel[2];     // releases of each weight slot (monotonic)
   unsigned prel[2];     // releases of each parameter slot
@@ -94,6 +97,7 @@ struct Pipe {
   uint32_t tmem;   // this group's TMEM base
   uint32_t mphase;
   int wuse, xc, puse;
+  int kvuse;  // cross-attention K / V stages consumed (kvb parity)
   int g, tid, r, h;
 #ifdef FSB_PROFILE
   long long prof[16];
@@ -293,8 +297,9 @@ __device__ void drain_q(Pipe& P, uint32_t qcol, const float* bq) {
   }
 }
 
-// key columns [kcol, +64) + bias -> key tiles (heads 2h, 2h+1)
-__device__ void drain_k(Pipe& P, uint32_t kcol, const float* bk) {
+// key columns [kcol, +64) + bias -> key tiles (heads 2h, 2h+1) at dst
+// (default: this group's S_K; the encoder's K / V epilogue: global memory)
+__device__ void drain_k(Pipe& P, uint32_t kcol, const float* bk, uint8_t* dst = nullptr) {
   float v[HC];
   tmem_ld32(P.lane_addr(kcol + HC * P.h), v);
 #pragma unroll
@@ -302,7 +307,7 @@ __device__ void drain_k(Pipe& P, uint32_t kcol, const float* bk) {
     const int hd = 2 * P.h + j;
 #pragma unroll
     for (int i = 0; i < 16; ++i) v[16 * j + i] += bk[16 * hd + i];
-    uint8_t* tk = P.smem + S_K + hd * 4096;
+    uint8_t* tk = (dst ? dst : P.smem + S_K) + hd * 4096;
     st_row8(tk, P.r, 0, DH, v + 16 * j);
     st_row8(tk, P.r, 8, DH, v + 16 * j + 8);
   }
@@ -313,11 +318,11 @@ __device__ void drain_k(Pipe& P, uint32_t kcol, const float* bk) {
 // V^T (lane 64 + d = value dim d, columns = keys).  The threads of lane
 // quadrants 2 and 3 write the per-head V^T tiles (16 x 128, K-major along
 // keys) with 16-byte stores; thread h takes keys [64 h, 64 h + 64).
-__device__ void drain_vt(Pipe& P, uint32_t vtcol, const float* bv) {
+__device__ void drain_vt(Pipe& P, uint32_t vtcol, const float* bv, uint8_t* dst = nullptr) {
   if (P.r < 64) return;  // warp-uniform: lane quadrants 0, 1 hold K^T
   const int d = P.r - 64, hd = d >> 4;
   const float b = bv[d];
-  uint8_t* tv = P.smem + S_VT + hd * 4096;
+  uint8_t* tv = (dst ? dst : P.smem + S_VT) + hd * 4096;
 #pragma unroll 1
   for (int c = 0; c < 2; ++c) {
     const int k0 = 64 * P.h + 32 * c;
@@ -578,27 +583,16 @@ __device__ void self_attn(Pipe& P, const float* prm, float* x, const float* a, b
   out_proj(P, prm + TCP_S_BO, x, valid);
 }
 
-// cross attention: x += MHA(LN_q(x), LN_kv(f))  (decoder.py:220-227).
-// LN_kv(f) is staged in the V^T tile (free until drain_kv refills it after
-// the K | V GEMM has read it).
-__device__ void cross_attn(Pipe& P, const float* prm, float* x, const float* frow, bool valid) {
-  float f[HC];
-#pragma unroll
-  for (int c = 0; c < HC; c += 4) {
-    const float4 v = __ldg(reinterpret_cast<const float4*>(frow + HC * P.h + c));
-    f[c] = v.x; f[c + 1] = v.y; f[c + 2] = v.z; f[c + 3] = v.w;
+// cross attention: x += MHA(LN_q(x), LN_kv(f))  (decoder.py:220-227).  The
+// tile's keys and values were projected ahead of the decoder (kv_project);
+// one bulk copy brings this layer's 32 KB image into S_K | S_VT while the
+// queries are formed.
+__device__ void cross_attn(Pipe& P, const float* prm, float* x, const uint8_t* kvimg, bool valid) {
+  uint64_t* bar = &P.sh->kvb[P.g][0];
+  if (P.tid == 0) {  // S_K / S_VT are free: the self-attention's MMAs have completed
+    tc::mbar_expect_tx(bar, FSB_KV_BODY_TILE);
+    tc::bulk_g2s(P.smem + S_K, kvimg, FSB_KV_BODY_TILE, bar);
   }
-  ln_half_to_tile(P, f, prm + TCP_C_LNKV_G, prm + TCP_C_LNKV_B, S_VT);
-  const uint32_t wkv = P.acquire();
-  P.before_issue();
-  if (P.tid == 0) {
-    gemm(P.sbase + S_VT, D, wkv, D, T_GEN, P.tmem);        // K
-    gemm_t(wkv, 0, P.sbase + S_VT, T_GEN + 128, P.tmem);  // (K | V)^T
-  }
-  P.prefetch();
-  P.commit_wait();
-  drain_k(P, T_GEN, prm + TCP_C_BQKV + 64);
-  drain_vt(P, T_GEN + 128, prm + TCP_C_BQKV + 128);
   ln_half_to_tile(P, x, prm + TCP_C_LNQ_G, prm + TCP_C_LNQ_B);
   const uint32_t wq = P.acquire();
   P.before_issue();
@@ -606,58 +600,187 @@ __device__ void cross_attn(Pipe& P, const float* prm, float* x, const float* fro
   P.prefetch();
   P.commit_wait();
   drain_q(P, T_GEN, prm + TCP_C_BQKV);
+  tc::mbar_wait(bar, (uint32_t)(P.kvuse & 1));
+  ++P.kvuse;
   attention<BLK>(P, true);
   out_proj(P, prm + TCP_C_BO, x, valid);
 }
 
-// cross attention of a hand tile (decoder.py:220-227 per hand): the queries
-// once, then one round per pair of hand slots (2c, 2c + 1): LN_kv of their
-// two crops' feature rows (block b of the 128 rows = slot 2c + b), K | V,
-// and an attention round in which only the slots' token rows are active.
-// Weight images in order t_q, t_kv (kept in its ring slot for all rounds),
-// t_o.
-__device__ void cross_attn_hands(Pipe& P, const float* prm, float* x, const DecodeArgs& a, int hand0, int nslots,
-                                 bool valid) {
+// bf16 pair (low half = even element) -> fp32 pair
+__device__ __forceinline__ float2 bf2(uint32_t u) {
+  return make_float2(__uint_as_float(u << 16), __uint_as_float(u & 0xffff0000u));
+}
+// packed FP32x2 FMA (sm_100 FFMA2): a * b + c on both lanes
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("{\n\t.reg .b64 ra, rb, rc, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rc, {%6, %7};\n\t"
+      "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+
+// cross attention of a hand tile (decoder.py:220-227 per hand): each hand's
+// four query rows attend to its own crop's 64 keys, so the tile's 32 hands
+// need 32 different key / value sets -- a batched GEMM with M = 4 per batch
+// entry, which the 128-row tensor-core tiles cannot serve without running
+// one round per crop pair.  The queries come from one tcgen05 GEMM; the
+// scores, softmax and P.V run on the CUDA cores (FFMA2) over the
+// precomputed bf16 K / V, streamed two keys (16 KB, all 32 hands) at a time
+// through a three-slot shared-memory ring filled by cp.async.bulk (one
+// 512-byte copy per hand, issued by the first warp).
+// The four threads of a hand (tokens t = 0..3, column half h) split each
+// key by 16-byte chunks: thread t reads chunk t (dims 32 h + 8 t .. + 8, of
+// head 2 h + t / 2) once and forms the partial scores of all four query rows
+// on it; a lane-pair shuffle completes each head's 16-dim score, so both
+// threads of a pair hold the head's four rows' scores, run the online softmax
+// for them and accumulate P.V on their chunk of the values.  A warp's 32
+// lanes read 32 distinct chunks (eight hands x four): no broadcast waste.
+constexpr int KV_STAGES = 3;
+constexpr uint32_t KV_STAGE_BYTES = 32 * 512;  // two keys of 32 hands
+constexpr int KV_STAGES_PER_LAYER = 64 / 2;
+static_assert(KV_STAGES * KV_STAGE_BYTES <= 3 * 16384, "the ring spans S_Q, S_K, S_VT");
+
+#ifndef FSB_HKV_EXP
+#define FSB_HKV_EXP 0  // experiments: 1 = no copies / waits (compute only), 2 = no compute (copies only)
+#endif
+__device__ void cross_attn_hands(Pipe& P, const float* prm, float* x, const uint8_t* hkv, int hand0, int nslots,
+                                 int l, int L, bool valid) {
+  const int u0 = P.kvuse;
+  // key pair s of this layer (16 KB: the tile's 32 hands x 512 bytes) ->
+  // ring slot (u0 + s) % 3, one bulk copy
+  const uint8_t* src = hkv + ((size_t)(hand0 / FSB_HANDS_PER_TILE) * L + l) * (32 * KV_STAGE_BYTES);
+  auto issue = [&](int s) {
+    const int n = u0 + s, slot = n % KV_STAGES;
+    uint64_t* bar = &P.sh->kvb[P.g][slot];
+    tc::mbar_expect_tx(bar, KV_STAGE_BYTES);
+    tc::bulk_g2s(P.smem + S_Q + slot * KV_STAGE_BYTES, src + (size_t)s * KV_STAGE_BYTES, KV_STAGE_BYTES, bar);
+  };
+  if (FSB_HKV_EXP != 1 && P.tid == 0)  // S_Q..S_VT are free: the self-attention's MMAs have completed
+    for (int s = 0; s < KV_STAGES; ++s) issue(s);
   ln_half_to_tile(P, x, prm + TCP_C_LNQ_G, prm + TCP_C_LNQ_B);
   const uint32_t wq = P.acquire();
   P.before_issue();
   if (P.tid == 0) gemm(P.sbase + S_A, D, wq, D, T_GEN, P.tmem);
   P.prefetch();
   P.commit_wait();
-  drain_q(P, T_GEN, prm + TCP_C_BQKV);
-  const uint32_t wkv = P.acquire();
-  const int blk = P.r / BLK, rb = P.r % BLK;
-  const int nr = (nslots + 1) / 2;
-  if (nr == 0) P.prefetch();  // an empty tile still releases t_q (the other group waits for t_o)
-#pragma unroll 1
-  for (int c = 0; c < nr; ++c) {
-    const int slot = 2 * c + blk;
-    float f[HC];
-    if (slot < nslots) {
-      const int u = hand0 + slot;
-      const int crop = a.hand_feat_first + (u / 2) * a.body_feat_stride + (u % 2);
-      const float* frow = a.feats + ((int64_t)crop * 64 + rb) * D + HC * P.h;
+  // the residual stream waits in TMEM columns [128 + 32 h, +32) (the query
+  // accumulator uses [0, 64))
+  {
+    uint32_t xu[HC];
 #pragma unroll
-      for (int q = 0; q < HC; q += 4) {
-        const float4 v = __ldg(reinterpret_cast<const float4*>(frow + q));
-        f[q] = v.x; f[q + 1] = v.y; f[q + 2] = v.z; f[q + 3] = v.w;
-      }
-    } else {
-#pragma unroll
-      for (int q = 0; q < HC; ++q) f[q] = 0.0f;
-    }
-    ln_half_to_tile(P, f, prm + TCP_C_LNKV_G, prm + TCP_C_LNKV_B, S_VT);
-    P.before_issue();
-    if (P.tid == 0) {
-      gemm(P.sbase + S_VT, D, wkv, D, T_GEN, P.tmem);
-      gemm_t(wkv, 0, P.sbase + S_VT, T_GEN + 128, P.tmem);
-    }
-    if (c == 0) P.prefetch();  // t_q's slot may be refilled
-    P.commit_wait();
-    drain_k(P, T_GEN, prm + TCP_C_BQKV + 64);
-    drain_vt(P, T_GEN + 128, prm + TCP_C_BQKV + 128);
-    attention<BLK>(P, (rb >> 2) == c);
+    for (int c = 0; c < HC; ++c) xu[c] = __float_as_uint(x[c]);
+    tc::tmem_st32u_nowait(P.lane_addr(T_GEN + 128 + HC * P.h), xu);
   }
+  const int t = P.r & 3, lane = P.r & 31;
+  // qc[tp][k]: query row 4 i + tp (+ bias, pre-scaled by 1/sqrt(16) log2(e)),
+  // on this thread's chunk (column 32 h + 8 t + 2k, + 1)
+  float2 qc[4][4];
+  {
+    float q[HC];
+    tmem_ld32(P.lane_addr(T_GEN + HC * P.h), q);
+#pragma unroll
+    for (int i = 0; i < HC; ++i) q[i] = (q[i] + prm[TCP_C_BQKV + HC * P.h + i]) * kScale;
+#pragma unroll
+    for (int sc = 0; sc < 4; ++sc)
+#pragma unroll
+      for (int k = 0; k < 8; k += 2)
+#pragma unroll
+        for (int tp = 0; tp < 4; ++tp) {
+          const float a0 = __shfl_sync(0xffffffffu, q[8 * sc + k], (lane & ~3) | tp);
+          const float a1 = __shfl_sync(0xffffffffu, q[8 * sc + k + 1], (lane & ~3) | tp);
+          if (t == sc) qc[tp][k / 2] = make_float2(a0, a1);
+        }
+  }
+  float2 o[4][4];
+  float m[4], lsum[4];
+#pragma unroll
+  for (int tp = 0; tp < 4; ++tp) {
+    m[tp] = -INFINITY;
+    lsum[tp] = 0.0f;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) o[tp][k] = make_float2(0.0f, 0.0f);
+  }
+  // this thread's chunks: hand i's 512 bytes, chunk q = kk 16 + kv 8 + 4 h + t
+  // at position q ^ (i & 7)
+  const int hi = P.r >> 2;
+  const uint32_t off = (uint32_t)hi * 512u;
+  const uint32_t pk = (uint32_t)(((4 * P.h + t) ^ (hi & 7)) * 16);  // K chunk of key 0 (V: + 128, key 1: + 256)
+#pragma unroll 1
+  for (int s = 0; s < KV_STAGES_PER_LAYER; ++s) {
+    const int n = u0 + s, slot = n % KV_STAGES;
+    if (FSB_HKV_EXP != 1) tc::mbar_wait(&P.sh->kvb[P.g][slot], (uint32_t)((n / KV_STAGES) & 1));
+    const uint8_t* st = P.smem + S_Q + slot * KV_STAGE_BYTES + off;
+    if (FSB_HKV_EXP != 2) {
+    float sc[2][4];
+#pragma unroll
+    for (int kk = 0; kk < 2; ++kk) {
+      const uint4 u = *reinterpret_cast<const uint4*>(st + kk * 256 + pk);
+      const float2 kx = bf2(u.x), ky = bf2(u.y), kz = bf2(u.z), kw = bf2(u.w);
+#pragma unroll
+      for (int tp = 0; tp < 4; ++tp) {
+        float2 acc = __fmul2_rn(qc[tp][0], kx);
+        acc = ffma2(qc[tp][1], ky, acc);
+        acc = ffma2(qc[tp][2], kz, acc);
+        acc = ffma2(qc[tp][3], kw, acc);
+        sc[kk][tp] = acc.x + acc.y;
+      }
+    }
+#pragma unroll
+    for (int kk = 0; kk < 2; ++kk)
+#pragma unroll
+      for (int tp = 0; tp < 4; ++tp) sc[kk][tp] += __shfl_xor_sync(0xffffffffu, sc[kk][tp], 1);
+    // online softmax (scores in log2 units): sc becomes the probabilities;
+    // the accumulators are rescaled only when a row of the warp raised its
+    // maximum (warp-uniform test; rare after the first keys)
+#pragma unroll
+    for (int tp = 0; tp < 4; ++tp) {
+      const float mn = fmaxf(m[tp], fmaxf(sc[0][tp], sc[1][tp]));
+      const float corr = ex2_approx(m[tp] - mn);
+      m[tp] = mn;
+      sc[0][tp] = ex2_approx(sc[0][tp] - mn);
+      sc[1][tp] = ex2_approx(sc[1][tp] - mn);
+      lsum[tp] = fmaf(lsum[tp], corr, sc[0][tp] + sc[1][tp]);
+      if (__any_sync(0xffffffffu, corr != 1.0f)) {
+        const float2 c2 = make_float2(corr, corr);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) o[tp][k] = __fmul2_rn(o[tp][k], c2);
+      }
+    }
+#pragma unroll
+    for (int kk = 0; kk < 2; ++kk) {
+      const uint4 u = *reinterpret_cast<const uint4*>(st + kk * 256 + 128 + pk);
+      const float2 vv[4] = {bf2(u.x), bf2(u.y), bf2(u.z), bf2(u.w)};
+#pragma unroll
+      for (int tp = 0; tp < 4; ++tp) {
+        const float2 pp = make_float2(sc[kk][tp], sc[kk][tp]);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) o[tp][k] = ffma2(pp, vv[k], o[tp][k]);
+      }
+    }
+    }
+    P.sync();  // every thread is done with the slot
+    if (FSB_HKV_EXP != 1 && P.tid == 0 && s + KV_STAGES < KV_STAGES_PER_LAYER) issue(s + KV_STAGES);
+  }
+  P.kvuse = u0 + KV_STAGES_PER_LAYER;
+  // context: rows 4 i + tp, columns 32 h + 8 t (head 2 h + t / 2) -> the A
+  // tile of the output projection
+  if (valid) {
+#pragma unroll
+    for (int tp = 0; tp < 4; ++tp) {
+      const float inv = 1.0f / lsum[tp];
+      float v[8];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        v[2 * k] = o[tp][k].x * inv;
+        v[2 * k + 1] = o[tp][k].y * inv;
+      }
+      st_row8(P.smem + S_A, (P.r & ~3) | tp, HC * P.h + 8 * t, D, v);
+    }
+  }
+  tc::tmem_wait_st();
+  tmem_ld32(P.lane_addr(T_GEN + 128 + HC * P.h), x);
   out_proj(P, prm + TCP_C_BO, x, valid);
 }
 
@@ -727,6 +850,7 @@ __device__ void setup(Pipe& P, Shared& sh, uint8_t* smem, const TcStream* tab, u
   P.r = P.tid & (ROWS - 1);
   P.h = P.tid / ROWS;
   P.mphase = 0;
+  P.kvuse = 0;
   P.wuse = 0;
   P.xc = 0;
   P.puse = 0;
@@ -742,7 +866,10 @@ __device__ void setup(Pipe& P, Shared& sh, uint8_t* smem, const TcStream* tab, u
       sh.wrel[i] = 0;
       sh.prel[i] = 0;
     }
-    for (int i = 0; i < NG; ++i) tc::mbar_init(&sh.mbar[i], 1);
+    for (int i = 0; i < NG; ++i) {
+      tc::mbar_init(&sh.mbar[i], 1);
+      for (int k = 0; k < 3; ++k) tc::mbar_init(&sh.kvb[i][k], 1);
+    }
     tc::mbar_fence_init();
   }
   if (threadIdx.x < 32) tc::tmem_alloc(&sh.tmem, 512);
@@ -776,26 +903,189 @@ __device__ void teardown(Pipe& P, int role) {
 }  // namespace
 
 // ===========================================================================
-// encoder: grid = ceil(ncrops / 4); group g, block f of CTA b encodes crop
-// 4b + 2g + f
+// K / V of every decoder layer (kv_project) from this tile's final features
+// y (decoder.py:220-227, each layer's LN_kv(f) Wk + bk, LN_kv(f) Wv + bv).
+// The features are normalised once (n(f), bf16 A tile); each layer's LN_kv
+// affine is folded into its weights and biases at upload (fsb_capi.cu), so
+// two layers' K | V come out of ONE N = 256 GEMM.  The bias-added bf16
+// results go straight to global memory in the decoders' layout (FSB_KV_* in
+// fsb_weights.h): hands row-major chunks; body tiles the decoder's shared-
+// memory image, V^T produced by staging V rows in shared memory and
+// transposing 8 x 8 blocks with ldmatrix.trans (one coalesced 128-byte
+// store per block).  Images / parameter blocks continue the CTA's stream.
+// ===========================================================================
+__device__ __forceinline__ void ldsm_x4_trans(uint32_t addr, uint32_t* d) {
+  asm volatile("ldmatrix.sync.aligned.m8n8.x4.trans.shared.b16 {%0, %1, %2, %3}, [%4];\n"
+               : "=r"(d[0]), "=r"(d[1]), "=r"(d[2]), "=r"(d[3])
+               : "r"(addr));
+}
+
+__device__ void kv_project(Pipe& P, const float* y, bool body, int tile, const KvArgs& kv) {
+  const int L = kv.layers[body ? 0 : 1];
+  const int c0 = HC * P.h;
+  {
+    float mu, rstd;
+    ln_stats(P, y, mu, rstd);
+#pragma unroll
+    for (int q = 0; q < HC; q += 8) {
+      float v[8];
+#pragma unroll
+      for (int c = 0; c < 8; ++c) v[c] = (y[q + c] - mu) * rstd;
+      st_row8(P.smem + S_A, P.r, c0 + q, D, v);
+    }
+  }
+  const int u = 2 * tile + P.r / BLK, j = P.r % BLK;  // hands: hand and key of this row
+  const int warp = (P.tid >> 5) & 7, lane = P.tid & 31;
+#pragma unroll 1
+  for (int l0 = 0; l0 < L; l0 += 2) {
+    const int nl = min(2, L - l0);
+    const float* prm = P.pacquire();
+    P.sync();  // every thread of the group is past the previous pair (TMEM drained, staging read)
+    P.prelease();
+    const uint32_t w = P.acquire();
+    P.before_issue();
+    if (P.tid == 0) gemm(P.sbase + S_A, D, w, 128 * nl, T_GEN, P.tmem);  // layers l0, l0 + 1: K | V each
+    P.prefetch();
+    P.commit_wait();
+#pragma unroll 1
+    for (int jl = 0; jl < nl; ++jl) {
+      const int l = l0 + jl, cb = 128 * jl;
+      float kk[HC], vv[HC];
+      tmem_ld32(P.lane_addr(T_GEN + cb + c0), kk);
+      tmem_ld32(P.lane_addr(T_GEN + cb + 64 + c0), vv);
+#pragma unroll
+      for (int i = 0; i < HC; ++i) {
+        kk[i] += prm[cb + c0 + i];
+        vv[i] += prm[cb + 64 + c0 + i];
+      }
+#ifndef FSB_KVP_EXP
+#define FSB_KVP_EXP 0  // experiments: 1 = no hand stores, 2 = no body stores / transposes
+#endif
+      if (body) {
+        if (FSB_KVP_EXP == 2) continue;
+        uint8_t* dst = kv.body_kv + ((size_t)tile * L + l) * FSB_KV_BODY_TILE;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {  // K rows of heads 2h, 2h + 1
+          st_row8(dst + (2 * P.h + e) * 4096, P.r, 0, DH, kk + 16 * e);
+          st_row8(dst + (2 * P.h + e) * 4096, P.r, 8, DH, kk + 16 * e + 8);
+        }
+        // V rows -> staging (S_Q / S_K by layer parity), 16-byte chunk q of
+        // row r at r * 128 + 16 (q ^ (r & 7))
+        uint8_t* stg = P.smem + (jl ? S_K : S_Q);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint4 w4;
+          w4.x = tc::pack_bf16(vv[8 * c], vv[8 * c + 1]);
+          w4.y = tc::pack_bf16(vv[8 * c + 2], vv[8 * c + 3]);
+          w4.z = tc::pack_bf16(vv[8 * c + 4], vv[8 * c + 5]);
+          w4.w = tc::pack_bf16(vv[8 * c + 6], vv[8 * c + 7]);
+          *reinterpret_cast<uint4*>(stg + P.r * 128 + (((4 * P.h + c) ^ (P.r & 7)) << 4)) = w4;
+        }
+        P.sync();
+        // warp w: token blocks 2w, 2w + 1 x the 8 dim blocks, four 8 x 8
+        // blocks per ldmatrix.x4; lane i then holds (dim 8 db + i / 4,
+        // keys 8 tb + 2 (i % 4), + 1) -> V^T image (head db / 2)
+        const uint32_t sstg = tc::smem_u32(stg);
+        uint8_t* vt = dst + 16384;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int tb = 2 * warp + (q >> 1);
+          const int tok = 8 * tb + (lane & 7), db_l = 4 * (q & 1) + (lane >> 3);
+          uint32_t d4[4];
+          ldsm_x4_trans(sstg + tok * 128 + ((db_l ^ (tok & 7)) << 4), d4);
+#pragma unroll
+          for (int m = 0; m < 4; ++m) {
+            const int db = 4 * (q & 1) + m;
+            *reinterpret_cast<uint32_t*>(vt + (db >> 1) * 4096 + (db & 1) * 2048 + tb * 128 + (lane >> 2) * 16 +
+                                         (lane & 3) * 4) = d4[m];
+          }
+        }
+      } else if (FSB_KVP_EXP != 1) {
+        // hand rows -> staging (S_Q: per hand 32 key pairs x 512 bytes in
+        // the global chunk order, additionally XOR-ed with the key pair so
+        // the stores spread over the banks) -> global: the tile's two hands
+        // are adjacent, 1 KB contiguous per key pair
+        const int sp = j >> 1;
+        uint8_t* stg = P.smem + S_Q + (P.r / BLK) * FSB_KV_HAND + sp * 512;
+#pragma unroll
+        for (int kvi = 0; kvi < 2; ++kvi) {
+          const float* v = kvi ? vv : kk;
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            uint4 w4;
+            w4.x = tc::pack_bf16(v[8 * c], v[8 * c + 1]);
+            w4.y = tc::pack_bf16(v[8 * c + 2], v[8 * c + 3]);
+            w4.z = tc::pack_bf16(v[8 * c + 4], v[8 * c + 5]);
+            w4.w = tc::pack_bf16(v[8 * c + 6], v[8 * c + 7]);
+            const int q = (j & 1) * 16 + kvi * 8 + 4 * P.h + c;
+            *reinterpret_cast<uint4*>(stg + ((q ^ (u & 7) ^ (sp & 7)) << 4)) = w4;
+          }
+        }
+        P.sync();
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int n = P.tid + GT * k, hb = n >> 10, o = n & 1023, osp = o >> 5;
+          const int uu = 2 * tile + hb;
+          const uint4 w4 = *reinterpret_cast<const uint4*>(P.smem + S_Q + hb * FSB_KV_HAND + o * 16);
+          if (uu < kv.nhand)
+            *reinterpret_cast<uint4*>(kv.hand_kv +
+                                      ((((size_t)(uu / FSB_HANDS_PER_TILE) * L + l) * 32 + osp) * 32 +
+                                       uu % FSB_HANDS_PER_TILE) * 512 + (((o & 31) ^ (osp & 7)) << 4)) = w4;
+        }
+        if (jl + 1 < nl) P.sync();  // staging reused by the pair's second layer
+      }
+    }
+  }
+}
+
+// ===========================================================================
+// encoder.  kv.mode 0: grid = ceil(ncrops / 4); group g, block f of CTA b
+// encodes crop 4b + 2g + f.  kv.mode 1 (frames) / 2 (given features): body
+// CTAs first, then hand CTAs; group g of a CTA takes tile 2 c + g of its
+// role, whose blocks are frames (hands) 2 tile, 2 tile + 1 -- the decoders'
+// body tiles pair the same frames -- and after the encoder (mode 1) or the
+// feature load (mode 2) projects the role's K / V for every decoder layer.
 // ===========================================================================
 __global__ void __launch_bounds__(NTH, 1) k_encoder_tc(const float* __restrict__ crops, int ncrops, EncW w,
-                                                       float* __restrict__ feats, int* nonfinite) {
+                                                       float* __restrict__ feats, int* nonfinite, KvArgs kv) {
   extern __shared__ __align__(1024) uint8_t smem[];
   __shared__ Shared sh;
   Pipe P;
-  setup(P, sh, smem, w.tcs, 4 * (int)blockIdx.x + 2 < ncrops ? 2u : 1u);
+  const int nbc = ((kv.nbody + 1) / 2 + 1) / 2;  // body CTAs (modes 1, 2)
+  const bool body = kv.mode != 0 && (int)blockIdx.x < nbc;
+  const int nunits = body ? kv.nbody : kv.nhand;
+  const int cta = body ? (int)blockIdx.x : (int)blockIdx.x - nbc;
+  bool has0, has1;
+  if (kv.mode == 0) {
+    has0 = true;
+    has1 = 4 * (int)blockIdx.x + 2 < ncrops;
+  } else {
+    has0 = 2 * (2 * cta) < nunits;
+    has1 = 2 * (2 * cta + 1) < nunits;
+  }
+  setup(P, sh, smem, kv.mode == 0 ? w.tcs : kv.tcs[body ? 0 : 1], has1 ? 2u : 1u);
   const int blk = P.r / BLK, p = P.r % BLK;
-  const int crop = 4 * blockIdx.x + 2 * P.g + blk;
-  const bool valid = crop < ncrops;
+  const int tile = 2 * cta + P.g;
+  int crop;
+  bool valid;
+  if (kv.mode == 0) {
+    crop = 4 * blockIdx.x + 2 * P.g + blk;
+    valid = crop < ncrops;
+  } else {
+    const int unit = 2 * tile + blk;
+    valid = unit < nunits;
+    crop = body ? unit * kv.body_feat_stride : kv.hand_feat_first + (unit / 2) * kv.body_feat_stride + unit % 2;
+  }
   // a group without a crop skips to the common teardown (one barrier site)
-  if (4 * (int)blockIdx.x + 2 * P.g < ncrops) {
+  if (kv.mode == 0 ? 4 * (int)blockIdx.x + 2 * P.g < ncrops : (P.g == 0 ? has0 : has1)) {
 
+  float y[HC];
+  if (kv.mode != 2) {
   // patchify (decoder.py:247-248): this thread packs image rows iy in
   // [4h, 4h + 4) of patch p into the K = 192 tile (k = iy*24 + ix*3 + c),
   // which spans this group's A, Q and K tiles
   {
-    uint8_t* tile = P.smem + S_A;
+    uint8_t* tile_a = P.smem + S_A;
     const int py = p / 8, px = p % 8;
     const float* src = crops + (int64_t)(valid ? crop : 0) * 64 * 64 * 3;
 #pragma unroll 1
@@ -809,7 +1099,7 @@ __global__ void __launch_bounds__(NTH, 1) k_encoder_tc(const float* __restrict__
       for (int q = 0; q < 3; ++q) {
         const float v[8] = {f4[2 * q].x, f4[2 * q].y, f4[2 * q].z, f4[2 * q].w,
                             f4[2 * q + 1].x, f4[2 * q + 1].y, f4[2 * q + 1].z, f4[2 * q + 1].w};
-        st_row8(tile, P.r, iy * 24 + 8 * q, 192, v);
+        st_row8(tile_a, P.r, iy * 24 + 8 * q, 192, v);
       }
     }
   }
@@ -835,7 +1125,6 @@ __global__ void __launch_bounds__(NTH, 1) k_encoder_tc(const float* __restrict__
     self_attn<BLK, false, true>(P, prm, x, x, valid);
     mlp(P, prm, x, valid);
   }
-  float y[HC];
   ln_half(P, x, w.norm_g, w.norm_b, y);
   if (valid) {
     float* out = feats + ((int64_t)crop * 64 + p) * D + HC * P.h;
@@ -847,6 +1136,15 @@ __global__ void __launch_bounds__(NTH, 1) k_encoder_tc(const float* __restrict__
     }
     flag_nonfinite(nonfinite, bad);
   }
+  } else {  // mode 2: the features are given
+    const float* in = kv.feats_in + ((int64_t)(valid ? crop : 0) * 64 + p) * D + HC * P.h;
+#pragma unroll
+    for (int c = 0; c < HC; c += 4) {
+      const float4 v = valid ? __ldg(reinterpret_cast<const float4*>(in + c)) : make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+      y[c] = v.x; y[c + 1] = v.y; y[c + 2] = v.z; y[c + 3] = v.w;
+    }
+  }
+  if (kv.mode != 0) kv_project(P, y, body, tile, kv);
   }  // group has crops
   teardown(P, 0);
 }
@@ -865,18 +1163,17 @@ struct BodyAux {  // fp32 scratch per body tile
   FKOut fk[2];
   float boxtok[2][4 * D];
 };
-// Hand tiles hold kHandsPerCta hands: slot i sits in row block i % 2, rows
-// 64 (i % 2) + 4 (i / 2) + token, so the two slots of a cross-attention
-// round (2c, 2c + 1) use key blocks 0 and 1 and every warp sees one.
-#ifndef FSB_HANDS_PER_CTA
-#define FSB_HANDS_PER_CTA 8  // 2 / 4 / 8 / 16 measured: DESIGN.md §4
+// Hand tiles hold FSB_HANDS_PER_TILE = 32 hands: slot i in rows [4 i, 4 i + 4)
+// (token t at row 4 i + t), so every warp holds eight whole hands.
+constexpr int kHandsPerCta = FSB_HANDS_PER_TILE;  // per tile
+#ifndef FSB_HAND_LATENCY_TILES
+#define FSB_HAND_LATENCY_TILES 2
 #endif
-constexpr int kHandsPerCta = FSB_HANDS_PER_CTA;  // per tile
-static_assert(kHandsPerCta >= 2 && kHandsPerCta <= 16 && kHandsPerCta % 2 == 0, "hand slots per tile");
+constexpr int kHandLatencyTiles = FSB_HAND_LATENCY_TILES;
 struct HandAux {
-  float t0[kHandsPerCta][D];
-  float rc[kHandsPerCta][8];   // rots[3], cams[3]
-  float pts[kHandsPerCta][6];  // 3 x (x, y) projected canonical points
+  float part[2][kHandsPerCta][6];  // head partial sums of the two column halves
+  float rc[kHandsPerCta][8];       // rots[3], cams[3]
+  float pts[kHandsPerCta][6];      // 3 x (x, y) projected canonical points
   int pred;
 };
 static_assert(sizeof(BodyAux) <= AUX_BYTES && sizeof(HandAux) <= AUX_BYTES, "aux scratch");
@@ -915,7 +1212,9 @@ __device__ void body_heads(Pipe& P, BodyAux& ax, const BodyW& w, const float* x)
   P.sync();
 }
 
-// LN(token 0) -> hand rotation / camera of every slot (decoder.py:384-391)
+// LN(token 0) -> hand rotation / camera of every slot (decoder.py:384-391):
+// each token-0 thread dots its 32 normalised columns with the six head
+// columns; the two halves meet in shared memory
 __device__ void hand_heads(Pipe& P, HandAux& ax, const HandW& w, const float* x) {
   float y[HC];
   if (x != nullptr) {
@@ -924,18 +1223,21 @@ __device__ void hand_heads(Pipe& P, HandAux& ax, const HandW& w, const float* x)
     load_row(P, y);
     ln_half(P, y, w.norm_g, w.norm_b, y);
   }
-  const int slot = 2 * ((P.r % BLK) >> 2) + P.r / BLK;
-  if ((P.r & 3) == 0 && slot < kHandsPerCta)
+  if ((P.r & 3) == 0) {
+    const int slot = P.r >> 2, c0 = HC * P.h;
+#pragma unroll 1
+    for (int o = 0; o < 6; ++o) {
+      const float* W = (o < 3 ? w.head_rot_w : w.head_cam_w) + o % 3;
+      float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
 #pragma unroll
-    for (int c = 0; c < HC; ++c) ax.t0[slot][HC * P.h + c] = y[c];
+      for (int k = 0; k < HC; ++k) acc[k & 3] = fmaf(y[k], __ldg(W + (c0 + k) * 3), acc[k & 3]);
+      ax.part[P.h][slot][o] = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+    }
+  }
   P.sync();
   if (P.tid < 6 * kHandsPerCta) {
     const int b = P.tid / 6, o = P.tid % 6;
-    const float* W = o < 3 ? w.head_rot_w : w.head_cam_w;
-    float acc[4] = {0.0f, 0.0f, 0.0f, 0.0f};
-#pragma unroll
-    for (int k = 0; k < D; ++k) acc[k & 3] = fmaf(ax.t0[b][k], __ldg(W + k * 3 + o % 3), acc[k & 3]);
-    ax.rc[b][o] = (acc[0] + acc[1]) + (acc[2] + acc[3]) + __ldg((o < 3 ? w.head_rot_b : w.head_cam_b) + o % 3);
+    ax.rc[b][o] = (ax.part[0][b][o] + ax.part[1][b][o]) + __ldg((o < 3 ? w.head_rot_b : w.head_cam_b) + o % 3);
   }
   P.sync();
 }
@@ -948,17 +1250,19 @@ __global__ void __launch_bounds__(NTH, 1) k_decoders_tc(DecodeArgs a, BodyW bw, 
   const bool body = (int)blockIdx.x < nbc;
   const int layers = body ? bw.layers : hw.layers;
   Pipe P;
+  // tiles per CTA: body NG; hands a.hand_tiles_per_cta (1: latency, 2: SM-time)
+  const int tpc = body ? NG : a.hand_tiles_per_cta;
   // groups with work in this CTA: tile 2 x + 1 exists?
-  const int tile1 = NG * (body ? (int)blockIdx.x : (int)blockIdx.x - nbc) + 1;
-  const bool has1 = body ? 2 * tile1 < a.nbody : kHandsPerCta * tile1 < a.nhand;
+  const int tile1 = tpc * (body ? (int)blockIdx.x : (int)blockIdx.x - nbc) + 1;
+  const bool has1 = tpc == 2 && (body ? 2 * tile1 < a.nbody : kHandsPerCta * tile1 < a.nhand);
   setup(P, sh, smem, body ? bw.tcs : hw.tcs, has1 ? 2u : 1u);
   const int t = P.tid;
   const int r = P.r, blk = r / BLK, c0 = HC * P.h;
-  const int tile = NG * (body ? (int)blockIdx.x : (int)blockIdx.x - nbc) + P.g;
-  // body: frame 2 tile + blk, token rb; hand: slot hs = 2 (r % 64 / 4) + blk, token rb
+  const int tile = tpc * (body ? (int)blockIdx.x : (int)blockIdx.x - nbc) + P.g;
+  // body: frame 2 tile + blk, token rb; hand: slot hs = r / 4, token rb
   const int hand0 = kHandsPerCta * tile;
   const int nslots = body ? 0 : max(0, min(kHandsPerCta, a.nhand - hand0));
-  const int hs = 2 * ((r % BLK) >> 2) + blk;
+  const int hs = r >> 2;
   const int rb = body ? r % BLK : (r & 3);
   const int unit = body ? 2 * tile + blk : 0;  // frame index (body tiles)
   const bool valid = body ? (unit < a.nbody && rb < 51) : hs < nslots;
@@ -966,9 +1270,9 @@ __global__ void __launch_bounds__(NTH, 1) k_decoders_tc(DecodeArgs a, BodyW bw, 
   // a group without a tile skips to the common teardown (one barrier site)
   if (P.g == 0 || has1) {
 
-  // feature row of this thread for the body's cross attention
-  const int crop = (body && unit < a.nbody ? unit : 0) * a.body_feat_stride;
-  const float* frow = a.feats + ((int64_t)crop * 64 + (r % BLK)) * D;
+  // this tile's projected cross-attention keys / values, one block per layer
+  const uint8_t* kvt = body ? a.body_kv + (size_t)tile * layers * FSB_KV_BODY_TILE
+                            : a.hand_kv;
 
   float x[HC];
   BodyAux& bx = *reinterpret_cast<BodyAux*>(smem + S_AUX + P.g * AUX_BYTES);
@@ -1080,9 +1384,9 @@ __global__ void __launch_bounds__(NTH, 1) k_decoders_tc(DecodeArgs a, BodyW bw, 
     P.prof[5] += ts1 - ts0;
 #endif
     if (body)
-      cross_attn(P, prm, x, frow, valid);
+      cross_attn(P, prm, x, kvt + (size_t)l * FSB_KV_BODY_TILE, valid);
     else
-      cross_attn_hands(P, prm, x, a, hand0, nslots, valid);
+      cross_attn_hands(P, prm, x, kvt, hand0, nslots, l, layers, valid);
 #ifdef FSB_PROFILE
     long long ts2 = clock64();
     P.prof[6] += ts2 - ts1;
@@ -1199,15 +1503,31 @@ cudaError_t init_attrs_transformer_tc() {
 }
 
 cudaError_t launch_encoder_tc(const float* crops, int ncrops, const EncW& w, float* feats, int* nonfinite,
-                              cudaStream_t st) {
-  if (ncrops == 0) return cudaSuccess;
-  k_encoder_tc<<<(ncrops + 2 * NG - 1) / (2 * NG), NTH, SMEM_TC, st>>>(crops, ncrops, w, feats, nonfinite);
+                              const KvArgs& kv, cudaStream_t st) {
+  int grid;
+  if (kv.mode == 0) {
+    grid = (ncrops + 2 * NG - 1) / (2 * NG);
+  } else {
+    const int bt = (kv.nbody + 1) / 2, ht = (kv.nhand + 1) / 2;
+    grid = (bt + NG - 1) / NG + (ht + NG - 1) / NG;
+  }
+  if (grid == 0) return cudaSuccess;
+  k_encoder_tc<<<grid, NTH, SMEM_TC, st>>>(crops, ncrops, w, feats, nonfinite, kv);
   return cudaGetLastError();
 }
 
-cudaError_t launch_decoders_tc(const DecodeArgs& a, const BodyW& bw, const HandW& hw, cudaStream_t st) {
+cudaError_t launch_decoders_tc(const DecodeArgs& a_in, const BodyW& bw, const HandW& hw, cudaStream_t st) {
+  DecodeArgs a = a_in;
   const int nbt = (a.nbody + 1) / 2, nht = (a.nhand + kHandsPerCta - 1) / kHandsPerCta;
-  const int n = (nbt + NG - 1) / NG + (nht + NG - 1) / NG;
+  // hand tiles per CTA: one each while the hands fit a few CTAs (the hand
+  // tiles' CUDA-core cross attention then has the SM to itself: latency),
+  // two per CTA for large batches (SM-time).  FSB_HAND_TPC overrides.
+  static const int forced = [] {
+    const char* e = getenv("FSB_HAND_TPC");
+    return e ? atoi(e) : 0;
+  }();
+  a.hand_tiles_per_cta = forced == 1 || forced == 2 ? forced : (nht <= kHandLatencyTiles ? 1 : 2);
+  const int n = (nbt + NG - 1) / NG + (nht + a.hand_tiles_per_cta - 1) / a.hand_tiles_per_cta;
   if (n == 0) return cudaSuccess;
   k_decoders_tc<<<n, NTH, SMEM_TC, st>>>(a, bw, hw);
   return cudaGetLastError();

@@ -66,6 +66,7 @@ _SIGS = {
     "fsb_bridge": (_i, [_p, _p, _i, _i, _p, _p, _i, _p, _p]),
     "fsb_bilinear": (_i, [_p, _p, _i, _i, _i, _p, _i64, _p, _p]),
     "fsb_encode": (_i, [_p, _p, _i, _p, _i, _p]),
+    "fsb_encode_frames": (_i, [_p, _p, _i, _p, _i, _p]),
     "fsb_decode_body": (_i, [_p, _p, _i, _i, _p, _u32, _p, _p, _p, _i, _p]),
     "fsb_decode_hands": (_i, [_p, _p, _i, _u32, _p, _i, _p]),
     "fsb_decode_frames": (_i, [_p, _p, _i, _p, _u32, _u32, _p, _p, _p, _p, _i, _p]),

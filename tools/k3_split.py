@@ -1,5 +1,6 @@
-"""Device time of the K3 decoder on body CTAs only, hand CTAs only and both
-(B = 32 frames, bf16, CUDA-graph replays): python tools/k3_split.py"""
+"""Device time of the K3 decoder on body CTAs only, hand CTAs only and both,
+of the encoder + K / V projection launch and of the decoders on projected
+K / V (B = 32 frames, bf16, CUDA-graph replays): python tools/k3_split.py"""
 import os
 import sys
 
@@ -38,7 +39,17 @@ if __name__ == "__main__":
         ctx.check(ctx.lib.fsb_decode_frames(ctx.h, rt.ptr(feats), B, rt.ptr(prompts), bsel, 0, rt.ptr(params),
                                             rt.ptr(cam), rt.ptr(rots), rt.ptr(merged), prec, ctx.stream))
 
-    for name, fn in (("body", body), ("hands", hands), ("both", both)):
+    crops = torch.rand((B, 3, 64, 64, 3), device="cuda")
+
+    def enc():  # encoder + K / V projection (fsb_encode_frames)
+        ctx.check(ctx.lib.fsb_encode_frames(ctx.h, rt.ptr(crops), B, rt.ptr(feats), prec, ctx.stream))
+
+    # body / hands / both: the decode API on given features (K / V projection
+    # + decoders); "decoders": the decoders alone on K / V projected by the
+    # encoder launch (the frame path)
+    for name, fn in (("body", body), ("hands", hands), ("both", both), ("encoder+kv", enc), ("decoders", both)):
+        if name == "decoders":
+            enc()
         for _ in range(3):
             fn()
         torch.cuda.synchronize()
