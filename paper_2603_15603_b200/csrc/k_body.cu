@@ -27,6 +27,7 @@ __global__ void __launch_bounds__(128) k_fk(const float* __restrict__ poses, int
   __shared__ float pose_s[4][66];
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int b = blockIdx.x * 4 + warp;
+  pdl_wait();
   if (b >= B) return;  // warp-uniform
   for (int i = lane; i < 66; i += 32) pose_s[warp][i] = poses[(int64_t)b * ld_pose + i];
   __syncwarp();
@@ -444,6 +445,7 @@ __global__ void __launch_bounds__(kLtThreads, 512 / kLtTmem)
     tc::mbar_expect_tx(&bar_basis, FSB_LBS_BASIS_BYTES);
     tc::bulk_g2s(lsm + kLtBasis, t.basis_img + (int64_t)blockIdx.x * FSB_LBS_BASIS_BYTES, FSB_LBS_BASIS_BYTES,
                  &bar_basis);
+    pdl_wait();  // the chunk records come from k_fk
     stage_in(c0, 0);
     if (c0 + G < nchunks) stage_in(c0 + G, 1);
   }
@@ -462,6 +464,7 @@ __global__ void __launch_bounds__(kLtThreads, 512 / kLtTmem)
 #pragma unroll
     for (int c = 0; c < 3; ++c) vr[e][c] = live ? __ldg(t.v_rest + (int64_t)v * 3 + c) : 0.0f;
   }
+  pdl_wait();  // (the template reads above are constant data)
   // every vertex pair of the warp has one joint set: one row read serves both
   bool same = true;
 #pragma unroll
@@ -718,6 +721,7 @@ __global__ void __launch_bounds__(kProjVcThreads) k_proj_inputs_vc(const float* 
   __shared__ float red[kProjVcThreads / 32][3];
   __shared__ float cen[3];
   const int b = blockIdx.x, tid = threadIdx.x;
+  pdl_wait();
   const float* Vb = V + (int64_t)b * nv * 3;
   const float o0 = __ldg(Vb), o1 = __ldg(Vb + 1), o2 = __ldg(Vb + 2);
   float acc[kProjVcPer][3];
@@ -869,8 +873,7 @@ __global__ void k_splitk_reduce(const float* __restrict__ P, int S, int M, int N
 cudaError_t launch_fk(const float* poses, int ld_pose, int B, const float* grest, float* joints, float* rel,
                       cudaStream_t st, uint8_t* lbs_in) {
   if (B == 0) return cudaSuccess;
-  k_fk<<<(B + 3) / 4, 128, 0, st>>>(poses, ld_pose, B, grest, joints, rel, lbs_in);
-  return cudaGetLastError();
+  return launch_pdl(k_fk, dim3((B + 3) / 4), dim3(128), 0, st, poses, ld_pose, B, grest, joints, rel, lbs_in);
 }
 
 // grid: (vertex tiles, chunk CTAs); each chunk CTA walks chunks y, y + G, ...
@@ -885,12 +888,11 @@ cudaError_t launch_lbs_tc(const TemplateDev& t, const uint8_t* lbs_in, int B, fl
   G = G < 1 ? 1 : (G > nchunks ? nchunks : G);
   dim3 grid(tiles, G);
   switch (t.nnz) {
-    case 2: k_lbs_tc<2><<<grid, kLtThreads, kLtSmem, st>>>(t, lbs_in, B, verts, nonfinite); break;
-    case 4: k_lbs_tc<4><<<grid, kLtThreads, kLtSmem, st>>>(t, lbs_in, B, verts, nonfinite); break;
-    case 8: k_lbs_tc<8><<<grid, kLtThreads, kLtSmem, st>>>(t, lbs_in, B, verts, nonfinite); break;
+    case 2: return launch_pdl(k_lbs_tc<2>, grid, dim3(kLtThreads), kLtSmem, st, t, lbs_in, B, verts, nonfinite);
+    case 4: return launch_pdl(k_lbs_tc<4>, grid, dim3(kLtThreads), kLtSmem, st, t, lbs_in, B, verts, nonfinite);
+    case 8: return launch_pdl(k_lbs_tc<8>, grid, dim3(kLtThreads), kLtSmem, st, t, lbs_in, B, verts, nonfinite);
     default: return cudaErrorInvalidValue;
   }
-  return cudaGetLastError();
 }
 
 cudaError_t launch_lbs(const TemplateDev& t, const float* rel, const float* poses, int ld_pose, int B, float* verts,
@@ -961,8 +963,7 @@ cudaError_t launch_proj_inputs_v(const float* V, int nv, const ProjectorDev& p, 
   if (B == 0) return cudaSuccess;
   if (p.n_sub > kProjVcThreads * kProjVcPer) return cudaErrorInvalidValue;
   (void)psum;
-  k_proj_inputs_vc<<<B, kProjVcThreads, 0, st>>>(V, nv, p, f32 ? sub : nullptr, xb);
-  return cudaGetLastError();
+  return launch_pdl(k_proj_inputs_vc, dim3(B), dim3(kProjVcThreads), 0, st, V, nv, p, f32 ? sub : nullptr, xb);
 }
 
 // number of K chunks of a layer: a function of K only (batch independence);

@@ -120,6 +120,8 @@ constexpr int kRowsPerCTA = 16;
 // sums of the reference), ahead of the gather CTAs that read them.
 __global__ void k_frame_boxes(const float* __restrict__ kps, int B, int W, int H, double alpha,
                               double* __restrict__ boxes_out, float* __restrict__ prompt_out) {
+  pdl_wait();
+  pdl_trigger();  // the gather CTAs may be scheduled right away (they wait for these boxes)
   const int f = blockIdx.x * blockDim.x + threadIdx.x;
   if (f >= B) return;
   float kp[2 * FSB_NJ];
@@ -140,6 +142,7 @@ __global__ void __launch_bounds__(256) k_boxes_crops(
   __shared__ float gx[512], gy[512];  // S <= 512 (checked by the launcher)
   const int f = blockIdx.z, crop = blockIdx.y, band = blockIdx.x;
   const int tid = threadIdx.x;
+  pdl_wait();
   // the frame's boxes come from k_frame_boxes (same stream, launched first)
   if (tid < 4) bx[tid] = boxes_out[((int64_t)f * 3 + crop) * 4 + tid];
   __syncthreads();
@@ -229,6 +232,7 @@ __global__ void __launch_bounds__(kStreamThreads) k_crops_stream(
   const int tid = threadIdx.x;
   const int r_begin = blockIdx.x * rows_per_cta;
   const int r_end = min(S, r_begin + rows_per_cta);
+  pdl_wait();
   if (r_begin >= S) return;
   if (tid < 2 * FSB_NJ) kp_s[tid] = clip_kp(kps[(int64_t)f * 2 * FSB_NJ + tid], tid, W, H);
   if (tid == 0) {
@@ -403,14 +407,14 @@ cudaError_t launch_boxes_crops(const float* images, const float* kps, int B, int
     const int rows_per_cta = ((nsub_total + bands - 1) / bands) * kRB;
     bands = (S + rows_per_cta - 1) / rows_per_cta;
     dim3 grid(bands, 3, B);
-    k_crops_stream<<<grid, kStreamThreads, stream_smem(rowcap4), st>>>(
-        images, kps, B, H, W, S, alpha, stride, rowcap4, rows_per_cta, boxes, prompt, crops, taps, nonfinite,
-        bytes_in);
+    return launch_pdl(k_crops_stream, grid, dim3(kStreamThreads), stream_smem(rowcap4), st, images, kps, B, H, W, S,
+                      alpha, stride, rowcap4, rows_per_cta, boxes, prompt, crops, taps, nonfinite, bytes_in);
   } else {  // HBM-resident (or very wide / unaligned host) frames: per-tap reads
-    k_frame_boxes<<<(B + 63) / 64, 64, 0, st>>>(kps, B, W, H, alpha, boxes, prompt);
+    cudaError_t e = launch_pdl(k_frame_boxes, dim3((B + 63) / 64), dim3(64), 0, st, kps, B, W, H, alpha, boxes, prompt);
+    if (e != cudaSuccess) return e;
     dim3 grid((S + kRowsPerCTA - 1) / kRowsPerCTA, 3, B);
-    k_boxes_crops<<<grid, 256, 0, st>>>(images, kps, B, H, W, S, alpha, stride, boxes, prompt, crops, taps,
-                                        nonfinite);
+    return launch_pdl(k_boxes_crops, grid, dim3(256), 0, st, images, kps, B, H, W, S, alpha, stride, boxes, prompt,
+                      crops, taps, nonfinite);
   }
   return cudaGetLastError();
 }

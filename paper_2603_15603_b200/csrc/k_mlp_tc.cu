@@ -31,6 +31,7 @@ __global__ void __launch_bounds__(128, 1) k_tile_gemm(const uint8_t* __restrict_
   const int tid = threadIdx.x, warp = tid / 32;
   const int nt = blockIdx.x, split = blockIdx.y, mt = blockIdx.z;
   const int kt0 = split * G, nk = min(G, KT - kt0);
+  pdl_wait();  // the A image comes from the previous kernel
   if (tid == 0) {
     for (int i = 0; i < 2; ++i) {
       tc::mbar_init(&bar_load[i], 1);
@@ -100,6 +101,7 @@ __global__ void k_tile_reduce(const float* __restrict__ P, int S, int M, int N, 
                               const float* __restrict__ mask, int relu, float* __restrict__ out, int ldo,
                               uint8_t* __restrict__ out_img, int KT_out, int* nonfinite) {
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  pdl_wait();
   if (idx >= (int64_t)M * N) return;
   const int m = (int)(idx / N), n = (int)(idx % N);
   float v = P[idx];
@@ -127,11 +129,9 @@ cudaError_t launch_tile_layer(const uint8_t* Aimg, const uint8_t* Bimg, int KT, 
   if (M == 0) return cudaSuccess;
   const int S = (KT + G - 1) / G;
   dim3 grid((N + 127) / 128, S, (M + 127) / 128);
-  k_tile_gemm<<<grid, 128, 4 * kTileBytes, st>>>(Aimg, KT, Bimg, G, M, N, partial);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_pdl(k_tile_gemm, grid, dim3(128), 4 * kTileBytes, st, Aimg, KT, Bimg, G, M, N, partial);
   if (e != cudaSuccess) return e;
   const int64_t tot = (int64_t)M * N;
-  k_tile_reduce<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(partial, S, M, N, bias, mask, relu, out, ldo, out_img,
-                                                               KT_out, nonfinite);
-  return cudaGetLastError();
+  return launch_pdl(k_tile_reduce, dim3((unsigned)((tot + 255) / 256)), dim3(256), 0, st, partial, S, M, N, bias, mask,
+                    relu, out, ldo, out_img, KT_out, nonfinite);
 }

@@ -886,6 +886,7 @@ __device__ void setup(Pipe& P, Shared& sh, uint8_t* smem, const TcStream* tab, u
 }
 
 __device__ void teardown(Pipe& P, int role) {
+  pdl_trigger();  // the next kernel's prologue may start (it waits for this grid's completion)
   tc::fence_before();
   __syncthreads();
   if (threadIdx.x < 32) tc::tmem_dealloc(P.sh->tmem, 512);
@@ -1064,6 +1065,7 @@ __global__ void __launch_bounds__(NTH, 1) k_encoder_tc(const float* __restrict__
     has1 = 2 * (2 * cta + 1) < nunits;
   }
   setup(P, sh, smem, kv.mode == 0 ? w.tcs : kv.tcs[body ? 0 : 1], has1 ? 2u : 1u);
+  pdl_wait();  // the weight stream is constant; crops / features come from the previous kernel
   const int blk = P.r / BLK, p = P.r % BLK;
   const int tile = 2 * cta + P.g;
   int crop;
@@ -1256,6 +1258,7 @@ __global__ void __launch_bounds__(NTH, 1) k_decoders_tc(DecodeArgs a, BodyW bw, 
   const int tile1 = tpc * (body ? (int)blockIdx.x : (int)blockIdx.x - nbc) + 1;
   const bool has1 = tpc == 2 && (body ? 2 * tile1 < a.nbody : kHandsPerCta * tile1 < a.nhand);
   setup(P, sh, smem, body ? bw.tcs : hw.tcs, has1 ? 2u : 1u);
+  pdl_wait();
   const int t = P.tid;
   const int r = P.r, blk = r / BLK, c0 = HC * P.h;
   const int tile = tpc * (body ? (int)blockIdx.x : (int)blockIdx.x - nbc) + P.g;
@@ -1512,8 +1515,7 @@ cudaError_t launch_encoder_tc(const float* crops, int ncrops, const EncW& w, flo
     grid = (bt + NG - 1) / NG + (ht + NG - 1) / NG;
   }
   if (grid == 0) return cudaSuccess;
-  k_encoder_tc<<<grid, NTH, SMEM_TC, st>>>(crops, ncrops, w, feats, nonfinite, kv);
-  return cudaGetLastError();
+  return launch_pdl(k_encoder_tc, dim3(grid), dim3(NTH), SMEM_TC, st, crops, ncrops, w, feats, nonfinite, kv);
 }
 
 cudaError_t launch_decoders_tc(const DecodeArgs& a_in, const BodyW& bw, const HandW& hw, cudaStream_t st) {
@@ -1529,6 +1531,5 @@ cudaError_t launch_decoders_tc(const DecodeArgs& a_in, const BodyW& bw, const Ha
   a.hand_tiles_per_cta = forced == 1 || forced == 2 ? forced : (nht <= kHandLatencyTiles ? 1 : 2);
   const int n = (nbt + NG - 1) / NG + (nht + a.hand_tiles_per_cta - 1) / a.hand_tiles_per_cta;
   if (n == 0) return cudaSuccess;
-  k_decoders_tc<<<n, NTH, SMEM_TC, st>>>(a, bw, hw);
-  return cudaGetLastError();
+  return launch_pdl(k_decoders_tc, dim3(n), dim3(NTH), SMEM_TC, st, a, bw, hw);
 }
