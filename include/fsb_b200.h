@@ -193,6 +193,13 @@ int fsb_bary_map(fsb_ctx* ctx, const double* src_verts, int nv, const int64_t* s
                  const double* tgt_verts, int nt, uint8_t* degenerate, int64_t* face_index, float* weights,
                  void* stream);
 
+/* Load (hidden > 0, host arrays w1 (63, hidden), b1 (hidden), w2 (hidden, 63),
+ * b2 (63)) or remove (hidden == 0) the kinematic-prior denoiser of
+ * projection.denoise (projection.py:684-697) as an epilogue of the SMPL tail:
+ * fsb_skin_project / fsb_frame_batch then return theta with theta[3:66]
+ * denoised and the SMPL joints of the denoised pose.  Part of the (shared)
+ * model. */
+int fsb_load_denoiser(fsb_ctx* ctx, const float* w1, const float* b1, const float* w2, const float* b2, int hidden);
 /* projection.denoise (projection.py:684-697): poses (B, 63) body-pose
  * parameters -> out (B, 63) = x + relu(x W1 + b1) W2 + b2, W1 (63, hidden),
  * W2 (hidden, 63), hidden <= 128; bit-identical to the reference's

@@ -28,7 +28,8 @@ cudaError_t launch_encoder_f32(const float* crops, int ncrops, const EncW& w, fl
                                cudaStream_t st);
 cudaError_t launch_decoders_f32(const DecodeArgs& a, const BodyW& bw, const HandW& hw, cudaStream_t st);
 cudaError_t launch_fk(const float* poses, int ld_pose, int B, const float* grest, float* joints, float* rel,
-                      cudaStream_t st, uint8_t* lbs_in = nullptr);
+                      cudaStream_t st, uint8_t* lbs_in = nullptr, const DenoiseW* dn = nullptr,
+                      int* nonfinite = nullptr);
 cudaError_t launch_lbs_tc(const TemplateDev& t, const uint8_t* lbs_in, int B, float* verts, int* nonfinite,
                           cudaStream_t st);
 cudaError_t launch_lbs(const TemplateDev& t, const float* rel, const float* poses, int ld_pose, int B, float* verts,
@@ -145,6 +146,10 @@ struct fsb_model {
   bool has_proj = false;
   DevMem proj_mem;
   ProjectorDev proj{};
+  // optional kinematic-prior denoiser, applied to theta[3:66] by the frame
+  // path's SMPL FK (fsb_load_denoiser)
+  DevMem dn_mem;
+  DenoiseW dn{nullptr, nullptr, nullptr, nullptr, 0};
 };
 
 struct fsb_ctx {
@@ -1433,10 +1438,10 @@ static bool lbs_simt() {
 }
 
 static int fk_lbs(fsb_ctx* c, int which, const float* poses, int B, float* rel, uint8_t* lbsin, float* joints,
-                  float* verts, cudaStream_t st) {
+                  float* verts, cudaStream_t st, const DenoiseW* dn = nullptr) {
   const TemplateDev& t = c->m->tmpl[which];
   const bool tc = verts != nullptr && !lbs_simt();
-  FSB_CUDA(c, launch_fk(poses, FSB_PARAM_DIM, B, t.joints_rest, joints, rel, st, tc ? lbsin : nullptr));
+  FSB_CUDA(c, launch_fk(poses, FSB_PARAM_DIM, B, t.joints_rest, joints, rel, st, tc ? lbsin : nullptr, dn, c->d_flag));
   c->launches += B > 0;
   if (verts == nullptr) return FSB_OK;
   if (tc)
@@ -1525,7 +1530,9 @@ static int skin_project_impl(fsb_ctx* c, const float* params, int B, float* v_mh
   }
   rc = run_mlp(c, B, theta, precision, st);
   if (rc) return rc;
-  return fk_lbs(c, FSB_SMPL, theta, B, v_smpl ? c->w_rel2 : nullptr, c->w_lbsin2, j_smpl, v_smpl, st);
+  // SMPL FK (+ the denoiser epilogue on theta[3:66] when one is loaded)
+  return fk_lbs(c, FSB_SMPL, theta, B, v_smpl ? c->w_rel2 : nullptr, c->w_lbsin2, j_smpl, v_smpl, st,
+                c->m->dn.H > 0 ? &c->m->dn : nullptr);
 }
 
 int fsb_skin_project(fsb_ctx* c, const float* params, int B, float* v_mhr, float* theta, float* j_smpl,
@@ -1659,6 +1666,31 @@ int fsb_bary_map(fsb_ctx* c, const double* src_verts, int nv, const int64_t* src
                           (cudaStream_t)stream));
   c->launches += 2 * (nt > 0);
   note_stream(c, (cudaStream_t)stream);
+  return FSB_OK;
+}
+
+int fsb_load_denoiser(fsb_ctx* c, const float* w1, const float* b1, const float* w2, const float* b2, int hidden) {
+  if (hidden == 0 || w1 == nullptr) {  // remove
+    c->m->dn = DenoiseW{nullptr, nullptr, nullptr, nullptr, 0};
+    c->m->dn_mem.release();
+    model_changed(c);
+    return FSB_OK;
+  }
+  if (hidden < 0 || hidden > FSB_DN_MAX_HIDDEN)
+    return fail(c, FSB_ERR_USAGE, "denoiser: hidden width %d not in [1, %d]", hidden, FSB_DN_MAX_HIDDEN);
+  if (!b1 || !w2 || !b2) return fail(c, FSB_ERR_USAGE, "denoiser: null weight");
+  const size_t n1 = (size_t)FSB_DN_IN * hidden, n2 = (size_t)hidden * FSB_DN_IN;
+  const size_t tot = n1 + hidden + n2 + FSB_DN_IN;
+  std::vector<float> h(tot);
+  memcpy(h.data(), w1, n1 * 4);
+  memcpy(h.data() + n1, b1, (size_t)hidden * 4);
+  memcpy(h.data() + n1 + hidden, w2, n2 * 4);
+  memcpy(h.data() + n1 + hidden + n2, b2, FSB_DN_IN * 4);
+  FSB_CUDA(c, c->m->dn_mem.alloc(tot * 4));
+  FSB_CUDA(c, cudaMemcpy(c->m->dn_mem.p, h.data(), tot * 4, cudaMemcpyHostToDevice));
+  const float* d = static_cast<const float*>(c->m->dn_mem.p);
+  c->m->dn = DenoiseW{d, d + n1, d + n1 + hidden, d + n1 + hidden + n2, hidden};
+  model_changed(c);
   return FSB_OK;
 }
 

@@ -171,3 +171,44 @@ __device__ __forceinline__ void fk_warp(const float* pose, const float* grest, F
   }
   __syncwarp();
 }
+
+// ---------------------------------------------------------------------------
+// kinematic-prior denoiser (reference projection.py:684-697,
+// _denoise_forward :684-686): out = x + (relu(x W1 + b1) W2 + b2) on a
+// (63,) body pose, one warp.  Both products follow numkit.matmul
+// (numkit.py:78-90): every dot product is a left-to-right sum from +0 with a
+// separately rounded product and add, so the result is bit-identical to the
+// reference.  Lane j owns hidden units j, j + 32, ...; outputs m = lane,
+// lane + 32.  Used by k_denoise and as the optional epilogue of the SMPL FK
+// (k_fk) on the frame path.
+// ---------------------------------------------------------------------------
+struct DenoiseW {
+  const float* w1;  // (63, H)
+  const float* b1;
+  const float* w2;  // (H, 63)
+  const float* b2;
+  int H;            // 0: no denoiser
+};
+#define FSB_DN_IN 63
+#define FSB_DN_MAX_HIDDEN 128
+
+// xs: the pose (shared, 63); hs: hidden scratch (shared, H); out: 63 values
+// (may alias nothing the warp still reads)
+__device__ __forceinline__ void denoise_warp(const float* xs, float* hs, const DenoiseW& d, int lane, float* out,
+                                             int* nonfinite) {
+  for (int j = lane; j < d.H; j += 32) {
+    float acc = 0.0f;
+    for (int k = 0; k < FSB_DN_IN; ++k) acc = __fadd_rn(acc, __fmul_rn(xs[k], __ldg(d.w1 + (int64_t)k * d.H + j)));
+    hs[j] = fmaxf(__fadd_rn(acc, __ldg(d.b1 + j)), 0.0f);
+  }
+  __syncwarp();
+  for (int m = lane; m < FSB_DN_IN; m += 32) {
+    float acc = 0.0f;
+    for (int j = 0; j < d.H; ++j) acc = __fadd_rn(acc, __fmul_rn(hs[j], __ldg(d.w2 + (int64_t)j * FSB_DN_IN + m)));
+    const float v = __fadd_rn(xs[m], __fadd_rn(acc, __ldg(d.b2 + m)));
+    flag_nonfinite(nonfinite, v);
+    out[m] = v;
+  }
+  __syncwarp();
+}
+

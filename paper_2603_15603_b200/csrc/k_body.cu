@@ -20,17 +20,32 @@
 // lbs_in (nullable): the k_lbs_tc chunk records (fsb_weights.h
 // FSB_LBS_REC_*): transforms interleaved by mesh pairs and the shape
 // coefficients split into bf16 hi + lo (hi = bf16(s), lo = bf16(s - hi)).
-__global__ void __launch_bounds__(128) k_fk(const float* __restrict__ poses, int ld_pose, int B,
+// dn.H > 0 (the SMPL FK of the frame path with a denoiser loaded): the body
+// pose theta[3:66] is first replaced by denoise(theta[3:66]) (projection.py:
+// 684-697), in `poses` too, so FK, skinning and the returned theta see it
+// (SURVEY §8(f) row 1 as a K4 epilogue).
+__global__ void __launch_bounds__(128) k_fk(float* __restrict__ poses, int ld_pose, int B,
                                             const float* __restrict__ grest, float* __restrict__ joints,
-                                            float* __restrict__ rel, uint8_t* __restrict__ lbs_in) {
+                                            float* __restrict__ rel, uint8_t* __restrict__ lbs_in, DenoiseW dn,
+                                            int* nonfinite) {
   __shared__ FKOut fk[4];
   __shared__ float pose_s[4][66];
+  __shared__ float dn_h[4][FSB_DN_MAX_HIDDEN];
+  __shared__ float dn_o[4][64];
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int b = blockIdx.x * 4 + warp;
   pdl_wait();
   if (b >= B) return;  // warp-uniform
   for (int i = lane; i < 66; i += 32) pose_s[warp][i] = poses[(int64_t)b * ld_pose + i];
   __syncwarp();
+  if (dn.H > 0) {
+    denoise_warp(pose_s[warp] + 3, dn_h[warp], dn, lane, dn_o[warp], nonfinite);
+    for (int i = lane; i < FSB_DN_IN; i += 32) {
+      pose_s[warp][3 + i] = dn_o[warp][i];
+      poses[(int64_t)b * ld_pose + 3 + i] = dn_o[warp][i];
+    }
+    __syncwarp();
+  }
   fk_warp(pose_s[warp], grest, fk[warp], lane);
   if (lane < FSB_NJ) {
     const int j = lane;
@@ -871,9 +886,12 @@ __global__ void k_splitk_reduce(const float* __restrict__ P, int S, int M, int N
 // launchers
 // ---------------------------------------------------------------------------
 cudaError_t launch_fk(const float* poses, int ld_pose, int B, const float* grest, float* joints, float* rel,
-                      cudaStream_t st, uint8_t* lbs_in) {
+                      cudaStream_t st, uint8_t* lbs_in, const DenoiseW* dn, int* nonfinite) {
   if (B == 0) return cudaSuccess;
-  return launch_pdl(k_fk, dim3((B + 3) / 4), dim3(128), 0, st, poses, ld_pose, B, grest, joints, rel, lbs_in);
+  const DenoiseW d = dn ? *dn : DenoiseW{nullptr, nullptr, nullptr, nullptr, 0};
+  // (poses is written only with a denoiser: the caller passes a writable theta then)
+  return launch_pdl(k_fk, dim3((B + 3) / 4), dim3(128), 0, st, const_cast<float*>(poses), ld_pose, B, grest, joints,
+                    rel, lbs_in, d, nonfinite);
 }
 
 // grid: (vertex tiles, chunk CTAs); each chunk CTA walks chunks y, y + G, ...

@@ -12,41 +12,27 @@
 
 namespace {
 constexpr int kDnWarps = 4;
-constexpr int kDnMaxHidden = 128;
-constexpr int kDnIn = 63;
 }  // namespace
 
-__global__ void __launch_bounds__(32 * kDnWarps) k_denoise(const float* __restrict__ x, int B, const float* __restrict__ w1,
-                                                          const float* __restrict__ b1, const float* __restrict__ w2,
-                                                          const float* __restrict__ b2, int H, float* __restrict__ out,
-                                                          int* nonfinite) {
+// one warp per pose (denoise_warp, fsb_common.cuh)
+__global__ void __launch_bounds__(32 * kDnWarps) k_denoise(const float* __restrict__ x, int B, DenoiseW d,
+                                                          float* __restrict__ out, int* nonfinite) {
   __shared__ float xs[kDnWarps][64];
-  __shared__ float hs[kDnWarps][kDnMaxHidden];
+  __shared__ float hs[kDnWarps][FSB_DN_MAX_HIDDEN];
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int b = blockIdx.x * kDnWarps + warp;
   if (b >= B) return;  // warp-uniform
-  const float* xb = x + (int64_t)b * kDnIn;
-  for (int k = lane; k < kDnIn; k += 32) xs[warp][k] = xb[k];
+  const float* xb = x + (int64_t)b * FSB_DN_IN;
+  for (int k = lane; k < FSB_DN_IN; k += 32) xs[warp][k] = xb[k];
   __syncwarp();
-  for (int j = lane; j < H; j += 32) {
-    float acc = 0.0f;
-    for (int k = 0; k < kDnIn; ++k) acc = __fadd_rn(acc, __fmul_rn(xs[warp][k], __ldg(w1 + (int64_t)k * H + j)));
-    hs[warp][j] = fmaxf(__fadd_rn(acc, __ldg(b1 + j)), 0.0f);
-  }
-  __syncwarp();
-  for (int m = lane; m < kDnIn; m += 32) {
-    float acc = 0.0f;
-    for (int j = 0; j < H; ++j) acc = __fadd_rn(acc, __fmul_rn(hs[warp][j], __ldg(w2 + (int64_t)j * kDnIn + m)));
-    const float v = __fadd_rn(xs[warp][m], __fadd_rn(acc, __ldg(b2 + m)));
-    flag_nonfinite(nonfinite, v);
-    out[(int64_t)b * kDnIn + m] = v;
-  }
+  denoise_warp(xs[warp], hs[warp], d, lane, out + (int64_t)b * FSB_DN_IN, nonfinite);
 }
 
 cudaError_t launch_denoise(const float* x, int B, const float* w1, const float* b1, const float* w2, const float* b2,
                            int H, float* out, int* nonfinite, cudaStream_t st) {
   if (B == 0) return cudaSuccess;
-  if (H <= 0 || H > kDnMaxHidden) return cudaErrorInvalidValue;
-  k_denoise<<<(B + kDnWarps - 1) / kDnWarps, 32 * kDnWarps, 0, st>>>(x, B, w1, b1, w2, b2, H, out, nonfinite);
+  if (H <= 0 || H > FSB_DN_MAX_HIDDEN) return cudaErrorInvalidValue;
+  const DenoiseW d{w1, b1, w2, b2, H};
+  k_denoise<<<(B + kDnWarps - 1) / kDnWarps, 32 * kDnWarps, 0, st>>>(x, B, d, out, nonfinite);
   return cudaGetLastError();
 }

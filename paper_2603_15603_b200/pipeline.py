@@ -265,11 +265,14 @@ _STAGE_GROUPS = (("crop", ("detect", "hand_boxes", "crop_body", "crop_hands")),
 class Pipeline:
     """Runs one Decoder (and, when given, the MHR -> SMPL tail) on the GPU."""
 
-    def __init__(self, decoder, mhr=None, bmap=None, projector=None, precision="fp32", device=None):
+    def __init__(self, decoder, mhr=None, bmap=None, projector=None, precision="fp32", device=None, denoiser=None):
         self.decoder = decoder
         self.template = decoder.template
         self.crop_size = decoder.config.crop_size
         self.mhr, self.bmap, self.projector = mhr, bmap, projector
+        # optional projection.DenoiserWeights: theta[3:66] = denoise(theta[3:66])
+        # before the SMPL FK, fused into the tail's FK kernel (projection.py:684-697)
+        self.denoiser = denoiser
         self.precision = precision
         if device is None:
             import torch
@@ -286,7 +289,7 @@ class Pipeline:
         uploaded model: one per in-flight stream (SPEC.md:383 -- pipelines
         are per thread; the frozen weights are not duplicated on the GPU)."""
         p = Pipeline(self.decoder, mhr=self.mhr, bmap=self.bmap, projector=self.projector,
-                     precision=self.precision, device=self.device)
+                     precision=self.precision, device=self.device, denoiser=self.denoiser)
         p._parent = self if self._parent is None else self._parent
         return p
 
@@ -306,6 +309,8 @@ class Pipeline:
             ctx.load_template(runtime.FSB_MHR, self.mhr)
         if st.get("projector", (None, None))[0] is not self.projector or st["projector"][1] is not self.bmap:
             ctx.load_projector(self.projector, self.bmap)
+        if st.get("denoiser") is not self.denoiser:
+            ctx.load_denoiser(self.denoiser)
 
     def context(self):
         model = self.decoder.context(self.device)

@@ -80,6 +80,7 @@ _SIGS = {
     "fsb_counters": (_i, [_p, ctypes.POINTER(CountersC)]),
     "fsb_input_bytes": (_i, [_p, ctypes.POINTER(ctypes.c_int64), _i]),
     "fsb_denoise": (_i, [_p, _p, _i, _p, _p, _p, _p, _i, _p, _p]),
+    "fsb_load_denoiser": (_i, [_p, _p, _p, _p, _p, _i]),
     "fsb_bary_map": (_i, [_p, _p, _i, _p, _i, _p, _i, _p, _p, _p, _p]),
     "fsb_fit_batch": (_i, [_p, _p, _i, _i, _p, _i, _d, ctypes.c_float, ctypes.c_float, _p, _p, _p, _p, _p, _p]),
     "fsb_kernel_launches": (_i64, [_p]),
@@ -308,6 +309,21 @@ class Context:
         freeze(weights.w1, weights.b1, weights.w2, weights.b2, weights.w3, weights.b3, weights.mask,
                weights.subsample, bmap.corners, bmap.weights)
         self.model_state["projector"] = (weights, bmap)
+
+    def load_denoiser(self, weights):
+        """Denoiser epilogue of the SMPL tail (projection.denoise on
+        theta[3:66] before the SMPL FK); None removes it."""
+        if weights is None:
+            self.check(self.lib.fsb_load_denoiser(self.h, None, None, None, None, 0), "load_denoiser")
+        else:
+            w1, b1, w2, b2 = [np.ascontiguousarray(a, np.float32) for a in (weights.w1, weights.b1, weights.w2, weights.b2)]
+            hid = w1.shape[1] if w1.ndim == 2 else -1
+            if w1.shape != (63, hid) or b1.shape != (hid,) or w2.shape != (hid, 63) or b2.shape != (63,):
+                raise ShapeError("denoiser weights must be (63, h), (h,), (h, 63), (63,)")
+            self.check(self.lib.fsb_load_denoiser(self.h, w1.ctypes.data, b1.ctypes.data, w2.ctypes.data,
+                                                  b2.ctypes.data, hid), "load_denoiser")
+            freeze(weights.w1, weights.b1, weights.w2, weights.b2)
+        self.model_state["denoiser"] = weights
 
 
 # ---------------------------------------------------------------------------
