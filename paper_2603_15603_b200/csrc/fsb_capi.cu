@@ -27,6 +27,17 @@ cudaError_t launch_bilinear(const float* img, int H, int W, int C, const float* 
 cudaError_t launch_encoder_f32(const float* crops, int ncrops, const EncW& w, float* feats, int* nonfinite,
                                cudaStream_t st);
 cudaError_t launch_decoders_f32(const DecodeArgs& a, const BodyW& bw, const HandW& hw, cudaStream_t st);
+bool proj_fused_ok(const ProjectorDev& p);
+// The one-launch cluster projector (k_proj_fused) is opt-in (FSB_PROJ_FUSED=1):
+// measured against the split-K tile GEMMs it lowers the saturated per-batch
+// cost (3.59 vs 4.46 us at cluster size 8) but raises the batch latency
+// (33 vs 23 us) and the C3 time (0.66 vs 0.54 ms) -- DESIGN.md §4.
+static bool proj_fused_on() {
+  static const bool on = getenv("FSB_PROJ_FUSED") != nullptr;
+  return on;
+}
+cudaError_t launch_proj_fused(const uint8_t* ximg, const ProjectorDev& p, int B, float* theta, const float* grest,
+                              float* joints, const DenoiseW* dn, int* nonfinite, cudaStream_t st);
 cudaError_t launch_fk(const float* poses, int ld_pose, int B, const float* grest, float* joints, float* rel,
                       cudaStream_t st, uint8_t* lbs_in = nullptr, const DenoiseW* dn = nullptr,
                       int* nonfinite = nullptr);
@@ -1505,6 +1516,13 @@ int fsb_project_vertices(fsb_ctx* c, const float* v_mhr, int B, int nv, float* t
   const bool tc = mlp_tc(c, precision);
   FSB_CUDA(c, launch_proj_inputs_v(v_mhr, nv, c->m->proj, B, c->w_x, !tc, tc ? c->w_xb : nullptr, c->w_psum, st));
   c->launches += B > 0;  // bridge + centre in one kernel
+  if (tc && proj_fused_ok(c->m->proj) && proj_fused_on()) {  // the MLP in one launch
+    FSB_CUDA(c, launch_proj_fused(reinterpret_cast<const uint8_t*>(c->w_xb), c->m->proj, B, theta, nullptr, nullptr,
+                                  nullptr, c->d_flag, st));
+    c->launches += B > 0;
+    note_stream(c, st);
+    return FSB_OK;
+  }
   rc = run_mlp(c, B, theta, precision, st);
   if (rc == FSB_OK) note_stream(c, st);
   return rc;
@@ -1528,11 +1546,18 @@ static int skin_project_impl(fsb_ctx* c, const float* params, int B, float* v_mh
                                    tc ? c->w_xb : nullptr, c->w_psum, st));
     c->launches += 2;  // re-skinned inputs, centre
   }
+  const DenoiseW* dn = c->m->dn.H > 0 ? &c->m->dn : nullptr;
+  if (tc && v_smpl == nullptr && proj_fused_ok(c->m->proj) && proj_fused_on()) {
+    // MLP (3 layers, mask), denoiser and SMPL FK in one cluster launch (k_mlp_tc.cu)
+    FSB_CUDA(c, launch_proj_fused(reinterpret_cast<const uint8_t*>(c->w_xb), c->m->proj, B, theta,
+                                  c->m->tmpl[FSB_SMPL].joints_rest, j_smpl, dn, c->d_flag, st));
+    c->launches += B > 0;
+    return FSB_OK;
+  }
   rc = run_mlp(c, B, theta, precision, st);
   if (rc) return rc;
   // SMPL FK (+ the denoiser epilogue on theta[3:66] when one is loaded)
-  return fk_lbs(c, FSB_SMPL, theta, B, v_smpl ? c->w_rel2 : nullptr, c->w_lbsin2, j_smpl, v_smpl, st,
-                c->m->dn.H > 0 ? &c->m->dn : nullptr);
+  return fk_lbs(c, FSB_SMPL, theta, B, v_smpl ? c->w_rel2 : nullptr, c->w_lbsin2, j_smpl, v_smpl, st, dn);
 }
 
 int fsb_skin_project(fsb_ctx* c, const float* params, int B, float* v_mhr, float* theta, float* j_smpl,

@@ -15,6 +15,7 @@
 // bias / ReLU / mask.  The K partition depends on K only, so a mesh gives the
 // same bits in a batch of 4096 as alone.
 #include "fsb_common.cuh"
+#include "fsb_weights.h"
 #include "tc_sm100.cuh"
 
 namespace {
@@ -134,4 +135,330 @@ cudaError_t launch_tile_layer(const uint8_t* Aimg, const uint8_t* Bimg, int KT, 
   const int64_t tot = (int64_t)M * N;
   return launch_pdl(k_tile_reduce, dim3((unsigned)((tot + 255) / 256)), dim3(256), 0, st, partial, S, M, N, bias, mask,
                     relu, out, ldo, out_img, KT_out, nonfinite);
+}
+
+// ===========================================================================
+// Fused projector (bf16 mode): the three MLP layers of
+// projection._projector_mlp (projection.py:468-472), the output mask, the
+// optional denoiser on theta[3:66] (projection.py:684-697) and the SMPL FK
+// (bodymodel.py:266) for NM meshes in ONE launch: a cluster of CS CTAs,
+// partial sums reduced through distributed shared memory instead of global
+// partial buffers and separate reduce launches.
+//
+// Transposed formulation: D^T (outputs x meshes) = W^T (outputs x K, the
+// uploaded K-major tile images, M = 128) . X^T, the meshes as the N = NM
+// operand -- a 32-mesh batch costs a 32-wide MMA instead of a 128-row tile.
+//   layer 1: CTA (mt = rank % 4, kq = rank / 4): h1 rows [128 mt, +128) over
+//            k-tiles [kq KTq, (kq + 1) KTq) of x (the projector-input image:
+//            rows = meshes); ranks 0..3 sum the four K quarters in order,
+//            + b1, ReLU -> h1 k-tile mt as the next layer's bf16 operand
+//   layer 2: rank u < 8: h2 rows [128 (u % 2), +128) x h1 k-tile u / 2
+//            (pulled from rank u / 2); ranks 0, 1 sum + b2, ReLU
+//   layer 3: ranks 0, 1: theta rows x h2 k-tile (own); rank 0 sums, + b3,
+//            * mask -> theta
+//   FK:      warp w of rank r takes mesh r + CS w (theta read from rank 0)
+// Every reduction adds the partials in a fixed order, so a mesh gives the
+// same bits at any batch position.
+// ===========================================================================
+namespace {
+template <int NM>
+constexpr int pf_stages() { return NM == 32 ? 3 : 2; }  // ring depth within the shared-memory budget
+
+__device__ __forceinline__ float4 ld_dsmem_f4(uint32_t addr) {
+  float4 v;
+  asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];\n"
+               : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w)
+               : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ uint4 ld_dsmem_u4(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared::cluster.v4.u32 {%0, %1, %2, %3}, [%4];\n"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w)
+               : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ float ld_dsmem_f(uint32_t addr) {
+  float v;
+  asm volatile("ld.shared::cluster.f32 %0, [%1];\n" : "=f"(v) : "r"(addr));
+  return v;
+}
+}  // namespace
+
+template <int NM, int CS>
+__global__ void __launch_bounds__(128, 1)
+    k_proj_fused(const uint8_t* __restrict__ ximg, ProjectorDev p, int B, float* __restrict__ theta,
+                 const float* __restrict__ grest, float* __restrict__ joints, DenoiseW dn, int* nonfinite) {
+  static_assert(NM == 32 || NM == 64, "meshes per cluster");
+  static_assert(CS == 8 || CS == 16, "cluster size");
+  constexpr int kPfStages = pf_stages<NM>();
+  constexpr uint32_t kX = NM * 256;                    // x / h slice: NM rows x K = 128 bf16
+  constexpr uint32_t kStage = kTileBytes + kX;
+  constexpr uint32_t oRing = 0;
+  constexpr uint32_t oPart = oRing + kPfStages * kStage;  // fp32 [128][NM]
+  constexpr uint32_t oHt = oPart + 128 * NM * 4;         // this CTA's produced operand slice
+  constexpr uint32_t oHb = oHt + kX;                     // the consumed (pulled) operand slice
+  constexpr uint32_t oTh = oHb + kX;                     // theta [NM][80] (rank 0)
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ __align__(8) uint64_t bar_full[3], bar_free[3], bar_mma, bar_w;
+  __shared__ uint32_t tmem_base;
+  __shared__ FKOut fk[4];
+  __shared__ float pose_s[4][66];
+  __shared__ float dn_h[4][FSB_DN_MAX_HIDDEN];
+  __shared__ float dn_o[4][64];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t rank = tc::cluster_rank();
+  const int m0 = (int)(blockIdx.x / CS) * NM;            // first mesh of this cluster
+  float* part = reinterpret_cast<float*>(smem + oPart);
+  uint8_t* ht = smem + oHt;
+  uint8_t* hb = smem + oHb;
+  float* th = reinterpret_cast<float*>(smem + oTh);
+  const uint32_t sbase = tc::smem_u32(smem);
+  const uint32_t idesc = tc::idesc_bf16(128, NM);
+  if (tid == 0) {
+    for (int i = 0; i < kPfStages; ++i) {
+      tc::mbar_init(&bar_full[i], 1);
+      tc::mbar_init(&bar_free[i], 1);
+    }
+    tc::mbar_init(&bar_mma, 1);
+    tc::mbar_init(&bar_w, 1);
+    tc::mbar_fence_init();
+  }
+  if (warp == 0) tc::tmem_alloc(&tmem_base, NM < 32 ? 32 : NM);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = tmem_base;
+  const uint32_t tl = tmem + ((uint32_t)(32 * warp) << 16);
+  uint32_t mma_phase = 0;
+  pdl_wait();  // x comes from the projector-input kernel
+
+  // D (TMEM, lanes = output rows of this tile, columns = meshes) -> part
+  auto drain = [&]() {
+    tc::mbar_wait(&bar_mma, mma_phase);
+    mma_phase ^= 1u;
+    tc::fence_after();
+#pragma unroll
+    for (int c = 0; c < NM; c += 32) {
+      float v[32];
+      tc::tmem_ld32(tl + c, v);
+#pragma unroll
+      for (int i = 0; i < 32; i += 4)
+        *reinterpret_cast<float4*>(part + tid * NM + c + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+    }
+    tc::fence_before();
+  };
+  // sum of the partials of `nsrc` ranks (rank0 + step k), row tid, fixed order
+  auto gather_sum = [&](int rank0, int step, int nsrc, float* acc) {
+#pragma unroll
+    for (int n = 0; n < NM; ++n) acc[n] = 0.0f;
+    for (int k = 0; k < nsrc; ++k) {
+      const uint32_t src = tc::mapa_shared(part + tid * NM, (uint32_t)(rank0 + step * k));
+#pragma unroll
+      for (int n = 0; n < NM; n += 4) {
+        const float4 v = ld_dsmem_f4(src + 4 * n);
+        acc[n] += v.x; acc[n + 1] += v.y; acc[n + 2] += v.z; acc[n + 3] += v.w;
+      }
+    }
+  };
+  // activations of rows [128 t0, +128) as the next layer's operand: mesh n,
+  // K index tid (bf16, K-major over 128)
+  auto store_operand = [&](const float* acc) {
+#pragma unroll
+    for (int n = 0; n < NM; ++n)
+      *reinterpret_cast<__nv_bfloat16*>(ht + tc::kmajor_off(n, tid, 128)) =
+          __float2bfloat16_rn(m0 + n < B ? acc[n] : 0.0f);
+    tc::fence_async_smem();
+  };
+
+  // ---- layer 1 ------------------------------------------------------------
+  constexpr int kNkq = CS / 4;  // K splits of layer 1
+  const int KT1 = p.KT1, KTq = (KT1 + kNkq - 1) / kNkq;  // (>= 1 k-tile each for the projector's K)
+  {
+    const int mt = (int)rank & 3, kq = (int)rank >> 2;
+    const int kt0 = kq * KTq, nk = max(0, min(KTq, KT1 - kt0));
+    if (tid == 0) {
+      const uint8_t* xsrc = ximg + ((size_t)(m0 / 128) * KT1) * kTileBytes + (size_t)((m0 % 128) / 8) * 2048;
+      auto load = [&](int i) {
+        const int s = i % kPfStages;
+        tc::mbar_expect_tx(&bar_full[s], kStage);
+        tc::bulk_g2s(smem + oRing + s * kStage, p.img_w1 + ((size_t)mt * KT1 + kt0 + i) * kTileBytes, kTileBytes,
+                     &bar_full[s]);
+        tc::bulk_g2s(smem + oRing + s * kStage + kTileBytes, xsrc + (size_t)(kt0 + i) * kTileBytes, kX,
+                     &bar_full[s]);
+      };
+      for (int i = 0; i < min(nk, kPfStages); ++i) load(i);
+      for (int i = 0; i < nk; ++i) {
+        const int s = i % kPfStages;
+        tc::mbar_wait(&bar_full[s], (uint32_t)((i / kPfStages) & 1));
+        tc::fence_after();
+        const uint32_t a = sbase + oRing + s * kStage, b = a + kTileBytes;
+        for (int k = 0; k < 128; k += 16)
+          tc::mma_bf16(tmem, tc::kmajor_desc(a, 128, k), tc::kmajor_desc(b, 128, k), idesc, (i | k) != 0);
+        tc::mma_commit(&bar_free[s]);
+        if (i + kPfStages < nk) {
+          tc::mbar_wait(&bar_free[s], (uint32_t)((i / kPfStages) & 1));
+          load(i + kPfStages);
+        }
+      }
+      tc::mma_commit(&bar_mma);
+    }
+    __syncwarp();
+    drain();
+  }
+  tc::cluster_sync_all();
+  if (rank < 4) {  // h1 k-tile `rank`
+    float acc[NM];
+    gather_sum((int)rank, 4, kNkq, acc);
+    const float b = __ldg(p.b1 + 128 * rank + tid);
+#pragma unroll
+    for (int n = 0; n < NM; ++n) acc[n] = fmaxf(acc[n] + b, 0.0f);
+    store_operand(acc);
+  }
+  tc::cluster_sync_all();
+
+  // ---- layer 2 ------------------------------------------------------------
+  const int KT2 = p.KT2;  // 4 (h1 = 512)
+  if ((int)rank < 2 * KT2) {
+    const int mt2 = (int)rank & 1, kt2 = (int)rank >> 1;
+    if (tid == 0) {
+      tc::mbar_expect_tx(&bar_w, kTileBytes);
+      tc::bulk_g2s(smem + oRing, p.img_w2 + ((size_t)mt2 * KT2 + kt2) * kTileBytes, kTileBytes, &bar_w);
+    }
+    const uint32_t src = tc::mapa_shared(ht, (uint32_t)kt2);
+    for (uint32_t o = 16 * tid; o < kX; o += 16 * 128)
+      *reinterpret_cast<uint4*>(hb + o) = ld_dsmem_u4(src + o);
+    tc::fence_async_smem();
+    __syncthreads();
+    if (tid == 0) {
+      tc::mbar_wait(&bar_w, 0);
+      tc::fence_after();
+      const uint32_t a = sbase + oRing, b = sbase + oHb;
+      for (int k = 0; k < 128; k += 16)
+        tc::mma_bf16(tmem, tc::kmajor_desc(a, 128, k), tc::kmajor_desc(b, 128, k), idesc, k != 0);
+      tc::mma_commit(&bar_mma);
+    }
+    __syncwarp();
+    drain();
+  }
+  tc::cluster_sync_all();
+  if (rank < 2) {  // h2 k-tile `rank`
+    float acc[NM];
+    gather_sum((int)rank, 2, KT2, acc);
+    const float b = __ldg(p.b2 + 128 * rank + tid);
+#pragma unroll
+    for (int n = 0; n < NM; ++n) acc[n] = fmaxf(acc[n] + b, 0.0f);
+    store_operand(acc);
+  }
+  tc::cluster_sync_all();
+
+  // ---- layer 3 ------------------------------------------------------------
+  const int KT3 = p.KT3;  // 2 (h2 = 256)
+  if ((int)rank < KT3) {
+    if (tid == 0) {
+      tc::mbar_expect_tx(&bar_w, kTileBytes);
+      tc::bulk_g2s(smem + oRing, p.img_w3 + (size_t)rank * kTileBytes, kTileBytes, &bar_w);
+      tc::mbar_wait(&bar_w, 1);
+      tc::fence_after();
+      const uint32_t a = sbase + oRing, b = sbase + oHt;  // h2 k-tile `rank` is this CTA's own
+      for (int k = 0; k < 128; k += 16)
+        tc::mma_bf16(tmem, tc::kmajor_desc(a, 128, k), tc::kmajor_desc(b, 128, k), idesc, k != 0);
+      tc::mma_commit(&bar_mma);
+    }
+    __syncwarp();
+    drain();
+  }
+  tc::cluster_sync_all();
+  if (rank == 0 && tid < FSB_PARAM_DIM) {  // theta = (sum + b3) * mask
+    float acc[NM];
+    gather_sum(0, 1, KT3, acc);
+    const float b = __ldg(p.b3 + tid), mk = __ldg(p.mask + tid);
+#pragma unroll
+    for (int n = 0; n < NM; ++n) {
+      const float v = (acc[n] + b) * mk;
+      th[n * 80 + tid] = v;
+      if (m0 + n < B) {
+        flag_nonfinite(nonfinite, v);
+        theta[(int64_t)(m0 + n) * FSB_PARAM_DIM + tid] = v;
+      }
+    }
+  }
+  tc::cluster_sync_all();
+
+  // ---- SMPL FK (+ denoiser) -------------------------------------------------
+  for (int w = warp; joints != nullptr && w * CS < NM; w += 4) {  // (joints == nullptr: projector only)
+    const int n = (int)rank + CS * w, b = m0 + n;
+    if (b >= B) continue;  // warp-uniform
+    const uint32_t src = tc::mapa_shared(th + n * 80, 0u);
+    for (int i = lane; i < 66; i += 32) pose_s[warp][i] = ld_dsmem_f(src + 4 * i);
+    __syncwarp();
+    if (dn.H > 0) {
+      denoise_warp(pose_s[warp] + 3, dn_h[warp], dn, lane, dn_o[warp], nonfinite);
+      for (int i = lane; i < FSB_DN_IN; i += 32) {
+        pose_s[warp][3 + i] = dn_o[warp][i];
+        theta[(int64_t)b * FSB_PARAM_DIM + 3 + i] = dn_o[warp][i];
+      }
+      __syncwarp();
+    }
+    fk_warp(pose_s[warp], grest, fk[warp], lane);
+    if (lane < FSB_NJ)
+      for (int a = 0; a < 3; ++a) joints[((int64_t)b * FSB_NJ + lane) * 3 + a] = fk[warp].tw[lane][a];
+    __syncwarp();
+  }
+  tc::cluster_sync_all();  // rank 0's theta and the operand slices stay alive until every CTA is done
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc(tmem, NM < 32 ? 32 : NM);
+}
+
+namespace {
+template <int NM, int CS>
+constexpr uint32_t proj_fused_smem() {
+  return pf_stages<NM>() * (kTileBytes + NM * 256) + 128 * NM * 4 + 2 * NM * 256 + NM * 80 * 4;
+}
+template <int NM, int CS>
+cudaError_t launch_pf(const uint8_t* ximg, const ProjectorDev& p, int B, float* theta, const float* grest,
+                      float* joints, const DenoiseW& dn, int* nonfinite, cudaStream_t st) {
+  auto k = k_proj_fused<NM, CS>;
+  static bool init = false;
+  if (!init) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)proj_fused_smem<NM, CS>());
+    if (e != cudaSuccess) return e;
+    if (CS > 8) {
+      e = cudaFuncSetAttribute(k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      if (e != cudaSuccess) return e;
+    }
+    init = true;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3((unsigned)(((B + NM - 1) / NM) * CS));
+  cfg.blockDim = dim3(128);
+  cfg.dynamicSmemBytes = proj_fused_smem<NM, CS>();
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CS;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 2;
+  return cudaLaunchKernelEx(&cfg, k, ximg, p, B, theta, grest, joints, dn, nonfinite);
+}
+}  // namespace
+
+#ifndef FSB_PF_CS
+#define FSB_PF_CS 8  // 16 measured slower under concurrent streams (cluster placement)
+#endif
+// true when the fused projector serves this projector's shape (h1 = 512,
+// h2 = 256, theta = 76 outputs: the default (512, 256) widths)
+bool proj_fused_ok(const ProjectorDev& p) { return p.h1 == 512 && p.h2 == 256 && p.KT2 == 4 && p.KT3 == 2; }
+
+cudaError_t launch_proj_fused(const uint8_t* ximg, const ProjectorDev& p, int B, float* theta, const float* grest,
+                              float* joints, const DenoiseW* dn, int* nonfinite, cudaStream_t st) {
+  if (B == 0) return cudaSuccess;
+  const DenoiseW d = dn ? *dn : DenoiseW{nullptr, nullptr, nullptr, nullptr, 0};
+  if (B <= 32) return launch_pf<32, FSB_PF_CS>(ximg, p, B, theta, grest, joints, d, nonfinite, st);
+  return launch_pf<64, FSB_PF_CS>(ximg, p, B, theta, grest, joints, d, nonfinite, st);
 }
