@@ -42,14 +42,14 @@ cudaError_t launch_fk(const float* poses, int ld_pose, int B, const float* grest
                       cudaStream_t st, uint8_t* lbs_in = nullptr, const DenoiseW* dn = nullptr,
                       int* nonfinite = nullptr);
 cudaError_t launch_lbs_tc(const TemplateDev& t, const uint8_t* lbs_in, int B, float* verts, int* nonfinite,
-                          cudaStream_t st);
+                          cudaStream_t st, CornerOut cu = CornerOut());
 cudaError_t launch_lbs(const TemplateDev& t, const float* rel, const float* poses, int ld_pose, int B, float* verts,
                        int* nonfinite, cudaStream_t st);
 cudaError_t launch_proj_inputs(const TemplateDev& t, const ProjectorDev& p, const float* rel, const float* poses,
                                int ld_pose, int B, float* sub, bool f32, __nv_bfloat16* xb, float* psum,
                                cudaStream_t st);
 cudaError_t launch_proj_inputs_v(const float* V, int nv, const ProjectorDev& p, int B, float* sub, bool f32,
-                                 __nv_bfloat16* xb, float* psum, cudaStream_t st);
+                                 __nv_bfloat16* xb, float* psum, cudaStream_t st, bool compacted = false);
 cudaError_t launch_gemm_f32(const float* A, int lda, const float* W, const float* bias, const float* mask, float* C,
                             int ldc, int M, int N, int K, int relu, int* nonfinite, float* partial,
                             cudaStream_t st);
@@ -189,7 +189,7 @@ struct fsb_ctx {
   double* w_boxes = nullptr;
   float *w_prompt = nullptr, *w_crops = nullptr, *w_feats = nullptr, *w_params = nullptr, *w_cam = nullptr,
         *w_rots = nullptr, *w_rel = nullptr, *w_rel2 = nullptr, *w_x = nullptr, *w_h1 = nullptr, *w_h2 = nullptr,
-        *w_theta = nullptr, *w_part = nullptr, *w_psum = nullptr;
+        *w_theta = nullptr, *w_part = nullptr, *w_psum = nullptr, *w_vu = nullptr;
   __nv_bfloat16* w_xb = nullptr;  // projector input as a bf16 A-tile image
   uint8_t *w_lbsin = nullptr, *w_lbsin2 = nullptr;  // k_lbs_tc chunk records (MHR, SMPL)
   uint8_t *w_bkv = nullptr, *w_hkv = nullptr;  // projected cross-attention K / V (bf16 decoders)
@@ -599,6 +599,7 @@ int fsb_reserve(fsb_ctx* c, int max_frames) {
   const int hmax = h1 > h2 ? (h1 > 76 ? h1 : 76) : (h2 > 76 ? h2 : 76);
   const size_t o_part = take(F * 16 * (size_t)hmax * 4);  // split-K partials (<= 16 chunks)
   const size_t o_psum = take(F * 8 * 3 * 4);               // projector-input centroid partials
+  const size_t o_vu = take(F * (size_t)(c->m->has_proj ? c->m->proj.nu : 1) * 3 * 4);  // compacted corners
   const size_t lbsin_bytes = (F + FSB_LBS_N - 1) / FSB_LBS_N * (size_t)FSB_LBS_REC_BYTES;
   const size_t o_lbsin = take(lbsin_bytes);
   const size_t o_lbsin2 = take(lbsin_bytes);
@@ -631,6 +632,7 @@ int fsb_reserve(fsb_ctx* c, int max_frames) {
   c->w_theta = reinterpret_cast<float*>(b + o_theta);
   c->w_part = reinterpret_cast<float*>(b + o_part);
   c->w_psum = reinterpret_cast<float*>(b + o_psum);
+  c->w_vu = reinterpret_cast<float*>(b + o_vu);
   // the shape images' K padding (k >= 10) and meshes past B stay zero
   FSB_CUDA(c, cudaMemset(b + o_lbsin, 0, o_lbsin2 - o_lbsin + lbsin_bytes));
   c->w_lbsin = b + o_lbsin;
@@ -1113,7 +1115,31 @@ int fsb_load_projector(fsb_ctx* c, int n_sub, int h1, int h2, const int64_t* cor
   if (n_sub <= 0 || h1 <= 0 || h2 <= 0) return fail(c, FSB_ERR_SHAPE, "projector sizes must be positive");
   const int K = 3 * n_sub;
   std::vector<int32_t> cr((size_t)n_sub * 3);
-  for (size_t i = 0; i < cr.size(); ++i) cr[i] = (int32_t)corners[i];
+  int32_t cmax = 0;
+  for (size_t i = 0; i < cr.size(); ++i) {
+    cr[i] = (int32_t)corners[i];
+    if (cr[i] < 0) return fail(c, FSB_ERR_SHAPE, "projector corner %d is negative", cr[i]);
+    cmax = cr[i] > cmax ? cr[i] : cmax;
+  }
+  // compacted corner slots (ProjectorDev::nu): vertex 0 first, then the
+  // distinct corners in vertex order
+  std::vector<int32_t> vslot((size_t)cmax + 1, -1), ucr(cr.size());
+  std::vector<char> used(vslot.size(), 0);
+  for (int32_t v : cr) used[v] = 1;
+  int32_t nu = 0;
+  vslot[0] = nu++;
+  for (size_t v = 1; v < vslot.size(); ++v)
+    if (used[v]) vslot[v] = nu++;
+  for (size_t i = 0; i < cr.size(); ++i) ucr[i] = vslot[cr[i]];
+  const size_t nblk = vslot.size() / 64 + 1;
+  std::vector<int32_t> ublk(nblk * 2, 0);
+  std::vector<uint8_t> ulist(nblk * 64, 0);
+  for (size_t v = 0; v < vslot.size(); ++v) {
+    if (vslot[v] < 0) continue;
+    const size_t bi = v / 64;
+    if (ublk[2 * bi + 1] == 0) ublk[2 * bi] = vslot[v];  // slots rise with v: the block's run starts here
+    ulist[bi * 64 + ublk[2 * bi + 1]++] = (uint8_t)(v % 64);
+  }
   // bf16 tile images of W^T (k_mlp_tc.cu): [n_tile][k_tile] 128 x 128
   // K-major tiles, zero padded in both n and k
   auto tile_image = [](const float* W, int Kin, int Nout) {
@@ -1136,6 +1162,10 @@ int fsb_load_projector(fsb_ctx* c, int n_sub, int h1, int h2, const int64_t* cor
   Packer pk;
   const size_t o_c = pk.add(cr.data(), cr.size() * 4);
   const size_t o_bw = pk.add(bary, (size_t)n_sub * 12);
+  const size_t o_vs = pk.add(vslot.data(), vslot.size() * 4);
+  const size_t o_uc = pk.add(ucr.data(), ucr.size() * 4);
+  const size_t o_ub = pk.add(ublk.data(), ublk.size() * 4);
+  const size_t o_ul = pk.add(ulist.data(), ulist.size());
   const size_t o_w1 = pk.add(w1, (size_t)K * h1 * 4);
   const size_t o_b1 = pk.add(b1, (size_t)h1 * 4);
   const size_t o_w2 = pk.add(w2, (size_t)h1 * h2 * 4);
@@ -1155,6 +1185,12 @@ int fsb_load_projector(fsb_ctx* c, int n_sub, int h1, int h2, const int64_t* cor
   p.h2 = h2;
   p.corners = reinterpret_cast<const int32_t*>(base + o_c);
   p.bw = reinterpret_cast<const float*>(base + o_bw);
+  p.nu = (nu + 3) & ~3;  // mesh stride of the buffer a multiple of 16 bytes (staged with 16-byte loads)
+  p.nvslot = (int)vslot.size();
+  p.vslot = reinterpret_cast<const int32_t*>(base + o_vs);
+  p.ucorners = reinterpret_cast<const int32_t*>(base + o_uc);
+  p.ublk = reinterpret_cast<const int32_t*>(base + o_ub);
+  p.ulist = reinterpret_cast<const uint8_t*>(base + o_ul);
   p.w1 = reinterpret_cast<const float*>(base + o_w1);
   p.b1 = reinterpret_cast<const float*>(base + o_b1);
   p.w2 = reinterpret_cast<const float*>(base + o_w2);
@@ -1449,14 +1485,14 @@ static bool lbs_simt() {
 }
 
 static int fk_lbs(fsb_ctx* c, int which, const float* poses, int B, float* rel, uint8_t* lbsin, float* joints,
-                  float* verts, cudaStream_t st, const DenoiseW* dn = nullptr) {
+                  float* verts, cudaStream_t st, const DenoiseW* dn = nullptr, CornerOut cu = CornerOut()) {
   const TemplateDev& t = c->m->tmpl[which];
   const bool tc = verts != nullptr && !lbs_simt();
   FSB_CUDA(c, launch_fk(poses, FSB_PARAM_DIM, B, t.joints_rest, joints, rel, st, tc ? lbsin : nullptr, dn, c->d_flag));
   c->launches += B > 0;
   if (verts == nullptr) return FSB_OK;
   if (tc)
-    FSB_CUDA(c, launch_lbs_tc(t, lbsin, B, verts, c->d_flag, st));
+    FSB_CUDA(c, launch_lbs_tc(t, lbsin, B, verts, c->d_flag, st, cu));
   else
     FSB_CUDA(c, launch_lbs(t, rel, poses, FSB_PARAM_DIM, B, verts, c->d_flag, st));
   c->launches += B > 0;
@@ -1533,13 +1569,30 @@ static int skin_project_impl(fsb_ctx* c, const float* params, int B, float* v_mh
   if (!c->m->has_proj || !c->m->has_tmpl[FSB_MHR] || !c->m->has_tmpl[FSB_SMPL])
     return fail(c, FSB_ERR_USAGE, "skin_project: projector or templates missing");
   const TemplateDev& mhr = c->m->tmpl[FSB_MHR];
-  int rc = fk_lbs(c, FSB_MHR, params, B, c->w_rel, c->w_lbsin, nullptr, v_mhr, st);
+  const ProjectorDev& pj = c->m->proj;
+  const bool bridge = v_mhr && getenv("FSB_PROJ_RESKIN") == nullptr;
+  // the LBS kernel also writes the projector's corner vertices compacted
+  // (tensor-core LBS only; FSB_PROJ_SCATTER=1 bridges from V_mhr's rows)
+  CornerOut cu;
+  if (bridge && !lbs_simt() && pj.nvslot <= mhr.nv && getenv("FSB_PROJ_SCATTER") == nullptr) {
+    cu.vu = c->w_vu;
+    cu.ublk = pj.ublk;
+    cu.ulist = pj.ulist;
+    cu.vslot = pj.vslot;
+    cu.nvslot = pj.nvslot;
+    cu.nu = pj.nu;
+  }
+  int rc = fk_lbs(c, FSB_MHR, params, B, c->w_rel, c->w_lbsin, nullptr, v_mhr, st, nullptr, cu);
   if (rc) return rc;
   const bool tc = mlp_tc(c, precision);
-  if (v_mhr && getenv("FSB_PROJ_RESKIN") == nullptr) {
+  if (bridge) {
     // V_mhr was just written: bridge its corner vertices (what the reference
-    // projects, projection.py:447-465) instead of re-skinning them
-    FSB_CUDA(c, launch_proj_inputs_v(v_mhr, mhr.nv, c->m->proj, B, c->w_x, !tc, tc ? c->w_xb : nullptr, c->w_psum, st));
+    // projects, projection.py:447-465) instead of re-skinning them -- from
+    // the compacted corner buffer when the LBS kernel filled it
+    if (cu.vu)
+      FSB_CUDA(c, launch_proj_inputs_v(cu.vu, pj.nu, pj, B, c->w_x, !tc, tc ? c->w_xb : nullptr, c->w_psum, st, true));
+    else
+      FSB_CUDA(c, launch_proj_inputs_v(v_mhr, mhr.nv, pj, B, c->w_x, !tc, tc ? c->w_xb : nullptr, c->w_psum, st));
     c->launches += 1;  // bridge + centre
   } else {
     FSB_CUDA(c, launch_proj_inputs(mhr, c->m->proj, c->w_rel, params, FSB_PARAM_DIM, B, c->w_x, !tc,

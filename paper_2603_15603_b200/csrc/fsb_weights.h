@@ -164,7 +164,12 @@ struct TemplateDev {
 // per-chunk record written by k_fk (lbs_in): the chunk's joint transforms
 // interleaved by mesh pairs (float2 [N/2][22 * 12]) and its shape
 // coefficients as bf16 hi / lo images (N meshes x K = 16, K-major)
-#define FSB_LBS_REC_A2 (FSB_LBS_N / 2 * 22 * 12 * 8)
+// float2 slots per joint in the interleaved transforms (12 used; padding to
+// 14 or 16 to spread the joints over the banks measured no faster at C3)
+#ifndef FSB_LBS_JS
+#define FSB_LBS_JS 12
+#endif
+#define FSB_LBS_REC_A2 (FSB_LBS_N / 2 * 22 * FSB_LBS_JS * 8)
 #define FSB_LBS_REC_B (FSB_LBS_N * 16 * 2)
 #define FSB_LBS_REC_BYTES (FSB_LBS_REC_A2 + 2 * FSB_LBS_REC_B)
 
@@ -187,6 +192,27 @@ struct ProjectorDev {
   const uint8_t* img_w2;  // (h2 / 128) x KT2, KT2 = h1 / 128
   const uint8_t* img_w3;  // 1 x KT3 (76 rows used), KT3 = h2 / 128
   int KT1, KT2, KT3;
+  // compacted corner vertices: the LBS kernel writes the nu distinct corner
+  // vertices of every mesh (vertex 0, the bridge origin, is slot 0) to a
+  // (B, nu, 3) buffer as it skins them, and the bridge gathers from that
+  // instead of from scattered rows of V_mhr
+  int nu;                 // distinct corner vertices (+ vertex 0)
+  int nvslot;             // length of vslot (max corner id + 1)
+  const int32_t* vslot;   // (nvslot) slot of a source vertex in the compacted buffer, -1 if unused
+  const int32_t* ucorners;  // (n_sub, 3) corners as slots
+  // per 64-vertex block (one LBS warp's vertices): first slot, corner count,
+  // and the block-local vertex of each of its corners in slot order
+  const int32_t* ublk;    // (nvslot / 64 + 1, 2)
+  const uint8_t* ulist;   // (nvslot / 64 + 1, 64)
+};
+
+// optional compacted corner output of the LBS kernel (ProjectorDev::nu)
+struct CornerOut {
+  float* vu = nullptr;             // (B, nu, 3) or null
+  const int32_t* ublk = nullptr;   // ProjectorDev::ublk / ulist
+  const uint8_t* ulist = nullptr;
+  const int32_t* vslot = nullptr;  // ProjectorDev::vslot (per-thread scatter variant, FSB_LBS_URUN=0)
+  int nvslot = 0, nu = 0;
 };
 
 // arguments of the fused decoder launch (k_transformer.cu)

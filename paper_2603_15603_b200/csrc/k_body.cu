@@ -63,7 +63,7 @@ __global__ void __launch_bounds__(128) k_fk(float* __restrict__ poses, int ld_po
     if (lbs_in != nullptr) {
       uint8_t* rec = lbs_in + (int64_t)(b / FSB_LBS_N) * FSB_LBS_REC_BYTES;
       const int m = b % FSB_LBS_N;
-      float* a2 = reinterpret_cast<float*>(rec) + ((m >> 1) * FSB_NJ * 12 + j * 12) * 2 + (m & 1);
+      float* a2 = reinterpret_cast<float*>(rec) + ((m >> 1) * FSB_NJ * FSB_LBS_JS + j * FSB_LBS_JS) * 2 + (m & 1);
       for (int a = 0; a < 3; ++a) {
         a2[2 * (4 * a + 0)] = fk[warp].rw[j][3 * a + 0];
         a2[2 * (4 * a + 1)] = fk[warp].rw[j][3 * a + 1];
@@ -412,7 +412,7 @@ __device__ __forceinline__ void lbs_apply(const float2* pairA, const int* jj, co
 #pragma unroll
   for (int z = 0; z < NZ; ++z) {
     const float2 wz = make_float2(w[z], w[z]);
-    const float4* row = reinterpret_cast<const float4*>(pairA + 12 * jj[z]);
+    const float4* row = reinterpret_cast<const float4*>(pairA + FSB_LBS_JS * jj[z]);
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
       const float4 r01 = row[2 * a], r23 = row[2 * a + 1];  // (R_a0, R_a1 | R_a2, t_a) x 2 meshes
@@ -426,7 +426,8 @@ __device__ __forceinline__ void lbs_apply(const float2* pairA, const int* jj, co
 
 template <int NZ>
 __global__ void __launch_bounds__(kLtThreads, 512 / kLtTmem)
-    k_lbs_tc(TemplateDev t, const uint8_t* __restrict__ lbs_in, int B, float* __restrict__ verts, int* nonfinite) {
+    k_lbs_tc(TemplateDev t, const uint8_t* __restrict__ lbs_in, int B, float* __restrict__ verts, int* nonfinite,
+             CornerOut cu) {
   extern __shared__ __align__(1024) uint8_t lsm[];
   __shared__ __align__(8) uint64_t bar_basis, bar_stage[2], bar_mma[2];
   __shared__ uint32_t tmem_base;
@@ -478,6 +479,30 @@ __global__ void __launch_bounds__(kLtThreads, 512 / kLtTmem)
     }
 #pragma unroll
     for (int c = 0; c < 3; ++c) vr[e][c] = live ? __ldg(t.v_rest + (int64_t)v * 3 + c) : 0.0f;
+  }
+  // the warp's projector corners (compacted buffer, ProjectorDev::ublk):
+  // nuf floats from slot u0 on; this lane stores floats lane + 32 i, whose
+  // staging-row offsets (< 192) are packed four to a register
+#ifndef FSB_LBS_URUN  // 1: the warp's corners as one contiguous run from the staging rows (measured slower)
+#define FSB_LBS_URUN 0
+#endif
+  int u0 = 0, nuf = 0;
+  uint32_t uoff[2] = {0u, 0u};
+#if !FSB_LBS_URUN
+  int slot[2];
+#pragma unroll
+  for (int e = 0; e < 2; ++e) slot[e] = cu.vu != nullptr && va + e < cu.nvslot ? __ldg(cu.vslot + va + e) : -1;
+#endif
+  if (FSB_LBS_URUN && cu.vu != nullptr && vw < cu.nvslot) {
+    const int bi = vw >> 6;
+    u0 = __ldg(cu.ublk + 2 * bi);
+    nuf = 3 * __ldg(cu.ublk + 2 * bi + 1);
+#pragma unroll
+    for (int i = 0; i < 6; ++i) {
+      const int f = lane + 32 * i;
+      const uint32_t o = f < nuf ? 3u * __ldg(cu.ulist + 64 * bi + f / 3) + f % 3 : 0u;
+      uoff[i >> 2] |= o << (8 * (i & 3));
+    }
   }
   pdl_wait();  // (the template reads above are constant data)
   // every vertex pair of the warp has one joint set: one row read serves both
@@ -531,7 +556,7 @@ __global__ void __launch_bounds__(kLtThreads, 512 / kLtTmem)
 #pragma unroll
     for (int p = 0; p < kLtHalf / 2; ++p) {
       if (2 * p >= nm) continue;  // warp-uniform (the last chunk of a batch)
-      const float2* pairA = A2 + (kLtHalf / 2 * mh + p) * (FSB_NJ * 12);
+      const float2* pairA = A2 + (kLtHalf / 2 * mh + p) * (FSB_NJ * FSB_LBS_JS);
       float2 vs[2][3], o[2][3];
 #pragma unroll
       for (int e = 0; e < 2; ++e)
@@ -540,7 +565,7 @@ __global__ void __launch_bounds__(kLtThreads, 512 / kLtTmem)
       if (reuse) {  // one read of each transform row for both vertices
 #pragma unroll
         for (int z = 0; z < NZ; ++z) {
-          const float4* row = reinterpret_cast<const float4*>(pairA + 12 * jj[0][z]);
+          const float4* row = reinterpret_cast<const float4*>(pairA + FSB_LBS_JS * jj[0][z]);
 #pragma unroll
           for (int a = 0; a < 3; ++a) {
             const float4 r01 = row[2 * a], r23 = row[2 * a + 1];
@@ -563,6 +588,18 @@ __global__ void __launch_bounds__(kLtThreads, 512 / kLtTmem)
         if (va + e < t.nv)
 #pragma unroll
           for (int a = 0; a < 3; ++a) chk = ffma2(o[e][a], make_float2(1.0f, 1.0f), chk);
+#if !FSB_LBS_URUN
+#pragma unroll
+      for (int e = 0; e < 2; ++e)
+        if (slot[e] >= 0) {
+          float* u = cu.vu + ((int64_t)(m0 + 2 * p) * cu.nu + slot[e]) * 3;
+#pragma unroll
+          for (int a = 0; a < 3; ++a) u[a] = o[e][a].x;
+          if (2 * p + 1 < nm)
+#pragma unroll
+            for (int a = 0; a < 3; ++a) u[(int64_t)cu.nu * 3 + a] = o[e][a].y;
+        }
+#endif
       // the warp's 64 vertices of meshes m, m + 1 leave as coalesced rows
       // through its staging buffer (2 x 192 floats).  Measured alternatives
       // (DESIGN.md §4): cp.async.bulk of the 16-byte-aligned interior and
@@ -589,6 +626,17 @@ __global__ void __launch_bounds__(kLtThreads, 512 / kLtTmem)
         for (int i = 0; i < 6; ++i) {
           const int idx = 32 * i + lane;
           if (idx < nfw) __stcs(dst + idx, stg[half * kLtRow + idx]);
+        }
+        // the warp's projector corners, one contiguous run of the
+        // compacted (B, nu, 3) corner buffer (L2-resident for the bridge)
+        if (nuf > 0) {
+          float* ud = cu.vu + ((int64_t)(m + half) * cu.nu + u0) * 3;
+#pragma unroll
+          for (int i = 0; i < 6; ++i) {
+            const int f = lane + 32 * i;
+            if (32 * i >= nuf) break;  // warp-uniform
+            if (f < nuf) ud[f] = stg[half * kLtRow + ((uoff[i >> 2] >> (8 * (i & 3))) & 0xffu)];
+          }
         }
       }
       __syncwarp();  // the staging rows are rewritten by the next pair
@@ -728,64 +776,130 @@ __global__ void __launch_bounds__(256) k_proj_inputs(TemplateDev t, ProjectorDev
 // and/or straight into the bf16 A-tile image of the tensor-core MLP -- the
 // centroid is a CTA reduction (fixed order, so a mesh gives the same bits
 // in any batch), no partial-sum buffer and no second kernel.
+// STAGED: V is the LBS kernel's compacted (B, nu, 3) corner buffer; a CTA
+// walks `mpc` consecutive meshes, each mesh's nu x 12 bytes bulk-copied
+// into one of two shared-memory buffers (the next mesh lands while this one
+// is bridged), and keeps its targets' corners and weights in registers
+// across them.  The bridged targets are collected in shared memory (xs) and
+// leave after the centroid removal as whole rows: fp32 with coalesced
+// stores, the bf16 A-tile image as one 16-byte K-major chunk (8 consecutive
+// k of the mesh's row) per store.
 constexpr int kProjVcThreads = 512, kProjVcPer = 4;  // targets per thread (n_sub <= 2048)
 
+template <bool STAGED>
 __global__ void __launch_bounds__(kProjVcThreads) k_proj_inputs_vc(const float* __restrict__ V, int nv,
-                                                                   ProjectorDev p, float* __restrict__ x32,
-                                                                   __nv_bfloat16* __restrict__ xb) {
+                                                                   ProjectorDev p, const int32_t* __restrict__ corners,
+                                                                   float* __restrict__ x32,
+                                                                   __nv_bfloat16* __restrict__ xb, int B, int mpc) {
   __shared__ float red[kProjVcThreads / 32][3];
   __shared__ float cen[3];
-  const int b = blockIdx.x, tid = threadIdx.x;
-  pdl_wait();
-  const float* Vb = V + (int64_t)b * nv * 3;
-  const float o0 = __ldg(Vb), o1 = __ldg(Vb + 1), o2 = __ldg(Vb + 2);
-  float acc[kProjVcPer][3];
-  float part[3] = {0.0f, 0.0f, 0.0f};
+  __shared__ __align__(8) uint64_t bar[2];
+  extern __shared__ __align__(16) float vsm[];
+  const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+  const int K = 3 * p.n_sub, KT = (K + 127) / 128;
+  float* xs = vsm + (STAGED ? 2 * nv * 3 : 0);  // (K) bridged targets, vertex-0 centred
+  const int b0 = blockIdx.x * mpc, nb = min(mpc, B - b0);
+  int cr[kProjVcPer][3];
+  float wc[kProjVcPer][3];
 #pragma unroll
   for (int q = 0; q < kProjVcPer; ++q) {
     const int t = tid + q * kProjVcThreads;
-    acc[q][0] = acc[q][1] = acc[q][2] = 0.0f;
-    if (t < p.n_sub) {
 #pragma unroll
-      for (int c = 0; c < 3; ++c) {
-        const float* vc = Vb + 3 * (int64_t)p.corners[3 * t + c];
-        const float wc = p.bw[3 * t + c];
-        acc[q][0] = fmaf(wc, __ldg(vc) - o0, acc[q][0]);
-        acc[q][1] = fmaf(wc, __ldg(vc + 1) - o1, acc[q][1]);
-        acc[q][2] = fmaf(wc, __ldg(vc + 2) - o2, acc[q][2]);
-      }
-#pragma unroll
-      for (int a = 0; a < 3; ++a) part[a] += acc[q][a];
+    for (int c = 0; c < 3; ++c) {
+      cr[q][c] = t < p.n_sub ? __ldg(corners + 3 * t + c) : 0;
+      wc[q][c] = t < p.n_sub ? __ldg(p.bw + 3 * t + c) : 0.0f;
     }
   }
-  const int warp = tid / 32, lane = tid % 32;
-#pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    const float r = warp_sum(part[a]);
-    if (lane == 0) red[warp][a] = r;
+  const uint32_t vbytes = (uint32_t)nv * 12;
+  if (STAGED && tid == 0) {
+    tc::mbar_init(&bar[0], 1);
+    tc::mbar_init(&bar[1], 1);
+    tc::mbar_fence_init();
   }
-  __syncthreads();
-  if (tid < 3) {
-    float sum = 0.0f;
-    for (int w = 0; w < kProjVcThreads / 32; ++w) sum += red[w][tid];
-    cen[tid] = sum / (float)p.n_sub;
+  if (STAGED) __syncthreads();
+  pdl_wait();
+  auto fetch = [&](int i) {  // mesh b0 + i into buffer i & 1 (thread 0)
+    tc::mbar_expect_tx(&bar[i & 1], vbytes);
+    tc::bulk_g2s(vsm + (i & 1) * nv * 3, V + (int64_t)(b0 + i) * nv * 3, vbytes, &bar[i & 1]);
+  };
+  if (STAGED && tid == 0) {
+    fetch(0);
+    if (nb > 1) fetch(1);
   }
-  __syncthreads();
-  const int K = 3 * p.n_sub, KT = (K + 127) / 128;
+  for (int i = 0; i < nb; ++i) {
+    const int b = b0 + i;
+    const float* Vb;
+    if (STAGED) {
+      tc::mbar_wait(&bar[i & 1], (uint32_t)((i >> 1) & 1));
+      Vb = vsm + (i & 1) * nv * 3;
+    } else {
+      Vb = V + (int64_t)b * nv * 3;
+    }
+    const float o0 = Vb[0], o1 = Vb[1], o2 = Vb[2];
+    float part[3] = {0.0f, 0.0f, 0.0f};
 #pragma unroll
-  for (int q = 0; q < kProjVcPer; ++q) {
-    const int t = tid + q * kProjVcThreads;
-    if (t >= p.n_sub) break;
+    for (int q = 0; q < kProjVcPer; ++q) {
+      const int t = tid + q * kProjVcThreads;
+      if (t < p.n_sub) {
+        float acc[3] = {0.0f, 0.0f, 0.0f};
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const float* vc = Vb + 3 * cr[q][c];
+          acc[0] = fmaf(wc[q][c], vc[0] - o0, acc[0]);
+          acc[1] = fmaf(wc[q][c], vc[1] - o1, acc[1]);
+          acc[2] = fmaf(wc[q][c], vc[2] - o2, acc[2]);
+        }
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          part[a] += acc[a];
+          xs[3 * t + a] = acc[a];
+        }
+      }
+    }
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-      const float v = acc[q][a] - cen[a];
-      const int k = 3 * t + a;
-      if (x32 != nullptr) x32[(int64_t)b * K + k] = v;
-      if (xb != nullptr) {
-        const size_t tile = (size_t)(b >> 7) * KT + (k >> 7);
-        xb[tile * 16384 + tc::kmajor_off(b & 127, k & 127, 128) / 2] = __float2bfloat16_rn(v);
+      const float r = warp_sum(part[a]);
+      if (lane == 0) red[warp][a] = r;
+    }
+    __syncthreads();  // xs, red complete; buffer i & 1 no longer read
+    if (STAGED && tid == 0 && i + 2 < nb) {
+      tc::fence_async_smem();
+      fetch(i + 2);
+    }
+    if (tid < 3) {
+      float sum = 0.0f;
+      for (int w = 0; w < kProjVcThreads / 32; ++w) sum += red[w][tid];
+      cen[tid] = sum / (float)p.n_sub;
+    }
+    __syncthreads();
+    const float c0 = cen[0], c1 = cen[1], c2 = cen[2];
+    auto val = [&](int k) { return k < K ? xs[k] - (k % 3 == 0 ? c0 : (k % 3 == 1 ? c1 : c2)) : 0.0f; };
+    if (x32 != nullptr)
+      for (int k = tid; k < K; k += kProjVcThreads) x32[(int64_t)b * K + k] = val(k);
+    if (xb != nullptr) {
+      uint8_t* img = reinterpret_cast<uint8_t*>(xb) + (size_t)(b >> 7) * KT * 32768;
+      for (int ch = tid; ch < (K + 7) / 8; ch += kProjVcThreads) {
+        const int k0 = 8 * ch;
+        float v8[8];
+        *reinterpret_cast<float4*>(v8) = *reinterpret_cast<const float4*>(xs + k0);  // (xs: K + 8 floats)
+        *reinterpret_cast<float4*>(v8 + 4) = *reinterpret_cast<const float4*>(xs + k0 + 4);
+        uint32_t w[4];
+        int r = k0 % 3;  // coordinate of k0
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          v8[j] = k0 + j < K ? v8[j] - (r == 0 ? c0 : (r == 1 ? c1 : c2)) : 0.0f;
+          r = r == 2 ? 0 : r + 1;
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const __nv_bfloat162 h = __floats2bfloat162_rn(v8[2 * j], v8[2 * j + 1]);
+          w[j] = *reinterpret_cast<const uint32_t*>(&h);
+        }
+        *reinterpret_cast<uint4*>(img + (size_t)(k0 >> 7) * 32768 + tc::kmajor_off(b & 127, k0 & 127, 128)) =
+            make_uint4(w[0], w[1], w[2], w[3]);
       }
     }
+    __syncthreads();  // xs, red and cen are rewritten by the next mesh
   }
 }
 
@@ -897,7 +1011,7 @@ cudaError_t launch_fk(const float* poses, int ld_pose, int B, const float* grest
 // grid: (vertex tiles, chunk CTAs); each chunk CTA walks chunks y, y + G, ...
 // with G chosen so the grid fills ~2 CTAs per SM
 cudaError_t launch_lbs_tc(const TemplateDev& t, const uint8_t* lbs_in, int B, float* verts, int* nonfinite,
-                          cudaStream_t st) {
+                          cudaStream_t st, CornerOut cu) {
   if (B == 0) return cudaSuccess;
   if (t.basis_img == nullptr) return cudaErrorInvalidValue;
   const int tiles = (t.nv + FSB_LBS_TILE - 1) / FSB_LBS_TILE;
@@ -906,9 +1020,9 @@ cudaError_t launch_lbs_tc(const TemplateDev& t, const uint8_t* lbs_in, int B, fl
   G = G < 1 ? 1 : (G > nchunks ? nchunks : G);
   dim3 grid(tiles, G);
   switch (t.nnz) {
-    case 2: return launch_pdl(k_lbs_tc<2>, grid, dim3(kLtThreads), kLtSmem, st, t, lbs_in, B, verts, nonfinite);
-    case 4: return launch_pdl(k_lbs_tc<4>, grid, dim3(kLtThreads), kLtSmem, st, t, lbs_in, B, verts, nonfinite);
-    case 8: return launch_pdl(k_lbs_tc<8>, grid, dim3(kLtThreads), kLtSmem, st, t, lbs_in, B, verts, nonfinite);
+    case 2: return launch_pdl(k_lbs_tc<2>, grid, dim3(kLtThreads), kLtSmem, st, t, lbs_in, B, verts, nonfinite, cu);
+    case 4: return launch_pdl(k_lbs_tc<4>, grid, dim3(kLtThreads), kLtSmem, st, t, lbs_in, B, verts, nonfinite, cu);
+    case 8: return launch_pdl(k_lbs_tc<8>, grid, dim3(kLtThreads), kLtSmem, st, t, lbs_in, B, verts, nonfinite, cu);
     default: return cudaErrorInvalidValue;
   }
 }
@@ -977,11 +1091,28 @@ cudaError_t launch_proj_inputs(const TemplateDev& t, const ProjectorDev& p, cons
 }
 
 cudaError_t launch_proj_inputs_v(const float* V, int nv, const ProjectorDev& p, int B, float* sub, bool f32,
-                                 __nv_bfloat16* xb, float* psum, cudaStream_t st) {
+                                 __nv_bfloat16* xb, float* psum, cudaStream_t st, bool compacted) {
   if (B == 0) return cudaSuccess;
   if (p.n_sub > kProjVcThreads * kProjVcPer) return cudaErrorInvalidValue;
   (void)psum;
-  return launch_pdl(k_proj_inputs_vc, dim3(B), dim3(kProjVcThreads), 0, st, V, nv, p, f32 ? sub : nullptr, xb);
+  // compacted: V is the LBS kernel's (B, nu, 3) corner buffer, indexed by slot
+  static bool attr = false;
+  if (!attr) {
+    for (auto* k : {k_proj_inputs_vc<false>, k_proj_inputs_vc<true>}) {
+      cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+      if (e != cudaSuccess) return e;
+    }
+    attr = true;
+  }
+  const size_t xs_bytes = (size_t)p.n_sub * 12 + 32;
+  if (!compacted)
+    return launch_pdl(k_proj_inputs_vc<false>, dim3(B), dim3(kProjVcThreads), xs_bytes, st, V, nv, p, p.corners,
+                      f32 ? sub : nullptr, xb, B, 1);
+  // meshes per CTA: 1 while that leaves SMs idle (latency of small batches),
+  // up to 4 for large batches (register-held corners reused, loads overlapped)
+  const int mpc = B >= 4 * 148 * 2 ? 4 : (B >= 2 * 148 * 2 ? 2 : 1);
+  return launch_pdl(k_proj_inputs_vc<true>, dim3((B + mpc - 1) / mpc), dim3(kProjVcThreads),
+                    (size_t)nv * 24 + xs_bytes, st, V, nv, p, p.ucorners, f32 ? sub : nullptr, xb, B, mpc);
 }
 
 // number of K chunks of a layer: a function of K only (batch independence);
