@@ -212,6 +212,15 @@ int fsb_denoise(fsb_ctx* ctx, const float* poses, int B, const float* w1, const 
  * float inv_two_sigma2; float pad; double gdir[2]} -> (B, H, W, 3) f32 */
 int fsb_render(fsb_ctx* ctx, const void* scenes, int B, int H, int W, float* out, void* stream);
 
+/* ---- host staging ------------------------------------------------------- */
+/* The single-frame path's input check and staging (numkit.bilinear_sample's
+ * check_finite, numkit.py:136-140, + the copy of the caller's host image
+ * into the pinned frame K1 reads over PCIe) in one pass on a small
+ * persistent pool of host threads: dst[i] = src[i] for i < n (HOST
+ * pointers), *nonfinite = 1 if any value is NaN / inf (else 0).  Returns
+ * FSB_OK; no context, no device work. */
+int fsb_stage_frame(const float* src, float* dst, int64_t n, int* nonfinite);
+
 /* ---- diagnostics -------------------------------------------------------- */
 /* reads (and optionally clears) this context's non-finite flag; waits only
  * for the work this context enqueued (an event per stream it used), never

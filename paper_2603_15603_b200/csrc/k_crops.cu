@@ -489,3 +489,58 @@ cudaError_t launch_crop_grid(const double* boxes, int n, int S, float* out, cuda
   k_crop_grid<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>(boxes, n, S, out);
   return cudaGetLastError();
 }
+
+// ---------------------------------------------------------------------------
+// Host-read peak (bench.py's e2e roofline denominator): stream `bytes` from
+// pinned, mapped host memory to HBM the way K1 reads host frames -- each CTA
+// pulls 16 KB chunks with cp.async.bulk into a two-slot shared-memory ring
+// and writes them out with 16-byte stores.  Test hook, not in the header.
+// ---------------------------------------------------------------------------
+constexpr uint32_t kHrChunk = 16384;
+
+__global__ void __launch_bounds__(256) k_host_read(const uint8_t* __restrict__ src, size_t nchunks,
+                                                   uint8_t* __restrict__ dst) {
+  extern __shared__ __align__(128) uint8_t hr_smem[];
+  __shared__ __align__(8) uint64_t bar[2];
+  if (threadIdx.x == 0) {
+    tc::mbar_init(&bar[0], 1);
+    tc::mbar_init(&bar[1], 1);
+    tc::mbar_fence_init();
+  }
+  __syncthreads();
+  auto fetch = [&](size_t c, int s) {
+    tc::mbar_expect_tx(&bar[s], kHrChunk);
+    tc::bulk_g2s(hr_smem + s * kHrChunk, src + c * kHrChunk, kHrChunk, &bar[s]);
+  };
+  size_t c = blockIdx.x;
+  if (threadIdx.x == 0) {
+    if (c < nchunks) fetch(c, 0);
+    if (c + gridDim.x < nchunks) fetch(c + gridDim.x, 1);
+  }
+  for (int it = 0; c < nchunks; c += gridDim.x, ++it) {
+    const int s = it & 1;
+    tc::mbar_wait(&bar[s], (uint32_t)((it >> 1) & 1));
+    const uint4* in = reinterpret_cast<const uint4*>(hr_smem + s * kHrChunk);
+    uint4* out = reinterpret_cast<uint4*>(dst + c * kHrChunk);
+    for (int i = threadIdx.x; i < (int)(kHrChunk / 16); i += blockDim.x) out[i] = in[i];
+    __syncthreads();
+    if (threadIdx.x == 0 && c + 2 * gridDim.x < nchunks) {
+      tc::fence_async_smem();
+      fetch(c + 2 * gridDim.x, s);
+    }
+  }
+}
+
+extern "C" int fsb_debug_host_read(const void* host_src, size_t bytes, void* dst, int ctas, void* stream) {
+  if (bytes % kHrChunk) return 1;
+  static bool attr = false;
+  if (!attr && cudaFuncSetAttribute(k_host_read, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * kHrChunk) !=
+                   cudaSuccess)
+    return 2;
+  attr = true;
+  k_host_read<<<ctas, 256, 2 * kHrChunk, (cudaStream_t)stream>>>(static_cast<const uint8_t*>(host_src),
+                                                                  bytes / kHrChunk, static_cast<uint8_t*>(dst));
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) fprintf(stderr, "fsb_debug_host_read: %s\n", cudaGetErrorString(e));
+  return e == cudaSuccess ? 0 : 3;
+}

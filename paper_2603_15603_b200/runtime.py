@@ -79,6 +79,7 @@ _SIGS = {
     "fsb_nonfinite": (_i, [_p, ctypes.POINTER(_i), _i]),
     "fsb_counters": (_i, [_p, ctypes.POINTER(CountersC)]),
     "fsb_input_bytes": (_i, [_p, ctypes.POINTER(ctypes.c_int64), _i]),
+    "fsb_stage_frame": (_i, [_p, _p, ctypes.c_int64, ctypes.POINTER(_i)]),
     "fsb_denoise": (_i, [_p, _p, _i, _p, _p, _p, _p, _i, _p, _p]),
     "fsb_load_denoiser": (_i, [_p, _p, _p, _p, _p, _i]),
     "fsb_bary_map": (_i, [_p, _p, _i, _p, _i, _p, _i, _p, _p, _p, _p]),

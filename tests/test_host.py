@@ -41,6 +41,30 @@ def test_runtime_binds_every_header_symbol():
     assert set(_header_functions()) == set(runtime.exported_symbols())
 
 
+@pytest.mark.parametrize("n", [0, 7, 1 << 16, 512 * 512 * 3, 1000003])
+def test_stage_frame_copies_and_flags_non_finite(lib, n):
+    """fsb_stage_frame (host-only): the single-frame path's check_finite +
+    pinned staging copy in one pass over a thread pool
+    (numkit.py:136-140 semantics: any NaN / inf raises)."""
+    fn = lib.fsb_stage_frame
+    fn.argtypes = [ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int64, ctypes.POINTER(ctypes.c_int)]
+    rng = np.random.default_rng(n)
+    src = rng.standard_normal(n).astype(np.float32)
+    dst = np.full(n, 7.0, np.float32)
+    bad = ctypes.c_int(-1)
+    assert fn(src.ctypes.data, dst.ctypes.data, n, ctypes.byref(bad)) == 0
+    assert bad.value == 0 and np.array_equal(src, dst)
+    for v in (np.nan, np.inf, -np.inf):
+        for pos in {0, n // 2, n - 1} if n else set():
+            s2 = src.copy()
+            s2[pos] = v
+            assert fn(s2.ctypes.data, dst.ctypes.data, n, ctypes.byref(bad)) == 0
+            assert bad.value == 1
+            assert np.array_equal(s2, dst, equal_nan=True)
+    big = np.full(n, np.finfo(np.float32).max, np.float32)  # large but finite
+    assert fn(big.ctypes.data, dst.ctypes.data, n, ctypes.byref(bad)) == 0 and bad.value == 0
+
+
 def test_build_info_without_gpu(lib):
     lib.fsb_build_info.restype = ctypes.c_char_p
     assert b"sm_100a" in lib.fsb_build_info()

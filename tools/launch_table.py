@@ -14,7 +14,10 @@ gi = h.index("Grid Size") if "Grid Size" in h else None
 t = collections.OrderedDict()
 for r in rows[hdr + 1:]:
     e = t.setdefault(r[ii], {"k": r[ki].split("(")[0][:40], "grid": r[gi] if gi is not None else ""})
-    e[r[mi]] = float(r[vi].replace(",", ""))
+    try:
+        e[r[mi]] = float(r[vi].replace(",", ""))
+    except ValueError:
+        pass
 n = int(sys.argv[2]) if len(sys.argv) > 2 else 40
 for k, v in list(t.items())[-n:]:
     print("%4s %-40s %-14s %9.1f us  rd %8.1f MB  wr %8.1f MB" % (
