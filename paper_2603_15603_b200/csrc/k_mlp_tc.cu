@@ -14,6 +14,8 @@
 // partial; k_tile_reduce adds the partials of all groups in order and applies
 // bias / ReLU / mask.  The K partition depends on K only, so a mesh gives the
 // same bits in a batch of 4096 as alone.
+#include <utility>
+
 #include "fsb_common.cuh"
 #include "fsb_weights.h"
 #include "tc_sm100.cuh"
@@ -119,19 +121,208 @@ __global__ void k_tile_reduce(const float* __restrict__ P, int S, int M, int N, 
   }
 }
 
-cudaError_t init_attrs_mlp_tc() {
-  return cudaFuncSetAttribute(k_tile_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(4 * kTileBytes));
+// ---------------------------------------------------------------------------
+// Large batches (C3: 4096 meshes, 1152 output-tile x K-group items for W1):
+// the same items and the same MMA sequence per item as k_tile_gemm (so the
+// partials, and every mesh's bits, do not depend on the batch), computed by
+// a persistent warp-specialised CTA per SM: warp 4 streams the A / B tiles
+// of consecutive items through a 3-deep bulk-copy ring, warp 5 issues the
+// MMAs into one of two TMEM accumulators, warps 0-3 drain the other one --
+// loads, MMAs and the partial-sum stores of neighbouring items overlap
+// instead of running back to back in one-item CTAs.
+// ---------------------------------------------------------------------------
+constexpr int kPStages = 3;
+
+__global__ void __launch_bounds__(192, 1) k_tile_gemm_p(const uint8_t* __restrict__ Aimg, int KT,
+                                                        const uint8_t* __restrict__ Bimg, int G, int M, int N,
+                                                        int S, int NT, int MT, float* __restrict__ partial) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bar_load[kPStages], bar_free[kPStages], bar_full[2], bar_tfree[2];
+  __shared__ uint32_t tmem_base;
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int items = MT * S * NT;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kPStages; ++i) {
+      tc::mbar_init(&bar_load[i], 1);
+      tc::mbar_init(&bar_free[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&bar_full[i], 1);
+      tc::mbar_init(&bar_tfree[i], 4);
+    }
+    tc::mbar_fence_init();
+  }
+  if (warp == 0) tc::tmem_alloc(&tmem_base, 256);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = tmem_base;
+  const uint32_t sbase = tc::smem_u32(smem);
+  pdl_wait();  // the A image comes from the previous kernel
+  // item i: n-tile fastest, then K group, then m-tile
+  auto decode = [&](int i, int& mt, int& split, int& nt) {
+    nt = i % NT;
+    split = (i / NT) % S;
+    mt = i / (NT * S);
+  };
+  if (warp == 4) {
+    if (lane == 0) {  // producer
+      int q = 0;
+      for (int i = blockIdx.x; i < items; i += gridDim.x) {
+        int mt, split, nt;
+        decode(i, mt, split, nt);
+        const int kt0 = split * G, nk = min(G, KT - kt0);
+        for (int k = 0; k < nk; ++k, ++q) {
+          const int s = q % kPStages, u = q / kPStages;
+          if (u > 0) tc::mbar_wait(&bar_free[s], (uint32_t)((u - 1) & 1));
+          tc::mbar_expect_tx(&bar_load[s], 2 * kTileBytes);
+          tc::bulk_g2s(smem + s * 2 * kTileBytes, Aimg + ((size_t)mt * KT + kt0 + k) * kTileBytes, kTileBytes,
+                       &bar_load[s]);
+          tc::bulk_g2s(smem + s * 2 * kTileBytes + kTileBytes, Bimg + ((size_t)nt * KT + kt0 + k) * kTileBytes,
+                       kTileBytes, &bar_load[s]);
+        }
+      }
+    }
+  } else if (warp == 5) {
+    if (lane == 0) {  // MMA issue
+      const uint32_t idesc = tc::idesc_bf16(128, 128);
+      int q = 0, t = 0;
+      for (int i = blockIdx.x; i < items; i += gridDim.x, ++t) {
+        int mt, split, nt;
+        decode(i, mt, split, nt);
+        const int kt0 = split * G, nk = min(G, KT - kt0);
+        const int b = t & 1, ut = t >> 1;
+        if (ut > 0) tc::mbar_wait(&bar_tfree[b], (uint32_t)((ut - 1) & 1));
+        tc::fence_after();
+        const uint32_t d = tmem + b * 128;
+        for (int k = 0; k < nk; ++k, ++q) {
+          const int s = q % kPStages, u = q / kPStages;
+          tc::mbar_wait(&bar_load[s], (uint32_t)(u & 1));
+          tc::fence_after();
+          const uint32_t a = sbase + s * 2 * kTileBytes, bb = a + kTileBytes;
+          for (int kk = 0; kk < 128; kk += 16)
+            tc::mma_bf16(d, tc::kmajor_desc(a, 128, kk), tc::kmajor_desc(bb, 128, kk), idesc, (k | kk) != 0);
+          tc::mma_commit(&bar_free[s]);  // slot s free once these MMAs have read it
+        }
+        tc::mma_commit(&bar_full[b]);
+      }
+    }
+  } else {  // warps 0-3: epilogue, TMEM lane quadrant = warp
+    int t = 0;
+    for (int i = blockIdx.x; i < items; i += gridDim.x, ++t) {
+      int mt, split, nt;
+      decode(i, mt, split, nt);
+      const int b = t & 1, ut = t >> 1;
+      tc::mbar_wait(&bar_full[b], (uint32_t)(ut & 1));
+      tc::fence_after();
+      const int row = mt * 128 + warp * 32 + lane;
+      const uint32_t taddr = tmem + b * 128 + ((uint32_t)(warp * 32) << 16);
+      float* dst = partial + ((size_t)split * M + row) * N + nt * 128;
+#pragma unroll 1
+      for (int c = 0; c < 128; c += 64) {
+        float v[64];
+        tc::tmem_ld64(taddr + c, v);
+        if (row < M)
+#pragma unroll
+          for (int j = 0; j < 64; j += 4) {
+            if (nt * 128 + c + j < N)
+              *reinterpret_cast<float4*>(dst + c + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+          }
+      }
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&bar_tfree[b]);
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc(tmem, 256);
 }
+
+// k_tile_reduce with one 16-byte K-major chunk (8 consecutive n of a row)
+// per thread: the same partial-sum order, bias / ReLU / mask, fp32 and bf16
+// image stores as whole vectors (N % 4 == 0)
+__global__ void k_tile_reduce8(const float* __restrict__ P, int S, int M, int N, const float* __restrict__ bias,
+                               const float* __restrict__ mask, int relu, float* __restrict__ out, int ldo,
+                               uint8_t* __restrict__ out_img, int KT_out, int* nonfinite) {
+  const int N8 = (N + 7) / 8;
+  const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  pdl_wait();
+  if (idx >= (int64_t)M * N8) return;
+  const int m = (int)(idx / N8), n0 = (int)(idx % N8) * 8;
+  const bool hi = n0 + 4 < N;
+  float v[8];
+  auto ld = [&](int s) {
+    const float* p = P + ((int64_t)s * M + m) * N + n0;
+    const float4 a = *reinterpret_cast<const float4*>(p);
+    const float4 b = hi ? *reinterpret_cast<const float4*>(p + 4) : make_float4(0.f, 0.f, 0.f, 0.f);
+    return std::make_pair(a, b);
+  };
+  {
+    const auto ab = ld(0);
+    v[0] = ab.first.x; v[1] = ab.first.y; v[2] = ab.first.z; v[3] = ab.first.w;
+    v[4] = ab.second.x; v[5] = ab.second.y; v[6] = ab.second.z; v[7] = ab.second.w;
+  }
+  for (int s = 1; s < S; ++s) {
+    const auto ab = ld(s);
+    v[0] += ab.first.x; v[1] += ab.first.y; v[2] += ab.first.z; v[3] += ab.first.w;
+    v[4] += ab.second.x; v[5] += ab.second.y; v[6] += ab.second.z; v[7] += ab.second.w;
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const int n = n0 + j;
+    if (n < N) {
+      v[j] += bias[n];
+      if (relu) v[j] = fmaxf(v[j], 0.0f);
+      if (mask != nullptr) v[j] *= mask[n];
+      flag_nonfinite(nonfinite, v[j]);
+    } else {
+      v[j] = 0.0f;
+    }
+  }
+  if (out != nullptr) {
+    *reinterpret_cast<float4*>(out + (int64_t)m * ldo + n0) = make_float4(v[0], v[1], v[2], v[3]);
+    if (hi) *reinterpret_cast<float4*>(out + (int64_t)m * ldo + n0 + 4) = make_float4(v[4], v[5], v[6], v[7]);
+  }
+  if (out_img != nullptr) {
+    const size_t tile = (size_t)(m >> 7) * KT_out + (n0 >> 7);
+    *reinterpret_cast<uint4*>(out_img + tile * kTileBytes + tc::kmajor_off(m & 127, n0 & 127, 128)) =
+        make_uint4(tc::pack_bf16(v[0], v[1]), tc::pack_bf16(v[2], v[3]), tc::pack_bf16(v[4], v[5]),
+                   tc::pack_bf16(v[6], v[7]));
+  }
+}
+
+cudaError_t init_attrs_mlp_tc() {
+  cudaError_t e = cudaFuncSetAttribute(k_tile_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(4 * kTileBytes));
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(k_tile_gemm_p, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)(2 * kPStages * kTileBytes));
+}
+
+#ifndef FSB_TILE_PERSIST_M
+#define FSB_TILE_PERSIST_M 1024  // batches from this size on: the persistent kernel
+#endif
 
 // one layer: C (M x N) = A_img (M x 128*KT) * B_img^T, K grouped in G k-tiles
 cudaError_t launch_tile_layer(const uint8_t* Aimg, const uint8_t* Bimg, int KT, int G, int M, int N,
                               float* partial, const float* bias, const float* mask, int relu, float* out, int ldo,
                               uint8_t* out_img, int KT_out, int* nonfinite, cudaStream_t st) {
   if (M == 0) return cudaSuccess;
-  const int S = (KT + G - 1) / G;
-  dim3 grid((N + 127) / 128, S, (M + 127) / 128);
-  cudaError_t e = launch_pdl(k_tile_gemm, grid, dim3(128), 4 * kTileBytes, st, Aimg, KT, Bimg, G, M, N, partial);
+  const int S = (KT + G - 1) / G, NT = (N + 127) / 128, MT = (M + 127) / 128;
+  cudaError_t e;
+  if (M >= FSB_TILE_PERSIST_M) {
+    const int items = MT * S * NT;
+    e = launch_pdl(k_tile_gemm_p, dim3(items < 148 ? items : 148), dim3(192), 2 * kPStages * kTileBytes, st, Aimg, KT,
+                   Bimg, G, M, N, S, NT, MT, partial);
+  } else {
+    e = launch_pdl(k_tile_gemm, dim3(NT, S, MT), dim3(128), 4 * kTileBytes, st, Aimg, KT, Bimg, G, M, N, partial);
+  }
   if (e != cudaSuccess) return e;
+  if (N % 4 == 0 && (out == nullptr || ldo % 4 == 0)) {
+    const int64_t tot = (int64_t)M * ((N + 7) / 8);
+    return launch_pdl(k_tile_reduce8, dim3((unsigned)((tot + 255) / 256)), dim3(256), 0, st, partial, S, M, N, bias,
+                      mask, relu, out, ldo, out_img, KT_out, nonfinite);
+  }
   const int64_t tot = (int64_t)M * N;
   return launch_pdl(k_tile_reduce, dim3((unsigned)((tot + 255) / 256)), dim3(256), 0, st, partial, S, M, N, bias, mask,
                     relu, out, ldo, out_img, KT_out, nonfinite);

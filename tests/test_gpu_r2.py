@@ -298,6 +298,40 @@ def test_c3_64_meshes(torch, g2, full_models, full_projector, precision):
             assert mpjpe_mm(got_j[m], g2["c3x.j_smpl"][m]) <= MPJPE_MM, m
 
 
+def test_c3_batch_independent_bits(torch, full_models, full_projector):
+    """The projector's large-batch kernels (persistent tile GEMM from 1024
+    meshes, compacted-corner bridge with 4 meshes per CTA) give every mesh
+    the same bits as the small-batch kernels: 1536 meshes in one call vs
+    the same meshes in calls of 32 (bf16 and fp32)."""
+    from paper_2603_15603_b200 import decoder as dc
+    from paper_2603_15603_b200 import runtime as rt
+
+    mhr, smpl, gt = full_models
+    n = 1536
+    rng = np.random.default_rng(11)
+    p = np.zeros((n, 76), np.float32)
+    p[:, :66] = rng.normal(0.0, 0.2, size=(n, 66))
+    p[:, 66:] = rng.normal(0.0, 0.45, size=(n, 10))
+    for precision in ("bf16", "fp32"):
+        pipe = _pipeline(dc.Decoder(smpl, dc.DecoderConfig(), seed=40), mhr, gt, full_projector, precision)
+        ctx = pipe.context()
+        ctx.reserve(n)
+        poses = torch.from_numpy(p).cuda()
+        outs = []
+        for step in (n, 32):
+            v = torch.empty((n, mhr.num_vertices, 3), dtype=torch.float32, device="cuda")
+            th = torch.empty((n, 76), dtype=torch.float32, device="cuda")
+            j = torch.empty((n, 22, 3), dtype=torch.float32, device="cuda")
+            for b0 in range(0, n, step):
+                ctx.check(ctx.lib.fsb_skin_project(ctx.h, rt.ptr(poses[b0:]), step, rt.ptr(v[b0:]), rt.ptr(th[b0:]),
+                                                   rt.ptr(j[b0:]), None, rt.PRECISIONS[precision], ctx.stream))
+            torch.cuda.synchronize()
+            ctx.check_finite("c3 batch")
+            outs.append((th.cpu(), j.cpu(), v[::97].cpu()))
+        for a, b in zip(*outs):
+            assert torch.equal(a, b), precision
+
+
 # ---------------------------------------------------------------------------
 # ViT-L-sized encoder, all 24 layers
 
