@@ -9,6 +9,7 @@ generators re-exported from ``synth.py``.
 
 from __future__ import annotations
 
+import json
 from dataclasses import dataclass
 
 import numpy as np
@@ -160,3 +161,46 @@ def crop_grid(box, out_size):
     ctx.check(ctx.lib.fsb_crop_grid(ctx.h, runtime.ptr(bb), 1, int(out_size), runtime.ptr(out), ctx.stream),
               "crop_grid")
     return out.cpu().numpy()[0]
+
+
+# ---------------------------------------------------------------------------
+# scene files (priors.py:130-159): the same JSON payload, so scene files move
+# between the reference and this package unchanged
+
+
+def save_scene(scene, path):
+    payload = {
+        "image_size": [int(scene.image_size[0]), int(scene.image_size[1])],
+        "camera": {"fx": scene.camera.fx, "fy": scene.camera.fy, "cx": scene.camera.cx, "cy": scene.camera.cy},
+        "pose": [float(v) for v in scene.pose],
+        "translation": [float(v) for v in scene.translation],
+        "seed": int(scene.seed),
+    }
+    with open(path, "w") as fh:
+        json.dump(payload, fh)
+
+
+def scene_from_dict(payload, template):
+    """Rebuild one scene from a save_scene payload (a plain JSON object)."""
+    try:
+        cam = CameraIntrinsics(**payload["camera"])
+        pose = np.asarray(payload["pose"], dtype=DTYPE)
+        translation = np.asarray(payload["translation"], dtype=DTYPE)
+        image_size = tuple(payload["image_size"])
+        seed = payload["seed"]
+    except (TypeError, KeyError) as exc:
+        raise UsageError("malformed scene payload: %s" % (exc,))
+    return make_scene(template, pose, translation, cam, image_size, seed)
+
+
+def load_scene(path, template):
+    with open(path) as fh:
+        payload = json.load(fh)
+    return scene_from_dict(payload, template)
+
+
+def detect_dense(image):
+    """The serial baseline's sliding-window detector (priors.py:272-300) is
+    not part of the accelerated path: raises UsageError."""
+    raise UsageError("detect_dense belongs to the serial baseline, which this package does not accelerate; "
+                     "use detect_stub (the fast path's keypoint prior)")

@@ -15,7 +15,7 @@ import numpy as np
 
 from . import runtime
 from .numkit import DTYPE, ShapeError, UsageError
-from .synth import PARAM_DIM, BaryMap, projector_arrays  # noqa: F401
+from .synth import PARAM_DIM, BaryMap, BodyTemplate, projector_arrays  # noqa: F401
 
 
 @dataclass
@@ -335,9 +335,16 @@ def _fit(v_src, bmap, target, cfg, init, want_grad):
     v = np.asarray(v_src, DTYPE) if not isinstance(v_src, torch.Tensor) else v_src
     if v.ndim != 3 or v.shape[-1] != 3:
         raise ShapeError("fit_batch expects (B, Nv, 3) meshes, got %r" % (tuple(v.shape),))
-    b = int(v.shape[0])
-    v_t = bridge(v, bmap)
-    v_t = v_t if isinstance(v_t, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(v_t))
+    return _fit_targets(bridge(v, bmap), target, cfg, init, want_grad)
+
+
+def _fit_targets(v_t, target, cfg, init, want_grad):
+    """fsb_fit_batch on bridged targets (B, Nv_target, 3)."""
+    torch = runtime._torch()
+    v_t = v_t if isinstance(v_t, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(v_t, DTYPE))
+    if v_t.ndim != 3 or v_t.shape[-1] != 3:
+        raise ShapeError("fit targets must be (B, Nv, 3), got %r" % (tuple(v_t.shape),))
+    b = int(v_t.shape[0])
     v_t = v_t.to(device=torch.device("cuda", torch.cuda.current_device()), dtype=torch.float32).contiguous()
     if not bool(torch.isfinite(v_t).all()):
         from .numkit import NumericError
@@ -376,14 +383,72 @@ def fit_batch(v_src, bmap, target, cfg=None, init=None):
                           curve=curve.mean(dim=0).cpu().numpy())
 
 
-def fit_objective_grad(theta, v_src, bmap, target, cfg=None):
-    """Gradient of the fit objective at theta (B, 76) for the bridged
-    targets of v_src (the reference's fit_objective_grad, :303-309, takes the
-    bridged targets directly)."""
-    cfg = cfg or FitConfig()
+def fit_objective_grad(theta, *args, **kwargs):
+    """Analytic gradient of the fit objective w.r.t. theta (B, 76)
+    (projection.py:304-310), on the GPU (k_fit).
+
+    Reference form: fit_objective_grad(theta, template, v_target, cfg=None),
+    v_target the bridged targets (B, Nv_template, 3).  Also accepted:
+    fit_objective_grad(theta, v_src, bmap, template, cfg=None), which bridges
+    the source meshes first."""
+    if args and isinstance(args[0], BodyTemplate):
+        template, v_target = args[0], args[1]
+        cfg = (args[2] if len(args) > 2 else kwargs.get("cfg")) or FitConfig()
+        one = FitConfig(steps=1, lr=cfg.lr, lambda_pose=cfg.lambda_pose, lambda_shape=cfg.lambda_shape)
+        _, _, _, grad = _fit_targets(v_target, template, one, theta, True)
+        return grad.cpu().numpy()
+    v_src, bmap, target = args[0], args[1], args[2]
+    cfg = (args[3] if len(args) > 3 else kwargs.get("cfg")) or FitConfig()
     _, _, _, grad = _fit(v_src, bmap, target, FitConfig(steps=1, lr=cfg.lr, lambda_pose=cfg.lambda_pose,
                                                         lambda_shape=cfg.lambda_shape), theta, True)
     return grad.cpu().numpy()
+
+
+def fit_objective_value(theta, template, v_target, cfg=None):
+    """Objective at theta (B, 76) -> (loss, per-item mean vertex gaps)
+    (projection.py:269-301): the skinning on the GPU (skin_batch), the
+    reduction in numpy in the reference's float32 order."""
+    from . import bodymodel as bm
+
+    cfg = cfg or FitConfig()
+    theta = np.asarray(theta, DTYPE)
+    v_target = np.asarray(v_target, DTYPE)
+    b = v_target.shape[0]
+    v_hat = np.asarray(bm.skin_batch(template, theta), DTYPE)
+    diff = v_hat - v_target
+    per_item = (diff * diff).reshape((b, -1)).sum(axis=1)
+    body, shape = theta[:, 3:66], theta[:, 66:]
+    reg = (body * body).reshape((b, -1)).sum(axis=1) * np.float32(cfg.lambda_pose) \
+        + (shape * shape).reshape((b, -1)).sum(axis=1) * np.float32(cfg.lambda_shape)
+    gap = np.linalg.norm(v_hat.astype(np.float64) - v_target.astype(np.float64), axis=-1).mean(axis=-1)
+    return float((per_item + reg).sum()), gap
+
+
+@dataclass
+class FitResult:
+    """(projection.py:230-234)"""
+
+    pose: object
+    vertex_error: float
+    curve: np.ndarray
+
+
+def iterative_fit(v_src, bmap, target, cfg=None, init=None):
+    """Single-mesh fit (projection.py:373-388); init may be a PoseState or a
+    76-vector.  One fit_batch of B = 1 on the GPU."""
+    from . import bodymodel as bm
+
+    v = np.asarray(v_src, DTYPE)
+    if v.ndim != 2:
+        raise ShapeError("iterative_fit expects one (Nv, 3) mesh; use fit_batch for batches")
+    init_vec = None
+    if init is not None:
+        vec = init.as_vector() if isinstance(init, bm.PoseState) else np.asarray(init, DTYPE)
+        init_vec = vec[None]
+    res = fit_batch(v[None], bmap, target, cfg=cfg, init=init_vec)
+    return FitResult(pose=bm.PoseState.from_vector(res.params[0]), vertex_error=float(res.vertex_error[0]),
+                     curve=res.curve)
+
 
 
 # ---------------------------------------------------------------------------

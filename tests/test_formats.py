@@ -11,6 +11,8 @@ from paper_2603_15603_b200 import bodymodel as bm
 from paper_2603_15603_b200 import projection as pj
 from paper_2603_15603_b200 import synth
 
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
 FMT = os.path.join(os.path.dirname(__file__), "golden", "formats")
 
 
@@ -63,3 +65,31 @@ def test_wrong_kind_rejected(tmp_path):
 
     with pytest.raises(UsageError):
         pj.load_denoiser(os.path.join(FMT, "projector"))
+
+
+def test_scene_files_match_reference(tmp_path, full_models):
+    """priors.load_scene reads scene files the REFERENCE's save_scene wrote
+    (tools/make_golden_scene.py; priors.py:130-159) into the same scene
+    (keypoints bit-identical), and save_scene writes them back byte for byte."""
+    from paper_2603_15603_b200 import priors as pr
+
+    _, smpl, _ = full_models
+    for i in range(2):
+        ref = os.path.join(GOLDEN, "scene_ref%d.json" % i)
+        sc = pr.load_scene(ref, smpl)
+        assert np.array_equal(sc.keypoints2d, np.load(os.path.join(GOLDEN, "scene_ref%d_kp.npy" % i)))
+        out = str(tmp_path / ("scene%d.json" % i))
+        pr.save_scene(sc, out)
+        assert filecmp.cmp(ref, out, shallow=False)
+
+
+def test_scene_payload_errors(full_models):
+    import pytest
+
+    from paper_2603_15603_b200 import priors as pr
+    from paper_2603_15603_b200.numkit import UsageError
+
+    with pytest.raises(UsageError):
+        pr.scene_from_dict({"camera": {}}, full_models[1])
+    with pytest.raises(UsageError):
+        pr.detect_dense(np.zeros((8, 8, 3), np.float32))

@@ -57,3 +57,28 @@ def test_fit_rejects_bad_input(small):
         pj.FitConfig(steps=0)
     with pytest.raises(ShapeError):
         pj.fit_batch(np.zeros((2, 252), np.float32), gt, smpl)
+
+
+def test_reference_signatures(small):
+    """fit_objective_grad(theta, template, v_target) / fit_objective_value /
+    iterative_fit with the reference's signatures (projection.py:296-310,
+    :373-388) against the reference's own outputs (tools/make_golden_fit.py)."""
+    from paper_2603_15603_b200 import bodymodel as bm
+    from paper_2603_15603_b200 import projection as pj
+
+    g = np.load(GOLD)
+    gv = np.load(GOLD.replace("fit.npz", "fit_value.npz"))
+    mhr, smpl, gt = small
+    cfg = pj.FitConfig(steps=60)
+    for k in ("0", "1"):
+        th = g["theta" + k]
+        got = pj.fit_objective_grad(th, smpl, g["v_t"], cfg)
+        assert np.abs(got - g["g" + k]).max() / np.abs(g["g" + k]).max() <= GRAD_TOL, k
+        loss, gap = pj.fit_objective_value(th, smpl, g["v_t"], cfg)
+        assert abs(loss - gv["loss" + k]) <= 1e-4 * abs(gv["loss" + k]), (k, loss, gv["loss" + k])
+        assert np.abs(gap - gv["gap" + k]).max() <= 1e-4 * np.abs(gv["gap" + k]).max(), k
+    one = pj.iterative_fit(g["v_src"][0], gt, smpl, cfg)
+    assert isinstance(one.pose, bm.PoseState) and one.curve.shape == (61,)
+    assert abs(one.vertex_error - float(gv["it_err"])) <= FIT_TOL * float(gv["it_err"])
+    with pytest.raises(Exception):
+        pj.iterative_fit(g["v_src"], gt, smpl, cfg)  # batches go through fit_batch

@@ -44,6 +44,15 @@ def main():
     np.savez_compressed(OUT, poses=poses, v_src=v_src, v_t=v_t, theta0=theta0, theta1=theta1, g0=g0, g1=g1,
                         params=res.params, vertex_error=res.vertex_error, curve=res.curve)
     print("wrote", OUT, res.vertex_error, res.curve[:3], res.curve[-1])
+    # fit_objective_value (:296-301) at the two points, and iterative_fit of mesh 0 (:373-388)
+    vals = {}
+    for k, th in (("0", theta0), ("1", theta1)):
+        loss, gap = pj.fit_objective_value(th, smpl, v_t, cfg)
+        vals["loss" + k], vals["gap" + k] = np.float64(loss), gap
+    one = pj.iterative_fit(v_src[0], gt, smpl, pj.FitConfig(steps=60))
+    np.savez_compressed(OUT.replace("fit.npz", "fit_value.npz"), **vals, it_err=np.float64(one.vertex_error),
+                        it_curve=one.curve, it_vec=one.pose.as_vector())
+    print("wrote fit_value.npz", vals["loss0"], vals["loss1"], one.vertex_error)
 
 
 if __name__ == "__main__":
