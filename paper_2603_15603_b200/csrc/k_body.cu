@@ -523,6 +523,36 @@ __global__ void __launch_bounds__(kLtThreads, 512 / kLtTmem)
     for (int z = 1; z < NZ; ++z)
       if (w[e][z] != 0.0f) zmax = max(zmax, z + 1);
   const int nzw = __reduce_max_sync(0xffffffffu, zmax);
+  // NZ == 2 (MHR): the union of the two vertices' joints (<= 4), each joint's
+  // rows read ONCE for both vertices, each vertex with its own weight (0 for
+  // a joint it does not use -- exact).  A vertex's joints keep their order
+  // within the union (vertex 0's first), so its sum is formed as before.
+  // Pairs straddling two bones (7 % of the blocks) read 3 joints' rows
+  // instead of 2 x 2.
+  int ju[4] = {0, 0, 0, 0};
+  float wu[2][4] = {{0.0f, 0.0f, 0.0f, 0.0f}, {0.0f, 0.0f, 0.0f, 0.0f}};
+  int nuw = 1;
+  if constexpr (NZ == 2) {
+    int nu = 0;
+#pragma unroll
+    for (int e = 0; e < 2; ++e)
+#pragma unroll
+      for (int z = 0; z < 2; ++z) {
+        if (w[e][z] == 0.0f) continue;
+        int k = nu;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (q < nu && ju[q] == jj[e][z]) k = q;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (q == k) {
+            ju[q] = jj[e][z];
+            wu[e][q] = w[e][z];
+          }
+        nu += k == nu;
+      }
+    nuw = max(1, __reduce_max_sync(0xffffffffu, nu));
+  }
   const uint32_t sbase = tc::smem_u32(lsm);
   auto issue = [&](int buf) {  // D[e][c] = basis(e, c) . shape^T: hi.hi + hi.lo + lo.hi
     const uint32_t bimg = sbase + kLtStage + buf * FSB_LBS_REC_BYTES + FSB_LBS_REC_A2;
@@ -575,7 +605,24 @@ __global__ void __launch_bounds__(kLtThreads, 512 / kLtTmem)
       for (int e = 0; e < 2; ++e)
 #pragma unroll
         for (int c = 0; c < 3; ++c) vs[e][c] = make_float2(vr[e][c] + off[e][c][2 * p], vr[e][c] + off[e][c][2 * p + 1]);
-      if (reuse) {  // one read of each transform row for both vertices
+      if constexpr (NZ == 2) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          if (k >= nuw) break;  // warp-uniform
+          const float4* row = reinterpret_cast<const float4*>(pairA + FSB_LBS_JS * ju[k]);
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            const float4 r01 = row[2 * a], r23 = row[2 * a + 1];
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              float2 pa = ffma2(make_float2(r01.x, r01.y), vs[e][0], make_float2(r23.z, r23.w));
+              pa = ffma2(make_float2(r01.z, r01.w), vs[e][1], pa);
+              pa = ffma2(make_float2(r23.x, r23.y), vs[e][2], pa);
+              o[e][a] = ffma2(make_float2(wu[e][k], wu[e][k]), pa, k == 0 ? make_float2(0.0f, 0.0f) : o[e][a]);
+            }
+          }
+        }
+      } else if (reuse) {  // one read of each transform row for both vertices
 #pragma unroll
         for (int z = 0; z < NZ; ++z) {
           if (z >= nzw) break;  // warp-uniform
