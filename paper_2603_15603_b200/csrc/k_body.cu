@@ -10,6 +10,8 @@
 // template (rest vertices, 1-2 nonzero skin weights per vertex, shape basis;
 // ~4 MB at 18,439 vertices) is read once per CTA into registers and reused
 // across a group of meshes, so HBM traffic is the vertex stream itself.
+#include <cstdlib>
+
 #include "fsb_common.cuh"
 #include "fsb_weights.h"
 #include "tc_sm100.cuh"
@@ -1078,6 +1080,15 @@ cudaError_t launch_lbs_tc(const TemplateDev& t, const uint8_t* lbs_in, int B, fl
   const int tiles = (t.nv + FSB_LBS_TILE - 1) / FSB_LBS_TILE;
   const int nchunks = (B + kLtN - 1) / kLtN;
   int G = (512 / kLtTmem) * 148 / tiles;  // whole waves
+  // at least two chunks per CTA: a small batch (the frame path's 32 meshes =
+  // 2 chunks) then runs one CTA per vertex tile, whose setup (48 KB basis
+  // image, template registers, TMEM) serves both chunks -- LBS saturated cost
+  // 3.08 -> 2.68 us per batch, C2 +0.8 % (FSB_LBS_MINCH overrides)
+  static const int min_chunks = [] {
+    const char* e = getenv("FSB_LBS_MINCH");
+    return e ? atoi(e) : 2;
+  }();
+  if (min_chunks > 1 && G > (nchunks + min_chunks - 1) / min_chunks) G = (nchunks + min_chunks - 1) / min_chunks;
   G = G < 1 ? 1 : (G > nchunks ? nchunks : G);
   dim3 grid(tiles, G);
   switch (t.nnz) {
