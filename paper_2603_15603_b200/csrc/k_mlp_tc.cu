@@ -14,6 +14,7 @@
 // partial; k_tile_reduce adds the partials of all groups in order and applies
 // bias / ReLU / mask.  The K partition depends on K only, so a mesh gives the
 // same bits in a batch of 4096 as alone.
+#include <cstdlib>
 #include <utility>
 
 #include "fsb_common.cuh"
@@ -239,6 +240,84 @@ __global__ void __launch_bounds__(192, 1) k_tile_gemm_p(const uint8_t* __restric
   if (warp == 0) tc::tmem_dealloc(tmem, 256);
 }
 
+// ---------------------------------------------------------------------------
+// Small batches (M = meshes <= 64: the frame path's 32): the same K groups,
+// transposed -- D^T (128 outputs x Np meshes) = W^T tile (the A operand, M =
+// 128) . X^T, the meshes as the N = Np operand (Np = M rounded up to 16).
+// Only the first Np rows of each x k-tile are copied (the K-major row groups
+// are contiguous: Np x 256 bytes instead of 32 KB) and each MMA is 128 x Np
+// instead of 128 x 128 on a mostly-padding A tile.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(128, 1) k_tile_gemm_t(const uint8_t* __restrict__ Aimg, int KT,
+                                                        const uint8_t* __restrict__ Bimg, int G, int M, int N, int Np,
+                                                        float* __restrict__ partial) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bar_load[2], bar_mma[2], bar_done;
+  __shared__ uint32_t tmem_base;
+  const int tid = threadIdx.x, warp = tid / 32;
+  const int nt = blockIdx.x, split = blockIdx.y;
+  const int kt0 = split * G, nk = min(G, KT - kt0);
+  const uint32_t xbytes = (uint32_t)Np * 256u;  // Np rows of a K-major 128 x 128 tile
+  pdl_wait();  // the A image comes from the previous kernel
+  if (tid == 0) {
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&bar_load[i], 1);
+      tc::mbar_init(&bar_mma[i], 1);
+    }
+    tc::mbar_init(&bar_done, 1);
+    tc::mbar_fence_init();
+  }
+  if (warp == 0) tc::tmem_alloc(&tmem_base, 64);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = tmem_base;
+  const uint32_t sbase = tc::smem_u32(smem);
+  constexpr uint32_t kStage = kTileBytes + 64 * 256;  // W^T tile + up to 64 x rows
+  if (tid == 0) {
+    const uint32_t idesc = tc::idesc_bf16(128, Np);
+    auto load = [&](int i) {
+      const int s = i & 1;
+      tc::mbar_expect_tx(&bar_load[s], kTileBytes + xbytes);
+      tc::bulk_g2s(smem + s * kStage, Bimg + ((size_t)nt * KT + kt0 + i) * kTileBytes, kTileBytes, &bar_load[s]);
+      tc::bulk_g2s(smem + s * kStage + kTileBytes, Aimg + ((size_t)kt0 + i) * kTileBytes, xbytes, &bar_load[s]);
+    };
+    load(0);
+    if (nk > 1) load(1);
+    for (int i = 0; i < nk; ++i) {
+      const int s = i & 1;
+      tc::mbar_wait(&bar_load[s], (uint32_t)((i >> 1) & 1));
+      tc::fence_after();
+      const uint32_t w = sbase + s * kStage, x = w + kTileBytes;
+      for (int k = 0; k < 128; k += 16)
+        tc::mma_bf16(tmem, tc::kmajor_desc(w, 128, k), tc::kmajor_desc(x, 128, k), idesc, (i | k) != 0);
+      tc::mma_commit(&bar_mma[s]);
+      if (i + 2 < nk) {
+        tc::mbar_wait(&bar_mma[s], (uint32_t)((i >> 1) & 1));
+        load(i + 2);
+      }
+    }
+    tc::mma_commit(&bar_done);
+  }
+  __syncwarp();
+  tc::mbar_wait(&bar_done, 0);
+  tc::fence_after();
+  // lane = output unit n of this tile, columns = meshes
+  const int n = nt * 128 + tid;
+  const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16);
+  for (int c = 0; c < Np; c += 16) {
+    float v[16];
+    tc::tmem_ld16(taddr + c, v);
+    if (n < N)
+#pragma unroll
+      for (int j = 0; j < 16; ++j)
+        if (c + j < M) partial[((size_t)split * M + c + j) * N + n] = v[j];
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc(tmem, 64);
+}
+
 // k_tile_reduce with one 16-byte K-major chunk (8 consecutive n of a row)
 // per thread: the same partial-sum order, bias / ReLU / mask, fp32 and bf16
 // image stores as whole vectors (N % 4 == 0)
@@ -295,6 +374,9 @@ __global__ void k_tile_reduce8(const float* __restrict__ P, int S, int M, int N,
 cudaError_t init_attrs_mlp_tc() {
   cudaError_t e = cudaFuncSetAttribute(k_tile_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(4 * kTileBytes));
   if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(k_tile_gemm_t, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)(2 * (kTileBytes + 64 * 256)));
+  if (e != cudaSuccess) return e;
   return cudaFuncSetAttribute(k_tile_gemm_p, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               (int)(2 * kPStages * kTileBytes));
 }
@@ -310,7 +392,12 @@ cudaError_t launch_tile_layer(const uint8_t* Aimg, const uint8_t* Bimg, int KT, 
   if (M == 0) return cudaSuccess;
   const int S = (KT + G - 1) / G, NT = (N + 127) / 128, MT = (M + 127) / 128;
   cudaError_t e;
-  if (M >= FSB_TILE_PERSIST_M) {
+  static const bool no_t = getenv("FSB_TILE_NO_T") != nullptr;  // A/B: the 128-row tiles at small M too
+  if (M <= 64 && !no_t) {
+    const int Np = (M + 15) / 16 * 16;
+    e = launch_pdl(k_tile_gemm_t, dim3(NT, S), dim3(128), 2 * (kTileBytes + 64 * 256), st, Aimg, KT, Bimg, G, M, N,
+                   Np, partial);
+  } else if (M >= FSB_TILE_PERSIST_M) {
     const int items = MT * S * NT;
     e = launch_pdl(k_tile_gemm_p, dim3(items < 148 ? items : 148), dim3(192), 2 * kPStages * kTileBytes, st, Aimg, KT,
                    Bimg, G, M, N, S, NT, MT, partial);
