@@ -1012,7 +1012,7 @@ def verify_streams(torch, pipes, outs_s, images, kps, cfg, B, steps, nslot, S):
     return bool(ok)
 
 
-E2E_STREAMS = int(os.environ.get("FSB_E2E_STREAMS", "6"))
+E2E_STREAMS = int(os.environ.get("FSB_E2E_STREAMS", "16"))
 
 
 def pinned_h2d_gbs(torch, dev, nbytes=256 << 20):
