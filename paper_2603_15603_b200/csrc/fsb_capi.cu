@@ -49,7 +49,8 @@ cudaError_t launch_proj_inputs(const TemplateDev& t, const ProjectorDev& p, cons
                                int ld_pose, int B, float* sub, bool f32, __nv_bfloat16* xb, float* psum,
                                cudaStream_t st);
 cudaError_t launch_proj_inputs_v(const float* V, int nv, const ProjectorDev& p, int B, float* sub, bool f32,
-                                 __nv_bfloat16* xb, float* psum, cudaStream_t st, bool compacted = false);
+                                 __nv_bfloat16* xb, float* psum, cudaStream_t st, bool compacted = false,
+                                 __nv_bfloat16* xb_lo = nullptr);
 cudaError_t launch_gemm_f32(const float* A, int lda, const float* W, const float* bias, const float* mask, float* C,
                             int ldc, int M, int N, int K, int relu, int* nonfinite, float* partial,
                             cudaStream_t st);
@@ -75,7 +76,8 @@ cudaError_t init_attrs_mlp_tc();
 cudaError_t init_attrs_gemm_tc();
 cudaError_t launch_tile_layer(const uint8_t* Aimg, const uint8_t* Bimg, int KT, int G, int M, int N, float* partial,
                               const float* bias, const float* mask, int relu, float* out, int ldo, uint8_t* out_img,
-                              int KT_out, int* nonfinite, cudaStream_t st);
+                              int KT_out, int* nonfinite, cudaStream_t st, const uint8_t* Aimg_lo = nullptr,
+                              const uint8_t* Bimg_lo = nullptr, uint8_t* out_img_lo = nullptr);
 cudaError_t launch_encoder_tc(const float* crops, int ncrops, const EncW& w, float* feats, int* nonfinite,
                               const KvArgs& kv, cudaStream_t st);
 cudaError_t launch_decoders_tc(const DecodeArgs& a, const BodyW& bw, const HandW& hw, cudaStream_t st);
@@ -199,6 +201,7 @@ struct fsb_ctx {
   const float* kv_feats = nullptr;
   int kv_frames = 0;
   unsigned char *w_h1img = nullptr, *w_h2img = nullptr;
+  unsigned char *w_xbl = nullptr, *w_h1l = nullptr, *w_h2l = nullptr;  // fp32 mode: remainder images
   // graphs
   bool graphs = true;
   struct GraphEntry {
@@ -593,11 +596,15 @@ int fsb_reserve(fsb_ctx* c, int max_frames) {
   const size_t o_xb = take(ximg_bytes);
   const size_t o_h1i = take(h1img_bytes);
   const size_t o_h2i = take(h2img_bytes);
+  // fp32 mode's remainder images (split-bf16), right behind (one memset)
+  const size_t o_xbl = take(ximg_bytes);
+  const size_t o_h1l = take(h1img_bytes);
+  const size_t o_h2l = take(h2img_bytes);
   const size_t o_h1 = take(F * h1 * 4);
   const size_t o_h2 = take(F * h2 * 4);
   const size_t o_theta = take(F * 76 * 4);
   const int hmax = h1 > h2 ? (h1 > 76 ? h1 : 76) : (h2 > 76 ? h2 : 76);
-  const size_t o_part = take(F * 16 * (size_t)hmax * 4);  // split-K partials (<= 16 chunks)
+  const size_t o_part = take(F * 48 * (size_t)hmax * 4);  // split-K partials (<= 16 chunks; x 3 split-bf16)
   const size_t o_psum = take(F * 8 * 3 * 4);               // projector-input centroid partials
   const size_t o_vu = take(F * (size_t)(c->m->has_proj ? c->m->proj.nu : 1) * 3 * 4);  // compacted corners
   const size_t lbsin_bytes = (F + FSB_LBS_N - 1) / FSB_LBS_N * (size_t)FSB_LBS_REC_BYTES;
@@ -613,9 +620,12 @@ int fsb_reserve(fsb_ctx* c, int max_frames) {
   unsigned char* b = static_cast<unsigned char*>(c->ws.p);
   // zero padding of the tile images (k columns past K, rows past B) must stay
   // finite: clear once, kernels only ever write the live region
-  FSB_CUDA(c, cudaMemset(b + o_xb, 0, ximg_bytes + h1img_bytes + h2img_bytes + 2 * 256));
+  FSB_CUDA(c, cudaMemset(b + o_xb, 0, o_h2l + h2img_bytes - o_xb));
   c->w_h1img = b + o_h1i;
   c->w_h2img = b + o_h2i;
+  c->w_xbl = b + o_xbl;
+  c->w_h1l = b + o_h1l;
+  c->w_h2l = b + o_h2l;
   c->w_boxes = reinterpret_cast<double*>(b + o_boxes);
   c->w_prompt = reinterpret_cast<float*>(b + o_prompt);
   c->w_crops = reinterpret_cast<float*>(b + o_crops);
@@ -1142,22 +1152,29 @@ int fsb_load_projector(fsb_ctx* c, int n_sub, int h1, int h2, const int64_t* cor
   }
   // bf16 tile images of W^T (k_mlp_tc.cu): [n_tile][k_tile] 128 x 128
   // K-major tiles, zero padded in both n and k
-  auto tile_image = [](const float* W, int Kin, int Nout) {
+  // lo = true: the remainder image bf16(W - bf16(W)) (fp32 mode's split-bf16)
+  auto tile_image = [](const float* W, int Kin, int Nout, bool lo) {
     const int KT = (Kin + 127) / 128, NT = (Nout + 127) / 128;
     std::vector<__nv_bfloat16> img((size_t)NT * KT * 128 * 128, __float2bfloat16_rn(0.0f));
     for (int k = 0; k < Kin; ++k)
       for (int n = 0; n < Nout; ++n) {
         const size_t tile = (size_t)(n / 128) * KT + (k / 128);
-        img[tile * 16384 + tc_kmajor_off(n % 128, k % 128, 128) / 2] = __float2bfloat16_rn(W[(size_t)k * Nout + n]);
+        const float w = W[(size_t)k * Nout + n];
+        const __nv_bfloat16 hi = __float2bfloat16_rn(w);
+        img[tile * 16384 + tc_kmajor_off(n % 128, k % 128, 128) / 2] =
+            lo ? __float2bfloat16_rn(w - __bfloat162float(hi)) : hi;
       }
     return img;
   };
   const bool tc_ok = h1 % 128 == 0 && h2 % 128 == 0;
-  std::vector<__nv_bfloat16> i1, i2, i3;
+  std::vector<__nv_bfloat16> i1, i2, i3, l1, l2, l3;
   if (tc_ok) {
-    i1 = tile_image(w1, K, h1);
-    i2 = tile_image(w2, h1, h2);
-    i3 = tile_image(w3, h2, 76);
+    i1 = tile_image(w1, K, h1, false);
+    i2 = tile_image(w2, h1, h2, false);
+    i3 = tile_image(w3, h2, 76, false);
+    l1 = tile_image(w1, K, h1, true);
+    l2 = tile_image(w2, h1, h2, true);
+    l3 = tile_image(w3, h2, 76, true);
   }
   Packer pk;
   const size_t o_c = pk.add(cr.data(), cr.size() * 4);
@@ -1176,6 +1193,9 @@ int fsb_load_projector(fsb_ctx* c, int n_sub, int h1, int h2, const int64_t* cor
   const size_t o_i1 = pk.add(i1.data(), i1.size() * 2);
   const size_t o_i2 = pk.add(i2.data(), i2.size() * 2);
   const size_t o_i3 = pk.add(i3.data(), i3.size() * 2);
+  const size_t o_l1 = pk.add(l1.data(), l1.size() * 2);
+  const size_t o_l2 = pk.add(l2.data(), l2.size() * 2);
+  const size_t o_l3 = pk.add(l3.data(), l3.size() * 2);
   FSB_CUDA(c, c->m->proj_mem.alloc(pk.host.size()));
   FSB_CUDA(c, cudaMemcpy(c->m->proj_mem.p, pk.host.data(), pk.host.size(), cudaMemcpyHostToDevice));
   const unsigned char* base = static_cast<const unsigned char*>(c->m->proj_mem.p);
@@ -1201,6 +1221,9 @@ int fsb_load_projector(fsb_ctx* c, int n_sub, int h1, int h2, const int64_t* cor
   p.img_w1 = tc_ok ? base + o_i1 : nullptr;
   p.img_w2 = tc_ok ? base + o_i2 : nullptr;
   p.img_w3 = tc_ok ? base + o_i3 : nullptr;
+  p.img_w1_lo = tc_ok ? base + o_l1 : nullptr;
+  p.img_w2_lo = tc_ok ? base + o_l2 : nullptr;
+  p.img_w3_lo = tc_ok ? base + o_l3 : nullptr;
   p.KT1 = (K + 127) / 128;
   p.KT2 = (h1 + 127) / 128;
   p.KT3 = (h2 + 127) / 128;
@@ -1516,9 +1539,31 @@ int fsb_skin(fsb_ctx* c, int which, const float* poses, int B, float* verts, voi
 constexpr int kMlpGroup = 4;
 
 static bool mlp_tc(const fsb_ctx* c, int precision) { return precision == FSB_BF16 && c->m->proj.img_w1 != nullptr; }
+// fp32 mode on the tensor cores: every product as hi.hi + hi.lo + lo.hi of
+// bf16 halves (x = hi + lo, hi = bf16(x), lo = bf16(x - hi)), fp32
+// accumulation; FSB_MLP_SIMT=1 keeps the CUDA-core fp32 GEMM
+static bool mlp_split(const fsb_ctx* c, int precision) {
+  static const bool simt = getenv("FSB_MLP_SIMT") != nullptr;
+  return precision == FSB_FP32 && c->m->proj.img_w1_lo != nullptr && !simt;
+}
 
-static int run_mlp(fsb_ctx* c, int B, float* theta, int precision, cudaStream_t st) {
+static int run_mlp(fsb_ctx* c, int B, float* theta, int precision, cudaStream_t st, bool split) {
   const ProjectorDev& p = c->m->proj;
+  if (split) {
+    // the three split-bf16 GEMMs of a layer fill three slices of the split-K
+    // partials; the reduce adds all of them in a fixed order and writes the
+    // next layer's hi and lo images
+    const uint8_t* ximg = reinterpret_cast<const uint8_t*>(c->w_xb);
+    FSB_CUDA(c, launch_tile_layer(ximg, p.img_w1, p.KT1, kMlpGroup, B, p.h1, c->w_part, p.b1, nullptr, 1, nullptr, 0,
+                                  c->w_h1img, p.KT2, nullptr, st, c->w_xbl, p.img_w1_lo, c->w_h1l));
+    FSB_CUDA(c, launch_tile_layer(c->w_h1img, p.img_w2, p.KT2, kMlpGroup, B, p.h2, c->w_part, p.b2, nullptr, 1,
+                                  nullptr, 0, c->w_h2img, p.KT3, nullptr, st, c->w_h1l, p.img_w2_lo, c->w_h2l));
+    FSB_CUDA(c, launch_tile_layer(c->w_h2img, p.img_w3, p.KT3, kMlpGroup, B, FSB_PARAM_DIM, c->w_part, p.b3, p.mask,
+                                  0, theta, FSB_PARAM_DIM, nullptr, 0, c->d_flag, st, c->w_h2l, p.img_w3_lo,
+                                  nullptr));
+    c->launches += 12;
+    return FSB_OK;
+  }
   if (mlp_tc(c, precision)) {
     // relu(x W1 + b1) -> relu(h1 W2 + b2) -> (h2 W3 + b3) * mask on tcgen05;
     // each reduce writes the next layer's bf16 A-tile image
@@ -1549,8 +1594,9 @@ int fsb_project_vertices(fsb_ctx* c, const float* v_mhr, int B, int nv, float* t
   cudaStream_t st = (cudaStream_t)stream;
   int rc = ensure_ws(c, B, st);
   if (rc) return rc;
-  const bool tc = mlp_tc(c, precision);
-  FSB_CUDA(c, launch_proj_inputs_v(v_mhr, nv, c->m->proj, B, c->w_x, !tc, tc ? c->w_xb : nullptr, c->w_psum, st));
+  const bool tc = mlp_tc(c, precision), split = mlp_split(c, precision), img = tc || split;
+  FSB_CUDA(c, launch_proj_inputs_v(v_mhr, nv, c->m->proj, B, c->w_x, !img, img ? c->w_xb : nullptr, c->w_psum, st,
+                                   false, split ? reinterpret_cast<__nv_bfloat16*>(c->w_xbl) : nullptr));
   c->launches += B > 0;  // bridge + centre in one kernel
   if (tc && proj_fused_ok(c->m->proj) && proj_fused_on()) {  // the MLP in one launch
     FSB_CUDA(c, launch_proj_fused(reinterpret_cast<const uint8_t*>(c->w_xb), c->m->proj, B, theta, nullptr, nullptr,
@@ -1559,7 +1605,7 @@ int fsb_project_vertices(fsb_ctx* c, const float* v_mhr, int B, int nv, float* t
     note_stream(c, st);
     return FSB_OK;
   }
-  rc = run_mlp(c, B, theta, precision, st);
+  rc = run_mlp(c, B, theta, precision, st, split);
   if (rc == FSB_OK) note_stream(c, st);
   return rc;
 }
@@ -1585,14 +1631,20 @@ static int skin_project_impl(fsb_ctx* c, const float* params, int B, float* v_mh
   int rc = fk_lbs(c, FSB_MHR, params, B, c->w_rel, c->w_lbsin, nullptr, v_mhr, st, nullptr, cu);
   if (rc) return rc;
   const bool tc = mlp_tc(c, precision);
+  // fp32 mode's split-bf16 MLP takes its inputs from the bridge kernel (the
+  // re-skin path without V_mhr keeps the CUDA-core fp32 GEMMs)
+  const bool split = bridge && mlp_split(c, precision), img = tc || split;
+  __nv_bfloat16* xbl = split ? reinterpret_cast<__nv_bfloat16*>(c->w_xbl) : nullptr;
   if (bridge) {
     // V_mhr was just written: bridge its corner vertices (what the reference
     // projects, projection.py:447-465) instead of re-skinning them -- from
     // the compacted corner buffer when the LBS kernel filled it
     if (cu.vu)
-      FSB_CUDA(c, launch_proj_inputs_v(cu.vu, pj.nu, pj, B, c->w_x, !tc, tc ? c->w_xb : nullptr, c->w_psum, st, true));
+      FSB_CUDA(c, launch_proj_inputs_v(cu.vu, pj.nu, pj, B, c->w_x, !img, img ? c->w_xb : nullptr, c->w_psum, st,
+                                       true, xbl));
     else
-      FSB_CUDA(c, launch_proj_inputs_v(v_mhr, mhr.nv, pj, B, c->w_x, !tc, tc ? c->w_xb : nullptr, c->w_psum, st));
+      FSB_CUDA(c, launch_proj_inputs_v(v_mhr, mhr.nv, pj, B, c->w_x, !img, img ? c->w_xb : nullptr, c->w_psum, st,
+                                       false, xbl));
     c->launches += 1;  // bridge + centre
   } else {
     FSB_CUDA(c, launch_proj_inputs(mhr, c->m->proj, c->w_rel, params, FSB_PARAM_DIM, B, c->w_x, !tc,
@@ -1607,7 +1659,7 @@ static int skin_project_impl(fsb_ctx* c, const float* params, int B, float* v_mh
     c->launches += B > 0;
     return FSB_OK;
   }
-  rc = run_mlp(c, B, theta, precision, st);
+  rc = run_mlp(c, B, theta, precision, st, split);
   if (rc) return rc;
   // SMPL FK (+ the denoiser epilogue on theta[3:66] when one is loaded)
   return fk_lbs(c, FSB_SMPL, theta, B, v_smpl ? c->w_rel2 : nullptr, c->w_lbsin2, j_smpl, v_smpl, st, dn);

@@ -191,6 +191,11 @@ struct ProjectorDev {
   const uint8_t* img_w1;  // (h1 / 128) x KT1, KT1 = ceil(3 * n_sub / 128)
   const uint8_t* img_w2;  // (h2 / 128) x KT2, KT2 = h1 / 128
   const uint8_t* img_w3;  // 1 x KT3 (76 rows used), KT3 = h2 / 128
+  // fp32 (reference-precision) mode on the same tensor-core kernels: the
+  // remainders W - bf16(W) as bf16 images (split-bf16: hi.hi + hi.lo + lo.hi)
+  const uint8_t* img_w1_lo;
+  const uint8_t* img_w2_lo;
+  const uint8_t* img_w3_lo;
   int KT1, KT2, KT3;
   // compacted corner vertices: the LBS kernel writes the nu distinct corner
   // vertices of every mesh (vertex 0, the bridge origin, is slot 0) to a

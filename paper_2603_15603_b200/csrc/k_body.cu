@@ -853,7 +853,8 @@ template <bool STAGED>
 __global__ void __launch_bounds__(kProjVcThreads) k_proj_inputs_vc(const float* __restrict__ V, int nv,
                                                                    ProjectorDev p, const int32_t* __restrict__ corners,
                                                                    float* __restrict__ x32,
-                                                                   __nv_bfloat16* __restrict__ xb, int B, int mpc) {
+                                                                   __nv_bfloat16* __restrict__ xb, int B, int mpc,
+                                                                   __nv_bfloat16* __restrict__ xb_lo) {
   __shared__ float red[kProjVcThreads / 32][3];
   __shared__ float cen[3];
   __shared__ __align__(8) uint64_t bar[2];
@@ -958,8 +959,20 @@ __global__ void __launch_bounds__(kProjVcThreads) k_proj_inputs_vc(const float* 
           const __nv_bfloat162 h = __floats2bfloat162_rn(v8[2 * j], v8[2 * j + 1]);
           w[j] = *reinterpret_cast<const uint32_t*>(&h);
         }
-        *reinterpret_cast<uint4*>(img + (size_t)(k0 >> 7) * 32768 + tc::kmajor_off(b & 127, k0 & 127, 128)) =
-            make_uint4(w[0], w[1], w[2], w[3]);
+        const size_t off = (size_t)(k0 >> 7) * 32768 + tc::kmajor_off(b & 127, k0 & 127, 128);
+        *reinterpret_cast<uint4*>(img + off) = make_uint4(w[0], w[1], w[2], w[3]);
+        if (xb_lo != nullptr) {  // fp32 mode: the remainders v - bf16(v)
+          uint32_t wl[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const __nv_bfloat162 h = *reinterpret_cast<const __nv_bfloat162*>(&w[j]);
+            const float2 hf = __bfloat1622float2(h);
+            const __nv_bfloat162 l = __floats2bfloat162_rn(v8[2 * j] - hf.x, v8[2 * j + 1] - hf.y);
+            wl[j] = *reinterpret_cast<const uint32_t*>(&l);
+          }
+          *reinterpret_cast<uint4*>(reinterpret_cast<uint8_t*>(xb_lo) + (size_t)(b >> 7) * KT * 32768 + off) =
+              make_uint4(wl[0], wl[1], wl[2], wl[3]);
+        }
       }
     }
     __syncthreads();  // xs, red and cen are rewritten by the next mesh
@@ -1163,7 +1176,8 @@ cudaError_t launch_proj_inputs(const TemplateDev& t, const ProjectorDev& p, cons
 }
 
 cudaError_t launch_proj_inputs_v(const float* V, int nv, const ProjectorDev& p, int B, float* sub, bool f32,
-                                 __nv_bfloat16* xb, float* psum, cudaStream_t st, bool compacted) {
+                                 __nv_bfloat16* xb, float* psum, cudaStream_t st, bool compacted,
+                                 __nv_bfloat16* xb_lo) {
   if (B == 0) return cudaSuccess;
   if (p.n_sub > kProjVcThreads * kProjVcPer) return cudaErrorInvalidValue;
   (void)psum;
@@ -1179,12 +1193,12 @@ cudaError_t launch_proj_inputs_v(const float* V, int nv, const ProjectorDev& p, 
   const size_t xs_bytes = (size_t)p.n_sub * 12 + 32;
   if (!compacted)
     return launch_pdl(k_proj_inputs_vc<false>, dim3(B), dim3(kProjVcThreads), xs_bytes, st, V, nv, p, p.corners,
-                      f32 ? sub : nullptr, xb, B, 1);
+                      f32 ? sub : nullptr, xb, B, 1, xb_lo);
   // meshes per CTA: 1 while that leaves SMs idle (latency of small batches),
   // up to 4 for large batches (register-held corners reused, loads overlapped)
   const int mpc = B >= 4 * 148 * 2 ? 4 : (B >= 2 * 148 * 2 ? 2 : 1);
   return launch_pdl(k_proj_inputs_vc<true>, dim3((B + mpc - 1) / mpc), dim3(kProjVcThreads),
-                    (size_t)nv * 24 + xs_bytes, st, V, nv, p, p.ucorners, f32 ? sub : nullptr, xb, B, mpc);
+                    (size_t)nv * 24 + xs_bytes, st, V, nv, p, p.ucorners, f32 ? sub : nullptr, xb, B, mpc, xb_lo);
 }
 
 // number of K chunks of a layer: a function of K only (batch independence);

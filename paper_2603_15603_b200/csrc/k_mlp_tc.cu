@@ -323,7 +323,8 @@ __global__ void __launch_bounds__(128, 1) k_tile_gemm_t(const uint8_t* __restric
 // image stores as whole vectors (N % 4 == 0)
 __global__ void k_tile_reduce8(const float* __restrict__ P, int S, int M, int N, const float* __restrict__ bias,
                                const float* __restrict__ mask, int relu, float* __restrict__ out, int ldo,
-                               uint8_t* __restrict__ out_img, int KT_out, int* nonfinite) {
+                               uint8_t* __restrict__ out_img, int KT_out, int* nonfinite,
+                               uint8_t* __restrict__ out_img_lo) {
   const int N8 = (N + 7) / 8;
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   pdl_wait();
@@ -365,9 +366,20 @@ __global__ void k_tile_reduce8(const float* __restrict__ P, int S, int M, int N,
   }
   if (out_img != nullptr) {
     const size_t tile = (size_t)(m >> 7) * KT_out + (n0 >> 7);
-    *reinterpret_cast<uint4*>(out_img + tile * kTileBytes + tc::kmajor_off(m & 127, n0 & 127, 128)) =
-        make_uint4(tc::pack_bf16(v[0], v[1]), tc::pack_bf16(v[2], v[3]), tc::pack_bf16(v[4], v[5]),
-                   tc::pack_bf16(v[6], v[7]));
+    const size_t off = tile * kTileBytes + tc::kmajor_off(m & 127, n0 & 127, 128);
+    uint32_t h[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) h[j] = tc::pack_bf16(v[2 * j], v[2 * j + 1]);
+    *reinterpret_cast<uint4*>(out_img + off) = make_uint4(h[0], h[1], h[2], h[3]);
+    if (out_img_lo != nullptr) {  // split-bf16: the remainders v - bf16(v)
+      uint32_t l[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const float2 hf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&h[j]));
+        l[j] = tc::pack_bf16(v[2 * j] - hf.x, v[2 * j + 1] - hf.y);
+      }
+      *reinterpret_cast<uint4*>(out_img_lo + off) = make_uint4(l[0], l[1], l[2], l[3]);
+    }
   }
 }
 
@@ -385,31 +397,47 @@ cudaError_t init_attrs_mlp_tc() {
 #define FSB_TILE_PERSIST_M 1024  // batches from this size on: the persistent kernel
 #endif
 
-// one layer: C (M x N) = A_img (M x 128*KT) * B_img^T, K grouped in G k-tiles
-cudaError_t launch_tile_layer(const uint8_t* Aimg, const uint8_t* Bimg, int KT, int G, int M, int N,
-                              float* partial, const float* bias, const float* mask, int relu, float* out, int ldo,
-                              uint8_t* out_img, int KT_out, int* nonfinite, cudaStream_t st) {
-  if (M == 0) return cudaSuccess;
-  const int S = (KT + G - 1) / G, NT = (N + 127) / 128, MT = (M + 127) / 128;
-  cudaError_t e;
+// one GEMM pass of a layer into `partial` (S split-K slices)
+static cudaError_t tile_gemm_pass(const uint8_t* Aimg, const uint8_t* Bimg, int KT, int G, int M, int N, int S,
+                                  float* partial, cudaStream_t st) {
+  const int NT = (N + 127) / 128, MT = (M + 127) / 128;
   static const bool no_t = getenv("FSB_TILE_NO_T") != nullptr;  // A/B: the 128-row tiles at small M too
   if (M <= 64 && !no_t) {
     const int Np = (M + 15) / 16 * 16;
-    e = launch_pdl(k_tile_gemm_t, dim3(NT, S), dim3(128), 2 * (kTileBytes + 64 * 256), st, Aimg, KT, Bimg, G, M, N,
-                   Np, partial);
-  } else if (M >= FSB_TILE_PERSIST_M) {
-    const int items = MT * S * NT;
-    e = launch_pdl(k_tile_gemm_p, dim3(items < 148 ? items : 148), dim3(192), 2 * kPStages * kTileBytes, st, Aimg, KT,
-                   Bimg, G, M, N, S, NT, MT, partial);
-  } else {
-    e = launch_pdl(k_tile_gemm, dim3(NT, S, MT), dim3(128), 4 * kTileBytes, st, Aimg, KT, Bimg, G, M, N, partial);
+    return launch_pdl(k_tile_gemm_t, dim3(NT, S), dim3(128), 2 * (kTileBytes + 64 * 256), st, Aimg, KT, Bimg, G, M,
+                      N, Np, partial);
   }
+  if (M >= FSB_TILE_PERSIST_M) {
+    const int items = MT * S * NT;
+    return launch_pdl(k_tile_gemm_p, dim3(items < 148 ? items : 148), dim3(192), 2 * kPStages * kTileBytes, st, Aimg,
+                      KT, Bimg, G, M, N, S, NT, MT, partial);
+  }
+  return launch_pdl(k_tile_gemm, dim3(NT, S, MT), dim3(128), 4 * kTileBytes, st, Aimg, KT, Bimg, G, M, N, partial);
+}
+
+// one layer: C (M x N) = A_img (M x 128*KT) * B_img^T, K grouped in G k-tiles.
+// Split-bf16 (fp32 mode, Aimg_lo / Bimg_lo given): three passes hi.hi,
+// hi.lo, lo.hi fill three slices of the partials (3 S in all), which the
+// reduce adds in that order; it then writes the next layer's hi AND lo images.
+cudaError_t launch_tile_layer(const uint8_t* Aimg, const uint8_t* Bimg, int KT, int G, int M, int N,
+                              float* partial, const float* bias, const float* mask, int relu, float* out, int ldo,
+                              uint8_t* out_img, int KT_out, int* nonfinite, cudaStream_t st, const uint8_t* Aimg_lo,
+                              const uint8_t* Bimg_lo, uint8_t* out_img_lo) {
+  if (M == 0) return cudaSuccess;
+  const int S = (KT + G - 1) / G;
+  const bool split = Aimg_lo != nullptr && Bimg_lo != nullptr;
+  cudaError_t e = tile_gemm_pass(Aimg, Bimg, KT, G, M, N, S, partial, st);
+  if (e == cudaSuccess && split) e = tile_gemm_pass(Aimg, Bimg_lo, KT, G, M, N, S, partial + (size_t)S * M * N, st);
+  if (e == cudaSuccess && split)
+    e = tile_gemm_pass(Aimg_lo, Bimg, KT, G, M, N, S, partial + (size_t)2 * S * M * N, st);
   if (e != cudaSuccess) return e;
+  const int St = split ? 3 * S : S;
   if (N % 4 == 0 && (out == nullptr || ldo % 4 == 0)) {
     const int64_t tot = (int64_t)M * ((N + 7) / 8);
-    return launch_pdl(k_tile_reduce8, dim3((unsigned)((tot + 255) / 256)), dim3(256), 0, st, partial, S, M, N, bias,
-                      mask, relu, out, ldo, out_img, KT_out, nonfinite);
+    return launch_pdl(k_tile_reduce8, dim3((unsigned)((tot + 255) / 256)), dim3(256), 0, st, partial, St, M, N, bias,
+                      mask, relu, out, ldo, out_img, KT_out, nonfinite, split ? out_img_lo : nullptr);
   }
+  if (split) return cudaErrorInvalidValue;  // (the projector widths are multiples of 4)
   const int64_t tot = (int64_t)M * N;
   return launch_pdl(k_tile_reduce, dim3((unsigned)((tot + 255) / 256)), dim3(256), 0, st, partial, S, M, N, bias, mask,
                     relu, out, ldo, out_img, KT_out, nonfinite);
