@@ -1,6 +1,6 @@
 """Device time of the K3 decoder on body CTAs only, hand CTAs only and both,
 of the encoder + K / V projection launch and of the decoders on projected
-K / V (B = 32 frames, bf16, CUDA-graph replays): python tools/k3_split.py"""
+K / V (B frames, default 32, bf16, CUDA-graph replays): python tools/k3_split.py [B]"""
 import os
 import sys
 
@@ -17,7 +17,7 @@ if __name__ == "__main__":
 
     pipe, _ = bench.build_models("bf16")
     ctx = pipe.context()
-    B = 32
+    B = int(sys.argv[1]) if len(sys.argv) > 1 else 32
     feats = torch.randn((B, 3, 64, 64), device="cuda")
     prompts = torch.rand((B, 8), device="cuda")
     params = torch.empty((B, 76), device="cuda")

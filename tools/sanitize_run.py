@@ -1,7 +1,10 @@
 """Small invocation of every kernel family for compute-sanitizer:
     compute-sanitizer --tool memcheck python tools/sanitize_run.py
 (K1 device + host frames, K2/K3 fp32 + bf16, K4 tail, C4 GEMM + attention +
-LayerNorm, denoise, fit, barycentric search)."""
+LayerNorm, denoise, fit, barycentric search; round 2: the tcgen05 projector
+kernels at small and large batches -- transposed, persistent, split-bf16 --
+with the compacted-corner LBS and multi-mesh bridge, the single-frame API and
+the host-read peak kernel)."""
 import os
 import sys
 
@@ -45,6 +48,45 @@ if __name__ == "__main__":
                                        torch.cuda.current_stream().cuda_stream) == 0
         torch.cuda.synchronize()
         print("attention ok")
+    # round 2: tensor-core projector (hidden 512 / 256) at B = 5 (transposed
+    # tile GEMM) and B = 1200 (persistent tile GEMM, 4 meshes per bridge
+    # CTA), bf16 and fp32 (split-bf16); single-frame API; host-read kernel
+    if not os.environ.get("SANITIZE_SKIP_R2"):
+        proj2 = pj.init_projector(pj.make_subsample(600, 300), (512, 256), seed=0)
+        nb = 1200
+        rng = np.random.default_rng(3)
+        p = np.zeros((nb, 76), np.float32)
+        p[:, :66] = rng.normal(0.0, 0.2, size=(nb, 66))
+        p[:, 66:] = rng.normal(0.0, 0.45, size=(nb, 10))
+        for prec in ("bf16", "fp32"):
+            pipe = pl.Pipeline(dc.Decoder(smpl, dc.DecoderConfig(), seed=40), mhr=mhr, bmap=gt, projector=proj2,
+                               precision=prec)
+            c2 = pipe.context()
+            c2.set_graphs(False)
+            pipe.run_batch(imgs, kps)
+            c2.reserve(nb)
+            poses = torch.from_numpy(p).cuda()
+            v = torch.empty((nb, mhr.num_vertices, 3), device="cuda")
+            th = torch.empty((nb, 76), device="cuda")
+            j = torch.empty((nb, 22, 3), device="cuda")
+            c2.check(c2.lib.fsb_skin_project(c2.h, rt.ptr(poses), nb, rt.ptr(v), rt.ptr(th), rt.ptr(j), None,
+                                             rt.PRECISIONS[prec], c2.stream))
+            torch.cuda.synchronize()
+            c2.check_finite("sanitize c3")
+            pipe.run_smpl(imgs[0], scenes[0])
+            print(prec, "projector kernels ok")
+        import ctypes
+
+        lib = ctypes.CDLL(rt.LIB_PATH)
+        lib.fsb_debug_host_read.argtypes = [ctypes.c_void_p, ctypes.c_size_t, ctypes.c_void_p, ctypes.c_int,
+                                            ctypes.c_void_p]
+        hb = torch.arange(1 << 18, dtype=torch.float32).pin_memory()
+        db = torch.empty_like(hb, device="cuda")
+        assert lib.fsb_debug_host_read(hb.data_ptr(), hb.numel() * 4, db.data_ptr(), 8,
+                                       torch.cuda.current_stream().cuda_stream) == 0
+        torch.cuda.synchronize()
+        assert torch.equal(db.cpu(), hb)
+        print("host read ok")
     cfg = dc.DecoderConfig(crop_size=384, patch=16, dim=1024, heads=16, enc_layers=2, body_layers=1, hand_layers=1)
     ctx = rt.Context()
     ctx.load_decoder(cfg, synth.decoder_weights(cfg, 40, encoder_only=True))
