@@ -226,6 +226,11 @@ int fsb_stage_frame(const float* src, float* dst, int64_t n, int* nonfinite);
  * for the work this context enqueued (an event per stream it used), never
  * for the whole device */
 int fsb_nonfinite(fsb_ctx* ctx, int* flag, int reset);
+/* the same read enqueued on `stream` (ordered after the work enqueued there
+ * before it; no host wait): the flag lands in `host_dst` (pinned host
+ * memory) when the stream reaches it, then is cleared if `reset`.  The
+ * single-frame path reads it together with its results (one sync). */
+int fsb_nonfinite_enqueue(fsb_ctx* ctx, int* host_dst, int reset, void* stream);
 int fsb_counters(const fsb_ctx* ctx, fsb_counters_t* out);
 /* bytes of frame data the crop gather (K1) has read from pinned host frames
  * since the last reset, i.e. the bytes that crossed PCIe (only the crop

@@ -180,6 +180,8 @@ struct fsb_ctx {
   // instead of synchronising the whole device
   std::vector<std::pair<cudaStream_t, cudaEvent_t>> done;
   cudaStream_t aux = nullptr;  // private non-blocking stream for flag reads
+  int* h_flag = nullptr;                  // pinned read-back slots (a pageable target turns the
+  unsigned long long* h_bytes = nullptr;  // 4-byte copy into a staged, synchronous transfer)
   // large-config encoder workspaces
   DevMem vit_ws_mem;
   VitWs vit_ws{};
@@ -531,7 +533,9 @@ static int ctx_new(int device, std::shared_ptr<fsb_model> model, fsb_ctx** out) 
   if (cudaMalloc(&c->d_flag, sizeof(int)) != cudaSuccess || cudaMemset(c->d_flag, 0, sizeof(int)) != cudaSuccess ||
       cudaMalloc(&c->d_bytes_in, sizeof(unsigned long long)) != cudaSuccess ||
       cudaMemset(c->d_bytes_in, 0, sizeof(unsigned long long)) != cudaSuccess ||
-      cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking) != cudaSuccess) {
+      cudaStreamCreateWithFlags(&c->aux, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaMallocHost(&c->h_flag, sizeof(int)) != cudaSuccess ||
+      cudaMallocHost(&c->h_bytes, sizeof(unsigned long long)) != cudaSuccess) {
     fsb_ctx_destroy(c);
     return FSB_ERR_CUDA;
   }
@@ -553,6 +557,8 @@ void fsb_ctx_destroy(fsb_ctx* c) {
   if (c->aux) cudaStreamDestroy(c->aux);
   if (c->d_flag) cudaFree(c->d_flag);
   if (c->d_bytes_in) cudaFree(c->d_bytes_in);
+  if (c->h_flag) cudaFreeHost(c->h_flag);
+  if (c->h_bytes) cudaFreeHost(c->h_bytes);
   delete c;  // the model is freed with its last context
 }
 
@@ -1843,23 +1849,29 @@ int fsb_render(fsb_ctx* c, const void* scenes, int B, int H, int W, float* out, 
 }
 
 int fsb_nonfinite(fsb_ctx* c, int* flag, int reset) {
-  int h = 0;
   FSB_CUDA(c, wait_own_work(c));
-  FSB_CUDA(c, cudaMemcpyAsync(&h, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, c->aux));
+  FSB_CUDA(c, cudaMemcpyAsync(c->h_flag, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, c->aux));
   if (reset) FSB_CUDA(c, cudaMemsetAsync(c->d_flag, 0, sizeof(int), c->aux));
   FSB_CUDA(c, cudaStreamSynchronize(c->aux));
-  if (flag) *flag = h;
+  if (flag) *flag = *c->h_flag;
+  return FSB_OK;
+}
+
+int fsb_nonfinite_enqueue(fsb_ctx* c, int* host_dst, int reset, void* stream) {
+  if (!c || !host_dst) return FSB_ERR_USAGE;
+  cudaStream_t st = (cudaStream_t)stream;
+  FSB_CUDA(c, cudaMemcpyAsync(host_dst, c->d_flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+  if (reset) FSB_CUDA(c, cudaMemsetAsync(c->d_flag, 0, sizeof(int), st));
   return FSB_OK;
 }
 
 int fsb_input_bytes(fsb_ctx* c, int64_t* total, int reset) {
   if (!c || !total) return FSB_ERR_USAGE;
-  unsigned long long h = 0;
   FSB_CUDA(c, wait_own_work(c));
-  FSB_CUDA(c, cudaMemcpyAsync(&h, c->d_bytes_in, sizeof h, cudaMemcpyDeviceToHost, c->aux));
-  if (reset) FSB_CUDA(c, cudaMemsetAsync(c->d_bytes_in, 0, sizeof h, c->aux));
+  FSB_CUDA(c, cudaMemcpyAsync(c->h_bytes, c->d_bytes_in, sizeof *c->h_bytes, cudaMemcpyDeviceToHost, c->aux));
+  if (reset) FSB_CUDA(c, cudaMemsetAsync(c->d_bytes_in, 0, sizeof *c->h_bytes, c->aux));
   FSB_CUDA(c, cudaStreamSynchronize(c->aux));
-  *total = (int64_t)h;
+  *total = (int64_t)*c->h_bytes;
   return FSB_OK;
 }
 

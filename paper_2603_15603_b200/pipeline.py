@@ -444,8 +444,10 @@ class Pipeline:
             out[k] = flat_d[o:o + n].view(shape)
             host[k] = flat_h[o:o + n].view(shape)
             o += n
+        h_flag = torch.zeros((1,), dtype=torch.int32).pin_memory()
         st = {"key": key, "h_img": h_img, "img_np": h_img.numpy()[0], "h_kp": h_kp, "kp_np": h_kp.numpy()[0],
               "out": out, "host": host, "flat_d": flat_d, "flat_h": flat_h, "prep": None, "prep_key": None,
+              "h_flag": h_flag, "h_flag_np": h_flag.numpy(),
               "ev": [torch.cuda.Event(enable_timing=True) for _ in range(3)]}
         self._fstate = st
         return st
@@ -492,9 +494,13 @@ class Pipeline:
         st["prep"].launch(stream)
         ev[1].record(stream)
         st["flat_h"].copy_(st["flat_d"], non_blocking=True)
+        # the device's non-finite flag comes back with the results (one sync)
+        ctx.check(ctx.lib.fsb_nonfinite_enqueue(ctx.h, st["h_flag"].data_ptr(), 1, stream.cuda_stream),
+                  "nonfinite")
         ev[2].record(stream)
         ev[2].synchronize()
-        ctx.check_finite("run")
+        if st["h_flag_np"][0]:
+            raise NumericError("run: non-finite values produced on the device")
         prompt = plan.buffer("prompt", (dc.PROMPT_DIM,))
         merged = plan.buffer("merged", (PARAM_DIM,))
         prompt[:] = st["host"]["prompt"].numpy()[0]

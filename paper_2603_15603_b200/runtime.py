@@ -77,6 +77,7 @@ _SIGS = {
     "fsb_frame_batch": (_i, [_p, _p, _i, _i, _i, _p, _d, _u32, _u32, _i, ctypes.POINTER(FrameOutputsC), _p]),
     "fsb_render": (_i, [_p, _p, _i, _i, _i, _p, _p]),
     "fsb_nonfinite": (_i, [_p, ctypes.POINTER(_i), _i]),
+    "fsb_nonfinite_enqueue": (_i, [_p, _p, _i, _p]),
     "fsb_counters": (_i, [_p, ctypes.POINTER(CountersC)]),
     "fsb_input_bytes": (_i, [_p, ctypes.POINTER(ctypes.c_int64), _i]),
     "fsb_stage_frame": (_i, [_p, _p, ctypes.c_int64, ctypes.POINTER(_i)]),
