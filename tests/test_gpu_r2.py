@@ -299,10 +299,11 @@ def test_c3_64_meshes(torch, g2, full_models, full_projector, precision):
 
 
 def test_c3_batch_independent_bits(torch, full_models, full_projector):
-    """The projector's large-batch kernels (persistent tile GEMM from 1024
-    meshes, compacted-corner bridge with 4 meshes per CTA) give every mesh
-    the same bits as the small-batch kernels: 1536 meshes in one call vs
-    the same meshes in calls of 32 (bf16 and fp32)."""
+    """The projector's batch-size-specific kernels -- persistent tile GEMM
+    from 1024 meshes (and the compacted-corner bridge with 4 meshes per CTA),
+    one-item tile GEMMs in between, the transposed tile GEMM up to 64 --
+    give every mesh the same bits: 1536 meshes in one call vs calls of 256
+    vs calls of 32 (bf16, and fp32 with its split-bf16 passes)."""
     from paper_2603_15603_b200 import decoder as dc
     from paper_2603_15603_b200 import runtime as rt
 
@@ -318,7 +319,7 @@ def test_c3_batch_independent_bits(torch, full_models, full_projector):
         ctx.reserve(n)
         poses = torch.from_numpy(p).cuda()
         outs = []
-        for step in (n, 32):
+        for step in (n, 256, 32):
             v = torch.empty((n, mhr.num_vertices, 3), dtype=torch.float32, device="cuda")
             th = torch.empty((n, 76), dtype=torch.float32, device="cuda")
             j = torch.empty((n, 22, 3), dtype=torch.float32, device="cuda")
@@ -328,8 +329,9 @@ def test_c3_batch_independent_bits(torch, full_models, full_projector):
             torch.cuda.synchronize()
             ctx.check_finite("c3 batch")
             outs.append((th.cpu(), j.cpu(), v[::97].cpu()))
-        for a, b in zip(*outs):
-            assert torch.equal(a, b), precision
+        for other in outs[1:]:
+            for a, b in zip(outs[0], other):
+                assert torch.equal(a, b), precision
 
 
 # ---------------------------------------------------------------------------
