@@ -1147,15 +1147,6 @@ int fsb_load_projector(fsb_ctx* c, int n_sub, int h1, int h2, const int64_t* cor
   for (size_t v = 1; v < vslot.size(); ++v)
     if (used[v]) vslot[v] = nu++;
   for (size_t i = 0; i < cr.size(); ++i) ucr[i] = vslot[cr[i]];
-  const size_t nblk = vslot.size() / 64 + 1;
-  std::vector<int32_t> ublk(nblk * 2, 0);
-  std::vector<uint8_t> ulist(nblk * 64, 0);
-  for (size_t v = 0; v < vslot.size(); ++v) {
-    if (vslot[v] < 0) continue;
-    const size_t bi = v / 64;
-    if (ublk[2 * bi + 1] == 0) ublk[2 * bi] = vslot[v];  // slots rise with v: the block's run starts here
-    ulist[bi * 64 + ublk[2 * bi + 1]++] = (uint8_t)(v % 64);
-  }
   // bf16 tile images of W^T (k_mlp_tc.cu): [n_tile][k_tile] 128 x 128
   // K-major tiles, zero padded in both n and k
   // lo = true: the remainder image bf16(W - bf16(W)) (fp32 mode's split-bf16)
@@ -1187,8 +1178,6 @@ int fsb_load_projector(fsb_ctx* c, int n_sub, int h1, int h2, const int64_t* cor
   const size_t o_bw = pk.add(bary, (size_t)n_sub * 12);
   const size_t o_vs = pk.add(vslot.data(), vslot.size() * 4);
   const size_t o_uc = pk.add(ucr.data(), ucr.size() * 4);
-  const size_t o_ub = pk.add(ublk.data(), ublk.size() * 4);
-  const size_t o_ul = pk.add(ulist.data(), ulist.size());
   const size_t o_w1 = pk.add(w1, (size_t)K * h1 * 4);
   const size_t o_b1 = pk.add(b1, (size_t)h1 * 4);
   const size_t o_w2 = pk.add(w2, (size_t)h1 * h2 * 4);
@@ -1215,8 +1204,6 @@ int fsb_load_projector(fsb_ctx* c, int n_sub, int h1, int h2, const int64_t* cor
   p.nvslot = (int)vslot.size();
   p.vslot = reinterpret_cast<const int32_t*>(base + o_vs);
   p.ucorners = reinterpret_cast<const int32_t*>(base + o_uc);
-  p.ublk = reinterpret_cast<const int32_t*>(base + o_ub);
-  p.ulist = reinterpret_cast<const uint8_t*>(base + o_ul);
   p.w1 = reinterpret_cast<const float*>(base + o_w1);
   p.b1 = reinterpret_cast<const float*>(base + o_b1);
   p.w2 = reinterpret_cast<const float*>(base + o_w2);
@@ -1628,8 +1615,6 @@ static int skin_project_impl(fsb_ctx* c, const float* params, int B, float* v_mh
   CornerOut cu;
   if (bridge && !lbs_simt() && pj.nvslot <= mhr.nv && getenv("FSB_PROJ_SCATTER") == nullptr) {
     cu.vu = c->w_vu;
-    cu.ublk = pj.ublk;
-    cu.ulist = pj.ulist;
     cu.vslot = pj.vslot;
     cu.nvslot = pj.nvslot;
     cu.nu = pj.nu;

@@ -205,18 +205,12 @@ struct ProjectorDev {
   int nvslot;             // length of vslot (max corner id + 1)
   const int32_t* vslot;   // (nvslot) slot of a source vertex in the compacted buffer, -1 if unused
   const int32_t* ucorners;  // (n_sub, 3) corners as slots
-  // per 64-vertex block (one LBS warp's vertices): first slot, corner count,
-  // and the block-local vertex of each of its corners in slot order
-  const int32_t* ublk;    // (nvslot / 64 + 1, 2)
-  const uint8_t* ulist;   // (nvslot / 64 + 1, 64)
 };
 
 // optional compacted corner output of the LBS kernel (ProjectorDev::nu)
 struct CornerOut {
   float* vu = nullptr;             // (B, nu, 3) or null
-  const int32_t* ublk = nullptr;   // ProjectorDev::ublk / ulist
-  const uint8_t* ulist = nullptr;
-  const int32_t* vslot = nullptr;  // ProjectorDev::vslot (per-thread scatter variant, FSB_LBS_URUN=0)
+  const int32_t* vslot = nullptr;  // ProjectorDev::vslot
   int nvslot = 0, nu = 0;
 };
 

@@ -483,30 +483,11 @@ __global__ void __launch_bounds__(kLtThreads, 512 / kLtTmem)
 #pragma unroll
     for (int c = 0; c < 3; ++c) vr[e][c] = live ? __ldg(t.v_rest + (int64_t)v * 3 + c) : 0.0f;
   }
-  // the warp's projector corners (compacted buffer, ProjectorDev::ublk):
-  // nuf floats from slot u0 on; this lane stores floats lane + 32 i, whose
-  // staging-row offsets (< 192) are packed four to a register
-#ifndef FSB_LBS_URUN  // 1: the warp's corners as one contiguous run from the staging rows (measured slower)
-#define FSB_LBS_URUN 0
-#endif
-  int u0 = 0, nuf = 0;
-  uint32_t uoff[2] = {0u, 0u};
-#if !FSB_LBS_URUN
+  // this thread's vertices' slots in the compacted corner buffer (-1: not
+  // a projector corner)
   int slot[2];
 #pragma unroll
   for (int e = 0; e < 2; ++e) slot[e] = cu.vu != nullptr && va + e < cu.nvslot ? __ldg(cu.vslot + va + e) : -1;
-#endif
-  if (FSB_LBS_URUN && cu.vu != nullptr && vw < cu.nvslot) {
-    const int bi = vw >> 6;
-    u0 = __ldg(cu.ublk + 2 * bi);
-    nuf = 3 * __ldg(cu.ublk + 2 * bi + 1);
-#pragma unroll
-    for (int i = 0; i < 6; ++i) {
-      const int f = lane + 32 * i;
-      const uint32_t o = f < nuf ? 3u * __ldg(cu.ulist + 64 * bi + f / 3) + f % 3 : 0u;
-      uoff[i >> 2] |= o << (8 * (i & 3));
-    }
-  }
   pdl_wait();  // (the template reads above are constant data)
   // every vertex pair of the warp has one joint set: one row read serves both
   bool same = true;
@@ -651,7 +632,8 @@ __global__ void __launch_bounds__(kLtThreads, 512 / kLtTmem)
         if (va + e < t.nv)
 #pragma unroll
           for (int a = 0; a < 3; ++a) chk = ffma2(o[e][a], make_float2(1.0f, 1.0f), chk);
-#if !FSB_LBS_URUN
+      // projector corners into the compacted (B, nu, 3) buffer (a warp-contiguous
+      // run gathered from the staging rows measured slower)
 #pragma unroll
       for (int e = 0; e < 2; ++e)
         if (slot[e] >= 0) {
@@ -662,7 +644,6 @@ __global__ void __launch_bounds__(kLtThreads, 512 / kLtTmem)
 #pragma unroll
             for (int a = 0; a < 3; ++a) u[(int64_t)cu.nu * 3 + a] = o[e][a].y;
         }
-#endif
       // the warp's 64 vertices of meshes m, m + 1 leave as coalesced rows
       // through its staging buffer (2 x 192 floats).  Measured alternatives
       // (DESIGN.md §4): cp.async.bulk of the 16-byte-aligned interior and
@@ -689,17 +670,6 @@ __global__ void __launch_bounds__(kLtThreads, 512 / kLtTmem)
         for (int i = 0; i < 6; ++i) {
           const int idx = 32 * i + lane;
           if (idx < nfw) __stcs(dst + idx, stg[half * kLtRow + idx]);
-        }
-        // the warp's projector corners, one contiguous run of the
-        // compacted (B, nu, 3) corner buffer (L2-resident for the bridge)
-        if (nuf > 0) {
-          float* ud = cu.vu + ((int64_t)(m + half) * cu.nu + u0) * 3;
-#pragma unroll
-          for (int i = 0; i < 6; ++i) {
-            const int f = lane + 32 * i;
-            if (32 * i >= nuf) break;  // warp-uniform
-            if (f < nuf) ud[f] = stg[half * kLtRow + ((uoff[i >> 2] >> (8 * (i & 3))) & 0xffu)];
-          }
         }
       }
       __syncwarp();  // the staging rows are rewritten by the next pair
