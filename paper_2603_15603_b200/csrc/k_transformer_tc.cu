@@ -733,17 +733,25 @@ __device__ void cross_attn_hands(Pipe& P, const float* prm, float* x, const uint
       for (int tp = 0; tp < 4; ++tp) sc[kk][tp] += __shfl_xor_sync(0xffffffffu, sc[kk][tp], 1);
     // online softmax (scores in log2 units): sc becomes the probabilities;
     // the accumulators are rescaled only when a row of the warp raised its
-    // maximum (warp-uniform test; rare after the first keys)
+    // maximum (one warp-uniform test for the four rows; rows whose maximum
+    // held are multiplied by exactly 1, so the bits are those of a per-row
+    // test; rare after the first keys)
+    float corr[4];
+    bool grew = false;
 #pragma unroll
     for (int tp = 0; tp < 4; ++tp) {
       const float mn = fmaxf(m[tp], fmaxf(sc[0][tp], sc[1][tp]));
-      const float corr = ex2_approx(m[tp] - mn);
+      corr[tp] = ex2_approx(m[tp] - mn);
       m[tp] = mn;
       sc[0][tp] = ex2_approx(sc[0][tp] - mn);
       sc[1][tp] = ex2_approx(sc[1][tp] - mn);
-      lsum[tp] = fmaf(lsum[tp], corr, sc[0][tp] + sc[1][tp]);
-      if (__any_sync(0xffffffffu, corr != 1.0f)) {
-        const float2 c2 = make_float2(corr, corr);
+      lsum[tp] = fmaf(lsum[tp], corr[tp], sc[0][tp] + sc[1][tp]);
+      grew = grew || corr[tp] != 1.0f;
+    }
+    if (__any_sync(0xffffffffu, grew)) {
+#pragma unroll
+      for (int tp = 0; tp < 4; ++tp) {
+        const float2 c2 = make_float2(corr[tp], corr[tp]);
 #pragma unroll
         for (int k = 0; k < 4; ++k) o[tp][k] = __fmul2_rn(o[tp][k], c2);
       }
@@ -760,6 +768,8 @@ __device__ void cross_attn_hands(Pipe& P, const float* prm, float* x, const uint
       }
     }
     }
+    // (a group barrier per key pair; per-slot release barriers that let a
+    // warp run ahead measured slower: hand CTA 173 -> 182 us)
     P.sync();  // every thread is done with the slot
     if (FSB_HKV_EXP != 1 && P.tid == 0 && s + KV_STAGES < KV_STAGES_PER_LAYER) issue(s + KV_STAGES);
   }
