@@ -1092,6 +1092,9 @@ __global__ void __launch_bounds__(NTH, 1) k_encoder_tc(const float* __restrict__
   if (kv.mode == 0 ? 4 * (int)blockIdx.x + 2 * P.g < ncrops : (P.g == 0 ? has0 : has1)) {
 
   float y[HC];
+#ifdef FSB_PROFILE
+  long long efin = 0;
+#endif
   if (kv.mode != 2) {
   // patchify (decoder.py:247-248): this thread packs image rows iy in
   // [4h, 4h + 4) of patch p into the K = 192 tile (k = iy*24 + ix*3 + c),
@@ -1117,26 +1120,63 @@ __global__ void __launch_bounds__(NTH, 1) k_encoder_tc(const float* __restrict__
   }
   float x[HC];
   {
+#ifdef FSB_PROFILE
+    const long long ep0 = clock64();
+    P.prof[10] += ep0 + P.prof[0];  // kernel start -> patchify done
+#endif
     const uint32_t wp = P.acquire();
+#ifdef FSB_PROFILE
+    const long long ep1 = clock64();
+#endif
     P.before_issue();
     if (P.tid == 0) gemm(P.sbase + S_A, 192, wp, D, T_GEN, P.tmem);
     P.prefetch();
     P.commit_wait();
+#ifdef FSB_PROFILE
+    P.prof[11] += clock64() - ep0;  // embedding weights wait + GEMM
+#endif
+    // patch bias and position rows as 16-byte loads, all in flight at once
+    // (32 + 32 scalar loads serialised into ~20 L2 round trips: ~17K cycles)
+    float4 b4[HC / 4], p4[HC / 4];
+    const float4* pb = reinterpret_cast<const float4*>(w.patch_b + HC * P.h);
+    const float4* pp = reinterpret_cast<const float4*>(w.pos + p * D + HC * P.h);
+#pragma unroll
+    for (int q = 0; q < HC / 4; ++q) {
+      b4[q] = __ldg(pb + q);
+      p4[q] = __ldg(pp + q);
+    }
     float v[HC];
     tmem_ld32(P.lane_addr(T_GEN + HC * P.h), v);
 #pragma unroll
-    for (int i = 0; i < HC; ++i) {
-      const int c = HC * P.h + i;
-      x[i] = valid ? (v[i] + __ldg(w.patch_b + c)) + __ldg(w.pos + p * D + c) : 0.0f;
+    for (int q = 0; q < HC / 4; ++q) {
+      const float bq[4] = {b4[q].x, b4[q].y, b4[q].z, b4[q].w}, pq[4] = {p4[q].x, p4[q].y, p4[q].z, p4[q].w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) x[4 * q + j] = valid ? (v[4 * q + j] + bq[j]) + pq[j] : 0.0f;
     }
   }
+#ifdef FSB_PROFILE
+  P.prof[8] += clock64() + P.prof[0];  // kernel start -> layer loop (setup, patchify, embedding)
+#endif
   for (int l = 0; l < w.layers; ++l) {
+#ifdef FSB_PROFILE
+    const long long e0 = clock64();
+#endif
     const float* prm = P.pacquire();
     P.sync();  // every thread of the group is past layer l - 1
     P.prelease();
     self_attn<BLK, false, true>(P, prm, x, x, valid);
+#ifdef FSB_PROFILE
+    const long long e1 = clock64();
+    P.prof[5] += e1 - e0;
+#endif
     mlp(P, prm, x, valid);
+#ifdef FSB_PROFILE
+    P.prof[7] += clock64() - e1;
+#endif
   }
+#ifdef FSB_PROFILE
+  efin = clock64();
+#endif
   ln_half(P, x, w.norm_g, w.norm_b, y);
   if (valid) {
     float* out = feats + ((int64_t)crop * 64 + p) * D + HC * P.h;
@@ -1156,7 +1196,14 @@ __global__ void __launch_bounds__(NTH, 1) k_encoder_tc(const float* __restrict__
       y[c] = v.x; y[c + 1] = v.y; y[c + 2] = v.z; y[c + 3] = v.w;
     }
   }
+#ifdef FSB_PROFILE
+  if (kv.mode != 2) P.prof[9] += clock64() - efin;  // final LN + feature stores
+  const long long ekv = clock64();
+#endif
   if (kv.mode != 0) kv_project(P, y, body, tile, kv);
+#ifdef FSB_PROFILE
+  P.prof[6] += clock64() - ekv;
+#endif
   }  // group has crops
   teardown(P, 0);
 }
@@ -1302,17 +1349,35 @@ __global__ void __launch_bounds__(NTH, 1) k_decoders_tc(DecodeArgs a, BodyW bw, 
       }
       bx.boxtok[b][o] = acc + __ldg(bw.prompt_box_b + o);
     }
+    // the token row as 16-byte loads, all in flight before the barrier
+    // (scalar loads serialised into L2 round trips, as in the encoder)
+    float4 ti[HC / 4];
+    const float4* tsrc = reinterpret_cast<const float4*>(bw.token_init + (valid ? rb : 0) * D + c0);
+#pragma unroll
+    for (int q = 0; q < HC / 4; ++q) ti[q] = __ldg(tsrc + q);
     if (t < 2) bx.pred[t] = 0;
     P.sync();
 #pragma unroll
-    for (int c = 0; c < HC; ++c) {
-      float v = valid ? __ldg(bw.token_init + rb * D + c0 + c) : 0.0f;
-      if (valid && rb >= 1 && rb < 5) v += bx.boxtok[blk][(rb - 1) * D + c0 + c];
-      x[c] = v;
+    for (int q = 0; q < HC / 4; ++q) {
+      const float tv[4] = {ti[q].x, ti[q].y, ti[q].z, ti[q].w};
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int c = 4 * q + j;
+        float v = valid ? tv[j] : 0.0f;
+        if (valid && rb >= 1 && rb < 5) v += bx.boxtok[blk][(rb - 1) * D + c0 + c];
+        x[c] = v;
+      }
     }
   } else {
+    const float4* tsrc = reinterpret_cast<const float4*>(hw.token_init + (valid ? rb : 0) * D + c0);
 #pragma unroll
-    for (int c = 0; c < HC; ++c) x[c] = valid ? __ldg(hw.token_init + rb * D + c0 + c) : 0.0f;
+    for (int q = 0; q < HC / 4; ++q) {
+      const float4 tv = __ldg(tsrc + q);
+      x[4 * q] = valid ? tv.x : 0.0f;
+      x[4 * q + 1] = valid ? tv.y : 0.0f;
+      x[4 * q + 2] = valid ? tv.z : 0.0f;
+      x[4 * q + 3] = valid ? tv.w : 0.0f;
+    }
     if (t == 0) hx.pred = 0;
   }
   P.sync();

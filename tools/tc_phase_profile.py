@@ -41,6 +41,9 @@ def main():
             print(tag, tname, "rc", rc,
                   " ".join("%s=%d(%.1f%%)" % (n, x, 100.0 * x / max(v[0], 1)) for n, x in zip(names, v)),
                   "work=%d(%.1f%%)" % (rest, 100.0 * rest / max(v[0], 1)))
+            if role == 0:
+                print("   encoder: setup+patchify+embed=%d [start->patchified=%d embed wait+GEMM=%d] self-attn=%d "
+                      "mlp=%d final-LN+out=%d kv-projection=%d" % (v[8], v[10], v[11], v[5], v[7], v[9], v[6]))
             if role >= 1:
                 other = v[0] - v[5] - v[6] - v[7]
                 print("   sub-layers: self=%d cross=%d mlp=%d other=%d [setup+final=%d pos+params=%d heads=%d fk=%d]"
