@@ -406,3 +406,41 @@ def test_render_odd_size_off_frame(torch, g2, d2, full_models):
     assert img.shape == (200, 300, 3)
     d = np.abs(img[::5].astype(np.float64) - g2["render_odd.rows"]).max()
     assert d <= RENDER_ABS, d
+
+
+# ---------------------------------------------------------------------------
+# single-frame API error contract (round 2: native staging + enqueued flag)
+
+
+def test_single_frame_api_nonfinite(torch, full_models, full_projector):
+    """Pipeline.run_smpl: a NaN / inf in the host image raises NumericError
+    before any device work (fsb_stage_frame, numkit.bilinear_sample's
+    check_finite); non-finite values produced on the device raise through the
+    flag read enqueued with the results (fsb_nonfinite_enqueue); the flag is
+    cleared, so the next good call succeeds and matches the first."""
+    from paper_2603_15603_b200 import decoder as dc
+    from paper_2603_15603_b200 import synth
+    from paper_2603_15603_b200.numkit import NumericError
+
+    mhr, smpl, gt = full_models
+    dec = dc.Decoder(smpl, dc.DecoderConfig(), seed=40)
+    pipe = _pipeline(dec, mhr, gt, full_projector, "bf16")
+    sc = synth.random_scene(np.random.default_rng(77), smpl, (512, 512))
+    img = synth.render_scene(sc, smpl)
+    good, _ = pipe.run_smpl(img, sc)
+    for v in (np.nan, np.inf):
+        bad = img.copy()
+        bad[100, 200, 1] = v
+        with pytest.raises(NumericError):
+            pipe.run_smpl(bad, sc)
+    again, _ = pipe.run_smpl(img, sc)
+    assert np.array_equal(again["theta"], good["theta"])
+    # a non-finite weight: the device flags it, the call raises, the flag resets
+    key = next(k for k in dec.weights if k.endswith("head_params_b") or k.endswith("head_params.b"))
+    saved = dec.weights[key]
+    dec.weights[key] = np.full_like(saved, np.inf)
+    with pytest.raises(NumericError):
+        pipe.run_smpl(img, sc)
+    dec.weights[key] = saved
+    after, _ = pipe.run_smpl(img, sc)
+    assert np.array_equal(after["theta"], good["theta"])
