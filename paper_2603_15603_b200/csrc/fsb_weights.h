@@ -233,6 +233,7 @@ struct DecodeArgs {
   const uint8_t* body_kv;   // FSB_KV_BODY_TILE bytes per (body tile, layer)
   const uint8_t* hand_kv;   // FSB_KV_HAND bytes per (hand, layer), 32 hands per tile
   int hand_tiles_per_cta;   // set by the launcher
+  int hand_split;           // set by the launcher: one-tile hand CTAs split the cross-attention keys over both groups
 };
 
 // Cross-attention K / V of the decoders depend only on the features

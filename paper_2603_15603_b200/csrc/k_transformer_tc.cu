@@ -645,71 +645,118 @@ static_assert(KV_STAGES * KV_STAGE_BYTES <= 3 * 16384, "the ring spans S_Q, S_K,
 #ifndef FSB_HKV_EXP
 #define FSB_HKV_EXP 0  // experiments: 1 = no copies / waits (compute only), 2 = no compute (copies only)
 #endif
-__device__ void cross_attn_hands(Pipe& P, const float* prm, float* x, const uint8_t* hkv, int hand0, int nslots,
-                                 int l, int L, bool valid) {
-  const int u0 = P.kvuse;
-  // key pair s of this layer (16 KB: the tile's 32 hands x 512 bytes) ->
-  // ring slot (u0 + s) % 3, one bulk copy
-  const uint8_t* src = hkv + ((size_t)(hand0 / FSB_HANDS_PER_TILE) * L + l) * (32 * KV_STAGE_BYTES);
-  auto issue = [&](int s) {
-    const int n = u0 + s, slot = n % KV_STAGES;
-    uint64_t* bar = &P.sh->kvb[P.g][slot];
-    tc::mbar_expect_tx(bar, KV_STAGE_BYTES);
-    tc::bulk_g2s(P.smem + S_Q + slot * KV_STAGE_BYTES, src + (size_t)s * KV_STAGE_BYTES, KV_STAGE_BYTES, bar);
-  };
-  if (FSB_HKV_EXP != 1 && P.tid == 0)  // S_Q..S_VT are free: the self-attention's MMAs have completed
-    for (int s = 0; s < KV_STAGES; ++s) issue(s);
-  ln_half_to_tile(P, x, prm + TCP_C_LNQ_G, prm + TCP_C_LNQ_B);
-  const uint32_t wq = P.acquire();
-  P.before_issue();
-  if (P.tid == 0) gemm(P.sbase + S_A, D, wq, D, T_GEN, P.tmem);
-  P.prefetch();
-  P.commit_wait();
-  // the residual stream waits in TMEM columns [128 + 32 h, +32) (the query
-  // accumulator uses [0, 64))
-  {
-    uint32_t xu[HC];
-#pragma unroll
-    for (int c = 0; c < HC; ++c) xu[c] = __float_as_uint(x[c]);
-    tc::tmem_st32u_nowait(P.lane_addr(T_GEN + 128 + HC * P.h), xu);
-  }
-  const int t = P.r & 3, lane = P.r & 31;
-  // qc[tp][k]: query row 4 i + tp (+ bias, pre-scaled by 1/sqrt(16) log2(e)),
-  // on this thread's chunk (column 32 h + 8 t + 2k, + 1)
-  float2 qc[4][4];
-  {
-    float q[HC];
-    tmem_ld32(P.lane_addr(T_GEN + HC * P.h), q);
-#pragma unroll
-    for (int i = 0; i < HC; ++i) q[i] = (q[i] + prm[TCP_C_BQKV + HC * P.h + i]) * kScale;
-#pragma unroll
-    for (int sc = 0; sc < 4; ++sc)
-#pragma unroll
-      for (int k = 0; k < 8; k += 2)
-#pragma unroll
-        for (int tp = 0; tp < 4; ++tp) {
-          const float a0 = __shfl_sync(0xffffffffu, q[8 * sc + k], (lane & ~3) | tp);
-          const float a1 = __shfl_sync(0xffffffffu, q[8 * sc + k + 1], (lane & ~3) | tp);
-          if (t == sc) qc[tp][k / 2] = make_float2(a0, a1);
-        }
-  }
+// online-softmax state of one thread's four query rows over a run of keys
+struct HandState {
   float2 o[4][4];
-  float m[4], lsum[4];
+  float m[4], l[4];
+};
+constexpr int KV_HALF = KV_STAGES_PER_LAYER / 2;  // key pairs per half
+
+// qc[tp][k]: query row 4 i + tp (+ bias, pre-scaled by 1/sqrt(16) log2(e)),
+// on this thread's chunk (column 32 h + 8 t + 2k, + 1), from the query
+// accumulator at TMEM lane address `qaddr`
+__device__ __forceinline__ void hand_queries(const Pipe& P, uint32_t qaddr, const float* prm, float2 (&qc)[4][4]) {
+  const int t = P.r & 3, lane = P.r & 31;
+  float q[HC];
+  tmem_ld32(qaddr, q);
+#pragma unroll
+  for (int i = 0; i < HC; ++i) q[i] = (q[i] + prm[TCP_C_BQKV + HC * P.h + i]) * kScale;
+#pragma unroll
+  for (int sc = 0; sc < 4; ++sc)
+#pragma unroll
+    for (int k = 0; k < 8; k += 2)
+#pragma unroll
+      for (int tp = 0; tp < 4; ++tp) {
+        const float a0 = __shfl_sync(0xffffffffu, q[8 * sc + k], (lane & ~3) | tp);
+        const float a1 = __shfl_sync(0xffffffffu, q[8 * sc + k + 1], (lane & ~3) | tp);
+        if (t == sc) qc[tp][k / 2] = make_float2(a0, a1);
+      }
+}
+
+// 40 state floats of a thread <-> 40 TMEM columns of its lane
+__device__ __forceinline__ void hand_state_st(uint32_t addr, const HandState& S) {
+  float v[40];
 #pragma unroll
   for (int tp = 0; tp < 4; ++tp) {
-    m[tp] = -INFINITY;
-    lsum[tp] = 0.0f;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) o[tp][k] = make_float2(0.0f, 0.0f);
+    for (int k = 0; k < 4; ++k) {
+      v[8 * tp + 2 * k] = S.o[tp][k].x;
+      v[8 * tp + 2 * k + 1] = S.o[tp][k].y;
+    }
+    v[32 + tp] = S.m[tp];
+    v[36 + tp] = S.l[tp];
   }
+  tc::tmem_st32(addr, v);
+  tc::tmem_st8(addr + 32, v + 32);
+}
+__device__ __forceinline__ void hand_state_ld(uint32_t addr, HandState& S) {
+  float v[40];
+  tmem_ld32(addr, v);
+  tc::tmem_ld8(addr + 32, v + 32);
+#pragma unroll
+  for (int tp = 0; tp < 4; ++tp) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) S.o[tp][k] = make_float2(v[8 * tp + 2 * k], v[8 * tp + 2 * k + 1]);
+    S.m[tp] = v[32 + tp];
+    S.l[tp] = v[36 + tp];
+  }
+}
+
+// The two halves of the keys (pairs [0, 16) and [16, 32)) always run as two
+// separate online-softmax passes merged by hand_merge: by one group in
+// sequence, or -- in a hand CTA holding one tile, whose second thread group
+// would idle -- by the two groups side by side.  Same arithmetic either way,
+// so a hand's bits do not depend on the launch shape.
+__device__ __forceinline__ void hand_merge(HandState& A, const HandState& B) {
+#pragma unroll
+  for (int tp = 0; tp < 4; ++tp) {
+    const float mm = fmaxf(A.m[tp], B.m[tp]);
+    const float ca = ex2_approx(A.m[tp] - mm), cb = ex2_approx(B.m[tp] - mm);
+    A.l[tp] = fmaf(A.l[tp], ca, B.l[tp] * cb);
+    A.m[tp] = mm;
+    const float2 ca2 = make_float2(ca, ca), cb2 = make_float2(cb, cb);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) A.o[tp][k] = ffma2(A.o[tp][k], ca2, __fmul2_rn(B.o[tp][k], cb2));
+  }
+}
+
+__device__ __forceinline__ void hand_state_reset(HandState& S) {
+#pragma unroll
+  for (int tp = 0; tp < 4; ++tp) {
+    S.m[tp] = -INFINITY;
+    S.l[tp] = 0.0f;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) S.o[tp][k] = make_float2(0.0f, 0.0f);
+  }
+}
+
+// `count` key pairs through this group's ring: pair j is layer pair
+// first + j in slot (u0 + j) % 3; the caller issued pairs 0..2.  With
+// `save_at` in range, the state of pairs [0, save_at) is parked in TMEM at
+// `save_addr` and the pass restarts (the sequential two-half schedule).
+__device__ void hand_keys(Pipe& P, const uint8_t* src, int first, int count, int u0, const float2 (&qc)[4][4],
+                          HandState& S, int save_at, uint32_t save_addr) {
+  const int t = P.r & 3;
+  auto issue = [&](int j) {
+    const int slot = (u0 + j) % KV_STAGES;
+    uint64_t* bar = &P.sh->kvb[P.g][slot];
+    tc::mbar_expect_tx(bar, KV_STAGE_BYTES);
+    tc::bulk_g2s(P.smem + S_Q + slot * KV_STAGE_BYTES, src + (size_t)(first + j) * KV_STAGE_BYTES, KV_STAGE_BYTES,
+                 bar);
+  };
+  hand_state_reset(S);
   // this thread's chunks: hand i's 512 bytes, chunk q = kk 16 + kv 8 + 4 h + t
   // at position q ^ (i & 7)
   const int hi = P.r >> 2;
   const uint32_t off = (uint32_t)hi * 512u;
   const uint32_t pk = (uint32_t)(((4 * P.h + t) ^ (hi & 7)) * 16);  // K chunk of key 0 (V: + 128, key 1: + 256)
 #pragma unroll 1
-  for (int s = 0; s < KV_STAGES_PER_LAYER; ++s) {
-    const int n = u0 + s, slot = n % KV_STAGES;
+  for (int j = 0; j < count; ++j) {
+    if (j == save_at) {  // warp-uniform: park the first half, restart
+      hand_state_st(save_addr, S);
+      hand_state_reset(S);
+    }
+    const int n = u0 + j, slot = n % KV_STAGES;
     if (FSB_HKV_EXP != 1) tc::mbar_wait(&P.sh->kvb[P.g][slot], (uint32_t)((n / KV_STAGES) & 1));
     const uint8_t* st = P.smem + S_Q + slot * KV_STAGE_BYTES + off;
     if (FSB_HKV_EXP != 2) {
@@ -740,12 +787,12 @@ __device__ void cross_attn_hands(Pipe& P, const float* prm, float* x, const uint
     bool grew = false;
 #pragma unroll
     for (int tp = 0; tp < 4; ++tp) {
-      const float mn = fmaxf(m[tp], fmaxf(sc[0][tp], sc[1][tp]));
-      corr[tp] = ex2_approx(m[tp] - mn);
-      m[tp] = mn;
+      const float mn = fmaxf(S.m[tp], fmaxf(sc[0][tp], sc[1][tp]));
+      corr[tp] = ex2_approx(S.m[tp] - mn);
+      S.m[tp] = mn;
       sc[0][tp] = ex2_approx(sc[0][tp] - mn);
       sc[1][tp] = ex2_approx(sc[1][tp] - mn);
-      lsum[tp] = fmaf(lsum[tp], corr[tp], sc[0][tp] + sc[1][tp]);
+      S.l[tp] = fmaf(S.l[tp], corr[tp], sc[0][tp] + sc[1][tp]);
       grew = grew || corr[tp] != 1.0f;
     }
     if (__any_sync(0xffffffffu, grew)) {
@@ -753,7 +800,7 @@ __device__ void cross_attn_hands(Pipe& P, const float* prm, float* x, const uint
       for (int tp = 0; tp < 4; ++tp) {
         const float2 c2 = make_float2(corr[tp], corr[tp]);
 #pragma unroll
-        for (int k = 0; k < 4; ++k) o[tp][k] = __fmul2_rn(o[tp][k], c2);
+        for (int k = 0; k < 4; ++k) S.o[tp][k] = __fmul2_rn(S.o[tp][k], c2);
       }
     }
 #pragma unroll
@@ -764,27 +811,90 @@ __device__ void cross_attn_hands(Pipe& P, const float* prm, float* x, const uint
       for (int tp = 0; tp < 4; ++tp) {
         const float2 pp = make_float2(sc[kk][tp], sc[kk][tp]);
 #pragma unroll
-        for (int k = 0; k < 4; ++k) o[tp][k] = ffma2(pp, vv[k], o[tp][k]);
+        for (int k = 0; k < 4; ++k) S.o[tp][k] = ffma2(pp, vv[k], S.o[tp][k]);
       }
     }
     }
     // (a group barrier per key pair; per-slot release barriers that let a
     // warp run ahead measured slower: hand CTA 173 -> 182 us)
     P.sync();  // every thread is done with the slot
-    if (FSB_HKV_EXP != 1 && P.tid == 0 && s + KV_STAGES < KV_STAGES_PER_LAYER) issue(s + KV_STAGES);
+    if (FSB_HKV_EXP != 1 && P.tid == 0 && j + KV_STAGES < count) issue(j + KV_STAGES);
   }
-  P.kvuse = u0 + KV_STAGES_PER_LAYER;
+}
+
+// the CTA-wide barrier between a hand tile's group and its helper group
+__device__ __forceinline__ void cta_pair_sync() { asm volatile("bar.sync 3, %0;\n" ::"r"(NTH) : "memory"); }
+
+// first three key pairs [first, first + 3) of a layer into this group's ring
+__device__ __forceinline__ void hand_ring_start(Pipe& P, const uint8_t* src, int first, int u0) {
+  if (FSB_HKV_EXP != 1 && P.tid == 0)
+    for (int j = 0; j < KV_STAGES; ++j) {
+      const int slot = (u0 + j) % KV_STAGES;
+      uint64_t* bar = &P.sh->kvb[P.g][slot];
+      tc::mbar_expect_tx(bar, KV_STAGE_BYTES);
+      tc::bulk_g2s(P.smem + S_Q + slot * KV_STAGE_BYTES, src + (size_t)(first + j) * KV_STAGE_BYTES, KV_STAGE_BYTES,
+                   bar);
+    }
+}
+
+// TMEM columns where a half's state waits: the tile group's own free
+// columns [64 + 128 h, +40) (sequential schedule), or the helper group's
+__device__ __forceinline__ uint32_t hand_park(const Pipe& P, uint32_t group_off) {
+  return P.lane_addr(64u + 128u * (uint32_t)P.h) + group_off;
+}
+
+__device__ void cross_attn_hands(Pipe& P, const float* prm, float* x, const uint8_t* hkv, int hand0, int nslots,
+                                 int l, int L, bool valid, bool helped) {
+  const int u0 = P.kvuse;
+  // key pair s of this layer (16 KB: the tile's 32 hands x 512 bytes)
+  const uint8_t* src = hkv + ((size_t)(hand0 / FSB_HANDS_PER_TILE) * L + l) * (32 * KV_STAGE_BYTES);
+  hand_ring_start(P, src, 0, u0);  // S_Q..S_VT are free: the self-attention's MMAs have completed
+  ln_half_to_tile(P, x, prm + TCP_C_LNQ_G, prm + TCP_C_LNQ_B);
+  const uint32_t wq = P.acquire();
+  P.before_issue();
+  if (P.tid == 0) gemm(P.sbase + S_A, D, wq, D, T_GEN, P.tmem);
+  P.prefetch();
+  P.commit_wait();
+  // the residual stream waits in TMEM columns [128 + 32 h, +32) (the query
+  // accumulator uses [0, 64))
+  {
+    uint32_t xu[HC];
+#pragma unroll
+    for (int c = 0; c < HC; ++c) xu[c] = __float_as_uint(x[c]);
+    tc::tmem_st32u_nowait(P.lane_addr(T_GEN + 128 + HC * P.h), xu);
+  }
+  if (helped) {  // the queries are in TMEM: the helper group may read them
+    tc::fence_before();
+    cta_pair_sync();
+    tc::fence_after();
+  }
+  const int t = P.r & 3;
+  float2 qc[4][4];
+  hand_queries(P, P.lane_addr(T_GEN + HC * P.h), prm, qc);
+  HandState A, B;
+  if (helped) {
+    hand_keys(P, src, 0, KV_HALF, u0, qc, A, -1, 0);
+    P.kvuse = u0 + KV_HALF;
+    cta_pair_sync();  // the helper's half is parked in its TMEM columns
+    tc::fence_after();
+    hand_state_ld(hand_park(P, 256u), B);
+  } else {
+    hand_keys(P, src, 0, KV_STAGES_PER_LAYER, u0, qc, B, KV_HALF, hand_park(P, 0u));
+    P.kvuse = u0 + KV_STAGES_PER_LAYER;
+    hand_state_ld(hand_park(P, 0u), A);
+  }
+  hand_merge(A, B);
   // context: rows 4 i + tp, columns 32 h + 8 t (head 2 h + t / 2) -> the A
   // tile of the output projection
   if (valid) {
 #pragma unroll
     for (int tp = 0; tp < 4; ++tp) {
-      const float inv = 1.0f / lsum[tp];
+      const float inv = 1.0f / A.l[tp];
       float v[8];
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        v[2 * k] = o[tp][k].x * inv;
-        v[2 * k + 1] = o[tp][k].y * inv;
+        v[2 * k] = A.o[tp][k].x * inv;
+        v[2 * k + 1] = A.o[tp][k].y * inv;
       }
       st_row8(P.smem + S_A, (P.r & ~3) | tp, HC * P.h + 8 * t, D, v);
     }
@@ -792,6 +902,30 @@ __device__ void cross_attn_hands(Pipe& P, const float* prm, float* x, const uint
   tc::tmem_wait_st();
   tmem_ld32(P.lane_addr(T_GEN + 128 + HC * P.h), x);
   out_proj(P, prm + TCP_C_BO, x, valid);
+}
+
+// The idle second group of a one-tile hand CTA runs the second half of every
+// layer's keys (pairs [16, 32)) through its own ring and parks its state in
+// its TMEM columns for the tile group (cross_attn_hands, helped = true).
+__device__ void hand_helper(Pipe& P, const uint8_t* hkv, int hand0, int L) {
+  for (int l = 0; l < L; ++l) {
+    const uint8_t* src = hkv + ((size_t)(hand0 / FSB_HANDS_PER_TILE) * L + l) * (32 * KV_STAGE_BYTES);
+    const int u0 = P.kvuse;
+    hand_ring_start(P, src, KV_HALF, u0);  // this group's ring is free: its previous pass has ended
+    const int slot = l & 1;                // the layer's parameter block (one pacquire per layer)
+    tc::mbar_wait(&P.sh->pbar[slot], (uint32_t)((l >> 1) & 1));
+    const float* prm = reinterpret_cast<const float*>(P.sall + S_PRM + slot * PRM_BYTES);
+    cta_pair_sync();  // the tile group's queries are in its TMEM columns
+    tc::fence_after();
+    float2 qc[4][4];
+    hand_queries(P, P.lane_addr(T_GEN + HC * P.h) - 256u, prm, qc);
+    HandState B;
+    hand_keys(P, src, KV_HALF, KV_HALF, u0, qc, B, -1, 0);
+    P.kvuse = u0 + KV_HALF;
+    hand_state_st(hand_park(P, 0u), B);
+    tc::fence_before();
+    cta_pair_sync();
+  }
 }
 
 // MLP: x += W2 relu(W1 LN(x) + b1) + b2  (decoder.py:205-212).  The hidden
@@ -1327,6 +1461,11 @@ __global__ void __launch_bounds__(NTH, 1) k_decoders_tc(DecodeArgs a, BodyW bw, 
   const int unit = body ? 2 * tile + blk : 0;  // frame index (body tiles)
   const bool valid = body ? (unit < a.nbody && rb < 51) : hs < nslots;
   const int fb0 = 2 * tile;                    // first frame of a body tile
+  // a one-tile hand CTA: its second group runs half of every layer's cross-
+  // attention keys (hand_helper); FSB_HAND_SPLIT=0 in the launcher turns
+  // this off (same bits: the halves are merged the same way in sequence)
+  const bool helped = !body && tpc == 1 && a.hand_split;
+  if (helped && P.g == 1) hand_helper(P, a.hand_kv, kHandsPerCta * ((int)blockIdx.x - nbc), hw.layers);
   // a group without a tile skips to the common teardown (one barrier site)
   if (P.g == 0 || has1) {
 
@@ -1464,7 +1603,7 @@ __global__ void __launch_bounds__(NTH, 1) k_decoders_tc(DecodeArgs a, BodyW bw, 
     if (body)
       cross_attn(P, prm, x, kvt + (size_t)l * FSB_KV_BODY_TILE, valid);
     else
-      cross_attn_hands(P, prm, x, kvt, hand0, nslots, l, layers, valid);
+      cross_attn_hands(P, prm, x, kvt, hand0, nslots, l, layers, valid, helped);
 #ifdef FSB_PROFILE
     long long ts2 = clock64();
     P.prof[6] += ts2 - ts1;
@@ -1604,6 +1743,11 @@ cudaError_t launch_decoders_tc(const DecodeArgs& a_in, const BodyW& bw, const Ha
     return e ? atoi(e) : 0;
   }();
   a.hand_tiles_per_cta = forced == 1 || forced == 2 ? forced : (nht <= kHandLatencyTiles ? 1 : 2);
+  static const bool split = [] {
+    const char* e = getenv("FSB_HAND_SPLIT");
+    return e == nullptr || atoi(e) != 0;
+  }();
+  a.hand_split = split ? 1 : 0;
   const int n = (nbt + NG - 1) / NG + (nht + a.hand_tiles_per_cta - 1) / a.hand_tiles_per_cta;
   if (n == 0) return cudaSuccess;
   return launch_pdl(k_decoders_tc, dim3(n), dim3(NTH), SMEM_TC, st, a, bw, hw);

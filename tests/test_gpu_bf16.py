@@ -128,6 +128,27 @@ def test_frame_batch_bf16_position_independent(setup):
                 assert np.array_equal(res[k][j], res[k][i]), (j, i, k)
 
 
+def test_decode_hand_bf16_split_schedule(setup, dec_weights):
+    """A one-tile hand CTA runs each layer's cross-attention key halves on its
+    two thread groups side by side; with more than two hand tiles the CTAs
+    hold two tiles and each group runs the halves in sequence.  Same bits:
+    7 hands alone (split) vs the same hands among 80 (3 tiles, sequential)."""
+    from paper_2603_15603_b200 import decoder as dc
+
+    pipe, frames = setup
+    cfg = dc.DecoderConfig()
+    feats = []
+    for f in frames[:4]:
+        _, _, _, crops = orc.frame_crops(f[0], f[1], 64)
+        feats.append(orc.encode(dec_weights, cfg, crops)[1:3])
+    feats = np.concatenate(feats)[:7]
+    few = pipe.decoder.decode_hand(feats, (), precision="bf16")
+    many_in = np.concatenate([feats[(np.arange(80) * 3) % 7]])
+    many = pipe.decoder.decode_hand(many_in, (), precision="bf16")
+    for j in range(80):
+        assert np.array_equal(many[j], few[(j * 3) % 7]), j
+
+
 def test_decode_hand_bf16_ragged(setup, dec_weights):
     """Seven hands: a full 4-hand tile and a 3-hand tile whose second
     cross-attention round has one slot (odd slot count), in one CTA."""
