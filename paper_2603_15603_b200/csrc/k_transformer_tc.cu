@@ -823,7 +823,14 @@ __device__ void hand_keys(Pipe& P, const uint8_t* src, int first, int count, int
 }
 
 // the CTA-wide barrier between a hand tile's group and its helper group
-__device__ __forceinline__ void cta_pair_sync() { asm volatile("bar.sync 3, %0;\n" ::"r"(NTH) : "memory"); }
+// (the two groups reach it from different code sites: the non-.aligned
+// form; after a spin on an mbarrier the warp's threads may leave the loop
+// apart: reconverge for the tcgen05 loads that follow)
+__device__ __forceinline__ void cta_pair_sync() {
+  __syncwarp();
+  asm volatile("barrier.sync 3, %0;\n" ::"r"(NTH) : "memory");
+  __syncwarp();
+}
 
 // first three key pairs [first, first + 3) of a layer into this group's ring
 __device__ __forceinline__ void hand_ring_start(Pipe& P, const uint8_t* src, int first, int u0) {

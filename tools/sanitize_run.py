@@ -34,6 +34,14 @@ if __name__ == "__main__":
         out = pipe.run_batch(torch.from_numpy(imgs).pin_memory(), torch.from_numpy(kps).pin_memory())
         torch.cuda.synchronize()
         print(prec, "frame batch ok", out["theta"].shape)
+    # hand decoder in both schedules: one-tile CTAs whose two thread groups
+    # split the cross-attention keys (10 hands) and two-tile CTAs that run
+    # the halves in sequence (80 hands)
+    feats = np.random.default_rng(9).normal(size=(80, 64, 64)).astype(np.float32)
+    for n in (10, 80):
+        pipe.decoder.decode_hand(feats[:n], (), precision="bf16")
+    torch.cuda.synchronize()
+    print("hand schedules ok")
     # C4 pipeline: 2 layers, 2 crops (SANITIZE_ATTN_ONLY=1: the attention
     # kernel alone, without the GEMMs)
     if os.environ.get("SANITIZE_ATTN_ONLY"):
