@@ -21,6 +21,11 @@ if __name__ == "__main__":
     images = pr.render_scenes(scenes)
     host = [images[i].cpu().numpy() for i in range(8)]
     cfg = pl.fast_config()
+    import ctypes
+
+    from paper_2603_15603_b200 import runtime as rt
+
+    lib = pipe.context().lib
     for i in range(10):
         pipe.run_smpl(host[i % 8], scenes[i % 8], cfg)
     T = {}
@@ -34,10 +39,14 @@ if __name__ == "__main__":
         img, sc = host[r % 8], scenes[r % 8]
         t = time.perf_counter()
         t0 = t
-        check_finite(img, "x")
-        t = tick("check_finite(image)", t)
         st = pipe._frame_state(512, 512, True)
+        bad = ctypes.c_int(0)
+        lib.fsb_stage_frame(img.ctypes.data, st["img_np"].ctypes.data, img.size, ctypes.byref(bad))
+        t = tick("fsb_stage_frame (check + copy)", t)
+        check_finite(img, "x")
+        t = tick("numpy check_finite (ref)", t)
         np.copyto(st["img_np"], img)
+        t = tick("numpy copyto (ref)", t)
         st["kp_np"][...] = sc.keypoints2d
         t = tick("copy to pinned", t)
         stream = torch.cuda.current_stream()
