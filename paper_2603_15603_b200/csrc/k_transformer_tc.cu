@@ -629,7 +629,9 @@ __device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
 // scores, softmax and P.V run on the CUDA cores (FFMA2) over the
 // precomputed bf16 K / V, streamed two keys (16 KB, all 32 hands) at a time
 // through a three-slot shared-memory ring filled by cp.async.bulk (one
-// 512-byte copy per hand, issued by the first warp).
+// 16 KB copy per key pair, issued by the group's first thread).  The 64 keys
+// run as two halves merged at the end (hand_merge below), on both thread
+// groups of a one-tile CTA or in sequence on one group.
 // The four threads of a hand (tokens t = 0..3, column half h) split each
 // key by 16-byte chunks: thread t reads chunk t (dims 32 h + 8 t .. + 8, of
 // head 2 h + t / 2) once and forms the partial scores of all four query rows
