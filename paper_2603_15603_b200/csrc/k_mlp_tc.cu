@@ -241,6 +241,186 @@ __global__ void __launch_bounds__(192, 1) k_tile_gemm_p(const uint8_t* __restric
 }
 
 // ---------------------------------------------------------------------------
+// Large batches, split-K reduced on chip: one persistent CTA per output tile
+// item (m-tile, n-tile) walks the layer's K groups (and, in split-bf16 mode,
+// the three passes) in the order k_tile_reduce8 adds the partial slices;
+// each group's 128 x 128 product lands in one of two TMEM accumulators and
+// the eight epilogue warps (lane quadrant w & 3, column half w >> 2) add it
+// into a running sum in registers, then apply bias / ReLU / mask and write
+// the outputs exactly as k_tile_reduce8 would.  Same bits as the partial-
+// buffer path (the same fp32 adds in the same order); the S x M x N fp32
+// partials (75 MB for layer 1 at 4096 meshes) never touch HBM.
+// Warps 0-7 epilogue, warp 8 producer (bulk copies into a 3-deep ring),
+// warp 9 MMA issue.
+// ---------------------------------------------------------------------------
+struct TileOperands {
+  const uint8_t* a[3];
+  const uint8_t* b[3];
+};
+
+// RELU / MASK / LO: the layer's epilogue variant (one instantiation each keeps
+// the kernel small: the generic form measured i-cache bound on short layers)
+template <bool RELU, bool MASK, bool LO>
+__global__ void __launch_bounds__(320, 1) k_tile_gemm_f(TileOperands ops, int passes, int KT, int G, int M, int N,
+                                                        int NT, int MT, const float* __restrict__ bias,
+                                                        const float* __restrict__ mask, float* __restrict__ out,
+                                                        int ldo, uint8_t* __restrict__ out_img, int KT_out,
+                                                        int* nonfinite, uint8_t* __restrict__ out_img_lo) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bar_load[kPStages], bar_free[kPStages], bar_full[2], bar_tfree[2];
+  __shared__ uint32_t tmem_base;
+  __shared__ float s_bias[128], s_mask[128];
+  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  const int items = MT * NT;
+  const int S = (KT + G - 1) / G;
+  const int units = passes * S;  // (pass, group) products per item, in the reduce's slice order
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < kPStages; ++i) {
+      tc::mbar_init(&bar_load[i], 1);
+      tc::mbar_init(&bar_free[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&bar_full[i], 1);
+      tc::mbar_init(&bar_tfree[i], 8);
+    }
+    tc::mbar_fence_init();
+  }
+  if (warp == 0) tc::tmem_alloc(&tmem_base, 256);
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = tmem_base;
+  const uint32_t sbase = tc::smem_u32(smem);
+  pdl_wait();  // the A image comes from the previous kernel
+  if (warp == 8) {
+    if (lane == 0) {  // producer
+      int q = 0;
+      for (int i = blockIdx.x; i < items; i += gridDim.x) {
+        const int nt = i % NT, mt = i / NT;
+        for (int u = 0; u < units; ++u) {
+          const int ps = u / S, kt0 = (u % S) * G, nk = min(G, KT - kt0);
+          for (int k = 0; k < nk; ++k, ++q) {
+            const int s = q % kPStages, r = q / kPStages;
+            if (r > 0) tc::mbar_wait(&bar_free[s], (uint32_t)((r - 1) & 1));
+            tc::mbar_expect_tx(&bar_load[s], 2 * kTileBytes);
+            tc::bulk_g2s(smem + s * 2 * kTileBytes, ops.a[ps] + ((size_t)mt * KT + kt0 + k) * kTileBytes, kTileBytes,
+                         &bar_load[s]);
+            tc::bulk_g2s(smem + s * 2 * kTileBytes + kTileBytes, ops.b[ps] + ((size_t)nt * KT + kt0 + k) * kTileBytes,
+                         kTileBytes, &bar_load[s]);
+          }
+        }
+      }
+    }
+  } else if (warp == 9) {
+    if (lane == 0) {  // MMA issue
+      const uint32_t idesc = tc::idesc_bf16(128, 128);
+      int q = 0, t = 0;
+      for (int i = blockIdx.x; i < items; i += gridDim.x) {
+        for (int u = 0; u < units; ++u, ++t) {
+          const int kt0 = (u % S) * G, nk = min(G, KT - kt0);
+          const int b = t & 1, ut = t >> 1;
+          if (ut > 0) tc::mbar_wait(&bar_tfree[b], (uint32_t)((ut - 1) & 1));
+          tc::fence_after();
+          const uint32_t d = tmem + b * 128;
+          for (int k = 0; k < nk; ++k, ++q) {
+            const int s = q % kPStages, r = q / kPStages;
+            tc::mbar_wait(&bar_load[s], (uint32_t)(r & 1));
+            tc::fence_after();
+            const uint32_t a = sbase + s * 2 * kTileBytes, bb = a + kTileBytes;
+            for (int kk = 0; kk < 128; kk += 16)
+              tc::mma_bf16(d, tc::kmajor_desc(a, 128, kk), tc::kmajor_desc(bb, 128, kk), idesc, (k | kk) != 0);
+            tc::mma_commit(&bar_free[s]);
+          }
+          tc::mma_commit(&bar_full[b]);
+        }
+      }
+    }
+  } else {  // warps 0-7: running sums of one row x 64 columns
+    const int quad = warp & 3, half = warp >> 2;
+    int t = 0;
+    for (int i = blockIdx.x; i < items; i += gridDim.x) {
+      const int nt = i % NT, mt = i / NT;
+      const int m = mt * 128 + quad * 32 + lane;
+      // the item's 128 bias / mask columns into shared memory while its
+      // first products are computed (per-element global loads in the
+      // epilogue serialised into L2 round trips)
+      asm volatile("bar.sync 1, 256;" ::: "memory");  // the previous item's epilogue is done with them
+      if (threadIdx.x < 128) {
+        const int n = nt * 128 + threadIdx.x;
+        s_bias[threadIdx.x] = n < N ? bias[n] : 0.0f;
+        s_mask[threadIdx.x] = n < N && mask != nullptr ? mask[n] : 1.0f;
+      }
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      float v[64];
+      for (int u = 0; u < units; ++u, ++t) {
+        const int b = t & 1, ut = t >> 1;
+        tc::mbar_wait(&bar_full[b], (uint32_t)(ut & 1));
+        tc::fence_after();
+#pragma unroll
+        for (int hq = 0; hq < 2; ++hq) {  // two 32-column loads: fewer live registers
+          float p[32];
+          tc::tmem_ld32(tmem + b * 128 + ((uint32_t)(quad * 32) << 16) + 64 * half + 32 * hq, p);
+          if (u == 0) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[32 * hq + j] = p[j];
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[32 * hq + j] += p[j];
+          }
+        }
+        tc::fence_before();
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&bar_tfree[b]);
+      }
+      if (m >= M) continue;
+      // the k_tile_reduce8 epilogue, eight columns at a time
+      bool bad = false;
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        const int n0 = nt * 128 + 64 * half + 8 * c;
+        if (n0 >= N) break;
+        const bool hi = n0 + 4 < N;  // (N % 4 == 0: a chunk holds 4 or 8 columns)
+        float w[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int cl = 64 * half + 8 * c + j;
+          float x = v[8 * c + j] + s_bias[cl];
+          if (RELU) x = fmaxf(x, 0.0f);
+          if (MASK) x *= s_mask[cl];
+          w[j] = (j < 4 || hi) ? x : 0.0f;
+          bad = bad || !isfinite(w[j]);
+        }
+        if (out != nullptr) {
+          *reinterpret_cast<float4*>(out + (int64_t)m * ldo + n0) = make_float4(w[0], w[1], w[2], w[3]);
+          if (hi) *reinterpret_cast<float4*>(out + (int64_t)m * ldo + n0 + 4) = make_float4(w[4], w[5], w[6], w[7]);
+        }
+        if (out_img != nullptr) {
+          const size_t tile = (size_t)(m >> 7) * KT_out + (n0 >> 7);
+          const size_t off = tile * kTileBytes + tc::kmajor_off(m & 127, n0 & 127, 128);
+          uint32_t h[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) h[j] = tc::pack_bf16(w[2 * j], w[2 * j + 1]);
+          *reinterpret_cast<uint4*>(out_img + off) = make_uint4(h[0], h[1], h[2], h[3]);
+          if (LO) {
+            uint32_t lo[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              const float2 hf = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&h[j]));
+              lo[j] = tc::pack_bf16(w[2 * j] - hf.x, w[2 * j + 1] - hf.y);
+            }
+            *reinterpret_cast<uint4*>(out_img_lo + off) = make_uint4(lo[0], lo[1], lo[2], lo[3]);
+          }
+        }
+      }
+      if (bad && nonfinite != nullptr) atomicOr(nonfinite, 1);
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_dealloc(tmem, 256);
+}
+
+// ---------------------------------------------------------------------------
 // Small batches (M = meshes <= 64: the frame path's 32): the same K groups,
 // transposed -- D^T (128 outputs x Np meshes) = W^T tile (the A operand, M =
 // 128) . X^T, the meshes as the N = Np operand (Np = M rounded up to 16).
@@ -389,8 +569,15 @@ cudaError_t init_attrs_mlp_tc() {
   e = cudaFuncSetAttribute(k_tile_gemm_t, cudaFuncAttributeMaxDynamicSharedMemorySize,
                            (int)(2 * (kTileBytes + 64 * 256)));
   if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(k_tile_gemm_p, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)(2 * kPStages * kTileBytes));
+  e = cudaFuncSetAttribute(k_tile_gemm_p, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           (int)(2 * kPStages * kTileBytes));
+  if (e != cudaSuccess) return e;
+  for (auto f : {k_tile_gemm_f<true, false, false>, k_tile_gemm_f<false, true, false>, k_tile_gemm_f<true, false, true>,
+                 k_tile_gemm_f<false, true, true>}) {
+    e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * kPStages * kTileBytes));
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 #ifndef FSB_TILE_PERSIST_M
@@ -426,6 +613,27 @@ cudaError_t launch_tile_layer(const uint8_t* Aimg, const uint8_t* Bimg, int KT, 
   if (M == 0) return cudaSuccess;
   const int S = (KT + G - 1) / G;
   const bool split = Aimg_lo != nullptr && Bimg_lo != nullptr;
+  // large batches: the K groups reduced on chip (same bits as the partials +
+  // k_tile_reduce8 below); FSB_TILE_PARTIALS=1 keeps the partial buffers
+  static const bool partials = getenv("FSB_TILE_PARTIALS") != nullptr && atoi(getenv("FSB_TILE_PARTIALS")) != 0;
+  if (M >= FSB_TILE_PERSIST_M && N % 4 == 0 && (out == nullptr || ldo % 4 == 0) && !partials &&
+      ((relu != 0) != (mask != nullptr))) {
+    TileOperands ops{{Aimg, Aimg, Aimg_lo}, {Bimg, Bimg_lo, Bimg}};
+    const int NT = (N + 127) / 128, MT = (M + 127) / 128, items = NT * MT;
+    const dim3 grid(items < 148 ? items : 148);
+    const size_t smem = 2 * kPStages * kTileBytes;
+    const int passes = split ? 3 : 1;
+    uint8_t* lo = split ? out_img_lo : nullptr;
+    if (relu)
+      return split ? launch_pdl(k_tile_gemm_f<true, false, true>, grid, dim3(320), smem, st, ops, passes, KT, G, M, N,
+                                NT, MT, bias, mask, out, ldo, out_img, KT_out, nonfinite, lo)
+                   : launch_pdl(k_tile_gemm_f<true, false, false>, grid, dim3(320), smem, st, ops, passes, KT, G, M, N,
+                                NT, MT, bias, mask, out, ldo, out_img, KT_out, nonfinite, lo);
+    return split ? launch_pdl(k_tile_gemm_f<false, true, true>, grid, dim3(320), smem, st, ops, passes, KT, G, M, N, NT,
+                              MT, bias, mask, out, ldo, out_img, KT_out, nonfinite, lo)
+                 : launch_pdl(k_tile_gemm_f<false, true, false>, grid, dim3(320), smem, st, ops, passes, KT, G, M, N, NT,
+                              MT, bias, mask, out, ldo, out_img, KT_out, nonfinite, lo);
+  }
   cudaError_t e = tile_gemm_pass(Aimg, Bimg, KT, G, M, N, S, partial, st);
   if (e == cudaSuccess && split) e = tile_gemm_pass(Aimg, Bimg_lo, KT, G, M, N, S, partial + (size_t)S * M * N, st);
   if (e == cudaSuccess && split)
