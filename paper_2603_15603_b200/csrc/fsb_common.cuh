@@ -128,7 +128,11 @@ __constant__ __device__ static const int8_t kDepth[FSB_NJ] = {0, 1, 2, 3, 4, 5, 
 template <bool FAST = false>
 __device__ __forceinline__ void fk_warp(const float* pose, const float* grest, FKOut& o, int lane) {
   const int j = lane;
+  // (parent and depth read once: the lanes' distinct constant-bank addresses
+  // serialise, and a per-level reload of kDepth[j] was the kernel's hottest
+  // stall)
   const int p = j < FSB_NJ ? kParents[j] : -1;
+  const int dj = j < FSB_NJ ? (int)kDepth[j] : -1;
   float loc[9], tl[3], g[3];
   if (j < FSB_NJ) {
     rodrigues3<FAST>(pose[3 * j], pose[3 * j + 1], pose[3 * j + 2], loc);
@@ -147,7 +151,7 @@ __device__ __forceinline__ void fk_warp(const float* pose, const float* grest, F
   __syncwarp();
 #pragma unroll 1
   for (int lvl = 1; lvl < 8; ++lvl) {
-    if (j < FSB_NJ && kDepth[j] == lvl) {
+    if (dj == lvl) {
       float rp[9], tp[3];
 #pragma unroll
       for (int e = 0; e < 9; ++e) rp[e] = o.rw[p][e];
