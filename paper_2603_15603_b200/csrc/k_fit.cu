@@ -92,6 +92,15 @@ __global__ void __launch_bounds__(kFitThreads) k_fit(TemplateDev t, const float*
   __shared__ FitShared sh;
   const int b = blockIdx.x;
   const int tid = threadIdx.x, warp = tid / 32, lane = tid % 32;
+  // this lane's joint: parent, tree depth and children (bit c set when
+  // parents[c] == joint), read from the constant bank once -- per-level
+  // reloads with the lanes' distinct addresses serialise (as in fk_warp)
+  const int jl = lane < FSB_NJ ? lane : 0;
+  const int par_l = lane < FSB_NJ ? (int)kParents[jl] : -1;
+  const int dep_l = lane < FSB_NJ ? (int)kFitDepth[jl] : -1;
+  uint32_t kids_l = 0;
+  for (int c = 0; c < FSB_NJ; ++c)  // (c is warp-uniform: broadcast reads)
+    if (lane < FSB_NJ && kParents[c] == lane) kids_l |= 1u << c;
   const int nv = t.nv;
   const float* tgt = target + (int64_t)b * nv * 3;
   float* gs = scratch + (int64_t)b * nv * 6;  // (dL/dp, s) per vertex
@@ -109,7 +118,7 @@ __global__ void __launch_bounds__(kFitThreads) k_fit(TemplateDev t, const float*
       float g[3], tl[3];
       if (j < FSB_NJ) {
         rodrigues3<false>(sh.theta[3 * j], sh.theta[3 * j + 1], sh.theta[3 * j + 2], sh.rl[j]);
-        const int p = kParents[j];
+        const int p = par_l;
         for (int a = 0; a < 3; ++a) {
           g[a] = t.joints_rest[3 * j + a];
           tl[a] = p < 0 ? g[a] : g[a] - t.joints_rest[3 * p + a];
@@ -121,8 +130,8 @@ __global__ void __launch_bounds__(kFitThreads) k_fit(TemplateDev t, const float*
       }
       __syncwarp();
       for (int lvl = 1; lvl < kMaxLevel; ++lvl) {
-        if (j < FSB_NJ && kFitDepth[j] == lvl) {
-          const int p = kParents[j];
+        if (dep_l == lvl) {
+          const int p = par_l;
           float rp[9], tp[3];
           for (int e = 0; e < 9; ++e) rp[e] = sh.rw[p][e];
           for (int a = 0; a < 3; ++a) tp[a] = sh.tw[p][a];
@@ -238,9 +247,9 @@ __global__ void __launch_bounds__(kFitThreads) k_fit(TemplateDev t, const float*
       __syncwarp();
       // children into parents, deepest level first
       for (int lvl = kMaxLevel - 2; lvl >= 0; --lvl) {
-        if (j < FSB_NJ && kFitDepth[j] == lvl) {
+        if (dep_l == lvl) {
           for (int c = j + 1; c < FSB_NJ; ++c) {
-            if (kParents[c] != j) continue;
+            if (!((kids_l >> c) & 1u)) continue;
             float tl[3];
             for (int a = 0; a < 3; ++a) tl[a] = t.joints_rest[3 * c + a] - g[a];
             for (int a = 0; a < 3; ++a) {
@@ -255,7 +264,7 @@ __global__ void __launch_bounds__(kFitThreads) k_fit(TemplateDev t, const float*
       }
       if (j < FSB_NJ) {
         // dR_l[j] = R_w[p]^T dR_w[j] (root: dR_w[0])
-        const int p = kParents[j];
+        const int p = par_l;
         float G[9];
         for (int a = 0; a < 3; ++a)
           for (int q = 0; q < 3; ++q)
