@@ -334,6 +334,42 @@ def test_c3_batch_independent_bits(torch, full_models, full_projector):
                 assert torch.equal(a, b), precision
 
 
+def test_c3_partial_last_tile_bits(torch, full_models, full_projector):
+    """The on-chip-reduced projector GEMM (k_tile_gemm_f, from 1024 meshes)
+    with a partial last 128-row tile: 1100 meshes in one call give the same
+    theta / joints bits as calls of 32 (transposed tiles + k_tile_reduce8),
+    and the rows past the batch are never written (bf16 and fp32)."""
+    from paper_2603_15603_b200 import decoder as dc
+    from paper_2603_15603_b200 import runtime as rt
+
+    mhr, smpl, gt = full_models
+    n = 1100
+    rng = np.random.default_rng(12)
+    p = np.zeros((n, 76), np.float32)
+    p[:, :66] = rng.normal(0.0, 0.2, size=(n, 66))
+    p[:, 66:] = rng.normal(0.0, 0.45, size=(n, 10))
+    for precision in ("bf16", "fp32"):
+        pipe = _pipeline(dc.Decoder(smpl, dc.DecoderConfig(), seed=40), mhr, gt, full_projector, precision)
+        ctx = pipe.context()
+        ctx.reserve(n)
+        poses = torch.from_numpy(p).cuda()
+        outs = []
+        for step in (n, 32):
+            v = torch.empty((n, mhr.num_vertices, 3), dtype=torch.float32, device="cuda")
+            th = torch.full((n + 4, 76), 7.0, dtype=torch.float32, device="cuda")
+            j = torch.empty((n, 22, 3), dtype=torch.float32, device="cuda")
+            for b0 in range(0, n, step):
+                m = min(step, n - b0)
+                ctx.check(ctx.lib.fsb_skin_project(ctx.h, rt.ptr(poses[b0:]), m, rt.ptr(v[b0:]), rt.ptr(th[b0:]),
+                                                   rt.ptr(j[b0:]), None, rt.PRECISIONS[precision], ctx.stream))
+            torch.cuda.synchronize()
+            ctx.check_finite("c3 partial tile")
+            assert torch.all(th[n:] == 7.0), precision  # nothing written past the batch
+            outs.append((th[:n].cpu(), j.cpu()))
+        for a, b in zip(outs[0], outs[1]):
+            assert torch.equal(a, b), precision
+
+
 # ---------------------------------------------------------------------------
 # ViT-L-sized encoder, all 24 layers
 
