@@ -1250,7 +1250,7 @@ int fsb_boxes_crops(fsb_ctx* c, const float* images, int B, int H, int W, const 
   }
   FSB_CUDA(c, launch_boxes_crops(images, kp, B, H, W, S, alpha, host_frames, boxes, prompt, crops, taps, c->d_flag,
                                  c->d_bytes_in, (cudaStream_t)stream));
-  c->launches += B > 0 ? (host_frames ? 1 : 2) : 0;  // HBM frames: k_frame_boxes + k_boxes_crops
+  c->launches += B > 0 ? (host_frames || B <= 2 ? 1 : 2) : 0;  // HBM frames from 3 on: k_frame_boxes + k_boxes_crops
   note_stream(c, (cudaStream_t)stream);
   return FSB_OK;
 }

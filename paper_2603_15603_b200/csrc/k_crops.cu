@@ -134,6 +134,11 @@ __global__ void k_frame_boxes(const float* __restrict__ kps, int B, int W, int H
   for (int e = 0; e < 8; ++e) prompt_out[(int64_t)f * 8 + e] = fb.prompt[e];
 }
 
+// SELF (a batch of one or two frames, the latency case): thread 0 derives
+// the frame's boxes itself (the same frame_boxes as k_frame_boxes; CTA
+// (0, 0) of each frame writes them out) instead of waiting for a separate
+// k_frame_boxes launch.
+template <bool SELF>
 __global__ void __launch_bounds__(256) k_boxes_crops(
     const float* __restrict__ images, const float* __restrict__ kps, int B, int H, int W, int S,
     double alpha, int64_t img_stride, double* __restrict__ boxes_out, float* __restrict__ prompt_out,
@@ -143,8 +148,23 @@ __global__ void __launch_bounds__(256) k_boxes_crops(
   const int f = blockIdx.z, crop = blockIdx.y, band = blockIdx.x;
   const int tid = threadIdx.x;
   pdl_wait();
-  // the frame's boxes come from k_frame_boxes (same stream, launched first)
-  if (tid < 4) bx[tid] = boxes_out[((int64_t)f * 3 + crop) * 4 + tid];
+  if (SELF) {
+    if (tid == 0) {
+      float kp[2 * FSB_NJ];
+      for (int i = 0; i < 2 * FSB_NJ; ++i) kp[i] = clip_kp(kps[(int64_t)f * 2 * FSB_NJ + i], i, W, H);
+      FrameBoxes fb;
+      frame_boxes(kp, W, H, alpha, fb);
+      for (int e = 0; e < 4; ++e) bx[e] = fb.box[crop][e];
+      if (band == 0 && crop == 0) {
+        for (int c = 0; c < 3; ++c)
+          for (int e = 0; e < 4; ++e) boxes_out[((int64_t)f * 3 + c) * 4 + e] = fb.box[c][e];
+        for (int e = 0; e < 8; ++e) prompt_out[(int64_t)f * 8 + e] = fb.prompt[e];
+      }
+    }
+  } else {
+    // the frame's boxes come from k_frame_boxes (same stream, launched first)
+    if (tid < 4) bx[tid] = boxes_out[((int64_t)f * 3 + crop) * 4 + tid];
+  }
   __syncthreads();
   for (int i = tid; i < S; i += blockDim.x) {
     gx[i] = lin_f32(bx[0], bx[2], S, i);
@@ -410,11 +430,14 @@ cudaError_t launch_boxes_crops(const float* images, const float* kps, int B, int
     return launch_pdl(k_crops_stream, grid, dim3(kStreamThreads), stream_smem(rowcap4), st, images, kps, B, H, W, S,
                       alpha, stride, rowcap4, rows_per_cta, boxes, prompt, crops, taps, nonfinite, bytes_in);
   } else {  // HBM-resident (or very wide / unaligned host) frames: per-tap reads
+    dim3 grid((S + kRowsPerCTA - 1) / kRowsPerCTA, 3, B);
+    if (B <= 2)  // latency: one launch, each CTA derives its frame's boxes
+      return launch_pdl(k_boxes_crops<true>, grid, dim3(256), 0, st, images, kps, B, H, W, S, alpha, stride, boxes,
+                        prompt, crops, taps, nonfinite);
     cudaError_t e = launch_pdl(k_frame_boxes, dim3((B + 63) / 64), dim3(64), 0, st, kps, B, W, H, alpha, boxes, prompt);
     if (e != cudaSuccess) return e;
-    dim3 grid((S + kRowsPerCTA - 1) / kRowsPerCTA, 3, B);
-    return launch_pdl(k_boxes_crops, grid, dim3(256), 0, st, images, kps, B, H, W, S, alpha, stride, boxes, prompt,
-                      crops, taps, nonfinite);
+    return launch_pdl(k_boxes_crops<false>, grid, dim3(256), 0, st, images, kps, B, H, W, S, alpha, stride, boxes,
+                      prompt, crops, taps, nonfinite);
   }
   return cudaGetLastError();
 }
