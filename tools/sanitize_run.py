@@ -31,6 +31,7 @@ if __name__ == "__main__":
                            precision=prec)
         pipe.context().set_graphs(False)
         out = pipe.run_batch(imgs, kps)
+        pipe.run_batch(imgs[:1], kps[:1])  # one HBM frame: boxes derived inside the crop CTAs
         out = pipe.run_batch(torch.from_numpy(imgs).pin_memory(), torch.from_numpy(kps).pin_memory())
         torch.cuda.synchronize()
         print(prec, "frame batch ok", out["theta"].shape)
